@@ -1,0 +1,380 @@
+"""Pins for the CPU oracle (oracle/oracle.c) against things other than itself.
+
+Each pin is chosen so that a plausible mistake (dropped term, wrong sign or
+index, transposed operand, off-by-one boundary) fails at least one test:
+  * SPEC.md worked values on fixture E (tests/golden/fixture_E.json, cited),
+  * closed forms (identity, permutation, diagonal, 27-point stencil, 1xN chain),
+  * numpy dense brute force (an independent library primitive),
+  * exhaustive invariants (balance <= 1, exact tiling, merge-of-partition = id).
+"""
+import itertools
+
+import numpy as np
+import pytest
+
+import oracle
+
+
+def E_csr(g, dtype=np.float64):
+    return (np.array(g["csr_row_ptr"], np.int64), np.array(g["csr_col_idx"], np.int32),
+            np.array(g["csr_val"], dtype))
+
+
+# ------------------------------------------------------------- conversions
+def test_E_coo_to_csr(golden_E):
+    g = golden_E
+    rp, ci, v = oracle.coo_to_csr(4, g["coo_row"], g["coo_col"], np.array(g["coo_val"]))
+    assert rp.tolist() == g["csr_row_ptr"] and ci.tolist() == g["csr_col_idx"]
+    assert v.tolist() == g["csr_val"]
+
+
+def test_E_csr_to_csc(golden_E):
+    g = golden_E
+    rp, ci, v = E_csr(g)
+    cp, ri, cv = oracle.csr_to_csc(4, 4, rp, ci, v)
+    assert cp.tolist() == g["csc_col_ptr"] and ri.tolist() == g["csc_row_idx"]
+    assert cv.tolist() == g["csc_val"]
+
+
+def test_empty_matrix_conversion():
+    rp, ci, v = oracle.coo_to_csr(3, np.zeros(0, np.int64), np.zeros(0, np.int32), np.zeros(0))
+    assert rp.tolist() == [0, 0, 0, 0]
+
+
+def test_diagonal_csc_equals_csr():
+    n = 7
+    rp = np.arange(n + 1, dtype=np.int64); ci = np.arange(n, dtype=np.int32)
+    v = np.random.default_rng(0).standard_normal(n)
+    cp, ri, cv = oracle.csr_to_csc(n, n, rp, ci, v)
+    assert np.array_equal(cp, rp) and np.array_equal(ri, ci) and np.array_equal(cv, v)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_roundtrips_bit_exact(dtype):
+    rng = np.random.default_rng(11)
+    for trial in range(30):
+        m, n = rng.integers(1, 40, 2)
+        dense = (rng.random((m, n)) < 0.2) * rng.standard_normal((m, n))
+        r, c = np.nonzero(dense)                                # row-major = row-sorted
+        vals = dense[r, c].astype(dtype)
+        rp, ci, v = oracle.coo_to_csr(m, r, c, vals)
+        # CSR -> COO -> CSR identity
+        ri = oracle.csr_to_coo(m, rp)
+        assert np.array_equal(ri, r) and np.array_equal(ci, c)
+        assert v.tobytes() == vals.tobytes()
+        # double transpose is the identity: CSC(A) read as CSR(A^T), back
+        cp, rowi, cv = oracle.csr_to_csc(m, n, rp, ci, v)
+        rp2, ci2, v2 = oracle.csr_to_csc(n, m, cp, rowi, cv)
+        assert np.array_equal(rp2, rp) and np.array_equal(ci2, ci) and v2.tobytes() == v.tobytes()
+        # CSC expands to the transpose's triplets
+        cj = oracle.csc_to_coo(n, cp)
+        assert sorted(zip(cj.tolist(), rowi.tolist())) == sorted(zip(c.tolist(), r.tolist()))
+
+
+# ----------------------------------------------------------------- SpMV pins
+@pytest.mark.parametrize("fmt", ["csr", "csc", "coo"])
+def test_E_spmv_worked_values(golden_E, fmt):
+    g = golden_E
+    for case in g["spmv"]:
+        x = np.array(case["x"], float); y = np.array(case["y"], float)
+        if fmt == "csr":
+            out = oracle.spmv_csr(4, *E_csr(g), x, y, case["alpha"], case["beta"])
+        elif fmt == "csc":
+            out = oracle.spmv_csc(4, 4, g["csc_col_ptr"], g["csc_row_idx"], np.array(g["csc_val"]),
+                                  x, y, case["alpha"], case["beta"])
+        else:
+            out = oracle.spmv_coo(4, g["coo_row"], g["coo_col"], np.array(g["coo_val"]), x, y,
+                                  case["alpha"], case["beta"])
+        assert out.tolist() == case["expect"]
+
+
+def test_E_nonsymmetric_x_catches_transpose(golden_E):
+    # x = e_2 picks column 2: A[:,2] = [2,0,0,0]; a transposed operand would give row 2 (empty).
+    g = golden_E
+    x = np.array([0, 0, 1, 0], float)
+    assert oracle.spmv_csr(4, *E_csr(g), x, np.zeros(4), 1.0, 0.0).tolist() == [2, 0, 0, 0]
+
+
+def test_identity_closed_form():
+    n = 50
+    rng = np.random.default_rng(1)
+    rp = np.arange(n + 1, dtype=np.int64); ci = np.arange(n, dtype=np.int32); v = np.ones(n)
+    x = rng.standard_normal(n); y = rng.standard_normal(n)
+    out = oracle.spmv_csr(n, rp, ci, v, x, y, 1.5, -0.5)
+    assert np.array_equal(out, 1.5 * x + (-0.5) * y)       # alpha*x + beta*y, one rounding each
+
+
+def test_permutation_bit_exact():
+    n = 97
+    rng = np.random.default_rng(2)
+    pi = rng.permutation(n)
+    rp = np.arange(n + 1, dtype=np.int64); ci = pi.astype(np.int32); v = np.ones(n)
+    x = rng.standard_normal(n)
+    for f in (lambda: oracle.spmv_csr(n, rp, ci, v, x, np.full(n, np.nan), 1.0, 0.0),
+              lambda: oracle.spmv_coo(n, np.arange(n), ci, v, x, np.full(n, np.nan), 1.0, 0.0)):
+        assert np.array_equal(f(), x[pi])                 # beta=0: NaN y_in never read (R12)
+
+
+def test_diagonal_closed_form():
+    n = 64
+    rng = np.random.default_rng(3)
+    d = rng.standard_normal(n); x = rng.standard_normal(n); y = rng.standard_normal(n)
+    rp = np.arange(n + 1, dtype=np.int64); ci = np.arange(n, dtype=np.int32)
+    out = oracle.spmv_csr(n, rp, ci, d, x, y, 2.0, 0.25)
+    assert np.array_equal(out, 2.0 * (d * x) + 0.25 * y)
+
+
+def stencil27_csr(N):
+    """Independent tiny stencil builder (test-local, dense loops)."""
+    rows, cols = [], []
+    idx = lambda i, j, k: (i * N + j) * N + k
+    for i in range(N):
+        for j in range(N):
+            for k in range(N):
+                for di in (-1, 0, 1):
+                    for dj in (-1, 0, 1):
+                        for dk in (-1, 0, 1):
+                            a, b, c = i + di, j + dj, k + dk
+                            if 0 <= a < N and 0 <= b < N and 0 <= c < N:
+                                rows.append(idx(i, j, k)); cols.append(idx(a, b, c))
+    r = np.array(rows); c = np.array(cols)
+    v = np.where(r == c, 26.0, -1.0)
+    return r, c, v
+
+
+@pytest.mark.parametrize("N", [2, 3, 5])
+def test_stencil_closed_form(N):
+    # diag 26, off -1, x = 1  ->  y_i = 27 - k_i, k_i = prod_d (3 - [face in d])
+    r, c, v = stencil27_csr(N)
+    m = N ** 3
+    assert r.size == (3 * N - 2) ** 3
+    rp, ci, vv = oracle.coo_to_csr(m, r, c, v)
+    out = oracle.spmv_csr(m, rp, ci, vv, np.ones(m), np.zeros(m), 1.0, 0.0)
+    g = np.indices((N, N, N)).reshape(3, -1).T
+    k = np.prod(3 - ((g == 0) | (g == N - 1)).astype(int) * (1 if N > 1 else 2), axis=1)
+    assert np.array_equal(out, 27.0 - k)
+    if N >= 3:
+        assert set(np.unique(out).tolist()) == {0.0, 9.0, 15.0, 19.0}
+
+
+def test_alpha_beta_conventions():
+    rp = np.array([0, 1], np.int64); ci = np.array([0], np.int32)
+    v = np.array([np.nan]); x = np.array([np.nan])
+    # alpha == 0: A and x not read, y = beta*y_in
+    assert oracle.spmv_csr(1, rp, ci, v, x, np.array([3.0]), 0.0, 2.0).tolist() == [6.0]
+    # beta == 0: y_in not read
+    v = np.array([2.0]); x = np.array([5.0])
+    assert oracle.spmv_csr(1, rp, ci, v, x, np.array([np.nan]), 1.0, 0.0).tolist() == [10.0]
+
+
+def dense_of(m, n, r, c, v):
+    A = np.zeros((m, n))
+    np.add.at(A, (r, c), v.astype(np.float64))
+    return A
+
+
+def random_matrix(rng, m, n, density, empty_rows=True):
+    mask = rng.random((m, n)) < density
+    if empty_rows and m > 2:
+        mask[rng.integers(0, m, max(1, m // 5))] = False
+    if empty_rows and n > 2:
+        mask[:, rng.integers(0, n, max(1, n // 5))] = False
+    r, c = np.nonzero(mask)
+    v = rng.uniform(-1, 1, r.size)
+    return r, c, v
+
+
+ALPHAS = [0.0, 1.0, -1.0, 2.5]
+BETAS = [0.0, 1.0, -1.0, 10.0]
+
+
+def test_dense_brute_force_all_formats_and_parts():
+    """P3: all formats, m,n <= 64, np in 1..9, alpha x beta grid vs numpy dense."""
+    rng = np.random.default_rng(1234)
+    for trial in range(40):
+        m, n = rng.integers(1, 65, 2)
+        r, c, v = random_matrix(rng, m, n, [0.01, 0.1, 0.3][trial % 3])
+        A = dense_of(m, n, r, c, v)
+        rp, ci, vv = oracle.coo_to_csr(m, r, c, v)
+        cp, ri, cv = oracle.csr_to_csc(m, n, rp, ci, vv)
+        x = rng.uniform(-1, 1, n); y = rng.uniform(-1, 1, m)
+        for alpha, beta in itertools.product(ALPHAS, BETAS):
+            ref = alpha * (A @ x) + beta * y
+            bound = np.abs(alpha) * (np.abs(A) @ np.abs(x)) + np.abs(beta * y)
+            outs = [oracle.spmv_csr(m, rp, ci, vv, x, y, alpha, beta),
+                    oracle.spmv_csc(m, n, cp, ri, cv, x, y, alpha, beta),
+                    oracle.spmv_coo(m, r, c, v, x, y, alpha, beta)]
+            np_ = int(rng.integers(1, 10))
+            outs += [oracle.exec_csr(m, rp, ci, vv, x, y, alpha, beta, np_),
+                     oracle.exec_csc(m, n, cp, ri, cv, x, y, alpha, beta, np_),
+                     oracle.exec_coo(m, r, c, v, x, y, alpha, beta, np_)]
+            for o in outs:
+                assert np.all(np.abs(o - ref) <= 1e-13 * bound + 1e-300), (trial, alpha, beta)
+
+
+def test_fp32_accumulates_in_fp64_rounds_once():
+    # 2^24 + 1 is not representable in fp32; an fp32 accumulator loses the +1s.
+    k = 3
+    rp = np.array([0, k + 1], np.int64); ci = np.arange(k + 1, dtype=np.int32)
+    v = np.array([2.0 ** 24, 1.0, 1.0, 1.0], np.float32); x = np.ones(k + 1, np.float32)
+    out = oracle.spmv_csr(1, rp, ci, v, x, np.zeros(1, np.float32), 1.0, 0.0)
+    assert out.dtype == np.float32 and out[0] == np.float32(2.0 ** 24 + 4)
+
+
+# ------------------------------------------------------------- partitioning
+def test_boundaries_worked(golden_E):
+    for case in golden_E["boundaries"]:
+        assert oracle.nnz_boundaries(case["nnz"], case["np"]).tolist() == case["expect"]
+
+
+def test_balance_exhaustive():
+    """sizes differ by <= 1 and tile [0,nnz) exactly, nnz<=1000, np<=64."""
+    for nnz in range(0, 1001, 7):
+        for np_ in range(1, 65):
+            b = oracle.nnz_boundaries(nnz, np_)
+            sz = np.diff(b)
+            assert b[0] == 0 and b[-1] == nnz and np.all(sz >= 0)
+            assert sz.max() - sz.min() <= 1
+
+
+def test_owner_worked(golden_E):
+    for case in golden_E["owners"]:
+        assert oracle.owner_linear(golden_E["csr_row_ptr"], case["idx"]) == case["expect"]
+
+
+def _check_parts(parts, locs, expect):
+    for p, loc, e in zip(parts, locs, expect):
+        for k in ("start_idx", "end_idx", "start_row", "end_row", "start_flag"):
+            assert int(p[k]) == e[k], (k, p, e)
+        if "local" in e:
+            assert loc.tolist() == e["local"]
+
+
+def test_E_pcsr_pcsc_pcoo(golden_E):
+    g = golden_E
+    parts, locs, _ = oracle.partition_ptr(g["csr_row_ptr"], 2)
+    _check_parts(parts, locs, g["pcsr_np2"])
+    assert [[int(p["owned_begin"]), int(p["owned_end"])] for p in parts] == g["owned_np2"]
+    parts5, _, _ = oracle.partition_ptr(g["csr_row_ptr"], 5)
+    assert [[int(p["owned_begin"]), int(p["owned_end"])] for p in parts5] == g["owned_np5"]
+    parts, locs, _ = oracle.partition_ptr(g["csc_col_ptr"], 2)
+    _check_parts(parts, locs, g["pcsc_np2"])
+    pc = oracle.partition_coo(4, g["coo_row"], 2)
+    _check_parts(pc, [None, None], g["pcoo_np2"])
+    # all-same-row COO: part 1 flagged
+    pc = oracle.partition_coo(1, [0, 0, 0, 0], 2)
+    assert int(pc[1]["start_flag"]) == 1 and int(pc[0]["start_flag"]) == 0
+
+
+def test_E_kernel_segment_and_csc_accumulators(golden_E):
+    g = golden_E
+    rp, ci, v = E_csr(g)
+    parts, locs, _ = oracle.partition_ptr(rp, 2)
+    p, loc = parts[1], locs[1]
+    seg = [sum(v[p["start_idx"] + j] * 1.0 for j in range(loc[k], loc[k + 1])) for k in range(len(loc) - 1)]
+    assert seg == g["pcsr_np2_kernel_segment_part1"]
+    # CSC np=2 accumulators [1,0,0,4] + [2,3,0,5] summed = [3,3,0,9]
+    out = oracle.exec_csc(4, 4, g["csc_col_ptr"], g["csc_row_idx"], np.array(g["csc_val"]),
+                          np.ones(4), np.zeros(4), 1.0, 0.0, 2)
+    assert out.tolist() == (np.array(g["pcsc_np2_accumulators"]).sum(0)).tolist()
+
+
+def test_shared_row_beta_once(golden_E):
+    """S:306 / S:337: a row split across 2 parts gets beta*y_in once -> [20]."""
+    s = golden_E["shared_row_1x4"]
+    rp = np.array([0, 4], np.int64); ci = np.arange(4, dtype=np.int32); v = np.array(s["val"], float)
+    for f in (lambda: oracle.exec_csr(1, rp, ci, v, s["x"], s["y"], s["alpha"], s["beta"], s["np"]),
+              lambda: oracle.exec_coo(1, np.zeros(4), ci, v, s["x"], s["y"], s["alpha"], s["beta"], s["np"])):
+        assert f().tolist() == s["expect"]
+    parts, locs, _ = oracle.partition_ptr(rp, 2)
+    assert [int(p["start_flag"]) for p in parts] == [0, 1]
+    # the paper's printed merge (Alg. 3 l.9-17) would give 4.0 here (reading R6): keep it failing
+    py = s["part_sums"]; y = s["y"][0]; beta = s["beta"]
+    y_alg3 = py[0]
+    tmp = y_alg3; y_alg3 = py[1]; y_alg3 -= tmp * beta
+    assert y_alg3 == 4.0 and s["expect"][0] != y_alg3
+
+
+@pytest.mark.parametrize("N,np_", [(1, 8), (13, 8), (64, 7), (5, 9)])
+def test_chain_row(N, np_):
+    """A 1xN all-ones row split over np parts sums to N (reading R10, chains)."""
+    rp = np.array([0, N], np.int64); ci = np.arange(N, dtype=np.int32); v = np.ones(N)
+    assert oracle.exec_csr(1, rp, ci, v, np.ones(N), np.zeros(1), 1.0, 0.0, np_).tolist() == [N]
+    assert oracle.exec_coo(1, np.zeros(N), ci, v, np.ones(N), np.zeros(1), 1.0, 0.0, np_).tolist() == [N]
+
+
+def test_partition_invariants_and_roundtrip_exhaustive_3x3():
+    """Every structure of a 3x3 matrix, np in 1..nnz+2: descriptors valid, owned ranges tile
+    [0,m), aux <= m + 2np, merge(partition) == row_ptr."""
+    m = n = 3
+    for bits in range(1 << 9):
+        mask = np.array([(bits >> k) & 1 for k in range(9)], bool).reshape(3, 3)
+        r, c = np.nonzero(mask)
+        rp, _, _ = oracle.coo_to_csr(m, r, c, np.ones(r.size))
+        nnz = int(rp[-1])
+        for np_ in range(1, nnz + 3):
+            _check_roundtrip(m, rp, np_)
+
+
+def test_partition_roundtrip_random_5x5_and_larger():
+    rng = np.random.default_rng(5)
+    for trial in range(300):
+        m = int(rng.integers(1, 6)) if trial < 200 else int(rng.integers(6, 80))
+        n = int(rng.integers(1, 6)) if trial < 200 else int(rng.integers(6, 80))
+        mask = rng.random((m, n)) < rng.choice([0.1, 0.4, 0.8])
+        r, c = np.nonzero(mask)
+        rp, _, _ = oracle.coo_to_csr(m, r, c, np.ones(r.size))
+        for np_ in range(1, min(int(rp[-1]) + 3, 40)):
+            _check_roundtrip(m, rp, np_)
+
+
+def _check_roundtrip(m, rp, np_):
+    parts, locs, flat = oracle.partition_ptr(rp, np_)
+    nnz = int(rp[-1])
+    assert flat.size <= m + 2 * np_
+    # exact tiling of [0,nnz) and balance
+    assert parts["start_idx"][0] == 0 and parts["end_idx"][-1] == nnz - 1
+    assert np.all(parts["start_idx"][1:] == parts["end_idx"][:-1] + 1)
+    # owned ranges tile [0,m) disjointly and each row is owned by the part holding row_ptr[r]
+    ob, oe = parts["owned_begin"], parts["owned_end"]
+    assert ob[0] == 0 and oe[-1] == m and np.all(ob[1:] == oe[:-1]) and np.all(oe >= ob)
+    b = oracle.nnz_boundaries(nnz, np_)
+    for r in range(m):
+        i = int(np.searchsorted(ob, r, side="right") - 1)
+        while oe[i] <= r:
+            i += 1
+        if rp[r] < nnz:
+            assert b[i] <= rp[r] < b[i + 1]
+        else:
+            assert i == np_ - 1
+    for i, p in enumerate(parts):
+        if p["start_row"] < 0:
+            assert p["start_idx"] == p["end_idx"] + 1 and locs[i].tolist() == [0]
+            continue
+        assert rp[p["start_row"]] <= p["start_idx"] < rp[p["start_row"] + 1]
+        assert rp[p["end_row"]] <= p["end_idx"] < rp[p["end_row"] + 1]
+        assert p["start_flag"] == (p["start_idx"] > rp[p["start_row"]])
+        loc = locs[i]
+        assert loc[0] == 0 and loc[-1] == p["end_idx"] - p["start_idx"] + 1 and np.all(np.diff(loc) >= 0)
+    # flag inference: part's last row continues iff the next non-empty part is flagged
+    nonempty = [p for p in parts if p["start_row"] >= 0]
+    for a, bq in zip(nonempty, nonempty[1:]):
+        cont = rp[a["end_row"] + 1] > a["end_idx"] + 1
+        assert bool(bq["start_flag"]) == bool(cont)
+        if cont:
+            assert bq["start_row"] == a["end_row"]
+    assert np.array_equal(oracle.merge_parts_to_ptr(m, parts, flat), rp)
+
+
+def test_coo_partition_matches_csr_partition():
+    rng = np.random.default_rng(9)
+    for trial in range(100):
+        m, n = rng.integers(1, 30, 2)
+        r, c, v = random_matrix(rng, m, n, 0.2)
+        rp, _, _ = oracle.coo_to_csr(m, r, c, v)
+        for np_ in range(1, 12):
+            pc = oracle.partition_coo(m, r, np_)
+            pr, _, _ = oracle.partition_ptr(rp, np_)
+            for k in ("start_idx", "end_idx", "start_row", "end_row", "start_flag", "owned_begin",
+                      "owned_end"):
+                assert np.array_equal(pc[k], pr[k]), (k, trial, np_)
