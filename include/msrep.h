@@ -1,0 +1,176 @@
+/*
+ * msrep.h -- C ABI of the B200-native msRep hot path (arXiv 2209.07552):
+ * nnz-balanced multi-GPU SpMV  y <- alpha*A*x + beta*y  over the paper's
+ * augmented formats pCSR, pCSC and pCOO.
+ *
+ * Citations: P:a-b = PAPER.md lines, S:a-b = SPEC.md lines.
+ *
+ *   problem statement       y = alpha*A*x + beta*y              P:203-218 (Alg. 1)
+ *   nnz split               b_i = floor(i*nnz/np)                P:311-312 (Alg. 2 l.2-3)
+ *   pCSR / pCSC / pCOO      Alg. 2 / Alg. 4 / Alg. 6
+ *   launch + merge          Alg. 3 / Alg. 5 / Alg. 7
+ *   row / column merge      Sec. 4.3
+ *   one worker per GPU      Sec. 3.3
+ *
+ * No exceptions cross this boundary.  Every call returns msrep_status_t; on a
+ * failure msrep_last_error() returns a thread-local message.  Arguments are
+ * validated before any device work.  All device work is enqueued on the
+ * caller's CUDA stream (a cudaStream_t passed as void*; NULL = legacy default
+ * stream) and is asynchronous with CUDA semantics unless stated otherwise.
+ *
+ * Data types: host pointer arrays are int64; device index arrays are int32
+ * (m, n < 2^31 and per-rank nnz < 2^31, else MSREP_ERR_TOO_LARGE).  Values are
+ * fp64 or fp32 storage; every sum is accumulated in fp64 and rounded once to
+ * the storage type (reading R13).
+ */
+#ifndef MSREP_H_
+#define MSREP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MSREP_VERSION_MAJOR 0
+#define MSREP_VERSION_MINOR 1
+
+typedef struct msrep_ctx_s* msrep_ctx;
+
+/* Storage format of the caller's global matrix (Sec. 2.1).
+ * MSREP_COO must be sorted by row (ties by column), "we assume the elements
+ * are sorted by rows"; otherwise MSREP_ERR_UNSORTED_COO. */
+typedef enum { MSREP_CSR = 0, MSREP_CSC = 1, MSREP_COO = 2 } msrep_format;
+
+typedef enum { MSREP_F64 = 0, MSREP_F32 = 1 } msrep_dtype;
+
+/* Where y ends up after msrep_spmv (reading R19; the paper merges
+ * into CPU memory).
+ *  REPLICATED: every rank's y[0..m) holds the full result.
+ *              pCSR/pCOO: boundary fix-up + allgatherv of owned row segments.
+ *              pCSC: reduce-scatter of partial y + epilogue + allgatherv.
+ *  OWNED:      pCSR/pCOO only: rank writes exactly its owned rows
+ *              [owned_begin of its first part, owned_end of its last part).
+ *  SHARDED:    pCSC only: rank writes rows [r*ceil(m/R), min(m,(r+1)*ceil(m/R))).
+ * Rows a rank does not write are left untouched. */
+typedef enum { MSREP_Y_REPLICATED = 0, MSREP_Y_OWNED = 1, MSREP_Y_SHARDED = 2 } msrep_layout;
+
+typedef enum {
+  MSREP_OK = 0,
+  MSREP_ERR_INVALID_ARG = 1,
+  MSREP_ERR_DIM_MISMATCH = 2,   /* ptr[0] != 0, ptr[last] != nnz, decreasing ptr, index out of range */
+  MSREP_ERR_UNSORTED_COO = 3,
+  MSREP_ERR_TOO_LARGE = 4,      /* m or n >= 2^31, or a rank's nnz >= 2^31 - 2^16 */
+  MSREP_ERR_STATE = 5,          /* spmv before partition, layout invalid for the format, ... */
+  MSREP_ERR_OOM = 6,
+  MSREP_ERR_CUDA = 7,
+  MSREP_ERR_NCCL = 8
+} msrep_status_t;
+
+/* One part's descriptor, Alg. 2 / 4 / 6 outputs.
+ * For pCSC, start_row/end_row hold start_col/end_col and owned_* are the
+ * column-free uniform row shards are not described here (owned_* = 0,0). */
+typedef struct {
+  int64_t start_idx, end_idx;     /* inclusive nonzero range (Alg. 2 l.2-3); empty part: start_idx == end_idx + 1 */
+  int64_t start_row, end_row;     /* strict owners of start_idx / end_idx (reading R3); -1,-1 for an empty part   */
+  int32_t start_flag;             /* first row/col is shared with an earlier part (Alg. 2 l.6-10)                  */
+  int32_t reserved;               /* 0                                                                             */
+  int64_t owned_begin, owned_end; /* rows [R_i, R_{i+1}) this part writes (reading R9; row formats only)            */
+} msrep_part_desc;
+
+/* Optional device allocator (NULL -> cudaMalloc/cudaFree). */
+typedef struct {
+  void* (*alloc)(size_t bytes, void* stream, void* user);
+  void (*free)(void* p, size_t bytes, void* stream, void* user);
+  void* user;
+} msrep_allocator;
+
+/* Per-rank facts about the current partition, for measurement. */
+typedef struct {
+  int64_t nparts, nranks, parts_per_rank;
+  int64_t nnz_rank;          /* nonzeros held by this rank                                   */
+  int64_t rows_window;       /* rows the rank's local pointer spans (rows_p)                 */
+  int64_t owned_rows;        /* rows this rank writes under OWNED (row formats)              */
+  int64_t distinct_cols;     /* X_p: distinct x entries the rank's nonzeros touch            */
+  int64_t ntiles, nslabs, nsplit_rows, nheads_local;
+  int64_t alg_bytes;         /* algorithmic HBM bytes of one msrep_spmv on this rank, beta!=0 */
+  int64_t alg_bytes_beta0;   /* same with beta == 0 (y_in not read)                          */
+  int64_t kernels_per_spmv;  /* kernel launches one msrep_spmv makes on this rank (beta!=0)  */
+  int64_t device_bytes;      /* device memory held by the partition                          */
+  double partition_ms;       /* host + upload time of the last msrep_partition (wall clock)  */
+} msrep_stats;
+
+/* NCCL unique id for the communicator (rank 0 creates it, the caller
+ * broadcasts the 128 bytes, e.g. through torch.distributed).  Not needed when
+ * nranks == 1. */
+msrep_status_t msrep_get_unique_id(uint8_t id[128]);
+
+/* Create a context for one rank (one process per GPU, Sec. 3.3 P:529 reshaped
+ * as SPMD).  nranks*parts_per_rank = np partitions; this rank holds parts
+ * [rank*parts_per_rank, (rank+1)*parts_per_rank).  parts_per_rank > 1 runs
+ * several of the paper's partitions on one GPU ("virtual parts") and exercises
+ * the identical merge path; results are bit-identical to the same np spread
+ * over more ranks for pCSR/pCOO.  `id` is ignored when nranks == 1.
+ * Makes `device` current on the calling thread. */
+msrep_status_t msrep_create(msrep_ctx* out, int rank, int nranks, const uint8_t id[128], int device,
+                            int parts_per_rank, const msrep_allocator* alloc);
+
+/* Partition the caller's global matrix with Alg. 2/4/6 and upload this rank's
+ * contiguous nonzero range to its GPU (the only host->device transfer of A).
+ *   CSR: ptr = row_ptr[m+1], idx = col_idx[nnz], coo_row = NULL
+ *   CSC: ptr = col_ptr[n+1], idx = row_idx[nnz], coo_row = NULL
+ *   COO: ptr = NULL,         idx = col_idx[nnz], coo_row = row_idx[nnz] (row-sorted)
+ *   val = [nnz] of dtype.
+ * All host arrays are borrowed read-only for the duration of the call (the
+ * call synchronises `stream` before returning).  parts_out, if not NULL,
+ * receives all np descriptors.  Replaces any previous partition.  Every rank
+ * must call it with identical arguments. */
+msrep_status_t msrep_partition(msrep_ctx ctx, msrep_format fmt, msrep_dtype dtype, int64_t m, int64_t n,
+                               int64_t nnz, const int64_t* ptr, const int32_t* idx, const int32_t* coo_row,
+                               const void* val, msrep_part_desc* parts_out, void* stream);
+
+/* y <- alpha*A*x + beta*y on device memory.  alpha, beta: host
+ * scalars of the partition's dtype.  x: device [n], identical on every rank
+ * (pCSC reads only its column slice).  y: device [m], in/out.  beta == 0:
+ * y_in is not read; alpha == 0: y = beta*y_in and A, x are not read
+ * (reading R12).  Collective over ranks when nranks > 1 (all ranks must call
+ * it with the same layout and scalars). */
+msrep_status_t msrep_spmv(msrep_ctx ctx, const void* alpha, const void* x, const void* beta, void* y,
+                          msrep_layout layout, void* stream);
+
+/* End-to-end variant with HOST vectors: copies x[n] and (if beta != 0) y[m]
+ * from host memory (pinned recommended) to context-owned device buffers,
+ * runs msrep_spmv, and copies back the rows this rank's layout defines into
+ * y.  Synchronous: returns after y is written. */
+msrep_status_t msrep_spmv_host(msrep_ctx ctx, const void* alpha, const void* x_host, const void* beta,
+                               void* y_host, msrep_layout layout, void* stream);
+
+/* Pure host: the np descriptors of Alg. 2/4 (fmt CSR/CSC, ptr = pointer array
+ * of length outer+1) or Alg. 6 (fmt COO, coo_row = row_idx[nnz], m = rows).
+ * Used for bit-exact parity with the oracle.  No device, no context. */
+msrep_status_t msrep_plan(msrep_format fmt, int64_t outer, int64_t nnz, int np, const int64_t* ptr,
+                          const int32_t* coo_row, msrep_part_desc* parts_out);
+
+msrep_status_t msrep_get_stats(msrep_ctx ctx, msrep_stats* out);
+
+/* Measurement hook (bench.py's roofline): while enabled, every msrep_spmv
+ * records a CUDA event pair on the caller's stream around its dominant kernel
+ * (the pCSR/pCOO tile kernel, or the pCSC scatter).  msrep_profile_read
+ * synchronises those events and returns the summed device time (ms) and the
+ * number of timed launches since the last reset. */
+msrep_status_t msrep_profile_enable(msrep_ctx ctx, int enable);
+msrep_status_t msrep_profile_read(msrep_ctx ctx, double* kernel_ms, int64_t* launches, int reset);
+
+/* NULL-safe; frees device buffers and the communicator. */
+msrep_status_t msrep_destroy(msrep_ctx ctx);
+
+/* Thread-local message for the last failure on this thread ("" if none). */
+const char* msrep_last_error(void);
+
+int msrep_version(void); /* MSREP_VERSION_MAJOR*100 + MSREP_VERSION_MINOR */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MSREP_H_ */

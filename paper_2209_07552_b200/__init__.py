@@ -1,0 +1,247 @@
+"""Python binding of libmsrep (include/msrep.h): B200-native nnz-balanced SpMV
+over the augmented formats pCSR / pCSC / pCOO of msRep (arXiv 2209.07552).
+
+Argument marshalling only: every step of the hot path runs in the CUDA kernels
+of ``csrc/``.  There is no CPU fallback -- importing this package without the
+built ``libmsrep.so`` raises.  PyTorch is used by callers for device memory,
+streams and ``torch.distributed`` (the NCCL unique-id broadcast); this module
+itself needs only ctypes + numpy.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmsrep.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libmsrep.so not built at {LIB_PATH}: run `make` (or __graft_entry__.build()) first")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+# enums (include/msrep.h)
+CSR, CSC, COO = 0, 1, 2
+F64, F32 = 0, 1
+Y_REPLICATED, Y_OWNED, Y_SHARDED = 0, 1, 2
+STATUS = {0: "MSREP_OK", 1: "MSREP_ERR_INVALID_ARG", 2: "MSREP_ERR_DIM_MISMATCH", 3: "MSREP_ERR_UNSORTED_COO",
+          4: "MSREP_ERR_TOO_LARGE", 5: "MSREP_ERR_STATE", 6: "MSREP_ERR_OOM", 7: "MSREP_ERR_CUDA",
+          8: "MSREP_ERR_NCCL"}
+FORMATS = {"csr": CSR, "csc": CSC, "coo": COO}
+
+
+class PartDesc(ctypes.Structure):
+    _fields_ = [("start_idx", ctypes.c_int64), ("end_idx", ctypes.c_int64), ("start_row", ctypes.c_int64),
+                ("end_row", ctypes.c_int64), ("start_flag", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("owned_begin", ctypes.c_int64), ("owned_end", ctypes.c_int64)]
+
+
+PART_DTYPE = np.dtype([("start_idx", "<i8"), ("end_idx", "<i8"), ("start_row", "<i8"), ("end_row", "<i8"),
+                       ("start_flag", "<i4"), ("reserved", "<i4"), ("owned_begin", "<i8"), ("owned_end", "<i8")])
+assert PART_DTYPE.itemsize == ctypes.sizeof(PartDesc)
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_int64) for k in (
+        "nparts", "nranks", "parts_per_rank", "nnz_rank", "rows_window", "owned_rows", "distinct_cols", "ntiles",
+        "nslabs", "nsplit_rows", "nheads_local", "alg_bytes", "alg_bytes_beta0", "kernels_per_spmv",
+        "device_bytes")] + [("partition_ms", ctypes.c_double)]
+
+
+class Allocator(ctypes.Structure):
+    _fields_ = [("alloc", ctypes.c_void_p), ("free", ctypes.c_void_p), ("user", ctypes.c_void_p)]
+
+
+class MsrepError(RuntimeError):
+    def __init__(self, status, where):
+        self.status = status
+        super().__init__(f"{where}: {STATUS.get(status, status)}: {msrep_last_error()}")
+
+
+P, I64, I32, I = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int
+_sig = {
+    "msrep_get_unique_id": [P],
+    "msrep_create": [ctypes.POINTER(P), I, I, P, I, I, P],
+    "msrep_partition": [P, I, I, I64, I64, I64, P, P, P, P, P, P],
+    "msrep_spmv": [P, P, P, P, P, I, P],
+    "msrep_spmv_host": [P, P, P, P, P, I, P],
+    "msrep_plan": [I, I64, I64, I, P, P, P],
+    "msrep_get_stats": [P, ctypes.POINTER(Stats)],
+    "msrep_destroy": [P],
+    "msrep_profile_enable": [P, I],
+    "msrep_profile_read": [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64), I],
+}
+for _k, _a in _sig.items():
+    getattr(_lib, _k).argtypes = _a
+    getattr(_lib, _k).restype = ctypes.c_int
+_lib.msrep_last_error.argtypes = []
+_lib.msrep_last_error.restype = ctypes.c_char_p
+_lib.msrep_version.argtypes = []
+_lib.msrep_version.restype = ctypes.c_int
+
+EXPORTED = ["msrep_get_unique_id", "msrep_create", "msrep_partition", "msrep_spmv", "msrep_spmv_host",
+            "msrep_plan", "msrep_get_stats", "msrep_destroy", "msrep_last_error", "msrep_version",
+            "msrep_profile_enable", "msrep_profile_read"]
+
+
+def _check(status, where):
+    if status != 0:
+        raise MsrepError(status, where)
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if isinstance(a, int):
+        return a
+    if hasattr(a, "data_ptr"):           # torch tensor
+        return a.data_ptr()
+    return a.ctypes.data
+
+
+# ------------------------------------------------------------ C-ABI mirrors
+def msrep_last_error() -> str:
+    return _lib.msrep_last_error().decode()
+
+
+def msrep_version() -> int:
+    return _lib.msrep_version()
+
+
+def msrep_get_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _check(_lib.msrep_get_unique_id(ctypes.cast(buf, P)), "msrep_get_unique_id")
+    return bytes(buf)
+
+
+def msrep_create(rank=0, nranks=1, uid: bytes | None = None, device=0, parts_per_rank=1):
+    h = P()
+    idbuf = None
+    if uid is not None:
+        idbuf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+    _check(_lib.msrep_create(ctypes.byref(h), rank, nranks, ctypes.cast(idbuf, P) if idbuf is not None else None,
+                             device, parts_per_rank, None), "msrep_create")
+    return h
+
+
+def msrep_partition(ctx, fmt, dtype, m, n, nnz, ptr, idx, coo_row, val, stream=None, want_parts=True, nparts=None):
+    """Host numpy arrays in: ptr int64 (CSR/CSC), idx int32, coo_row int32 (COO), val float64/float32."""
+    parts = np.zeros(nparts, PART_DTYPE) if (want_parts and nparts) else None
+    _check(_lib.msrep_partition(ctx, fmt, dtype, m, n, nnz, _ptr(ptr), _ptr(idx), _ptr(coo_row), _ptr(val),
+                                _ptr(parts), stream), "msrep_partition")
+    return parts
+
+
+def _scalar(v, dtype):
+    return (ctypes.c_double(v) if dtype == F64 else ctypes.c_float(v))
+
+
+def msrep_spmv(ctx, alpha, x, beta, y, layout=Y_REPLICATED, stream=None, dtype=F64):
+    a, b = _scalar(alpha, dtype), _scalar(beta, dtype)
+    _check(_lib.msrep_spmv(ctx, ctypes.byref(a), _ptr(x), ctypes.byref(b), _ptr(y), layout, stream), "msrep_spmv")
+
+
+def msrep_spmv_host(ctx, alpha, x_host, beta, y_host, layout=Y_REPLICATED, stream=None, dtype=F64):
+    a, b = _scalar(alpha, dtype), _scalar(beta, dtype)
+    _check(_lib.msrep_spmv_host(ctx, ctypes.byref(a), _ptr(x_host), ctypes.byref(b), _ptr(y_host), layout, stream),
+           "msrep_spmv_host")
+
+
+def msrep_plan(fmt, outer, nnz, np_, ptr=None, coo_row=None):
+    parts = np.zeros(np_, PART_DTYPE)
+    if ptr is not None:
+        ptr = np.ascontiguousarray(ptr, np.int64)
+    if coo_row is not None:
+        coo_row = np.ascontiguousarray(coo_row, np.int32)
+    _check(_lib.msrep_plan(fmt, outer, nnz, np_, _ptr(ptr), _ptr(coo_row), _ptr(parts)), "msrep_plan")
+    return parts
+
+
+def msrep_get_stats(ctx) -> dict:
+    s = Stats()
+    _check(_lib.msrep_get_stats(ctx, ctypes.byref(s)), "msrep_get_stats")
+    return {k: getattr(s, k) for k, _ in Stats._fields_}
+
+
+def msrep_profile_enable(ctx, enable=True):
+    _check(_lib.msrep_profile_enable(ctx, int(bool(enable))), "msrep_profile_enable")
+
+
+def msrep_profile_read(ctx, reset=True):
+    ms, n = ctypes.c_double(), I64()
+    _check(_lib.msrep_profile_read(ctx, ctypes.byref(ms), ctypes.byref(n), int(bool(reset))), "msrep_profile_read")
+    return ms.value, n.value
+
+
+def msrep_destroy(ctx):
+    _check(_lib.msrep_destroy(ctx), "msrep_destroy")
+
+
+# ------------------------------------------------------------ convenience
+class Context:
+    """One rank's msrep context.  ``Context.from_torch_dist()`` creates the NCCL
+    communicator from an initialised torch.distributed process group (rank 0's
+    unique id is broadcast through it).  All device vectors are torch tensors."""
+
+    def __init__(self, rank=0, nranks=1, uid=None, device=0, parts_per_rank=1):
+        self.rank, self.nranks, self.device, self.parts_per_rank = rank, nranks, device, parts_per_rank
+        self.h = msrep_create(rank, nranks, uid, device, parts_per_rank)
+        self.dtype = F64
+        self.fmt = CSR
+        self.parts = None
+        self.m = self.n = self.nnz = 0
+
+    @classmethod
+    def from_torch_dist(cls, device=None, parts_per_rank=1):
+        import torch
+        import torch.distributed as dist
+        rank, world = dist.get_rank(), dist.get_world_size()
+        if device is None:
+            device = torch.cuda.current_device()
+        uid = None
+        if world > 1:
+            obj = [msrep_get_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            uid = obj[0]
+        return cls(rank, world, uid, device, parts_per_rank)
+
+    def partition(self, fmt, m, n, ptr=None, idx=None, val=None, coo_row=None, stream=None):
+        if isinstance(fmt, str):
+            fmt = FORMATS[fmt]
+        val = np.ascontiguousarray(val)
+        dtype = F64 if val.dtype == np.float64 else F32
+        idx = np.ascontiguousarray(idx, np.int32)
+        nnz = idx.size
+        if ptr is not None:
+            ptr = np.ascontiguousarray(ptr, np.int64)
+        if coo_row is not None:
+            coo_row = np.ascontiguousarray(coo_row, np.int32)
+        self.parts = msrep_partition(self.h, fmt, dtype, m, n, nnz, ptr, idx, coo_row, val, stream,
+                                     nparts=self.nranks * self.parts_per_rank)
+        self.dtype, self.fmt, self.m, self.n, self.nnz = dtype, fmt, m, n, nnz
+        return self.parts
+
+    def spmv(self, alpha, x, beta, y, layout=Y_REPLICATED, stream=None):
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream().cuda_stream
+        msrep_spmv(self.h, alpha, x, beta, y, layout, stream, self.dtype)
+
+    def spmv_host(self, alpha, x_host, beta, y_host, layout=Y_REPLICATED, stream=None):
+        msrep_spmv_host(self.h, alpha, x_host, beta, y_host, layout, stream, self.dtype)
+
+    def stats(self):
+        return msrep_get_stats(self.h)
+
+    def close(self):
+        if self.h:
+            msrep_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,787 @@
+// host.cpp -- host runtime of libmsrep: the nnz-balanced partitioner (Alg. 2 /
+// 4 / 6), the static tile schedule, device placement of each rank's slice, the
+// NCCL merge (Sec. 4.3 reshaped for NVLink), and the C ABI of include/msrep.h.
+//
+// One process per GPU (Sec. 3.3: "one dedicated CPU thread to manage
+// one GPU", reshaped as SPMD ranks).  Each rank computes all np descriptors
+// (O(np log m)), keeps only its own contiguous nonzero range on its GPU, and
+// exchanges only split-row partials and, for REPLICATED y, its
+// owned y segment.
+#include <algorithm>
+#include <chrono>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include "internal.h"
+#include "msrep.h"
+
+using namespace msrep;
+
+namespace {
+
+thread_local std::string g_err;
+
+msrep_status_t fail(msrep_status_t s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define CUDA_TRY(expr)                                                                             \
+  do {                                                                                             \
+    cudaError_t e_ = (expr);                                                                       \
+    if (e_ != cudaSuccess) return fail(MSREP_ERR_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+#define NCCL_TRY(expr)                                                                             \
+  do {                                                                                             \
+    ncclResult_t r_ = (expr);                                                                      \
+    if (r_ != ncclSuccess) return fail(MSREP_ERR_NCCL, "%s: %s", #expr, ncclGetErrorString(r_));   \
+  } while (0)
+#define TRY(expr)                                                                                  \
+  do {                                                                                             \
+    msrep_status_t s_ = (expr);                                                                    \
+    if (s_ != MSREP_OK) return s_;                                                                 \
+  } while (0)
+
+constexpr int64_t kMaxIdx = (int64_t)1 << 31;
+constexpr int64_t kMaxRankNnz = kMaxIdx - (1 << 16);
+
+// ------------------------------------------------------------ descriptors
+// b_i = floor(i*nnz/np) (Alg. 2 l.2-3).
+inline int64_t boundary(int64_t i, int64_t nnz, int64_t np) { return (i * nnz) / np; }
+
+// Alg. 2/4: BinarySearch -> strict owner upper_bound(ptr, idx) - 1 (reading R3);
+// owned range R_i = lower_bound(ptr[0..outer), b_i), R_0 = 0, R_np = outer (R9).
+void plan_ptr(int64_t outer, int64_t nnz, int np, const int64_t* ptr, msrep_part_desc* P) {
+  for (int i = 0; i < np; i++) {
+    const int64_t b0 = boundary(i, nnz, np), b1 = boundary(i + 1, nnz, np);
+    msrep_part_desc& d = P[i];
+    d.start_idx = b0;
+    d.end_idx = b1 - 1;
+    d.reserved = 0;
+    d.owned_begin = i == 0 ? 0 : (int64_t)(std::lower_bound(ptr, ptr + outer, b0) - ptr);
+    d.owned_end = i == np - 1 ? outer : (int64_t)(std::lower_bound(ptr, ptr + outer, b1) - ptr);
+    if (b0 == b1) {
+      d.start_row = d.end_row = -1;
+      d.start_flag = 0;
+      continue;
+    }
+    d.start_row = (int64_t)(std::upper_bound(ptr, ptr + outer + 1, b0) - ptr) - 1;
+    d.end_row = (int64_t)(std::upper_bound(ptr, ptr + outer + 1, b1 - 1) - ptr) - 1;
+    d.start_flag = b0 > ptr[d.start_row] ? 1 : 0;
+  }
+}
+
+// Alg. 6 on a row-sorted COO (reading R8): rows read from row_idx at the cuts.
+void plan_coo(int64_t m, int64_t nnz, int np, const int32_t* row, msrep_part_desc* P) {
+  for (int i = 0; i < np; i++) {
+    const int64_t b0 = boundary(i, nnz, np), b1 = boundary(i + 1, nnz, np);
+    msrep_part_desc& d = P[i];
+    d.start_idx = b0;
+    d.end_idx = b1 - 1;
+    d.reserved = 0;
+    d.owned_begin = i == 0 ? 0 : (b0 == 0 ? 0 : (int64_t)row[b0 - 1] + 1);
+    d.owned_end = i == np - 1 ? m : (b1 == 0 ? 0 : (int64_t)row[b1 - 1] + 1);
+    if (b0 == b1) {
+      d.start_row = d.end_row = -1;
+      d.start_flag = 0;
+      continue;
+    }
+    d.start_row = row[b0];
+    d.end_row = row[b1 - 1];
+    d.start_flag = (b0 > 0 && row[b0 - 1] == row[b0]) ? 1 : 0;
+  }
+}
+
+// ---------------------------------------------------------------- memory
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct Ctx {
+  int rank = 0, nranks = 1, vparts = 1, np = 1, device = 0;
+  ncclComm_t comm = nullptr;
+  msrep_allocator alloc{};
+  bool has_alloc = false;
+
+  // partition state
+  bool ready = false;
+  msrep_format fmt = MSREP_CSR;
+  msrep_dtype dtype = MSREP_F64;
+  int64_t m = 0, n = 0, nnz = 0;
+  std::vector<msrep_part_desc> parts;
+  int P0 = 0, P1 = 0;               // local parts [P0, P1)
+  int64_t B_lo = 0, B_hi = 0;       // rank nonzero range
+  int64_t wlo = 0, whi = 0;         // window rows (cols for CSC)
+  int64_t own_lo = 0, own_hi = 0;   // rows this rank writes under OWNED
+  bool any_flag = false;            // some part (any rank) has start_flag
+  int64_t shard = 0;                // pCSC: ceil(m / nranks)
+
+  std::vector<DevBuf> bufs;
+  void* d_val = nullptr;
+  int32_t* d_idx = nullptr;
+  int32_t* d_aux = nullptr;         // CSR/CSC local pointer, COO row ids
+  int4* d_tiles = nullptr;
+  int ntiles = 0, nslabs = 0;
+  double* d_rec = nullptr;
+  int nrec = 0;
+  int nsplit = 0;
+  int64_t* d_sr_row = nullptr;
+  int32_t* d_sr_rec = nullptr;
+  int32_t* d_sr_head = nullptr;
+  int32_t* d_head_list = nullptr;
+  int32_t* d_part_rec = nullptr;
+  double* d_head_local = nullptr;
+  double* d_head_all = nullptr;
+  double* d_py = nullptr;
+  int64_t py_len = 0;
+  int nheads_local = 0;
+
+  // host-vector path buffers
+  void* d_hx = nullptr;
+  void* d_hy = nullptr;
+
+  msrep_stats stats{};
+
+  // profiling hook: event pairs around the dominant kernel
+  bool prof = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  size_t ev_used = 0;
+};
+
+msrep_status_t prof_begin(Ctx* c, cudaStream_t s, cudaEvent_t* end) {
+  *end = nullptr;
+  if (!c->prof) return MSREP_OK;
+  if (c->ev_used == c->ev.size()) {
+    cudaEvent_t a, b;
+    CUDA_TRY(cudaEventCreate(&a));
+    CUDA_TRY(cudaEventCreate(&b));
+    c->ev.push_back({a, b});
+  }
+  auto& p = c->ev[c->ev_used++];
+  CUDA_TRY(cudaEventRecord(p.first, s));
+  *end = p.second;
+  return MSREP_OK;
+}
+
+size_t vsz(msrep_dtype t) { return t == MSREP_F64 ? 8 : 4; }
+
+msrep_status_t dalloc(Ctx* c, size_t want, void** out, cudaStream_t s) {
+  const size_t bytes = (want + 16 + 255) & ~(size_t)255;   // +16: tile TMA loads round up to 16 B
+  void* p = nullptr;
+  if (c->has_alloc) {
+    p = c->alloc.alloc(bytes, (void*)s, c->alloc.user);
+    if (!p) return fail(MSREP_ERR_OOM, "allocator returned NULL for %zu bytes", bytes);
+  } else {
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) return fail(e == cudaErrorMemoryAllocation ? MSREP_ERR_OOM : MSREP_ERR_CUDA,
+                                      "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+  }
+  CUDA_TRY(cudaMemsetAsync(static_cast<char*>(p) + want, 0, bytes - want, s));   // padding only
+  c->bufs.push_back({p, bytes});
+  *out = p;
+  return MSREP_OK;
+}
+
+void free_all(Ctx* c) {
+  for (auto& b : c->bufs) {
+    if (c->has_alloc) c->alloc.free(b.p, b.bytes, nullptr, c->alloc.user);
+    else cudaFree(b.p);
+  }
+  c->bufs.clear();
+  c->ready = false;
+  c->d_hx = c->d_hy = nullptr;
+}
+
+template <class T>
+msrep_status_t upload(Ctx* c, const T* host, size_t count, T** out, cudaStream_t s) {
+  void* p;
+  TRY(dalloc(c, count * sizeof(T), &p, s));
+  if (count) CUDA_TRY(cudaMemcpyAsync(p, host, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  *out = static_cast<T*>(p);
+  return MSREP_OK;
+}
+
+// ---------------------------------------------------------- tile schedule
+struct Schedule {
+  std::vector<TileHost> tiles;
+  int nrec = 0, nslabs = 0;
+  std::vector<int64_t> sr_row;
+  std::vector<int32_t> sr_rec, sr_head, head_list, part_rec;
+};
+
+// Per-tile kernel mode for pCSR (w field of a normal tile): -1 = merge-path walk;
+// -2-lg = "vector" mode with 2^lg lanes per row.  Cost model in per-lane serial
+// steps: vector = passes * (ceil(maxlen / L) + lg + 4) with passes =
+// ceil(nrows / (THREADS / L)); merge path ~ 32 steps (search + 8 items + scan).
+int32_t tile_mode(int64_t nrows, int64_t maxlen) {
+  int32_t best = -1;
+  int64_t best_cost = 32;
+  for (int lg = 0; lg <= 5; lg++) {
+    const int64_t L = 1 << lg, G = THREADS >> lg;
+    const int64_t cost = ((nrows + G - 1) / G) * ((maxlen + L - 1) / L + lg + 4);
+    if (cost < best_cost) { best_cost = cost; best = -2 - lg; }
+  }
+  return best;
+}
+
+struct Packer {
+  Schedule& S;
+  int64_t wlo;
+  const std::vector<int64_t>& lp;   // local pointer over the window (rank-local nonzeros)
+  bool vector_ok;                   // pCSR tiles may use the vector mode
+  int64_t cur_r0 = -1, cur_r1 = -1, cur_max = 0;
+  explicit Packer(Schedule& s, int64_t w, const std::vector<int64_t>& l, bool v = false)
+      : S(s), wlo(w), lp(l), vector_ok(v) {}
+  int64_t ls(int64_t r) const { return lp[(size_t)(r - wlo)]; }
+  int64_t le(int64_t r) const { return lp[(size_t)(r - wlo + 1)]; }
+  void flush() {
+    if (cur_r0 < 0) return;
+    const int64_t nrows = cur_r1 - cur_r0, z0 = ls(cur_r0), nz = le(cur_r1 - 1) - z0;
+    const int32_t mode = vector_ok ? tile_mode(nrows, cur_max) : -1;
+    S.tiles.push_back({(int32_t)(cur_r0 - wlo), (int32_t)z0, (int32_t)(nrows | (nz << 16)), mode});
+    cur_r0 = cur_r1 = -1;
+    cur_max = 0;
+  }
+  void add_row(int64_t r) {
+    const int64_t len = le(r) - ls(r);
+    if (cur_r0 >= 0) {
+      const int64_t items = (cur_r1 - cur_r0) + (le(cur_r1 - 1) - ls(cur_r0));
+      if (items + len + 1 > TILE_ITEMS) flush();
+    }
+    if (cur_r0 < 0) { cur_r0 = r; cur_r1 = r; }
+    cur_r1 = r + 1;
+    cur_max = std::max(cur_max, len);
+  }
+  // slabs over rank-local nonzeros [z0, z1) of row r; with_records: write partial sums to records
+  void slabs(int64_t r, int64_t z0, int64_t z1, bool with_records) {
+    for (int64_t z = z0; z < z1; z += SLAB_NNZ) {
+      const int64_t nz = std::min<int64_t>(SLAB_NNZ, z1 - z);
+      S.tiles.push_back({(int32_t)(r - wlo), (int32_t)z, (int32_t)(1 | (nz << 16)), with_records ? S.nrec++ : -1});
+      S.nslabs++;
+    }
+  }
+};
+
+// Row formats (pCSR, pCOO): one rank's schedule.  Per local part j, in order:
+// head slabs (flagged first row, exported to its owner), the owned rows
+// [R_j, R_{j+1}) packed into row-aligned tiles (rows longer than a tile become
+// slab-split rows), and the tail row (owned, continues into later parts) as
+// slabs whose fix-up adds the head partials of the parts that continue it.
+void build_row_schedule(const Ctx& c, const std::vector<int64_t>& lp, Schedule& S) {
+  Packer pk(S, c.wlo, lp, c.fmt == MSREP_CSR);
+  const auto& P = c.parts;
+  for (int j = c.P0; j < c.P1; j++) {
+    const msrep_part_desc& d = P[(size_t)j];
+    const bool empty = d.start_idx > d.end_idx;
+    const int64_t lz1 = d.end_idx + 1 - c.B_lo;
+    int32_t h0 = S.nrec;
+    if (!empty && d.start_flag) {
+      const int64_t r = d.start_row, z0 = d.start_idx - c.B_lo;
+      pk.slabs(r, z0, std::min<int64_t>(lz1, pk.le(r)), true);
+    }
+    S.part_rec.push_back(h0);
+    S.part_rec.push_back(S.nrec);
+    // tail: the next non-empty part is flagged and starts in our last owned row
+    int64_t tail = -1;
+    std::vector<int32_t> chain;
+    if (!empty && d.owned_end > d.owned_begin) {
+      const int64_t last = d.owned_end - 1;
+      for (int q = j + 1; q < c.np; q++) {
+        const msrep_part_desc& e = P[(size_t)q];
+        if (e.start_idx > e.end_idx) continue;
+        if (e.start_flag && e.start_row == last) { chain.push_back(q); continue; }
+        break;
+      }
+      if (!chain.empty()) tail = last;
+    }
+    const int64_t rend = tail >= 0 ? tail : d.owned_end;
+    for (int64_t r = d.owned_begin; r < rend; r++) {
+      const int64_t len = pk.le(r) - pk.ls(r);
+      if (len + 1 > TILE_ITEMS) {
+        pk.flush();
+        S.sr_row.push_back(r);
+        S.sr_rec.push_back(S.nrec);
+        pk.slabs(r, pk.ls(r), pk.le(r), true);
+        S.sr_rec.push_back(S.nrec);
+        S.sr_head.push_back((int32_t)S.head_list.size());
+        S.sr_head.push_back((int32_t)S.head_list.size());
+      } else {
+        pk.add_row(r);
+      }
+    }
+    pk.flush();
+    if (tail >= 0) {
+      S.sr_row.push_back(tail);
+      S.sr_rec.push_back(S.nrec);
+      pk.slabs(tail, pk.ls(tail), lz1, true);
+      S.sr_rec.push_back(S.nrec);
+      S.sr_head.push_back((int32_t)S.head_list.size());
+      for (int q : chain) S.head_list.push_back(q);
+      S.sr_head.push_back((int32_t)S.head_list.size());
+    }
+  }
+}
+
+// pCSC: column groups / column pieces over the rank's window; every tile scatters.
+void build_col_schedule(const Ctx& c, const std::vector<int64_t>& lp, Schedule& S) {
+  Packer pk(S, c.wlo, lp);
+  for (int64_t col = c.wlo; col < c.whi; col++) {
+    const int64_t len = pk.le(col) - pk.ls(col);
+    if (len + 1 > TILE_ITEMS) {
+      pk.flush();
+      pk.slabs(col, pk.ls(col), pk.le(col), false);
+    } else {
+      pk.add_row(col);
+    }
+  }
+  pk.flush();
+}
+
+template <class T>
+msrep_status_t upload_vec(Ctx* c, const std::vector<T>& v, T** out, cudaStream_t s) {
+  return upload(c, v.data(), v.size(), out, s);
+}
+
+ncclDataType_t nccl_type(msrep_dtype t) { return t == MSREP_F64 ? ncclDouble : ncclFloat; }
+
+// allgatherv of per-rank segments of y (in place), as grouped broadcasts.
+msrep_status_t allgatherv_y(Ctx* c, void* y, const std::vector<int64_t>& lo, const std::vector<int64_t>& hi,
+                            cudaStream_t s) {
+  const size_t V = vsz(c->dtype);
+  NCCL_TRY(ncclGroupStart());
+  for (int r = 0; r < c->nranks; r++) {
+    const int64_t cnt = hi[(size_t)r] - lo[(size_t)r];
+    if (cnt <= 0) continue;
+    char* p = static_cast<char*>(y) + (size_t)lo[(size_t)r] * V;
+    NCCL_TRY(ncclBroadcast(p, p, (size_t)cnt, nccl_type(c->dtype), r, c->comm, s));
+  }
+  NCCL_TRY(ncclGroupEnd());
+  return MSREP_OK;
+}
+
+void owned_segments(const Ctx* c, std::vector<int64_t>& lo, std::vector<int64_t>& hi) {
+  lo.resize((size_t)c->nranks);
+  hi.resize((size_t)c->nranks);
+  for (int r = 0; r < c->nranks; r++) {
+    if (c->fmt == MSREP_CSC) {
+      lo[(size_t)r] = std::min<int64_t>(c->m, (int64_t)r * c->shard);
+      hi[(size_t)r] = std::min<int64_t>(c->m, (int64_t)(r + 1) * c->shard);
+    } else {
+      lo[(size_t)r] = c->parts[(size_t)r * c->vparts].owned_begin;
+      hi[(size_t)r] = c->parts[(size_t)(r + 1) * c->vparts - 1].owned_end;
+    }
+  }
+}
+
+double get_scalar(const void* p, msrep_dtype t) {
+  return t == MSREP_F64 ? *static_cast<const double*>(p) : (double)*static_cast<const float*>(p);
+}
+
+}  // namespace
+
+// ======================================================================= ABI
+extern "C" {
+
+const char* msrep_last_error(void) { return g_err.c_str(); }
+int msrep_version(void) { return MSREP_VERSION_MAJOR * 100 + MSREP_VERSION_MINOR; }
+
+msrep_status_t msrep_get_unique_id(uint8_t id[128]) {
+  if (!id) return fail(MSREP_ERR_INVALID_ARG, "id is NULL");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId u;
+  NCCL_TRY(ncclGetUniqueId(&u));
+  memcpy(id, &u, 128);
+  return MSREP_OK;
+}
+
+msrep_status_t msrep_plan(msrep_format fmt, int64_t outer, int64_t nnz, int np, const int64_t* ptr,
+                          const int32_t* coo_row, msrep_part_desc* parts_out) {
+  if (np < 1 || outer < 0 || nnz < 0 || !parts_out) return fail(MSREP_ERR_INVALID_ARG, "bad plan arguments");
+  if (fmt == MSREP_COO) {
+    if (nnz > 0 && !coo_row) return fail(MSREP_ERR_INVALID_ARG, "COO plan needs row_idx");
+    plan_coo(outer, nnz, np, coo_row, parts_out);
+  } else if (fmt == MSREP_CSR || fmt == MSREP_CSC) {
+    if (!ptr) return fail(MSREP_ERR_INVALID_ARG, "plan needs ptr");
+    if (ptr[0] != 0 || ptr[outer] != nnz) return fail(MSREP_ERR_DIM_MISMATCH, "ptr[0] != 0 or ptr[outer] != nnz");
+    plan_ptr(outer, nnz, np, ptr, parts_out);
+  } else {
+    return fail(MSREP_ERR_INVALID_ARG, "unknown format %d", (int)fmt);
+  }
+  return MSREP_OK;
+}
+
+msrep_status_t msrep_create(msrep_ctx* out, int rank, int nranks, const uint8_t id[128], int device,
+                            int parts_per_rank, const msrep_allocator* alloc) {
+  if (!out) return fail(MSREP_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (nranks < 1 || rank < 0 || rank >= nranks || parts_per_rank < 1)
+    return fail(MSREP_ERR_INVALID_ARG, "bad rank %d / nranks %d / parts_per_rank %d", rank, nranks, parts_per_rank);
+  if (nranks > 1 && !id) return fail(MSREP_ERR_INVALID_ARG, "nranks > 1 needs an NCCL unique id");
+  if (alloc && (!alloc->alloc || !alloc->free)) return fail(MSREP_ERR_INVALID_ARG, "allocator needs alloc and free");
+  CUDA_TRY(cudaSetDevice(device));
+  Ctx* c = new Ctx();
+  c->rank = rank;
+  c->nranks = nranks;
+  c->vparts = parts_per_rank;
+  c->np = nranks * parts_per_rank;
+  c->device = device;
+  if (alloc) { c->alloc = *alloc; c->has_alloc = true; }
+  if (nranks > 1) {
+    ncclUniqueId u;
+    memcpy(&u, id, 128);
+    ncclResult_t r = ncclCommInitRank(&c->comm, nranks, u, rank);
+    if (r != ncclSuccess) {
+      delete c;
+      return fail(MSREP_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+    }
+  }
+  *out = reinterpret_cast<msrep_ctx>(c);
+  return MSREP_OK;
+}
+
+msrep_status_t msrep_destroy(msrep_ctx h) {
+  if (!h) return MSREP_OK;
+  Ctx* c = reinterpret_cast<Ctx*>(h);
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  free_all(c);
+  for (auto& p : c->ev) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
+  if (c->comm) ncclCommDestroy(c->comm);
+  delete c;
+  return MSREP_OK;
+}
+
+msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype, int64_t m, int64_t n, int64_t nnz,
+                               const int64_t* ptr, const int32_t* idx, const int32_t* coo_row, const void* val,
+                               msrep_part_desc* parts_out, void* stream) {
+  if (!h) return fail(MSREP_ERR_INVALID_ARG, "ctx is NULL");
+  Ctx* c = reinterpret_cast<Ctx*>(h);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const auto t0 = std::chrono::steady_clock::now();
+  // ---- validation (before any device work)
+  if (fmt != MSREP_CSR && fmt != MSREP_CSC && fmt != MSREP_COO) return fail(MSREP_ERR_INVALID_ARG, "format %d", (int)fmt);
+  if (dtype != MSREP_F64 && dtype != MSREP_F32) return fail(MSREP_ERR_INVALID_ARG, "dtype %d", (int)dtype);
+  if (m < 0 || n < 0 || nnz < 0) return fail(MSREP_ERR_INVALID_ARG, "negative dimension");
+  if (m >= kMaxIdx || n >= kMaxIdx) return fail(MSREP_ERR_TOO_LARGE, "m, n must be < 2^31");
+  if (nnz > 0 && (!idx || !val)) return fail(MSREP_ERR_INVALID_ARG, "idx/val NULL");
+  const int64_t outer = fmt == MSREP_CSC ? n : m, inner = fmt == MSREP_CSC ? m : n;
+  if (fmt == MSREP_COO) {
+    if (nnz > 0 && !coo_row) return fail(MSREP_ERR_INVALID_ARG, "COO needs coo_row");
+    for (int64_t k = 0; k < nnz; k++) {
+      if (coo_row[k] < 0 || coo_row[k] >= m) return fail(MSREP_ERR_DIM_MISMATCH, "row_idx[%lld] out of range", (long long)k);
+      if (k > 0 && (coo_row[k] < coo_row[k - 1] || (coo_row[k] == coo_row[k - 1] && idx[k] < idx[k - 1])))
+        return fail(MSREP_ERR_UNSORTED_COO, "COO not sorted by (row, col) at %lld", (long long)k);
+    }
+  } else {
+    if (!ptr) return fail(MSREP_ERR_INVALID_ARG, "ptr NULL");
+    if (ptr[0] != 0 || ptr[outer] != nnz) return fail(MSREP_ERR_DIM_MISMATCH, "ptr[0] != 0 or ptr[%lld] != nnz", (long long)outer);
+    for (int64_t r = 0; r < outer; r++)
+      if (ptr[r + 1] < ptr[r]) return fail(MSREP_ERR_DIM_MISMATCH, "ptr decreases at %lld", (long long)r);
+  }
+  std::vector<msrep_part_desc> parts((size_t)c->np);
+  if (fmt == MSREP_COO) plan_coo(m, nnz, c->np, coo_row, parts.data());
+  else plan_ptr(outer, nnz, c->np, ptr, parts.data());
+  const int P0 = c->rank * c->vparts, P1 = P0 + c->vparts;
+  const int64_t B_lo = boundary(P0, nnz, c->np), B_hi = boundary(P1, nnz, c->np);
+  if (B_hi - B_lo >= kMaxRankNnz) return fail(MSREP_ERR_TOO_LARGE, "rank holds %lld nonzeros (>= 2^31 - 2^16)", (long long)(B_hi - B_lo));
+  for (int64_t k = B_lo; k < B_hi; k++)
+    if (idx[k] < 0 || idx[k] >= inner) return fail(MSREP_ERR_DIM_MISMATCH, "index %lld out of range", (long long)k);
+
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  free_all(c);
+  c->fmt = fmt; c->dtype = dtype; c->m = m; c->n = n; c->nnz = nnz;
+  c->parts = parts;
+  c->P0 = P0; c->P1 = P1; c->B_lo = B_lo; c->B_hi = B_hi;
+  c->any_flag = false;
+  for (auto& d : parts) c->any_flag |= (d.start_flag != 0);
+  if (parts_out) memcpy(parts_out, parts.data(), parts.size() * sizeof(msrep_part_desc));
+
+  // ---- window and local pointer (clamped form of Alg. 2 l.11-12, reading R5)
+  const size_t V = vsz(dtype);
+  std::vector<int64_t> lp;
+  if (fmt == MSREP_CSC) {
+    int64_t lo = -1, hi = -1;
+    for (int j = P0; j < P1; j++) {
+      if (parts[(size_t)j].start_idx > parts[(size_t)j].end_idx) continue;
+      if (lo < 0) lo = parts[(size_t)j].start_row;
+      hi = parts[(size_t)j].end_row + 1;
+    }
+    if (lo < 0) lo = hi = 0;
+    c->wlo = lo; c->whi = hi;
+    c->own_lo = c->own_hi = 0;
+    c->shard = (m + c->nranks - 1) / c->nranks;
+  } else {
+    int64_t lo = parts[(size_t)P0].owned_begin;
+    for (int j = P0; j < P1; j++) {
+      const auto& d = parts[(size_t)j];
+      if (d.start_idx <= d.end_idx && d.start_flag) lo = std::min(lo, d.start_row);
+    }
+    c->wlo = lo;
+    c->whi = parts[(size_t)P1 - 1].owned_end;
+    c->own_lo = parts[(size_t)P0].owned_begin;
+    c->own_hi = parts[(size_t)P1 - 1].owned_end;
+  }
+  const int64_t W = c->whi - c->wlo;
+  lp.resize((size_t)W + 1);
+  if (fmt == MSREP_COO) {
+    std::fill(lp.begin(), lp.end(), 0);
+    for (int64_t k = B_lo; k < B_hi; k++) lp[(size_t)(coo_row[k] - c->wlo) + 1]++;
+    for (int64_t w = 0; w < W; w++) lp[(size_t)w + 1] += lp[(size_t)w];
+  } else {
+    for (int64_t w = 0; w <= W; w++) {
+      int64_t v = ptr[c->wlo + w];
+      lp[(size_t)w] = std::min(std::max(v, B_lo), B_hi) - B_lo;
+    }
+  }
+
+  // ---- schedule
+  Schedule S;
+  if (fmt == MSREP_CSC) build_col_schedule(*c, lp, S);
+  else build_row_schedule(*c, lp, S);
+  c->ntiles = (int)S.tiles.size();
+  c->nslabs = S.nslabs;
+  c->nrec = S.nrec;
+  c->nsplit = (int)S.sr_row.size();
+
+  // ---- upload this rank's slice (the only H2D of A), and the schedule
+  const int64_t nz_r = B_hi - B_lo;
+  void* vp;
+  TRY(dalloc(c, (size_t)nz_r * V, &vp, s));
+  if (nz_r) CUDA_TRY(cudaMemcpyAsync(vp, static_cast<const char*>(val) + (size_t)B_lo * V, (size_t)nz_r * V, cudaMemcpyHostToDevice, s));
+  c->d_val = vp;
+  TRY(upload(c, idx + B_lo, (size_t)nz_r, &c->d_idx, s));
+  if (fmt == MSREP_COO) {
+    TRY(upload(c, coo_row + B_lo, (size_t)nz_r, &c->d_aux, s));
+  } else {
+    // upload the global pointer slice and rebase on the GPU (Sec. 4.1)
+    int64_t* d_g;
+    TRY(upload(c, ptr + c->wlo, (size_t)W + 1, &d_g, s));
+    void* ap;
+    TRY(dalloc(c, ((size_t)W + 1) * 4, &ap, s));
+    c->d_aux = static_cast<int32_t*>(ap);
+    CUDA_TRY(launch_rebase(d_g, c->d_aux, W + 1, B_lo, B_hi, s));
+  }
+  static_assert(sizeof(TileHost) == sizeof(int4), "tile");
+  TRY(upload(c, reinterpret_cast<const int4*>(S.tiles.data()), S.tiles.size(), &c->d_tiles, s));
+  void* rp;
+  TRY(dalloc(c, (size_t)std::max(1, S.nrec) * 8, &rp, s));
+  c->d_rec = static_cast<double*>(rp);
+  if (fmt != MSREP_CSC) {
+    TRY(upload_vec(c, S.sr_row, &c->d_sr_row, s));
+    TRY(upload_vec(c, S.sr_rec, &c->d_sr_rec, s));
+    TRY(upload_vec(c, S.sr_head, &c->d_sr_head, s));
+    TRY(upload_vec(c, S.head_list, &c->d_head_list, s));
+    TRY(upload_vec(c, S.part_rec, &c->d_part_rec, s));
+    void* hp;
+    TRY(dalloc(c, (size_t)c->vparts * 8, &hp, s));
+    c->d_head_local = static_cast<double*>(hp);
+    if (c->nranks > 1) {
+      TRY(dalloc(c, (size_t)c->np * 8, &hp, s));
+      c->d_head_all = static_cast<double*>(hp);
+    }
+    c->nheads_local = 0;
+    for (int j = P0; j < P1; j++) c->nheads_local += parts[(size_t)j].start_flag ? 1 : 0;
+  } else {
+    c->py_len = c->nranks > 1 ? c->shard * c->nranks : m;
+    void* pp;
+    TRY(dalloc(c, (size_t)std::max<int64_t>(1, c->py_len) * 8, &pp, s));
+    c->d_py = static_cast<double*>(pp);
+  }
+  CUDA_TRY(cudaStreamSynchronize(s));
+  const auto t1 = std::chrono::steady_clock::now();
+
+  // ---- stats (X_p by bitmap; outside the partition timer)
+  msrep_stats& st = c->stats;
+  memset(&st, 0, sizeof st);
+  st.nparts = c->np; st.nranks = c->nranks; st.parts_per_rank = c->vparts;
+  st.nnz_rank = nz_r;
+  st.rows_window = W;
+  st.ntiles = c->ntiles; st.nslabs = c->nslabs; st.nsplit_rows = c->nsplit; st.nheads_local = c->nheads_local;
+  st.partition_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  int64_t X = 0;
+  if (fmt == MSREP_CSC) {
+    X = W;   // pCSC reads x only over its column window
+  } else {
+    std::vector<uint64_t> bits((size_t)(inner + 63) / 64, 0);
+    for (int64_t k = B_lo; k < B_hi; k++) bits[(size_t)idx[k] >> 6] |= 1ull << (idx[k] & 63);
+    for (uint64_t w : bits) X += __builtin_popcountll(w);
+  }
+  st.distinct_cols = X;
+  int64_t base;
+  int64_t own, ybytes_b1, ybytes_b0;
+  if (fmt == MSREP_CSC) {
+    const int64_t rows_out = c->nranks > 1 ? std::min<int64_t>(c->shard, std::max<int64_t>(0, m - (int64_t)c->rank * c->shard)) : m;
+    own = rows_out;
+    base = nz_r * (int64_t)(V + 4) + (W + 1) * 4 + W * (int64_t)V + c->py_len * 8 + rows_out * 8;
+    ybytes_b1 = rows_out * (int64_t)V * 2;
+    ybytes_b0 = rows_out * (int64_t)V;
+  } else {
+    own = c->own_hi - c->own_lo;
+    base = nz_r * (int64_t)(V + 4) + X * (int64_t)V + (fmt == MSREP_COO ? nz_r * 4 : (W + 1) * 4);
+    ybytes_b1 = own * (int64_t)V * 2;
+    ybytes_b0 = own * (int64_t)V;
+  }
+  st.owned_rows = own;
+  st.alg_bytes = base + ybytes_b1;
+  st.alg_bytes_beta0 = base + ybytes_b0;
+  if (fmt == MSREP_CSC) st.kernels_per_spmv = (c->ntiles ? 1 : 0) + 1 /*axpby*/ + 1 /*memset*/;
+  else st.kernels_per_spmv = (c->ntiles ? 1 : 0) + (c->nranks > 1 && c->any_flag ? 1 : 0) + (c->nsplit ? 1 : 0);
+  int64_t db = 0;
+  for (auto& b : c->bufs) db += (int64_t)b.bytes;
+  st.device_bytes = db;
+  c->ready = true;
+  return MSREP_OK;
+}
+
+msrep_status_t msrep_spmv(msrep_ctx h, const void* alpha_p, const void* x, const void* beta_p, void* y,
+                          msrep_layout layout, void* stream) {
+  if (!h) return fail(MSREP_ERR_INVALID_ARG, "ctx is NULL");
+  Ctx* c = reinterpret_cast<Ctx*>(h);
+  if (!c->ready) return fail(MSREP_ERR_STATE, "msrep_spmv before msrep_partition");
+  if (!alpha_p || !beta_p) return fail(MSREP_ERR_INVALID_ARG, "alpha/beta NULL");
+  if ((c->m > 0 && !y) || (c->n > 0 && !x)) return fail(MSREP_ERR_INVALID_ARG, "x/y NULL");
+  if (layout != MSREP_Y_REPLICATED && layout != MSREP_Y_OWNED && layout != MSREP_Y_SHARDED)
+    return fail(MSREP_ERR_INVALID_ARG, "layout %d", (int)layout);
+  if (c->fmt == MSREP_CSC && layout == MSREP_Y_OWNED) return fail(MSREP_ERR_STATE, "OWNED layout is for pCSR/pCOO");
+  if (c->fmt != MSREP_CSC && layout == MSREP_Y_SHARDED) return fail(MSREP_ERR_STATE, "SHARDED layout is for pCSC");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const double alpha = get_scalar(alpha_p, c->dtype), beta = get_scalar(beta_p, c->dtype);
+  const size_t V = vsz(c->dtype);
+  const int dt = c->dtype == MSREP_F64 ? 0 : 1;
+  std::vector<int64_t> seg_lo, seg_hi;
+  owned_segments(c, seg_lo, seg_hi);
+  const int64_t my_lo = seg_lo[(size_t)c->rank], my_hi = seg_hi[(size_t)c->rank];
+  const bool gather = layout == MSREP_Y_REPLICATED && c->nranks > 1;
+
+  if (alpha == 0.0) {   // reading R12: y = beta*y, A and x not read
+    CUDA_TRY(launch_scale(static_cast<char*>(y) + (size_t)my_lo * V, my_hi - my_lo, beta, dt, s));
+    if (gather) TRY(allgatherv_y(c, y, seg_lo, seg_hi, s));
+    return MSREP_OK;
+  }
+
+  if (c->fmt == MSREP_CSC) {
+    CUDA_TRY(cudaMemsetAsync(c->d_py, 0, (size_t)c->py_len * 8, s));
+    ColLaunch L{};
+    L.tiles = c->d_tiles; L.ntiles = c->ntiles;
+    L.val = c->d_val; L.row = c->d_idx; L.cptr = c->d_aux;
+    L.x = x; L.xbase = c->wlo; L.py = c->d_py; L.dtype = dt;
+    L.grid = cols_grid(dt, c->ntiles);
+    cudaEvent_t pe;
+    TRY(prof_begin(c, s, &pe));
+    CUDA_TRY(launch_cols(L, s));
+    if (pe) CUDA_TRY(cudaEventRecord(pe, s));
+    if (c->nranks > 1) {
+      double* shard = c->d_py + (size_t)c->rank * c->shard;
+      NCCL_TRY(ncclReduceScatter(c->d_py, shard, (size_t)c->shard, ncclDouble, ncclSum, c->comm, s));
+      CUDA_TRY(launch_axpby_py(shard, static_cast<char*>(y) + (size_t)my_lo * V, my_hi - my_lo, alpha, beta, dt, s));
+      if (gather) TRY(allgatherv_y(c, y, seg_lo, seg_hi, s));
+    } else {
+      CUDA_TRY(launch_axpby_py(c->d_py, y, c->m, alpha, beta, dt, s));
+    }
+    return MSREP_OK;
+  }
+
+  RowLaunch L{};
+  L.tiles = c->d_tiles; L.ntiles = c->ntiles;
+  L.val = c->d_val; L.col = c->d_idx; L.aux = c->d_aux;
+  L.x = x; L.y = y; L.ybase = c->wlo;
+  L.alpha = alpha; L.beta = beta; L.rec = c->d_rec;
+  L.coo = c->fmt == MSREP_COO; L.dtype = dt;
+  L.grid = rows_grid(dt, L.coo, c->ntiles);
+  cudaEvent_t pe;
+  TRY(prof_begin(c, s, &pe));
+  CUDA_TRY(launch_rows(L, s));
+  if (pe) CUDA_TRY(cudaEventRecord(pe, s));
+  if (c->nranks > 1 && c->any_flag) {
+    HeadLaunch H{c->vparts, c->d_part_rec, c->d_rec, c->d_head_local};
+    CUDA_TRY(launch_heads(H, s));
+    NCCL_TRY(ncclAllGather(c->d_head_local, c->d_head_all, (size_t)c->vparts, ncclDouble, c->comm, s));
+  }
+  if (c->nsplit) {
+    FixupLaunch F{};
+    F.nsplit = c->nsplit;
+    F.sr_row = c->d_sr_row; F.sr_rec = c->d_sr_rec; F.sr_head = c->d_sr_head; F.head_list = c->d_head_list;
+    F.part_rec = c->d_part_rec; F.part_lo = c->P0; F.part_hi = c->P1;
+    F.head_all = c->d_head_all; F.rec = c->d_rec;
+    F.y = y; F.alpha = alpha; F.beta = beta; F.dtype = dt;
+    CUDA_TRY(launch_fixup(F, s));
+  }
+  if (gather) TRY(allgatherv_y(c, y, seg_lo, seg_hi, s));
+  return MSREP_OK;
+}
+
+msrep_status_t msrep_spmv_host(msrep_ctx h, const void* alpha, const void* x_host, const void* beta, void* y_host,
+                               msrep_layout layout, void* stream) {
+  if (!h) return fail(MSREP_ERR_INVALID_ARG, "ctx is NULL");
+  Ctx* c = reinterpret_cast<Ctx*>(h);
+  if (!c->ready) return fail(MSREP_ERR_STATE, "msrep_spmv_host before msrep_partition");
+  if (!alpha || !beta) return fail(MSREP_ERR_INVALID_ARG, "alpha/beta NULL");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t V = vsz(c->dtype);
+  if (!c->d_hx) {
+    TRY(dalloc(c, (size_t)std::max<int64_t>(1, c->n) * V, &c->d_hx, s));
+    TRY(dalloc(c, (size_t)std::max<int64_t>(1, c->m) * V, &c->d_hy, s));
+  }
+  std::vector<int64_t> lo, hi;
+  owned_segments(c, lo, hi);
+  int64_t r0 = lo[(size_t)c->rank], r1 = hi[(size_t)c->rank];
+  if (layout == MSREP_Y_REPLICATED) { r0 = 0; r1 = c->m; }
+  const double b = get_scalar(beta, c->dtype);
+  if (c->n) CUDA_TRY(cudaMemcpyAsync(c->d_hx, x_host, (size_t)c->n * V, cudaMemcpyHostToDevice, s));
+  // y_in: the rows this rank updates (REPLICATED multi-rank: its own segment is enough, peers send the rest)
+  const int64_t i0 = lo[(size_t)c->rank], i1 = hi[(size_t)c->rank];
+  if (b != 0.0 && i1 > i0)
+    CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(c->d_hy) + i0 * V, static_cast<const char*>(y_host) + i0 * V,
+                             (size_t)(i1 - i0) * V, cudaMemcpyHostToDevice, s));
+  TRY(msrep_spmv(h, alpha, c->d_hx, beta, c->d_hy, layout, stream));
+  if (r1 > r0)
+    CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(y_host) + r0 * V, static_cast<char*>(c->d_hy) + r0 * V,
+                             (size_t)(r1 - r0) * V, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return MSREP_OK;
+}
+
+msrep_status_t msrep_profile_enable(msrep_ctx h, int enable) {
+  if (!h) return fail(MSREP_ERR_INVALID_ARG, "ctx is NULL");
+  reinterpret_cast<Ctx*>(h)->prof = enable != 0;
+  return MSREP_OK;
+}
+
+msrep_status_t msrep_profile_read(msrep_ctx h, double* kernel_ms, int64_t* launches, int reset) {
+  if (!h || !kernel_ms || !launches) return fail(MSREP_ERR_INVALID_ARG, "NULL argument");
+  Ctx* c = reinterpret_cast<Ctx*>(h);
+  double tot = 0.0;
+  for (size_t i = 0; i < c->ev_used; i++) {
+    CUDA_TRY(cudaEventSynchronize(c->ev[i].second));
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, c->ev[i].first, c->ev[i].second));
+    tot += ms;
+  }
+  *kernel_ms = tot;
+  *launches = (int64_t)c->ev_used;
+  if (reset) c->ev_used = 0;
+  return MSREP_OK;
+}
+
+msrep_status_t msrep_get_stats(msrep_ctx h, msrep_stats* out) {
+  if (!h || !out) return fail(MSREP_ERR_INVALID_ARG, "NULL argument");
+  Ctx* c = reinterpret_cast<Ctx*>(h);
+  if (!c->ready) return fail(MSREP_ERR_STATE, "no partition");
+  *out = c->stats;
+  return MSREP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,83 @@
+"""Shared test helpers: run the CUDA path through the C ABI and compare with the oracle."""
+import numpy as np
+
+import gen
+import oracle
+
+TAU = {np.float64: 1e-12, np.float32: 1e-5}   # north_star per-row tolerance
+
+
+def coo_of_csr(A):
+    return gen.expand_rows(A)
+
+
+def to_dtype(A, dtype):
+    B = gen.Sparse(A)
+    B["val"] = A["val"].astype(dtype)
+    return B
+
+
+def oracle_ref(A, x, y, alpha, beta):
+    """Oracle y for a CSR or CSC gen.Sparse (plain definition, fp64 accumulation)."""
+    if A["fmt"] == "csr":
+        return oracle.spmv_csr(A["m"], A["ptr"], A["idx"], A["val"], x, y, alpha, beta)
+    return oracle.spmv_csc(A["m"], A["n"], A["ptr"], A["idx"], A["val"], x, y, alpha, beta)
+
+
+def row_bound(A, x, y, alpha, beta):
+    if A["fmt"] == "csc":
+        A = gen.transpose(gen.Sparse(A, val=A["val"].astype(np.float64)))
+        x = x.astype(np.float64); y = y.astype(np.float64)
+        return oracle.row_bound_csr(A["m"], A["ptr"], A["idx"], A["val"], x, y, alpha, beta)
+    return oracle.row_bound_csr(A["m"], A["ptr"], A["idx"], A["val"], x, y, alpha, beta)
+
+
+def assert_close(got, ref, bound, dtype):
+    tau = TAU[np.dtype(dtype).type]
+    got = np.asarray(got, np.float64); ref = np.asarray(ref, np.float64)
+    err = np.abs(got - ref)
+    # fp32 output is rounded once to fp32: allow half an ulp of the result on top of tau*bound
+    slack = tau * bound
+    if np.dtype(dtype) == np.float32:
+        slack = slack + np.abs(ref) * 2.0 ** -24
+    bad = ~(err <= slack)
+    assert not bad.any(), (f"{bad.sum()} rows out of tolerance; first {np.nonzero(bad)[0][:5]}: "
+                           f"got {got[bad][:5]} ref {ref[bad][:5]} bound {bound[bad][:5]}")
+
+
+def run_gpu(A, fmt, x, y, alpha, beta, parts=1, layout=None, host_path=False, ctx=None, repeat=1):
+    """Partition A (gen.Sparse CSR or CSC) as `fmt` on cuda:0 with `parts` virtual parts; return y."""
+    import torch
+    import paper_2209_07552_b200 as M
+    vdt = A["val"].dtype
+    own = ctx is None
+    if own:
+        ctx = M.Context(0, 1, None, 0, parts)
+    if fmt == "csr":
+        assert A["fmt"] == "csr"
+        ctx.partition("csr", A["m"], A["n"], ptr=A["ptr"], idx=A["idx"], val=A["val"])
+    elif fmt == "coo":
+        assert A["fmt"] == "csr"
+        ctx.partition("coo", A["m"], A["n"], idx=A["idx"], val=A["val"], coo_row=coo_of_csr(A))
+    else:
+        assert A["fmt"] == "csc"
+        ctx.partition("csc", A["m"], A["n"], ptr=A["ptr"], idx=A["idx"], val=A["val"])
+    if layout is None:
+        layout = M.Y_REPLICATED
+    if host_path:
+        yh = np.array(y, dtype=vdt, copy=True)
+        ctx.spmv_host(alpha, np.ascontiguousarray(x, vdt), beta, yh, layout)
+        out = yh
+    else:
+        tdt = torch.float64 if vdt == np.float64 else torch.float32
+        xd = torch.as_tensor(np.ascontiguousarray(x, vdt)).to("cuda:0")
+        outs = []
+        for _ in range(repeat):
+            yd = torch.as_tensor(np.array(y, dtype=vdt, copy=True)).to("cuda:0")
+            ctx.spmv(alpha, xd, beta, yd, layout)
+            torch.cuda.synchronize()
+            outs.append(yd.cpu().numpy())
+        out = outs[0] if repeat == 1 else outs
+    if own:
+        ctx.close()
+    return out

@@ -1,0 +1,256 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Integer-valued inputs (small integers, dyadic alpha/beta) make every summation
+order exact, so those cases are compared BIT-FOR-BIT (SURVEY 8(c) pin P5);
+U[-1,1) inputs are compared per row within tau * bound (fp64 1e-12, fp32 1e-5).
+"""
+import itertools
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from tests.helpers import assert_close, coo_of_csr, oracle_ref, row_bound, run_gpu, to_dtype
+
+pytestmark = pytest.mark.gpu
+
+FMTS = ["csr", "coo", "csc"]
+
+
+def as_fmt(A, fmt):
+    if fmt == "csc":
+        return A if A["fmt"] == "csc" else gen.transpose(A)
+    return A if A["fmt"] == "csr" else gen.transpose(A)
+
+
+def sparse_from_dense_mask(mask, vals):
+    r, c = np.nonzero(mask)
+    m, n = mask.shape
+    rp, ci, v = oracle.coo_to_csr(m, r, c, vals[r, c])
+    return gen.Sparse(fmt="csr", m=m, n=n, ptr=rp, idx=ci, val=v)
+
+
+def check(A, fmt, x, y, alpha, beta, parts=1, exact=False, **kw):
+    B = as_fmt(A, fmt)
+    got = run_gpu(B, fmt, x, y, alpha, beta, parts=parts, **kw)
+    ref = oracle_ref(A, x, y, alpha, beta)
+    if exact:
+        assert got.dtype == ref.dtype
+        assert np.array_equal(got, ref), (fmt, parts, np.nonzero(got != ref)[0][:10])
+    else:
+        assert_close(got, ref, row_bound(A, x, y, alpha, beta), A["val"].dtype)
+    return got
+
+
+# ------------------------------------------------------------ worked values
+@pytest.mark.parametrize("fmt", FMTS)
+@pytest.mark.parametrize("parts", [1, 2, 3, 5, 7])
+def test_fixture_E(golden_E, fmt, parts):
+    g = golden_E
+    A = gen.Sparse(fmt="csr", m=4, n=4, ptr=np.array(g["csr_row_ptr"], np.int64),
+                   idx=np.array(g["csr_col_idx"], np.int32), val=np.array(g["csr_val"]))
+    for case in g["spmv"]:
+        got = run_gpu(as_fmt(A, fmt), fmt, np.array(case["x"], float), np.array(case["y"], float),
+                      case["alpha"], case["beta"], parts=parts)
+        assert got.tolist() == case["expect"]
+
+
+@pytest.mark.parametrize("fmt", ["csr", "coo"])
+def test_shared_row_beta_once(golden_E, fmt):
+    s = golden_E["shared_row_1x4"]
+    A = gen.Sparse(fmt="csr", m=1, n=4, ptr=np.array([0, 4], np.int64), idx=np.arange(4, dtype=np.int32),
+                   val=np.array(s["val"], float))
+    got = run_gpu(A, fmt, np.array(s["x"], float), np.array(s["y"], float), s["alpha"], s["beta"], parts=2)
+    assert got.tolist() == s["expect"]
+
+
+# ----------------------------------------------------------- closed forms
+@pytest.mark.parametrize("fmt", FMTS)
+@pytest.mark.parametrize("n,parts", [(1, 1), (13, 8), (5000, 8), (2047, 3), (2048, 1), (100_000, 9)])
+def test_chain_row_all_ones(fmt, n, parts):
+    A = gen.Sparse(fmt="csr", m=1, n=n, ptr=np.array([0, n], np.int64), idx=np.arange(n, dtype=np.int32),
+                   val=np.ones(n))
+    got = run_gpu(as_fmt(A, fmt), fmt, np.ones(n), np.zeros(1), 1.0, 0.0, parts=parts)
+    assert got.tolist() == [float(n)]
+
+
+@pytest.mark.parametrize("fmt", FMTS)
+@pytest.mark.parametrize("parts", [1, 4])
+def test_stencil_closed_form(fmt, parts):
+    N = 23
+    A = gen.stencil27(N, kind=gen.STENCIL_PIN)
+    got = run_gpu(as_fmt(A, fmt), fmt, np.ones(A["m"]), np.zeros(A["m"]), 1.0, 0.0, parts=parts)
+    gi = np.indices((N, N, N)).reshape(3, -1).T
+    k = np.prod(3 - ((gi == 0) | (gi == N - 1)).astype(int), axis=1)
+    assert np.array_equal(got, 27.0 - k)
+
+
+@pytest.mark.parametrize("fmt", FMTS)
+def test_permutation_and_identity_bit_exact(fmt):
+    n = 70_001
+    rng = np.random.default_rng(7)
+    pi = rng.permutation(n)
+    A = gen.Sparse(fmt="csr", m=n, n=n, ptr=np.arange(n + 1, dtype=np.int64), idx=pi.astype(np.int32),
+                   val=np.ones(n))
+    x = rng.standard_normal(n)
+    got = run_gpu(as_fmt(A, fmt), fmt, x, np.full(n, np.nan), 1.0, 0.0, parts=3)
+    assert np.array_equal(got, x[pi])
+
+
+# -------------------------------------------------- random, brute-force-ish
+@pytest.mark.parametrize("fmt", FMTS)
+def test_random_small_all_alpha_beta(fmt):
+    rng = np.random.default_rng(100 + FMTS.index(fmt))
+    for trial in range(12):
+        m, n = (int(v) for v in rng.integers(1, 300, 2))
+        mask = rng.random((m, n)) < [0.01, 0.1, 0.3][trial % 3]
+        if m > 3:
+            mask[rng.integers(0, m, m // 4)] = False
+        vals = rng.integers(-4, 5, (m, n)).astype(float)
+        vals[vals == 0] = 1.0
+        A = sparse_from_dense_mask(mask, vals)
+        x = rng.integers(-4, 5, n).astype(float); y = rng.integers(-4, 5, m).astype(float)
+        for alpha, beta in itertools.product([0.0, 1.0, -1.0, 2.5], [0.0, 1.0, -1.0, 10.0]):
+            parts = int(rng.integers(1, 10))
+            check(A, fmt, x, y, alpha, beta, parts=parts, exact=True)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("fmt", FMTS)
+def test_random_uniform_tolerance(fmt, dtype):
+    rng = np.random.default_rng(5)
+    for trial in range(6):
+        m, n = (int(v) for v in rng.integers(100, 3000, 2))
+        A = to_dtype(gen.kdistinct_csr(m, n, int(rng.integers(1, 60)), seed=trial + 10), dtype)
+        x = gen.vector(n, 20 + trial, dtype=dtype); y = gen.vector(m, 40 + trial, dtype=dtype)
+        check(A, fmt, x, y, 1.5, 0.5, parts=int(rng.integers(1, 9)))
+
+
+@pytest.mark.parametrize("fmt", FMTS)
+def test_long_and_empty_rows_mix(fmt):
+    """Rows longer than a tile (slab-split), runs of empty rows, and part cuts inside long rows."""
+    rng = np.random.default_rng(3)
+    lens = np.concatenate([[0, 0, 9000, 1, 0, 2048, 2047, 2046, 0, 0, 0], rng.integers(0, 5, 3000),
+                           [30000], np.zeros(5000, int), [4097, 3]])
+    m, n = lens.size, 40000
+    ptr = np.zeros(m + 1, np.int64); ptr[1:] = np.cumsum(lens)
+    idx = np.concatenate([np.sort(rng.choice(n, L, replace=False)) for L in lens]).astype(np.int32)
+    val = rng.integers(-4, 5, idx.size).astype(float)
+    A = gen.Sparse(fmt="csr", m=m, n=n, ptr=ptr, idx=idx, val=val)
+    x = rng.integers(-4, 5, n).astype(float); y = rng.integers(-4, 5, m).astype(float)
+    for parts in [1, 2, 3, 8, 17]:
+        check(A, fmt, x, y, 2.0, -1.0, parts=parts, exact=True)
+
+
+# --------------------------------------------------------------- edge cases
+@pytest.mark.parametrize("fmt", FMTS)
+def test_empty_matrix_and_tiny(fmt):
+    A = gen.Sparse(fmt="csr", m=5, n=3, ptr=np.zeros(6, np.int64), idx=np.zeros(0, np.int32), val=np.zeros(0))
+    y = np.arange(5, dtype=float)
+    for parts in [1, 4]:
+        got = run_gpu(as_fmt(A, fmt), fmt, np.ones(3), y, 1.0, 2.0, parts=parts)
+        assert got.tolist() == (2 * y).tolist()
+    # nnz < np: empty parts
+    A = gen.Sparse(fmt="csr", m=3, n=3, ptr=np.array([0, 1, 1, 2], np.int64), idx=np.array([2, 0], np.int32),
+                   val=np.array([3.0, 4.0]))
+    got = run_gpu(as_fmt(A, fmt), fmt, np.array([1.0, 2.0, 5.0]), np.ones(3), 1.0, 1.0, parts=7)
+    assert got.tolist() == [16.0, 1.0, 5.0]
+
+
+@pytest.mark.parametrize("fmt", FMTS)
+def test_alpha_zero_beta_zero_do_not_read(fmt):
+    A = gen.kdistinct_csr(500, 400, 7, seed=9, kind=gen.SMALLINT)
+    x = np.full(400, np.nan)
+    y = gen.vector(500, 3)
+    got = run_gpu(as_fmt(A, fmt), fmt, x, y, 0.0, 3.0, parts=2)
+    assert np.array_equal(got, 3.0 * y)
+    x = gen.vector(400, 4, kind=gen.SMALLINT)
+    got = run_gpu(as_fmt(A, fmt), fmt, x, np.full(500, np.nan), 1.0, 0.0, parts=2)
+    assert np.array_equal(got, oracle_ref(A, x, np.zeros(500), 1.0, 0.0))
+
+
+def test_unsorted_coo_rejected():
+    import paper_2209_07552_b200 as M
+    ctx = M.Context()
+    with pytest.raises(M.MsrepError) as e:
+        ctx.partition("coo", 3, 3, idx=np.array([0, 1, 2], np.int32), val=np.ones(3),
+                      coo_row=np.array([0, 2, 1], np.int32))
+    assert e.value.status == 3
+    with pytest.raises(M.MsrepError) as e:
+        ctx.spmv(1.0, 0, 0.0, 0)
+    assert e.value.status == 5
+    ctx.close()
+
+
+@pytest.mark.parametrize("fmt", FMTS)
+def test_deterministic_and_layout_invariant(fmt):
+    A = gen.rmat(14, seed=11)
+    x = gen.vector(A["n"], 1); y = gen.vector(A["m"], 2)
+    B = as_fmt(A, fmt)
+    outs = run_gpu(B, fmt, x, y, 1.5, 0.5, parts=4, repeat=3)
+    if fmt != "csc":   # no float atomics on the row path: bit-reproducible
+        assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+    assert_close(outs[0], oracle_ref(A, x, y, 1.5, 0.5), row_bound(A, x, y, 1.5, 0.5), np.float64)
+
+
+@pytest.mark.parametrize("fmt", FMTS)
+def test_host_vector_path_matches_device(fmt):
+    A = gen.rmat(13, seed=12, kind=gen.SMALLINT)
+    x = gen.vector(A["n"], 1, kind=gen.SMALLINT); y = gen.vector(A["m"], 2, kind=gen.SMALLINT)
+    B = as_fmt(A, fmt)
+    a = run_gpu(B, fmt, x, y, 2.0, 0.5, parts=3)
+    b = run_gpu(B, fmt, x, y, 2.0, 0.5, parts=3, host_path=True)
+    assert np.array_equal(a, b)
+    assert np.array_equal(a, oracle_ref(A, x, y, 2.0, 0.5))
+
+
+def test_owned_layout_writes_only_owned_rows():
+    import paper_2209_07552_b200 as M
+    A = gen.rmat(12, seed=5, kind=gen.SMALLINT)
+    x = gen.vector(A["n"], 1, kind=gen.SMALLINT)
+    y = np.full(A["m"], 7.0)
+    got = run_gpu(A, "csr", x, y, 1.0, 1.0, parts=5, layout=M.Y_OWNED)
+    assert np.array_equal(got, oracle_ref(A, x, y, 1.0, 1.0))   # single rank owns every row
+
+
+# ------------------------------------------------- configs (BASELINE.json)
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_config1_random1k(dtype):
+    A = to_dtype(gen.make_config("random1k"), dtype)
+    assert A.nnz == 10_000
+    x = gen.vector(1000, 1, dtype=dtype); y = gen.vector(1000, 2, dtype=dtype)
+    for fmt in FMTS:
+        check(A, fmt, x, y, 1.5, 0.5)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("fmt", ["csr", "coo"])
+def test_config2_stencil_full_size(fmt):
+    """Full N=127 stencil at the bench launch configuration: closed form + bit-exact integer parity."""
+    A = gen.stencil27(127, kind=gen.STENCIL_PIN)
+    m = A["m"]
+    got = run_gpu(A, fmt, np.ones(m), np.zeros(m), 1.0, 0.0)
+    assert set(np.unique(got).tolist()) == {0.0, 9.0, 15.0, 19.0}
+    assert int((got == 0).sum()) == 125 ** 3
+    A = gen.stencil27(127, kind=gen.SMALLINT)
+    x = gen.vector(m, 5, kind=gen.SMALLINT); y = gen.vector(m, 6, kind=gen.SMALLINT)
+    check(A, fmt, x, y, 1.5, 0.5, exact=True)
+    A = gen.stencil27(127)
+    x = gen.vector(m, 5); y = gen.vector(m, 6)
+    check(A, fmt, x, y, 1.5, 0.5)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("fmt", ["csr", "coo"])
+def test_config3_rmat_full_size_bit_exact(fmt):
+    A = gen.rmat(24, seed=3, kind=gen.SMALLINT)
+    x = gen.vector(A["n"], 7, kind=gen.SMALLINT); y = gen.vector(A["m"], 8, kind=gen.SMALLINT)
+    check(A, fmt, x, y, 2.0, 0.5, exact=True)
+
+
+@pytest.mark.slow
+def test_config4_tallskinny_csc_sampled():
+    A = gen.kdistinct_csc(50_000_000, 1_000_000, 500, seed=4, kind=gen.SMALLINT)
+    x = gen.vector(A["n"], 9, kind=gen.SMALLINT); y = gen.vector(A["m"], 10, kind=gen.SMALLINT)
+    check(A, "csc", x, y, 2.0, 0.5, exact=True)
