@@ -85,7 +85,7 @@ struct RowSmem {
   static constexpr int STAGE_B = VAL_B + COL_B + AUX_B;
   static constexpr int BUF_OFF = STAGES * STAGE_B;                       // fp64 products / row sums [TILE_ITEMS]
   static constexpr int BAR_OFF = BUF_OFF + TILE_ITEMS * 8;
-  static constexpr int DESC_OFF = (BAR_OFF + STAGES * 8 + 15) & ~15;    // int4 descriptors, 16-B aligned
+  static constexpr int DESC_OFF = (BAR_OFF + 2 * STAGES * 8 + 15) & ~15; // full/empty mbarriers, then int4 descriptors
   static constexpr int WK_OFF = DESC_OFF + STAGES * 16;
   static constexpr int WV_OFF = WK_OFF + 32;
   static constexpr int TOTAL = WV_OFF + 64;
@@ -148,55 +148,138 @@ __device__ __forceinline__ void issue_row_tile(const RowLaunch& P, int4 d, unsig
   if (ab) tma_1d(st + L::VAL_B + L::COL_B, P.aux + a0, ab, bar, pol);
 }
 
+// Consumer-only barrier (named barrier 1, the THREADS consumer threads; the
+// producer warp never takes part).
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(THREADS) : "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(bar)) : "memory");
+}
+
+// Same as block_seg_scan but synchronising only the consumer warps.
+__device__ __forceinline__ void consumer_seg_scan(int key, double val, int& pk, double& pv, int* swk, double* swv) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int ik = key;
+  double iv = val;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    int k2 = __shfl_up_sync(FULL, ik, off);
+    double v2 = __shfl_up_sync(FULL, iv, off);
+    if (lane >= off && k2 == ik) iv = v2 + iv;
+  }
+  if (lane == 31) { swk[warp] = ik; swv[warp] = iv; }
+  consumer_sync();
+  int wk = INT_MIN;
+  double wv = 0.0;
+  for (int w = 0; w < warp; w++) {
+    int k2 = swk[w];
+    double v2 = swv[w];
+    if (k2 == wk) wv = wv + v2; else { wk = k2; wv = v2; }
+  }
+  int ek = __shfl_up_sync(FULL, ik, 1);
+  double ev = __shfl_up_sync(FULL, iv, 1);
+  if (lane == 0) { pk = wk; pv = wv; }
+  else { pk = ek; pv = (wk == ek) ? wv + ev : ev; }
+}
+
+constexpr int VEC_UNROLL = 16;
+
+// Warp-specialised persistent kernel: warp THREADS/32 is the TMA producer
+// (one elected lane walks this CTA's tiles, waits for a free stage, issues the
+// bulk copies); warps 0..THREADS/32-1 consume.  Stages are released per warp
+// through an "empty" mbarrier, so vector tiles need no CTA-wide barrier at all.
 template <typename VT, bool COO>
-__global__ void __launch_bounds__(THREADS, 2) rows_kernel(const RowLaunch P) {
+__global__ void __launch_bounds__(THREADS + 32, 2) rows_kernel(const RowLaunch P) {
   using L = RowSmem<VT>;
+  constexpr int NW = THREADS / 32;
   extern __shared__ __align__(128) unsigned char smem[];
   double* sbuf = reinterpret_cast<double*>(smem + L::BUF_OFF);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* empty = full + STAGES;
   int4* sdesc = reinterpret_cast<int4*>(smem + L::DESC_OFF);
   int* swk = reinterpret_cast<int*>(smem + L::WK_OFF);
   double* swv = reinterpret_cast<double*>(smem + L::WV_OFF);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const VT* __restrict__ x = static_cast<const VT*>(P.x);
-  VT* __restrict__ y = static_cast<VT*>(P.y);
-  const double alpha = P.alpha, beta = P.beta;
-
-  uint64_t pol = 0;
-  int4 next_desc = make_int4(0, 0, 0, -1);
   if (tid == 0) {
-    pol = policy_evict_first();
-    for (int s = 0; s < STAGES; s++) mbar_init(&bars[s], 1);
+    for (int s = 0; s < STAGES; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], NW); }
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid == 0) {
-    for (int s = 0; s < STAGES; s++) {
-      int t = blockIdx.x + s * gridDim.x;
-      if (t < P.ntiles) {
-        int4 d = P.tiles[t];
+
+  if (warp == NW) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      for (int i = 0;; i++) {
+        const int t = blockIdx.x + i * gridDim.x;
+        if (t >= P.ntiles) break;
+        const int s = i % STAGES;
+        const int4 d = P.tiles[t];
+        if (i >= STAGES) mbar_wait(&empty[s], (uint32_t)(((i / STAGES) - 1) & 1));
         sdesc[s] = d;
-        issue_row_tile<VT, COO>(P, d, smem + s * L::STAGE_B, &bars[s], pol);
+        fence_proxy_async();
+        issue_row_tile<VT, COO>(P, d, smem + s * L::STAGE_B, &full[s], pol);
       }
     }
-    int tn = blockIdx.x + STAGES * gridDim.x;
-    if (tn < P.ntiles) next_desc = P.tiles[tn];
+    return;
   }
+
+  // -------------------------------------------------------------- consumers
+  const VT* __restrict__ x = static_cast<const VT*>(P.x);
+  VT* __restrict__ y = static_cast<VT*>(P.y);
+  const double alpha = P.alpha, beta = P.beta;
 
   for (int i = 0;; i++) {
     const int t = blockIdx.x + i * gridDim.x;
     if (t >= P.ntiles) break;
     const int s = i % STAGES;
-    mbar_wait(&bars[s], (uint32_t)((i / STAGES) & 1));
+    mbar_wait(&full[s], (uint32_t)((i / STAGES) & 1));
     const int4 d = sdesc[s];
     unsigned char* st = smem + s * L::STAGE_B;
     const int nrows = d.z & 0xffff, nnz = d.z >> 16;
     const VT* sv = reinterpret_cast<const VT*>(st) + (d.y & (L::VPA - 1));
     const int* sc = reinterpret_cast<const int*>(st + L::VAL_B) + (d.y & 3);
 
-    if (d.w >= 0) {
+    if (!COO && d.w <= -2) {
+      // ---- vector tile (pCSR, regular rows): L = 2^(-w-2) lanes per row, products fused into
+      // the per-lane sums (no product pass), xor-shuffle tree, coalesced y.  L is chosen at
+      // partition time from the tile's row-length profile (host.cpp, tile_mode()).
+      const int lg = -d.w - 2;
+      const int Lw = 1 << lg, G = THREADS >> lg;
+      const int g = tid >> lg, j = tid & (Lw - 1);
+      const int* sa = reinterpret_cast<const int*>(st + L::VAL_B + L::COL_B) + (d.x & 3);
+      const int base = sa[0];
+      const int64_t yrow0 = P.ybase + d.x;
+      for (int rp = 0; rp < nrows; rp += G) {
+        const int r = rp + g;
+        double acc = 0.0, yv = 0.0;
+        if (r < nrows) {
+          if (beta != 0.0) yv = (double)y[yrow0 + r];
+          const int ke = sa[r + 1] - base;
+          for (int k = sa[r] - base + j; k < ke; k += VEC_UNROLL * Lw) {
+            int cidx[VEC_UNROLL];
+            VT xv[VEC_UNROLL];
+#pragma unroll
+            for (int u = 0; u < VEC_UNROLL; u++) { int kk = k + u * Lw; cidx[u] = kk < ke ? sc[kk] : 0; }
+#pragma unroll
+            for (int u = 0; u < VEC_UNROLL; u++) { int kk = k + u * Lw; xv[u] = kk < ke ? ldg_ro(x + cidx[u]) : VT(0); }
+#pragma unroll
+            for (int u = 0; u < VEC_UNROLL; u++) {
+              int kk = k + u * Lw;
+              if (kk < ke) acc = fma((double)sv[kk], (double)xv[u], acc);
+            }
+          }
+        }
+        for (int off = Lw >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(FULL, acc, off);
+        if (r < nrows && j == 0) {
+          double v = alpha * acc;
+          if (beta != 0.0) v += beta * yv;
+          y[yrow0 + r] = (VT)v;
+        }
+      }
+    } else if (d.w >= 0) {
       // ---- slab: partial sum of one split row -> record (deterministic order)
+      consumer_sync();   // swv reuse guard
       int cidx[8];
       VT xv[8];
 #pragma unroll
@@ -209,51 +292,15 @@ __global__ void __launch_bounds__(THREADS, 2) rows_kernel(const RowLaunch P) {
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(FULL, acc, off);
       if (lane == 0) swv[warp] = acc;
-      __syncthreads();
+      consumer_sync();
       if (tid == 0) {
         double tot = 0.0;
-        for (int w = 0; w < THREADS / 32; w++) tot = tot + swv[w];
+        for (int w = 0; w < NW; w++) tot = tot + swv[w];
         P.rec[d.w] = tot;
       }
-    } else if (!COO && d.w <= -2) {
-      // ---- vector tile (pCSR, regular rows): L = 2^(-w-2) lanes per row, products fused into
-      // the per-lane sums (no product pass), xor-shuffle tree, coalesced y.  L is chosen at
-      // partition time from the tile's row-length profile (host.cpp, tile_mode()).
-      const int lg = -d.w - 2;
-      const int L = 1 << lg, G = THREADS >> lg;
-      const int g = tid >> lg, j = tid & (L - 1);
-      const int* sa = reinterpret_cast<const int*>(st + L::VAL_B + L::COL_B) + (d.x & 3);
-      const int base = sa[0];
-      const int64_t yrow0 = P.ybase + d.x;
-      for (int rp = 0; rp < nrows; rp += G) {
-        const int r = rp + g;
-        double acc = 0.0, yv = 0.0;
-        if (r < nrows) {
-          if (beta != 0.0) yv = (double)y[yrow0 + r];
-          const int ke = sa[r + 1] - base;
-          for (int k = sa[r] - base + j; k < ke; k += 8 * L) {
-            int cidx[8];
-            VT xv[8];
-#pragma unroll
-            for (int u = 0; u < 8; u++) { int kk = k + u * L; cidx[u] = kk < ke ? sc[kk] : 0; }
-#pragma unroll
-            for (int u = 0; u < 8; u++) { int kk = k + u * L; xv[u] = kk < ke ? ldg_ro(x + cidx[u]) : VT(0); }
-#pragma unroll
-            for (int u = 0; u < 8; u++) {
-              int kk = k + u * L;
-              if (kk < ke) acc = fma((double)sv[kk], (double)xv[u], acc);
-            }
-          }
-        }
-        for (int off = L >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(FULL, acc, off);
-        if (r < nrows && j == 0) {
-          double v = alpha * acc;
-          if (beta != 0.0) v += beta * yv;
-          y[yrow0 + r] = (VT)v;
-        }
-      }
     } else {
-      // ---- merge-path / key-walk tile: whole rows [row0, row0+nrows), irregular lengths
+      // ---- merge-path (CSR) / key-walk (COO) tile: whole rows, irregular lengths
+      consumer_sync();   // all consumers are done with the previous tile's sbuf / scratch
       const int64_t yrow0 = P.ybase + d.x;
       double yin[8];
 #pragma unroll
@@ -277,7 +324,7 @@ __global__ void __launch_bounds__(THREADS, 2) rows_kernel(const RowLaunch P) {
       }
       if (COO)
         for (int r = tid; r < nrows; r += THREADS) sbuf[nnz + r] = 0.0;
-      __syncthreads();
+      consumer_sync();
 
       double* rsum = sbuf + nnz;   // row sums live after the products (nrows + nnz <= TILE_ITEMS)
       int key;
@@ -331,7 +378,7 @@ __global__ void __launch_bounds__(THREADS, 2) rows_kernel(const RowLaunch P) {
       }
       int pk;
       double pv;
-      block_seg_scan(key, acc, pk, pv, swk, swv);
+      consumer_seg_scan(key, acc, pk, pv, swk, swv);
       if (!COO) {
         if (nseg >= 2 && pk == first) rsum[first] += pv;
       } else {
@@ -342,7 +389,7 @@ __global__ void __launch_bounds__(THREADS, 2) rows_kernel(const RowLaunch P) {
           if (last_of_row) rsum[cur] = (pk == cur) ? pv + acc : acc;
         }
       }
-      __syncthreads();
+      consumer_sync();
       // coalesced epilogue, alpha and beta applied exactly once per row
 #pragma unroll
       for (int u = 0; u < 8; u++) {
@@ -354,17 +401,8 @@ __global__ void __launch_bounds__(THREADS, 2) rows_kernel(const RowLaunch P) {
         }
       }
     }
-    __syncthreads();   // stage s and sbuf are free
-    if (tid == 0) {
-      int tn = t + STAGES * gridDim.x;
-      if (tn < P.ntiles) {
-        sdesc[s] = next_desc;
-        fence_proxy_async();
-        issue_row_tile<VT, COO>(P, next_desc, st, &bars[s], pol);
-        int tnn = tn + STAGES * gridDim.x;
-        if (tnn < P.ntiles) next_desc = P.tiles[tnn];
-      }
-    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);   // this warp is done with stage s
   }
 }
 
@@ -564,12 +602,12 @@ cudaError_t launch_rows(const RowLaunch& L, cudaStream_t s) {
   cudaError_t e;
   if (L.dtype == 0) {
     int b = RowSmem<double>::TOTAL;
-    if (L.coo) { if ((e = set_smem(rows_kernel<double, true>, b))) return e; rows_kernel<double, true><<<L.grid, THREADS, b, s>>>(L); }
-    else { if ((e = set_smem(rows_kernel<double, false>, b))) return e; rows_kernel<double, false><<<L.grid, THREADS, b, s>>>(L); }
+    if (L.coo) { if ((e = set_smem(rows_kernel<double, true>, b))) return e; rows_kernel<double, true><<<L.grid, THREADS + 32, b, s>>>(L); }
+    else { if ((e = set_smem(rows_kernel<double, false>, b))) return e; rows_kernel<double, false><<<L.grid, THREADS + 32, b, s>>>(L); }
   } else {
     int b = RowSmem<float>::TOTAL;
-    if (L.coo) { if ((e = set_smem(rows_kernel<float, true>, b))) return e; rows_kernel<float, true><<<L.grid, THREADS, b, s>>>(L); }
-    else { if ((e = set_smem(rows_kernel<float, false>, b))) return e; rows_kernel<float, false><<<L.grid, THREADS, b, s>>>(L); }
+    if (L.coo) { if ((e = set_smem(rows_kernel<float, true>, b))) return e; rows_kernel<float, true><<<L.grid, THREADS + 32, b, s>>>(L); }
+    else { if ((e = set_smem(rows_kernel<float, false>, b))) return e; rows_kernel<float, false><<<L.grid, THREADS + 32, b, s>>>(L); }
   }
   return cudaGetLastError();
 }
