@@ -320,8 +320,8 @@ def main():
             "gpu_launches": int(a.steps * st["kernels_per_spmv"]),
             "clocks": clocks,
             "partition_ms": st["partition_ms"],
-            "stats_rank0": {k: st[k] for k in ("nnz_rank", "ntiles", "nslabs", "nsplit_rows", "distinct_cols",
-                                               "kernels_per_spmv")},
+            "stats_rank0": {k: st[k] for k in ("nnz_rank", "ntiles", "nsell", "nslabs", "nsplit_rows",
+                                               "distinct_cols", "kernels_per_spmv", "tile_bytes")},
         }
         print(json.dumps(out), flush=True)
     ctx.close()

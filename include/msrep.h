@@ -99,6 +99,9 @@ typedef struct {
   int64_t kernels_per_spmv;  /* kernel launches one msrep_spmv makes on this rank (beta!=0)  */
   int64_t device_bytes;      /* device memory held by the partition                          */
   double partition_ms;       /* host + upload time of the last msrep_partition (wall clock)  */
+  int64_t tile_bytes;        /* bytes of the rank's tile blobs as stored on the GPU (what one
+                                SpMV streams from HBM for A, incl. 16-B / SELL padding)      */
+  int64_t nsell;             /* SELL tiles among the rank's tiles (regular pCSR rows)        */
 } msrep_stats;
 
 /* NCCL unique id for the communicator (rank 0 creates it, the caller

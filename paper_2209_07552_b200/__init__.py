@@ -15,7 +15,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmsrep.so")
+LIB_PATH = os.environ.get("MSREP_LIB_VARIANT") or os.path.join(_HERE, "libmsrep.so")   # variant: tuning builds
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libmsrep.so not built at {LIB_PATH}: run `make` (or __graft_entry__.build()) first")
@@ -47,7 +47,8 @@ class Stats(ctypes.Structure):
     _fields_ = [(k, ctypes.c_int64) for k in (
         "nparts", "nranks", "parts_per_rank", "nnz_rank", "rows_window", "owned_rows", "distinct_cols", "ntiles",
         "nslabs", "nsplit_rows", "nheads_local", "alg_bytes", "alg_bytes_beta0", "kernels_per_spmv",
-        "device_bytes")] + [("partition_ms", ctypes.c_double)]
+        "device_bytes")] + [("partition_ms", ctypes.c_double), ("tile_bytes", ctypes.c_int64),
+                                         ("nsell", ctypes.c_int64)]
 
 
 class Allocator(ctypes.Structure):

@@ -129,11 +129,11 @@ struct Ctx {
   int64_t shard = 0;                // pCSC: ceil(m / nranks)
 
   std::vector<DevBuf> bufs;
-  void* d_val = nullptr;
-  int32_t* d_idx = nullptr;
-  int32_t* d_aux = nullptr;         // CSR/CSC local pointer, COO row ids
+  char* d_blob = nullptr;           // tile blobs [aux][val][idx] (the rank's partition on the GPU)
+  int64_t blob_bytes = 0;
   int4* d_tiles = nullptr;
-  int ntiles = 0, nslabs = 0;
+  int4* d_sell = nullptr;
+  int ntiles = 0, nsell = 0, nslabs = 0;
   double* d_rec = nullptr;
   int nrec = 0;
   int nsplit = 0;
@@ -194,6 +194,14 @@ msrep_status_t dalloc(Ctx* c, size_t want, void** out, cudaStream_t s) {
   return MSREP_OK;
 }
 
+void release_range(Ctx* c, size_t lo, size_t hi) {
+  for (size_t i = lo; i < hi; i++) {
+    if (c->has_alloc) c->alloc.free(c->bufs[i].p, c->bufs[i].bytes, nullptr, c->alloc.user);
+    else cudaFree(c->bufs[i].p);
+  }
+  c->bufs.erase(c->bufs.begin() + (ptrdiff_t)lo, c->bufs.begin() + (ptrdiff_t)hi);
+}
+
 void free_all(Ctx* c) {
   for (auto& b : c->bufs) {
     if (c->has_alloc) c->alloc.free(b.p, b.bytes, nullptr, c->alloc.user);
@@ -215,54 +223,50 @@ msrep_status_t upload(Ctx* c, const T* host, size_t count, T** out, cudaStream_t
 
 // ---------------------------------------------------------- tile schedule
 struct Schedule {
-  std::vector<TileHost> tiles;
+  std::vector<TileHost> tiles;      // general tiles (merge / COO walk / slabs / pCSC)
+  std::vector<TileHost> sell;       // pCSR SELL tiles
   int nrec = 0, nslabs = 0;
   std::vector<int64_t> sr_row;
   std::vector<int32_t> sr_rec, sr_head, head_list, part_rec;
 };
 
-// Per-tile kernel mode for pCSR (w field of a normal tile): -1 = merge-path walk;
-// -2-lg = "vector" mode with 2^lg lanes per row.  Cost model in per-lane serial
-// steps: vector = passes * (ceil(maxlen / L) + lg + 4) with passes =
-// ceil(nrows / (THREADS / L)); merge path ~ 32 steps (search + 8 items + scan).
-int32_t tile_mode(int64_t nrows, int64_t maxlen) {
-  int32_t best = -1;
-  int64_t best_cost = 32;
-  for (int lg = 0; lg <= 5; lg++) {
-    const int64_t L = 1 << lg, G = THREADS >> lg;
-    const int64_t cost = ((nrows + G - 1) / G) * ((maxlen + L - 1) / L + lg + 4);
-    if (cost < best_cost) { best_cost = cost; best = -2 - lg; }
-  }
-  return best;
-}
-
 struct Packer {
   Schedule& S;
   int64_t wlo;
   const std::vector<int64_t>& lp;   // local pointer over the window (rank-local nonzeros)
-  bool vector_ok;                   // pCSR tiles may use the vector mode
-  int64_t cur_r0 = -1, cur_r1 = -1, cur_max = 0;
-  explicit Packer(Schedule& s, int64_t w, const std::vector<int64_t>& l, bool v = false)
-      : S(s), wlo(w), lp(l), vector_ok(v) {}
+  int64_t cur_r0 = -1, cur_r1 = -1;
+  explicit Packer(Schedule& s, int64_t w, const std::vector<int64_t>& l) : S(s), wlo(w), lp(l) {}
   int64_t ls(int64_t r) const { return lp[(size_t)(r - wlo)]; }
   int64_t le(int64_t r) const { return lp[(size_t)(r - wlo + 1)]; }
   void flush() {
     if (cur_r0 < 0) return;
     const int64_t nrows = cur_r1 - cur_r0, z0 = ls(cur_r0), nz = le(cur_r1 - 1) - z0;
-    const int32_t mode = vector_ok ? tile_mode(nrows, cur_max) : -1;
-    S.tiles.push_back({(int32_t)(cur_r0 - wlo), (int32_t)z0, (int32_t)(nrows | (nz << 16)), mode});
+    S.tiles.push_back({(int32_t)(cur_r0 - wlo), (int32_t)z0, (int32_t)(nrows | (nz << 16)), -1});
     cur_r0 = cur_r1 = -1;
-    cur_max = 0;
   }
   void add_row(int64_t r) {
     const int64_t len = le(r) - ls(r);
     if (cur_r0 >= 0) {
       const int64_t items = (cur_r1 - cur_r0) + (le(cur_r1 - 1) - ls(cur_r0));
-      if (items + len + 1 > TILE_ITEMS) flush();
+      if (items + len + 1 > TILE_ITEMS || cur_r1 - cur_r0 >= MAX_TILE_ROWS) flush();
     }
     if (cur_r0 < 0) { cur_r0 = r; cur_r1 = r; }
     cur_r1 = r + 1;
-    cur_max = std::max(cur_max, len);
+  }
+  // SELL tile for rows [r, e) (<= SELL_ROWS whole owned rows) if every row has <= SELL_W_MAX
+  // nonzeros and padding to the longest row is <= 1/8 of the stored elements.
+  bool try_sell(int64_t r, int64_t e) {
+    int64_t W = 0, sum = 0;
+    for (int64_t q = r; q < e; q++) {
+      const int64_t len = le(q) - ls(q);
+      if (len > SELL_W_MAX) return false;
+      W = std::max(W, len);
+      sum += len;
+    }
+    if (W == 0 || 8 * sum < 7 * W * SELL_ROWS) return false;
+    flush();
+    S.sell.push_back({(int32_t)(r - wlo), (int32_t)ls(r), (int32_t)((e - r) | (W << 16)), -2});
+    return true;
   }
   // slabs over rank-local nonzeros [z0, z1) of row r; with_records: write partial sums to records
   void slabs(int64_t r, int64_t z0, int64_t z1, bool with_records) {
@@ -280,7 +284,7 @@ struct Packer {
 // slab-split rows), and the tail row (owned, continues into later parts) as
 // slabs whose fix-up adds the head partials of the parts that continue it.
 void build_row_schedule(const Ctx& c, const std::vector<int64_t>& lp, Schedule& S) {
-  Packer pk(S, c.wlo, lp, c.fmt == MSREP_CSR);
+  Packer pk(S, c.wlo, lp);
   const auto& P = c.parts;
   for (int j = c.P0; j < c.P1; j++) {
     const msrep_part_desc& d = P[(size_t)j];
@@ -307,7 +311,7 @@ void build_row_schedule(const Ctx& c, const std::vector<int64_t>& lp, Schedule& 
       if (!chain.empty()) tail = last;
     }
     const int64_t rend = tail >= 0 ? tail : d.owned_end;
-    for (int64_t r = d.owned_begin; r < rend; r++) {
+    auto one_row = [&](int64_t r) {
       const int64_t len = pk.le(r) - pk.ls(r);
       if (len + 1 > TILE_ITEMS) {
         pk.flush();
@@ -320,6 +324,11 @@ void build_row_schedule(const Ctx& c, const std::vector<int64_t>& lp, Schedule& 
       } else {
         pk.add_row(r);
       }
+    };
+    for (int64_t r = d.owned_begin; r < rend;) {
+      const int64_t e = std::min<int64_t>(r + SELL_ROWS, rend);
+      if (c.fmt == MSREP_CSR && pk.try_sell(r, e)) { r = e; continue; }
+      for (; r < e; r++) one_row(r);
     }
     pk.flush();
     if (tail >= 0) {
@@ -552,30 +561,59 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   if (fmt == MSREP_CSC) build_col_schedule(*c, lp, S);
   else build_row_schedule(*c, lp, S);
   c->ntiles = (int)S.tiles.size();
+  c->nsell = (int)S.sell.size();
   c->nslabs = S.nslabs;
   c->nrec = S.nrec;
   c->nsplit = (int)S.sr_row.size();
 
-  // ---- upload this rank's slice (the only H2D of A), and the schedule
+  // ---- upload this rank's slice (the only H2D of A) and build the tile blobs on the GPU
   const int64_t nz_r = B_hi - B_lo;
+  const size_t mark = c->bufs.size();   // temporaries allocated from here are freed after packing
   void* vp;
   TRY(dalloc(c, (size_t)nz_r * V, &vp, s));
   if (nz_r) CUDA_TRY(cudaMemcpyAsync(vp, static_cast<const char*>(val) + (size_t)B_lo * V, (size_t)nz_r * V, cudaMemcpyHostToDevice, s));
-  c->d_val = vp;
-  TRY(upload(c, idx + B_lo, (size_t)nz_r, &c->d_idx, s));
+  int32_t *d_idx, *d_aux;
+  TRY(upload(c, idx + B_lo, (size_t)nz_r, &d_idx, s));
   if (fmt == MSREP_COO) {
-    TRY(upload(c, coo_row + B_lo, (size_t)nz_r, &c->d_aux, s));
+    TRY(upload(c, coo_row + B_lo, (size_t)nz_r, &d_aux, s));
   } else {
-    // upload the global pointer slice and rebase on the GPU (Sec. 4.1)
+    // upload the global pointer slice and rebase it on the GPU (Sec. 4.1)
     int64_t* d_g;
     TRY(upload(c, ptr + c->wlo, (size_t)W + 1, &d_g, s));
     void* ap;
     TRY(dalloc(c, ((size_t)W + 1) * 4, &ap, s));
-    c->d_aux = static_cast<int32_t*>(ap);
-    CUDA_TRY(launch_rebase(d_g, c->d_aux, W + 1, B_lo, B_hi, s));
+    d_aux = static_cast<int32_t*>(ap);
+    CUDA_TRY(launch_rebase(d_g, d_aux, W + 1, B_lo, B_hi, s));
   }
   static_assert(sizeof(TileHost) == sizeof(int4), "tile");
-  TRY(upload(c, reinterpret_cast<const int4*>(S.tiles.data()), S.tiles.size(), &c->d_tiles, s));
+  const size_t ngen = S.tiles.size();
+  S.tiles.insert(S.tiles.end(), S.sell.begin(), S.sell.end());   // packed together, launched apart
+  std::vector<int32_t> blob16(S.tiles.size());
+  int64_t blob_total = 0;
+  for (size_t t = 0; t < S.tiles.size(); t++) {
+    const TileHost& th = S.tiles[t];
+    const int kind = th.rec == -2 ? KIND_SELL : th.rec >= 0 ? KIND_SLAB : (fmt == MSREP_COO ? KIND_COO : KIND_PTR);
+    if (blob_total / 16 >= (int64_t)1 << 31) return fail(MSREP_ERR_TOO_LARGE, "tile blob exceeds 32 GiB");
+    blob16[t] = (int32_t)(blob_total / 16);
+    blob_total += blob_bytes(kind, th.packed & 0xffff, th.packed >> 16, (int)V);
+  }
+  int4* d_tiles_orig;
+  int32_t* d_blob16;
+  TRY(upload(c, reinterpret_cast<const int4*>(S.tiles.data()), S.tiles.size(), &d_tiles_orig, s));
+  TRY(upload_vec(c, blob16, &d_blob16, s));
+  const size_t keep_from = c->bufs.size();
+  void* bp;
+  TRY(dalloc(c, (size_t)std::max<int64_t>(16, blob_total), &bp, s));
+  c->d_blob = static_cast<char*>(bp);
+  PackLaunch PL{d_tiles_orig, d_blob16, (int)S.tiles.size(), vp, d_idx, d_aux, fmt == MSREP_COO, (int)V, c->d_blob};
+  CUDA_TRY(launch_pack(PL, s));
+  std::vector<TileHost> fin(S.tiles);
+  for (size_t t = 0; t < fin.size(); t++) fin[t].nz0 = blob16[t];
+  CUDA_TRY(cudaStreamSynchronize(s));
+  release_range(c, mark, keep_from);   // plain slices are no longer needed: the blobs hold the partition
+  TRY(upload(c, reinterpret_cast<const int4*>(fin.data()), ngen, &c->d_tiles, s));
+  TRY(upload(c, reinterpret_cast<const int4*>(fin.data() + ngen), fin.size() - ngen, &c->d_sell, s));
+  c->blob_bytes = blob_total;
   void* rp;
   TRY(dalloc(c, (size_t)std::max(1, S.nrec) * 8, &rp, s));
   c->d_rec = static_cast<double*>(rp);
@@ -609,7 +647,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   st.nparts = c->np; st.nranks = c->nranks; st.parts_per_rank = c->vparts;
   st.nnz_rank = nz_r;
   st.rows_window = W;
-  st.ntiles = c->ntiles; st.nslabs = c->nslabs; st.nsplit_rows = c->nsplit; st.nheads_local = c->nheads_local;
+  st.ntiles = c->ntiles; st.nsell = c->nsell; st.nslabs = c->nslabs; st.nsplit_rows = c->nsplit; st.nheads_local = c->nheads_local;
   st.partition_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
   int64_t X = 0;
   if (fmt == MSREP_CSC) {
@@ -638,10 +676,11 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   st.alg_bytes = base + ybytes_b1;
   st.alg_bytes_beta0 = base + ybytes_b0;
   if (fmt == MSREP_CSC) st.kernels_per_spmv = (c->ntiles ? 1 : 0) + 1 /*axpby*/ + 1 /*memset*/;
-  else st.kernels_per_spmv = (c->ntiles ? 1 : 0) + (c->nranks > 1 && c->any_flag ? 1 : 0) + (c->nsplit ? 1 : 0);
+  else st.kernels_per_spmv = (c->ntiles ? 1 : 0) + (c->nsell ? 1 : 0) + (c->nranks > 1 && c->any_flag ? 1 : 0) + (c->nsplit ? 1 : 0);
   int64_t db = 0;
   for (auto& b : c->bufs) db += (int64_t)b.bytes;
   st.device_bytes = db;
+  st.tile_bytes = c->blob_bytes;
   c->ready = true;
   return MSREP_OK;
 }
@@ -676,9 +715,8 @@ msrep_status_t msrep_spmv(msrep_ctx h, const void* alpha_p, const void* x, const
     CUDA_TRY(cudaMemsetAsync(c->d_py, 0, (size_t)c->py_len * 8, s));
     ColLaunch L{};
     L.tiles = c->d_tiles; L.ntiles = c->ntiles;
-    L.val = c->d_val; L.row = c->d_idx; L.cptr = c->d_aux;
+    L.blob = c->d_blob;
     L.x = x; L.xbase = c->wlo; L.py = c->d_py; L.dtype = dt;
-    L.grid = cols_grid(dt, c->ntiles);
     cudaEvent_t pe;
     TRY(prof_begin(c, s, &pe));
     CUDA_TRY(launch_cols(L, s));
@@ -696,13 +734,15 @@ msrep_status_t msrep_spmv(msrep_ctx h, const void* alpha_p, const void* x, const
 
   RowLaunch L{};
   L.tiles = c->d_tiles; L.ntiles = c->ntiles;
-  L.val = c->d_val; L.col = c->d_idx; L.aux = c->d_aux;
+  L.blob = c->d_blob;
   L.x = x; L.y = y; L.ybase = c->wlo;
+  L.xmax = c->n > 0 ? (uint32_t)(c->n - 1) : 0u;
   L.alpha = alpha; L.beta = beta; L.rec = c->d_rec;
   L.coo = c->fmt == MSREP_COO; L.dtype = dt;
-  L.grid = rows_grid(dt, L.coo, c->ntiles);
+  SellLaunch SL{c->d_sell, c->nsell, c->d_blob, x, y, c->wlo, alpha, beta, dt};
   cudaEvent_t pe;
   TRY(prof_begin(c, s, &pe));
+  CUDA_TRY(launch_sell(SL, s));
   CUDA_TRY(launch_rows(L, s));
   if (pe) CUDA_TRY(cudaEventRecord(pe, s));
   if (c->nranks > 1 && c->any_flag) {

@@ -7,34 +7,77 @@
 
 namespace msrep {
 
-// A tile is the unit of work one CTA processes: a row-aligned group of whole
+// A tile is the unit of work one WARP processes: a row-aligned group of whole
 // rows whose merge items (rows + nonzeros) fit TILE_ITEMS, or a "slab" -- a
 // contiguous piece (<= SLAB_NNZ nonzeros) of one split row whose partial sum
 // goes to a record instead of y.  For pCSC, tiles are
 // column groups / column pieces and every tile scatters into py.
-constexpr int TILE_ITEMS = 2048;
-constexpr int SLAB_NNZ = 2047;
-constexpr int THREADS = 256;
+constexpr int TILE_ITEMS = 512;
+constexpr int MAX_TILE_ROWS = 64;    // rows (or columns) per normal tile
+constexpr int SLAB_NNZ = 512;
+constexpr int WARPS = 4;             // warps per CTA (each with its own TMA ring)
 
-// int4 tile descriptor: x = first row (window-local), y = first nonzero
-// (rank-local), z = nrows | (nnz << 16), w = record index (-1: normal tile).
+// Device layout: every tile is one contiguous, 16-byte aligned "blob"
+//   [aux][val][idx]
+// aux = tile-local row (col) pointer as uint16 (nrows+1 entries; pCSR/pCSC
+// normal tiles), or the global row ids (int32, one per nonzero; pCOO normal
+// tiles), or nothing (slabs); val = nnz values; idx = nnz column (row) ids.
+// Each segment is padded to 16 bytes so one TMA bulk copy moves the tile.
+//
+// SELL tiles (regular rows, pCSR only): SELL_ROWS consecutive rows, lane = row;
+// element t of lane l sits at t * SELL_ROWS + l (sliced-ELL within the tile,
+// W = longest row <= SELL_W_MAX, shorter rows padded with val 0 / col 0 and
+// masked in the kernel); aux = the SELL_ROWS row lengths (uint16).  The host
+// only forms a SELL tile when padding is <= 1/8 of its elements.
+enum TileKind { KIND_PTR = 0, KIND_COO = 1, KIND_SLAB = 2, KIND_SELL = 3 };
+constexpr int SELL_ROWS = 32;
+constexpr int SELL_W_MAX = 32;
+__host__ __device__ inline int align16(int b) { return (b + 15) & ~15; }
+__host__ __device__ inline int blob_aux_bytes(int kind, int nrows, int nnz) {
+  return kind == KIND_PTR ? align16((nrows + 1) * 2)
+                          : (kind == KIND_COO ? align16(nnz * 4) : (kind == KIND_SELL ? SELL_ROWS * 2 : 0));
+}
+// for KIND_SELL, `nnz` is the slice width W
+__host__ __device__ inline int blob_bytes(int kind, int nrows, int nnz, int vsize) {
+  if (kind == KIND_SELL) return SELL_ROWS * 2 + nnz * SELL_ROWS * (vsize + 4);
+  return blob_aux_bytes(kind, nrows, nnz) + align16(nnz * vsize) + align16(nnz * 4);
+}
+
+// int4 tile descriptor: x = first row (col), window-local; y = blob offset in
+// 16-byte units; z = nrows | (nnz << 16) (SELL: nrows | (W << 16)); w = kind
+// of work (>= 0: slab record index; -1: merge-path / key walk; -2: SELL).
 struct TileHost { int32_t row0, nz0, packed, rec; };
+
+struct PackLaunch {        // build the tile blobs from the rank's plain slices (partition time)
+  const int4* tiles; const int32_t* blob16; int ntiles;       // tiles: {row0, nz0 (rank-local), packed, w}
+  const void* val; const int32_t* idx; const int32_t* ptr;    // ptr: window-local pointer (CSR/CSC), or COO row ids
+  int coo; int vsize;
+  char* blob;
+};
 
 struct RowLaunch {
   const int4* tiles; int ntiles;
-  const void* val; const int32_t* col; const int32_t* aux;  // aux: local row ptr (CSR) or global row ids (COO)
+  const char* blob;
   const void* x; void* y; int64_t ybase;                     // y row of window row 0
+  uint32_t xmax;                                             // n - 1 (clamp for padding lanes)
   double alpha, beta; double* rec;
   int coo; int dtype;                                        // dtype 0 = f64, 1 = f32
-  int grid;                                                  // persistent CTAs
+};
+
+struct SellLaunch {
+  const int4* tiles; int ntiles;
+  const char* blob;
+  const void* x; void* y; int64_t ybase;
+  double alpha, beta;
+  int dtype;
 };
 
 struct ColLaunch {
   const int4* tiles; int ntiles;
-  const void* val; const int32_t* row; const int32_t* cptr;   // cptr: rank-local column pointer (window)
+  const char* blob;
   const void* x; int64_t xbase;                              // x index of window column 0
   double* py;
-  int dtype; int grid;
+  int dtype;
 };
 
 struct FixupLaunch {
@@ -55,6 +98,7 @@ struct HeadLaunch {
 
 // kernels.cu entry points (all enqueue on `s`)
 cudaError_t launch_rows(const RowLaunch& L, cudaStream_t s);
+cudaError_t launch_sell(const SellLaunch& L, cudaStream_t s);
 cudaError_t launch_cols(const ColLaunch& L, cudaStream_t s);
 cudaError_t launch_fixup(const FixupLaunch& L, cudaStream_t s);
 cudaError_t launch_heads(const HeadLaunch& L, cudaStream_t s);
@@ -63,7 +107,6 @@ cudaError_t launch_axpby_py(const double* py, void* y, int64_t count, double alp
                             cudaStream_t s);                                                // y = alpha*py + beta*y
 cudaError_t launch_rebase(const int64_t* gptr, int32_t* lptr, int64_t count, int64_t lo, int64_t hi,
                           cudaStream_t s);                                                  // clamp(gptr,lo,hi)-lo
-int rows_grid(int dtype, int coo, int ntiles);
-int cols_grid(int dtype, int ntiles);
+cudaError_t launch_pack(const PackLaunch& L, cudaStream_t s);
 
 }  // namespace msrep

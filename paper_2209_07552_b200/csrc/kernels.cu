@@ -32,7 +32,6 @@ namespace msrep {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int STAGES = 2;
 
 __device__ __forceinline__ uint32_t saddr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -76,26 +75,45 @@ template <typename T>
 __device__ __forceinline__ T ldg_ro(const T* p) { return __ldg(p); }
 
 // ---------------------------------------------------------------- layout
-template <typename VT>
-struct RowSmem {
-  static constexpr int VPA = 16 / (int)sizeof(VT);                       // values per 16 bytes
-  static constexpr int VAL_B = (((TILE_ITEMS + VPA) * (int)sizeof(VT)) + 15) & ~15;
-  static constexpr int COL_B = (((TILE_ITEMS + 4) * 4) + 15) & ~15;
-  static constexpr int AUX_B = (((TILE_ITEMS + 8) * 4) + 15) & ~15;
-  static constexpr int STAGE_B = VAL_B + COL_B + AUX_B;
-  static constexpr int BUF_OFF = STAGES * STAGE_B;                       // fp64 products / row sums [TILE_ITEMS]
-  static constexpr int BAR_OFF = BUF_OFF + TILE_ITEMS * 8;
-  static constexpr int DESC_OFF = (BAR_OFF + 2 * STAGES * 8 + 15) & ~15; // full/empty mbarriers, then int4 descriptors
-  static constexpr int WK_OFF = DESC_OFF + STAGES * 16;
-  static constexpr int WV_OFF = WK_OFF + 32;
-  static constexpr int TOTAL = WV_OFF + 64;
+// Every warp owns an independent NS-stage ring of tile blobs in shared memory.
+// Lane 0 issues ONE 1-D TMA bulk copy per tile (the blob is contiguous in HBM);
+// the warp waits on the stage's mbarrier, computes, and refills the stage --
+// no cross-warp synchronisation, so a slow warp never stalls another's loads.
+template <typename VT, bool COO>
+struct RStage {
+  static constexpr int AUX_CAP = COO ? TILE_ITEMS * 4 : ((MAX_TILE_ROWS + 1) * 2 + 15) / 16 * 16;
+  static constexpr int BYTES = AUX_CAP + TILE_ITEMS * (int)sizeof(VT) + TILE_ITEMS * 4;
+  // products (fp64) are written in place from byte `aux` on: 8 * TILE_ITEMS bytes must fit
+  static_assert(TILE_ITEMS * ((int)sizeof(VT) + 4) >= 8 * TILE_ITEMS, "in-place product buffer");
 };
 
-// Deterministic block-wide exclusive segmented scan of (key, value) pairs whose
-// keys are non-decreasing in thread order.  op((ka,va),(kb,vb)) =
-// (kb, ka==kb ? va+vb : vb).  Returns the exclusive prefix (INT_MIN key if none).
-__device__ __forceinline__ void block_seg_scan(int key, double val, int& pk, double& pv, int* swk, double* swv) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+template <int STAGE_B, int NS, int SCRATCH>
+struct WLayout {
+  static constexpr int S = NS;
+  static constexpr int DESC_OFF = NS * STAGE_B;                          // int4 per stage
+  static constexpr int SCR_OFF = DESC_OFF + NS * 16;                     // per-warp fp64 scratch
+  static constexpr int WARP_B = (SCR_OFF + SCRATCH + 15) & ~15;
+  static constexpr int BAR_OFF = WARPS * WARP_B;
+  static constexpr int TOTAL = BAR_OFF + WARPS * NS * 8;
+};
+
+#ifndef MSREP_ROW_NS
+#define MSREP_ROW_NS 2
+#endif
+constexpr int ROW_NS = MSREP_ROW_NS;   // stages per warp (rows kernel)
+constexpr int COL_NS = 3;   // stages per warp (cols kernel)
+constexpr int PER_LANE = TILE_ITEMS / 32;   // 16 nonzeros per lane in a full tile
+
+template <typename VT, bool COO>
+using RowLayout = WLayout<RStage<VT, COO>::BYTES, ROW_NS, MAX_TILE_ROWS * 8>;
+template <typename VT>
+using ColLayout = WLayout<RStage<VT, false>::BYTES, COL_NS, MAX_TILE_ROWS * 8>;
+
+// Warp-level exclusive segmented scan of (key, value) pairs with keys
+// non-decreasing by lane: op((ka,va),(kb,vb)) = (kb, ka==kb ? va+vb : vb).
+// Deterministic (fixed shuffle tree).  Returns INT_MIN as the key of lane 0.
+__device__ __forceinline__ void warp_seg_scan(int key, double val, int& pk, double& pv) {
+  const int lane = threadIdx.x & 31;
   int ik = key;
   double iv = val;
 #pragma unroll
@@ -104,296 +122,194 @@ __device__ __forceinline__ void block_seg_scan(int key, double val, int& pk, dou
     double v2 = __shfl_up_sync(FULL, iv, off);
     if (lane >= off && k2 == ik) iv = v2 + iv;
   }
-  if (lane == 31) { swk[warp] = ik; swv[warp] = iv; }
-  __syncthreads();
-  int wk = INT_MIN;
-  double wv = 0.0;
-  for (int w = 0; w < warp; w++) {
-    int k2 = swk[w];
-    double v2 = swv[w];
-    if (k2 == wk) wv = wv + v2; else { wk = k2; wv = v2; }
-  }
   int ek = __shfl_up_sync(FULL, ik, 1);
   double ev = __shfl_up_sync(FULL, iv, 1);
-  if (lane == 0) { pk = wk; pv = wv; }
-  else { pk = ek; pv = (wk == ek) ? wv + ev : ev; }
+  pk = lane == 0 ? INT_MIN : ek;
+  pv = lane == 0 ? 0.0 : ev;
 }
 
-// Issue the TMA copies of one tile into a stage (thread 0 only).
+__device__ __forceinline__ int tile_kind(int4 d, bool coo) { return d.w >= 0 ? KIND_SLAB : (coo ? KIND_COO : KIND_PTR); }
+
+__device__ __forceinline__ void issue_blob(const char* blob, int4 d, int kind, int vsize, unsigned char* st,
+                                           uint64_t* bar, uint64_t pol) {
+  const int bytes = blob_bytes(kind, d.z & 0xffff, d.z >> 16, vsize);
+  mbar_arrive_expect_tx(bar, (uint32_t)bytes);
+  tma_1d(st, blob + (int64_t)d.y * 16, (uint32_t)bytes, bar, pol);
+}
+
+// pCSR / pCOO general tile kernel (SELL tiles run in sell_kernel).  Tile kinds:
+//   w >= 0   slab: partial sum of a piece of one split row -> rec[w]
+//   w == -1  merge-path walk (pCSR) / key-segmented walk (pCOO): irregular rows
+// Every tile first forms its products val*x[col] lane-strided (coalesced shared
+// memory reads, PER_LANE independent gathers in flight per lane, no per-element
+// predicates: padding lanes gather a clamped, valid x and are never summed);
+// normal tiles store them (fp64) in place in the stage, reduce rows from shared
+// memory and write y = alpha*s + beta*y coalesced.
 template <typename VT, bool COO>
-__device__ __forceinline__ void issue_row_tile(const RowLaunch& P, int4 d, unsigned char* st, uint64_t* bar,
-                                               uint64_t pol) {
-  using L = RowSmem<VT>;
-  const int nrows = d.z & 0xffff, nnz = d.z >> 16;
-  const bool slab = d.w >= 0;
-  uint32_t vb = 0, cb = 0, ab = 0;
-  int64_t v0 = 0, c0 = 0, a0 = 0;
-  if (nnz > 0) {
-    v0 = (int64_t)d.y & ~(int64_t)(L::VPA - 1);
-    int64_t v1 = ((int64_t)d.y + nnz + L::VPA - 1) & ~(int64_t)(L::VPA - 1);
-    vb = (uint32_t)((v1 - v0) * (int64_t)sizeof(VT));
-    c0 = (int64_t)d.y & ~(int64_t)3;
-    int64_t c1 = ((int64_t)d.y + nnz + 3) & ~(int64_t)3;
-    cb = (uint32_t)((c1 - c0) * 4);
-    if (COO && !slab) { a0 = c0; ab = cb; }
-  }
-  if (!COO && !slab) {
-    a0 = (int64_t)d.x & ~(int64_t)3;
-    int64_t a1 = ((int64_t)d.x + nrows + 1 + 3) & ~(int64_t)3;
-    ab = (uint32_t)((a1 - a0) * 4);
-  }
-  mbar_arrive_expect_tx(bar, vb + cb + ab);
-  if (vb) tma_1d(st, (const VT*)P.val + v0, vb, bar, pol);
-  if (cb) tma_1d(st + L::VAL_B, P.col + c0, cb, bar, pol);
-  if (ab) tma_1d(st + L::VAL_B + L::COL_B, P.aux + a0, ab, bar, pol);
-}
-
-// Consumer-only barrier (named barrier 1, the THREADS consumer threads; the
-// producer warp never takes part).
-__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(THREADS) : "memory"); }
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(bar)) : "memory");
-}
-
-// Same as block_seg_scan but synchronising only the consumer warps.
-__device__ __forceinline__ void consumer_seg_scan(int key, double val, int& pk, double& pv, int* swk, double* swv) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int ik = key;
-  double iv = val;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    int k2 = __shfl_up_sync(FULL, ik, off);
-    double v2 = __shfl_up_sync(FULL, iv, off);
-    if (lane >= off && k2 == ik) iv = v2 + iv;
-  }
-  if (lane == 31) { swk[warp] = ik; swv[warp] = iv; }
-  consumer_sync();
-  int wk = INT_MIN;
-  double wv = 0.0;
-  for (int w = 0; w < warp; w++) {
-    int k2 = swk[w];
-    double v2 = swv[w];
-    if (k2 == wk) wv = wv + v2; else { wk = k2; wv = v2; }
-  }
-  int ek = __shfl_up_sync(FULL, ik, 1);
-  double ev = __shfl_up_sync(FULL, iv, 1);
-  if (lane == 0) { pk = wk; pv = wv; }
-  else { pk = ek; pv = (wk == ek) ? wv + ev : ev; }
-}
-
-constexpr int VEC_UNROLL = 16;
-
-// Warp-specialised persistent kernel: warp THREADS/32 is the TMA producer
-// (one elected lane walks this CTA's tiles, waits for a free stage, issues the
-// bulk copies); warps 0..THREADS/32-1 consume.  Stages are released per warp
-// through an "empty" mbarrier, so vector tiles need no CTA-wide barrier at all.
-template <typename VT, bool COO>
-__global__ void __launch_bounds__(THREADS + 32, 2) rows_kernel(const RowLaunch P) {
-  using L = RowSmem<VT>;
-  constexpr int NW = THREADS / 32;
+__global__ void __launch_bounds__(WARPS * 32) rows_kernel(const RowLaunch P) {
+  using St = RStage<VT, COO>;
+  using Lay = RowLayout<VT, COO>;
+  constexpr int NS = ROW_NS;
+  constexpr int V = (int)sizeof(VT);
   extern __shared__ __align__(128) unsigned char smem[];
-  double* sbuf = reinterpret_cast<double*>(smem + L::BUF_OFF);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
-  uint64_t* empty = full + STAGES;
-  int4* sdesc = reinterpret_cast<int4*>(smem + L::DESC_OFF);
-  int* swk = reinterpret_cast<int*>(smem + L::WK_OFF);
-  double* swv = reinterpret_cast<double*>(smem + L::WV_OFF);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned char* wb = smem + warp * Lay::WARP_B;
+  int4* sdesc = reinterpret_cast<int4*>(wb + Lay::DESC_OFF);
+  double* rsum = reinterpret_cast<double*>(wb + Lay::SCR_OFF);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Lay::BAR_OFF) + warp * NS;
+  const int gw = blockIdx.x * WARPS + warp, nw = gridDim.x * WARPS;
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) {
-    for (int s = 0; s < STAGES; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], NW); }
-    fence_mbar_init();
-  }
-  __syncthreads();
-
-  if (warp == NW) {
-    // ------------------------------------------------------------ producer
-    if (lane == 0) {
-      const uint64_t pol = policy_evict_first();
-      for (int i = 0;; i++) {
-        const int t = blockIdx.x + i * gridDim.x;
-        if (t >= P.ntiles) break;
-        const int s = i % STAGES;
-        const int4 d = P.tiles[t];
-        if (i >= STAGES) mbar_wait(&empty[s], (uint32_t)(((i / STAGES) - 1) & 1));
-        sdesc[s] = d;
-        fence_proxy_async();
-        issue_row_tile<VT, COO>(P, d, smem + s * L::STAGE_B, &full[s], pol);
-      }
-    }
-    return;
-  }
-
-  // -------------------------------------------------------------- consumers
   const VT* __restrict__ x = static_cast<const VT*>(P.x);
   VT* __restrict__ y = static_cast<VT*>(P.y);
   const double alpha = P.alpha, beta = P.beta;
+  const uint32_t xmax = P.xmax;
+
+  uint64_t pol = 0;
+  int4 dn = make_int4(0, 0, 0, -1);
+  if (lane == 0) {
+    for (int s = 0; s < NS; s++) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+    pol = policy_evict_first();
+    for (int s = 0; s < NS; s++) {
+      const int t = gw + s * nw;
+      if (t < P.ntiles) {
+        const int4 d = P.tiles[t];
+        sdesc[s] = d;
+        issue_blob(P.blob, d, tile_kind(d, COO), V, wb + s * St::BYTES, &bars[s], pol);
+      }
+    }
+    if (gw + NS * nw < P.ntiles) dn = P.tiles[gw + NS * nw];
+  }
+  __syncwarp();
 
   for (int i = 0;; i++) {
-    const int t = blockIdx.x + i * gridDim.x;
+    const int t = gw + i * nw;
     if (t >= P.ntiles) break;
-    const int s = i % STAGES;
-    mbar_wait(&full[s], (uint32_t)((i / STAGES) & 1));
+    const int s = i % NS;
+    mbar_wait(&bars[s], (uint32_t)((i / NS) & 1));
     const int4 d = sdesc[s];
-    unsigned char* st = smem + s * L::STAGE_B;
+    unsigned char* st = wb + s * St::BYTES;
     const int nrows = d.z & 0xffff, nnz = d.z >> 16;
-    const VT* sv = reinterpret_cast<const VT*>(st) + (d.y & (L::VPA - 1));
-    const int* sc = reinterpret_cast<const int*>(st + L::VAL_B) + (d.y & 3);
+    const int kind = tile_kind(d, COO);
+    const int ab = blob_aux_bytes(kind, nrows, nnz);
+    const int vb = align16(nnz * V);
+    const VT* sv = reinterpret_cast<const VT*>(st + ab);
+    const uint32_t* sc = reinterpret_cast<const uint32_t*>(st + ab + vb);
+    const int U = (nnz + 31) >> 5;   // warp-uniform number of 32-wide element rows
 
-    if (!COO && d.w <= -2) {
-      // ---- vector tile (pCSR, regular rows): L = 2^(-w-2) lanes per row, products fused into
-      // the per-lane sums (no product pass), xor-shuffle tree, coalesced y.  L is chosen at
-      // partition time from the tile's row-length profile (host.cpp, tile_mode()).
-      const int lg = -d.w - 2;
-      const int Lw = 1 << lg, G = THREADS >> lg;
-      const int g = tid >> lg, j = tid & (Lw - 1);
-      const int* sa = reinterpret_cast<const int*>(st + L::VAL_B + L::COL_B) + (d.x & 3);
-      const int base = sa[0];
-      const int64_t yrow0 = P.ybase + d.x;
-      for (int rp = 0; rp < nrows; rp += G) {
-        const int r = rp + g;
-        double acc = 0.0, yv = 0.0;
-        if (r < nrows) {
-          if (beta != 0.0) yv = (double)y[yrow0 + r];
-          const int ke = sa[r + 1] - base;
-          for (int k = sa[r] - base + j; k < ke; k += VEC_UNROLL * Lw) {
-            int cidx[VEC_UNROLL];
-            VT xv[VEC_UNROLL];
+    // ---- products: lane-strided over the tile's nonzeros, up to PER_LANE gathers in flight
+    uint32_t c[PER_LANE];
+    VT vv[PER_LANE], xv[PER_LANE];
+    if (U == PER_LANE) {   // full tile (the common case): no predicates at all
 #pragma unroll
-            for (int u = 0; u < VEC_UNROLL; u++) { int kk = k + u * Lw; cidx[u] = kk < ke ? sc[kk] : 0; }
-#pragma unroll
-            for (int u = 0; u < VEC_UNROLL; u++) { int kk = k + u * Lw; xv[u] = kk < ke ? ldg_ro(x + cidx[u]) : VT(0); }
-#pragma unroll
-            for (int u = 0; u < VEC_UNROLL; u++) {
-              int kk = k + u * Lw;
-              if (kk < ke) acc = fma((double)sv[kk], (double)xv[u], acc);
-            }
-          }
-        }
-        for (int off = Lw >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(FULL, acc, off);
-        if (r < nrows && j == 0) {
-          double v = alpha * acc;
-          if (beta != 0.0) v += beta * yv;
-          y[yrow0 + r] = (VT)v;
-        }
+      for (int u = 0; u < PER_LANE; u++) {
+        c[u] = min(sc[lane + 32 * u], xmax);
+        vv[u] = sv[lane + 32 * u];
       }
-    } else if (d.w >= 0) {
-      // ---- slab: partial sum of one split row -> record (deterministic order)
-      consumer_sync();   // swv reuse guard
-      int cidx[8];
-      VT xv[8];
 #pragma unroll
-      for (int u = 0; u < 8; u++) { int k = tid + u * THREADS; cidx[u] = k < nnz ? sc[k] : 0; }
+      for (int u = 0; u < PER_LANE; u++) xv[u] = ldg_ro(x + c[u]);
+    } else {
 #pragma unroll
-      for (int u = 0; u < 8; u++) { int k = tid + u * THREADS; xv[u] = k < nnz ? ldg_ro(x + cidx[u]) : VT(0); }
+      for (int u = 0; u < PER_LANE; u++) {
+        const bool on = u < U;
+        c[u] = on ? min(sc[lane + 32 * u], xmax) : 0u;
+        vv[u] = on ? sv[lane + 32 * u] : VT(0);
+      }
+#pragma unroll
+      for (int u = 0; u < PER_LANE; u++) xv[u] = u < U ? ldg_ro(x + c[u]) : VT(0);
+    }
+
+    if (kind == KIND_SLAB) {
+      // ---- slab: partial sum of one split row -> record (fixed order, bit-reproducible)
       double acc = 0.0;
 #pragma unroll
-      for (int u = 0; u < 8; u++) { int k = tid + u * THREADS; if (k < nnz) acc += (double)sv[k] * (double)xv[u]; }
+      for (int u = 0; u < PER_LANE; u++)
+        if (u < U && lane + 32 * u < nnz) acc += (double)vv[u] * (double)xv[u];
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(FULL, acc, off);
-      if (lane == 0) swv[warp] = acc;
-      consumer_sync();
-      if (tid == 0) {
-        double tot = 0.0;
-        for (int w = 0; w < NW; w++) tot = tot + swv[w];
-        P.rec[d.w] = tot;
-      }
+      if (lane == 0) P.rec[d.w] = acc;
     } else {
-      // ---- merge-path (CSR) / key-walk (COO) tile: whole rows, irregular lengths
-      consumer_sync();   // all consumers are done with the previous tile's sbuf / scratch
       const int64_t yrow0 = P.ybase + d.x;
-      double yin[8];
+      double yin[MAX_TILE_ROWS / 32];
 #pragma unroll
-      for (int u = 0; u < 8; u++) {
-        int r = tid + u * THREADS;
+      for (int u = 0; u < MAX_TILE_ROWS / 32; u++) {
+        const int r = lane + 32 * u;
         yin[u] = (beta != 0.0 && r < nrows) ? (double)y[yrow0 + r] : 0.0;
       }
-      // phase A: products, coalesced over the tile's nonzeros, 8 gathers in flight per thread
-      {
-        int cidx[8];
-        VT xv[8];
+      double* prod = reinterpret_cast<double*>(st + ab);
+      __syncwarp();   // every lane holds its inputs: val/idx bytes may now be overwritten
+      if (U == PER_LANE) {
 #pragma unroll
-        for (int u = 0; u < 8; u++) { int k = tid + u * THREADS; cidx[u] = k < nnz ? sc[k] : 0; }
+        for (int u = 0; u < PER_LANE; u++) prod[lane + 32 * u] = (double)vv[u] * (double)xv[u];
+      } else {
 #pragma unroll
-        for (int u = 0; u < 8; u++) { int k = tid + u * THREADS; xv[u] = k < nnz ? ldg_ro(x + cidx[u]) : VT(0); }
-#pragma unroll
-        for (int u = 0; u < 8; u++) {
-          int k = tid + u * THREADS;
-          if (k < nnz) sbuf[k] = (double)sv[k] * (double)xv[u];
-        }
+        for (int u = 0; u < PER_LANE; u++)
+          if (u < U) prod[lane + 32 * u] = (double)vv[u] * (double)xv[u];
       }
       if (COO)
-        for (int r = tid; r < nrows; r += THREADS) sbuf[nnz + r] = 0.0;
-      consumer_sync();
+        for (int r = lane; r < nrows; r += 32) rsum[r] = 0.0;
+      __syncwarp();
 
-      double* rsum = sbuf + nnz;   // row sums live after the products (nrows + nnz <= TILE_ITEMS)
-      int key;
-      double acc = 0.0;
-      int first = 0, nseg = 0;
-      double firstv = 0.0;
-      int k1 = 0, cur = 0;
       if (!COO) {
-        // merge path over (row ends, nonzero indices) -- Merrill & Garland style, tile-local
-        const int* sa = reinterpret_cast<const int*>(st + L::VAL_B + L::COL_B) + (d.x & 3);
-        const int base = sa[0];
-        const int items = nrows + nnz;
-        const int per = (items + THREADS - 1) / THREADS;
-        const int d0 = min(tid * per, items), d1 = min(d0 + per, items);
-        int lo = max(0, d0 - nnz), hi = min(d0, nrows);
-        while (lo < hi) {
-          int mid = (lo + hi) >> 1;
-          if (sa[mid + 1] - base <= d0 - mid - 1) lo = mid + 1; else hi = mid;
+        const uint16_t* sa = reinterpret_cast<const uint16_t*>(st);   // tile-local row ends
+        {
+          // merge path over (row ends, nonzero indices), tile-local (Merrill & Garland)
+          const int items = nrows + nnz;
+          const int per = (items + 31) >> 5;
+          const int d0 = min(lane * per, items), d1 = min(d0 + per, items);
+          int lo = max(0, d0 - nnz), hi = min(d0, nrows);
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if ((int)sa[mid + 1] <= d0 - mid - 1) lo = mid + 1; else hi = mid;
+          }
+          int xr = lo, yz = d0 - lo;
+          const int first = xr;
+          double acc = 0.0;
+          for (int dd = d0; dd < d1; dd++) {
+            if (xr < nrows && yz < (int)sa[xr + 1]) { acc += prod[yz]; yz++; }
+            else { rsum[xr] = acc; acc = 0.0; xr++; }
+          }
+          int pk;
+          double pv;
+          warp_seg_scan(xr, acc, pk, pv);
+          if (xr > first && pk == first) rsum[first] += pv;
         }
-        int xr = lo, yz = d0 - lo;
-        first = xr;
-        for (int dd = d0; dd < d1; dd++) {
-          if (xr < nrows && yz < sa[xr + 1] - base) { acc += sbuf[yz]; yz++; }
-          else { rsum[xr] = acc; acc = 0.0; xr++; }
-        }
-        key = xr;
-        nseg = (xr > first) ? 2 : 1;   // >= 2 means the first row was completed here
       } else {
         // key-segmented walk over row_idx - row0 (pCOO row index rebased in-kernel)
-        const int* sr = reinterpret_cast<const int*>(st + L::VAL_B + L::COL_B) + (d.y & 3);
+        const int* sr = reinterpret_cast<const int*>(st);
         const int rg0 = (int)yrow0;
-        const int per = (nnz + THREADS - 1) / THREADS;
-        const int k0 = min(tid * per, nnz);
-        k1 = min(k0 + per, nnz);
-        cur = nrows + 1;
+        const int per = (nnz + 31) >> 5;
+        const int k0 = min(lane * per, nnz), k1 = min(k0 + per, nnz);
+        int cur = nrows + 1, first = 0, nseg = 0;
+        double acc = 0.0, firstv = 0.0;
         if (k0 < k1) {
           cur = sr[k0] - rg0;
           nseg = 1;
           for (int k = k0; k < k1; k++) {
-            int kk = sr[k] - rg0;
+            const int kk = sr[k] - rg0;
             if (kk != cur) {
               if (nseg == 1) { first = cur; firstv = acc; } else rsum[cur] = acc;
               nseg++;
               cur = kk;
               acc = 0.0;
             }
-            acc += sbuf[k];
+            acc += prod[k];
           }
         }
-        key = cur;
-      }
-      int pk;
-      double pv;
-      consumer_seg_scan(key, acc, pk, pv, swk, swv);
-      if (!COO) {
-        if (nseg >= 2 && pk == first) rsum[first] += pv;
-      } else {
+        int pk;
+        double pv;
+        warp_seg_scan(cur, acc, pk, pv);
         if (nseg >= 2) rsum[first] = (pk == first) ? firstv + pv : firstv;
         if (nseg >= 1) {
-          const int* sr = reinterpret_cast<const int*>(st + L::VAL_B + L::COL_B) + (d.y & 3);
-          bool last_of_row = (k1 >= nnz) || (sr[k1] - (int)yrow0 != cur);
+          const bool last_of_row = (k1 >= nnz) || (sr[k1] - rg0 != cur);
           if (last_of_row) rsum[cur] = (pk == cur) ? pv + acc : acc;
         }
       }
-      consumer_sync();
-      // coalesced epilogue, alpha and beta applied exactly once per row
+      __syncwarp();
+      // coalesced epilogue: alpha and beta applied exactly once per row
 #pragma unroll
-      for (int u = 0; u < 8; u++) {
-        int r = tid + u * THREADS;
+      for (int u = 0; u < MAX_TILE_ROWS / 32; u++) {
+        const int r = lane + 32 * u;
         if (r < nrows) {
           double v = alpha * rsum[r];
           if (beta != 0.0) v += beta * yin[u];
@@ -401,112 +317,240 @@ __global__ void __launch_bounds__(THREADS + 32, 2) rows_kernel(const RowLaunch P
         }
       }
     }
+    __syncwarp();   // stage s and the scratch are free
+    if (lane == 0) {
+      const int tn = t + NS * nw;
+      if (tn < P.ntiles) {
+        sdesc[s] = dn;
+        issue_blob(P.blob, dn, tile_kind(dn, COO), V, st, &bars[s], pol);
+        if (tn + nw < P.ntiles) dn = P.tiles[tn + nw];
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------- SELL tiles
+// pCSR regular rows: one warp = SELL_ROWS consecutive rows, lane = row.  The
+// tile's elements are slice-major in the blob, so each shared-memory load is a
+// conflict-free 32-lane vector and each x gather of 32 consecutive rows touches
+// few sectors.  All W column indices are read first, then all W gathers are in
+// flight before the first FMA (one L2 round trip per tile); padding elements are
+// masked by the row length, so results equal the plain row sums.
+template <typename VT>
+struct SStage { static constexpr int BYTES = SELL_ROWS * 2 + SELL_W_MAX * SELL_ROWS * ((int)sizeof(VT) + 4); };
+constexpr int SELL_NS = 2;
+template <typename VT>
+using SellLayout = WLayout<SStage<VT>::BYTES, SELL_NS, 16>;
+
+template <typename VT>
+__global__ void __launch_bounds__(WARPS * 32) sell_kernel(const SellLaunch P) {
+  using Lay = SellLayout<VT>;
+  constexpr int NS = SELL_NS;
+  constexpr int V = (int)sizeof(VT);
+  constexpr int SB = SStage<VT>::BYTES;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned char* wb = smem + warp * Lay::WARP_B;
+  int4* sdesc = reinterpret_cast<int4*>(wb + Lay::DESC_OFF);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Lay::BAR_OFF) + warp * NS;
+  const int gw = blockIdx.x * WARPS + warp, nw = gridDim.x * WARPS;
+  const VT* __restrict__ x = static_cast<const VT*>(P.x);
+  VT* __restrict__ y = static_cast<VT*>(P.y);
+  const double alpha = P.alpha, beta = P.beta;
+
+  uint64_t pol = 0;
+  int4 dn = make_int4(0, 0, 0, -1);
+  if (lane == 0) {
+    for (int s = 0; s < NS; s++) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+    pol = policy_evict_first();
+    for (int s = 0; s < NS; s++) {
+      const int t = gw + s * nw;
+      if (t < P.ntiles) {
+        const int4 d = P.tiles[t];
+        sdesc[s] = d;
+        issue_blob(P.blob, d, KIND_SELL, V, wb + s * SB, &bars[s], pol);
+      }
+    }
+    if (gw + NS * nw < P.ntiles) dn = P.tiles[gw + NS * nw];
+  }
+  __syncwarp();
+  for (int i = 0;; i++) {
+    const int t = gw + i * nw;
+    if (t >= P.ntiles) break;
+    const int s = i % NS;
+    mbar_wait(&bars[s], (uint32_t)((i / NS) & 1));
+    const int4 d = sdesc[s];
+    unsigned char* st = wb + s * SB;
+    const int nrows = d.z & 0xffff, W = d.z >> 16;
+    const int mylen = reinterpret_cast<const uint16_t*>(st)[lane];
+    const VT* sv = reinterpret_cast<const VT*>(st + SELL_ROWS * 2);
+    const uint32_t* sc = reinterpret_cast<const uint32_t*>(st + SELL_ROWS * 2 + W * SELL_ROWS * V);
+    const int64_t yr = P.ybase + d.x + lane;
+    const bool live = lane < nrows;
+    const double yv = (beta != 0.0 && live) ? (double)y[yr] : 0.0;
+    uint32_t c[SELL_W_MAX];
+    VT xv[SELL_W_MAX];
+#pragma unroll
+    for (int u = 0; u < SELL_W_MAX; u++)
+      if (u < W) c[u] = sc[u * SELL_ROWS + lane];
+#pragma unroll
+    for (int u = 0; u < SELL_W_MAX; u++)
+      if (u < W) xv[u] = ldg_ro(x + c[u]);
+    double acc = 0.0;
+#pragma unroll
+    for (int u = 0; u < SELL_W_MAX; u++)
+      if (u < W && u < mylen) acc = fma((double)sv[u * SELL_ROWS + lane], (double)xv[u], acc);
+    if (live) {
+      double v = alpha * acc;
+      if (beta != 0.0) v += beta * yv;
+      y[yr] = (VT)v;
+    }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);   // this warp is done with stage s
+    if (lane == 0) {
+      const int tn = t + NS * nw;
+      if (tn < P.ntiles) {
+        sdesc[s] = dn;
+        issue_blob(P.blob, dn, KIND_SELL, V, st, &bars[s], pol);
+        if (tn + nw < P.ntiles) dn = P.tiles[tn + nw];
+      }
+    }
   }
 }
 
 // ------------------------------------------------------------------ pCSC
+// pCSC scatter: per warp tile (a column group, or a piece of one long column),
+// stage x for its columns, then a merge-path walk over (column ends, nonzeros)
+// issues red.global.add.f64 of val*x[col] into the fp64 partial vector py.
 template <typename VT>
-__device__ __forceinline__ void issue_col_tile(const ColLaunch& P, int4 d, unsigned char* st, uint64_t* bar,
-                                               uint64_t pol) {
-  using L = RowSmem<VT>;
-  const int ncols = d.z & 0xffff, nnz = d.z >> 16;
-  uint32_t vb = 0, cb = 0, ab = 0;
-  int64_t v0 = 0, c0 = 0;
-  if (nnz > 0) {
-    v0 = (int64_t)d.y & ~(int64_t)(L::VPA - 1);
-    int64_t v1 = ((int64_t)d.y + nnz + L::VPA - 1) & ~(int64_t)(L::VPA - 1);
-    vb = (uint32_t)((v1 - v0) * (int64_t)sizeof(VT));
-    c0 = (int64_t)d.y & ~(int64_t)3;
-    int64_t c1 = ((int64_t)d.y + nnz + 3) & ~(int64_t)3;
-    cb = (uint32_t)((c1 - c0) * 4);
-  }
-  int64_t a0 = (int64_t)d.x & ~(int64_t)3;
-  int64_t a1 = ((int64_t)d.x + ncols + 1 + 3) & ~(int64_t)3;
-  ab = (uint32_t)((a1 - a0) * 4);
-  mbar_arrive_expect_tx(bar, vb + cb + ab);
-  if (vb) tma_1d(st, (const VT*)P.val + v0, vb, bar, pol);
-  if (cb) tma_1d(st + L::VAL_B, P.row + c0, cb, bar, pol);
-  tma_1d(st + L::VAL_B + L::COL_B, P.cptr + a0, ab, bar, pol);
-}
-
-template <typename VT>
-__global__ void __launch_bounds__(THREADS, 2) cols_kernel(const ColLaunch P) {
-  using L = RowSmem<VT>;
+__global__ void __launch_bounds__(WARPS * 32) cols_kernel(const ColLaunch P) {
+  using St = RStage<VT, false>;
+  using Lay = ColLayout<VT>;
+  constexpr int NS = COL_NS;
+  constexpr int V = (int)sizeof(VT);
   extern __shared__ __align__(128) unsigned char smem[];
-  double* sx = reinterpret_cast<double*>(smem + L::BUF_OFF);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
-  int4* sdesc = reinterpret_cast<int4*>(smem + L::DESC_OFF);
-  const int tid = threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned char* wb = smem + warp * Lay::WARP_B;
+  int4* sdesc = reinterpret_cast<int4*>(wb + Lay::DESC_OFF);
+  double* sx = reinterpret_cast<double*>(wb + Lay::SCR_OFF);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Lay::BAR_OFF) + warp * NS;
+  const int gw = blockIdx.x * WARPS + warp, nw = gridDim.x * WARPS;
   const VT* __restrict__ x = static_cast<const VT*>(P.x);
   double* __restrict__ py = P.py;
 
   uint64_t pol = 0;
-  int4 next_desc = make_int4(0, 0, 0, -1);
-  if (tid == 0) {
-    pol = policy_evict_first();
-    for (int s = 0; s < STAGES; s++) mbar_init(&bars[s], 1);
+  int4 dn = make_int4(0, 0, 0, -1);
+  if (lane == 0) {
+    for (int s = 0; s < NS; s++) mbar_init(&bars[s], 1);
     fence_mbar_init();
-  }
-  __syncthreads();
-  if (tid == 0) {
-    for (int s = 0; s < STAGES; s++) {
-      int t = blockIdx.x + s * gridDim.x;
+    pol = policy_evict_first();
+    for (int s = 0; s < NS; s++) {
+      const int t = gw + s * nw;
       if (t < P.ntiles) {
-        int4 d = P.tiles[t];
+        const int4 d = P.tiles[t];
         sdesc[s] = d;
-        issue_col_tile<VT>(P, d, smem + s * L::STAGE_B, &bars[s], pol);
+        issue_blob(P.blob, d, KIND_PTR, V, wb + s * St::BYTES, &bars[s], pol);
       }
     }
-    int tn = blockIdx.x + STAGES * gridDim.x;
-    if (tn < P.ntiles) next_desc = P.tiles[tn];
+    if (gw + NS * nw < P.ntiles) dn = P.tiles[gw + NS * nw];
   }
+  __syncwarp();
   for (int i = 0;; i++) {
-    const int t = blockIdx.x + i * gridDim.x;
+    const int t = gw + i * nw;
     if (t >= P.ntiles) break;
-    const int s = i % STAGES;
-    mbar_wait(&bars[s], (uint32_t)((i / STAGES) & 1));
-    const int4 dd = sdesc[s];
-    unsigned char* st = smem + s * L::STAGE_B;
-    const int ncols = dd.z & 0xffff, nnz = dd.z >> 16;
-    const VT* sv = reinterpret_cast<const VT*>(st) + (dd.y & (L::VPA - 1));
-    const int* sr = reinterpret_cast<const int*>(st + L::VAL_B) + (dd.y & 3);
-    const int* sa = reinterpret_cast<const int*>(st + L::VAL_B + L::COL_B) + (dd.x & 3);
-    for (int c = tid; c < ncols; c += THREADS) sx[c] = (double)ldg_ro(x + P.xbase + dd.x + c);
-    __syncthreads();
-    // merge path over (column ends clamped to the tile's nonzero range, nonzero indices)
-    const int z0 = dd.y, z1 = dd.y + nnz;
-    auto cend = [&](int c) { int e = sa[c + 1]; e = e < z0 ? z0 : (e > z1 ? z1 : e); return e - z0; };
+    const int s = i % NS;
+    mbar_wait(&bars[s], (uint32_t)((i / NS) & 1));
+    const int4 d = sdesc[s];
+    unsigned char* st = wb + s * St::BYTES;
+    const int ncols = d.z & 0xffff, nnz = d.z >> 16;
+    const int ab = blob_aux_bytes(KIND_PTR, ncols, nnz);
+    const uint16_t* sa = reinterpret_cast<const uint16_t*>(st);
+    const VT* sv = reinterpret_cast<const VT*>(st + ab);
+    const int* sr = reinterpret_cast<const int*>(st + ab + align16(nnz * V));
+    for (int cc = lane; cc < ncols; cc += 32) sx[cc] = (double)ldg_ro(x + P.xbase + d.x + cc);
+    __syncwarp();
     const int items = ncols + nnz;
-    const int per = (items + THREADS - 1) / THREADS;
-    const int d0 = min(tid * per, items), d1 = min(d0 + per, items);
+    const int per = (items + 31) >> 5;
+    const int d0 = min(lane * per, items), d1 = min(d0 + per, items);
     int lo = max(0, d0 - nnz), hi = min(d0, ncols);
     while (lo < hi) {
-      int mid = (lo + hi) >> 1;
-      if (cend(mid) <= d0 - mid - 1) lo = mid + 1; else hi = mid;
+      const int mid = (lo + hi) >> 1;
+      if ((int)sa[mid + 1] <= d0 - mid - 1) lo = mid + 1; else hi = mid;
     }
     int xc = lo, yz = d0 - lo;
+    int ce = xc < ncols ? (int)sa[xc + 1] : 0;
     for (int q = d0; q < d1; q++) {
-      if (xc < ncols && yz < cend(xc)) {
+      if (xc < ncols && yz < ce) {
         atomicAdd(py + sr[yz], (double)sv[yz] * sx[xc]);
         yz++;
       } else {
         xc++;
+        ce = xc < ncols ? (int)sa[xc + 1] : 0;
       }
     }
-    __syncthreads();
-    if (tid == 0) {
-      int tn = t + STAGES * gridDim.x;
+    __syncwarp();
+    if (lane == 0) {
+      const int tn = t + NS * nw;
       if (tn < P.ntiles) {
-        sdesc[s] = next_desc;
-        fence_proxy_async();
-        issue_col_tile<VT>(P, next_desc, st, &bars[s], pol);
-        int tnn = tn + STAGES * gridDim.x;
-        if (tnn < P.ntiles) next_desc = P.tiles[tnn];
+        sdesc[s] = dn;
+        issue_blob(P.blob, dn, KIND_PTR, V, st, &bars[s], pol);
+        if (tn + nw < P.ntiles) dn = P.tiles[tn + nw];
       }
     }
   }
+}
+
+// ------------------------------------------------------------ tile packing
+// Partition-time layout transform (Sec. 4.1, "offload ... to GPUs as specially
+// designed kernels"): one warp per tile copies the tile's aux / val / idx into
+// its contiguous blob.  aux for pointer kinds = tile-local pointer, i.e.
+// clamp(ptr[row0 + j], z0, z1) - z0 for j = 0..nrows (the rebase of Alg. 2 l.12).
+__global__ void pack_kernel(const PackLaunch L) {
+  const int lane = threadIdx.x & 31;
+  const int t = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  if (t >= L.ntiles) return;
+  const int4 d = L.tiles[t];
+  const int nrows = d.z & 0xffff, nnz = d.z >> 16;
+  char* b = L.blob + (int64_t)L.blob16[t] * 16;
+  if (d.w == -2) {   // SELL: lane = row, element u at u * SELL_ROWS + lane, padded with 0 / col 0
+    const int W = nnz;
+    const int rs = lane < nrows ? L.ptr[d.x + lane] : 0;
+    const int len = lane < nrows ? L.ptr[d.x + lane + 1] - rs : 0;
+    reinterpret_cast<uint16_t*>(b)[lane] = (uint16_t)len;
+    char* vb0 = b + SELL_ROWS * 2;
+    int* ix = reinterpret_cast<int*>(vb0 + W * SELL_ROWS * L.vsize);
+    for (int u = 0; u < W; u++) {
+      const bool on = u < len;
+      if (L.vsize == 8) reinterpret_cast<double*>(vb0)[u * SELL_ROWS + lane] = on ? static_cast<const double*>(L.val)[rs + u] : 0.0;
+      else reinterpret_cast<float*>(vb0)[u * SELL_ROWS + lane] = on ? static_cast<const float*>(L.val)[rs + u] : 0.0f;
+      ix[u * SELL_ROWS + lane] = on ? L.idx[rs + u] : 0;
+    }
+    return;
+  }
+  const int kind = d.w >= 0 ? KIND_SLAB : (L.coo ? KIND_COO : KIND_PTR);
+  const int ab = blob_aux_bytes(kind, nrows, nnz);
+  const int vb = align16(nnz * L.vsize);
+  const int z0 = d.y, z1 = d.y + nnz;
+  if (kind == KIND_PTR) {
+    uint16_t* a = reinterpret_cast<uint16_t*>(b);
+    for (int j = lane; j <= nrows; j += 32) {
+      int v = L.ptr[d.x + j];
+      v = v < z0 ? z0 : (v > z1 ? z1 : v);
+      a[j] = (uint16_t)(v - z0);
+    }
+  } else if (kind == KIND_COO) {
+    int* a = reinterpret_cast<int*>(b);
+    for (int k = lane; k < nnz; k += 32) a[k] = L.ptr[z0 + k];
+  }
+  if (L.vsize == 8) {
+    double* v = reinterpret_cast<double*>(b + ab);
+    for (int k = lane; k < nnz; k += 32) v[k] = static_cast<const double*>(L.val)[z0 + k];
+  } else {
+    float* v = reinterpret_cast<float*>(b + ab);
+    for (int k = lane; k < nnz; k += 32) v[k] = static_cast<const float*>(L.val)[z0 + k];
+  }
+  int* ix = reinterpret_cast<int*>(b + ab + vb);
+  for (int k = lane; k < nnz; k += 32) ix[k] = L.idx[z0 + k];
 }
 
 // --------------------------------------------------------- small kernels
@@ -588,42 +632,65 @@ cudaError_t set_smem(K kernel, int bytes) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
-}  // namespace
-
-int rows_grid(int dtype, int coo, int ntiles) {
-  (void)dtype; (void)coo;
-  int g = num_sms() * 2;
-  return ntiles < g ? (ntiles < 1 ? 1 : ntiles) : g;
+template <typename K>
+int grid_for(K kernel, int smem_bytes, int ntiles) {
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, WARPS * 32, smem_bytes);
+  if (occ < 1) occ = 1;
+  const int64_t want = ((int64_t)ntiles + WARPS - 1) / WARPS;
+  const int64_t g = (int64_t)num_sms() * occ;
+  return (int)(want < g ? (want < 1 ? 1 : want) : g);
 }
-int cols_grid(int dtype, int ntiles) { return rows_grid(dtype, 0, ntiles); }
+
+template <typename VT, bool COO>
+cudaError_t launch_rows_t(const RowLaunch& L, cudaStream_t s) {
+  constexpr int b = RowLayout<VT, COO>::TOTAL;
+  cudaError_t e = set_smem(rows_kernel<VT, COO>, b);
+  if (e) return e;
+  rows_kernel<VT, COO><<<grid_for(rows_kernel<VT, COO>, b, L.ntiles), WARPS * 32, b, s>>>(L);
+  return cudaGetLastError();
+}
+
+template <typename VT>
+cudaError_t launch_sell_t(const SellLaunch& L, cudaStream_t s) {
+  constexpr int b = SellLayout<VT>::TOTAL;
+  cudaError_t e = set_smem(sell_kernel<VT>, b);
+  if (e) return e;
+  sell_kernel<VT><<<grid_for(sell_kernel<VT>, b, L.ntiles), WARPS * 32, b, s>>>(L);
+  return cudaGetLastError();
+}
+
+template <typename VT>
+cudaError_t launch_cols_t(const ColLaunch& L, cudaStream_t s) {
+  constexpr int b = ColLayout<VT>::TOTAL;
+  cudaError_t e = set_smem(cols_kernel<VT>, b);
+  if (e) return e;
+  cols_kernel<VT><<<grid_for(cols_kernel<VT>, b, L.ntiles), WARPS * 32, b, s>>>(L);
+  return cudaGetLastError();
+}
+
+}  // namespace
 
 cudaError_t launch_rows(const RowLaunch& L, cudaStream_t s) {
   if (L.ntiles == 0) return cudaSuccess;
-  cudaError_t e;
-  if (L.dtype == 0) {
-    int b = RowSmem<double>::TOTAL;
-    if (L.coo) { if ((e = set_smem(rows_kernel<double, true>, b))) return e; rows_kernel<double, true><<<L.grid, THREADS + 32, b, s>>>(L); }
-    else { if ((e = set_smem(rows_kernel<double, false>, b))) return e; rows_kernel<double, false><<<L.grid, THREADS + 32, b, s>>>(L); }
-  } else {
-    int b = RowSmem<float>::TOTAL;
-    if (L.coo) { if ((e = set_smem(rows_kernel<float, true>, b))) return e; rows_kernel<float, true><<<L.grid, THREADS + 32, b, s>>>(L); }
-    else { if ((e = set_smem(rows_kernel<float, false>, b))) return e; rows_kernel<float, false><<<L.grid, THREADS + 32, b, s>>>(L); }
-  }
-  return cudaGetLastError();
+  if (L.dtype == 0) return L.coo ? launch_rows_t<double, true>(L, s) : launch_rows_t<double, false>(L, s);
+  return L.coo ? launch_rows_t<float, true>(L, s) : launch_rows_t<float, false>(L, s);
+}
+
+cudaError_t launch_sell(const SellLaunch& L, cudaStream_t s) {
+  if (L.ntiles == 0) return cudaSuccess;
+  return L.dtype == 0 ? launch_sell_t<double>(L, s) : launch_sell_t<float>(L, s);
 }
 
 cudaError_t launch_cols(const ColLaunch& L, cudaStream_t s) {
   if (L.ntiles == 0) return cudaSuccess;
-  cudaError_t e;
-  if (L.dtype == 0) {
-    int b = RowSmem<double>::TOTAL;
-    if ((e = set_smem(cols_kernel<double>, b))) return e;
-    cols_kernel<double><<<L.grid, THREADS, b, s>>>(L);
-  } else {
-    int b = RowSmem<float>::TOTAL;
-    if ((e = set_smem(cols_kernel<float>, b))) return e;
-    cols_kernel<float><<<L.grid, THREADS, b, s>>>(L);
-  }
+  return L.dtype == 0 ? launch_cols_t<double>(L, s) : launch_cols_t<float>(L, s);
+}
+
+cudaError_t launch_pack(const PackLaunch& L, cudaStream_t s) {
+  if (L.ntiles == 0) return cudaSuccess;
+  const int64_t threads = (int64_t)L.ntiles * 32;
+  pack_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(L);
   return cudaGetLastError();
 }
 
