@@ -15,7 +15,10 @@ namespace msrep {
 constexpr int TILE_ITEMS = 512;
 constexpr int MAX_TILE_ROWS = 64;    // rows (or columns) per normal tile
 constexpr int SLAB_NNZ = 512;
-constexpr int WARPS = 4;             // warps per CTA (each with its own TMA ring)
+#ifndef MSREP_WARPS
+#define MSREP_WARPS 8
+#endif
+constexpr int WARPS = MSREP_WARPS;   // warps per CTA (each with its own TMA ring)
 
 // Device layout: every tile is one contiguous, 16-byte aligned "blob"
 //   [aux][val][idx]

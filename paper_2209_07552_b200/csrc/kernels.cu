@@ -98,7 +98,7 @@ struct WLayout {
 };
 
 #ifndef MSREP_ROW_NS
-#define MSREP_ROW_NS 2
+#define MSREP_ROW_NS 1
 #endif
 constexpr int ROW_NS = MSREP_ROW_NS;   // stages per warp (rows kernel)
 constexpr int COL_NS = 3;   // stages per warp (cols kernel)
@@ -338,7 +338,10 @@ __global__ void __launch_bounds__(WARPS * 32) rows_kernel(const RowLaunch P) {
 // masked by the row length, so results equal the plain row sums.
 template <typename VT>
 struct SStage { static constexpr int BYTES = SELL_ROWS * 2 + SELL_W_MAX * SELL_ROWS * ((int)sizeof(VT) + 4); };
-constexpr int SELL_NS = 2;
+#ifndef MSREP_SELL_NS
+#define MSREP_SELL_NS 1
+#endif
+constexpr int SELL_NS = MSREP_SELL_NS;
 template <typename VT>
 using SellLayout = WLayout<SStage<VT>::BYTES, SELL_NS, 16>;
 
