@@ -343,19 +343,63 @@ void build_row_schedule(const Ctx& c, const std::vector<int64_t>& lp, Schedule& 
   }
 }
 
-// pCSC: column groups / column pieces over the rank's window; every tile scatters.
-void build_col_schedule(const Ctx& c, const std::vector<int64_t>& lp, Schedule& S) {
-  Packer pk(S, c.wlo, lp);
-  for (int64_t col = c.wlo; col < c.whi; col++) {
-    const int64_t len = pk.le(col) - pk.ls(col);
-    if (len + 1 > TILE_ITEMS) {
-      pk.flush();
-      pk.slabs(col, pk.ls(col), pk.le(col), false);
-    } else {
-      pk.add_row(col);
+// pCSC: tiles are (row band, group of consecutive columns) -- each column
+// contributes the piece of its nonzeros whose rows fall in the band.  Bands are
+// sized so one band of the fp64 partial vector py stays L2-resident while its
+// red.global.add.f64 scatter runs (B200: 126 MB L2).  Tiles are emitted band by
+// band, so concurrently running warps touch one or two bands.  Needs row indices
+// sorted within each column (checked); otherwise one band.  pieces[] holds the
+// (start, end) rank-local nonzero range of every (tile, column).
+constexpr int64_t PY_BAND_BYTES = 40ll << 20;
+
+void build_col_schedule(const Ctx& c, const std::vector<int64_t>& lp, const int32_t* idx, Schedule& S,
+                        std::vector<int32_t>& pieces) {
+  const int64_t W = c.whi - c.wlo;
+  const int32_t* rows = idx + c.B_lo;   // rank-local view
+  bool sorted = true;
+  for (int64_t q = 0; q < W && sorted; q++)
+    for (int64_t z = lp[(size_t)q] + 1; z < lp[(size_t)q + 1]; z++)
+      if (rows[z] < rows[z - 1]) { sorted = false; break; }
+  const int64_t band_rows = std::max<int64_t>(1, PY_BAND_BYTES / 8);
+  const int64_t nb = sorted ? std::max<int64_t>(1, (c.m + band_rows - 1) / band_rows) : 1;
+  for (int64_t b = 0; b < nb; b++) {
+    const int32_t rlo = (int32_t)(b * band_rows), rhi = (int32_t)std::min<int64_t>(c.m, (b + 1) * band_rows);
+    int64_t c0 = -1, ncols = 0, nnz = 0, pbase = 0;
+    auto flush = [&]() {
+      if (c0 >= 0 && nnz > 0)
+        S.tiles.push_back({(int32_t)(c0 - c.wlo), (int32_t)pbase, (int32_t)(ncols | (nnz << 16)), -1});
+      else if (c0 >= 0)
+        pieces.resize((size_t)pbase * 2);   // drop an all-empty group
+      c0 = -1; ncols = 0; nnz = 0;
+    };
+    for (int64_t col = c.wlo; col < c.whi; col++) {
+      const int64_t z0 = lp[(size_t)(col - c.wlo)], z1 = lp[(size_t)(col - c.wlo + 1)];
+      int64_t ps = z0, pe = z1;
+      if (nb > 1) {
+        ps = std::lower_bound(rows + z0, rows + z1, rlo) - rows;
+        pe = std::lower_bound(rows + ps, rows + z1, rhi) - rows;
+      }
+      const int64_t len = pe - ps;
+      if (len + 1 > TILE_ITEMS) {            // a long column piece: single-column tiles of <= SLAB_NNZ
+        flush();
+        for (int64_t z = ps; z < pe; z += SLAB_NNZ) {
+          const int64_t e = std::min<int64_t>(pe, z + SLAB_NNZ);
+          S.tiles.push_back({(int32_t)(col - c.wlo), (int32_t)pieces.size() / 2, (int32_t)(1 | ((e - z) << 16)), -1});
+          pieces.push_back((int32_t)z);
+          pieces.push_back((int32_t)e);
+          S.nslabs++;
+        }
+        continue;
+      }
+      if (c0 >= 0 && (ncols + nnz + len + 1 > TILE_ITEMS || ncols >= MAX_TILE_ROWS)) flush();
+      if (c0 < 0) { c0 = col; pbase = (int64_t)pieces.size() / 2; }
+      pieces.push_back((int32_t)ps);
+      pieces.push_back((int32_t)pe);
+      ncols++;
+      nnz += len;
     }
+    flush();
   }
-  pk.flush();
 }
 
 template <class T>
@@ -558,7 +602,8 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
 
   // ---- schedule
   Schedule S;
-  if (fmt == MSREP_CSC) build_col_schedule(*c, lp, S);
+  std::vector<int32_t> pieces;
+  if (fmt == MSREP_CSC) build_col_schedule(*c, lp, idx, S, pieces);
   else build_row_schedule(*c, lp, S);
   c->ntiles = (int)S.tiles.size();
   c->nsell = (int)S.sell.size();
@@ -599,13 +644,16 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   }
   int4* d_tiles_orig;
   int32_t* d_blob16;
+  int32_t* d_pieces = nullptr;
+  if (fmt == MSREP_CSC) TRY(upload_vec(c, pieces, &d_pieces, s));
   TRY(upload(c, reinterpret_cast<const int4*>(S.tiles.data()), S.tiles.size(), &d_tiles_orig, s));
   TRY(upload_vec(c, blob16, &d_blob16, s));
   const size_t keep_from = c->bufs.size();
   void* bp;
   TRY(dalloc(c, (size_t)std::max<int64_t>(16, blob_total), &bp, s));
   c->d_blob = static_cast<char*>(bp);
-  PackLaunch PL{d_tiles_orig, d_blob16, (int)S.tiles.size(), vp, d_idx, d_aux, fmt == MSREP_COO, (int)V, c->d_blob};
+  PackLaunch PL{d_tiles_orig, d_blob16, (int)S.tiles.size(), vp, d_idx, d_aux, fmt == MSREP_COO, (int)V, c->d_blob,
+                reinterpret_cast<const int2*>(d_pieces)};
   CUDA_TRY(launch_pack(PL, s));
   std::vector<TileHost> fin(S.tiles);
   for (size_t t = 0; t < fin.size(); t++) fin[t].nz0 = blob16[t];

@@ -56,6 +56,7 @@ struct PackLaunch {        // build the tile blobs from the rank's plain slices 
   const void* val; const int32_t* idx; const int32_t* ptr;    // ptr: window-local pointer (CSR/CSC), or COO row ids
   int coo; int vsize;
   char* blob;
+  const int2* pieces;      // pCSC: (start, end) rank-local nonzero range per tile column; tile.y = first piece
 };
 
 struct RowLaunch {

@@ -530,6 +530,30 @@ __global__ void pack_kernel(const PackLaunch L) {
     }
     return;
   }
+  if (L.pieces) {   // pCSC band tile: gather each column's band piece, aux = local column ends
+    const int ncols = nrows;
+    const int2* pc = L.pieces + d.y;
+    uint16_t* a = reinterpret_cast<uint16_t*>(b);
+    if (lane == 0) {
+      int acc = 0;
+      a[0] = 0;
+      for (int j = 0; j < ncols; j++) { acc += pc[j].y - pc[j].x; a[j + 1] = (uint16_t)acc; }
+    }
+    const int ab = blob_aux_bytes(KIND_PTR, ncols, nnz);
+    const int vb = align16(nnz * L.vsize);
+    int* ix = reinterpret_cast<int*>(b + ab + vb);
+    int o = 0;
+    for (int j = 0; j < ncols; j++) {
+      const int s0 = pc[j].x, len = pc[j].y - pc[j].x;
+      for (int k = lane; k < len; k += 32) {
+        if (L.vsize == 8) reinterpret_cast<double*>(b + ab)[o + k] = static_cast<const double*>(L.val)[s0 + k];
+        else reinterpret_cast<float*>(b + ab)[o + k] = static_cast<const float*>(L.val)[s0 + k];
+        ix[o + k] = L.idx[s0 + k];
+      }
+      o += len;
+    }
+    return;
+  }
   const int kind = d.w >= 0 ? KIND_SLAB : (L.coo ? KIND_COO : KIND_PTR);
   const int ab = blob_aux_bytes(kind, nrows, nnz);
   const int vb = align16(nnz * L.vsize);
