@@ -155,6 +155,23 @@ msrep_status_t msrep_spmv_host(msrep_ctx ctx, const void* alpha, const void* x_h
 msrep_status_t msrep_plan(msrep_format fmt, int64_t outer, int64_t nnz, int np, const int64_t* ptr,
                           const int32_t* coo_row, msrep_part_desc* parts_out);
 
+/* Pure host: the exchange step of msrep_spmv for nranks > 1 (Sec. 4.3,
+ * P:602-607; readings R6, R9, R10) as msrep_spmv performs it, with
+ * np = nranks*parts_per_rank parts planned as msrep_plan does.
+ *   seg_out[2r], seg_out[2r+1]: y rows [lo, hi) rank r writes under OWNED /
+ *       SHARDED and broadcasts in the REPLICATED allgatherv (row formats: its
+ *       parts' owned rows; pCSC: uniform shards of ceil(m/nranks) rows, the
+ *       reduce-scatter blocks).  Array of 2*nranks, required.
+ *   head_row_out[j]: the row that receives part j's head partial (its flagged
+ *       first row, summed by the owner before alpha/beta), -1 if none. [np] or NULL.
+ *   head_part_out[j]: the part whose fix-up adds that partial (rank =
+ *       head_part_out[j] / parts_per_rank), -1 if none.  [np] or NULL.
+ * pCSC has no head exchange (heads -1): its partial vectors are summed.
+ * Errors as msrep_plan.  No device, no context. */
+msrep_status_t msrep_exchange_plan(msrep_format fmt, int64_t m, int64_t n, int64_t nnz, int nranks,
+                                   int parts_per_rank, const int64_t* ptr, const int32_t* coo_row, int64_t* seg_out,
+                                   int64_t* head_row_out, int32_t* head_part_out);
+
 msrep_status_t msrep_get_stats(msrep_ctx ctx, msrep_stats* out);
 
 /* Measurement hook (bench.py's roofline): while enabled, every msrep_spmv

@@ -278,6 +278,41 @@ struct Packer {
   }
 };
 
+// The parts q > j whose flagged head row is part j's last owned row, in part
+// order: the chain that continues j's tail row (reading R10).  Only
+// empty parts may sit between them.  Part j's fix-up adds their head partials.
+void tail_chain(const std::vector<msrep_part_desc>& P, int j, std::vector<int32_t>& chain) {
+  chain.clear();
+  const msrep_part_desc& d = P[(size_t)j];
+  if (d.start_idx > d.end_idx || d.owned_end <= d.owned_begin) return;
+  const int64_t last = d.owned_end - 1;
+  for (size_t q = (size_t)j + 1; q < P.size(); q++) {
+    const msrep_part_desc& e = P[q];
+    if (e.start_idx > e.end_idx) continue;
+    if (e.start_flag && e.start_row == last) { chain.push_back((int32_t)q); continue; }
+    break;
+  }
+}
+
+// y rows each rank writes (OWNED) and contributes to the allgatherv (REPLICATED):
+// row formats: the union of its parts' owned ranges [R_first, R_last) (reading R9);
+// pCSC: uniform shards of ceil(m / nranks) rows (the reduce-scatter blocks).
+void rank_segments(msrep_format fmt, int64_t m, int nranks, int vparts, const std::vector<msrep_part_desc>& parts,
+                   std::vector<int64_t>& lo, std::vector<int64_t>& hi) {
+  lo.resize((size_t)nranks);
+  hi.resize((size_t)nranks);
+  const int64_t shard = (m + nranks - 1) / nranks;
+  for (int r = 0; r < nranks; r++) {
+    if (fmt == MSREP_CSC) {
+      lo[(size_t)r] = std::min<int64_t>(m, (int64_t)r * shard);
+      hi[(size_t)r] = std::min<int64_t>(m, (int64_t)(r + 1) * shard);
+    } else {
+      lo[(size_t)r] = parts[(size_t)r * vparts].owned_begin;
+      hi[(size_t)r] = parts[(size_t)(r + 1) * vparts - 1].owned_end;
+    }
+  }
+}
+
 // Row formats (pCSR, pCOO): one rank's schedule.  Per local part j, in order:
 // head slabs (flagged first row, exported to its owner), the owned rows
 // [R_j, R_{j+1}) packed into row-aligned tiles (rows longer than a tile become
@@ -298,18 +333,9 @@ void build_row_schedule(const Ctx& c, const std::vector<int64_t>& lp, Schedule& 
     S.part_rec.push_back(h0);
     S.part_rec.push_back(S.nrec);
     // tail: the next non-empty part is flagged and starts in our last owned row
-    int64_t tail = -1;
     std::vector<int32_t> chain;
-    if (!empty && d.owned_end > d.owned_begin) {
-      const int64_t last = d.owned_end - 1;
-      for (int q = j + 1; q < c.np; q++) {
-        const msrep_part_desc& e = P[(size_t)q];
-        if (e.start_idx > e.end_idx) continue;
-        if (e.start_flag && e.start_row == last) { chain.push_back(q); continue; }
-        break;
-      }
-      if (!chain.empty()) tail = last;
-    }
+    tail_chain(P, j, chain);
+    const int64_t tail = chain.empty() ? -1 : d.owned_end - 1;
     const int64_t rend = tail >= 0 ? tail : d.owned_end;
     auto one_row = [&](int64_t r) {
       const int64_t len = pk.le(r) - pk.ls(r);
@@ -425,17 +451,7 @@ msrep_status_t allgatherv_y(Ctx* c, void* y, const std::vector<int64_t>& lo, con
 }
 
 void owned_segments(const Ctx* c, std::vector<int64_t>& lo, std::vector<int64_t>& hi) {
-  lo.resize((size_t)c->nranks);
-  hi.resize((size_t)c->nranks);
-  for (int r = 0; r < c->nranks; r++) {
-    if (c->fmt == MSREP_CSC) {
-      lo[(size_t)r] = std::min<int64_t>(c->m, (int64_t)r * c->shard);
-      hi[(size_t)r] = std::min<int64_t>(c->m, (int64_t)(r + 1) * c->shard);
-    } else {
-      lo[(size_t)r] = c->parts[(size_t)r * c->vparts].owned_begin;
-      hi[(size_t)r] = c->parts[(size_t)(r + 1) * c->vparts - 1].owned_end;
-    }
-  }
+  rank_segments(c->fmt, c->m, c->nranks, c->vparts, c->parts, lo, hi);
 }
 
 double get_scalar(const void* p, msrep_dtype t) {
@@ -472,6 +488,35 @@ msrep_status_t msrep_plan(msrep_format fmt, int64_t outer, int64_t nnz, int np, 
   } else {
     return fail(MSREP_ERR_INVALID_ARG, "unknown format %d", (int)fmt);
   }
+  return MSREP_OK;
+}
+
+msrep_status_t msrep_exchange_plan(msrep_format fmt, int64_t m, int64_t n, int64_t nnz, int nranks,
+                                   int parts_per_rank, const int64_t* ptr, const int32_t* coo_row, int64_t* seg_out,
+                                   int64_t* head_row_out, int32_t* head_part_out) {
+  if (nranks < 1 || parts_per_rank < 1 || m < 0 || n < 0 || nnz < 0 || !seg_out)
+    return fail(MSREP_ERR_INVALID_ARG, "bad exchange-plan arguments");
+  const int np = nranks * parts_per_rank;
+  const int64_t outer = fmt == MSREP_CSC ? n : m;
+  std::vector<msrep_part_desc> parts((size_t)np);
+  TRY(msrep_plan(fmt, outer, nnz, np, ptr, coo_row, parts.data()));
+  std::vector<int64_t> lo, hi;
+  rank_segments(fmt, m, nranks, parts_per_rank, parts, lo, hi);
+  for (int r = 0; r < nranks; r++) { seg_out[2 * r] = lo[(size_t)r]; seg_out[2 * r + 1] = hi[(size_t)r]; }
+  std::vector<int64_t> hrow((size_t)np, -1);
+  std::vector<int32_t> hpart((size_t)np, -1);
+  if (fmt != MSREP_CSC) {
+    std::vector<int32_t> chain;
+    for (int j = 0; j < np; j++) {
+      tail_chain(parts, j, chain);
+      for (int32_t q : chain) { hrow[(size_t)q] = parts[(size_t)j].owned_end - 1; hpart[(size_t)q] = j; }
+    }
+    for (int q = 0; q < np; q++)
+      if (parts[(size_t)q].start_idx <= parts[(size_t)q].end_idx && parts[(size_t)q].start_flag && hpart[(size_t)q] < 0)
+        return fail(MSREP_ERR_STATE, "internal: head of part %d has no owner", q);
+  }
+  if (head_row_out) memcpy(head_row_out, hrow.data(), hrow.size() * sizeof(int64_t));
+  if (head_part_out) memcpy(head_part_out, hpart.data(), hpart.size() * sizeof(int32_t));
   return MSREP_OK;
 }
 
