@@ -69,6 +69,7 @@ _sig = {
     "msrep_spmv": [P, P, P, P, P, I, P],
     "msrep_spmv_host": [P, P, P, P, P, I, P],
     "msrep_plan": [I, I64, I64, I, P, P, P],
+    "msrep_exchange_plan": [I, I64, I64, I64, I, I, P, P, P, P, P],
     "msrep_get_stats": [P, ctypes.POINTER(Stats)],
     "msrep_destroy": [P],
     "msrep_profile_enable": [P, I],
@@ -83,7 +84,7 @@ _lib.msrep_version.argtypes = []
 _lib.msrep_version.restype = ctypes.c_int
 
 EXPORTED = ["msrep_get_unique_id", "msrep_create", "msrep_partition", "msrep_spmv", "msrep_spmv_host",
-            "msrep_plan", "msrep_get_stats", "msrep_destroy", "msrep_last_error", "msrep_version",
+            "msrep_plan", "msrep_exchange_plan", "msrep_get_stats", "msrep_destroy", "msrep_last_error", "msrep_version",
             "msrep_profile_enable", "msrep_profile_read"]
 
 
@@ -158,6 +159,22 @@ def msrep_plan(fmt, outer, nnz, np_, ptr=None, coo_row=None):
         coo_row = np.ascontiguousarray(coo_row, np.int32)
     _check(_lib.msrep_plan(fmt, outer, nnz, np_, _ptr(ptr), _ptr(coo_row), _ptr(parts)), "msrep_plan")
     return parts
+
+
+def msrep_exchange_plan(fmt, m, n, nnz, nranks, parts_per_rank, ptr=None, coo_row=None):
+    """Pure host: the multi-rank exchange step msrep_spmv performs (include/msrep.h).
+    Returns (seg[nranks, 2] y-row segments per rank, head_row[np], head_part[np])."""
+    np_ = nranks * parts_per_rank
+    seg = np.zeros(2 * nranks, np.int64)
+    hrow = np.zeros(np_, np.int64)
+    hpart = np.zeros(np_, np.int32)
+    if ptr is not None:
+        ptr = np.ascontiguousarray(ptr, np.int64)
+    if coo_row is not None:
+        coo_row = np.ascontiguousarray(coo_row, np.int32)
+    _check(_lib.msrep_exchange_plan(fmt, m, n, nnz, nranks, parts_per_rank, _ptr(ptr), _ptr(coo_row), _ptr(seg),
+                                    _ptr(hrow), _ptr(hpart)), "msrep_exchange_plan")
+    return seg.reshape(nranks, 2), hrow, hpart
 
 
 def msrep_get_stats(ctx) -> dict:
