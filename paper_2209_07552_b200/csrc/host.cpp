@@ -12,7 +12,9 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -146,6 +148,12 @@ struct Ctx {
   double* d_head_all = nullptr;
   double* d_py = nullptr;
   int64_t py_len = 0;
+  // pCSC row-band layout
+  int4* d_citems = nullptr;
+  int32_t* d_band_item = nullptr;
+  char* d_cval = nullptr;
+  uint32_t* d_cpk = nullptr;
+  int64_t cnb = 0, citems = 0;
   int nheads_local = 0;
 
   // host-vector path buffers
@@ -369,63 +377,96 @@ void build_row_schedule(const Ctx& c, const std::vector<int64_t>& lp, Schedule& 
   }
 }
 
-// pCSC: tiles are (row band, group of consecutive columns) -- each column
-// contributes the piece of its nonzeros whose rows fall in the band.  Bands are
-// sized so one band of the fp64 partial vector py stays L2-resident while its
-// red.global.add.f64 scatter runs (B200: 126 MB L2).  Tiles are emitted band by
-// band, so concurrently running warps touch one or two bands.  Needs row indices
-// sorted within each column (checked); otherwise one band.  pieces[] holds the
-// (start, end) rank-local nonzero range of every (tile, column).
-constexpr int64_t PY_BAND_BYTES = 40ll << 20;
+// pCSC device layout (internal.h "row-band layout"): a stable parallel counting
+// sort of the rank's nonzeros by (row band, column chunk), done on the host
+// threads at partition time.  CSC order is kept inside every (band, chunk)
+// item, each item is padded to a multiple of 4 entries (16-B aligned TMA).
+struct CscBands {
+  int64_t nb = 0, nch = 1, total = 0;     // bands, column chunks, padded entries
+  std::vector<int4> items;                // {begin lo, begin hi, count, window col base}
+  std::vector<int32_t> band_item;         // [nb + 1]
+  std::unique_ptr<char[]> val;            // total * V
+  std::unique_ptr<uint32_t[]> pk;         // total
+};
 
-void build_col_schedule(const Ctx& c, const std::vector<int64_t>& lp, const int32_t* idx, Schedule& S,
-                        std::vector<int32_t>& pieces) {
+msrep_status_t build_csc_bands(const Ctx& c, const std::vector<int64_t>& lp, const int32_t* idx, const void* val,
+                               size_t V, CscBands& B) {
   const int64_t W = c.whi - c.wlo;
-  const int32_t* rows = idx + c.B_lo;   // rank-local view
-  bool sorted = true;
-  for (int64_t q = 0; q < W && sorted; q++)
-    for (int64_t z = lp[(size_t)q] + 1; z < lp[(size_t)q + 1]; z++)
-      if (rows[z] < rows[z - 1]) { sorted = false; break; }
-  const int64_t band_rows = std::max<int64_t>(1, PY_BAND_BYTES / 8);
-  const int64_t nb = sorted ? std::max<int64_t>(1, (c.m + band_rows - 1) / band_rows) : 1;
-  for (int64_t b = 0; b < nb; b++) {
-    const int32_t rlo = (int32_t)(b * band_rows), rhi = (int32_t)std::min<int64_t>(c.m, (b + 1) * band_rows);
-    int64_t c0 = -1, ncols = 0, nnz = 0, pbase = 0;
-    auto flush = [&]() {
-      if (c0 >= 0 && nnz > 0)
-        S.tiles.push_back({(int32_t)(c0 - c.wlo), (int32_t)pbase, (int32_t)(ncols | (nnz << 16)), -1});
-      else if (c0 >= 0)
-        pieces.resize((size_t)pbase * 2);   // drop an all-empty group
-      c0 = -1; ncols = 0; nnz = 0;
-    };
-    for (int64_t col = c.wlo; col < c.whi; col++) {
-      const int64_t z0 = lp[(size_t)(col - c.wlo)], z1 = lp[(size_t)(col - c.wlo + 1)];
-      int64_t ps = z0, pe = z1;
-      if (nb > 1) {
-        ps = std::lower_bound(rows + z0, rows + z1, rlo) - rows;
-        pe = std::lower_bound(rows + ps, rows + z1, rhi) - rows;
-      }
-      const int64_t len = pe - ps;
-      if (len + 1 > TILE_ITEMS) {            // a long column piece: single-column tiles of <= SLAB_NNZ
-        flush();
-        for (int64_t z = ps; z < pe; z += SLAB_NNZ) {
-          const int64_t e = std::min<int64_t>(pe, z + SLAB_NNZ);
-          S.tiles.push_back({(int32_t)(col - c.wlo), (int32_t)pieces.size() / 2, (int32_t)(1 | ((e - z) << 16)), -1});
-          pieces.push_back((int32_t)z);
-          pieces.push_back((int32_t)e);
-          S.nslabs++;
-        }
-        continue;
-      }
-      if (c0 >= 0 && (ncols + nnz + len + 1 > TILE_ITEMS || ncols >= MAX_TILE_ROWS)) flush();
-      if (c0 < 0) { c0 = col; pbase = (int64_t)pieces.size() / 2; }
-      pieces.push_back((int32_t)ps);
-      pieces.push_back((int32_t)pe);
-      ncols++;
-      nnz += len;
+  const int64_t nz = c.B_hi - c.B_lo;
+  const int32_t* rows = idx + c.B_lo;
+  const char* vals = static_cast<const char*>(val) + (size_t)c.B_lo * V;
+  B.nb = (c.m + CB_ROWS - 1) / CB_ROWS;
+  B.nch = std::max<int64_t>(1, (W + ((int64_t)1 << CB_COL_BITS) - 1) >> CB_COL_BITS);
+  const int64_t keys = B.nb * B.nch;
+  if (keys > ((int64_t)1 << 24))
+    return fail(MSREP_ERR_TOO_LARGE, "pCSC band layout: ceil(m/%d)*ceil(cols/2^%d) = %lld keys > 2^24", CB_ROWS,
+                CB_COL_BITS, (long long)keys);
+  int T = (int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  while (T > 1 && (int64_t)T * keys > ((int64_t)1 << 25)) T--;
+  if (nz < (1 << 20)) T = 1;
+  // column ranges with ~equal nonzeros per thread
+  std::vector<int64_t> cb((size_t)T + 1, W);
+  cb[0] = 0;
+  for (int t = 1; t < T; t++)
+    cb[(size_t)t] = std::lower_bound(lp.begin(), lp.end(), nz * t / T) - lp.begin();
+  for (int t = 1; t <= T; t++) cb[(size_t)t] = std::max(cb[(size_t)t], cb[(size_t)t - 1]);
+  std::vector<std::vector<int64_t>> off((size_t)T, std::vector<int64_t>((size_t)keys, 0));
+  auto key_of = [&](int64_t q, int32_t r) { return ((int64_t)r >> CB_LOG2) * B.nch + (q >> CB_COL_BITS); };
+  auto run = [&](auto&& f) {
+    std::vector<std::thread> th;
+    for (int t = 1; t < T; t++) th.emplace_back(f, t);
+    f(0);
+    for (auto& x : th) x.join();
+  };
+  run([&](int t) {
+    auto& o = off[(size_t)t];
+    for (int64_t q = cb[(size_t)t]; q < cb[(size_t)t + 1]; q++)
+      for (int64_t z = lp[(size_t)q]; z < lp[(size_t)q + 1]; z++) o[(size_t)key_of(q, rows[z])]++;
+  });
+  std::vector<int64_t> kcount((size_t)keys), kbase((size_t)keys);
+  int64_t run_off = 0;
+  for (int64_t k = 0; k < keys; k++) {
+    int64_t tot = 0;
+    for (int t = 0; t < T; t++) {
+      const int64_t cnt = off[(size_t)t][(size_t)k];
+      off[(size_t)t][(size_t)k] = run_off + tot;
+      tot += cnt;
     }
-    flush();
+    kcount[(size_t)k] = tot;
+    kbase[(size_t)k] = run_off;
+    run_off += (tot + 3) & ~(int64_t)3;
   }
+  B.total = run_off;
+  B.val.reset(new char[(size_t)std::max<int64_t>(1, B.total) * V]);
+  B.pk.reset(new uint32_t[(size_t)std::max<int64_t>(1, B.total)]);
+  run([&](int t) {
+    auto& o = off[(size_t)t];
+    for (int64_t q = cb[(size_t)t]; q < cb[(size_t)t + 1]; q++)
+      for (int64_t z = lp[(size_t)q]; z < lp[(size_t)q + 1]; z++) {
+        const int32_t r = rows[z];
+        const int64_t dst = o[(size_t)key_of(q, r)]++;
+        memcpy(B.val.get() + (size_t)dst * V, vals + (size_t)z * V, V);
+        B.pk[(size_t)dst] = (uint32_t)(r & (CB_ROWS - 1)) |
+                            ((uint32_t)(q & (((int64_t)1 << CB_COL_BITS) - 1)) << CB_LOG2);
+      }
+  });
+  B.band_item.assign((size_t)B.nb + 1, 0);
+  for (int64_t b = 0; b < B.nb; b++) {
+    B.band_item[(size_t)b] = (int32_t)B.items.size();
+    for (int64_t ch = 0; ch < B.nch; ch++) {
+      const int64_t k = b * B.nch + ch, cnt = kcount[(size_t)k], beg = kbase[(size_t)k];
+      if (cnt == 0) continue;
+      for (int64_t e = beg + cnt; e < ((beg + cnt + 3) & ~(int64_t)3); e++) {   // padding: never read
+        memset(B.val.get() + (size_t)e * V, 0, V);
+        B.pk[(size_t)e] = 0;
+      }
+      if (cnt >= ((int64_t)1 << 31)) return fail(MSREP_ERR_TOO_LARGE, "pCSC band item too large");
+      B.items.push_back(make_int4((int32_t)(uint32_t)(beg & 0xffffffffll), (int32_t)(beg >> 32), (int32_t)cnt,
+                                  (int32_t)(ch << CB_COL_BITS)));
+    }
+  }
+  B.band_item[(size_t)B.nb] = (int32_t)B.items.size();
+  return MSREP_OK;
 }
 
 template <class T>
@@ -645,91 +686,104 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     }
   }
 
-  // ---- schedule
-  Schedule S;
-  std::vector<int32_t> pieces;
-  if (fmt == MSREP_CSC) build_col_schedule(*c, lp, idx, S, pieces);
-  else build_row_schedule(*c, lp, S);
-  c->ntiles = (int)S.tiles.size();
-  c->nsell = (int)S.sell.size();
-  c->nslabs = S.nslabs;
-  c->nrec = S.nrec;
-  c->nsplit = (int)S.sr_row.size();
-
-  // ---- upload this rank's slice (the only H2D of A) and build the tile blobs on the GPU
   const int64_t nz_r = B_hi - B_lo;
-  const size_t mark = c->bufs.size();   // temporaries allocated from here are freed after packing
-  void* vp;
-  TRY(dalloc(c, (size_t)nz_r * V, &vp, s));
-  if (nz_r) CUDA_TRY(cudaMemcpyAsync(vp, static_cast<const char*>(val) + (size_t)B_lo * V, (size_t)nz_r * V, cudaMemcpyHostToDevice, s));
-  int32_t *d_idx, *d_aux;
-  TRY(upload(c, idx + B_lo, (size_t)nz_r, &d_idx, s));
-  if (fmt == MSREP_COO) {
-    TRY(upload(c, coo_row + B_lo, (size_t)nz_r, &d_aux, s));
-  } else {
-    // upload the global pointer slice and rebase it on the GPU (Sec. 4.1)
-    int64_t* d_g;
-    TRY(upload(c, ptr + c->wlo, (size_t)W + 1, &d_g, s));
-    void* ap;
-    TRY(dalloc(c, ((size_t)W + 1) * 4, &ap, s));
-    d_aux = static_cast<int32_t*>(ap);
-    CUDA_TRY(launch_rebase(d_g, d_aux, W + 1, B_lo, B_hi, s));
-  }
-  static_assert(sizeof(TileHost) == sizeof(int4), "tile");
-  const size_t ngen = S.tiles.size();
-  S.tiles.insert(S.tiles.end(), S.sell.begin(), S.sell.end());   // packed together, launched apart
-  std::vector<int32_t> blob16(S.tiles.size());
-  int64_t blob_total = 0;
-  for (size_t t = 0; t < S.tiles.size(); t++) {
-    const TileHost& th = S.tiles[t];
-    const int kind = th.rec == -2 ? KIND_SELL : th.rec >= 0 ? KIND_SLAB : (fmt == MSREP_COO ? KIND_COO : KIND_PTR);
-    if (blob_total / 16 >= (int64_t)1 << 31) return fail(MSREP_ERR_TOO_LARGE, "tile blob exceeds 32 GiB");
-    blob16[t] = (int32_t)(blob_total / 16);
-    blob_total += blob_bytes(kind, th.packed & 0xffff, th.packed >> 16, (int)V);
-  }
-  int4* d_tiles_orig;
-  int32_t* d_blob16;
-  int32_t* d_pieces = nullptr;
-  if (fmt == MSREP_CSC) TRY(upload_vec(c, pieces, &d_pieces, s));
-  TRY(upload(c, reinterpret_cast<const int4*>(S.tiles.data()), S.tiles.size(), &d_tiles_orig, s));
-  TRY(upload_vec(c, blob16, &d_blob16, s));
-  const size_t keep_from = c->bufs.size();
-  void* bp;
-  TRY(dalloc(c, (size_t)std::max<int64_t>(16, blob_total), &bp, s));
-  c->d_blob = static_cast<char*>(bp);
-  PackLaunch PL{d_tiles_orig, d_blob16, (int)S.tiles.size(), vp, d_idx, d_aux, fmt == MSREP_COO, (int)V, c->d_blob,
-                reinterpret_cast<const int2*>(d_pieces)};
-  CUDA_TRY(launch_pack(PL, s));
-  std::vector<TileHost> fin(S.tiles);
-  for (size_t t = 0; t < fin.size(); t++) fin[t].nz0 = blob16[t];
-  CUDA_TRY(cudaStreamSynchronize(s));
-  release_range(c, mark, keep_from);   // plain slices are no longer needed: the blobs hold the partition
-  TRY(upload(c, reinterpret_cast<const int4*>(fin.data()), ngen, &c->d_tiles, s));
-  TRY(upload(c, reinterpret_cast<const int4*>(fin.data() + ngen), fin.size() - ngen, &c->d_sell, s));
-  c->blob_bytes = blob_total;
-  void* rp;
-  TRY(dalloc(c, (size_t)std::max(1, S.nrec) * 8, &rp, s));
-  c->d_rec = static_cast<double*>(rp);
-  if (fmt != MSREP_CSC) {
-    TRY(upload_vec(c, S.sr_row, &c->d_sr_row, s));
-    TRY(upload_vec(c, S.sr_rec, &c->d_sr_rec, s));
-    TRY(upload_vec(c, S.sr_head, &c->d_sr_head, s));
-    TRY(upload_vec(c, S.head_list, &c->d_head_list, s));
-    TRY(upload_vec(c, S.part_rec, &c->d_part_rec, s));
-    void* hp;
-    TRY(dalloc(c, (size_t)c->vparts * 8, &hp, s));
-    c->d_head_local = static_cast<double*>(hp);
-    if (c->nranks > 1) {
-      TRY(dalloc(c, (size_t)c->np * 8, &hp, s));
-      c->d_head_all = static_cast<double*>(hp);
+  if (fmt == MSREP_CSC) {
+    // ---- pCSC: row-band layout built on the host threads, uploaded once
+    CscBands CB;
+    TRY(build_csc_bands(*c, lp, idx, val, V, CB));
+    TRY(upload_vec(c, CB.items, &c->d_citems, s));
+    TRY(upload_vec(c, CB.band_item, &c->d_band_item, s));
+    TRY(upload(c, CB.val.get(), (size_t)CB.total * V, &c->d_cval, s));
+    TRY(upload(c, CB.pk.get(), (size_t)CB.total, &c->d_cpk, s));
+    c->cnb = CB.nb;
+    c->citems = (int64_t)CB.items.size();
+    c->ntiles = 0; c->nsell = 0; c->nslabs = 0; c->nrec = 0; c->nsplit = 0;
+    c->blob_bytes = CB.total * (int64_t)(V + 4) + c->citems * 16 + (CB.nb + 1) * 4;
+    c->py_len = c->nranks > 1 ? c->shard * c->nranks : 0;
+    if (c->py_len) {
+      void* pp;
+      TRY(dalloc(c, (size_t)c->py_len * 8, &pp, s));
+      c->d_py = static_cast<double*>(pp);
+      // rows [m, py_len) are never written by the band kernel: zero them once
+      CUDA_TRY(cudaMemsetAsync(c->d_py + m, 0, (size_t)(c->py_len - m) * 8, s));
     }
-    c->nheads_local = 0;
-    for (int j = P0; j < P1; j++) c->nheads_local += parts[(size_t)j].start_flag ? 1 : 0;
+    CUDA_TRY(cudaStreamSynchronize(s));   // host staging buffers are freed on return
   } else {
-    c->py_len = c->nranks > 1 ? c->shard * c->nranks : m;
-    void* pp;
-    TRY(dalloc(c, (size_t)std::max<int64_t>(1, c->py_len) * 8, &pp, s));
-    c->d_py = static_cast<double*>(pp);
+    // ---- schedule
+    Schedule S;
+    build_row_schedule(*c, lp, S);
+    c->ntiles = (int)S.tiles.size();
+    c->nsell = (int)S.sell.size();
+    c->nslabs = S.nslabs;
+    c->nrec = S.nrec;
+    c->nsplit = (int)S.sr_row.size();
+
+    // ---- upload this rank's slice (the only H2D of A) and build the tile blobs on the GPU
+    const size_t mark = c->bufs.size();   // temporaries allocated from here are freed after packing
+    void* vp;
+    TRY(dalloc(c, (size_t)nz_r * V, &vp, s));
+    if (nz_r) CUDA_TRY(cudaMemcpyAsync(vp, static_cast<const char*>(val) + (size_t)B_lo * V, (size_t)nz_r * V, cudaMemcpyHostToDevice, s));
+    int32_t *d_idx, *d_aux;
+    TRY(upload(c, idx + B_lo, (size_t)nz_r, &d_idx, s));
+    if (fmt == MSREP_COO) {
+      TRY(upload(c, coo_row + B_lo, (size_t)nz_r, &d_aux, s));
+    } else {
+      // upload the global pointer slice and rebase it on the GPU (Sec. 4.1)
+      int64_t* d_g;
+      TRY(upload(c, ptr + c->wlo, (size_t)W + 1, &d_g, s));
+      void* ap;
+      TRY(dalloc(c, ((size_t)W + 1) * 4, &ap, s));
+      d_aux = static_cast<int32_t*>(ap);
+      CUDA_TRY(launch_rebase(d_g, d_aux, W + 1, B_lo, B_hi, s));
+    }
+    static_assert(sizeof(TileHost) == sizeof(int4), "tile");
+    const size_t ngen = S.tiles.size();
+    S.tiles.insert(S.tiles.end(), S.sell.begin(), S.sell.end());   // packed together, launched apart
+    std::vector<int32_t> blob16(S.tiles.size());
+    int64_t blob_total = 0;
+    for (size_t t = 0; t < S.tiles.size(); t++) {
+      const TileHost& th = S.tiles[t];
+      const int kind = th.rec == -2 ? KIND_SELL : th.rec >= 0 ? KIND_SLAB : (fmt == MSREP_COO ? KIND_COO : KIND_PTR);
+      if (blob_total / 16 >= (int64_t)1 << 31) return fail(MSREP_ERR_TOO_LARGE, "tile blob exceeds 32 GiB");
+      blob16[t] = (int32_t)(blob_total / 16);
+      blob_total += blob_bytes(kind, th.packed & 0xffff, th.packed >> 16, (int)V);
+    }
+    int4* d_tiles_orig;
+    int32_t* d_blob16;
+    TRY(upload(c, reinterpret_cast<const int4*>(S.tiles.data()), S.tiles.size(), &d_tiles_orig, s));
+    TRY(upload_vec(c, blob16, &d_blob16, s));
+    const size_t keep_from = c->bufs.size();
+    void* bp;
+    TRY(dalloc(c, (size_t)std::max<int64_t>(16, blob_total), &bp, s));
+    c->d_blob = static_cast<char*>(bp);
+    PackLaunch PL{d_tiles_orig, d_blob16, (int)S.tiles.size(), vp, d_idx, d_aux, fmt == MSREP_COO, (int)V, c->d_blob};
+    CUDA_TRY(launch_pack(PL, s));
+    std::vector<TileHost> fin(S.tiles);
+    for (size_t t = 0; t < fin.size(); t++) fin[t].nz0 = blob16[t];
+    CUDA_TRY(cudaStreamSynchronize(s));
+    release_range(c, mark, keep_from);   // plain slices are no longer needed: the blobs hold the partition
+    TRY(upload(c, reinterpret_cast<const int4*>(fin.data()), ngen, &c->d_tiles, s));
+    TRY(upload(c, reinterpret_cast<const int4*>(fin.data() + ngen), fin.size() - ngen, &c->d_sell, s));
+    c->blob_bytes = blob_total;
+    void* rp;
+    TRY(dalloc(c, (size_t)std::max(1, S.nrec) * 8, &rp, s));
+    c->d_rec = static_cast<double*>(rp);
+    {
+      TRY(upload_vec(c, S.sr_row, &c->d_sr_row, s));
+      TRY(upload_vec(c, S.sr_rec, &c->d_sr_rec, s));
+      TRY(upload_vec(c, S.sr_head, &c->d_sr_head, s));
+      TRY(upload_vec(c, S.head_list, &c->d_head_list, s));
+      TRY(upload_vec(c, S.part_rec, &c->d_part_rec, s));
+      void* hp;
+      TRY(dalloc(c, (size_t)c->vparts * 8, &hp, s));
+      c->d_head_local = static_cast<double*>(hp);
+      if (c->nranks > 1) {
+        TRY(dalloc(c, (size_t)c->np * 8, &hp, s));
+        c->d_head_all = static_cast<double*>(hp);
+      }
+      c->nheads_local = 0;
+      for (int j = P0; j < P1; j++) c->nheads_local += parts[(size_t)j].start_flag ? 1 : 0;
+    }
   }
   CUDA_TRY(cudaStreamSynchronize(s));
   const auto t1 = std::chrono::steady_clock::now();
@@ -740,7 +794,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   st.nparts = c->np; st.nranks = c->nranks; st.parts_per_rank = c->vparts;
   st.nnz_rank = nz_r;
   st.rows_window = W;
-  st.ntiles = c->ntiles; st.nsell = c->nsell; st.nslabs = c->nslabs; st.nsplit_rows = c->nsplit; st.nheads_local = c->nheads_local;
+  st.ntiles = fmt == MSREP_CSC ? c->citems : c->ntiles; st.nsell = c->nsell; st.nslabs = c->nslabs; st.nsplit_rows = c->nsplit; st.nheads_local = c->nheads_local;
   st.partition_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
   int64_t X = 0;
   if (fmt == MSREP_CSC) {
@@ -756,7 +810,9 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   if (fmt == MSREP_CSC) {
     const int64_t rows_out = c->nranks > 1 ? std::min<int64_t>(c->shard, std::max<int64_t>(0, m - (int64_t)c->rank * c->shard)) : m;
     own = rows_out;
-    base = nz_r * (int64_t)(V + 4) + (W + 1) * 4 + W * (int64_t)V + c->py_len * 8 + rows_out * 8;
+    // the rank's entries + its column pointer + its x window + (p > 1) the fp64 py write and the
+    // shard read after the reduce-scatter; p = 1 fuses alpha/beta into the band kernel (no py)
+    base = nz_r * (int64_t)(V + 4) + (W + 1) * 4 + W * (int64_t)V + (c->nranks > 1 ? m * 8 + rows_out * 8 : 0);
     ybytes_b1 = rows_out * (int64_t)V * 2;
     ybytes_b0 = rows_out * (int64_t)V;
   } else {
@@ -768,7 +824,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   st.owned_rows = own;
   st.alg_bytes = base + ybytes_b1;
   st.alg_bytes_beta0 = base + ybytes_b0;
-  if (fmt == MSREP_CSC) st.kernels_per_spmv = (c->ntiles ? 1 : 0) + 1 /*axpby*/ + 1 /*memset*/;
+  if (fmt == MSREP_CSC) st.kernels_per_spmv = (c->cnb ? 1 : 0) + (c->nranks > 1 ? 1 /*shard epilogue*/ : 0);
   else st.kernels_per_spmv = (c->ntiles ? 1 : 0) + (c->nsell ? 1 : 0) + (c->nranks > 1 && c->any_flag ? 1 : 0) + (c->nsplit ? 1 : 0);
   int64_t db = 0;
   for (auto& b : c->bufs) db += (int64_t)b.bytes;
@@ -805,11 +861,13 @@ msrep_status_t msrep_spmv(msrep_ctx h, const void* alpha_p, const void* x, const
   }
 
   if (c->fmt == MSREP_CSC) {
-    CUDA_TRY(cudaMemsetAsync(c->d_py, 0, (size_t)c->py_len * 8, s));
     ColLaunch L{};
-    L.tiles = c->d_tiles; L.ntiles = c->ntiles;
-    L.blob = c->d_blob;
-    L.x = x; L.xbase = c->wlo; L.py = c->d_py; L.dtype = dt;
+    L.items = c->d_citems; L.band_item = c->d_band_item; L.nb = (int)c->cnb;
+    L.val = c->d_cval; L.pk = c->d_cpk;
+    L.x = x; L.xbase = c->wlo;
+    L.fused = c->nranks == 1;
+    L.out = L.fused ? y : static_cast<void*>(c->d_py);
+    L.m = c->m; L.alpha = alpha; L.beta = beta; L.dtype = dt;
     cudaEvent_t pe;
     TRY(prof_begin(c, s, &pe));
     CUDA_TRY(launch_cols(L, s));
@@ -819,8 +877,6 @@ msrep_status_t msrep_spmv(msrep_ctx h, const void* alpha_p, const void* x, const
       NCCL_TRY(ncclReduceScatter(c->d_py, shard, (size_t)c->shard, ncclDouble, ncclSum, c->comm, s));
       CUDA_TRY(launch_axpby_py(shard, static_cast<char*>(y) + (size_t)my_lo * V, my_hi - my_lo, alpha, beta, dt, s));
       if (gather) TRY(allgatherv_y(c, y, seg_lo, seg_hi, s));
-    } else {
-      CUDA_TRY(launch_axpby_py(c->d_py, y, c->m, alpha, beta, dt, s));
     }
     return MSREP_OK;
   }

@@ -56,7 +56,6 @@ struct PackLaunch {        // build the tile blobs from the rank's plain slices 
   const void* val; const int32_t* idx; const int32_t* ptr;    // ptr: window-local pointer (CSR/CSC), or COO row ids
   int coo; int vsize;
   char* blob;
-  const int2* pieces;      // pCSC: (start, end) rank-local nonzero range per tile column; tile.y = first piece
 };
 
 struct RowLaunch {
@@ -76,12 +75,26 @@ struct SellLaunch {
   int dtype;
 };
 
+// pCSC row-band layout: the rank's nonzeros regrouped into
+// bands of CB_ROWS consecutive rows; inside a band they stay in CSC order
+// (column-major, stable) and are cut into items by column chunk (window column
+// >> CB_COL_BITS).  Per entry: the value, and a packed word
+// (row & (CB_ROWS-1)) | ((window col & (2^CB_COL_BITS-1)) << CB_LOG2).  Every
+// item starts 16-byte aligned (entry counts padded to a multiple of 4, padding
+// never read) so a 1-D TMA bulk copy moves it.  One CTA owns a band: its fp64
+// partial y lives in shared memory, so the scatter needs no global atomics.
+constexpr int CB_LOG2 = 13;
+constexpr int CB_ROWS = 1 << CB_LOG2;      // 8192 rows: 64 KB fp64 accumulator
+constexpr int CB_COL_BITS = 32 - CB_LOG2;  // 19: columns per chunk = 524288
 struct ColLaunch {
-  const int4* tiles; int ntiles;
-  const char* blob;
+  const int4* items;          // {begin lo, begin hi (entries), count, window col base}
+  const int32_t* band_item;   // [nb + 1]: items of band b are [band_item[b], band_item[b+1])
+  int nb;
+  const char* val; const uint32_t* pk;
   const void* x; int64_t xbase;                              // x index of window column 0
-  double* py;
-  int dtype;
+  void* out; int64_t m;                                      // fused: y (dtype); else fp64 py
+  double alpha, beta;
+  int fused; int dtype;
 };
 
 struct FixupLaunch {

@@ -20,9 +20,11 @@
 //               are bit-reproducible.
 //  fixup_kernel the beta-deferred merge of split rows (reading R6):
 //               y_r = alpha*(tail records + head partials, part order) + beta*y_r.
-//  cols_kernel  pCSC scatter (Alg. 5; "switch the role of x and
-//               y") into a full-length fp64 partial vector py with
-//               red.global.add.f64, same TMA tile staging.
+//  csc_band_kernel  pCSC scatter (Alg. 5; "switch the role of x
+//               and y"): one CTA per row band, fp64 partial y in
+//               shared memory, band entries TMA-streamed in CSC order, the
+//               alpha/beta epilogue (or the py write for the reduce-scatter)
+//               fused at band end.
 #include <climits>
 #include <cstdint>
 
@@ -101,13 +103,10 @@ struct WLayout {
 #define MSREP_ROW_NS 1
 #endif
 constexpr int ROW_NS = MSREP_ROW_NS;   // stages per warp (rows kernel)
-constexpr int COL_NS = 3;   // stages per warp (cols kernel)
 constexpr int PER_LANE = TILE_ITEMS / 32;   // 16 nonzeros per lane in a full tile
 
 template <typename VT, bool COO>
 using RowLayout = WLayout<RStage<VT, COO>::BYTES, ROW_NS, MAX_TILE_ROWS * 8>;
-template <typename VT>
-using ColLayout = WLayout<RStage<VT, false>::BYTES, COL_NS, MAX_TILE_ROWS * 8>;
 
 // Warp-level exclusive segmented scan of (key, value) pairs with keys
 // non-decreasing by lane: op((ka,va),(kb,vb)) = (kb, ka==kb ? va+vb : vb).
@@ -422,83 +421,146 @@ __global__ void __launch_bounds__(WARPS * 32) sell_kernel(const SellLaunch P) {
 }
 
 // ------------------------------------------------------------------ pCSC
-// pCSC scatter: per warp tile (a column group, or a piece of one long column),
-// stage x for its columns, then a merge-path walk over (column ends, nonzeros)
-// issues red.global.add.f64 of val*x[col] into the fp64 partial vector py.
+// pCSC per-GPU kernel (Alg. 5 "Launch": each part scatters its
+// columns' contributions into a partial y, "switch the role of x and y",
+// P:199).  The scatter target is a shared-memory fp64 accumulator of one row
+// band (CB_ROWS rows) owned by the CTA, so no global atomics and no global
+// zero-fill are needed; the band's entries (CSC order inside the band) stream
+// through a CB_NS-stage TMA ring filled by one producer warp.  At the end of a
+// band the consumers write it out once: fused y = alpha*acc + beta*y when one
+// rank holds the whole partial sum, else acc -> fp64 py for the reduce-scatter.
+constexpr int CB_E = 4096;                 // entries per stage
+constexpr int CB_NS = 3;                   // stages
+constexpr int CB_CW = 16;                  // consumer warps
+constexpr int CB_NC = CB_CW * 32;
+constexpr int CB_THREADS = CB_NC + 32;     // + one producer warp
 template <typename VT>
-__global__ void __launch_bounds__(WARPS * 32) cols_kernel(const ColLaunch P) {
-  using St = RStage<VT, false>;
-  using Lay = ColLayout<VT>;
-  constexpr int NS = COL_NS;
+struct CBLayout {
+  static constexpr int STAGE = CB_E * ((int)sizeof(VT) + 4);
+  static constexpr int ST_OFF = CB_ROWS * 8;
+  static constexpr int DESC_OFF = ST_OFF + CB_NS * STAGE;
+  static constexpr int BAR_OFF = DESC_OFF + CB_NS * 16;
+  static constexpr int TOTAL = BAR_OFF + 2 * CB_NS * 8;
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(bar)) : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+template <typename VT>
+__global__ void __launch_bounds__(CB_THREADS, 1) csc_band_kernel(const ColLaunch P) {
+  using L = CBLayout<VT>;
   constexpr int V = (int)sizeof(VT);
   extern __shared__ __align__(128) unsigned char smem[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  unsigned char* wb = smem + warp * Lay::WARP_B;
-  int4* sdesc = reinterpret_cast<int4*>(wb + Lay::DESC_OFF);
-  double* sx = reinterpret_cast<double*>(wb + Lay::SCR_OFF);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Lay::BAR_OFF) + warp * NS;
-  const int gw = blockIdx.x * WARPS + warp, nw = gridDim.x * WARPS;
-  const VT* __restrict__ x = static_cast<const VT*>(P.x);
-  double* __restrict__ py = P.py;
-
-  uint64_t pol = 0;
-  int4 dn = make_int4(0, 0, 0, -1);
-  if (lane == 0) {
-    for (int s = 0; s < NS; s++) mbar_init(&bars[s], 1);
+  double* acc = reinterpret_cast<double*>(smem);
+  int4* sdesc = reinterpret_cast<int4*>(smem + L::DESC_OFF);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* empty = full + CB_NS;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < CB_NS; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CB_CW);
+    }
     fence_mbar_init();
-    pol = policy_evict_first();
-    for (int s = 0; s < NS; s++) {
-      const int t = gw + s * nw;
-      if (t < P.ntiles) {
-        const int4 d = P.tiles[t];
-        sdesc[s] = d;
-        issue_blob(P.blob, d, KIND_PTR, V, wb + s * St::BYTES, &bars[s], pol);
-      }
-    }
-    if (gw + NS * nw < P.ntiles) dn = P.tiles[gw + NS * nw];
   }
-  __syncwarp();
-  for (int i = 0;; i++) {
-    const int t = gw + i * nw;
-    if (t >= P.ntiles) break;
-    const int s = i % NS;
-    mbar_wait(&bars[s], (uint32_t)((i / NS) & 1));
-    const int4 d = sdesc[s];
-    unsigned char* st = wb + s * St::BYTES;
-    const int ncols = d.z & 0xffff, nnz = d.z >> 16;
-    const int ab = blob_aux_bytes(KIND_PTR, ncols, nnz);
-    const uint16_t* sa = reinterpret_cast<const uint16_t*>(st);
-    const VT* sv = reinterpret_cast<const VT*>(st + ab);
-    const int* sr = reinterpret_cast<const int*>(st + ab + align16(nnz * V));
-    for (int cc = lane; cc < ncols; cc += 32) sx[cc] = (double)ldg_ro(x + P.xbase + d.x + cc);
-    __syncwarp();
-    const int items = ncols + nnz;
-    const int per = (items + 31) >> 5;
-    const int d0 = min(lane * per, items), d1 = min(d0 + per, items);
-    int lo = max(0, d0 - nnz), hi = min(d0, ncols);
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if ((int)sa[mid + 1] <= d0 - mid - 1) lo = mid + 1; else hi = mid;
-    }
-    int xc = lo, yz = d0 - lo;
-    int ce = xc < ncols ? (int)sa[xc + 1] : 0;
-    for (int q = d0; q < d1; q++) {
-      if (xc < ncols && yz < ce) {
-        atomicAdd(py + sr[yz], (double)sv[yz] * sx[xc]);
-        yz++;
-      } else {
-        xc++;
-        ce = xc < ncols ? (int)sa[xc + 1] : 0;
-      }
-    }
-    __syncwarp();
+  __syncthreads();
+
+  if (warp == CB_CW) {   // ---- producer: walks the CTA's bands, items and stage chunks
     if (lane == 0) {
-      const int tn = t + NS * nw;
-      if (tn < P.ntiles) {
-        sdesc[s] = dn;
-        issue_blob(P.blob, dn, KIND_PTR, V, st, &bars[s], pol);
-        if (tn + nw < P.ntiles) dn = P.tiles[tn + nw];
+      const uint64_t pol = policy_evict_first();
+      int it = 0;
+      auto acquire = [&](int4 d) {
+        const int s = it % CB_NS;
+        if (it >= CB_NS) mbar_wait(&empty[s], (uint32_t)(((it / CB_NS) - 1) & 1));
+        sdesc[s] = d;
+        return s;
+      };
+      for (int b = blockIdx.x; b < P.nb; b += gridDim.x) {
+        const int i0 = P.band_item[b], i1 = P.band_item[b + 1];
+        if (i0 == i1) {   // empty band: still written out (zeros / beta*y)
+          const int s = acquire(make_int4(b, 0, 0, 1));
+          mbar_arrive_expect_tx(&full[s], 0);
+          it++;
+          continue;
+        }
+        for (int i = i0; i < i1; i++) {
+          const int4 item = P.items[i];
+          const int64_t beg = (int64_t)(uint32_t)item.x | ((int64_t)item.y << 32);
+          for (int e = 0; e < item.z; e += CB_E) {
+            const int n = min(CB_E, item.z - e);
+            const int last = (i == i1 - 1 && e + CB_E >= item.z) ? 1 : 0;
+            const int s = acquire(make_int4(b, n, item.w, last));
+            const int n4 = (n + 3) & ~3;
+            unsigned char* st = smem + L::ST_OFF + s * L::STAGE;
+            mbar_arrive_expect_tx(&full[s], (uint32_t)(n4 * (V + 4)));
+            tma_1d(st, P.val + (beg + e) * V, (uint32_t)(n4 * V), &full[s], pol);
+            tma_1d(st + CB_E * V, P.pk + beg + e, (uint32_t)(n4 * 4), &full[s], pol);
+            it++;
+          }
+        }
       }
+      const int s = acquire(make_int4(-1, 0, 0, 0));
+      mbar_arrive_expect_tx(&full[s], 0);
+    }
+    return;
+  }
+
+  // ---- consumers
+  const int ct = threadIdx.x;
+  const VT* __restrict__ x = static_cast<const VT*>(P.x) + P.xbase;
+  for (int r = ct; r < CB_ROWS; r += CB_NC) acc[r] = 0.0;
+  named_bar_sync(1, CB_NC);
+  constexpr int PER = CB_E / CB_NC;
+  for (int it = 0;; it++) {
+    const int s = it % CB_NS;
+    mbar_wait(&full[s], (uint32_t)((it / CB_NS) & 1));
+    const int4 d = sdesc[s];
+    if (d.x < 0) break;
+    const unsigned char* st = smem + L::ST_OFF + s * L::STAGE;
+    const VT* sv = reinterpret_cast<const VT*>(st);
+    const uint32_t* sp = reinterpret_cast<const uint32_t*>(st + CB_E * V);
+    const VT* xb = x + d.z;
+    uint32_t pk[PER];
+    VT v[PER], xv[PER];
+#pragma unroll
+    for (int k = 0; k < PER; k++) {
+      const int i = ct + k * CB_NC;
+      pk[k] = i < d.y ? sp[i] : 0u;
+      v[k] = i < d.y ? sv[i] : VT(0);
+    }
+#pragma unroll
+    for (int k = 0; k < PER; k++) xv[k] = (ct + k * CB_NC < d.y) ? ldg_ro(xb + (pk[k] >> CB_LOG2)) : VT(0);
+#pragma unroll
+    for (int k = 0; k < PER; k++)
+      if (ct + k * CB_NC < d.y) atomicAdd(&acc[pk[k] & (CB_ROWS - 1)], (double)v[k] * (double)xv[k]);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (d.w) {   // band complete: write it out once, re-zero the accumulator
+      named_bar_sync(1, CB_NC);
+      const int64_t r0 = (int64_t)d.x * CB_ROWS;
+      const int64_t rem = P.m - r0;
+      const int nr = rem < CB_ROWS ? (int)rem : CB_ROWS;
+      if (P.fused) {
+        VT* y = static_cast<VT*>(P.out) + r0;
+        const double alpha = P.alpha, beta = P.beta;
+        for (int r = ct; r < nr; r += CB_NC) {
+          double o = alpha * acc[r];
+          if (beta != 0.0) o += beta * (double)y[r];
+          y[r] = (VT)o;
+          acc[r] = 0.0;
+        }
+      } else {
+        double* py = static_cast<double*>(P.out) + r0;
+        for (int r = ct; r < nr; r += CB_NC) {
+          py[r] = acc[r];
+          acc[r] = 0.0;
+        }
+      }
+      named_bar_sync(1, CB_NC);
     }
   }
 }
@@ -527,30 +589,6 @@ __global__ void pack_kernel(const PackLaunch L) {
       if (L.vsize == 8) reinterpret_cast<double*>(vb0)[u * SELL_ROWS + lane] = on ? static_cast<const double*>(L.val)[rs + u] : 0.0;
       else reinterpret_cast<float*>(vb0)[u * SELL_ROWS + lane] = on ? static_cast<const float*>(L.val)[rs + u] : 0.0f;
       ix[u * SELL_ROWS + lane] = on ? L.idx[rs + u] : 0;
-    }
-    return;
-  }
-  if (L.pieces) {   // pCSC band tile: gather each column's band piece, aux = local column ends
-    const int ncols = nrows;
-    const int2* pc = L.pieces + d.y;
-    uint16_t* a = reinterpret_cast<uint16_t*>(b);
-    if (lane == 0) {
-      int acc = 0;
-      a[0] = 0;
-      for (int j = 0; j < ncols; j++) { acc += pc[j].y - pc[j].x; a[j + 1] = (uint16_t)acc; }
-    }
-    const int ab = blob_aux_bytes(KIND_PTR, ncols, nnz);
-    const int vb = align16(nnz * L.vsize);
-    int* ix = reinterpret_cast<int*>(b + ab + vb);
-    int o = 0;
-    for (int j = 0; j < ncols; j++) {
-      const int s0 = pc[j].x, len = pc[j].y - pc[j].x;
-      for (int k = lane; k < len; k += 32) {
-        if (L.vsize == 8) reinterpret_cast<double*>(b + ab)[o + k] = static_cast<const double*>(L.val)[s0 + k];
-        else reinterpret_cast<float*>(b + ab)[o + k] = static_cast<const float*>(L.val)[s0 + k];
-        ix[o + k] = L.idx[s0 + k];
-      }
-      o += len;
     }
     return;
   }
@@ -689,10 +727,11 @@ cudaError_t launch_sell_t(const SellLaunch& L, cudaStream_t s) {
 
 template <typename VT>
 cudaError_t launch_cols_t(const ColLaunch& L, cudaStream_t s) {
-  constexpr int b = ColLayout<VT>::TOTAL;
-  cudaError_t e = set_smem(cols_kernel<VT>, b);
+  constexpr int b = CBLayout<VT>::TOTAL;
+  cudaError_t e = set_smem(csc_band_kernel<VT>, b);
   if (e) return e;
-  cols_kernel<VT><<<grid_for(cols_kernel<VT>, b, L.ntiles), WARPS * 32, b, s>>>(L);
+  const int g = L.nb < num_sms() ? L.nb : num_sms();
+  csc_band_kernel<VT><<<g, CB_THREADS, b, s>>>(L);
   return cudaGetLastError();
 }
 
@@ -710,7 +749,7 @@ cudaError_t launch_sell(const SellLaunch& L, cudaStream_t s) {
 }
 
 cudaError_t launch_cols(const ColLaunch& L, cudaStream_t s) {
-  if (L.ntiles == 0) return cudaSuccess;
+  if (L.nb == 0) return cudaSuccess;
   return L.dtype == 0 ? launch_cols_t<double>(L, s) : launch_cols_t<float>(L, s);
 }
 

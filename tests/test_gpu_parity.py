@@ -254,3 +254,32 @@ def test_config4_tallskinny_csc_sampled():
     A = gen.kdistinct_csc(50_000_000, 1_000_000, 500, seed=4, kind=gen.SMALLINT)
     x = gen.vector(A["n"], 9, kind=gen.SMALLINT); y = gen.vector(A["m"], 10, kind=gen.SMALLINT)
     check(A, "csc", x, y, 2.0, 0.5, exact=True)
+
+
+# ------------------------------------------------------ pCSC row-band layout
+def _csc_drop_rows(A, lo, hi):
+    """CSC copy of A without the entries whose row is in [lo, hi) (empty row bands)."""
+    keep = ~((A["idx"] >= lo) & (A["idx"] < hi))
+    cols = np.repeat(np.arange(A["n"]), np.diff(A["ptr"]))[keep]
+    ptr = np.zeros(A["n"] + 1, np.int64)
+    np.add.at(ptr, cols + 1, 1)
+    return gen.Sparse(fmt="csc", m=A["m"], n=A["n"], ptr=np.cumsum(ptr), idx=A["idx"][keep], val=A["val"][keep])
+
+
+@pytest.mark.parametrize("parts", [1, 3])
+def test_csc_bands_column_chunks_bit_exact(parts):
+    """Several 8192-row bands (ragged last band), > 2^19 columns (two column chunks per
+    band), an entirely empty band: bit-exact vs the oracle on integer data."""
+    A = gen.kdistinct_csc(3 * 8192 + 17, (1 << 19) + 1000, 2, seed=41, kind=gen.SMALLINT)
+    A = _csc_drop_rows(A, 8192, 2 * 8192)
+    x = gen.vector(A["n"], 42, kind=gen.SMALLINT); y = gen.vector(A["m"], 43, kind=gen.SMALLINT)
+    for alpha, beta in [(1.5, 0.5), (2.0, 0.0), (-1.0, 1.0)]:
+        check(A, "csc", x, y, alpha, beta, parts=parts, exact=True)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_csc_bands_uniform_tolerance(dtype):
+    """Dense-ish columns spanning many bands, U[-1,1) values: per-row tolerance."""
+    A = to_dtype(gen.kdistinct_csc(100_000, 3000, 400, seed=44), dtype)
+    x = gen.vector(A["n"], 45, dtype=dtype); y = gen.vector(A["m"], 46, dtype=dtype)
+    check(A, "csc", x, y, 1.5, 0.5, parts=2)
