@@ -255,8 +255,8 @@ struct Packer {
   void add_row(int64_t r) {
     const int64_t len = le(r) - ls(r);
     if (cur_r0 >= 0) {
-      const int64_t items = (cur_r1 - cur_r0) + (le(cur_r1 - 1) - ls(cur_r0));
-      if (items + len + 1 > TILE_ITEMS || cur_r1 - cur_r0 >= MAX_TILE_ROWS) flush();
+      const int64_t nz = le(cur_r1 - 1) - ls(cur_r0);
+      if (nz + len > TILE_NNZ || cur_r1 - cur_r0 >= MAX_TILE_ROWS) flush();
     }
     if (cur_r0 < 0) { cur_r0 = r; cur_r1 = r; }
     cur_r1 = r + 1;
@@ -347,7 +347,7 @@ void build_row_schedule(const Ctx& c, const std::vector<int64_t>& lp, Schedule& 
     const int64_t rend = tail >= 0 ? tail : d.owned_end;
     auto one_row = [&](int64_t r) {
       const int64_t len = pk.le(r) - pk.ls(r);
-      if (len + 1 > TILE_ITEMS) {
+      if (len > TILE_NNZ) {
         pk.flush();
         S.sr_row.push_back(r);
         S.sr_rec.push_back(S.nrec);
@@ -743,7 +743,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     int64_t blob_total = 0;
     for (size_t t = 0; t < S.tiles.size(); t++) {
       const TileHost& th = S.tiles[t];
-      const int kind = th.rec == -2 ? KIND_SELL : th.rec >= 0 ? KIND_SLAB : (fmt == MSREP_COO ? KIND_COO : KIND_PTR);
+      const int kind = th.rec == -2 ? KIND_SELL : th.rec >= 0 ? KIND_SLAB : KIND_SEG;
       if (blob_total / 16 >= (int64_t)1 << 31) return fail(MSREP_ERR_TOO_LARGE, "tile blob exceeds 32 GiB");
       blob16[t] = (int32_t)(blob_total / 16);
       blob_total += blob_bytes(kind, th.packed & 0xffff, th.packed >> 16, (int)V);
@@ -756,7 +756,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     void* bp;
     TRY(dalloc(c, (size_t)std::max<int64_t>(16, blob_total), &bp, s));
     c->d_blob = static_cast<char*>(bp);
-    PackLaunch PL{d_tiles_orig, d_blob16, (int)S.tiles.size(), vp, d_idx, d_aux, fmt == MSREP_COO, (int)V, c->d_blob};
+    PackLaunch PL{d_tiles_orig, d_blob16, (int)S.tiles.size(), vp, d_idx, d_aux, fmt == MSREP_COO, (int)V, c->wlo, c->d_blob};
     CUDA_TRY(launch_pack(PL, s));
     std::vector<TileHost> fin(S.tiles);
     for (size_t t = 0; t < fin.size(); t++) fin[t].nz0 = blob16[t];
@@ -887,7 +887,7 @@ msrep_status_t msrep_spmv(msrep_ctx h, const void* alpha_p, const void* x, const
   L.x = x; L.y = y; L.ybase = c->wlo;
   L.xmax = c->n > 0 ? (uint32_t)(c->n - 1) : 0u;
   L.alpha = alpha; L.beta = beta; L.rec = c->d_rec;
-  L.coo = c->fmt == MSREP_COO; L.dtype = dt;
+  L.dtype = dt;
   SellLaunch SL{c->d_sell, c->nsell, c->d_blob, x, y, c->wlo, alpha, beta, dt};
   cudaEvent_t pe;
   TRY(prof_begin(c, s, &pe));

@@ -8,53 +8,66 @@
 namespace msrep {
 
 // A tile is the unit of work one WARP processes: a row-aligned group of whole
-// rows whose merge items (rows + nonzeros) fit TILE_ITEMS, or a "slab" -- a
+// rows (<= MAX_TILE_ROWS rows, <= TILE_NNZ nonzeros), or a "slab" -- a
 // contiguous piece (<= SLAB_NNZ nonzeros) of one split row whose partial sum
-// goes to a record instead of y.  For pCSC, tiles are
-// column groups / column pieces and every tile scatters into py.
-constexpr int TILE_ITEMS = 512;
-constexpr int MAX_TILE_ROWS = 64;    // rows (or columns) per normal tile
+// goes to a record instead of y.
+constexpr int TILE_NNZ = 512;
+constexpr int MAX_TILE_ROWS = 128;   // rows per segment tile (uint8 tile-local row keys)
 constexpr int SLAB_NNZ = 512;
 #ifndef MSREP_WARPS
 #define MSREP_WARPS 8
 #endif
 constexpr int WARPS = MSREP_WARPS;   // warps per CTA (each with its own TMA ring)
 
-// Device layout: every tile is one contiguous, 16-byte aligned "blob"
-//   [aux][val][idx]
-// aux = tile-local row (col) pointer as uint16 (nrows+1 entries; pCSR/pCSC
-// normal tiles), or the global row ids (int32, one per nonzero; pCOO normal
-// tiles), or nothing (slabs); val = nnz values; idx = nnz column (row) ids.
-// Each segment is padded to 16 bytes so one TMA bulk copy moves the tile.
+// Device layout: every tile is one contiguous, 16-byte aligned "blob"; each
+// segment is padded to 16 bytes so one TMA bulk copy moves the tile.
 //
-// SELL tiles (regular rows, pCSR only): SELL_ROWS consecutive rows, lane = row;
-// element t of lane l sits at t * SELL_ROWS + l (sliced-ELL within the tile,
-// W = longest row <= SELL_W_MAX, shorter rows padded with val 0 / col 0 and
-// masked in the kernel); aux = the SELL_ROWS row lengths (uint16).  The host
-// only forms a SELL tile when padding is <= 1/8 of its elements.
-enum TileKind { KIND_PTR = 0, KIND_COO = 1, KIND_SLAB = 2, KIND_SELL = 3 };
+// SEG tile (pCSR and pCOO irregular rows): [key u8 x nnz][val x nnz][col i32 x nnz]
+//   key = tile-local row of the nonzero.  Lane-chunked order: lane l owns the
+//   contiguous nonzeros [b_l, b_l + len_l) of the tile, b_l = l*q + min(l, r),
+//   len_l = q + (l < r), with q = nnz / 32, r = nnz % 32; its j-th nonzero
+//   (j < q) sits in slot j*32 + l and its extra one (j == q, l < r) in slot
+//   32*q + l.  Every shared-memory read of the kernel is a conflict-free
+//   32-lane vector and the lane's products stay in registers.  pCOO tiles use
+//   the same layout (row ids rebased at pack time): the paper also runs its
+//   CSR kernel on COO input.
+// SLAB tile: [val x nnz][col x nnz] in natural order.
+// SELL tile (regular pCSR rows): SELL_ROWS consecutive rows, lane = row;
+//   element t of lane l sits at t * SELL_ROWS + l (sliced-ELL within the tile,
+//   W = longest row <= SELL_W_MAX, shorter rows padded with val 0 / col 0 and
+//   masked in the kernel); aux = the SELL_ROWS row lengths (uint16).  The host
+//   only forms a SELL tile when padding is <= 1/8 of its elements.
+enum TileKind { KIND_SEG = 0, KIND_SLAB = 2, KIND_SELL = 3 };
 constexpr int SELL_ROWS = 32;
 constexpr int SELL_W_MAX = 32;
 __host__ __device__ inline int align16(int b) { return (b + 15) & ~15; }
 __host__ __device__ inline int blob_aux_bytes(int kind, int nrows, int nnz) {
-  return kind == KIND_PTR ? align16((nrows + 1) * 2)
-                          : (kind == KIND_COO ? align16(nnz * 4) : (kind == KIND_SELL ? SELL_ROWS * 2 : 0));
+  return kind == KIND_SEG ? align16(nnz) : (kind == KIND_SELL ? SELL_ROWS * 2 : 0);
 }
 // for KIND_SELL, `nnz` is the slice width W
 __host__ __device__ inline int blob_bytes(int kind, int nrows, int nnz, int vsize) {
   if (kind == KIND_SELL) return SELL_ROWS * 2 + nnz * SELL_ROWS * (vsize + 4);
   return blob_aux_bytes(kind, nrows, nnz) + align16(nnz * vsize) + align16(nnz * 4);
 }
+// slot of element e (0 <= e < nnz) in a SEG tile's lane-chunked order
+__host__ __device__ inline int seg_slot(int e, int nnz) {
+  const int q = nnz >> 5, r = nnz & 31;
+  const int big = r * (q + 1);   // elements owned by the r lanes with q+1 nonzeros
+  int lane, j;
+  if (e < big) { lane = e / (q + 1); j = e - lane * (q + 1); }
+  else { lane = r + (e - big) / q; j = e - (lane * q + r); }
+  return j < q ? j * 32 + lane : 32 * q + lane;
+}
 
-// int4 tile descriptor: x = first row (col), window-local; y = blob offset in
+// int4 tile descriptor: x = first row, window-local; y = blob offset in
 // 16-byte units; z = nrows | (nnz << 16) (SELL: nrows | (W << 16)); w = kind
-// of work (>= 0: slab record index; -1: merge-path / key walk; -2: SELL).
+// of work (>= 0: slab record index; -1: SEG tile; -2: SELL).
 struct TileHost { int32_t row0, nz0, packed, rec; };
 
 struct PackLaunch {        // build the tile blobs from the rank's plain slices (partition time)
   const int4* tiles; const int32_t* blob16; int ntiles;       // tiles: {row0, nz0 (rank-local), packed, w}
-  const void* val; const int32_t* idx; const int32_t* ptr;    // ptr: window-local pointer (CSR/CSC), or COO row ids
-  int coo; int vsize;
+  const void* val; const int32_t* idx; const int32_t* ptr;    // ptr: window-local pointer (CSR), or COO row ids
+  int coo; int vsize; int64_t row_base;                       // COO: global row of window row 0
   char* blob;
 };
 
@@ -64,7 +77,7 @@ struct RowLaunch {
   const void* x; void* y; int64_t ybase;                     // y row of window row 0
   uint32_t xmax;                                             // n - 1 (clamp for padding lanes)
   double alpha, beta; double* rec;
-  int coo; int dtype;                                        // dtype 0 = f64, 1 = f32
+  int dtype;                                                 // dtype 0 = f64, 1 = f32
 };
 
 struct SellLaunch {

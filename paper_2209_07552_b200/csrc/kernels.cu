@@ -59,6 +59,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(bar)) : "memory");
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -75,18 +78,33 @@ __device__ __forceinline__ void tma_1d(void* dst, const void* src, uint32_t byte
 
 template <typename T>
 __device__ __forceinline__ T ldg_ro(const T* p) { return __ldg(p); }
+// L2 policies: the matrix stream and y are touched once per SpMV (evict_first,
+// .cs); x is re-gathered by every nonzero of its column (evict_last), so the
+// y stream must not push it out of L2.
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double ldx(const double* p, uint64_t pol) {
+  double v;
+  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float ldx(const float* p, uint64_t pol) {
+  float v;
+  asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  return v;
+}
 
 // ---------------------------------------------------------------- layout
 // Every warp owns an independent NS-stage ring of tile blobs in shared memory.
 // Lane 0 issues ONE 1-D TMA bulk copy per tile (the blob is contiguous in HBM);
 // the warp waits on the stage's mbarrier, computes, and refills the stage --
 // no cross-warp synchronisation, so a slow warp never stalls another's loads.
-template <typename VT, bool COO>
+template <typename VT>
 struct RStage {
-  static constexpr int AUX_CAP = COO ? TILE_ITEMS * 4 : ((MAX_TILE_ROWS + 1) * 2 + 15) / 16 * 16;
-  static constexpr int BYTES = AUX_CAP + TILE_ITEMS * (int)sizeof(VT) + TILE_ITEMS * 4;
-  // products (fp64) are written in place from byte `aux` on: 8 * TILE_ITEMS bytes must fit
-  static_assert(TILE_ITEMS * ((int)sizeof(VT) + 4) >= 8 * TILE_ITEMS, "in-place product buffer");
+  static constexpr int BYTES = TILE_NNZ + TILE_NNZ * (int)sizeof(VT) + TILE_NNZ * 4;
 };
 
 template <int STAGE_B, int NS, int SCRATCH>
@@ -99,14 +117,8 @@ struct WLayout {
   static constexpr int TOTAL = BAR_OFF + WARPS * NS * 8;
 };
 
-#ifndef MSREP_ROW_NS
-#define MSREP_ROW_NS 1
-#endif
-constexpr int ROW_NS = MSREP_ROW_NS;   // stages per warp (rows kernel)
-constexpr int PER_LANE = TILE_ITEMS / 32;   // 16 nonzeros per lane in a full tile
+constexpr int QMAX = TILE_NNZ / 32;    // 16: nonzeros per lane in a full tile (+1 extra slot when ragged)
 
-template <typename VT, bool COO>
-using RowLayout = WLayout<RStage<VT, COO>::BYTES, ROW_NS, MAX_TILE_ROWS * 8>;
 
 // Warp-level exclusive segmented scan of (key, value) pairs with keys
 // non-decreasing by lane: op((ka,va),(kb,vb)) = (kb, ka==kb ? va+vb : vb).
@@ -127,7 +139,7 @@ __device__ __forceinline__ void warp_seg_scan(int key, double val, int& pk, doub
   pv = lane == 0 ? 0.0 : ev;
 }
 
-__device__ __forceinline__ int tile_kind(int4 d, bool coo) { return d.w >= 0 ? KIND_SLAB : (coo ? KIND_COO : KIND_PTR); }
+__device__ __forceinline__ int tile_kind(int4 d) { return d.w >= 0 ? KIND_SLAB : KIND_SEG; }
 
 __device__ __forceinline__ void issue_blob(const char* blob, int4 d, int kind, int vsize, unsigned char* st,
                                            uint64_t* bar, uint64_t pol) {
@@ -136,195 +148,179 @@ __device__ __forceinline__ void issue_blob(const char* blob, int4 d, int kind, i
   tma_1d(st, blob + (int64_t)d.y * 16, (uint32_t)bytes, bar, pol);
 }
 
-// pCSR / pCOO general tile kernel (SELL tiles run in sell_kernel).  Tile kinds:
+// pCSR / pCOO segment-tile kernel (SELL tiles run in sell_kernel).  Tile kinds:
 //   w >= 0   slab: partial sum of a piece of one split row -> rec[w]
-//   w == -1  merge-path walk (pCSR) / key-segmented walk (pCOO): irregular rows
-// Every tile first forms its products val*x[col] lane-strided (coalesced shared
-// memory reads, PER_LANE independent gathers in flight per lane, no per-element
-// predicates: padding lanes gather a clamped, valid x and are never summed);
-// normal tiles store them (fp64) in place in the stage, reduce rows from shared
-// memory and write y = alpha*s + beta*y coalesced.
-template <typename VT, bool COO>
-__global__ void __launch_bounds__(WARPS * 32) rows_kernel(const RowLaunch P) {
-  using St = RStage<VT, COO>;
-  using Lay = RowLayout<VT, COO>;
-  constexpr int NS = ROW_NS;
+//   w == -1  SEG tile: whole rows; lane l reduces its contiguous chunk of
+//            nonzeros in registers (keyed by the uint8 tile-local row), rows
+//            crossing lanes are joined by one deterministic warp segmented
+//            scan, y = alpha*s + beta*y is written coalesced.
+// pCSR / pCOO tile kernel (SELL tiles run in sell_kernel).  Persistent CTAs;
+// every warp owns a one-slot TMA ring and walks tiles gw, gw+nw, ...  A tile is
+// copied from its slot into registers as soon as it lands and the warp's next
+// tile is issued into the slot right away, so that TMA overlaps this tile's
+// x gathers and reduction.  Tile kinds (internal.h):
+//   slab: partial sum of a piece of one split row -> rec[w] (natural order,
+//         fixed shuffle tree: bit-reproducible)
+//   SEG:  whole rows; lane l reduces its contiguous chunk of nonzeros keyed by
+//         the uint8 tile-local row, rows crossing lanes are joined by one
+//         deterministic warp segmented scan, y = alpha*s + beta*y is written
+//         coalesced.
+#ifndef MSREP_ROW_MINB
+#define MSREP_ROW_MINB 2
+#endif
+template <typename VT>
+using RowLayout = WLayout<RStage<VT>::BYTES, 1, MAX_TILE_ROWS * 8>;
+
+template <typename VT>
+__global__ void __launch_bounds__(WARPS * 32, MSREP_ROW_MINB) rows_kernel(const RowLaunch P) {
+  using Lay = RowLayout<VT>;
   constexpr int V = (int)sizeof(VT);
+  constexpr int YR = MAX_TILE_ROWS / 32;
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  unsigned char* wb = smem + warp * Lay::WARP_B;
-  int4* sdesc = reinterpret_cast<int4*>(wb + Lay::DESC_OFF);
-  double* rsum = reinterpret_cast<double*>(wb + Lay::SCR_OFF);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Lay::BAR_OFF) + warp * NS;
+  unsigned char* st = smem + warp * Lay::WARP_B;
+  int4* sdesc = reinterpret_cast<int4*>(st + Lay::DESC_OFF);
+  double* rsum = reinterpret_cast<double*>(st + Lay::SCR_OFF);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Lay::BAR_OFF) + warp;
   const int gw = blockIdx.x * WARPS + warp, nw = gridDim.x * WARPS;
 
   const VT* __restrict__ x = static_cast<const VT*>(P.x);
   VT* __restrict__ y = static_cast<VT*>(P.y);
   const double alpha = P.alpha, beta = P.beta;
   const uint32_t xmax = P.xmax;
+  const uint64_t xpol = policy_evict_last();
 
   uint64_t pol = 0;
   int4 dn = make_int4(0, 0, 0, -1);
   if (lane == 0) {
-    for (int s = 0; s < NS; s++) mbar_init(&bars[s], 1);
+    mbar_init(bar, 1);
     fence_mbar_init();
     pol = policy_evict_first();
-    for (int s = 0; s < NS; s++) {
-      const int t = gw + s * nw;
-      if (t < P.ntiles) {
-        const int4 d = P.tiles[t];
-        sdesc[s] = d;
-        issue_blob(P.blob, d, tile_kind(d, COO), V, wb + s * St::BYTES, &bars[s], pol);
-      }
+    if (gw < P.ntiles) {
+      const int4 d = P.tiles[gw];
+      *sdesc = d;
+      issue_blob(P.blob, d, tile_kind(d), V, st, bar, pol);
     }
-    if (gw + NS * nw < P.ntiles) dn = P.tiles[gw + NS * nw];
+    if (gw + nw < P.ntiles) dn = P.tiles[gw + nw];
   }
   __syncwarp();
 
   for (int i = 0;; i++) {
     const int t = gw + i * nw;
     if (t >= P.ntiles) break;
-    const int s = i % NS;
-    mbar_wait(&bars[s], (uint32_t)((i / NS) & 1));
-    const int4 d = sdesc[s];
-    unsigned char* st = wb + s * St::BYTES;
+    mbar_wait(bar, (uint32_t)(i & 1));
+    const int4 d = *sdesc;
     const int nrows = d.z & 0xffff, nnz = d.z >> 16;
-    const int kind = tile_kind(d, COO);
-    const int ab = blob_aux_bytes(kind, nrows, nnz);
-    const int vb = align16(nnz * V);
-    const VT* sv = reinterpret_cast<const VT*>(st + ab);
-    const uint32_t* sc = reinterpret_cast<const uint32_t*>(st + ab + vb);
-    const int U = (nnz + 31) >> 5;   // warp-uniform number of 32-wide element rows
-
-    // ---- products: lane-strided over the tile's nonzeros, up to PER_LANE gathers in flight
-    uint32_t c[PER_LANE];
-    VT vv[PER_LANE], xv[PER_LANE];
-    if (U == PER_LANE) {   // full tile (the common case): no predicates at all
+    const bool slab = d.w >= 0;
+    // ---- stage -> registers (conflict-free 32-lane vectors), then refill the slot
+    const int q = slab ? 0 : nnz >> 5, r = nnz & 31;
+    const bool extra = !slab && lane < r;
+    uint32_t c[QMAX + 1];
+    VT v[QMAX + 1];
+    uint32_t kp[(QMAX + 4) / 4];   // SEG keys, 4 per register
 #pragma unroll
-      for (int u = 0; u < PER_LANE; u++) {
-        c[u] = min(sc[lane + 32 * u], xmax);
-        vv[u] = sv[lane + 32 * u];
-      }
+    for (int u = 0; u < (QMAX + 4) / 4; u++) kp[u] = 0u;
+    if (slab) {
+      const VT* sv = reinterpret_cast<const VT*>(st);
+      const uint32_t* sc = reinterpret_cast<const uint32_t*>(st + align16(nnz * V));
 #pragma unroll
-      for (int u = 0; u < PER_LANE; u++) xv[u] = ldg_ro(x + c[u]);
-    } else {
-#pragma unroll
-      for (int u = 0; u < PER_LANE; u++) {
-        const bool on = u < U;
+      for (int u = 0; u < QMAX; u++) {
+        const bool on = lane + 32 * u < nnz;
         c[u] = on ? min(sc[lane + 32 * u], xmax) : 0u;
-        vv[u] = on ? sv[lane + 32 * u] : VT(0);
+        v[u] = on ? sv[lane + 32 * u] : VT(0);
       }
-#pragma unroll
-      for (int u = 0; u < PER_LANE; u++) xv[u] = u < U ? ldg_ro(x + c[u]) : VT(0);
-    }
-
-    if (kind == KIND_SLAB) {
-      // ---- slab: partial sum of one split row -> record (fixed order, bit-reproducible)
-      double acc = 0.0;
-#pragma unroll
-      for (int u = 0; u < PER_LANE; u++)
-        if (u < U && lane + 32 * u < nnz) acc += (double)vv[u] * (double)xv[u];
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(FULL, acc, off);
-      if (lane == 0) P.rec[d.w] = acc;
+      c[QMAX] = 0u;
+      v[QMAX] = VT(0);
     } else {
-      const int64_t yrow0 = P.ybase + d.x;
-      double yin[MAX_TILE_ROWS / 32];
+      const uint8_t* sk = st;
+      const VT* sv = reinterpret_cast<const VT*>(st + align16(nnz));
+      const uint32_t* sc = reinterpret_cast<const uint32_t*>(st + align16(nnz) + align16(nnz * V));
 #pragma unroll
-      for (int u = 0; u < MAX_TILE_ROWS / 32; u++) {
-        const int r = lane + 32 * u;
-        yin[u] = (beta != 0.0 && r < nrows) ? (double)y[yrow0 + r] : 0.0;
-      }
-      double* prod = reinterpret_cast<double*>(st + ab);
-      __syncwarp();   // every lane holds its inputs: val/idx bytes may now be overwritten
-      if (U == PER_LANE) {
-#pragma unroll
-        for (int u = 0; u < PER_LANE; u++) prod[lane + 32 * u] = (double)vv[u] * (double)xv[u];
-      } else {
-#pragma unroll
-        for (int u = 0; u < PER_LANE; u++)
-          if (u < U) prod[lane + 32 * u] = (double)vv[u] * (double)xv[u];
-      }
-      if (COO)
-        for (int r = lane; r < nrows; r += 32) rsum[r] = 0.0;
-      __syncwarp();
-
-      if (!COO) {
-        const uint16_t* sa = reinterpret_cast<const uint16_t*>(st);   // tile-local row ends
-        {
-          // merge path over (row ends, nonzero indices), tile-local (Merrill & Garland)
-          const int items = nrows + nnz;
-          const int per = (items + 31) >> 5;
-          const int d0 = min(lane * per, items), d1 = min(d0 + per, items);
-          int lo = max(0, d0 - nnz), hi = min(d0, nrows);
-          while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if ((int)sa[mid + 1] <= d0 - mid - 1) lo = mid + 1; else hi = mid;
-          }
-          int xr = lo, yz = d0 - lo;
-          const int first = xr;
-          double acc = 0.0;
-          for (int dd = d0; dd < d1; dd++) {
-            if (xr < nrows && yz < (int)sa[xr + 1]) { acc += prod[yz]; yz++; }
-            else { rsum[xr] = acc; acc = 0.0; xr++; }
-          }
-          int pk;
-          double pv;
-          warp_seg_scan(xr, acc, pk, pv);
-          if (xr > first && pk == first) rsum[first] += pv;
-        }
-      } else {
-        // key-segmented walk over row_idx - row0 (pCOO row index rebased in-kernel)
-        const int* sr = reinterpret_cast<const int*>(st);
-        const int rg0 = (int)yrow0;
-        const int per = (nnz + 31) >> 5;
-        const int k0 = min(lane * per, nnz), k1 = min(k0 + per, nnz);
-        int cur = nrows + 1, first = 0, nseg = 0;
-        double acc = 0.0, firstv = 0.0;
-        if (k0 < k1) {
-          cur = sr[k0] - rg0;
-          nseg = 1;
-          for (int k = k0; k < k1; k++) {
-            const int kk = sr[k] - rg0;
-            if (kk != cur) {
-              if (nseg == 1) { first = cur; firstv = acc; } else rsum[cur] = acc;
-              nseg++;
-              cur = kk;
-              acc = 0.0;
-            }
-            acc += prod[k];
-          }
-        }
-        int pk;
-        double pv;
-        warp_seg_scan(cur, acc, pk, pv);
-        if (nseg >= 2) rsum[first] = (pk == first) ? firstv + pv : firstv;
-        if (nseg >= 1) {
-          const bool last_of_row = (k1 >= nnz) || (sr[k1] - rg0 != cur);
-          if (last_of_row) rsum[cur] = (pk == cur) ? pv + acc : acc;
-        }
-      }
-      __syncwarp();
-      // coalesced epilogue: alpha and beta applied exactly once per row
-#pragma unroll
-      for (int u = 0; u < MAX_TILE_ROWS / 32; u++) {
-        const int r = lane + 32 * u;
-        if (r < nrows) {
-          double v = alpha * rsum[r];
-          if (beta != 0.0) v += beta * yin[u];
-          y[yrow0 + r] = (VT)v;
-        }
+      for (int j = 0; j <= QMAX; j++) {
+        const bool on = j < QMAX ? j < q : extra;
+        const int sl = (j < QMAX ? j : q) * 32 + lane;
+        c[j] = on ? min(sc[sl], xmax) : 0u;
+        v[j] = on ? sv[sl] : VT(0);
+        if (on) kp[j >> 2] |= (uint32_t)sk[sl] << (8 * (j & 3));
       }
     }
-    __syncwarp();   // stage s and the scratch are free
+    fence_proxy_async();   // order this lane's generic-proxy reads of the slot before the TMA refill
+    __syncwarp();          // every lane holds its tile: the slot may be refilled
     if (lane == 0) {
-      const int tn = t + NS * nw;
+      const int tn = t + nw;
       if (tn < P.ntiles) {
-        sdesc[s] = dn;
-        issue_blob(P.blob, dn, tile_kind(dn, COO), V, st, &bars[s], pol);
+        *sdesc = dn;
+        issue_blob(P.blob, dn, tile_kind(dn), V, st, bar, pol);
         if (tn + nw < P.ntiles) dn = P.tiles[tn + nw];
       }
     }
+    // ---- x gathers: all in flight before the first use
+    VT xv[QMAX + 1];
+    if (slab) {
+#pragma unroll
+      for (int u = 0; u < QMAX; u++) xv[u] = lane + 32 * u < nnz ? ldx(x + c[u], xpol) : VT(0);
+      double acc = 0.0;
+#pragma unroll
+      for (int u = 0; u < QMAX; u++) acc = fma((double)v[u], (double)xv[u], acc);   // padding: 0 * 0
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(FULL, acc, off);
+      if (lane == 0) P.rec[d.w] = acc;
+      continue;
+    }
+    const int64_t yrow0 = P.ybase + d.x;
+    double yin[YR];
+#pragma unroll
+    for (int u = 0; u < YR; u++) {
+      const int rr = lane + 32 * u;
+      yin[u] = (beta != 0.0 && rr < nrows) ? (double)__ldcs(y + yrow0 + rr) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j <= QMAX; j++) {
+      const bool on = j < QMAX ? j < q : extra;
+      xv[j] = on ? ldx(x + c[j], xpol) : VT(0);
+    }
+    for (int rr = lane; rr < nrows; rr += 32) rsum[rr] = 0.0;
+    __syncwarp();
+    // ---- walk the lane's chunk: complete rows inside it go straight to rsum
+    const int len = q + (extra ? 1 : 0);
+    const int key0 = (int)(q > 0 ? (kp[0] & 0xffu) : (kp[QMAX >> 2] >> (8 * (QMAX & 3))) & 0xffu);
+    int cur = len > 0 ? key0 : INT_MAX;
+    int first = cur, nseg = len > 0 ? 1 : 0;
+    double acc = 0.0, firstv = 0.0;
+#pragma unroll
+    for (int j = 0; j <= QMAX; j++) {
+      const bool on = j < QMAX ? j < q : extra;
+      if (on) {
+        const int k = (int)((kp[j >> 2] >> (8 * (j & 3))) & 0xffu);
+        if (k != cur) {
+          if (nseg == 1) firstv = acc; else rsum[cur] = acc;
+          nseg++;
+          cur = k;
+          acc = 0.0;
+        }
+        acc = fma((double)v[j], (double)xv[j], acc);
+      }
+    }
+    // ---- join rows that cross lanes: inclusive run of preceding lanes ending in the same row
+    int pk;
+    double pv;
+    warp_seg_scan(cur, acc, pk, pv);
+    const int next_first = __shfl_down_sync(FULL, key0, 1);
+    const bool next_has = lane < 31 && (q > 0 || lane + 1 < r);
+    if (nseg >= 2) rsum[first] = (pk == first) ? firstv + pv : firstv;
+    if (nseg >= 1 && !(next_has && next_first == cur)) rsum[cur] = (pk == cur) ? pv + acc : acc;
+    __syncwarp();
+    // ---- coalesced epilogue: alpha and beta applied exactly once per row
+#pragma unroll
+    for (int u = 0; u < YR; u++) {
+      const int rr = lane + 32 * u;
+      if (rr < nrows) {
+        double o = alpha * rsum[rr];
+        if (beta != 0.0) o += beta * yin[u];
+        __stcs(y + yrow0 + rr, (VT)o);
+      }
+    }
+    __syncwarp();   // rsum is free
   }
 }
 
@@ -443,9 +439,6 @@ struct CBLayout {
   static constexpr int TOTAL = BAR_OFF + 2 * CB_NS * 8;
 };
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(bar)) : "memory");
-}
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -537,6 +530,7 @@ __global__ void __launch_bounds__(CB_THREADS, 1) csc_band_kernel(const ColLaunch
 #pragma unroll
     for (int k = 0; k < PER; k++)
       if (ct + k * CB_NC < d.y) atomicAdd(&acc[pk[k] & (CB_ROWS - 1)], (double)v[k] * (double)xv[k]);
+    fence_proxy_async();   // the stage's reads are ordered before the producer's next TMA into it
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     if (d.w) {   // band complete: write it out once, re-zero the accumulator
@@ -592,30 +586,38 @@ __global__ void pack_kernel(const PackLaunch L) {
     }
     return;
   }
-  const int kind = d.w >= 0 ? KIND_SLAB : (L.coo ? KIND_COO : KIND_PTR);
-  const int ab = blob_aux_bytes(kind, nrows, nnz);
-  const int vb = align16(nnz * L.vsize);
-  const int z0 = d.y, z1 = d.y + nnz;
-  if (kind == KIND_PTR) {
-    uint16_t* a = reinterpret_cast<uint16_t*>(b);
-    for (int j = lane; j <= nrows; j += 32) {
-      int v = L.ptr[d.x + j];
-      v = v < z0 ? z0 : (v > z1 ? z1 : v);
-      a[j] = (uint16_t)(v - z0);
+  const int z0 = d.y;
+  if (d.w >= 0) {   // slab: natural order [val][col]
+    const int vb = align16(nnz * L.vsize);
+    int* ix = reinterpret_cast<int*>(b + vb);
+    for (int k = lane; k < nnz; k += 32) {
+      if (L.vsize == 8) reinterpret_cast<double*>(b)[k] = static_cast<const double*>(L.val)[z0 + k];
+      else reinterpret_cast<float*>(b)[k] = static_cast<const float*>(L.val)[z0 + k];
+      ix[k] = L.idx[z0 + k];
     }
-  } else if (kind == KIND_COO) {
-    int* a = reinterpret_cast<int*>(b);
-    for (int k = lane; k < nnz; k += 32) a[k] = L.ptr[z0 + k];
+    return;
   }
-  if (L.vsize == 8) {
-    double* v = reinterpret_cast<double*>(b + ab);
-    for (int k = lane; k < nnz; k += 32) v[k] = static_cast<const double*>(L.val)[z0 + k];
+  // SEG tile: [key u8][val][col] in lane-chunked slot order (internal.h)
+  uint8_t* key = reinterpret_cast<uint8_t*>(b);
+  char* vb0 = b + align16(nnz);
+  int* ix = reinterpret_cast<int*>(vb0 + align16(nnz * L.vsize));
+  if (L.coo) {
+    const int64_t r0 = L.row_base + d.x;
+    for (int e = lane; e < nnz; e += 32) key[seg_slot(e, nnz)] = (uint8_t)(L.ptr[z0 + e] - r0);
   } else {
-    float* v = reinterpret_cast<float*>(b + ab);
-    for (int k = lane; k < nnz; k += 32) v[k] = static_cast<const float*>(L.val)[z0 + k];
+    for (int j = 0; j < nrows; j++) {
+      int e0 = L.ptr[d.x + j], e1 = L.ptr[d.x + j + 1];
+      e0 = min(max(e0, z0), z0 + nnz) - z0;
+      e1 = min(max(e1, z0), z0 + nnz) - z0;
+      for (int e = e0 + lane; e < e1; e += 32) key[seg_slot(e, nnz)] = (uint8_t)j;
+    }
   }
-  int* ix = reinterpret_cast<int*>(b + ab + vb);
-  for (int k = lane; k < nnz; k += 32) ix[k] = L.idx[z0 + k];
+  for (int e = lane; e < nnz; e += 32) {
+    const int sl = seg_slot(e, nnz);
+    if (L.vsize == 8) reinterpret_cast<double*>(vb0)[sl] = static_cast<const double*>(L.val)[z0 + e];
+    else reinterpret_cast<float*>(vb0)[sl] = static_cast<const float*>(L.val)[z0 + e];
+    ix[sl] = L.idx[z0 + e];
+  }
 }
 
 // --------------------------------------------------------- small kernels
@@ -707,12 +709,12 @@ int grid_for(K kernel, int smem_bytes, int ntiles) {
   return (int)(want < g ? (want < 1 ? 1 : want) : g);
 }
 
-template <typename VT, bool COO>
+template <typename VT>
 cudaError_t launch_rows_t(const RowLaunch& L, cudaStream_t s) {
-  constexpr int b = RowLayout<VT, COO>::TOTAL;
-  cudaError_t e = set_smem(rows_kernel<VT, COO>, b);
+  constexpr int b = RowLayout<VT>::TOTAL;
+  cudaError_t e = set_smem(rows_kernel<VT>, b);
   if (e) return e;
-  rows_kernel<VT, COO><<<grid_for(rows_kernel<VT, COO>, b, L.ntiles), WARPS * 32, b, s>>>(L);
+  rows_kernel<VT><<<grid_for(rows_kernel<VT>, b, L.ntiles), WARPS * 32, b, s>>>(L);
   return cudaGetLastError();
 }
 
@@ -739,8 +741,7 @@ cudaError_t launch_cols_t(const ColLaunch& L, cudaStream_t s) {
 
 cudaError_t launch_rows(const RowLaunch& L, cudaStream_t s) {
   if (L.ntiles == 0) return cudaSuccess;
-  if (L.dtype == 0) return L.coo ? launch_rows_t<double, true>(L, s) : launch_rows_t<double, false>(L, s);
-  return L.coo ? launch_rows_t<float, true>(L, s) : launch_rows_t<float, false>(L, s);
+  return L.dtype == 0 ? launch_rows_t<double>(L, s) : launch_rows_t<float>(L, s);
 }
 
 cudaError_t launch_sell(const SellLaunch& L, cudaStream_t s) {
