@@ -8,6 +8,7 @@
 // exchanges only split-row partials and, for REPLICATED y, its
 // owned y segment.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdarg>
 #include <cstdio>
@@ -150,9 +151,10 @@ struct Ctx {
   int64_t py_len = 0;
   // pCSC row-band layout
   int4* d_citems = nullptr;
+  int64_t* d_item_off = nullptr;
   int32_t* d_band_item = nullptr;
-  char* d_cval = nullptr;
-  uint32_t* d_cpk = nullptr;
+  int32_t* d_split = nullptr;
+  char* d_cblob = nullptr;
   int64_t cnb = 0, citems = 0;
   int nheads_local = 0;
 
@@ -377,17 +379,60 @@ void build_row_schedule(const Ctx& c, const std::vector<int64_t>& lp, Schedule& 
   }
 }
 
-// pCSC device layout (internal.h "row-band layout"): a stable parallel counting
-// sort of the rank's nonzeros by (row band, column chunk), done on the host
-// threads at partition time.  CSC order is kept inside every (band, chunk)
-// item, each item is padded to a multiple of 4 entries (16-B aligned TMA).
+// pCSC device layout (internal.h "pCSC row-band layout"), built on the host
+// threads at partition time: per-row counts -> balanced warp row ranges per
+// band -> a stable parallel counting sort by (band, column chunk, warp) -> per
+// warp list, the greedy arrangement that gives every aligned group of 32
+// entries distinct rows (run twice: once to size the lists, once to write
+// them into the stage blobs).
 struct CscBands {
-  int64_t nb = 0, nch = 1, total = 0;     // bands, column chunks, padded entries
-  std::vector<int4> items;                // {begin lo, begin hi, count, window col base}
+  int64_t nb = 0, nch = 1, bytes = 0;     // bands, column chunks, blob bytes
+  std::vector<int4> items;                // {band, nstages, window col base, last-stage seg}
+  std::vector<int64_t> item_off;          // byte offset of each item's blob
   std::vector<int32_t> band_item;         // [nb + 1]
-  std::unique_ptr<char[]> val;            // total * V
-  std::unique_ptr<uint32_t[]> pk;         // total
+  std::vector<int32_t> split;             // [nb * (CB_W + 1)]
+  std::unique_ptr<char[]> blob;
 };
+
+// Greedy group arrangement of one warp list (entries [0, n) of pk/val, CSC
+// order): emits groups of 32 with distinct rows (pk & (CB_ROWS-1)); an entry
+// whose row is already in the open group waits in `pend` for a later group.
+// A group that cannot be filled while entries remain is closed with holes.
+// emit(pos, e) receives every output position with its entry (e < 0: hole).
+// Returns the arranged length.
+template <class Emit>
+int64_t arrange_list(const uint32_t* pk, int64_t n, std::vector<int64_t>& pend, std::vector<uint64_t>& used,
+                     Emit&& emit) {
+  pend.clear();
+  used.assign(CB_ROWS / 64, 0);
+  int64_t next = 0, w = 0;
+  uint32_t grp[32];
+  while (next < n || !pend.empty()) {
+    int g = 0;
+    auto busy = [&](int64_t e) { const uint32_t r = pk[e] & (CB_ROWS - 1); return (used[r >> 6] >> (r & 63)) & 1; };
+    auto take = [&](int64_t e) {
+      const uint32_t r = pk[e] & (CB_ROWS - 1);
+      used[r >> 6] |= 1ull << (r & 63);
+      grp[g++] = r;
+      emit(w++, e);
+    };
+    size_t keep = 0;
+    for (size_t k = 0; k < pend.size(); k++) {   // deferred entries first, order kept
+      const int64_t e = pend[k];
+      if (g < 32 && !busy(e)) take(e); else pend[keep++] = e;
+    }
+    pend.resize(keep);
+    while (g < 32 && next < n) {
+      const int64_t e = next++;
+      if (busy(e)) pend.push_back(e); else take(e);
+    }
+    const int real = g;
+    if (g < 32 && (next < n || !pend.empty()))   // close the group with holes
+      for (; g < 32; g++) emit(w++, -1);
+    for (int k = 0; k < real; k++) used[grp[k] >> 6] &= ~(1ull << (grp[k] & 63));
+  }
+  return w;
+}
 
 msrep_status_t build_csc_bands(const Ctx& c, const std::vector<int64_t>& lp, const int32_t* idx, const void* val,
                                size_t V, CscBands& B) {
@@ -396,76 +441,150 @@ msrep_status_t build_csc_bands(const Ctx& c, const std::vector<int64_t>& lp, con
   const int32_t* rows = idx + c.B_lo;
   const char* vals = static_cast<const char*>(val) + (size_t)c.B_lo * V;
   B.nb = (c.m + CB_ROWS - 1) / CB_ROWS;
-  B.nch = std::max<int64_t>(1, (W + ((int64_t)1 << CB_COL_BITS) - 1) >> CB_COL_BITS);
-  const int64_t keys = B.nb * B.nch;
-  if (keys > ((int64_t)1 << 24))
-    return fail(MSREP_ERR_TOO_LARGE, "pCSC band layout: ceil(m/%d)*ceil(cols/2^%d) = %lld keys > 2^24", CB_ROWS,
-                CB_COL_BITS, (long long)keys);
+  B.nch = std::max<int64_t>(1, (W + CB_CHUNK - 1) / CB_CHUNK);
+  const int64_t keys = B.nb * B.nch * CB_W;
+  if (keys > ((int64_t)1 << 26))
+    return fail(MSREP_ERR_TOO_LARGE, "pCSC band layout: %lld (band, chunk, warp) lists > 2^26", (long long)keys);
   int T = (int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
-  while (T > 1 && (int64_t)T * keys > ((int64_t)1 << 25)) T--;
+  while (T > 1 && (int64_t)T * keys > ((int64_t)1 << 26)) T--;
   if (nz < (1 << 20)) T = 1;
-  // column ranges with ~equal nonzeros per thread
-  std::vector<int64_t> cb((size_t)T + 1, W);
-  cb[0] = 0;
-  for (int t = 1; t < T; t++)
-    cb[(size_t)t] = std::lower_bound(lp.begin(), lp.end(), nz * t / T) - lp.begin();
-  for (int t = 1; t <= T; t++) cb[(size_t)t] = std::max(cb[(size_t)t], cb[(size_t)t - 1]);
-  std::vector<std::vector<int64_t>> off((size_t)T, std::vector<int64_t>((size_t)keys, 0));
-  auto key_of = [&](int64_t q, int32_t r) { return ((int64_t)r >> CB_LOG2) * B.nch + (q >> CB_COL_BITS); };
   auto run = [&](auto&& f) {
     std::vector<std::thread> th;
     for (int t = 1; t < T; t++) th.emplace_back(f, t);
     f(0);
     for (auto& x : th) x.join();
   };
+  std::vector<int64_t> cb((size_t)T + 1, W);   // column ranges with ~equal nonzeros per thread
+  cb[0] = 0;
+  for (int t = 1; t < T; t++) cb[(size_t)t] = std::lower_bound(lp.begin(), lp.end(), nz * t / T) - lp.begin();
+  for (int t = 1; t <= T; t++) cb[(size_t)t] = std::max(cb[(size_t)t], cb[(size_t)t - 1]);
+  // 0. entries per row -> balanced warp row ranges per band
+  std::unique_ptr<int32_t[]> rc(new int32_t[(size_t)std::max<int64_t>(1, c.m)]());
+  run([&](int t) {
+    for (int64_t z = lp[(size_t)cb[(size_t)t]]; z < lp[(size_t)cb[(size_t)t + 1]]; z++)
+      __atomic_fetch_add(&rc[(size_t)rows[z]], 1, __ATOMIC_RELAXED);
+  });
+  constexpr int SW = CB_W + 1;
+  B.split.assign((size_t)(B.nb * SW), 0);
+  for (int64_t b = 0; b < B.nb; b++) {
+    const int64_t r0 = b * CB_ROWS, nr = std::min<int64_t>(CB_ROWS, c.m - r0);
+    int64_t tot = 0;
+    for (int64_t o = 0; o < nr; o++) tot += rc[(size_t)(r0 + o)];
+    int32_t* sp = &B.split[(size_t)(b * SW)];
+    int64_t cum = 0, o = 0;
+    for (int w = 1; w < CB_W; w++) {
+      const int64_t target = tot * w / CB_W;
+      while (o < nr && cum < target) cum += rc[(size_t)(r0 + o++)];
+      sp[w] = (int32_t)o;
+    }
+    sp[0] = 0;
+    sp[CB_W] = (int32_t)nr;
+  }
+  rc.reset();
+  auto warp_of = [&](int64_t b, int32_t ro) {
+    const int32_t* sp = &B.split[(size_t)(b * SW)];
+    const int w = (int)(std::upper_bound(sp, sp + SW, ro) - sp) - 1;
+    return w < CB_W - 1 ? w : CB_W - 1;
+  };
+  auto key_of = [&](int64_t q, int32_t r) {
+    const int64_t b = r / CB_ROWS;
+    return (b * B.nch + q / CB_CHUNK) * CB_W + warp_of(b, r % CB_ROWS);
+  };
+  // 1. stable counting sort by key into temporary (pk, val) arrays
+  std::vector<std::vector<int64_t>> off((size_t)T, std::vector<int64_t>((size_t)keys, 0));
   run([&](int t) {
     auto& o = off[(size_t)t];
     for (int64_t q = cb[(size_t)t]; q < cb[(size_t)t + 1]; q++)
       for (int64_t z = lp[(size_t)q]; z < lp[(size_t)q + 1]; z++) o[(size_t)key_of(q, rows[z])]++;
   });
-  std::vector<int64_t> kcount((size_t)keys), kbase((size_t)keys);
+  std::vector<int64_t> kbeg((size_t)keys + 1);
   int64_t run_off = 0;
   for (int64_t k = 0; k < keys; k++) {
-    int64_t tot = 0;
+    kbeg[(size_t)k] = run_off;
     for (int t = 0; t < T; t++) {
       const int64_t cnt = off[(size_t)t][(size_t)k];
-      off[(size_t)t][(size_t)k] = run_off + tot;
-      tot += cnt;
+      off[(size_t)t][(size_t)k] = run_off;
+      run_off += cnt;
     }
-    kcount[(size_t)k] = tot;
-    kbase[(size_t)k] = run_off;
-    run_off += (tot + 3) & ~(int64_t)3;
   }
-  B.total = run_off;
-  B.val.reset(new char[(size_t)std::max<int64_t>(1, B.total) * V]);
-  B.pk.reset(new uint32_t[(size_t)std::max<int64_t>(1, B.total)]);
+  kbeg[(size_t)keys] = run_off;
+  std::unique_ptr<uint32_t[]> tpk(new uint32_t[(size_t)std::max<int64_t>(1, nz)]);
+  std::unique_ptr<char[]> tval(new char[(size_t)std::max<int64_t>(1, nz) * V]);
   run([&](int t) {
     auto& o = off[(size_t)t];
     for (int64_t q = cb[(size_t)t]; q < cb[(size_t)t + 1]; q++)
       for (int64_t z = lp[(size_t)q]; z < lp[(size_t)q + 1]; z++) {
         const int32_t r = rows[z];
         const int64_t dst = o[(size_t)key_of(q, r)]++;
-        memcpy(B.val.get() + (size_t)dst * V, vals + (size_t)z * V, V);
-        B.pk[(size_t)dst] = (uint32_t)(r & (CB_ROWS - 1)) |
-                            ((uint32_t)(q & (((int64_t)1 << CB_COL_BITS) - 1)) << CB_LOG2);
+        tpk[(size_t)dst] = (uint32_t)(r % CB_ROWS) | ((uint32_t)(q % CB_CHUNK) << CB_LOG2);
+        memcpy(tval.get() + (size_t)dst * V, vals + (size_t)z * V, V);
       }
   });
+  off.clear();
+  off.shrink_to_fit();
+  std::atomic<int64_t> next_key{0};
+  auto each_key = [&](auto&& f) {
+    run([&](int) {
+      std::vector<int64_t> pend;
+      std::vector<uint64_t> used;
+      for (;;) {
+        const int64_t k0 = next_key.fetch_add(64);
+        if (k0 >= keys) break;
+        for (int64_t k = k0; k < std::min(keys, k0 + 64); k++) f(k, pend, used);
+      }
+    });
+    next_key = 0;
+  };
+  // 2. arranged length of every list (holes included)
+  std::vector<int64_t> alen((size_t)keys, 0);
+  each_key([&](int64_t k, std::vector<int64_t>& pend, std::vector<uint64_t>& used) {
+    const int64_t b0 = kbeg[(size_t)k], n = kbeg[(size_t)k + 1] - b0;
+    alen[(size_t)k] = n ? arrange_list(tpk.get() + b0, n, pend, used, [](int64_t, int64_t) {}) : 0;
+  });
+  // 3. items: one per non-empty (band, chunk); stage geometry and blob offsets
   B.band_item.assign((size_t)B.nb + 1, 0);
+  std::vector<int64_t> key_item((size_t)(B.nb * B.nch), -1);
+  int64_t bytes = 0;
   for (int64_t b = 0; b < B.nb; b++) {
     B.band_item[(size_t)b] = (int32_t)B.items.size();
     for (int64_t ch = 0; ch < B.nch; ch++) {
-      const int64_t k = b * B.nch + ch, cnt = kcount[(size_t)k], beg = kbase[(size_t)k];
-      if (cnt == 0) continue;
-      for (int64_t e = beg + cnt; e < ((beg + cnt + 3) & ~(int64_t)3); e++) {   // padding: never read
-        memset(B.val.get() + (size_t)e * V, 0, V);
-        B.pk[(size_t)e] = 0;
-      }
-      if (cnt >= ((int64_t)1 << 31)) return fail(MSREP_ERR_TOO_LARGE, "pCSC band item too large");
-      B.items.push_back(make_int4((int32_t)(uint32_t)(beg & 0xffffffffll), (int32_t)(beg >> 32), (int32_t)cnt,
-                                  (int32_t)(ch << CB_COL_BITS)));
+      const int64_t k0 = (b * B.nch + ch) * CB_W;
+      int64_t L = 0;
+      for (int w = 0; w < CB_W; w++) L = std::max(L, alen[(size_t)(k0 + w)]);
+      if (L == 0) continue;
+      const int64_t nst = (L + CB_SEG - 1) / CB_SEG;
+      const int64_t last = ((L - (nst - 1) * CB_SEG) + 3) & ~(int64_t)3;
+      if (nst >= ((int64_t)1 << 31)) return fail(MSREP_ERR_TOO_LARGE, "pCSC warp list too long");
+      key_item[(size_t)(b * B.nch + ch)] = (int64_t)B.items.size();
+      B.items.push_back(make_int4((int32_t)b, (int32_t)nst, (int32_t)(ch * CB_CHUNK), (int32_t)last));
+      B.item_off.push_back(bytes);
+      bytes += ((nst - 1) * CB_SEG + last) * CB_W * (int64_t)(V + 4);
     }
   }
   B.band_item[(size_t)B.nb] = (int32_t)B.items.size();
+  B.bytes = bytes;
+  B.blob.reset(new char[(size_t)std::max<int64_t>(16, bytes)]);
+  // 4. write every list into its item's stage blobs; pad it with holes to the item's length
+  each_key([&](int64_t k, std::vector<int64_t>& pend, std::vector<uint64_t>& used) {
+    const int64_t it = key_item[(size_t)(k / CB_W)];
+    if (it < 0) return;
+    const int w = (int)(k % CB_W);
+    const int4 item = B.items[(size_t)it];
+    const int64_t nst = item.y, last = item.w, L = (nst - 1) * CB_SEG + last;
+    char* base = B.blob.get() + B.item_off[(size_t)it];
+    const int64_t b0 = kbeg[(size_t)k], n = kbeg[(size_t)k + 1] - b0;
+    auto put = [&](int64_t pos, int64_t e) {
+      const int64_t s = pos / CB_SEG, j = pos % CB_SEG;
+      const int64_t seg = s == nst - 1 ? last : CB_SEG;
+      char* st = base + s * CB_SEG * CB_W * (int64_t)(V + 4);
+      const int64_t slot = (int64_t)w * seg + j;
+      uint32_t* pkp = reinterpret_cast<uint32_t*>(st + CB_W * seg * (int64_t)V) + slot;
+      if (e >= 0) { *pkp = tpk[(size_t)(b0 + e)]; memcpy(st + slot * (int64_t)V, tval.get() + (size_t)(b0 + e) * V, V); }
+      else { *pkp = CB_HOLE; memset(st + slot * (int64_t)V, 0, V); }
+    };
+    int64_t pos = n ? arrange_list(tpk.get() + b0, n, pend, used, put) : 0;
+    for (; pos < L; pos++) put(pos, -1);
+  });
   return MSREP_OK;
 }
 
@@ -692,13 +811,14 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     CscBands CB;
     TRY(build_csc_bands(*c, lp, idx, val, V, CB));
     TRY(upload_vec(c, CB.items, &c->d_citems, s));
+    TRY(upload_vec(c, CB.item_off, &c->d_item_off, s));
     TRY(upload_vec(c, CB.band_item, &c->d_band_item, s));
-    TRY(upload(c, CB.val.get(), (size_t)CB.total * V, &c->d_cval, s));
-    TRY(upload(c, CB.pk.get(), (size_t)CB.total, &c->d_cpk, s));
+    TRY(upload_vec(c, CB.split, &c->d_split, s));
+    TRY(upload(c, CB.blob.get(), (size_t)CB.bytes, &c->d_cblob, s));
     c->cnb = CB.nb;
     c->citems = (int64_t)CB.items.size();
     c->ntiles = 0; c->nsell = 0; c->nslabs = 0; c->nrec = 0; c->nsplit = 0;
-    c->blob_bytes = CB.total * (int64_t)(V + 4) + c->citems * 16 + (CB.nb + 1) * 4;
+    c->blob_bytes = CB.bytes + c->citems * 24 + (CB.nb + 1) * 4 + CB.nb * (CB_W + 1) * 4;
     c->py_len = c->nranks > 1 ? c->shard * c->nranks : 0;
     if (c->py_len) {
       void* pp;
@@ -862,8 +982,8 @@ msrep_status_t msrep_spmv(msrep_ctx h, const void* alpha_p, const void* x, const
 
   if (c->fmt == MSREP_CSC) {
     ColLaunch L{};
-    L.items = c->d_citems; L.band_item = c->d_band_item; L.nb = (int)c->cnb;
-    L.val = c->d_cval; L.pk = c->d_cpk;
+    L.items = c->d_citems; L.item_off = c->d_item_off; L.band_item = c->d_band_item; L.split = c->d_split;
+    L.nb = (int)c->cnb; L.blob = c->d_cblob;
     L.x = x; L.xbase = c->wlo;
     L.fused = c->nranks == 1;
     L.out = L.fused ? y : static_cast<void*>(c->d_py);

@@ -88,22 +88,37 @@ struct SellLaunch {
   int dtype;
 };
 
-// pCSC row-band layout: the rank's nonzeros regrouped into
-// bands of CB_ROWS consecutive rows; inside a band they stay in CSC order
-// (column-major, stable) and are cut into items by column chunk (window column
-// >> CB_COL_BITS).  Per entry: the value, and a packed word
-// (row & (CB_ROWS-1)) | ((window col & (2^CB_COL_BITS-1)) << CB_LOG2).  Every
-// item starts 16-byte aligned (entry counts padded to a multiple of 4, padding
-// never read) so a 1-D TMA bulk copy moves it.  One CTA owns a band: its fp64
-// partial y lives in shared memory, so the scatter needs no global atomics.
+// pCSC row-band layout.  The rank's nonzeros are regrouped
+// into bands of CB_ROWS consecutive rows, one CTA per band at a time, the
+// band's fp64 partial y in shared memory.  Each of the CB_W consumer warps OWNS
+// a contiguous row range of the band (ranges balanced by entry count at
+// partition time), so the scatter needs no atomics.  Per (band, column chunk)
+// "item", each warp's entries form a "warp list" in CSC order (column-major),
+// except that every aligned group of 32 entries is arranged to hold 32
+// distinct rows (an entry that would repeat a row of its group is deferred to
+// a later group); the lists of an item are padded with holes to one common
+// length and cut into stages of CB_SEG entries per warp (the last stage
+// shorter, a multiple of 4).  A stage is one contiguous blob
+//   [val: CB_W x seg][packed: CB_W x seg]
+// moved by one 1-D TMA.  packed = (row & (CB_ROWS-1)) | ((window col - chunk
+// base) << CB_LOG2); 0xffffffff marks a hole (never a valid entry: a chunk
+// spans CB_CHUNK = 2^19 - 1 columns).
 constexpr int CB_LOG2 = 13;
-constexpr int CB_ROWS = 1 << CB_LOG2;      // 8192 rows: 64 KB fp64 accumulator
-constexpr int CB_COL_BITS = 32 - CB_LOG2;  // 19: columns per chunk = 524288
+constexpr int CB_ROWS = 1 << CB_LOG2;      // 8192 rows per band: 64 KB fp64 accumulator
+constexpr int CB_W = 15;                   // consumer warps (+1 producer: 16 warps, 128 registers)
+constexpr int64_t CB_CHUNK = (1ll << (32 - CB_LOG2)) - 1;
+constexpr uint32_t CB_HOLE = 0xffffffffu;
+#ifndef MSREP_CB_SEG
+#define MSREP_CB_SEG 128
+#endif
+constexpr int CB_SEG = MSREP_CB_SEG;       // entries per warp per pipeline stage
 struct ColLaunch {
-  const int4* items;          // {begin lo, begin hi (entries), count, window col base}
+  const int4* items;          // per item: {band, nstages, window col base, last-stage entries per warp}
+  const int64_t* item_off;    // byte offset of each item's first stage blob
   const int32_t* band_item;   // [nb + 1]: items of band b are [band_item[b], band_item[b+1])
+  const int32_t* split;       // [nb * (CB_W + 1)]: warp w owns band rows [split[b*(CB_W+1)+w], ...[w+1])
   int nb;
-  const char* val; const uint32_t* pk;
+  const char* blob;
   const void* x; int64_t xbase;                              // x index of window column 0
   void* out; int64_t m;                                      // fused: y (dtype); else fp64 py
   double alpha, beta;

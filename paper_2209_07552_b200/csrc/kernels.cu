@@ -419,20 +419,26 @@ __global__ void __launch_bounds__(WARPS * 32) sell_kernel(const SellLaunch P) {
 // ------------------------------------------------------------------ pCSC
 // pCSC per-GPU kernel (Alg. 5 "Launch": each part scatters its
 // columns' contributions into a partial y, "switch the role of x and y",
-// P:199).  The scatter target is a shared-memory fp64 accumulator of one row
-// band (CB_ROWS rows) owned by the CTA, so no global atomics and no global
-// zero-fill are needed; the band's entries (CSC order inside the band) stream
-// through a CB_NS-stage TMA ring filled by one producer warp.  At the end of a
-// band the consumers write it out once: fused y = alpha*acc + beta*y when one
-// rank holds the whole partial sum, else acc -> fp64 py for the reduce-scatter.
-constexpr int CB_E = 4096;                 // entries per stage
-constexpr int CB_NS = 3;                   // stages
-constexpr int CB_CW = 16;                  // consumer warps
-constexpr int CB_NC = CB_CW * 32;
+// P:199).  One CTA per row band (CB_ROWS rows) at a time; the band's fp64
+// partial y lives in shared memory and consumer warp w OWNS a contiguous row
+// range of it, so the scatter is a plain read-modify-write (no atomics,
+// bit-reproducible): every 32-entry step of a warp list holds 32 distinct rows
+// (arranged at partition time, internal.h).  A producer lane streams the
+// stage blobs with one 1-D TMA each into a CB_NS-stage ring.  Each consumer
+// warp is software-pipelined: the next stage's x gathers are in flight while
+// it scatters the current one.  At the end of a band every warp writes its own
+// rows once: fused y = alpha*acc + beta*y when one rank holds the whole partial
+// sum, else acc -> fp64 py for the reduce-scatter.
+#ifndef MSREP_CB_NS
+#define MSREP_CB_NS 4
+#endif
+constexpr int CB_NS = MSREP_CB_NS;         // stages
+constexpr int CB_NC = CB_W * 32;
 constexpr int CB_THREADS = CB_NC + 32;     // + one producer warp
+constexpr int CB_PER = CB_SEG / 32;        // entries per lane per stage
 template <typename VT>
 struct CBLayout {
-  static constexpr int STAGE = CB_E * ((int)sizeof(VT) + 4);
+  static constexpr int STAGE = CB_W * CB_SEG * ((int)sizeof(VT) + 4);
   static constexpr int ST_OFF = CB_ROWS * 8;
   static constexpr int DESC_OFF = ST_OFF + CB_NS * STAGE;
   static constexpr int BAR_OFF = DESC_OFF + CB_NS * 16;
@@ -441,6 +447,41 @@ struct CBLayout {
 
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// one consumer warp's share of a stage, in registers
+template <typename VT>
+struct CBStage {
+  int4 d;                 // {band (-1: end), seg, window col base, last of band}
+  uint32_t pk[CB_PER];
+  VT v[CB_PER], xv[CB_PER];
+};
+
+template <typename VT>
+__device__ __forceinline__ void cb_load(CBStage<VT>& S, int it, const unsigned char* smem, const int4* sdesc,
+                                        uint64_t* full, uint64_t* empty, const VT* x, uint64_t xpol, int warp,
+                                        int lane) {
+  using L = CBLayout<VT>;
+  constexpr int V = (int)sizeof(VT);
+  const int s = it % CB_NS;
+  mbar_wait(&full[s], (uint32_t)((it / CB_NS) & 1));
+  S.d = sdesc[s];
+  const int seg = S.d.y;
+  const unsigned char* st = smem + L::ST_OFF + s * L::STAGE;
+  const VT* sv = reinterpret_cast<const VT*>(st) + warp * seg;
+  const uint32_t* sp = reinterpret_cast<const uint32_t*>(st + CB_W * seg * V) + warp * seg;
+#pragma unroll
+  for (int k = 0; k < CB_PER; k++) {
+    const int i = k * 32 + lane;
+    S.pk[k] = i < seg ? sp[i] : CB_HOLE;
+    S.v[k] = i < seg ? sv[i] : VT(0);
+  }
+  fence_proxy_async();   // the stage's reads are ordered before the producer's next TMA into it
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&empty[s]);   // the stage is free: the data is in registers
+  const VT* xb = x + S.d.z;
+#pragma unroll
+  for (int k = 0; k < CB_PER; k++) S.xv[k] = S.pk[k] != CB_HOLE ? ldx(xb + (S.pk[k] >> CB_LOG2), xpol) : VT(0);
 }
 
 template <typename VT>
@@ -456,106 +497,99 @@ __global__ void __launch_bounds__(CB_THREADS, 1) csc_band_kernel(const ColLaunch
   if (threadIdx.x == 0) {
     for (int s = 0; s < CB_NS; s++) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CB_CW);
+      mbar_init(&empty[s], CB_W);
     }
     fence_mbar_init();
   }
   __syncthreads();
 
-  if (warp == CB_CW) {   // ---- producer: walks the CTA's bands, items and stage chunks
+  if (warp == CB_W) {   // ---- producer (one lane): bands -> items -> stage blobs
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
       int it = 0;
-      auto acquire = [&](int4 d) {
+      auto stage = [&](int4 d, const char* src, int bytes) {
         const int s = it % CB_NS;
         if (it >= CB_NS) mbar_wait(&empty[s], (uint32_t)(((it / CB_NS) - 1) & 1));
         sdesc[s] = d;
-        return s;
+        mbar_arrive_expect_tx(&full[s], (uint32_t)bytes);
+        if (bytes) tma_1d(smem + L::ST_OFF + s * L::STAGE, src, (uint32_t)bytes, &full[s], pol);
+        it++;
       };
       for (int b = blockIdx.x; b < P.nb; b += gridDim.x) {
         const int i0 = P.band_item[b], i1 = P.band_item[b + 1];
         if (i0 == i1) {   // empty band: still written out (zeros / beta*y)
-          const int s = acquire(make_int4(b, 0, 0, 1));
-          mbar_arrive_expect_tx(&full[s], 0);
-          it++;
+          stage(make_int4(b, 0, 0, 1), nullptr, 0);
           continue;
         }
         for (int i = i0; i < i1; i++) {
           const int4 item = P.items[i];
-          const int64_t beg = (int64_t)(uint32_t)item.x | ((int64_t)item.y << 32);
-          for (int e = 0; e < item.z; e += CB_E) {
-            const int n = min(CB_E, item.z - e);
-            const int last = (i == i1 - 1 && e + CB_E >= item.z) ? 1 : 0;
-            const int s = acquire(make_int4(b, n, item.w, last));
-            const int n4 = (n + 3) & ~3;
-            unsigned char* st = smem + L::ST_OFF + s * L::STAGE;
-            mbar_arrive_expect_tx(&full[s], (uint32_t)(n4 * (V + 4)));
-            tma_1d(st, P.val + (beg + e) * V, (uint32_t)(n4 * V), &full[s], pol);
-            tma_1d(st + CB_E * V, P.pk + beg + e, (uint32_t)(n4 * 4), &full[s], pol);
-            it++;
+          const char* src = P.blob + P.item_off[i];
+          for (int sg = 0; sg < item.y; sg++) {
+            const int seg = sg == item.y - 1 ? item.w : CB_SEG;
+            const int bytes = CB_W * seg * (V + 4);
+            stage(make_int4(b, seg, item.z, (i == i1 - 1 && sg == item.y - 1) ? 1 : 0), src, bytes);
+            src += bytes;
           }
         }
       }
-      const int s = acquire(make_int4(-1, 0, 0, 0));
-      mbar_arrive_expect_tx(&full[s], 0);
+      stage(make_int4(-1, 0, 0, 0), nullptr, 0);
     }
     return;
   }
 
-  // ---- consumers
-  const int ct = threadIdx.x;
+  // ---- consumer warps
   const VT* __restrict__ x = static_cast<const VT*>(P.x) + P.xbase;
-  for (int r = ct; r < CB_ROWS; r += CB_NC) acc[r] = 0.0;
+  const uint64_t xpol = policy_evict_last();
+  for (int r = threadIdx.x; r < CB_ROWS; r += CB_NC) acc[r] = 0.0;
   named_bar_sync(1, CB_NC);
-  constexpr int PER = CB_E / CB_NC;
-  for (int it = 0;; it++) {
-    const int s = it % CB_NS;
-    mbar_wait(&full[s], (uint32_t)((it / CB_NS) & 1));
-    const int4 d = sdesc[s];
-    if (d.x < 0) break;
-    const unsigned char* st = smem + L::ST_OFF + s * L::STAGE;
-    const VT* sv = reinterpret_cast<const VT*>(st);
-    const uint32_t* sp = reinterpret_cast<const uint32_t*>(st + CB_E * V);
-    const VT* xb = x + d.z;
-    uint32_t pk[PER];
-    VT v[PER], xv[PER];
+  CBStage<VT> A, B;
+  int it = 0;
+  cb_load(A, it++, smem, sdesc, full, empty, x, xpol, warp, lane);
+  while (A.d.x >= 0) {
+    cb_load(B, it++, smem, sdesc, full, empty, x, xpol, warp, lane);   // next stage's gathers fly during A's scatter
+    // the scatter: 32 distinct rows per step, steps in list order (deterministic)
 #pragma unroll
-    for (int k = 0; k < PER; k++) {
-      const int i = ct + k * CB_NC;
-      pk[k] = i < d.y ? sp[i] : 0u;
-      v[k] = i < d.y ? sv[i] : VT(0);
-    }
-#pragma unroll
-    for (int k = 0; k < PER; k++) xv[k] = (ct + k * CB_NC < d.y) ? ldg_ro(xb + (pk[k] >> CB_LOG2)) : VT(0);
-#pragma unroll
-    for (int k = 0; k < PER; k++)
-      if (ct + k * CB_NC < d.y) atomicAdd(&acc[pk[k] & (CB_ROWS - 1)], (double)v[k] * (double)xv[k]);
-    fence_proxy_async();   // the stage's reads are ordered before the producer's next TMA into it
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-    if (d.w) {   // band complete: write it out once, re-zero the accumulator
-      named_bar_sync(1, CB_NC);
-      const int64_t r0 = (int64_t)d.x * CB_ROWS;
-      const int64_t rem = P.m - r0;
-      const int nr = rem < CB_ROWS ? (int)rem : CB_ROWS;
+    for (int k = 0; k < CB_PER; k++)
+      if (A.pk[k] != CB_HOLE) {
+        double* a = acc + (A.pk[k] & (CB_ROWS - 1));
+        *a = fma((double)A.v[k], (double)A.xv[k], *a);
+      }
+    if (A.d.w) {   // band complete: this warp writes its rows once and re-zeroes them
+      __syncwarp();
+      const int b = A.d.x;
+      const int lo = P.split[b * (CB_W + 1) + warp], hi = P.split[b * (CB_W + 1) + warp + 1];
+      const int64_t r0 = (int64_t)b * CB_ROWS;
       if (P.fused) {
         VT* y = static_cast<VT*>(P.out) + r0;
         const double alpha = P.alpha, beta = P.beta;
-        for (int r = ct; r < nr; r += CB_NC) {
-          double o = alpha * acc[r];
-          if (beta != 0.0) o += beta * (double)y[r];
-          y[r] = (VT)o;
-          acc[r] = 0.0;
+        for (int rb = lo; rb < hi; rb += 128) {
+          double yv[4];
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            const int r = rb + lane + 32 * u;
+            yv[u] = (beta != 0.0 && r < hi) ? (double)__ldcs(y + r) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            const int r = rb + lane + 32 * u;
+            if (r < hi) {
+              double o = alpha * acc[r];
+              if (beta != 0.0) o += beta * yv[u];
+              __stcs(y + r, (VT)o);
+              acc[r] = 0.0;
+            }
+          }
         }
       } else {
         double* py = static_cast<double*>(P.out) + r0;
-        for (int r = ct; r < nr; r += CB_NC) {
-          py[r] = acc[r];
+        for (int r = lo + lane; r < hi; r += 32) {
+          __stcs(py + r, acc[r]);
           acc[r] = 0.0;
         }
       }
-      named_bar_sync(1, CB_NC);
+      named_bar_sync(1, CB_NC);   // every warp's rows are written and zero before the next band
     }
+    A = B;
   }
 }
 
@@ -727,9 +761,14 @@ cudaError_t launch_sell_t(const SellLaunch& L, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+#ifndef MSREP_CB_SMEM_MIN
+#define MSREP_CB_SMEM_MIN (116 * 1024)
+#endif
 template <typename VT>
 cudaError_t launch_cols_t(const ColLaunch& L, cudaStream_t s) {
-  constexpr int b = CBLayout<VT>::TOTAL;
+  // at least MSREP_CB_SMEM_MIN: exactly one CTA per SM (two would share an SM while another idles);
+  // no more than the layout needs: the rest of the 256 KB is L1, which holds the x-gather misses
+  constexpr int b = CBLayout<VT>::TOTAL > MSREP_CB_SMEM_MIN ? CBLayout<VT>::TOTAL : MSREP_CB_SMEM_MIN;
   cudaError_t e = set_smem(csc_band_kernel<VT>, b);
   if (e) return e;
   const int g = L.nb < num_sms() ? L.nb : num_sms();

@@ -39,8 +39,8 @@ def test_library_is_sm100a_and_uses_tma():
     out = subprocess.run(["cuobjdump", "-sass", M.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out
     assert "UBLKCP" in out          # cp.async.bulk (1-D TMA) staging in the SpMV kernels
-    assert "ATOMS.CAST.SPIN.64" in out   # pCSC scatter into the shared-memory band accumulator (fp64 CAS)
-    assert "REDG.E.ADD.F64" not in out   # ... and no global float atomics anywhere
+    assert "REDG.E.ADD.F64" not in out   # no float atomics anywhere: pCSC scatters into warp-owned
+    assert "ATOMS.CAST" not in out       # shared-memory sub-bands with plain read-modify-writes
 
 
 def _parts_equal(a, b):
