@@ -289,6 +289,15 @@ def main():
 
     # roofline of the dominant kernel (per rank 0's launch; algorithmic bytes / event-timed duration)
     hbm_peak, peak_kind = load_peaks()
+    kname = "csc_band_kernel" if a.format == "csc" else "rows_kernel"
+    traffic = None
+    try:   # DRAM bytes per launch of that kernel from a committed `ncu --set full` capture (profiles/)
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tr = json.load(f).get(workload_name(a, A))
+        if tr and tr.get("kernel") == kname:
+            traffic = tr["dram_bytes_per_launch"]
+    except Exception:
+        traffic = None
     alg_bytes = st["alg_bytes"]
     achieved = alg_bytes / (kern_avg_ms * 1e-3) / 1e9
     step_gbs = alg_bytes / (step_ms * 1e-3) / 1e9
@@ -311,9 +320,10 @@ def main():
             "hbm": {"alg_bytes_per_step_rank0": alg_bytes, "step_GBps_rank0": step_gbs,
                     "frac_of_8TBps": step_gbs / 8000.0},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved / hbm_peak, "traffic": None,
-                         "kernel": "rows_kernel" if a.format != "csc" else "cols_kernel",
-                         "kernel_avg_ms": kern_avg_ms, "peak_kind": peak_kind},
+                         "frac": achieved / hbm_peak, "traffic": traffic, "kernel": kname,
+                         "kernel_avg_ms": kern_avg_ms, "alg_bytes_per_launch": alg_bytes,
+                         "peak_kind": peak_kind + " (MEASURED_PEAKS.json hbm_gbs, a copy)" if peak_kind == "measured"
+                         else peak_kind},
             "cpu_baseline": cpu,
             "e2e": {"value": flops / (e2e_step_ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": e2e_step_ms,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "api": "msrep_spmv_host"},

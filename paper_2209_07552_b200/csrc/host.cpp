@@ -135,7 +135,6 @@ struct Ctx {
   char* d_blob = nullptr;           // tile blobs [aux][val][idx] (the rank's partition on the GPU)
   int64_t blob_bytes = 0;
   int4* d_tiles = nullptr;
-  int4* d_sell = nullptr;
   int ntiles = 0, nsell = 0, nslabs = 0;
   double* d_rec = nullptr;
   int nrec = 0;
@@ -832,7 +831,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     // ---- schedule
     Schedule S;
     build_row_schedule(*c, lp, S);
-    c->ntiles = (int)S.tiles.size();
+    c->ntiles = (int)(S.tiles.size() + S.sell.size());
     c->nsell = (int)S.sell.size();
     c->nslabs = S.nslabs;
     c->nrec = S.nrec;
@@ -857,8 +856,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
       CUDA_TRY(launch_rebase(d_g, d_aux, W + 1, B_lo, B_hi, s));
     }
     static_assert(sizeof(TileHost) == sizeof(int4), "tile");
-    const size_t ngen = S.tiles.size();
-    S.tiles.insert(S.tiles.end(), S.sell.begin(), S.sell.end());   // packed together, launched apart
+    S.tiles.insert(S.tiles.begin(), S.sell.begin(), S.sell.end());   // one list: SELL tiles first
     std::vector<int32_t> blob16(S.tiles.size());
     int64_t blob_total = 0;
     for (size_t t = 0; t < S.tiles.size(); t++) {
@@ -882,8 +880,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     for (size_t t = 0; t < fin.size(); t++) fin[t].nz0 = blob16[t];
     CUDA_TRY(cudaStreamSynchronize(s));
     release_range(c, mark, keep_from);   // plain slices are no longer needed: the blobs hold the partition
-    TRY(upload(c, reinterpret_cast<const int4*>(fin.data()), ngen, &c->d_tiles, s));
-    TRY(upload(c, reinterpret_cast<const int4*>(fin.data() + ngen), fin.size() - ngen, &c->d_sell, s));
+    TRY(upload(c, reinterpret_cast<const int4*>(fin.data()), fin.size(), &c->d_tiles, s));
     c->blob_bytes = blob_total;
     void* rp;
     TRY(dalloc(c, (size_t)std::max(1, S.nrec) * 8, &rp, s));
@@ -945,7 +942,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   st.alg_bytes = base + ybytes_b1;
   st.alg_bytes_beta0 = base + ybytes_b0;
   if (fmt == MSREP_CSC) st.kernels_per_spmv = (c->cnb ? 1 : 0) + (c->nranks > 1 ? 1 /*shard epilogue*/ : 0);
-  else st.kernels_per_spmv = (c->ntiles ? 1 : 0) + (c->nsell ? 1 : 0) + (c->nranks > 1 && c->any_flag ? 1 : 0) + (c->nsplit ? 1 : 0);
+  else st.kernels_per_spmv = (c->ntiles ? 1 : 0) + (c->nranks > 1 && c->any_flag ? 1 : 0) + (c->nsplit ? 1 : 0);
   int64_t db = 0;
   for (auto& b : c->bufs) db += (int64_t)b.bytes;
   st.device_bytes = db;
@@ -1007,11 +1004,10 @@ msrep_status_t msrep_spmv(msrep_ctx h, const void* alpha_p, const void* x, const
   L.x = x; L.y = y; L.ybase = c->wlo;
   L.xmax = c->n > 0 ? (uint32_t)(c->n - 1) : 0u;
   L.alpha = alpha; L.beta = beta; L.rec = c->d_rec;
-  L.dtype = dt;
-  SellLaunch SL{c->d_sell, c->nsell, c->d_blob, x, y, c->wlo, alpha, beta, dt};
+  L.dtype = dt; L.has_sell = c->nsell > 0;
+
   cudaEvent_t pe;
   TRY(prof_begin(c, s, &pe));
-  CUDA_TRY(launch_sell(SL, s));
   CUDA_TRY(launch_rows(L, s));
   if (pe) CUDA_TRY(cudaEventRecord(pe, s));
   if (c->nranks > 1 && c->any_flag) {

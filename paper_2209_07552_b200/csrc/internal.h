@@ -78,14 +78,7 @@ struct RowLaunch {
   uint32_t xmax;                                             // n - 1 (clamp for padding lanes)
   double alpha, beta; double* rec;
   int dtype;                                                 // dtype 0 = f64, 1 = f32
-};
-
-struct SellLaunch {
-  const int4* tiles; int ntiles;
-  const char* blob;
-  const void* x; void* y; int64_t ybase;
-  double alpha, beta;
-  int dtype;
+  int has_sell;                                              // tiles begin with SELL tiles
 };
 
 // pCSC row-band layout.  The rank's nonzeros are regrouped
@@ -143,7 +136,6 @@ struct HeadLaunch {
 
 // kernels.cu entry points (all enqueue on `s`)
 cudaError_t launch_rows(const RowLaunch& L, cudaStream_t s);
-cudaError_t launch_sell(const SellLaunch& L, cudaStream_t s);
 cudaError_t launch_cols(const ColLaunch& L, cudaStream_t s);
 cudaError_t launch_fixup(const FixupLaunch& L, cudaStream_t s);
 cudaError_t launch_heads(const HeadLaunch& L, cudaStream_t s);

@@ -139,7 +139,7 @@ __device__ __forceinline__ void warp_seg_scan(int key, double val, int& pk, doub
   pv = lane == 0 ? 0.0 : ev;
 }
 
-__device__ __forceinline__ int tile_kind(int4 d) { return d.w >= 0 ? KIND_SLAB : KIND_SEG; }
+__device__ __forceinline__ int tile_kind(int4 d) { return d.w >= 0 ? KIND_SLAB : (d.w == -2 ? KIND_SELL : KIND_SEG); }
 
 __device__ __forceinline__ void issue_blob(const char* blob, int4 d, int kind, int vsize, unsigned char* st,
                                            uint64_t* bar, uint64_t pol) {
@@ -154,26 +154,33 @@ __device__ __forceinline__ void issue_blob(const char* blob, int4 d, int kind, i
 //            nonzeros in registers (keyed by the uint8 tile-local row), rows
 //            crossing lanes are joined by one deterministic warp segmented
 //            scan, y = alpha*s + beta*y is written coalesced.
-// pCSR / pCOO tile kernel (SELL tiles run in sell_kernel).  Persistent CTAs;
-// every warp owns a one-slot TMA ring and walks tiles gw, gw+nw, ...  A tile is
-// copied from its slot into registers as soon as it lands and the warp's next
-// tile is issued into the slot right away, so that TMA overlaps this tile's
-// x gathers and reduction.  Tile kinds (internal.h):
+// pCSR / pCOO tile kernel: ONE persistent launch per SpMV.  Every warp owns a
+// one-slot TMA ring and walks tiles gw, gw+nw, ... of the rank's tile list
+// (SELL tiles first, then SEG / slab tiles; internal.h).
+//   SELL: lane = row of 32 consecutive regular rows; all W column indices are
+//         read from the slot, then all W x gathers are in flight before the
+//         first FMA; padding is masked by the row length.  The slot is refilled
+//         after the tile.
+//   SEG:  whole rows; the tile is copied from the slot into registers as soon
+//         as it lands and the warp's next tile is issued into the slot right
+//         away, so that TMA overlaps this tile's x gathers and reduction.  Lane
+//         l reduces its contiguous chunk of nonzeros keyed by the uint8
+//         tile-local row, rows crossing lanes are joined by one deterministic
+//         warp segmented scan, y = alpha*s + beta*y is written coalesced.
 //   slab: partial sum of a piece of one split row -> rec[w] (natural order,
-//         fixed shuffle tree: bit-reproducible)
-//   SEG:  whole rows; lane l reduces its contiguous chunk of nonzeros keyed by
-//         the uint8 tile-local row, rows crossing lanes are joined by one
-//         deterministic warp segmented scan, y = alpha*s + beta*y is written
-//         coalesced.
+//         fixed shuffle tree: bit-reproducible).
 #ifndef MSREP_ROW_MINB
 #define MSREP_ROW_MINB 2
 #endif
 template <typename VT>
-using RowLayout = WLayout<RStage<VT>::BYTES, 1, MAX_TILE_ROWS * 8>;
+struct SStage { static constexpr int BYTES = SELL_ROWS * 2 + SELL_W_MAX * SELL_ROWS * ((int)sizeof(VT) + 4); };
+template <typename VT, bool SELL>
+using RowLayout = WLayout<(SELL && SStage<VT>::BYTES > RStage<VT>::BYTES) ? SStage<VT>::BYTES : RStage<VT>::BYTES, 1,
+                          MAX_TILE_ROWS * 8>;
 
-template <typename VT>
+template <typename VT, bool SELL>
 __global__ void __launch_bounds__(WARPS * 32, MSREP_ROW_MINB) rows_kernel(const RowLaunch P) {
-  using Lay = RowLayout<VT>;
+  using Lay = RowLayout<VT, SELL>;
   constexpr int V = (int)sizeof(VT);
   constexpr int YR = MAX_TILE_ROWS / 32;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -210,6 +217,44 @@ __global__ void __launch_bounds__(WARPS * 32, MSREP_ROW_MINB) rows_kernel(const 
     if (t >= P.ntiles) break;
     mbar_wait(bar, (uint32_t)(i & 1));
     const int4 d = *sdesc;
+    auto refill = [&]() {
+      if (lane == 0) {
+        const int tn = t + nw;
+        if (tn < P.ntiles) {
+          *sdesc = dn;
+          issue_blob(P.blob, dn, tile_kind(dn), V, st, bar, pol);
+          if (tn + nw < P.ntiles) dn = P.tiles[tn + nw];
+        }
+      }
+    };
+    if (SELL && d.w == -2) {
+      // ---- SELL tile (read in place; the slot is refilled after the tile)
+      const int nrows = d.z & 0xffff, Wd = d.z >> 16;
+      const int mylen = reinterpret_cast<const uint16_t*>(st)[lane];
+      const VT* sv = reinterpret_cast<const VT*>(st + SELL_ROWS * 2);
+      const uint32_t* sc = reinterpret_cast<const uint32_t*>(st + SELL_ROWS * 2 + Wd * SELL_ROWS * V);
+      const int64_t yr = P.ybase + d.x + lane;
+      const bool live = lane < nrows;
+      const double yv = (beta != 0.0 && live) ? (double)y[yr] : 0.0;
+      uint32_t c[SELL_W_MAX];
+      VT xs[SELL_W_MAX];
+#pragma unroll
+      for (int u = 0; u < SELL_W_MAX; u++) c[u] = u < Wd ? sc[u * SELL_ROWS + lane] : 0u;   // no loop-carried state
+#pragma unroll
+      for (int u = 0; u < SELL_W_MAX; u++) xs[u] = u < Wd ? ldg_ro(x + c[u]) : VT(0);
+      double acc = 0.0;
+#pragma unroll
+      for (int u = 0; u < SELL_W_MAX; u++)
+        if (u < Wd && u < mylen) acc = fma((double)sv[u * SELL_ROWS + lane], (double)xs[u], acc);
+      if (live) {
+        double o = alpha * acc;
+        if (beta != 0.0) o += beta * yv;
+        y[yr] = (VT)o;
+      }
+      __syncwarp();
+      refill();
+      continue;
+    }
     const int nrows = d.z & 0xffff, nnz = d.z >> 16;
     const bool slab = d.w >= 0;
     // ---- stage -> registers (conflict-free 32-lane vectors), then refill the slot
@@ -246,14 +291,7 @@ __global__ void __launch_bounds__(WARPS * 32, MSREP_ROW_MINB) rows_kernel(const 
     }
     fence_proxy_async();   // order this lane's generic-proxy reads of the slot before the TMA refill
     __syncwarp();          // every lane holds its tile: the slot may be refilled
-    if (lane == 0) {
-      const int tn = t + nw;
-      if (tn < P.ntiles) {
-        *sdesc = dn;
-        issue_blob(P.blob, dn, tile_kind(dn), V, st, bar, pol);
-        if (tn + nw < P.ntiles) dn = P.tiles[tn + nw];
-      }
-    }
+    refill();
     // ---- x gathers: all in flight before the first use
     VT xv[QMAX + 1];
     if (slab) {
@@ -321,98 +359,6 @@ __global__ void __launch_bounds__(WARPS * 32, MSREP_ROW_MINB) rows_kernel(const 
       }
     }
     __syncwarp();   // rsum is free
-  }
-}
-
-// ------------------------------------------------------------- SELL tiles
-// pCSR regular rows: one warp = SELL_ROWS consecutive rows, lane = row.  The
-// tile's elements are slice-major in the blob, so each shared-memory load is a
-// conflict-free 32-lane vector and each x gather of 32 consecutive rows touches
-// few sectors.  All W column indices are read first, then all W gathers are in
-// flight before the first FMA (one L2 round trip per tile); padding elements are
-// masked by the row length, so results equal the plain row sums.
-template <typename VT>
-struct SStage { static constexpr int BYTES = SELL_ROWS * 2 + SELL_W_MAX * SELL_ROWS * ((int)sizeof(VT) + 4); };
-#ifndef MSREP_SELL_NS
-#define MSREP_SELL_NS 1
-#endif
-constexpr int SELL_NS = MSREP_SELL_NS;
-template <typename VT>
-using SellLayout = WLayout<SStage<VT>::BYTES, SELL_NS, 16>;
-
-template <typename VT>
-__global__ void __launch_bounds__(WARPS * 32) sell_kernel(const SellLaunch P) {
-  using Lay = SellLayout<VT>;
-  constexpr int NS = SELL_NS;
-  constexpr int V = (int)sizeof(VT);
-  constexpr int SB = SStage<VT>::BYTES;
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  unsigned char* wb = smem + warp * Lay::WARP_B;
-  int4* sdesc = reinterpret_cast<int4*>(wb + Lay::DESC_OFF);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Lay::BAR_OFF) + warp * NS;
-  const int gw = blockIdx.x * WARPS + warp, nw = gridDim.x * WARPS;
-  const VT* __restrict__ x = static_cast<const VT*>(P.x);
-  VT* __restrict__ y = static_cast<VT*>(P.y);
-  const double alpha = P.alpha, beta = P.beta;
-
-  uint64_t pol = 0;
-  int4 dn = make_int4(0, 0, 0, -1);
-  if (lane == 0) {
-    for (int s = 0; s < NS; s++) mbar_init(&bars[s], 1);
-    fence_mbar_init();
-    pol = policy_evict_first();
-    for (int s = 0; s < NS; s++) {
-      const int t = gw + s * nw;
-      if (t < P.ntiles) {
-        const int4 d = P.tiles[t];
-        sdesc[s] = d;
-        issue_blob(P.blob, d, KIND_SELL, V, wb + s * SB, &bars[s], pol);
-      }
-    }
-    if (gw + NS * nw < P.ntiles) dn = P.tiles[gw + NS * nw];
-  }
-  __syncwarp();
-  for (int i = 0;; i++) {
-    const int t = gw + i * nw;
-    if (t >= P.ntiles) break;
-    const int s = i % NS;
-    mbar_wait(&bars[s], (uint32_t)((i / NS) & 1));
-    const int4 d = sdesc[s];
-    unsigned char* st = wb + s * SB;
-    const int nrows = d.z & 0xffff, W = d.z >> 16;
-    const int mylen = reinterpret_cast<const uint16_t*>(st)[lane];
-    const VT* sv = reinterpret_cast<const VT*>(st + SELL_ROWS * 2);
-    const uint32_t* sc = reinterpret_cast<const uint32_t*>(st + SELL_ROWS * 2 + W * SELL_ROWS * V);
-    const int64_t yr = P.ybase + d.x + lane;
-    const bool live = lane < nrows;
-    const double yv = (beta != 0.0 && live) ? (double)y[yr] : 0.0;
-    uint32_t c[SELL_W_MAX];
-    VT xv[SELL_W_MAX];
-#pragma unroll
-    for (int u = 0; u < SELL_W_MAX; u++)
-      if (u < W) c[u] = sc[u * SELL_ROWS + lane];
-#pragma unroll
-    for (int u = 0; u < SELL_W_MAX; u++)
-      if (u < W) xv[u] = ldg_ro(x + c[u]);
-    double acc = 0.0;
-#pragma unroll
-    for (int u = 0; u < SELL_W_MAX; u++)
-      if (u < W && u < mylen) acc = fma((double)sv[u * SELL_ROWS + lane], (double)xv[u], acc);
-    if (live) {
-      double v = alpha * acc;
-      if (beta != 0.0) v += beta * yv;
-      y[yr] = (VT)v;
-    }
-    __syncwarp();
-    if (lane == 0) {
-      const int tn = t + NS * nw;
-      if (tn < P.ntiles) {
-        sdesc[s] = dn;
-        issue_blob(P.blob, dn, KIND_SELL, V, st, &bars[s], pol);
-        if (tn + nw < P.ntiles) dn = P.tiles[tn + nw];
-      }
-    }
   }
 }
 
@@ -743,21 +689,12 @@ int grid_for(K kernel, int smem_bytes, int ntiles) {
   return (int)(want < g ? (want < 1 ? 1 : want) : g);
 }
 
-template <typename VT>
+template <typename VT, bool SELL>
 cudaError_t launch_rows_t(const RowLaunch& L, cudaStream_t s) {
-  constexpr int b = RowLayout<VT>::TOTAL;
-  cudaError_t e = set_smem(rows_kernel<VT>, b);
+  constexpr int b = RowLayout<VT, SELL>::TOTAL;
+  cudaError_t e = set_smem(rows_kernel<VT, SELL>, b);
   if (e) return e;
-  rows_kernel<VT><<<grid_for(rows_kernel<VT>, b, L.ntiles), WARPS * 32, b, s>>>(L);
-  return cudaGetLastError();
-}
-
-template <typename VT>
-cudaError_t launch_sell_t(const SellLaunch& L, cudaStream_t s) {
-  constexpr int b = SellLayout<VT>::TOTAL;
-  cudaError_t e = set_smem(sell_kernel<VT>, b);
-  if (e) return e;
-  sell_kernel<VT><<<grid_for(sell_kernel<VT>, b, L.ntiles), WARPS * 32, b, s>>>(L);
+  rows_kernel<VT, SELL><<<grid_for(rows_kernel<VT, SELL>, b, L.ntiles), WARPS * 32, b, s>>>(L);
   return cudaGetLastError();
 }
 
@@ -780,12 +717,8 @@ cudaError_t launch_cols_t(const ColLaunch& L, cudaStream_t s) {
 
 cudaError_t launch_rows(const RowLaunch& L, cudaStream_t s) {
   if (L.ntiles == 0) return cudaSuccess;
-  return L.dtype == 0 ? launch_rows_t<double>(L, s) : launch_rows_t<float>(L, s);
-}
-
-cudaError_t launch_sell(const SellLaunch& L, cudaStream_t s) {
-  if (L.ntiles == 0) return cudaSuccess;
-  return L.dtype == 0 ? launch_sell_t<double>(L, s) : launch_sell_t<float>(L, s);
+  if (L.has_sell) return L.dtype == 0 ? launch_rows_t<double, true>(L, s) : launch_rows_t<float, true>(L, s);
+  return L.dtype == 0 ? launch_rows_t<double, false>(L, s) : launch_rows_t<float, false>(L, s);
 }
 
 cudaError_t launch_cols(const ColLaunch& L, cudaStream_t s) {
