@@ -36,7 +36,9 @@ def parse():
     p.add_argument("--steps", type=int, default=2000)
     p.add_argument("--warmup", type=int, default=20)
     p.add_argument("--impl", default="msrep", choices=["msrep", "reference"])
-    p.add_argument("--config", default="stencil", choices=["stencil", "rmat", "tallskinny", "random1k"])
+    p.add_argument("--config", default="stencil",
+                   choices=["stencil", "rmat", "tallskinny", "random1k"] +
+                   [f"suite-{s}-{z}" for s in gen.SUITE_SHAPES for z in gen.SUITE_SIZES])
     p.add_argument("--format", default=None, choices=["csr", "coo", "csc"])
     p.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     p.add_argument("--layout", default=None, choices=["replicated", "owned", "sharded"])

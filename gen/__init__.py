@@ -193,4 +193,42 @@ def make_config(name, kind=UNIFORM, scale_down=1):
         return rmat(s, seed=3, kind=kind)
     if name == "tallskinny":
         return kdistinct_csc(50_000_000 // scale_down, 1_000_000 // scale_down, 500, seed=4, kind=kind)
+    if name.startswith("suite-"):
+        return suite(name, kind=kind)
+    raise KeyError(name)
+
+
+SUITE_SHAPES = ("banded", "blockdiag", "powerlaw", "shortwide")
+SUITE_SIZES = {"1M": 10**6, "10M": 10**7, "100M": 10**8, "1B": 10**9}
+
+
+def powerlaw_mean_degree(R, kmax):
+    k = np.arange(1, kmax + 1, dtype=np.float64)
+    w = k ** -R
+    return float((k * w).sum() / w.sum())
+
+
+def suite(name, kind=UNIFORM):
+    """BASELINE.json config 5, SuiteSparse-shaped synthetic matrices:
+    suite-<shape>-<size>, shape in SUITE_SHAPES, size in SUITE_SIZES (target nnz).
+      banded     full band of 141 per row (HV15R-like), square
+      blockdiag  dense 64x64 diagonal blocks, square
+      powerlaw   power-law column degrees P(k) ~ k^-2.13, kmax 10^5 (wb-edu / Orkut R), square, CSC
+      shortwide  exactly 500 distinct uniform columns per row, n = 50 m (transpose of config 4)"""
+    _, shape, size = name.split("-")
+    target = SUITE_SIZES[size]
+    seed = 500 + SUITE_SHAPES.index(shape)
+    if shape == "banded":
+        m = max(1, target // 141)
+        return banded(m, m, 70, seed=seed, kind=kind)
+    if shape == "blockdiag":
+        m = max(64, target // 64 // 64 * 64)
+        return blockdiag(m, 64, seed=seed, kind=kind)
+    if shape == "powerlaw":
+        R, kmax = 2.13, 100_000
+        n = max(1, int(target / powerlaw_mean_degree(R, kmax)))
+        return powerlaw_csc(n, n, R, min(kmax, n), seed=seed, kind=kind)
+    if shape == "shortwide":
+        m = max(1, target // 500)
+        return kdistinct_csr(m, 50 * m, 500, seed=seed, kind=kind)
     raise KeyError(name)

@@ -155,6 +155,7 @@ struct Ctx {
   int32_t* d_split = nullptr;
   char* d_cblob = nullptr;
   int64_t cnb = 0, citems = 0;
+  bool csplit = false;
   int nheads_local = 0;
 
   // host-vector path buffers
@@ -386,6 +387,8 @@ void build_row_schedule(const Ctx& c, const std::vector<int64_t>& lp, Schedule& 
 // them into the stage blobs).
 struct CscBands {
   int64_t nb = 0, nch = 1, bytes = 0;     // bands, column chunks, blob bytes
+  int64_t chunk = CB_CHUNK;               // columns per chunk
+  bool split_items = false;               // few bands: items are the units of work
   std::vector<int4> items;                // {band, nstages, window col base, last-stage seg}
   std::vector<int64_t> item_off;          // byte offset of each item's blob
   std::vector<int32_t> band_item;         // [nb + 1]
@@ -434,13 +437,22 @@ int64_t arrange_list(const uint32_t* pk, int64_t n, std::vector<int64_t>& pend, 
 }
 
 msrep_status_t build_csc_bands(const Ctx& c, const std::vector<int64_t>& lp, const int32_t* idx, const void* val,
-                               size_t V, CscBands& B) {
+                               size_t V, int sms, CscBands& B) {
   const int64_t W = c.whi - c.wlo;
   const int64_t nz = c.B_hi - c.B_lo;
   const int32_t* rows = idx + c.B_lo;
   const char* vals = static_cast<const char*>(val) + (size_t)c.B_lo * V;
   B.nb = (c.m + CB_ROWS - 1) / CB_ROWS;
   B.nch = std::max<int64_t>(1, (W + CB_CHUNK - 1) / CB_CHUNK);
+  // short-wide matrices have fewer bands than SMs: cut the columns into more chunks and let
+  // every (band, chunk) item be a unit of work whose partial band is added into py
+  const int64_t units = 2 * (int64_t)sms;
+  if (B.nb < units && W > 0) {
+    B.split_items = true;
+    B.nch = std::max(B.nch, std::min<int64_t>((units + B.nb - 1) / B.nb, std::max<int64_t>(1, W / 4096)));
+  }
+  B.chunk = std::max<int64_t>(1, (W + B.nch - 1) / B.nch);
+  B.nch = std::max<int64_t>(1, (W + B.chunk - 1) / B.chunk);
   const int64_t keys = B.nb * B.nch * CB_W;
   if (keys > ((int64_t)1 << 26))
     return fail(MSREP_ERR_TOO_LARGE, "pCSC band layout: %lld (band, chunk, warp) lists > 2^26", (long long)keys);
@@ -487,7 +499,7 @@ msrep_status_t build_csc_bands(const Ctx& c, const std::vector<int64_t>& lp, con
   };
   auto key_of = [&](int64_t q, int32_t r) {
     const int64_t b = r / CB_ROWS;
-    return (b * B.nch + q / CB_CHUNK) * CB_W + warp_of(b, r % CB_ROWS);
+    return (b * B.nch + q / B.chunk) * CB_W + warp_of(b, r % CB_ROWS);
   };
   // 1. stable counting sort by key into temporary (pk, val) arrays
   std::vector<std::vector<int64_t>> off((size_t)T, std::vector<int64_t>((size_t)keys, 0));
@@ -515,7 +527,7 @@ msrep_status_t build_csc_bands(const Ctx& c, const std::vector<int64_t>& lp, con
       for (int64_t z = lp[(size_t)q]; z < lp[(size_t)q + 1]; z++) {
         const int32_t r = rows[z];
         const int64_t dst = o[(size_t)key_of(q, r)]++;
-        tpk[(size_t)dst] = (uint32_t)(r % CB_ROWS) | ((uint32_t)(q % CB_CHUNK) << CB_LOG2);
+        tpk[(size_t)dst] = (uint32_t)(r % CB_ROWS) | ((uint32_t)(q % B.chunk) << CB_LOG2);
         memcpy(tval.get() + (size_t)dst * V, vals + (size_t)z * V, V);
       }
   });
@@ -555,7 +567,7 @@ msrep_status_t build_csc_bands(const Ctx& c, const std::vector<int64_t>& lp, con
       const int64_t last = ((L - (nst - 1) * CB_SEG) + 3) & ~(int64_t)3;
       if (nst >= ((int64_t)1 << 31)) return fail(MSREP_ERR_TOO_LARGE, "pCSC warp list too long");
       key_item[(size_t)(b * B.nch + ch)] = (int64_t)B.items.size();
-      B.items.push_back(make_int4((int32_t)b, (int32_t)nst, (int32_t)(ch * CB_CHUNK), (int32_t)last));
+      B.items.push_back(make_int4((int32_t)b, (int32_t)nst, (int32_t)(ch * B.chunk), (int32_t)last));
       B.item_off.push_back(bytes);
       bytes += ((nst - 1) * CB_SEG + last) * CB_W * (int64_t)(V + 4);
     }
@@ -808,7 +820,10 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   if (fmt == MSREP_CSC) {
     // ---- pCSC: row-band layout built on the host threads, uploaded once
     CscBands CB;
-    TRY(build_csc_bands(*c, lp, idx, val, V, CB));
+    int sms = 148;
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+    TRY(build_csc_bands(*c, lp, idx, val, V, sms, CB));
+    c->csplit = CB.split_items;
     TRY(upload_vec(c, CB.items, &c->d_citems, s));
     TRY(upload_vec(c, CB.item_off, &c->d_item_off, s));
     TRY(upload_vec(c, CB.band_item, &c->d_band_item, s));
@@ -818,7 +833,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     c->citems = (int64_t)CB.items.size();
     c->ntiles = 0; c->nsell = 0; c->nslabs = 0; c->nrec = 0; c->nsplit = 0;
     c->blob_bytes = CB.bytes + c->citems * 24 + (CB.nb + 1) * 4 + CB.nb * (CB_W + 1) * 4;
-    c->py_len = c->nranks > 1 ? c->shard * c->nranks : 0;
+    c->py_len = c->nranks > 1 ? c->shard * c->nranks : (c->csplit ? m : 0);
     if (c->py_len) {
       void* pp;
       TRY(dalloc(c, (size_t)c->py_len * 8, &pp, s));
@@ -929,7 +944,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     own = rows_out;
     // the rank's entries + its column pointer + its x window + (p > 1) the fp64 py write and the
     // shard read after the reduce-scatter; p = 1 fuses alpha/beta into the band kernel (no py)
-    base = nz_r * (int64_t)(V + 4) + (W + 1) * 4 + W * (int64_t)V + (c->nranks > 1 ? m * 8 + rows_out * 8 : 0);
+    base = nz_r * (int64_t)(V + 4) + (W + 1) * 4 + W * (int64_t)V + ((c->nranks > 1 || c->csplit) ? m * 8 + rows_out * 8 : 0);
     ybytes_b1 = rows_out * (int64_t)V * 2;
     ybytes_b0 = rows_out * (int64_t)V;
   } else {
@@ -941,7 +956,8 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   st.owned_rows = own;
   st.alg_bytes = base + ybytes_b1;
   st.alg_bytes_beta0 = base + ybytes_b0;
-  if (fmt == MSREP_CSC) st.kernels_per_spmv = (c->cnb ? 1 : 0) + (c->nranks > 1 ? 1 /*shard epilogue*/ : 0);
+  if (fmt == MSREP_CSC)
+    st.kernels_per_spmv = (c->cnb ? 1 : 0) + ((c->nranks > 1 || c->csplit) ? 1 /*py epilogue*/ : 0) + (c->csplit ? 1 /*memset*/ : 0);
   else st.kernels_per_spmv = (c->ntiles ? 1 : 0) + (c->nranks > 1 && c->any_flag ? 1 : 0) + (c->nsplit ? 1 : 0);
   int64_t db = 0;
   for (auto& b : c->bufs) db += (int64_t)b.bytes;
@@ -982,8 +998,10 @@ msrep_status_t msrep_spmv(msrep_ctx h, const void* alpha_p, const void* x, const
     L.items = c->d_citems; L.item_off = c->d_item_off; L.band_item = c->d_band_item; L.split = c->d_split;
     L.nb = (int)c->cnb; L.blob = c->d_cblob;
     L.x = x; L.xbase = c->wlo;
-    L.fused = c->nranks == 1;
+    L.split_items = c->csplit; L.nitems = (int)c->citems;
+    L.fused = c->nranks == 1 && !c->csplit;
     L.out = L.fused ? y : static_cast<void*>(c->d_py);
+    if (c->csplit) CUDA_TRY(cudaMemsetAsync(c->d_py, 0, (size_t)c->m * 8, s));   // items add into py
     L.m = c->m; L.alpha = alpha; L.beta = beta; L.dtype = dt;
     cudaEvent_t pe;
     TRY(prof_begin(c, s, &pe));
@@ -994,6 +1012,8 @@ msrep_status_t msrep_spmv(msrep_ctx h, const void* alpha_p, const void* x, const
       NCCL_TRY(ncclReduceScatter(c->d_py, shard, (size_t)c->shard, ncclDouble, ncclSum, c->comm, s));
       CUDA_TRY(launch_axpby_py(shard, static_cast<char*>(y) + (size_t)my_lo * V, my_hi - my_lo, alpha, beta, dt, s));
       if (gather) TRY(allgatherv_y(c, y, seg_lo, seg_hi, s));
+    } else if (c->csplit) {
+      CUDA_TRY(launch_axpby_py(c->d_py, y, c->m, alpha, beta, dt, s));
     }
     return MSREP_OK;
   }

@@ -116,6 +116,7 @@ struct ColLaunch {
   void* out; int64_t m;                                      // fused: y (dtype); else fp64 py
   double alpha, beta;
   int fused; int dtype;
+  int split_items, nitems;    // few bands (m small): one CTA per item, partial bands added into py
 };
 
 struct FixupLaunch {

@@ -461,6 +461,20 @@ __global__ void __launch_bounds__(CB_THREADS, 1) csc_band_kernel(const ColLaunch
         if (bytes) tma_1d(smem + L::ST_OFF + s * L::STAGE, src, (uint32_t)bytes, &full[s], pol);
         it++;
       };
+      if (P.split_items) {   // one item at a time; every item ends its own (partial) band
+        for (int i = blockIdx.x; i < P.nitems; i += gridDim.x) {
+          const int4 item = P.items[i];
+          const char* src = P.blob + P.item_off[i];
+          for (int sg = 0; sg < item.y; sg++) {
+            const int seg = sg == item.y - 1 ? item.w : CB_SEG;
+            const int bytes = CB_W * seg * (V + 4);
+            stage(make_int4(item.x, seg, item.z, sg == item.y - 1 ? 1 : 0), src, bytes);
+            src += bytes;
+          }
+        }
+        stage(make_int4(-1, 0, 0, 0), nullptr, 0);
+        return;
+      }
       for (int b = blockIdx.x; b < P.nb; b += gridDim.x) {
         const int i0 = P.band_item[b], i1 = P.band_item[b + 1];
         if (i0 == i1) {   // empty band: still written out (zeros / beta*y)
@@ -525,6 +539,13 @@ __global__ void __launch_bounds__(CB_THREADS, 1) csc_band_kernel(const ColLaunch
               acc[r] = 0.0;
             }
           }
+        }
+      } else if (P.split_items) {   // partial band of one item: add (other items of the band do too)
+        double* py = static_cast<double*>(P.out) + r0;
+        for (int r = lo + lane; r < hi; r += 32) {
+          const double a = acc[r];
+          if (a != 0.0) atomicAdd(py + r, a);
+          acc[r] = 0.0;
         }
       } else {
         double* py = static_cast<double*>(P.out) + r0;
@@ -708,7 +729,9 @@ cudaError_t launch_cols_t(const ColLaunch& L, cudaStream_t s) {
   constexpr int b = CBLayout<VT>::TOTAL > MSREP_CB_SMEM_MIN ? CBLayout<VT>::TOTAL : MSREP_CB_SMEM_MIN;
   cudaError_t e = set_smem(csc_band_kernel<VT>, b);
   if (e) return e;
-  const int g = L.nb < num_sms() ? L.nb : num_sms();
+  const int units = L.split_items ? L.nitems : L.nb;
+  const int g = units < num_sms() ? units : num_sms();
+  if (g < 1) return cudaSuccess;
   csc_band_kernel<VT><<<g, CB_THREADS, b, s>>>(L);
   return cudaGetLastError();
 }

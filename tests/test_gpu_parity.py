@@ -283,3 +283,46 @@ def test_csc_bands_uniform_tolerance(dtype):
     A = to_dtype(gen.kdistinct_csc(100_000, 3000, 400, seed=44), dtype)
     x = gen.vector(A["n"], 45, dtype=dtype); y = gen.vector(A["m"], 46, dtype=dtype)
     check(A, "csc", x, y, 1.5, 0.5, parts=2)
+
+
+# --------------------------------------------- config 5: SuiteSparse-shaped suite
+def _suite_small(shape, kind):
+    if shape == "banded":
+        return gen.banded(3000, 3000, 70, seed=501, kind=kind)         # 141 per row, rows > one SEG tile
+    if shape == "blockdiag":
+        return gen.blockdiag(64 * 40, 64, seed=502, kind=kind)          # dense 64x64 blocks
+    if shape == "powerlaw":
+        return gen.transpose(gen.powerlaw_csc(20000, 20000, 2.13, 5000, seed=503, kind=kind))
+    return gen.kdistinct_csr(300, 15000, 500, seed=504, kind=kind)     # short-wide, 500 per row
+
+
+@pytest.mark.parametrize("shape", ["banded", "blockdiag", "powerlaw", "shortwide"])
+@pytest.mark.parametrize("fmt", FMTS)
+def test_suite_shapes_bit_exact(shape, fmt):
+    """Config 5 shapes at test size, integer data: bit-exact in every format, 1 and 3 parts."""
+    A = _suite_small(shape, gen.SMALLINT)
+    x = gen.vector(A["n"], 61, kind=gen.SMALLINT); y = gen.vector(A["m"], 62, kind=gen.SMALLINT)
+    for parts in (1, 3):
+        check(A, fmt, x, y, 1.5, 0.5, parts=parts, exact=True)
+
+
+@pytest.mark.parametrize("shape", ["banded", "blockdiag", "powerlaw", "shortwide"])
+@pytest.mark.parametrize("fmt", FMTS)
+def test_suite_shapes_fp32_tolerance(shape, fmt):
+    """Config 5 shapes, fp32 storage, U[-1,1): per-row tolerance 1e-5 of sum |a_ij x_j|."""
+    A = to_dtype(_suite_small(shape, gen.UNIFORM), np.float32)
+    x = gen.vector(A["n"], 63, dtype=np.float32); y = gen.vector(A["m"], 64, dtype=np.float32)
+    check(A, fmt, x, y, 1.5, 0.5, parts=2)
+
+
+@pytest.mark.parametrize("parts", [1, 2])
+def test_csc_split_items_short_wide(parts):
+    """Fewer row bands than SMs (m = 3 bands): the pCSC split-item path (partial bands added into
+    py, then the alpha/beta epilogue) -- integer data, bit-exact; and fp32 within tolerance."""
+    A = gen.kdistinct_csr(3 * 8192 - 5, 300_000, 40, seed=71, kind=gen.SMALLINT)
+    x = gen.vector(A["n"], 72, kind=gen.SMALLINT); y = gen.vector(A["m"], 73, kind=gen.SMALLINT)
+    check(A, "csc", x, y, 1.5, 0.5, parts=parts, exact=True)
+    check(A, "csc", x, y, 2.0, 0.0, parts=parts, exact=True)
+    B = to_dtype(gen.kdistinct_csr(1000, 200_000, 300, seed=74), np.float32)
+    xb = gen.vector(B["n"], 75, dtype=np.float32); yb = gen.vector(B["m"], 76, dtype=np.float32)
+    check(B, "csc", xb, yb, 1.5, 0.5, parts=parts)
