@@ -61,6 +61,11 @@ def lib():
             "or_exec_coo": [I64, I64, P, P, P, I, P, P, D, D, I64],
             "or_exec_csc": [I64, I64, P, P, P, I, P, P, D, D, I64],
             "or_merge_parts_to_ptr": [I64, I64, P, P, P],
+            "or_block_boundaries": [I64, P, I64, P],
+            "or_block_boundaries_coo": [I64, I64, P, I64, P],
+            "or_relative_throughput": [I64, P],
+            "or_partition_ptr_b": [I64, P, I64, P, P, P],
+            "or_partition_coo_b": [I64, P, I64, P, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -68,6 +73,8 @@ def lib():
             f.restype = None
         L.or_owner_linear.restype = I64
         L.or_partition_ptr.restype = I64
+        L.or_partition_ptr_b.restype = I64
+        L.or_relative_throughput.restype = D
         _lib = L
     return _lib
 
@@ -193,6 +200,42 @@ def partition_coo(m, row_idx, np_):
     row_idx = _c(row_idx, np.int64)
     parts = np.zeros(np_, PART_DTYPE)
     lib().or_partition_coo(m, row_idx.size, _p(row_idx), np_, _p(parts))
+    return parts
+
+
+def block_boundaries(ptr, np_):
+    """Baseline row/column-block split (Sec. 5.1): b_i = ptr[floor(i*m/np)]."""
+    ptr = _c(ptr, np.int64)
+    b = np.zeros(np_ + 1, np.int64)
+    lib().or_block_boundaries(ptr.size - 1, _p(ptr), np_, _p(b))
+    return b
+
+
+def block_boundaries_coo(m, row_idx, np_):
+    row_idx = _c(row_idx, np.int64)
+    b = np.zeros(np_ + 1, np.int64)
+    lib().or_block_boundaries_coo(m, row_idx.size, _p(row_idx), np_, _p(b))
+    return b
+
+
+def relative_throughput(b):
+    """Fig. 6 cost model: (sum nnz_i / np) / max nnz_i."""
+    b = _c(b, np.int64)
+    return float(lib().or_relative_throughput(b.size - 1, _p(b)))
+
+
+def partition_ptr_b(ptr, b):
+    """Alg. 2 / Alg. 4 for given boundaries b[0..np] -> parts (the descriptors only)."""
+    ptr = _c(ptr, np.int64); b = _c(b, np.int64)
+    parts = np.zeros(b.size - 1, PART_DTYPE)
+    lib().or_partition_ptr_b(ptr.size - 1, _p(ptr), b.size - 1, _p(b), _p(parts), None)
+    return parts
+
+
+def partition_coo_b(m, row_idx, b):
+    row_idx = _c(row_idx, np.int64); b = _c(b, np.int64)
+    parts = np.zeros(b.size - 1, PART_DTYPE)
+    lib().or_partition_coo_b(m, _p(row_idx), b.size - 1, _p(b), _p(parts))
     return parts
 
 

@@ -196,6 +196,40 @@ void or_nnz_boundaries(int64_t nnz, int64_t np, int64_t *b)
     for (int64_t i = 0; i <= np; i++) b[i] = (i * nnz) / np;
 }
 
+/* Row/column-block split of the paper's "Baseline" (Sec. 5.1: "the
+ * input matrix is partitioned in either row blocks (for CSR and COO) or column
+ * blocks (for CSC) without considering the distribution of non-zero
+ * elements"): part i holds the whole rows (columns) [floor(i*m/np),
+ * floor((i+1)*m/np)), i.e. b_i = ptr[floor(i*m/np)]. */
+void or_block_boundaries(int64_t m, const int64_t *ptr, int64_t np, int64_t *b)
+{
+    for (int64_t i = 0; i <= np; i++) b[i] = ptr[(i * m) / np];
+}
+
+/* The same row-block split on a row-sorted COO: b_i = number of nonzeros whose
+ * row is below floor(i*m/np), counted by a linear scan. */
+void or_block_boundaries_coo(int64_t m, int64_t nnz, const int64_t *row_idx, int64_t np, int64_t *b)
+{
+    for (int64_t i = 0; i <= np; i++) {
+        int64_t r = (i * m) / np, k = 0;
+        while (k < nnz && row_idx[k] < r) k++;
+        b[i] = k;
+    }
+}
+
+/* The workload-imbalance cost model behind Fig. 6: a
+ * memory-bound SpMV's time is set by the part with the most nonzeros, so the
+ * throughput of a plan relative to a perfectly balanced one is
+ * (sum_i nnz_i / np) / max_i nnz_i. */
+double or_relative_throughput(int64_t np, const int64_t *b)
+{
+    int64_t mx = 0;
+    for (int64_t i = 0; i < np; i++)
+        if (b[i + 1] - b[i] > mx) mx = b[i + 1] - b[i];
+    if (mx == 0) return 1.0;
+    return ((double)(b[np] - b[0]) / (double)np) / (double)mx;
+}
+
 /* Strict owner of nonzero position idx: the unique r with
  * ptr[r] <= idx < ptr[r+1] (reading R3).  LINEAR scan on purpose:
  * the library uses a binary search, so this is an independent check. */
@@ -225,12 +259,24 @@ typedef struct {
  *   owned range R_i = smallest r with ptr[r] >= b_i, R_0 = 0, R_np = m (R9).
  * local_out receives, for each part in order, its end_row-start_row+2 local
  * pointers (1 entry [0] for an empty part); returns total entries written. */
+int64_t or_partition_ptr_b(int64_t m, const int64_t *ptr, int64_t np, const int64_t *b,
+                           or_part *parts, int64_t *local_out);
+
 int64_t or_partition_ptr(int64_t m, const int64_t *ptr, int64_t np,
                          or_part *parts, int64_t *local_out)
 {
-    int64_t nnz = ptr[m];
     int64_t *b = (int64_t *)malloc((size_t)(np + 1) * sizeof(int64_t));
-    or_nnz_boundaries(nnz, np, b);
+    or_nnz_boundaries(ptr[m], np, b);
+    int64_t w = or_partition_ptr_b(m, ptr, np, b, parts, local_out);
+    free(b);
+    return w;
+}
+
+/* Alg. 2 / Alg. 4 lines 4-12 for given part boundaries b[0..np] (nnz split or
+ * the Baseline's row/column blocks). */
+int64_t or_partition_ptr_b(int64_t m, const int64_t *ptr, int64_t np, const int64_t *b,
+                           or_part *parts, int64_t *local_out)
+{
     int64_t w = 0;
     for (int64_t i = 0; i < np; i++) {
         or_part *p = &parts[i];
@@ -267,7 +313,6 @@ int64_t or_partition_ptr(int64_t m, const int64_t *ptr, int64_t np,
             w += 1;
         }
     }
-    free(b);
     return w;
 }
 
@@ -276,10 +321,19 @@ int64_t or_partition_ptr(int64_t m, const int64_t *ptr, int64_t np,
  * row_idx[start_idx], end_row = row_idx[end_idx], start_flag = start_idx > 0
  * && row_idx[start_idx-1] == row_idx[start_idx]; owned_begin =
  * row_idx[b_i - 1] + 1 (R_0 = 0), owned_end = next part's owned_begin (R_np=m). */
+void or_partition_coo_b(int64_t m, const int64_t *row_idx, int64_t np, const int64_t *b, or_part *parts);
+
 void or_partition_coo(int64_t m, int64_t nnz, const int64_t *row_idx, int64_t np, or_part *parts)
 {
     int64_t *b = (int64_t *)malloc((size_t)(np + 1) * sizeof(int64_t));
     or_nnz_boundaries(nnz, np, b);
+    or_partition_coo_b(m, row_idx, np, b, parts);
+    free(b);
+}
+
+/* Alg. 6 for given part boundaries b[0..np]. */
+void or_partition_coo_b(int64_t m, const int64_t *row_idx, int64_t np, const int64_t *b, or_part *parts)
+{
     for (int64_t i = 0; i < np; i++) {
         or_part *p = &parts[i];
         p->start_idx = b[i];
@@ -293,7 +347,6 @@ void or_partition_coo(int64_t m, int64_t nnz, const int64_t *row_idx, int64_t np
         p->end_row = row_idx[p->end_idx];
         p->start_flag = (p->start_idx > 0 && row_idx[p->start_idx - 1] == row_idx[p->start_idx]) ? 1 : 0;
     }
-    free(b);
 }
 
 /* ------------------------------------------------------------------------ */

@@ -378,3 +378,65 @@ def test_coo_partition_matches_csr_partition():
             for k in ("start_idx", "end_idx", "start_row", "end_row", "start_flag", "owned_begin",
                       "owned_end"):
                 assert np.array_equal(pc[k], pr[k]), (k, trial, np_)
+
+
+# ------------------------------------------------ Baseline row/column-block split (NEXT f1)
+def test_block_split_fixture_E_hand_worked():
+    """Baseline row blocks (Sec. 5.1) of SPEC fixture E (row_ptr [0,2,3,3,5]),
+    np = 2 -> rows {0,1} | {2,3}: b = [ptr[0], ptr[2], ptr[4]] = [0, 3, 5].  Part 0 holds
+    nonzeros 0..2 of rows 0..1 (no flag) and owns rows [0,2); part 1 holds nonzeros 3..4;
+    row 2 is empty, so nonzero 3's strict owner is row 3, no flag, owned rows [2,4)
+    (R_1 = lower_bound(ptr, 3) = 2: the empty row goes to the part holding the next nonzero)."""
+    ptr = np.array([0, 2, 3, 3, 5])
+    b = oracle.block_boundaries(ptr, 2)
+    assert b.tolist() == [0, 3, 5]
+    p = oracle.partition_ptr_b(ptr, b)
+    got = [(int(q["start_idx"]), int(q["end_idx"]), int(q["start_row"]), int(q["end_row"]), int(q["start_flag"]),
+            int(q["owned_begin"]), int(q["owned_end"])) for q in p]
+    assert got == [(0, 2, 0, 1, 0, 0, 2), (3, 4, 3, 3, 0, 2, 4)]
+
+
+def test_block_split_equals_nnz_split_on_uniform_rows():
+    """Closed form: with exactly k nonzeros per row and np | m, row blocks and the nnz split cut
+    at the same places (b_i = i*k*m/np), so Alg. 2 yields identical descriptors."""
+    for m, k, np_ in [(8, 3, 4), (60, 7, 6), (64, 1, 8)]:
+        ptr = np.arange(m + 1, dtype=np.int64) * k
+        bb, bn = oracle.block_boundaries(ptr, np_), oracle.nnz_boundaries(m * k, np_)
+        assert np.array_equal(bb, bn)
+        assert np.array_equal(oracle.partition_ptr_b(ptr, bb), oracle.partition_ptr(ptr, np_)[0])
+
+
+def test_block_split_whole_rows_no_flags_random():
+    """Brute force: part i of the row-block split holds exactly the nonzeros of rows
+    [floor(i*m/np), floor((i+1)*m/np)), never shares a row (start_flag = 0), and the COO
+    form (counted by scanning row ids) gives the same descriptors."""
+    rng = np.random.default_rng(31)
+    for _ in range(200):
+        m = int(rng.integers(1, 40)); np_ = int(rng.integers(1, 12))
+        ptr = np.concatenate([[0], np.cumsum(rng.integers(0, 6, m))]).astype(np.int64)
+        b = oracle.block_boundaries(ptr, np_)
+        for i in range(np_):
+            r0, r1 = i * m // np_, (i + 1) * m // np_
+            assert b[i] == ptr[r0] and b[i + 1] == ptr[r1]
+        parts = oracle.partition_ptr_b(ptr, b)
+        assert (parts["start_flag"] == 0).all()
+        rows = oracle.csr_to_coo(m, ptr)
+        bc = oracle.block_boundaries_coo(m, rows, np_)
+        assert np.array_equal(bc, b)
+        pc = oracle.partition_coo_b(m, rows, bc)
+        for k in ("start_idx", "end_idx", "start_row", "end_row", "start_flag", "owned_begin", "owned_end"):
+            assert np.array_equal(pc[k], parts[k]), k
+
+
+def test_relative_throughput_fig6_two_class():
+    """Fig. 6: 4 of 8 GPUs hold 1/10 of the nonzeros of the other 4 ->
+    throughput 'about half (559/1028)'.  The cost model's closed form:
+    (4h + 4h/10)/8 / h = 0.55, within 0.01 of the paper's 559/1028 = 0.5438."""
+    h = 1000
+    sizes = [h] * 4 + [h // 10] * 4
+    b = np.concatenate([[0], np.cumsum(sizes)])
+    r = oracle.relative_throughput(b)
+    assert r == pytest.approx(0.55, abs=1e-12)
+    assert abs(r - 559 / 1028) < 0.01
+    assert oracle.relative_throughput(oracle.nnz_boundaries(int(b[-1]), 8)) > 0.99
+    assert oracle.relative_throughput(np.array([0, 5, 10])) == 1.0
