@@ -48,6 +48,7 @@ def lib():
             "gen_powerlaw_csc_count": [I64, I64, D, I64, U64, P],
             "gen_powerlaw_csc_fill": [I64, I64, D, I64, U64, I, P, P, P],
             "gen_vector": [I64, U64, I, P],
+            "gen_kvar_fill": [I64, I64, U64, I, P, P, P],
             "gen_expand_ptr": [I64, P, P],
             "gen_transpose": [I64, I64, P, P, P, P, P, P],
         }
@@ -93,6 +94,16 @@ def kdistinct_csc(m, n, k, seed, kind=UNIFORM):
     counts = np.full(n, min(k, m), np.int64)
     return _finish("csc", m, n, counts,
                    lambda p, i, v: lib().gen_kdistinct_fill(n, m, k, seed, kind, 1, _p(p), _p(i), _p(v)))
+
+
+def two_class(m, n, nblocks, heavy_blocks, k_heavy, ratio, seed=600, kind=UNIFORM):
+    """Fig. 6's imbalance workload: m rows in nblocks equal row blocks; rows of the
+    first heavy_blocks blocks get k_heavy distinct uniform columns, the others round(k_heavy*ratio)
+    (at least 1), so a row-block split gives two classes of per-GPU nnz with low/high = ratio."""
+    blk = np.arange(m, dtype=np.int64) * nblocks // m
+    counts = np.where(blk < heavy_blocks, k_heavy, max(1, int(round(k_heavy * ratio)))).astype(np.int64)
+    counts = np.minimum(counts, n)
+    return _finish("csr", m, n, counts, lambda p, i, v: lib().gen_kvar_fill(m, n, seed, kind, _p(p), _p(i), _p(v)))
 
 
 def stencil27(N, seed=2, kind=UNIFORM):

@@ -199,6 +199,15 @@ void gen_kdistinct_fill(int64_t outer, int64_t inner, int64_t k, uint64_t seed, 
   });
 }
 
+// --- row-dependent k: row r gets ptr[r+1]-ptr[r] distinct uniform columns (two-class imbalance matrices).
+void gen_kvar_fill(int64_t outer, int64_t inner, uint64_t seed, int kind, const int64_t* ptr, int32_t* idx, double* val) {
+  parallel_rows(outer, [&](int64_t r, std::vector<int64_t>& s) {
+    k_distinct(seed, r, inner, ptr[r + 1] - ptr[r], s);
+    int64_t o = ptr[r];
+    for (size_t q = 0; q < s.size(); q++) { idx[o + (int64_t)q] = (int32_t)s[q]; val[o + (int64_t)q] = entry_value(seed, kind, r, s[q]); }
+  });
+}
+
 // --- config 2: 27-point stencil on an N^3 grid, lexicographic order (i,j,k), k fastest.
 void gen_stencil27_count(int64_t N, int64_t* counts) {
   parallel_rows(N * N * N, [&](int64_t r, std::vector<int64_t>&) {

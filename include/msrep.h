@@ -45,6 +45,15 @@ typedef enum { MSREP_CSR = 0, MSREP_CSC = 1, MSREP_COO = 2 } msrep_format;
 
 typedef enum { MSREP_F64 = 0, MSREP_F32 = 1 } msrep_dtype;
 
+/* How the nonzeros are cut into the np parts.
+ *  NNZ:   the msRep split b_i = floor(i*nnz/np) (Alg. 2 / 4 / 6 lines 2-3):
+ *         every part holds nnz/np nonzeros (+-1), rows/columns may be shared.
+ *  BLOCK: the paper's "Baseline" (Sec. 5.1): whole row blocks (CSR, COO) or
+ *         column blocks (CSC) [floor(i*outer/np), floor((i+1)*outer/np)),
+ *         b_i = ptr[floor(i*outer/np)]; never shares a row, imbalanced when the
+ *         nonzeros are (Fig. 6).  Same kernels and merge. */
+typedef enum { MSREP_SPLIT_NNZ = 0, MSREP_SPLIT_BLOCK = 1 } msrep_split;
+
 /* Where y ends up after msrep_spmv (reading R19; the paper merges
  * into CPU memory).
  *  REPLICATED: every rank's y[0..m) holds the full result.
@@ -149,15 +158,22 @@ msrep_status_t msrep_spmv(msrep_ctx ctx, const void* alpha, const void* x, const
 msrep_status_t msrep_spmv_host(msrep_ctx ctx, const void* alpha, const void* x_host, const void* beta,
                                void* y_host, msrep_layout layout, void* stream);
 
+/* Select the split used by the next msrep_partition on this context (default
+ * MSREP_SPLIT_NNZ).  All ranks must select the same split. */
+msrep_status_t msrep_set_split(msrep_ctx ctx, msrep_split split);
+
 /* Pure host: the np descriptors of Alg. 2/4 (fmt CSR/CSC, ptr = pointer array
  * of length outer+1) or Alg. 6 (fmt COO, coo_row = row_idx[nnz], m = rows).
  * Used for bit-exact parity with the oracle.  No device, no context. */
 msrep_status_t msrep_plan(msrep_format fmt, int64_t outer, int64_t nnz, int np, const int64_t* ptr,
                           const int32_t* coo_row, msrep_part_desc* parts_out);
+/* The same for either split (msrep_plan == msrep_plan_split(fmt, MSREP_SPLIT_NNZ, ...)). */
+msrep_status_t msrep_plan_split(msrep_format fmt, msrep_split split, int64_t outer, int64_t nnz, int np,
+                                const int64_t* ptr, const int32_t* coo_row, msrep_part_desc* parts_out);
 
 /* Pure host: the exchange step of msrep_spmv for nranks > 1 (Sec. 4.3,
  * P:602-607; readings R6, R9, R10) as msrep_spmv performs it, with
- * np = nranks*parts_per_rank parts planned as msrep_plan does.
+ * np = nranks*parts_per_rank parts planned as msrep_plan_split does.
  *   seg_out[2r], seg_out[2r+1]: y rows [lo, hi) rank r writes under OWNED /
  *       SHARDED and broadcasts in the REPLICATED allgatherv (row formats: its
  *       parts' owned rows; pCSC: uniform shards of ceil(m/nranks) rows, the
@@ -168,9 +184,9 @@ msrep_status_t msrep_plan(msrep_format fmt, int64_t outer, int64_t nnz, int np, 
  *       head_part_out[j] / parts_per_rank), -1 if none.  [np] or NULL.
  * pCSC has no head exchange (heads -1): its partial vectors are summed.
  * Errors as msrep_plan.  No device, no context. */
-msrep_status_t msrep_exchange_plan(msrep_format fmt, int64_t m, int64_t n, int64_t nnz, int nranks,
-                                   int parts_per_rank, const int64_t* ptr, const int32_t* coo_row, int64_t* seg_out,
-                                   int64_t* head_row_out, int32_t* head_part_out);
+msrep_status_t msrep_exchange_plan(msrep_format fmt, msrep_split split, int64_t m, int64_t n, int64_t nnz,
+                                   int nranks, int parts_per_rank, const int64_t* ptr, const int32_t* coo_row,
+                                   int64_t* seg_out, int64_t* head_row_out, int32_t* head_part_out);
 
 msrep_status_t msrep_get_stats(msrep_ctx ctx, msrep_stats* out);
 

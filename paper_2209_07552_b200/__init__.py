@@ -24,6 +24,8 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 # enums (include/msrep.h)
 CSR, CSC, COO = 0, 1, 2
+SPLIT_NNZ, SPLIT_BLOCK = 0, 1
+SPLITS = {"nnz": SPLIT_NNZ, "block": SPLIT_BLOCK}
 F64, F32 = 0, 1
 Y_REPLICATED, Y_OWNED, Y_SHARDED = 0, 1, 2
 STATUS = {0: "MSREP_OK", 1: "MSREP_ERR_INVALID_ARG", 2: "MSREP_ERR_DIM_MISMATCH", 3: "MSREP_ERR_UNSORTED_COO",
@@ -69,7 +71,9 @@ _sig = {
     "msrep_spmv": [P, P, P, P, P, I, P],
     "msrep_spmv_host": [P, P, P, P, P, I, P],
     "msrep_plan": [I, I64, I64, I, P, P, P],
-    "msrep_exchange_plan": [I, I64, I64, I64, I, I, P, P, P, P, P],
+    "msrep_exchange_plan": [I, I, I64, I64, I64, I, I, P, P, P, P, P],
+    "msrep_plan_split": [I, I, I64, I64, I, P, P, P],
+    "msrep_set_split": [P, I],
     "msrep_get_stats": [P, ctypes.POINTER(Stats)],
     "msrep_destroy": [P],
     "msrep_profile_enable": [P, I],
@@ -84,7 +88,7 @@ _lib.msrep_version.argtypes = []
 _lib.msrep_version.restype = ctypes.c_int
 
 EXPORTED = ["msrep_get_unique_id", "msrep_create", "msrep_partition", "msrep_spmv", "msrep_spmv_host",
-            "msrep_plan", "msrep_exchange_plan", "msrep_get_stats", "msrep_destroy", "msrep_last_error", "msrep_version",
+            "msrep_plan", "msrep_plan_split", "msrep_set_split", "msrep_exchange_plan", "msrep_get_stats", "msrep_destroy", "msrep_last_error", "msrep_version",
             "msrep_profile_enable", "msrep_profile_read"]
 
 
@@ -161,7 +165,22 @@ def msrep_plan(fmt, outer, nnz, np_, ptr=None, coo_row=None):
     return parts
 
 
-def msrep_exchange_plan(fmt, m, n, nnz, nranks, parts_per_rank, ptr=None, coo_row=None):
+def msrep_plan_split(fmt, split, outer, nnz, np_, ptr=None, coo_row=None):
+    parts = np.zeros(np_, PART_DTYPE)
+    if ptr is not None:
+        ptr = np.ascontiguousarray(ptr, np.int64)
+    if coo_row is not None:
+        coo_row = np.ascontiguousarray(coo_row, np.int32)
+    _check(_lib.msrep_plan_split(fmt, split, outer, nnz, np_, _ptr(ptr), _ptr(coo_row), _ptr(parts)),
+           "msrep_plan_split")
+    return parts
+
+
+def msrep_set_split(ctx, split):
+    _check(_lib.msrep_set_split(ctx, split), "msrep_set_split")
+
+
+def msrep_exchange_plan(fmt, m, n, nnz, nranks, parts_per_rank, ptr=None, coo_row=None, split=SPLIT_NNZ):
     """Pure host: the multi-rank exchange step msrep_spmv performs (include/msrep.h).
     Returns (seg[nranks, 2] y-row segments per rank, head_row[np], head_part[np])."""
     np_ = nranks * parts_per_rank
@@ -172,7 +191,7 @@ def msrep_exchange_plan(fmt, m, n, nnz, nranks, parts_per_rank, ptr=None, coo_ro
         ptr = np.ascontiguousarray(ptr, np.int64)
     if coo_row is not None:
         coo_row = np.ascontiguousarray(coo_row, np.int32)
-    _check(_lib.msrep_exchange_plan(fmt, m, n, nnz, nranks, parts_per_rank, _ptr(ptr), _ptr(coo_row), _ptr(seg),
+    _check(_lib.msrep_exchange_plan(fmt, split, m, n, nnz, nranks, parts_per_rank, _ptr(ptr), _ptr(coo_row), _ptr(seg),
                                     _ptr(hrow), _ptr(hpart)), "msrep_exchange_plan")
     return seg.reshape(nranks, 2), hrow, hpart
 
@@ -225,9 +244,10 @@ class Context:
             uid = obj[0]
         return cls(rank, world, uid, device, parts_per_rank)
 
-    def partition(self, fmt, m, n, ptr=None, idx=None, val=None, coo_row=None, stream=None):
+    def partition(self, fmt, m, n, ptr=None, idx=None, val=None, coo_row=None, stream=None, split="nnz"):
         if isinstance(fmt, str):
             fmt = FORMATS[fmt]
+        msrep_set_split(self.h, SPLITS[split] if isinstance(split, str) else split)
         val = np.ascontiguousarray(val)
         dtype = F64 if val.dtype == np.float64 else F32
         idx = np.ascontiguousarray(idx, np.int32)

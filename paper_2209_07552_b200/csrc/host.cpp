@@ -9,6 +9,7 @@
 // owned y segment.
 #include <algorithm>
 #include <atomic>
+#include <climits>
 #include <chrono>
 #include <cstdarg>
 #include <cstdio>
@@ -60,14 +61,26 @@ constexpr int64_t kMaxIdx = (int64_t)1 << 31;
 constexpr int64_t kMaxRankNnz = kMaxIdx - (1 << 16);
 
 // ------------------------------------------------------------ descriptors
-// b_i = floor(i*nnz/np) (Alg. 2 l.2-3).
-inline int64_t boundary(int64_t i, int64_t nnz, int64_t np) { return (i * nnz) / np; }
+// Part boundaries b[0..np]: the nnz split b_i = floor(i*nnz/np) (Alg. 2 l.2-3,
+// P:311-312), or the paper's "Baseline" row/column blocks (Sec. 5.1):
+// b_i = ptr[floor(i*outer/np)] (COO: the first nonzero of row floor(i*m/np)).
+void split_bounds(msrep_format fmt, msrep_split split, int64_t outer, int64_t nnz, int np, const int64_t* ptr,
+                  const int32_t* row, std::vector<int64_t>& b) {
+  b.resize((size_t)np + 1);
+  for (int i = 0; i <= np; i++) {
+    if (split == MSREP_SPLIT_NNZ) b[(size_t)i] = ((int64_t)i * nnz) / np;
+    else if (fmt == MSREP_COO) {
+      const int64_t r = ((int64_t)i * outer) / np;
+      b[(size_t)i] = (int64_t)(std::lower_bound(row, row + nnz, (int32_t)std::min<int64_t>(r, INT32_MAX)) - row);
+    } else b[(size_t)i] = ptr[((int64_t)i * outer) / np];
+  }
+}
 
 // Alg. 2/4: BinarySearch -> strict owner upper_bound(ptr, idx) - 1 (reading R3);
 // owned range R_i = lower_bound(ptr[0..outer), b_i), R_0 = 0, R_np = outer (R9).
-void plan_ptr(int64_t outer, int64_t nnz, int np, const int64_t* ptr, msrep_part_desc* P) {
+void plan_ptr(int64_t outer, int np, const int64_t* ptr, const std::vector<int64_t>& b, msrep_part_desc* P) {
   for (int i = 0; i < np; i++) {
-    const int64_t b0 = boundary(i, nnz, np), b1 = boundary(i + 1, nnz, np);
+    const int64_t b0 = b[(size_t)i], b1 = b[(size_t)i + 1];
     msrep_part_desc& d = P[i];
     d.start_idx = b0;
     d.end_idx = b1 - 1;
@@ -86,9 +99,9 @@ void plan_ptr(int64_t outer, int64_t nnz, int np, const int64_t* ptr, msrep_part
 }
 
 // Alg. 6 on a row-sorted COO (reading R8): rows read from row_idx at the cuts.
-void plan_coo(int64_t m, int64_t nnz, int np, const int32_t* row, msrep_part_desc* P) {
+void plan_coo(int64_t m, int np, const int32_t* row, const std::vector<int64_t>& b, msrep_part_desc* P) {
   for (int i = 0; i < np; i++) {
-    const int64_t b0 = boundary(i, nnz, np), b1 = boundary(i + 1, nnz, np);
+    const int64_t b0 = b[(size_t)i], b1 = b[(size_t)i + 1];
     msrep_part_desc& d = P[i];
     d.start_idx = b0;
     d.end_idx = b1 - 1;
@@ -114,6 +127,7 @@ struct DevBuf {
 
 struct Ctx {
   int rank = 0, nranks = 1, vparts = 1, np = 1, device = 0;
+  msrep_split split = MSREP_SPLIT_NNZ;
   ncclComm_t comm = nullptr;
   msrep_allocator alloc{};
   bool has_alloc = false;
@@ -263,20 +277,26 @@ struct Packer {
     if (cur_r0 < 0) { cur_r0 = r; cur_r1 = r; }
     cur_r1 = r + 1;
   }
-  // SELL tile for rows [r, e) (<= SELL_ROWS whole owned rows) if every row has <= SELL_W_MAX
-  // nonzeros and padding to the longest row is <= 1/8 of the stored elements.
-  bool try_sell(int64_t r, int64_t e) {
-    int64_t W = 0, sum = 0;
-    for (int64_t q = r; q < e; q++) {
-      const int64_t len = le(q) - ls(q);
-      if (len > SELL_W_MAX) return false;
-      W = std::max(W, len);
-      sum += len;
+  // SELL tile for rows [r, r + 32R) (R rows per lane, R*W <= SELL_W_MAX, whole owned rows < rend)
+  // if padding to the longest row is <= 1/8 of the stored elements; tries R = 4, 2, 1.
+  int64_t try_sell(int64_t r, int64_t rend) {
+    for (int R = SELL_R_MAX; R >= 1; R >>= 1) {
+      const int64_t e = std::min<int64_t>(r + 32 * R, rend);
+      if (R > 1 && e - r <= 32 * (R / 2)) continue;   // a smaller R covers these rows
+      int64_t W = 0, sum = 0;
+      bool ok = true;
+      for (int64_t q = r; q < e && ok; q++) {
+        const int64_t len = le(q) - ls(q);
+        if (len * R > SELL_W_MAX) ok = false;
+        W = std::max(W, len);
+        sum += len;
+      }
+      if (!ok || W == 0 || 8 * sum < 7 * W * (e - r)) continue;
+      flush();
+      S.sell.push_back({(int32_t)(r - wlo), (int32_t)ls(r), (int32_t)((e - r) | (W << 16)), -2});
+      return e;
     }
-    if (W == 0 || 8 * sum < 7 * W * SELL_ROWS) return false;
-    flush();
-    S.sell.push_back({(int32_t)(r - wlo), (int32_t)ls(r), (int32_t)((e - r) | (W << 16)), -2});
-    return true;
+    return -1;
   }
   // slabs over rank-local nonzeros [z0, z1) of row r; with_records: write partial sums to records
   void slabs(int64_t r, int64_t z0, int64_t z1, bool with_records) {
@@ -362,8 +382,11 @@ void build_row_schedule(const Ctx& c, const std::vector<int64_t>& lp, Schedule& 
       }
     };
     for (int64_t r = d.owned_begin; r < rend;) {
+      if (c.fmt == MSREP_CSR) {
+        const int64_t e = pk.try_sell(r, rend);
+        if (e > r) { r = e; continue; }
+      }
       const int64_t e = std::min<int64_t>(r + SELL_ROWS, rend);
-      if (c.fmt == MSREP_CSR && pk.try_sell(r, e)) { r = e; continue; }
       for (; r < e; r++) one_row(r);
     }
     pk.flush();
@@ -646,31 +669,47 @@ msrep_status_t msrep_get_unique_id(uint8_t id[128]) {
   return MSREP_OK;
 }
 
-msrep_status_t msrep_plan(msrep_format fmt, int64_t outer, int64_t nnz, int np, const int64_t* ptr,
-                          const int32_t* coo_row, msrep_part_desc* parts_out) {
+msrep_status_t msrep_plan_split(msrep_format fmt, msrep_split split, int64_t outer, int64_t nnz, int np,
+                                const int64_t* ptr, const int32_t* coo_row, msrep_part_desc* parts_out) {
   if (np < 1 || outer < 0 || nnz < 0 || !parts_out) return fail(MSREP_ERR_INVALID_ARG, "bad plan arguments");
+  if (split != MSREP_SPLIT_NNZ && split != MSREP_SPLIT_BLOCK) return fail(MSREP_ERR_INVALID_ARG, "unknown split %d", (int)split);
+  std::vector<int64_t> b;
   if (fmt == MSREP_COO) {
     if (nnz > 0 && !coo_row) return fail(MSREP_ERR_INVALID_ARG, "COO plan needs row_idx");
-    plan_coo(outer, nnz, np, coo_row, parts_out);
+    split_bounds(fmt, split, outer, nnz, np, nullptr, coo_row, b);
+    plan_coo(outer, np, coo_row, b, parts_out);
   } else if (fmt == MSREP_CSR || fmt == MSREP_CSC) {
     if (!ptr) return fail(MSREP_ERR_INVALID_ARG, "plan needs ptr");
     if (ptr[0] != 0 || ptr[outer] != nnz) return fail(MSREP_ERR_DIM_MISMATCH, "ptr[0] != 0 or ptr[outer] != nnz");
-    plan_ptr(outer, nnz, np, ptr, parts_out);
+    split_bounds(fmt, split, outer, nnz, np, ptr, nullptr, b);
+    plan_ptr(outer, np, ptr, b, parts_out);
   } else {
     return fail(MSREP_ERR_INVALID_ARG, "unknown format %d", (int)fmt);
   }
   return MSREP_OK;
 }
 
-msrep_status_t msrep_exchange_plan(msrep_format fmt, int64_t m, int64_t n, int64_t nnz, int nranks,
-                                   int parts_per_rank, const int64_t* ptr, const int32_t* coo_row, int64_t* seg_out,
-                                   int64_t* head_row_out, int32_t* head_part_out) {
+msrep_status_t msrep_plan(msrep_format fmt, int64_t outer, int64_t nnz, int np, const int64_t* ptr,
+                          const int32_t* coo_row, msrep_part_desc* parts_out) {
+  return msrep_plan_split(fmt, MSREP_SPLIT_NNZ, outer, nnz, np, ptr, coo_row, parts_out);
+}
+
+msrep_status_t msrep_set_split(msrep_ctx h, msrep_split split) {
+  if (!h) return fail(MSREP_ERR_INVALID_ARG, "ctx is NULL");
+  if (split != MSREP_SPLIT_NNZ && split != MSREP_SPLIT_BLOCK) return fail(MSREP_ERR_INVALID_ARG, "unknown split %d", (int)split);
+  reinterpret_cast<Ctx*>(h)->split = split;
+  return MSREP_OK;
+}
+
+msrep_status_t msrep_exchange_plan(msrep_format fmt, msrep_split split, int64_t m, int64_t n, int64_t nnz,
+                                   int nranks, int parts_per_rank, const int64_t* ptr, const int32_t* coo_row,
+                                   int64_t* seg_out, int64_t* head_row_out, int32_t* head_part_out) {
   if (nranks < 1 || parts_per_rank < 1 || m < 0 || n < 0 || nnz < 0 || !seg_out)
     return fail(MSREP_ERR_INVALID_ARG, "bad exchange-plan arguments");
   const int np = nranks * parts_per_rank;
   const int64_t outer = fmt == MSREP_CSC ? n : m;
   std::vector<msrep_part_desc> parts((size_t)np);
-  TRY(msrep_plan(fmt, outer, nnz, np, ptr, coo_row, parts.data()));
+  TRY(msrep_plan_split(fmt, split, outer, nnz, np, ptr, coo_row, parts.data()));
   std::vector<int64_t> lo, hi;
   rank_segments(fmt, m, nranks, parts_per_rank, parts, lo, hi);
   for (int r = 0; r < nranks; r++) { seg_out[2 * r] = lo[(size_t)r]; seg_out[2 * r + 1] = hi[(size_t)r]; }
@@ -760,10 +799,12 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
       if (ptr[r + 1] < ptr[r]) return fail(MSREP_ERR_DIM_MISMATCH, "ptr decreases at %lld", (long long)r);
   }
   std::vector<msrep_part_desc> parts((size_t)c->np);
-  if (fmt == MSREP_COO) plan_coo(m, nnz, c->np, coo_row, parts.data());
-  else plan_ptr(outer, nnz, c->np, ptr, parts.data());
+  std::vector<int64_t> bnd;
+  split_bounds(fmt, c->split, outer, nnz, c->np, ptr, coo_row, bnd);
+  if (fmt == MSREP_COO) plan_coo(m, c->np, coo_row, bnd, parts.data());
+  else plan_ptr(outer, c->np, ptr, bnd, parts.data());
   const int P0 = c->rank * c->vparts, P1 = P0 + c->vparts;
-  const int64_t B_lo = boundary(P0, nnz, c->np), B_hi = boundary(P1, nnz, c->np);
+  const int64_t B_lo = bnd[(size_t)P0], B_hi = bnd[(size_t)P1];
   if (B_hi - B_lo >= kMaxRankNnz) return fail(MSREP_ERR_TOO_LARGE, "rank holds %lld nonzeros (>= 2^31 - 2^16)", (long long)(B_hi - B_lo));
   for (int64_t k = B_lo; k < B_hi; k++)
     if (idx[k] < 0 || idx[k] >= inner) return fail(MSREP_ERR_DIM_MISMATCH, "index %lld out of range", (long long)k);

@@ -32,21 +32,29 @@ constexpr int WARPS = MSREP_WARPS;   // warps per CTA (each with its own TMA rin
 //   the same layout (row ids rebased at pack time): the paper also runs its
 //   CSR kernel on COO input.
 // SLAB tile: [val x nnz][col x nnz] in natural order.
-// SELL tile (regular pCSR rows): SELL_ROWS consecutive rows, lane = row;
-//   element t of lane l sits at t * SELL_ROWS + l (sliced-ELL within the tile,
-//   W = longest row <= SELL_W_MAX, shorter rows padded with val 0 / col 0 and
-//   masked in the kernel); aux = the SELL_ROWS row lengths (uint16).  The host
-//   only forms a SELL tile when padding is <= 1/8 of its elements.
+// SELL tile (regular pCSR rows): 32*R consecutive rows, R in {1, 2, 4} rows per
+//   lane, lane l owning rows l, l+32, ... (R*W <= SELL_W_MAX); element t of
+//   the lane's k-th row sits at (t*R + k) * 32 + l (sliced-ELL within the tile,
+//   W = longest row, shorter rows padded with val 0 / col 0 and masked in the
+//   kernel); aux = the 32*R row lengths (uint16, lane-fastest).  R > 1 keeps
+//   tiles of short regular rows big (~1000 elements).  The host only forms a
+//   SELL tile when padding is <= 1/8 of its elements.
 enum TileKind { KIND_SEG = 0, KIND_SLAB = 2, KIND_SELL = 3 };
 constexpr int SELL_ROWS = 32;
-constexpr int SELL_W_MAX = 32;
+constexpr int SELL_W_MAX = 32;    // R * W per lane
+constexpr int SELL_R_MAX = 4;
 __host__ __device__ inline int align16(int b) { return (b + 15) & ~15; }
+// rows per lane of a SELL tile of `nrows` rows (1, 2 or 4)
+__host__ __device__ inline int sell_r(int nrows) { return nrows <= 32 ? 1 : (nrows <= 64 ? 2 : 4); }
 __host__ __device__ inline int blob_aux_bytes(int kind, int nrows, int nnz) {
-  return kind == KIND_SEG ? align16(nnz) : (kind == KIND_SELL ? SELL_ROWS * 2 : 0);
+  return kind == KIND_SEG ? align16(nnz) : (kind == KIND_SELL ? align16(sell_r(nrows) * 32 * 2) : 0);
 }
 // for KIND_SELL, `nnz` is the slice width W
 __host__ __device__ inline int blob_bytes(int kind, int nrows, int nnz, int vsize) {
-  if (kind == KIND_SELL) return SELL_ROWS * 2 + nnz * SELL_ROWS * (vsize + 4);
+  if (kind == KIND_SELL) {
+    const int r32 = sell_r(nrows) * 32;
+    return align16(r32 * 2) + nnz * r32 * (vsize + 4);
+  }
   return blob_aux_bytes(kind, nrows, nnz) + align16(nnz * vsize) + align16(nnz * 4);
 }
 // slot of element e (0 <= e < nnz) in a SEG tile's lane-chunked order

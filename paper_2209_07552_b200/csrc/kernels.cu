@@ -173,10 +173,56 @@ __device__ __forceinline__ void issue_blob(const char* blob, int4 d, int kind, i
 #define MSREP_ROW_MINB 2
 #endif
 template <typename VT>
-struct SStage { static constexpr int BYTES = SELL_ROWS * 2 + SELL_W_MAX * SELL_ROWS * ((int)sizeof(VT) + 4); };
+struct SStage { static constexpr int BYTES = SELL_R_MAX * 32 * 2 + SELL_W_MAX * SELL_ROWS * ((int)sizeof(VT) + 4); };
 template <typename VT, bool SELL>
 using RowLayout = WLayout<(SELL && SStage<VT>::BYTES > RStage<VT>::BYTES) ? SStage<VT>::BYTES : RStage<VT>::BYTES, 1,
                           MAX_TILE_ROWS * 8>;
+
+// One SELL tile with R rows per lane (internal.h): all R*W column indices are read from the
+// slot, then all R*W x gathers are in flight before the first FMA; padding is masked by the
+// row length, so results equal the plain row sums.
+template <typename VT, int R>
+__device__ __forceinline__ void sell_tile(const RowLaunch& P, const int4 d, const unsigned char* st, const int lane,
+                                          const VT* __restrict__ x, VT* __restrict__ y, double alpha, double beta) {
+  constexpr int V = (int)sizeof(VT);
+  constexpr int U = SELL_W_MAX;              // R*W <= U register slots per lane
+  const int nrows = d.z & 0xffff, W = d.z >> 16;
+  const uint16_t* lens = reinterpret_cast<const uint16_t*>(st);
+  const VT* sv = reinterpret_cast<const VT*>(st + align16(R * 32 * 2));
+  const uint32_t* sc = reinterpret_cast<const uint32_t*>(st + align16(R * 32 * 2) + W * R * 32 * V);
+  const int RW = R * W;
+  int mylen[R];
+  double yv[R];
+#pragma unroll
+  for (int k = 0; k < R; k++) {
+    const int row = k * 32 + lane;
+    mylen[k] = lens[k * 32 + lane];
+    yv[k] = (beta != 0.0 && row < nrows) ? (double)y[P.ybase + d.x + row] : 0.0;
+  }
+  uint32_t c[U];
+  VT xs[U];
+#pragma unroll
+  for (int u = 0; u < U; u++) c[u] = u < RW ? sc[u * 32 + lane] : 0u;   // no loop-carried state
+#pragma unroll
+  for (int u = 0; u < U; u++) xs[u] = u < RW ? ldg_ro(x + c[u]) : VT(0);
+  double acc[R];
+#pragma unroll
+  for (int k = 0; k < R; k++) acc[k] = 0.0;
+#pragma unroll
+  for (int u = 0; u < U; u++) {
+    const int k = u % R, t = u / R;           // compile-time after unrolling
+    if (u < RW && t < mylen[k]) acc[k] = fma((double)sv[u * 32 + lane], (double)xs[u], acc[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < R; k++) {
+    const int row = k * 32 + lane;
+    if (row < nrows) {
+      double o = alpha * acc[k];
+      if (beta != 0.0) o += beta * yv[k];
+      y[P.ybase + d.x + row] = (VT)o;
+    }
+  }
+}
 
 template <typename VT, bool SELL>
 __global__ void __launch_bounds__(WARPS * 32, MSREP_ROW_MINB) rows_kernel(const RowLaunch P) {
@@ -230,27 +276,11 @@ __global__ void __launch_bounds__(WARPS * 32, MSREP_ROW_MINB) rows_kernel(const 
     if (SELL && d.w == -2) {
       // ---- SELL tile (read in place; the slot is refilled after the tile)
       const int nrows = d.z & 0xffff, Wd = d.z >> 16;
-      const int mylen = reinterpret_cast<const uint16_t*>(st)[lane];
-      const VT* sv = reinterpret_cast<const VT*>(st + SELL_ROWS * 2);
-      const uint32_t* sc = reinterpret_cast<const uint32_t*>(st + SELL_ROWS * 2 + Wd * SELL_ROWS * V);
-      const int64_t yr = P.ybase + d.x + lane;
-      const bool live = lane < nrows;
-      const double yv = (beta != 0.0 && live) ? (double)y[yr] : 0.0;
-      uint32_t c[SELL_W_MAX];
-      VT xs[SELL_W_MAX];
-#pragma unroll
-      for (int u = 0; u < SELL_W_MAX; u++) c[u] = u < Wd ? sc[u * SELL_ROWS + lane] : 0u;   // no loop-carried state
-#pragma unroll
-      for (int u = 0; u < SELL_W_MAX; u++) xs[u] = u < Wd ? ldg_ro(x + c[u]) : VT(0);
-      double acc = 0.0;
-#pragma unroll
-      for (int u = 0; u < SELL_W_MAX; u++)
-        if (u < Wd && u < mylen) acc = fma((double)sv[u * SELL_ROWS + lane], (double)xs[u], acc);
-      if (live) {
-        double o = alpha * acc;
-        if (beta != 0.0) o += beta * yv;
-        y[yr] = (VT)o;
-      }
+      const int R = sell_r(nrows);
+      if (R == 1) sell_tile<VT, 1>(P, d, st, lane, x, y, alpha, beta);
+      else if (R == 2) sell_tile<VT, 2>(P, d, st, lane, x, y, alpha, beta);
+      else sell_tile<VT, 4>(P, d, st, lane, x, y, alpha, beta);
+      (void)Wd;
       __syncwarp();
       refill();
       continue;
@@ -572,18 +602,23 @@ __global__ void pack_kernel(const PackLaunch L) {
   const int4 d = L.tiles[t];
   const int nrows = d.z & 0xffff, nnz = d.z >> 16;
   char* b = L.blob + (int64_t)L.blob16[t] * 16;
-  if (d.w == -2) {   // SELL: lane = row, element u at u * SELL_ROWS + lane, padded with 0 / col 0
-    const int W = nnz;
-    const int rs = lane < nrows ? L.ptr[d.x + lane] : 0;
-    const int len = lane < nrows ? L.ptr[d.x + lane + 1] - rs : 0;
-    reinterpret_cast<uint16_t*>(b)[lane] = (uint16_t)len;
-    char* vb0 = b + SELL_ROWS * 2;
-    int* ix = reinterpret_cast<int*>(vb0 + W * SELL_ROWS * L.vsize);
-    for (int u = 0; u < W; u++) {
-      const bool on = u < len;
-      if (L.vsize == 8) reinterpret_cast<double*>(vb0)[u * SELL_ROWS + lane] = on ? static_cast<const double*>(L.val)[rs + u] : 0.0;
-      else reinterpret_cast<float*>(vb0)[u * SELL_ROWS + lane] = on ? static_cast<const float*>(L.val)[rs + u] : 0.0f;
-      ix[u * SELL_ROWS + lane] = on ? L.idx[rs + u] : 0;
+  if (d.w == -2) {   // SELL: lane l owns rows l + 32k (k < R); element t of row k at (t*R + k)*32 + l
+    const int W = nnz, R = sell_r(nrows);
+    uint16_t* lens = reinterpret_cast<uint16_t*>(b);
+    char* vb0 = b + align16(R * 32 * 2);
+    int* ix = reinterpret_cast<int*>(vb0 + W * R * 32 * L.vsize);
+    for (int k = 0; k < R; k++) {
+      const int row = k * 32 + lane;
+      const int rs = row < nrows ? L.ptr[d.x + row] : 0;
+      const int len = row < nrows ? L.ptr[d.x + row + 1] - rs : 0;
+      lens[k * 32 + lane] = (uint16_t)len;
+      for (int t = 0; t < W; t++) {
+        const bool on = t < len;
+        const int sl = (t * R + k) * 32 + lane;
+        if (L.vsize == 8) reinterpret_cast<double*>(vb0)[sl] = on ? static_cast<const double*>(L.val)[rs + t] : 0.0;
+        else reinterpret_cast<float*>(vb0)[sl] = on ? static_cast<const float*>(L.val)[rs + t] : 0.0f;
+        ix[sl] = on ? L.idx[rs + t] : 0;
+      }
     }
     return;
   }

@@ -109,3 +109,24 @@ def test_create_rejects_bad_args_without_device():
     with pytest.raises(M.MsrepError) as e:
         M.msrep_create(rank=2, nranks=2)
     assert e.value.status == 1
+
+
+def test_block_split_plan_bit_exact_vs_oracle():
+    """msrep_plan_split(BLOCK) (binary searches) == the oracle's Baseline row/column blocks
+    (linear scans) on random CSR / CSC / COO structures, including empty rows and np > m."""
+    import paper_2209_07552_b200 as M
+    rng = np.random.default_rng(23)
+    for trial in range(300):
+        m = int(rng.integers(0, 50)); np_ = int(rng.integers(1, 12))
+        lens = rng.integers(0, 7, m) * (rng.random(m) < 0.7)
+        ptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        nnz = int(ptr[-1])
+        ours = M.msrep_plan_split(M.CSR, M.SPLIT_BLOCK, m, nnz, np_, ptr=ptr)
+        ref = oracle.partition_ptr_b(ptr, oracle.block_boundaries(ptr, np_))
+        _parts_equal(ours, ref)
+        ours = M.msrep_plan_split(M.CSC, M.SPLIT_BLOCK, m, nnz, np_, ptr=ptr)
+        _parts_equal(ours, ref)
+        rows = oracle.csr_to_coo(m, ptr)
+        ours = M.msrep_plan_split(M.COO, M.SPLIT_BLOCK, m, nnz, np_, coo_row=rows)
+        refc = oracle.partition_coo_b(m, rows, oracle.block_boundaries_coo(m, rows, np_))
+        _parts_equal(ours, refc)

@@ -326,3 +326,41 @@ def test_csc_split_items_short_wide(parts):
     B = to_dtype(gen.kdistinct_csr(1000, 200_000, 300, seed=74), np.float32)
     xb = gen.vector(B["n"], 75, dtype=np.float32); yb = gen.vector(B["m"], 76, dtype=np.float32)
     check(B, "csc", xb, yb, 1.5, 0.5, parts=parts)
+
+
+# ------------------------------------------------ Baseline row/column-block split (NEXT f1)
+@pytest.mark.parametrize("fmt", FMTS)
+@pytest.mark.parametrize("parts", [2, 5, 8])
+def test_block_split_bit_exact(fmt, parts):
+    """The paper's Baseline split (whole row / column blocks) through the same kernels and
+    merge: bit-exact vs the oracle on integer R-MAT (heavy rows) and a two-class matrix."""
+    import paper_2209_07552_b200 as M
+    import torch
+    for A in (gen.rmat(11, seed=5, kind=gen.SMALLINT), gen.two_class(4000, 3000, 8, 4, 40, 0.1, kind=gen.SMALLINT)):
+        B = as_fmt(A, fmt)
+        x = gen.vector(A["n"], 81, kind=gen.SMALLINT); y = gen.vector(A["m"], 82, kind=gen.SMALLINT)
+        ctx = M.Context(0, 1, None, 0, parts)
+        if fmt == "coo":
+            ctx.partition("coo", B["m"], B["n"], idx=B["idx"], val=B["val"], coo_row=coo_of_csr(B), split="block")
+        else:
+            ctx.partition(fmt, B["m"], B["n"], ptr=B["ptr"], idx=B["idx"], val=B["val"], split="block")
+        assert (ctx.parts["start_flag"] == 0).all()
+        xd = torch.as_tensor(x).cuda(); yd = torch.as_tensor(y.copy()).cuda()
+        ctx.spmv(1.5, xd, 0.5, yd)
+        torch.cuda.synchronize()
+        assert np.array_equal(yd.cpu().numpy(), oracle_ref(A, x, y, 1.5, 0.5))
+        ctx.close()
+
+
+@pytest.mark.parametrize("k", [1, 3, 6, 8, 12, 16, 20])
+def test_sell_rows_per_lane(k):
+    """Regular short rows become SELL tiles with R = 4 / 2 / 1 rows per lane (R*W <= 32), incl.
+    ragged last tiles and a sprinkle of empty rows: bit-exact vs the oracle."""
+    A = gen.kdistinct_csr(32 * 4 * 7 + 45, 5000, k, seed=90 + k, kind=gen.SMALLINT)
+    x = gen.vector(A["n"], 91, kind=gen.SMALLINT); y = gen.vector(A["m"], 92, kind=gen.SMALLINT)
+    for parts in (1, 3):
+        check(A, "csr", x, y, 1.5, 0.5, parts=parts, exact=True)
+    # shorter rows mixed in (padding <= 1/8 may still hold or not): still exact
+    B = gen.two_class(32 * 4 * 9, 4000, 9, 4, k, 0.5, kind=gen.SMALLINT)
+    xb = gen.vector(B["n"], 93, kind=gen.SMALLINT); yb = gen.vector(B["m"], 94, kind=gen.SMALLINT)
+    check(B, "csr", xb, yb, 2.0, 0.5, parts=2, exact=True)

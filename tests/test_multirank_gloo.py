@@ -1,7 +1,8 @@
 """N>1 host logic on CPU: world_size-2/3 `gloo` process groups run the exchange
 step of msrep_spmv (Sec. 4.3; readings R6, R9, R10) with
 the library's own multi-rank plan (msrep_plan + msrep_exchange_plan, pure host)
-and the collectives the NCCL path issues, in the same shape:
+and the collectives the NCCL path issues, in the same shape, for both splits
+(msRep's nnz split and the paper's row/column-block Baseline):
 
   pCSR / pCOO  per-part pure partial sums (oracle, one part at a time, alpha=1, beta=0)
                -> all_gather of parts_per_rank head partials per rank (ncclAllGather)
@@ -15,6 +16,7 @@ Inputs are small integers with dyadic alpha/beta, so every summation order is
 exact and the result must equal the single-process oracle bit for bit.  The
 device kernels that produce the partial sums are covered by the GPU tests
 (virtual parts on one B200, tests/test_gpu_parity.py)."""
+import itertools
 import os
 import socket
 
@@ -52,7 +54,7 @@ def _cases():
     return out
 
 
-def _row_rank(rank, world, vparts, fmt, A, x, y_in):
+def _row_rank(rank, world, vparts, fmt, A, x, y_in, split):
     """One rank of the pCSR/pCOO exchange; returns its full replicated y."""
     import torch
     import torch.distributed as dist
@@ -63,11 +65,11 @@ def _row_rank(rank, world, vparts, fmt, A, x, y_in):
     np_ = world * vparts
     rows = oracle.csr_to_coo(m, ptr)
     if fmt == "csr":
-        parts = M.msrep_plan(M.CSR, m, nnz, np_, ptr=ptr)
-        seg, hrow, hpart = M.msrep_exchange_plan(M.CSR, m, n, nnz, world, vparts, ptr=ptr)
+        parts = M.msrep_plan_split(M.CSR, split, m, nnz, np_, ptr=ptr)
+        seg, hrow, hpart = M.msrep_exchange_plan(M.CSR, m, n, nnz, world, vparts, ptr=ptr, split=split)
     else:
-        parts = M.msrep_plan(M.COO, m, nnz, np_, coo_row=rows)
-        seg, hrow, hpart = M.msrep_exchange_plan(M.COO, m, n, nnz, world, vparts, coo_row=rows)
+        parts = M.msrep_plan_split(M.COO, split, m, nnz, np_, coo_row=rows)
+        seg, hrow, hpart = M.msrep_exchange_plan(M.COO, m, n, nnz, world, vparts, coo_row=rows, split=split)
     lo, hi = int(seg[rank, 0]), int(seg[rank, 1])
     acc = np.zeros(m, np.float64)
     head_local = np.zeros(vparts, np.float64)
@@ -109,7 +111,7 @@ def _row_rank(rank, world, vparts, fmt, A, x, y_in):
     return yt.numpy(), seg
 
 
-def _csc_rank(rank, world, vparts, A, x, y_in):
+def _csc_rank(rank, world, vparts, A, x, y_in, split):
     import torch
     import torch.distributed as dist
     import oracle
@@ -118,8 +120,8 @@ def _csc_rank(rank, world, vparts, A, x, y_in):
     cp, ri, cv = oracle.csr_to_csc(m, n, A["ptr"], A["idx"], A["val"])
     nnz = ri.size
     np_ = world * vparts
-    parts = M.msrep_plan(M.CSC, n, nnz, np_, ptr=cp)
-    seg, hrow, hpart = M.msrep_exchange_plan(M.CSC, m, n, nnz, world, vparts, ptr=cp)
+    parts = M.msrep_plan_split(M.CSC, split, n, nnz, np_, ptr=cp)
+    seg, hrow, hpart = M.msrep_exchange_plan(M.CSC, m, n, nnz, world, vparts, ptr=cp, split=split)
     assert (hrow == -1).all() and (hpart == -1).all()
     py = np.zeros(m, np.float64)
     for jl in range(vparts):
@@ -157,17 +159,16 @@ def _worker(rank, world, port, vparts_list, q):
             x = gen.vector(A["n"], 7, kind=gen.SMALLINT)
             y_in = gen.vector(A["m"], 8, kind=gen.SMALLINT)
             ref = oracle.spmv_csr(A["m"], A["ptr"], A["idx"], A["val"], x, y_in, ALPHA, BETA)
-            for vp in vparts_list:
-                for fmt in ("csr", "coo", "csc"):
-                    if fmt == "csc":
-                        y, seg = _csc_rank(rank, world, vp, A, x, y_in)
-                    else:
-                        y, seg = _row_rank(rank, world, vp, fmt, A, x, y_in)
-                    # segments tile [0, m) in rank order
-                    ok_tiles = seg[0, 0] == 0 and seg[-1, 1] == A["m"] and all(
-                        seg[r, 1] == seg[r + 1, 0] for r in range(world - 1))
-                    if not ok_tiles or not np.array_equal(y, ref):
-                        fails.append((name, fmt, vp, bool(ok_tiles)))
+            for vp, split, fmt in itertools.product(vparts_list, (0, 1), ("csr", "coo", "csc")):
+                if fmt == "csc":
+                    y, seg = _csc_rank(rank, world, vp, A, x, y_in, split)
+                else:
+                    y, seg = _row_rank(rank, world, vp, fmt, A, x, y_in, split)
+                # segments tile [0, m) in rank order
+                ok_tiles = seg[0, 0] == 0 and seg[-1, 1] == A["m"] and all(
+                    seg[r, 1] == seg[r + 1, 0] for r in range(world - 1))
+                if not ok_tiles or not np.array_equal(y, ref):
+                    fails.append((name, fmt, vp, split, bool(ok_tiles)))
     finally:
         dist.destroy_process_group()
     q.put((rank, fails))
