@@ -39,13 +39,15 @@ def parse():
     p.add_argument("--config", default="stencil",
                    choices=["stencil", "rmat", "tallskinny", "random1k"] +
                    [f"suite-{s}-{z}" for s in gen.SUITE_SHAPES for z in gen.SUITE_SIZES])
-    p.add_argument("--format", default=None, choices=["csr", "coo", "csc"])
+    p.add_argument("--format", default=None, choices=["csr", "coo", "csc", "coo_col"])
     p.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     p.add_argument("--layout", default=None, choices=["replicated", "owned", "sharded"])
     p.add_argument("--e2e-steps", type=int, default=50)
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--parts-per-rank", type=int, default=1)
+    p.add_argument("--split", default="nnz", choices=["nnz", "block"],
+                   help="nnz: msRep's nnz-balanced split; block: the paper's row/column-block Baseline")
     a = p.parse_args()
     if a.format is None:
         a.format = "csc" if a.config == "tallskinny" else "csr"
@@ -66,9 +68,10 @@ def load_peaks():
 def build_matrix(a):
     """Synthetic matrix of the named config (gen/, seeded): CSR, or CSC for pCSC."""
     A = gen.make_config(a.config)
-    if a.format == "csc" and A["fmt"] == "csr":
+    colwise = a.format in ("csc", "coo_col")
+    if colwise and A["fmt"] == "csr":
         A = gen.transpose(A)
-    if a.format != "csc" and A["fmt"] == "csc":
+    if not colwise and A["fmt"] == "csc":
         A = gen.transpose(A)
     if a.dtype == "f32":
         A["val"] = A["val"].astype(np.float32)
@@ -214,15 +217,16 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     A = build_matrix(a)
-    fmt = {"csr": M.CSR, "coo": M.COO, "csc": M.CSC}[a.format]
+    fmt = M.FORMATS[a.format]
     layout = {"replicated": M.Y_REPLICATED, "owned": M.Y_OWNED, "sharded": M.Y_SHARDED}[a.layout]
     if world > 1:
         ctx = M.Context.from_torch_dist(device=local, parts_per_rank=a.parts_per_rank)
     else:
         ctx = M.Context(0, 1, None, local, a.parts_per_rank)
-    coo_row = gen.expand_rows(A) if a.format == "coo" else None
-    ctx.partition(a.format, A["m"], A["n"], ptr=None if a.format == "coo" else A["ptr"], idx=A["idx"], val=A["val"],
-                  coo_row=coo_row)
+    coo = a.format in ("coo", "coo_col")   # COO views carry their sorted major index (rows / columns)
+    coo_row = gen.expand_rows(A) if coo else None
+    ctx.partition(a.format, A["m"], A["n"], ptr=None if coo else A["ptr"], idx=A["idx"], val=A["val"],
+                  coo_row=coo_row, split=a.split)
     del coo_row
     st = ctx.stats()
     vdt = A["val"].dtype
@@ -291,7 +295,7 @@ def main():
 
     # roofline of the dominant kernel (per rank 0's launch; algorithmic bytes / event-timed duration)
     hbm_peak, peak_kind = load_peaks()
-    kname = "csc_band_kernel" if a.format == "csc" else "rows_kernel"
+    kname = "csc_band_kernel" if a.format in ("csc", "coo_col") else "rows_kernel"
     traffic = None
     try:   # DRAM bytes per launch of that kernel from a committed `ncu --set full` capture (profiles/)
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
@@ -315,7 +319,7 @@ def main():
             "vs_baseline": None, "dtype": a.dtype, "data": "synthetic (gen/, seeded; no SuiteSparse offline)",
             "config": {"workload": workload_name(a, A), "format": "p" + a.format.upper(), "layout": a.layout,
                        "m": A["m"], "n": A["n"], "nnz": A.nnz, "alpha": ALPHA, "beta": BETA,
-                       "parts_per_rank": a.parts_per_rank,
+                       "parts_per_rank": a.parts_per_rank, "split": a.split,
                        "l2": "no flush: per-step matrix bytes exceed the 126 MB L2 (inputs larger than L2); "
                              "x stays L2-resident across steps as in an iterative solver",
                        "parallelism": f"nnz-balanced dp{world}"},

@@ -167,9 +167,10 @@ def transpose(A: Sparse) -> Sparse:
 
 
 def expand_rows(A: Sparse) -> np.ndarray:
-    """Row index per nonzero (row-sorted COO view of a CSR matrix)."""
+    """Major index per nonzero: the row of each nonzero of a CSR matrix (row-sorted COO view),
+    or the column of each nonzero of a CSC matrix (column-sorted COO view)."""
     out = np.empty(max(A.nnz, 1), np.int32)[:A.nnz]
-    lib().gen_expand_ptr(A["m"], _p(A["ptr"]), _p(out))
+    lib().gen_expand_ptr(A["ptr"].size - 1, _p(A["ptr"]), _p(out))
     return out
 
 

@@ -40,8 +40,12 @@ typedef struct msrep_ctx_s* msrep_ctx;
 
 /* Storage format of the caller's global matrix (Sec. 2.1).
  * MSREP_COO must be sorted by row (ties by column), "we assume the elements
- * are sorted by rows"; otherwise MSREP_ERR_UNSORTED_COO. */
-typedef enum { MSREP_CSR = 0, MSREP_CSC = 1, MSREP_COO = 2 } msrep_format;
+ * are sorted by rows"; otherwise MSREP_ERR_UNSORTED_COO.
+ * MSREP_COO_COL is a COO sorted by column (ties by row), the variant the paper
+ * describes and defers (merged "like pCSC", P:597 Fig. col-gather):
+ * Alg. 6 runs on the column ids, parts own column ranges, partial y vectors
+ * are summed (reduce-scatter).  It uses the pCSC kernel. */
+typedef enum { MSREP_CSR = 0, MSREP_CSC = 1, MSREP_COO = 2, MSREP_COO_COL = 3 } msrep_format;
 
 typedef enum { MSREP_F64 = 0, MSREP_F32 = 1 } msrep_dtype;
 
@@ -133,6 +137,8 @@ msrep_status_t msrep_create(msrep_ctx* out, int rank, int nranks, const uint8_t 
  *   CSR: ptr = row_ptr[m+1], idx = col_idx[nnz], coo_row = NULL
  *   CSC: ptr = col_ptr[n+1], idx = row_idx[nnz], coo_row = NULL
  *   COO: ptr = NULL,         idx = col_idx[nnz], coo_row = row_idx[nnz] (row-sorted)
+ *   COO_COL: ptr = NULL,     idx = row_idx[nnz], coo_row = col_idx[nnz] (column-sorted:
+ *            coo_row carries the sorted major index)
  *   val = [nnz] of dtype.
  * All host arrays are borrowed read-only for the duration of the call (the
  * call synchronises `stream` before returning).  parts_out, if not NULL,

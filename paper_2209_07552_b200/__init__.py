@@ -23,7 +23,7 @@ if not os.path.exists(LIB_PATH):
 _lib = ctypes.CDLL(LIB_PATH)
 
 # enums (include/msrep.h)
-CSR, CSC, COO = 0, 1, 2
+CSR, CSC, COO, COO_COL = 0, 1, 2, 3
 SPLIT_NNZ, SPLIT_BLOCK = 0, 1
 SPLITS = {"nnz": SPLIT_NNZ, "block": SPLIT_BLOCK}
 F64, F32 = 0, 1
@@ -31,7 +31,7 @@ Y_REPLICATED, Y_OWNED, Y_SHARDED = 0, 1, 2
 STATUS = {0: "MSREP_OK", 1: "MSREP_ERR_INVALID_ARG", 2: "MSREP_ERR_DIM_MISMATCH", 3: "MSREP_ERR_UNSORTED_COO",
           4: "MSREP_ERR_TOO_LARGE", 5: "MSREP_ERR_STATE", 6: "MSREP_ERR_OOM", 7: "MSREP_ERR_CUDA",
           8: "MSREP_ERR_NCCL"}
-FORMATS = {"csr": CSR, "csc": CSC, "coo": COO}
+FORMATS = {"csr": CSR, "csc": CSC, "coo": COO, "coo_col": COO_COL}
 
 
 class PartDesc(ctypes.Structure):

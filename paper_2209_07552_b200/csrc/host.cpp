@@ -58,6 +58,11 @@ msrep_status_t fail(msrep_status_t s, const char* fmt, ...) {
   } while (0)
 
 constexpr int64_t kMaxIdx = (int64_t)1 << 31;
+
+// column-wise formats merge partial y vectors (pCSC, column-sorted pCOO); COO formats carry
+// their sorted major index (row ids, or column ids for MSREP_COO_COL) in `coo_row`
+inline bool colwise(msrep_format f) { return f == MSREP_CSC || f == MSREP_COO_COL; }
+inline bool coo_like(msrep_format f) { return f == MSREP_COO || f == MSREP_COO_COL; }
 constexpr int64_t kMaxRankNnz = kMaxIdx - (1 << 16);
 
 // ------------------------------------------------------------ descriptors
@@ -69,7 +74,7 @@ void split_bounds(msrep_format fmt, msrep_split split, int64_t outer, int64_t nn
   b.resize((size_t)np + 1);
   for (int i = 0; i <= np; i++) {
     if (split == MSREP_SPLIT_NNZ) b[(size_t)i] = ((int64_t)i * nnz) / np;
-    else if (fmt == MSREP_COO) {
+    else if (coo_like(fmt)) {
       const int64_t r = ((int64_t)i * outer) / np;
       b[(size_t)i] = (int64_t)(std::lower_bound(row, row + nnz, (int32_t)std::min<int64_t>(r, INT32_MAX)) - row);
     } else b[(size_t)i] = ptr[((int64_t)i * outer) / np];
@@ -170,6 +175,10 @@ struct Ctx {
   char* d_cblob = nullptr;
   int64_t cnb = 0, citems = 0;
   bool csplit = false;
+  int4* d_cunits = nullptr;
+  int32_t* d_item_hst = nullptr;
+  int32_t* d_item_hw = nullptr;
+  int64_t cunits = 0;
   int nheads_local = 0;
 
   // host-vector path buffers
@@ -333,7 +342,7 @@ void rank_segments(msrep_format fmt, int64_t m, int nranks, int vparts, const st
   hi.resize((size_t)nranks);
   const int64_t shard = (m + nranks - 1) / nranks;
   for (int r = 0; r < nranks; r++) {
-    if (fmt == MSREP_CSC) {
+    if (colwise(fmt)) {
       lo[(size_t)r] = std::min<int64_t>(m, (int64_t)r * shard);
       hi[(size_t)r] = std::min<int64_t>(m, (int64_t)(r + 1) * shard);
     } else {
@@ -411,7 +420,10 @@ void build_row_schedule(const Ctx& c, const std::vector<int64_t>& lp, Schedule& 
 struct CscBands {
   int64_t nb = 0, nch = 1, bytes = 0;     // bands, column chunks, blob bytes
   int64_t chunk = CB_CHUNK;               // columns per chunk
-  bool split_items = false;               // few bands: items are the units of work
+  bool split_items = false;               // split mode: stage ranges of items are the units of work
+  std::vector<int4> units;                // split mode: {band, first stage, end stage, 0} (band stage order)
+  std::vector<int32_t> item_hst;          // [items]: stages that may hold same-row groups
+  std::vector<int32_t> item_hw;           // [items * CB_W]: same-row groups leading each warp list
   std::vector<int4> items;                // {band, nstages, window col base, last-stage seg}
   std::vector<int64_t> item_off;          // byte offset of each item's blob
   std::vector<int32_t> band_item;         // [nb + 1]
@@ -419,43 +431,109 @@ struct CscBands {
   std::unique_ptr<char[]> blob;
 };
 
-// Greedy group arrangement of one warp list (entries [0, n) of pk/val, CSC
-// order): emits groups of 32 with distinct rows (pk & (CB_ROWS-1)); an entry
-// whose row is already in the open group waits in `pend` for a later group.
-// A group that cannot be filled while entries remain is closed with holes.
-// emit(pos, e) receives every output position with its entry (e < 0: hole).
-// Returns the arranged length.
+// Group arrangement of one warp list (entries [0, n) of pk/val, CSC order).
+// Rows with more entries than the greedy pass has groups first emit full SAME-ROW groups (32
+// entries of one row; the kernel detects them and adds one warp-reduced sum),
+// the rest go through a greedy pass that emits groups of 32 DISTINCT rows
+// (pk & (CB_ROWS-1)); an entry whose row is already in the open group waits in
+// `pend` for a later group, and a group that cannot be filled while entries
+// remain is closed with holes.  emit(pos, e) receives every output position
+// with its entry (e < 0: hole).  Returns the arranged length.
+struct ArrangeScratch {
+  int64_t same = 0;   // entries the last arrange_list placed in same-row groups
+  std::vector<int64_t> pend, rest;
+  std::vector<int> rows;
+  std::vector<uint64_t> used;
+  std::vector<int32_t> cnt, taken;
+};
+
 template <class Emit>
-int64_t arrange_list(const uint32_t* pk, int64_t n, std::vector<int64_t>& pend, std::vector<uint64_t>& used,
-                     Emit&& emit) {
-  pend.clear();
-  used.assign(CB_ROWS / 64, 0);
-  int64_t next = 0, w = 0;
+int64_t arrange_list(const uint32_t* pk, int64_t n, ArrangeScratch& A, Emit&& emit) {
+  auto rowof = [&](int64_t e) { return (int)(pk[e] & (CB_ROWS - 1)); };
+  if (A.cnt.size() != (size_t)CB_ROWS) { A.cnt.assign(CB_ROWS, 0); A.taken.assign(CB_ROWS, 0); }   // zero between lists
+  A.rows.clear();
+  for (int64_t e = 0; e < n; e++)
+    if (A.cnt[(size_t)rowof(e)]++ == 0) A.rows.push_back(rowof(e));
+  // A row forces holes in the greedy pass iff it has more entries than the pass has groups
+  // (G = remaining entries / 32).  Such "heavy" rows move their full 32-blocks into same-row
+  // groups; G shrinks as they leave, so iterate to a fixed point.
+  int64_t G = n / 32;
+  for (int it = 0; it < 8; it++) {
+    int64_t H = 0;
+    for (int r : A.rows)
+      if (A.cnt[(size_t)r] > std::max<int64_t>(G, 31)) H += A.cnt[(size_t)r] / 32 * 32;
+    const int64_t G2 = (n - H) / 32;
+    if (G2 == G) break;
+    G = G2;
+  }
+  const int64_t heavy_min = std::max<int64_t>(G, 31) + 1;
+  auto nheavy = [&](int r) -> int64_t { return A.cnt[(size_t)r] >= heavy_min ? A.cnt[(size_t)r] / 32 * 32 : 0; };
+  int64_t w = 0;
+  // 1. same-row groups: the first 32*floor(cnt/32) entries of every heavy row, in list order
+  A.rest.clear();
+  for (int64_t e = 0; e < n; e++) {
+    const int r = rowof(e);
+    if (A.taken[(size_t)r] < nheavy(r)) A.taken[(size_t)r]++;
+    else A.rest.push_back(e);
+  }
+  for (int64_t e = 0; e < n; e++) A.taken[(size_t)rowof(e)] = 0;
+  {
+    // emit heavy entries row by row (rows in first-appearance order, entries in list order),
+    // 32 per group: one stable bucket pass
+    std::vector<int64_t> order, heavy;
+    std::vector<int64_t> start;
+    for (int64_t e = 0; e < n; e++) {
+      const int r = rowof(e);
+      if (nheavy(r) > 0 && A.taken[(size_t)r] == 0) {
+        A.taken[(size_t)r] = 1 + (int32_t)order.size();   // 1-based slot of the row
+        order.push_back(r);
+      }
+    }
+    start.assign(order.size() + 1, 0);
+    for (size_t k = 0; k < order.size(); k++) start[k + 1] = start[k] + nheavy((int)order[k]);
+    heavy.assign((size_t)start.back(), 0);
+    std::vector<int64_t> fill(start.begin(), start.end() - 1);
+    for (int64_t e = 0; e < n; e++) {
+      const int r = rowof(e);
+      if (nheavy(r) == 0) continue;
+      const size_t k = (size_t)A.taken[(size_t)r] - 1;
+      if (fill[k] < start[k + 1]) heavy[(size_t)fill[k]++] = e;
+    }
+    for (int64_t e : heavy) emit(w++, e);
+    A.same = (int64_t)heavy.size();
+    for (int r : order) A.taken[(size_t)r] = 0;
+  }
+  // 2. greedy distinct-row groups over the remaining entries
+  A.pend.clear();
+  if (A.used.size() != (size_t)(CB_ROWS / 64)) A.used.assign(CB_ROWS / 64, 0);   // cleared per group
+  int64_t next = 0;
+  const int64_t nr = (int64_t)A.rest.size();
   uint32_t grp[32];
-  while (next < n || !pend.empty()) {
+  while (next < nr || !A.pend.empty()) {
     int g = 0;
-    auto busy = [&](int64_t e) { const uint32_t r = pk[e] & (CB_ROWS - 1); return (used[r >> 6] >> (r & 63)) & 1; };
+    auto busy = [&](int64_t e) { const uint32_t r = (uint32_t)rowof(e); return (A.used[r >> 6] >> (r & 63)) & 1; };
     auto take = [&](int64_t e) {
-      const uint32_t r = pk[e] & (CB_ROWS - 1);
-      used[r >> 6] |= 1ull << (r & 63);
+      const uint32_t r = (uint32_t)rowof(e);
+      A.used[r >> 6] |= 1ull << (r & 63);
       grp[g++] = r;
       emit(w++, e);
     };
     size_t keep = 0;
-    for (size_t k = 0; k < pend.size(); k++) {   // deferred entries first, order kept
-      const int64_t e = pend[k];
-      if (g < 32 && !busy(e)) take(e); else pend[keep++] = e;
+    for (size_t k = 0; k < A.pend.size(); k++) {   // deferred entries first, order kept
+      const int64_t e = A.pend[k];
+      if (g < 32 && !busy(e)) take(e); else A.pend[keep++] = e;
     }
-    pend.resize(keep);
-    while (g < 32 && next < n) {
-      const int64_t e = next++;
-      if (busy(e)) pend.push_back(e); else take(e);
+    A.pend.resize(keep);
+    while (g < 32 && next < nr) {
+      const int64_t e = A.rest[(size_t)next++];
+      if (busy(e)) A.pend.push_back(e); else take(e);
     }
     const int real = g;
-    if (g < 32 && (next < n || !pend.empty()))   // close the group with holes
+    if (g < 32 && (next < nr || !A.pend.empty()))   // close the group with holes
       for (; g < 32; g++) emit(w++, -1);
-    for (int k = 0; k < real; k++) used[grp[k] >> 6] &= ~(1ull << (grp[k] & 63));
+    for (int k = 0; k < real; k++) A.used[grp[k] >> 6] &= ~(1ull << (grp[k] & 63));
   }
+  for (int r : A.rows) A.cnt[(size_t)r] = 0;   // leave the scratch zero
   return w;
 }
 
@@ -470,8 +548,7 @@ msrep_status_t build_csc_bands(const Ctx& c, const std::vector<int64_t>& lp, con
   // short-wide matrices have fewer bands than SMs: cut the columns into more chunks and let
   // every (band, chunk) item be a unit of work whose partial band is added into py
   const int64_t units = 2 * (int64_t)sms;
-  if (B.nb < units && W > 0) {
-    B.split_items = true;
+  if (B.nb < (int64_t)sms && W > 0) {
     B.nch = std::max(B.nch, std::min<int64_t>((units + B.nb - 1) / B.nb, std::max<int64_t>(1, W / 4096)));
   }
   B.chunk = std::max<int64_t>(1, (W + B.nch - 1) / B.nch);
@@ -559,21 +636,22 @@ msrep_status_t build_csc_bands(const Ctx& c, const std::vector<int64_t>& lp, con
   std::atomic<int64_t> next_key{0};
   auto each_key = [&](auto&& f) {
     run([&](int) {
-      std::vector<int64_t> pend;
-      std::vector<uint64_t> used;
+      ArrangeScratch scratch;
       for (;;) {
         const int64_t k0 = next_key.fetch_add(64);
         if (k0 >= keys) break;
-        for (int64_t k = k0; k < std::min(keys, k0 + 64); k++) f(k, pend, used);
+        for (int64_t k = k0; k < std::min(keys, k0 + 64); k++) f(k, scratch);
       }
     });
     next_key = 0;
   };
   // 2. arranged length of every list (holes included)
-  std::vector<int64_t> alen((size_t)keys, 0);
-  each_key([&](int64_t k, std::vector<int64_t>& pend, std::vector<uint64_t>& used) {
+  std::vector<int64_t> alen((size_t)keys, 0), asame((size_t)keys, 0);
+  each_key([&](int64_t k, ArrangeScratch& scr) {
     const int64_t b0 = kbeg[(size_t)k], n = kbeg[(size_t)k + 1] - b0;
-    alen[(size_t)k] = n ? arrange_list(tpk.get() + b0, n, pend, used, [](int64_t, int64_t) {}) : 0;
+    scr.same = 0;
+    alen[(size_t)k] = n ? arrange_list(tpk.get() + b0, n, scr, [](int64_t, int64_t) {}) : 0;
+    asame[(size_t)k] = scr.same;
   });
   // 3. items: one per non-empty (band, chunk); stage geometry and blob offsets
   B.band_item.assign((size_t)B.nb + 1, 0);
@@ -583,9 +661,14 @@ msrep_status_t build_csc_bands(const Ctx& c, const std::vector<int64_t>& lp, con
     B.band_item[(size_t)b] = (int32_t)B.items.size();
     for (int64_t ch = 0; ch < B.nch; ch++) {
       const int64_t k0 = (b * B.nch + ch) * CB_W;
-      int64_t L = 0;
-      for (int w = 0; w < CB_W; w++) L = std::max(L, alen[(size_t)(k0 + w)]);
+      int64_t L = 0, H = 0;
+      for (int w = 0; w < CB_W; w++) {
+        L = std::max(L, alen[(size_t)(k0 + w)]);
+        H = std::max(H, asame[(size_t)(k0 + w)]);
+      }
       if (L == 0) continue;
+      B.item_hst.push_back((int32_t)((H + CB_SEG - 1) / CB_SEG));
+      for (int w = 0; w < CB_W; w++) B.item_hw.push_back((int32_t)(asame[(size_t)(k0 + w)] / 32));
       const int64_t nst = (L + CB_SEG - 1) / CB_SEG;
       const int64_t last = ((L - (nst - 1) * CB_SEG) + 3) & ~(int64_t)3;
       if (nst >= ((int64_t)1 << 31)) return fail(MSREP_ERR_TOO_LARGE, "pCSC warp list too long");
@@ -597,9 +680,29 @@ msrep_status_t build_csc_bands(const Ctx& c, const std::vector<int64_t>& lp, con
   }
   B.band_item[(size_t)B.nb] = (int32_t)B.items.size();
   B.bytes = bytes;
+  // split mode: few bands, or a band much heavier than one SM's share -> units = stage ranges
+  {
+    int64_t tot = 0, heaviest = 0;
+    for (int64_t b = 0; b < B.nb; b++) {
+      int64_t st = 0;
+      for (int32_t i = B.band_item[(size_t)b]; i < B.band_item[(size_t)b + 1]; i++) st += B.items[(size_t)i].y;
+      tot += st;
+      heaviest = std::max(heaviest, st);
+    }
+    B.split_items = B.nb < (int64_t)sms || heaviest * sms > 2 * tot;
+    if (B.split_items) {   // units: stage ranges of a band (across its items), >= 64 stages
+      const int64_t per = std::max<int64_t>(32, (tot + 4 * (int64_t)sms - 1) / (4 * (int64_t)sms));
+      for (int64_t b = 0; b < B.nb; b++) {
+        int64_t st = 0;
+        for (int32_t i = B.band_item[(size_t)b]; i < B.band_item[(size_t)b + 1]; i++) st += B.items[(size_t)i].y;
+        for (int64_t sb = 0; sb < st; sb += per)
+          B.units.push_back(make_int4((int32_t)b, (int32_t)sb, (int32_t)std::min<int64_t>(st, sb + per), 0));
+      }
+    }
+  }
   B.blob.reset(new char[(size_t)std::max<int64_t>(16, bytes)]);
   // 4. write every list into its item's stage blobs; pad it with holes to the item's length
-  each_key([&](int64_t k, std::vector<int64_t>& pend, std::vector<uint64_t>& used) {
+  each_key([&](int64_t k, ArrangeScratch& scr) {
     const int64_t it = key_item[(size_t)(k / CB_W)];
     if (it < 0) return;
     const int w = (int)(k % CB_W);
@@ -616,7 +719,7 @@ msrep_status_t build_csc_bands(const Ctx& c, const std::vector<int64_t>& lp, con
       if (e >= 0) { *pkp = tpk[(size_t)(b0 + e)]; memcpy(st + slot * (int64_t)V, tval.get() + (size_t)(b0 + e) * V, V); }
       else { *pkp = CB_HOLE; memset(st + slot * (int64_t)V, 0, V); }
     };
-    int64_t pos = n ? arrange_list(tpk.get() + b0, n, pend, used, put) : 0;
+    int64_t pos = n ? arrange_list(tpk.get() + b0, n, scr, put) : 0;
     for (; pos < L; pos++) put(pos, -1);
   });
   return MSREP_OK;
@@ -674,8 +777,8 @@ msrep_status_t msrep_plan_split(msrep_format fmt, msrep_split split, int64_t out
   if (np < 1 || outer < 0 || nnz < 0 || !parts_out) return fail(MSREP_ERR_INVALID_ARG, "bad plan arguments");
   if (split != MSREP_SPLIT_NNZ && split != MSREP_SPLIT_BLOCK) return fail(MSREP_ERR_INVALID_ARG, "unknown split %d", (int)split);
   std::vector<int64_t> b;
-  if (fmt == MSREP_COO) {
-    if (nnz > 0 && !coo_row) return fail(MSREP_ERR_INVALID_ARG, "COO plan needs row_idx");
+  if (coo_like(fmt)) {
+    if (nnz > 0 && !coo_row) return fail(MSREP_ERR_INVALID_ARG, "COO plan needs its sorted major index");
     split_bounds(fmt, split, outer, nnz, np, nullptr, coo_row, b);
     plan_coo(outer, np, coo_row, b, parts_out);
   } else if (fmt == MSREP_CSR || fmt == MSREP_CSC) {
@@ -707,7 +810,7 @@ msrep_status_t msrep_exchange_plan(msrep_format fmt, msrep_split split, int64_t 
   if (nranks < 1 || parts_per_rank < 1 || m < 0 || n < 0 || nnz < 0 || !seg_out)
     return fail(MSREP_ERR_INVALID_ARG, "bad exchange-plan arguments");
   const int np = nranks * parts_per_rank;
-  const int64_t outer = fmt == MSREP_CSC ? n : m;
+  const int64_t outer = colwise(fmt) ? n : m;
   std::vector<msrep_part_desc> parts((size_t)np);
   TRY(msrep_plan_split(fmt, split, outer, nnz, np, ptr, coo_row, parts.data()));
   std::vector<int64_t> lo, hi;
@@ -715,7 +818,7 @@ msrep_status_t msrep_exchange_plan(msrep_format fmt, msrep_split split, int64_t 
   for (int r = 0; r < nranks; r++) { seg_out[2 * r] = lo[(size_t)r]; seg_out[2 * r + 1] = hi[(size_t)r]; }
   std::vector<int64_t> hrow((size_t)np, -1);
   std::vector<int32_t> hpart((size_t)np, -1);
-  if (fmt != MSREP_CSC) {
+  if (!colwise(fmt)) {
     std::vector<int32_t> chain;
     for (int j = 0; j < np; j++) {
       tail_chain(parts, j, chain);
@@ -779,18 +882,20 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const auto t0 = std::chrono::steady_clock::now();
   // ---- validation (before any device work)
-  if (fmt != MSREP_CSR && fmt != MSREP_CSC && fmt != MSREP_COO) return fail(MSREP_ERR_INVALID_ARG, "format %d", (int)fmt);
+  if (fmt != MSREP_CSR && fmt != MSREP_CSC && fmt != MSREP_COO && fmt != MSREP_COO_COL)
+    return fail(MSREP_ERR_INVALID_ARG, "format %d", (int)fmt);
   if (dtype != MSREP_F64 && dtype != MSREP_F32) return fail(MSREP_ERR_INVALID_ARG, "dtype %d", (int)dtype);
   if (m < 0 || n < 0 || nnz < 0) return fail(MSREP_ERR_INVALID_ARG, "negative dimension");
   if (m >= kMaxIdx || n >= kMaxIdx) return fail(MSREP_ERR_TOO_LARGE, "m, n must be < 2^31");
   if (nnz > 0 && (!idx || !val)) return fail(MSREP_ERR_INVALID_ARG, "idx/val NULL");
-  const int64_t outer = fmt == MSREP_CSC ? n : m, inner = fmt == MSREP_CSC ? m : n;
-  if (fmt == MSREP_COO) {
-    if (nnz > 0 && !coo_row) return fail(MSREP_ERR_INVALID_ARG, "COO needs coo_row");
+  const int64_t outer = colwise(fmt) ? n : m, inner = colwise(fmt) ? m : n;
+  if (coo_like(fmt)) {
+    if (nnz > 0 && !coo_row) return fail(MSREP_ERR_INVALID_ARG, "COO needs its sorted major index (coo_row)");
+    const char* what = fmt == MSREP_COO ? "(row, col)" : "(col, row)";
     for (int64_t k = 0; k < nnz; k++) {
-      if (coo_row[k] < 0 || coo_row[k] >= m) return fail(MSREP_ERR_DIM_MISMATCH, "row_idx[%lld] out of range", (long long)k);
+      if (coo_row[k] < 0 || coo_row[k] >= outer) return fail(MSREP_ERR_DIM_MISMATCH, "major index [%lld] out of range", (long long)k);
       if (k > 0 && (coo_row[k] < coo_row[k - 1] || (coo_row[k] == coo_row[k - 1] && idx[k] < idx[k - 1])))
-        return fail(MSREP_ERR_UNSORTED_COO, "COO not sorted by (row, col) at %lld", (long long)k);
+        return fail(MSREP_ERR_UNSORTED_COO, "COO not sorted by %s at %lld", what, (long long)k);
     }
   } else {
     if (!ptr) return fail(MSREP_ERR_INVALID_ARG, "ptr NULL");
@@ -801,7 +906,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   std::vector<msrep_part_desc> parts((size_t)c->np);
   std::vector<int64_t> bnd;
   split_bounds(fmt, c->split, outer, nnz, c->np, ptr, coo_row, bnd);
-  if (fmt == MSREP_COO) plan_coo(m, c->np, coo_row, bnd, parts.data());
+  if (coo_like(fmt)) plan_coo(outer, c->np, coo_row, bnd, parts.data());
   else plan_ptr(outer, c->np, ptr, bnd, parts.data());
   const int P0 = c->rank * c->vparts, P1 = P0 + c->vparts;
   const int64_t B_lo = bnd[(size_t)P0], B_hi = bnd[(size_t)P1];
@@ -822,7 +927,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   // ---- window and local pointer (clamped form of Alg. 2 l.11-12, reading R5)
   const size_t V = vsz(dtype);
   std::vector<int64_t> lp;
-  if (fmt == MSREP_CSC) {
+  if (colwise(fmt)) {
     int64_t lo = -1, hi = -1;
     for (int j = P0; j < P1; j++) {
       if (parts[(size_t)j].start_idx > parts[(size_t)j].end_idx) continue;
@@ -846,7 +951,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   }
   const int64_t W = c->whi - c->wlo;
   lp.resize((size_t)W + 1);
-  if (fmt == MSREP_COO) {
+  if (coo_like(fmt)) {
     std::fill(lp.begin(), lp.end(), 0);
     for (int64_t k = B_lo; k < B_hi; k++) lp[(size_t)(coo_row[k] - c->wlo) + 1]++;
     for (int64_t w = 0; w < W; w++) lp[(size_t)w + 1] += lp[(size_t)w];
@@ -858,7 +963,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   }
 
   const int64_t nz_r = B_hi - B_lo;
-  if (fmt == MSREP_CSC) {
+  if (colwise(fmt)) {
     // ---- pCSC: row-band layout built on the host threads, uploaded once
     CscBands CB;
     int sms = 148;
@@ -866,6 +971,10 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     TRY(build_csc_bands(*c, lp, idx, val, V, sms, CB));
     c->csplit = CB.split_items;
     TRY(upload_vec(c, CB.items, &c->d_citems, s));
+    TRY(upload_vec(c, CB.units, &c->d_cunits, s));
+    TRY(upload_vec(c, CB.item_hst, &c->d_item_hst, s));
+    TRY(upload_vec(c, CB.item_hw, &c->d_item_hw, s));
+    c->cunits = (int64_t)CB.units.size();
     TRY(upload_vec(c, CB.item_off, &c->d_item_off, s));
     TRY(upload_vec(c, CB.band_item, &c->d_band_item, s));
     TRY(upload_vec(c, CB.split, &c->d_split, s));
@@ -967,10 +1076,10 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   st.nparts = c->np; st.nranks = c->nranks; st.parts_per_rank = c->vparts;
   st.nnz_rank = nz_r;
   st.rows_window = W;
-  st.ntiles = fmt == MSREP_CSC ? c->citems : c->ntiles; st.nsell = c->nsell; st.nslabs = c->nslabs; st.nsplit_rows = c->nsplit; st.nheads_local = c->nheads_local;
+  st.ntiles = colwise(fmt) ? c->citems : c->ntiles; st.nsell = c->nsell; st.nslabs = c->nslabs; st.nsplit_rows = c->nsplit; st.nheads_local = c->nheads_local;
   st.partition_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
   int64_t X = 0;
-  if (fmt == MSREP_CSC) {
+  if (colwise(fmt)) {
     X = W;   // pCSC reads x only over its column window
   } else {
     std::vector<uint64_t> bits((size_t)(inner + 63) / 64, 0);
@@ -980,12 +1089,13 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   st.distinct_cols = X;
   int64_t base;
   int64_t own, ybytes_b1, ybytes_b0;
-  if (fmt == MSREP_CSC) {
+  if (colwise(fmt)) {
     const int64_t rows_out = c->nranks > 1 ? std::min<int64_t>(c->shard, std::max<int64_t>(0, m - (int64_t)c->rank * c->shard)) : m;
     own = rows_out;
     // the rank's entries + its column pointer + its x window + (p > 1) the fp64 py write and the
     // shard read after the reduce-scatter; p = 1 fuses alpha/beta into the band kernel (no py)
-    base = nz_r * (int64_t)(V + 4) + (W + 1) * 4 + W * (int64_t)V + ((c->nranks > 1 || c->csplit) ? m * 8 + rows_out * 8 : 0);
+    base = nz_r * (int64_t)(V + 4) + (fmt == MSREP_COO_COL ? nz_r * 4 : (W + 1) * 4) + W * (int64_t)V +
+           ((c->nranks > 1 || c->csplit) ? m * 8 + rows_out * 8 : 0);
     ybytes_b1 = rows_out * (int64_t)V * 2;
     ybytes_b0 = rows_out * (int64_t)V;
   } else {
@@ -997,7 +1107,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   st.owned_rows = own;
   st.alg_bytes = base + ybytes_b1;
   st.alg_bytes_beta0 = base + ybytes_b0;
-  if (fmt == MSREP_CSC)
+  if (colwise(fmt))
     st.kernels_per_spmv = (c->cnb ? 1 : 0) + ((c->nranks > 1 || c->csplit) ? 1 /*py epilogue*/ : 0) + (c->csplit ? 1 /*memset*/ : 0);
   else st.kernels_per_spmv = (c->ntiles ? 1 : 0) + (c->nranks > 1 && c->any_flag ? 1 : 0) + (c->nsplit ? 1 : 0);
   int64_t db = 0;
@@ -1017,8 +1127,8 @@ msrep_status_t msrep_spmv(msrep_ctx h, const void* alpha_p, const void* x, const
   if ((c->m > 0 && !y) || (c->n > 0 && !x)) return fail(MSREP_ERR_INVALID_ARG, "x/y NULL");
   if (layout != MSREP_Y_REPLICATED && layout != MSREP_Y_OWNED && layout != MSREP_Y_SHARDED)
     return fail(MSREP_ERR_INVALID_ARG, "layout %d", (int)layout);
-  if (c->fmt == MSREP_CSC && layout == MSREP_Y_OWNED) return fail(MSREP_ERR_STATE, "OWNED layout is for pCSR/pCOO");
-  if (c->fmt != MSREP_CSC && layout == MSREP_Y_SHARDED) return fail(MSREP_ERR_STATE, "SHARDED layout is for pCSC");
+  if (colwise(c->fmt) && layout == MSREP_Y_OWNED) return fail(MSREP_ERR_STATE, "OWNED layout is for pCSR/pCOO");
+  if (!colwise(c->fmt) && layout == MSREP_Y_SHARDED) return fail(MSREP_ERR_STATE, "SHARDED layout is for pCSC / column-sorted pCOO");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const double alpha = get_scalar(alpha_p, c->dtype), beta = get_scalar(beta_p, c->dtype);
   const size_t V = vsz(c->dtype);
@@ -1034,12 +1144,13 @@ msrep_status_t msrep_spmv(msrep_ctx h, const void* alpha_p, const void* x, const
     return MSREP_OK;
   }
 
-  if (c->fmt == MSREP_CSC) {
+  if (colwise(c->fmt)) {
     ColLaunch L{};
     L.items = c->d_citems; L.item_off = c->d_item_off; L.band_item = c->d_band_item; L.split = c->d_split;
     L.nb = (int)c->cnb; L.blob = c->d_cblob;
     L.x = x; L.xbase = c->wlo;
-    L.split_items = c->csplit; L.nitems = (int)c->citems;
+    L.split_items = c->csplit; L.nunits = (int)c->cunits; L.units = c->d_cunits; L.item_hst = c->d_item_hst;
+    L.item_hw = c->d_item_hw;
     L.fused = c->nranks == 1 && !c->csplit;
     L.out = L.fused ? y : static_cast<void*>(c->d_py);
     if (c->csplit) CUDA_TRY(cudaMemsetAsync(c->d_py, 0, (size_t)c->m * 8, s));   // items add into py

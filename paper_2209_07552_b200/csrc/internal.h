@@ -124,7 +124,13 @@ struct ColLaunch {
   void* out; int64_t m;                                      // fused: y (dtype); else fp64 py
   double alpha, beta;
   int fused; int dtype;
-  int split_items, nitems;    // few bands (m small): one CTA per item, partial bands added into py
+  // split mode (few bands, or bands much heavier than one SM's share): the units of work are
+  // stage ranges of a band, {band, first stage, end stage, 0} counted over the band's items in
+  // order; each unit adds its partial band into py
+  int split_items, nunits;
+  const int4* units;
+  const int32_t* item_hst;    // [items]: stages [0, item_hst[i]) may hold same-row groups
+  const int32_t* item_hw;     // [items * CB_W]: same-row groups leading warp w's list of item i
 };
 
 struct FixupLaunch {

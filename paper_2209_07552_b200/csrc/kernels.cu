@@ -428,7 +428,7 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 // one consumer warp's share of a stage, in registers
 template <typename VT>
 struct CBStage {
-  int4 d;                 // {band (-1: end), seg, window col base, last of band}
+  int4 d;                 // {band (-1: end), seg | stage << 8, window col base, last | same-row << 1 | item << 2}
   uint32_t pk[CB_PER];
   VT v[CB_PER], xv[CB_PER];
 };
@@ -442,7 +442,7 @@ __device__ __forceinline__ void cb_load(CBStage<VT>& S, int it, const unsigned c
   const int s = it % CB_NS;
   mbar_wait(&full[s], (uint32_t)((it / CB_NS) & 1));
   S.d = sdesc[s];
-  const int seg = S.d.y;
+  const int seg = S.d.y & 0xff;
   const unsigned char* st = smem + L::ST_OFF + s * L::STAGE;
   const VT* sv = reinterpret_cast<const VT*>(st) + warp * seg;
   const uint32_t* sp = reinterpret_cast<const uint32_t*>(st + CB_W * seg * V) + warp * seg;
@@ -491,15 +491,25 @@ __global__ void __launch_bounds__(CB_THREADS, 1) csc_band_kernel(const ColLaunch
         if (bytes) tma_1d(smem + L::ST_OFF + s * L::STAGE, src, (uint32_t)bytes, &full[s], pol);
         it++;
       };
-      if (P.split_items) {   // one item at a time; every item ends its own (partial) band
-        for (int i = blockIdx.x; i < P.nitems; i += gridDim.x) {
-          const int4 item = P.items[i];
-          const char* src = P.blob + P.item_off[i];
-          for (int sg = 0; sg < item.y; sg++) {
-            const int seg = sg == item.y - 1 ? item.w : CB_SEG;
-            const int bytes = CB_W * seg * (V + 4);
-            stage(make_int4(item.x, seg, item.z, sg == item.y - 1 ? 1 : 0), src, bytes);
-            src += bytes;
+      if (P.split_items) {   // one unit (a stage range of a band) at a time; each ends a partial band
+        for (int u = blockIdx.x; u < P.nunits; u += gridDim.x) {
+          const int4 un = P.units[u];
+          const int b = un.x, i0 = P.band_item[b], i1 = P.band_item[b + 1];
+          int g = 0;   // band stage index
+          for (int i = i0; i < i1 && g < un.z; i++) {
+            const int4 item = P.items[i];
+            if (g + item.y <= un.y) { g += item.y; continue; }
+            const int hst = P.item_hst[i];
+            const int s0 = un.y > g ? un.y - g : 0, s1 = min(item.y, un.z - g);
+            const char* src = P.blob + P.item_off[i] + (int64_t)s0 * CB_W * CB_SEG * (V + 4);
+            for (int sg = s0; sg < s1; sg++) {
+              const int seg = sg == item.y - 1 ? item.w : CB_SEG;
+              const int bytes = CB_W * seg * (V + 4);
+              stage(make_int4(b, seg | (sg << 8), item.z, (g + sg == un.z - 1 ? 1 : 0) | (sg < hst ? 2 : 0) | (i << 2)),
+                    src, bytes);
+              src += bytes;
+            }
+            g += item.y;
           }
         }
         stage(make_int4(-1, 0, 0, 0), nullptr, 0);
@@ -514,10 +524,12 @@ __global__ void __launch_bounds__(CB_THREADS, 1) csc_band_kernel(const ColLaunch
         for (int i = i0; i < i1; i++) {
           const int4 item = P.items[i];
           const char* src = P.blob + P.item_off[i];
+          const int hst = P.item_hst[i];
           for (int sg = 0; sg < item.y; sg++) {
             const int seg = sg == item.y - 1 ? item.w : CB_SEG;
             const int bytes = CB_W * seg * (V + 4);
-            stage(make_int4(b, seg, item.z, (i == i1 - 1 && sg == item.y - 1) ? 1 : 0), src, bytes);
+            stage(make_int4(b, seg | (sg << 8), item.z,
+                            ((i == i1 - 1 && sg == item.y - 1) ? 1 : 0) | (sg < hst ? 2 : 0) | (i << 2)), src, bytes);
             src += bytes;
           }
         }
@@ -538,13 +550,32 @@ __global__ void __launch_bounds__(CB_THREADS, 1) csc_band_kernel(const ColLaunch
   while (A.d.x >= 0) {
     cb_load(B, it++, smem, sdesc, full, empty, x, xpol, warp, lane);   // next stage's gathers fly during A's scatter
     // the scatter: 32 distinct rows per step, steps in list order (deterministic)
+    if (A.d.w & 2) {   // this stage may hold SAME-ROW groups (heavy rows; placed first in each list)
+      const int hw = P.item_hw[(A.d.w >> 2) * CB_W + warp];   // same-row groups leading this warp's list
+      const int j0 = (A.d.y >> 8) * CB_PER;                   // list step of k = 0
 #pragma unroll
-    for (int k = 0; k < CB_PER; k++)
-      if (A.pk[k] != CB_HOLE) {
-        double* a = acc + (A.pk[k] & (CB_ROWS - 1));
-        *a = fma((double)A.v[k], (double)A.xv[k], *a);
+      for (int k = 0; k < CB_PER; k++) {
+        if (j0 + k < hw) {   // 32 entries of one heavy row: one warp-reduced update
+          double t = (double)A.v[k] * (double)A.xv[k];
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(FULL, t, off);
+          if (lane == 0) acc[A.pk[k] & (CB_ROWS - 1)] += t;
+          __syncwarp();   // visible to the next step's lanes
+        } else if (A.pk[k] != CB_HOLE) {
+          double* a = acc + (A.pk[k] & (CB_ROWS - 1));
+          *a = fma((double)A.v[k], (double)A.xv[k], *a);
+        }
       }
-    if (A.d.w) {   // band complete: this warp writes its rows once and re-zeroes them
+    } else {
+      // the scatter: 32 distinct rows per step, steps in list order (deterministic)
+#pragma unroll
+      for (int k = 0; k < CB_PER; k++)
+        if (A.pk[k] != CB_HOLE) {
+          double* a = acc + (A.pk[k] & (CB_ROWS - 1));
+          *a = fma((double)A.v[k], (double)A.xv[k], *a);
+        }
+    }
+    if (A.d.w & 1) {   // band (or split unit) complete: this warp writes its rows once and re-zeroes them
       __syncwarp();
       const int b = A.d.x;
       const int lo = P.split[b * (CB_W + 1) + warp], hi = P.split[b * (CB_W + 1) + warp + 1];
@@ -764,7 +795,7 @@ cudaError_t launch_cols_t(const ColLaunch& L, cudaStream_t s) {
   constexpr int b = CBLayout<VT>::TOTAL > MSREP_CB_SMEM_MIN ? CBLayout<VT>::TOTAL : MSREP_CB_SMEM_MIN;
   cudaError_t e = set_smem(csc_band_kernel<VT>, b);
   if (e) return e;
-  const int units = L.split_items ? L.nitems : L.nb;
+  const int units = L.split_items ? L.nunits : L.nb;
   const int g = units < num_sms() ? units : num_sms();
   if (g < 1) return cudaSuccess;
   csc_band_kernel<VT><<<g, CB_THREADS, b, s>>>(L);

@@ -59,6 +59,9 @@ def run_gpu(A, fmt, x, y, alpha, beta, parts=1, layout=None, host_path=False, ct
     elif fmt == "coo":
         assert A["fmt"] == "csr"
         ctx.partition("coo", A["m"], A["n"], idx=A["idx"], val=A["val"], coo_row=coo_of_csr(A))
+    elif fmt == "coo_col":   # column-sorted COO: coo_row carries the sorted column ids
+        assert A["fmt"] == "csc"
+        ctx.partition("coo_col", A["m"], A["n"], idx=A["idx"], val=A["val"], coo_row=coo_of_csr(A))
     else:
         assert A["fmt"] == "csc"
         ctx.partition("csc", A["m"], A["n"], ptr=A["ptr"], idx=A["idx"], val=A["val"])

@@ -130,3 +130,23 @@ def test_block_split_plan_bit_exact_vs_oracle():
         ours = M.msrep_plan_split(M.COO, M.SPLIT_BLOCK, m, nnz, np_, coo_row=rows)
         refc = oracle.partition_coo_b(m, rows, oracle.block_boundaries_coo(m, rows, np_))
         _parts_equal(ours, refc)
+
+
+def test_coo_col_plan_matches_csc_and_oracle():
+    """Column-sorted pCOO: Alg. 6 on the sorted column ids gives exactly the pCSC
+    descriptors of Alg. 4 on the same matrix, and the oracle's linear-scan Alg. 6."""
+    import paper_2209_07552_b200 as M
+    rng = np.random.default_rng(29)
+    for trial in range(200):
+        n = int(rng.integers(0, 40)); np_ = int(rng.integers(1, 10))
+        lens = rng.integers(0, 6, n) * (rng.random(n) < 0.7)
+        cp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        nnz = int(cp[-1])
+        cols = oracle.csr_to_coo(n, cp)
+        for split in (M.SPLIT_NNZ, M.SPLIT_BLOCK):
+            a = M.msrep_plan_split(M.COO_COL, split, n, nnz, np_, coo_row=cols)
+            b = M.msrep_plan_split(M.CSC, split, n, nnz, np_, ptr=cp)
+            for k in ("start_idx", "end_idx", "start_row", "end_row", "start_flag"):
+                assert np.array_equal(a[k], b[k]), k
+        ref = oracle.partition_coo(n, cols, np_)
+        _parts_equal(M.msrep_plan(M.COO_COL, n, nnz, np_, coo_row=cols), ref)

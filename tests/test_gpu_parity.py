@@ -15,11 +15,11 @@ from tests.helpers import assert_close, coo_of_csr, oracle_ref, row_bound, run_g
 
 pytestmark = pytest.mark.gpu
 
-FMTS = ["csr", "coo", "csc"]
+FMTS = ["csr", "coo", "csc", "coo_col"]   # coo_col: column-sorted pCOO (merged like pCSC)
 
 
 def as_fmt(A, fmt):
-    if fmt == "csc":
+    if fmt in ("csc", "coo_col"):
         return A if A["fmt"] == "csc" else gen.transpose(A)
     return A if A["fmt"] == "csr" else gen.transpose(A)
 
@@ -189,7 +189,7 @@ def test_deterministic_and_layout_invariant(fmt):
     x = gen.vector(A["n"], 1); y = gen.vector(A["m"], 2)
     B = as_fmt(A, fmt)
     outs = run_gpu(B, fmt, x, y, 1.5, 0.5, parts=4, repeat=3)
-    if fmt != "csc":   # no float atomics on the row path: bit-reproducible
+    if fmt in ("csr", "coo"):   # no float atomics on the row path: bit-reproducible
         assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
     assert_close(outs[0], oracle_ref(A, x, y, 1.5, 0.5), row_bound(A, x, y, 1.5, 0.5), np.float64)
 
@@ -340,8 +340,8 @@ def test_block_split_bit_exact(fmt, parts):
         B = as_fmt(A, fmt)
         x = gen.vector(A["n"], 81, kind=gen.SMALLINT); y = gen.vector(A["m"], 82, kind=gen.SMALLINT)
         ctx = M.Context(0, 1, None, 0, parts)
-        if fmt == "coo":
-            ctx.partition("coo", B["m"], B["n"], idx=B["idx"], val=B["val"], coo_row=coo_of_csr(B), split="block")
+        if fmt in ("coo", "coo_col"):
+            ctx.partition(fmt, B["m"], B["n"], idx=B["idx"], val=B["val"], coo_row=coo_of_csr(B), split="block")
         else:
             ctx.partition(fmt, B["m"], B["n"], ptr=B["ptr"], idx=B["idx"], val=B["val"], split="block")
         assert (ctx.parts["start_flag"] == 0).all()
@@ -364,3 +364,19 @@ def test_sell_rows_per_lane(k):
     B = gen.two_class(32 * 4 * 9, 4000, 9, 4, k, 0.5, kind=gen.SMALLINT)
     xb = gen.vector(B["n"], 93, kind=gen.SMALLINT); yb = gen.vector(B["m"], 94, kind=gen.SMALLINT)
     check(B, "csr", xb, yb, 2.0, 0.5, parts=2, exact=True)
+
+
+@pytest.mark.parametrize("fmt", ["csc", "coo_col"])
+def test_csc_heavy_rows_same_row_groups(fmt):
+    """Rows with thousands of entries inside one band (R-MAT heavy rows, and a dense row): the
+    pCSC lists carry same-row groups of 32 (one warp-reduced update) -- bit-exact."""
+    A = gen.rmat(14, seed=13, kind=gen.SMALLINT)
+    x = gen.vector(A["n"], 95, kind=gen.SMALLINT); y = gen.vector(A["m"], 96, kind=gen.SMALLINT)
+    for parts in (1, 3):
+        check(A, fmt, x, y, 1.5, 0.5, parts=parts, exact=True)
+    n = 50_000
+    D = gen.Sparse(fmt="csr", m=3, n=n, ptr=np.array([0, n, n + 7, 2 * n + 7], np.int64),
+                   idx=np.concatenate([np.arange(n), np.arange(7) * 11, np.arange(n)]).astype(np.int32),
+                   val=np.ones(2 * n + 7))
+    xd = gen.vector(n, 97, kind=gen.SMALLINT)
+    check(D, fmt, xd, np.zeros(3), 1.0, 0.0, parts=2, exact=True)
