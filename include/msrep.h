@@ -194,6 +194,25 @@ msrep_status_t msrep_exchange_plan(msrep_format fmt, msrep_split split, int64_t 
                                    int nranks, int parts_per_rank, const int64_t* ptr, const int32_t* coo_row,
                                    int64_t* seg_out, int64_t* head_row_out, int32_t* head_part_out);
 
+/* Conjugate gradient (Hestenes-Stiefel) for a symmetric positive definite A
+ * (m == n) on top of msrep_spmv: the iterative-solver use of SpMV that the
+ * paper's applications point to (Sec. 6 "Benefits to applications").
+ * b: device [n] (dtype of the partition), identical on every rank; x: device
+ * [n], in = x0, out = the iterate, replicated on every rank.  Each iteration:
+ * one msrep_spmv into the rank's owned rows (OWNED / SHARDED layout), a
+ * deterministic dot p.Ap, the fused update x += a p, r -= a Ap with r.r, and
+ * p = r + b p; the vectors are updated on the owned segment only, p is
+ * allgathered before each SpMV and the two dot products are all-reduced
+ * (NCCL) when nranks > 1.  Scalars stay on the device; the host reads r.r
+ * every `check_every` iterations and stops when ||r|| <= tol * ||b|| or after
+ * maxit iterations.  iters_out / relres_out (host, may be NULL): iterations
+ * done and ||r|| / ||b|| at exit.  Collective; synchronous.  Workspace (4
+ * vectors of n) is allocated on first use and freed with the partition.
+ * Errors: MSREP_ERR_DIM_MISMATCH (m != n), MSREP_ERR_STATE (no partition, or
+ * a NaN residual: breakdown, A not SPD). */
+msrep_status_t msrep_cg(msrep_ctx ctx, const void* b, void* x, double tol, int maxit, int check_every,
+                        int* iters_out, double* relres_out, void* stream);
+
 msrep_status_t msrep_get_stats(msrep_ctx ctx, msrep_stats* out);
 
 /* Measurement hook (bench.py's roofline): while enabled, every msrep_spmv

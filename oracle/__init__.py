@@ -66,6 +66,7 @@ def lib():
             "or_relative_throughput": [I64, P],
             "or_partition_ptr_b": [I64, P, I64, P, P, P],
             "or_partition_coo_b": [I64, P, I64, P, P],
+            "or_cg_csr": [I64, P, P, P, P, P, D, I64, P, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -237,6 +238,15 @@ def partition_coo_b(m, row_idx, b):
     parts = np.zeros(b.size - 1, PART_DTYPE)
     lib().or_partition_coo_b(m, _p(row_idx), b.size - 1, _p(b), _p(parts))
     return parts
+
+
+def cg_csr(m, row_ptr, col_idx, val, b, x0, tol, maxit):
+    """Textbook CG (Hestenes-Stiefel) on an SPD CSR matrix, fp64. Returns (x, iterations, relres)."""
+    row_ptr = _c(row_ptr, np.int64); col_idx = _c(col_idx, np.int32)
+    val = _c(val, np.float64); b = _c(b, np.float64); x = np.array(x0, dtype=np.float64, copy=True)
+    it = np.zeros(1, np.int64); rr = np.zeros(1, np.float64)
+    lib().or_cg_csr(m, _p(row_ptr), _p(col_idx), _p(val), _p(b), _p(x), float(tol), int(maxit), _p(it), _p(rr))
+    return x, int(it[0]), float(rr[0])
 
 
 def merge_parts_to_ptr(m, parts, loc_flat):

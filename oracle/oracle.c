@@ -472,3 +472,47 @@ void or_merge_parts_to_ptr(int64_t m, int64_t np, const or_part *parts,
     for (int64_t r = 0; r < m; r++) ptr_out[r + 1] = ptr_out[r] + len[r];
     free(len);
 }
+
+/* ------------------------------------------------------------------------ */
+/* Conjugate gradient (Hestenes & Stiefel 1952, the textbook algorithm) for a */
+/* symmetric positive definite CSR matrix, the iterative-solver application   */
+/* of SpMV (Sec. 6).  fp64 throughout; A*p by or_spmv_csr (alpha=1,    */
+/* beta=0).  x0 in x; stops when ||r|| <= tol*||b|| or after maxit iterations */
+/* (the residual is tested after every iteration).  Writes the iteration      */
+/* count and ||r||/||b||.                                                      */
+/* ------------------------------------------------------------------------ */
+void or_cg_csr(int64_t m, const int64_t *row_ptr, const int32_t *col_idx, const double *val,
+               const double *b, double *x, double tol, int64_t maxit, int64_t *iters, double *relres)
+{
+    double *r = (double *)malloc((size_t)(m > 0 ? m : 1) * sizeof(double));
+    double *p = (double *)malloc((size_t)(m > 0 ? m : 1) * sizeof(double));
+    double *ap = (double *)malloc((size_t)(m > 0 ? m : 1) * sizeof(double));
+    or_spmv_csr(m, row_ptr, col_idx, val, OR_F64, x, ap, 1.0, 0.0);      /* ap = A x0 */
+    double rs = 0.0, bn = 0.0;
+    for (int64_t i = 0; i < m; i++) {
+        r[i] = b[i] - ap[i];
+        p[i] = r[i];
+        rs += r[i] * r[i];
+        bn += b[i] * b[i];
+    }
+    int64_t it = 0;
+    while (!(rs <= tol * tol * bn) && it < maxit) {
+        it++;
+        or_spmv_csr(m, row_ptr, col_idx, val, OR_F64, p, ap, 1.0, 0.0);  /* ap = A p */
+        double pap = 0.0;
+        for (int64_t i = 0; i < m; i++) pap += p[i] * ap[i];
+        double alpha = rs / pap, rs_new = 0.0;
+        for (int64_t i = 0; i < m; i++) {
+            x[i] += alpha * p[i];
+            r[i] -= alpha * ap[i];
+            rs_new += r[i] * r[i];
+        }
+        if (rs_new <= tol * tol * bn) { rs = rs_new; break; }
+        double beta = rs_new / rs;
+        for (int64_t i = 0; i < m; i++) p[i] = r[i] + beta * p[i];
+        rs = rs_new;
+    }
+    *iters = it;
+    *relres = bn > 0.0 ? sqrt(rs / bn) : sqrt(rs);
+    free(r); free(p); free(ap);
+}

@@ -74,6 +74,7 @@ _sig = {
     "msrep_exchange_plan": [I, I, I64, I64, I64, I, I, P, P, P, P, P],
     "msrep_plan_split": [I, I, I64, I64, I, P, P, P],
     "msrep_set_split": [P, I],
+    "msrep_cg": [P, P, P, ctypes.c_double, I, I, ctypes.POINTER(I), ctypes.POINTER(ctypes.c_double), P],
     "msrep_get_stats": [P, ctypes.POINTER(Stats)],
     "msrep_destroy": [P],
     "msrep_profile_enable": [P, I],
@@ -88,7 +89,7 @@ _lib.msrep_version.argtypes = []
 _lib.msrep_version.restype = ctypes.c_int
 
 EXPORTED = ["msrep_get_unique_id", "msrep_create", "msrep_partition", "msrep_spmv", "msrep_spmv_host",
-            "msrep_plan", "msrep_plan_split", "msrep_set_split", "msrep_exchange_plan", "msrep_get_stats", "msrep_destroy", "msrep_last_error", "msrep_version",
+            "msrep_plan", "msrep_plan_split", "msrep_set_split", "msrep_cg", "msrep_exchange_plan", "msrep_get_stats", "msrep_destroy", "msrep_last_error", "msrep_version",
             "msrep_profile_enable", "msrep_profile_read"]
 
 
@@ -196,6 +197,15 @@ def msrep_exchange_plan(fmt, m, n, nnz, nranks, parts_per_rank, ptr=None, coo_ro
     return seg.reshape(nranks, 2), hrow, hpart
 
 
+def msrep_cg(ctx, b, x, tol=1e-10, maxit=1000, check_every=10, stream=None):
+    """CG on the partitioned SPD matrix (include/msrep.h): x (device, in/out) <- iterate.
+    Returns (iterations, ||r|| / ||b||)."""
+    it, rr = I(), ctypes.c_double()
+    _check(_lib.msrep_cg(ctx, _ptr(b), _ptr(x), float(tol), int(maxit), int(check_every), ctypes.byref(it),
+                         ctypes.byref(rr), stream), "msrep_cg")
+    return it.value, rr.value
+
+
 def msrep_get_stats(ctx) -> dict:
     s = Stats()
     _check(_lib.msrep_get_stats(ctx, ctypes.byref(s)), "msrep_get_stats")
@@ -272,6 +282,12 @@ class Context:
 
     def stats(self):
         return msrep_get_stats(self.h)
+
+    def cg(self, b, x, tol=1e-10, maxit=1000, check_every=10, stream=None):
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream().cuda_stream
+        return msrep_cg(self.h, b, x, tol, maxit, check_every, stream)
 
     def close(self):
         if self.h:

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <atomic>
 #include <climits>
+#include <cmath>
 #include <chrono>
 #include <cstdarg>
 #include <cstdio>
@@ -181,6 +182,13 @@ struct Ctx {
   int64_t cunits = 0;
   int nheads_local = 0;
 
+  // CG workspace (msrep_cg): r, p (full length), Ap, partial sums, scalars {rs, pAp, rs_new, bnorm2}
+  void* d_cg_r = nullptr;
+  void* d_cg_p = nullptr;
+  void* d_cg_ap = nullptr;
+  double* d_cg_part = nullptr;
+  double* d_cg_sc = nullptr;
+
   // host-vector path buffers
   void* d_hx = nullptr;
   void* d_hy = nullptr;
@@ -243,6 +251,8 @@ void free_all(Ctx* c) {
   c->bufs.clear();
   c->ready = false;
   c->d_hx = c->d_hy = nullptr;
+  c->d_cg_r = c->d_cg_p = c->d_cg_ap = nullptr;
+  c->d_cg_part = c->d_cg_sc = nullptr;
 }
 
 template <class T>
@@ -1228,6 +1238,81 @@ msrep_status_t msrep_spmv_host(msrep_ctx h, const void* alpha, const void* x_hos
     CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(y_host) + r0 * V, static_cast<char*>(c->d_hy) + r0 * V,
                              (size_t)(r1 - r0) * V, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
+  return MSREP_OK;
+}
+
+msrep_status_t msrep_cg(msrep_ctx h, const void* b, void* x, double tol, int maxit, int check_every,
+                        int* iters_out, double* relres_out, void* stream) {
+  if (!h) return fail(MSREP_ERR_INVALID_ARG, "ctx is NULL");
+  Ctx* c = reinterpret_cast<Ctx*>(h);
+  if (!c->ready) return fail(MSREP_ERR_STATE, "msrep_cg before msrep_partition");
+  if (c->m != c->n) return fail(MSREP_ERR_DIM_MISMATCH, "CG needs a square matrix (m %lld, n %lld)", (long long)c->m, (long long)c->n);
+  if ((c->m > 0 && (!b || !x)) || maxit < 0 || !(tol >= 0.0)) return fail(MSREP_ERR_INVALID_ARG, "bad CG arguments");
+  if (check_every < 1) check_every = 1;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t V = vsz(c->dtype);
+  const int dt = c->dtype == MSREP_F64 ? 0 : 1;
+  if (!c->d_cg_r) {
+    void* q;
+    TRY(dalloc(c, (size_t)std::max<int64_t>(1, c->m) * V, &q, s)); c->d_cg_r = q;
+    TRY(dalloc(c, (size_t)std::max<int64_t>(1, c->m) * V, &q, s)); c->d_cg_p = q;
+    TRY(dalloc(c, (size_t)std::max<int64_t>(1, c->m) * V, &q, s)); c->d_cg_ap = q;
+    TRY(dalloc(c, (size_t)2 * CG_PARTS * 8, &q, s)); c->d_cg_part = static_cast<double*>(q);
+    TRY(dalloc(c, 8 * 8, &q, s)); c->d_cg_sc = static_cast<double*>(q);
+  }
+  std::vector<int64_t> seg_lo, seg_hi;
+  owned_segments(c, seg_lo, seg_hi);
+  const int64_t lo = seg_lo[(size_t)c->rank], nloc = seg_hi[(size_t)c->rank] - lo;
+  const msrep_layout lay = colwise(c->fmt) ? MSREP_Y_SHARDED : MSREP_Y_OWNED;
+  double one64 = 1.0, zero64 = 0.0;
+  float one32 = 1.0f, zero32 = 0.0f;
+  const void* one = dt == 0 ? (const void*)&one64 : (const void*)&one32;
+  const void* zero = dt == 0 ? (const void*)&zero64 : (const void*)&zero32;
+  auto off = [&](const void* v) { return static_cast<char*>(const_cast<void*>(v)) + (size_t)lo * V; };
+  double* sc = c->d_cg_sc;
+  double* p1 = c->d_cg_part;              // partial sums of p.Ap (and of r0.r0, b.b at the start)
+  double* p2 = c->d_cg_part + CG_PARTS;   // partial sums of r.r
+  auto allreduce_parts = [&](double* part) -> msrep_status_t {   // same partials on every rank
+    if (c->nranks > 1) NCCL_TRY(ncclAllReduce(part, part, CG_PARTS, ncclDouble, ncclSum, c->comm, s));
+    return MSREP_OK;
+  };
+  // r0 = b - A x0, p0 = r0, rs = r0.r0 (sc[0], parity 0), bnorm2 = b.b (sc[3])
+  TRY(msrep_spmv(h, one, x, zero, c->d_cg_ap, lay, stream));
+  CUDA_TRY(launch_cg(CG_RESIDUAL, dt, off(b), off(c->d_cg_ap), off(c->d_cg_r), off(c->d_cg_p), nloc, sc, 0, nullptr, p1, s));
+  TRY(allreduce_parts(p1));
+  CUDA_TRY(launch_cg(CG_SUM, dt, nullptr, nullptr, nullptr, nullptr, 0, sc + 0, 0, p1, nullptr, s));
+  CUDA_TRY(launch_cg(CG_DOT, dt, off(b), off(b), nullptr, nullptr, nloc, sc, 0, nullptr, p2, s));
+  TRY(allreduce_parts(p2));
+  CUDA_TRY(launch_cg(CG_SUM, dt, nullptr, nullptr, nullptr, nullptr, 0, sc + 3, 0, p2, nullptr, s));
+  double hs[4] = {0, 0, 0, 0};
+  CUDA_TRY(cudaMemcpyAsync(hs, sc, 4 * 8, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  const double bn2 = hs[3], stop = tol * tol * bn2;
+  double rs = hs[0];
+  int it = 0, par = 0;
+  std::vector<int64_t> lo_v = seg_lo, hi_v = seg_hi;
+  // per iteration: SpMV, dot(p, Ap), update x and r (+ r.r), update p (+ rs) -- four launches
+  while (!(rs <= stop) && it < maxit) {
+    it++;
+    if (c->nranks > 1) TRY(allgatherv_y(c, c->d_cg_p, lo_v, hi_v, s));   // the SpMV needs the whole p
+    TRY(msrep_spmv(h, one, c->d_cg_p, zero, c->d_cg_ap, lay, stream));   // Ap, owned rows
+    CUDA_TRY(launch_cg(CG_DOT, dt, off(c->d_cg_p), off(c->d_cg_ap), nullptr, nullptr, nloc, sc, par, nullptr, p1, s));
+    TRY(allreduce_parts(p1));
+    CUDA_TRY(launch_cg(CG_UPDATE_XR, dt, off(x), off(c->d_cg_r), off(c->d_cg_p), off(c->d_cg_ap), nloc, sc, par, p1, p2, s));
+    TRY(allreduce_parts(p2));
+    CUDA_TRY(launch_cg(CG_UPDATE_P, dt, off(c->d_cg_p), off(c->d_cg_r), nullptr, nullptr, nloc, sc, par, p2, nullptr, s));
+    par ^= 1;                                                              // sc[par] = rs_new
+    if (it % check_every == 0 || it == maxit) {
+      CUDA_TRY(cudaMemcpyAsync(hs, sc, 4 * 8, cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaStreamSynchronize(s));
+      if (std::isnan(hs[par])) return fail(MSREP_ERR_STATE, "CG breakdown at iteration %d (matrix not SPD?)", it);
+      rs = hs[par];
+    }
+  }
+  if (c->nranks > 1) TRY(allgatherv_y(c, x, lo_v, hi_v, s));   // x replicated on exit
+  CUDA_TRY(cudaStreamSynchronize(s));
+  if (iters_out) *iters_out = it;
+  if (relres_out) *relres_out = bn2 > 0.0 ? std::sqrt(rs / bn2) : std::sqrt(rs);
   return MSREP_OK;
 }
 

@@ -160,5 +160,12 @@ cudaError_t launch_axpby_py(const double* py, void* y, int64_t count, double alp
 cudaError_t launch_rebase(const int64_t* gptr, int32_t* lptr, int64_t count, int64_t lo, int64_t hi,
                           cudaStream_t s);                                                  // clamp(gptr,lo,hi)-lo
 cudaError_t launch_pack(const PackLaunch& L, cudaStream_t s);
+// CG vector kernels on an owned segment of n entries (kernels.cu).  sc = device scalars
+// {rs (parity 0), rs (parity 1), -, bnorm2}; part_in / part_out = CG_PARTS per-block partial
+// sums (every consumer block re-sums part_in in the same fixed order).
+enum CgOp { CG_RESIDUAL = 0, CG_DOT = 1, CG_UPDATE_XR = 2, CG_UPDATE_P = 3, CG_SUM = 4 };
+constexpr int CG_PARTS = 296;
+cudaError_t launch_cg(int op, int dtype, void* a, void* b, void* c, const void* d, int64_t n, double* sc, int par,
+                      const double* part_in, double* part_out, cudaStream_t s);
 
 }  // namespace msrep

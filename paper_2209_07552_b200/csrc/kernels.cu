@@ -744,6 +744,94 @@ __global__ void rebase_kernel(const int64_t* __restrict__ g, int32_t* __restrict
   }
 }
 
+// ------------------------------------------------------------ CG vector kernels
+// Conjugate gradient (Hestenes-Stiefel) on top of msrep_spmv (include/msrep.h
+// msrep_cg).  Every kernel works on the rank's owned segment; dot products are
+// deterministic: a fixed grid of CG_BLOCKS blocks writes per-block partial sums
+// (fixed shuffle tree), one block adds them in index order.
+constexpr int CG_BLOCKS = 296, CG_THREADS = 256;
+
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double ws[CG_THREADS / 32];
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(FULL, v, off);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < CG_THREADS / 32; w++) t += ws[w];
+  __syncthreads();
+  return t;   // valid in thread 0
+}
+
+// r = b - Ax, p = r, partial r.r
+template <typename VT>
+__global__ void cg_residual_kernel(const VT* __restrict__ b, const VT* __restrict__ ax, VT* __restrict__ r,
+                                   VT* __restrict__ p, int64_t n, double* part) {
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const VT v = (VT)((double)b[i] - (double)ax[i]);
+    r[i] = v;
+    p[i] = v;
+    acc += (double)v * (double)v;
+  }
+  const double t = block_sum(acc);
+  if (threadIdx.x == 0) part[blockIdx.x] = t;
+}
+
+template <typename VT>
+__global__ void cg_dot_kernel(const VT* __restrict__ a, const VT* __restrict__ b, int64_t n, double* part) {
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    acc += (double)a[i] * (double)b[i];
+  const double t = block_sum(acc);
+  if (threadIdx.x == 0) part[blockIdx.x] = t;
+}
+
+// every block sums the CG_BLOCKS partial sums in the same fixed order (same value everywhere)
+__device__ __forceinline__ double sum_parts(const double* part) {
+  double t = 0.0;
+  for (int i = threadIdx.x; i < CG_BLOCKS; i += blockDim.x) t += part[i];
+  __shared__ double tot;
+  const double v = block_sum(t);
+  if (threadIdx.x == 0) tot = v;
+  __syncthreads();
+  return tot;
+}
+
+// alpha = rs / pAp (pAp = sum of part_in);  x += alpha p;  r -= alpha Ap;  partial r.r -> part_out
+template <typename VT>
+__global__ void cg_update_xr_kernel(VT* __restrict__ x, VT* __restrict__ r, const VT* __restrict__ p,
+                                    const VT* __restrict__ ap, int64_t n, const double* sc, int par,
+                                    const double* part_in, double* part_out) {
+  const double alpha = sc[par] / sum_parts(part_in);
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] = (VT)((double)x[i] + alpha * (double)p[i]);
+    const VT v = (VT)((double)r[i] - alpha * (double)ap[i]);
+    r[i] = v;
+    acc += (double)v * (double)v;
+  }
+  const double t = block_sum(acc);
+  if (threadIdx.x == 0) part_out[blockIdx.x] = t;
+}
+
+// rs_new = sum of part_in;  beta = rs_new / rs;  p = r + beta p;  rs of the other parity <- rs_new
+template <typename VT>
+__global__ void cg_update_p_kernel(VT* __restrict__ p, const VT* __restrict__ r, int64_t n, double* sc, int par,
+                                   const double* part_in) {
+  const double rs_new = sum_parts(part_in);
+  const double beta = rs_new / sc[par];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = (VT)((double)r[i] + beta * (double)p[i]);
+  if (blockIdx.x == 0 && threadIdx.x == 0) sc[par ^ 1] = rs_new;
+}
+
+// *out = sum of part (one block, fixed order)
+__global__ void cg_sum_kernel(const double* part, double* out) {
+  const double t = sum_parts(part);
+  if (threadIdx.x == 0) *out = t;
+}
+
 int g_sms = 0;
 int num_sms() {
   if (g_sms == 0) {
@@ -854,6 +942,27 @@ cudaError_t launch_axpby_py(const double* py, void* y, int64_t n, double alpha, 
 cudaError_t launch_rebase(const int64_t* g, int32_t* l, int64_t n, int64_t lo, int64_t hi, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   rebase_kernel<<<elementwise_grid(n), 256, 0, s>>>(g, l, n, lo, hi);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cg(int op, int dtype, void* a, void* b, void* c, const void* d, int64_t n, double* sc, int par,
+                      const double* part_in, double* part_out, cudaStream_t s) {
+  const int g = CG_BLOCKS;
+  if (op == CG_RESIDUAL) {   // a=b_vec, b=ax, c=r, d=p -> part_out
+    if (dtype == 0) cg_residual_kernel<double><<<g, CG_THREADS, 0, s>>>((const double*)a, (const double*)b, (double*)c, (double*)d, n, part_out);
+    else cg_residual_kernel<float><<<g, CG_THREADS, 0, s>>>((const float*)a, (const float*)b, (float*)c, (float*)d, n, part_out);
+  } else if (op == CG_DOT) {   // a . b -> part_out
+    if (dtype == 0) cg_dot_kernel<double><<<g, CG_THREADS, 0, s>>>((const double*)a, (const double*)b, n, part_out);
+    else cg_dot_kernel<float><<<g, CG_THREADS, 0, s>>>((const float*)a, (const float*)b, n, part_out);
+  } else if (op == CG_UPDATE_XR) {   // a=x, b=r, c=p, d=ap
+    if (dtype == 0) cg_update_xr_kernel<double><<<g, CG_THREADS, 0, s>>>((double*)a, (double*)b, (const double*)c, (const double*)d, n, sc, par, part_in, part_out);
+    else cg_update_xr_kernel<float><<<g, CG_THREADS, 0, s>>>((float*)a, (float*)b, (const float*)c, (const float*)d, n, sc, par, part_in, part_out);
+  } else if (op == CG_UPDATE_P) {   // a=p, b=r
+    if (dtype == 0) cg_update_p_kernel<double><<<g, CG_THREADS, 0, s>>>((double*)a, (const double*)b, n, sc, par, part_in);
+    else cg_update_p_kernel<float><<<g, CG_THREADS, 0, s>>>((float*)a, (const float*)b, n, sc, par, part_in);
+  } else if (op == CG_SUM) {   // part_in -> *sc
+    cg_sum_kernel<<<1, CG_THREADS, 0, s>>>(part_in, sc);
+  }
   return cudaGetLastError();
 }
 

@@ -380,3 +380,67 @@ def test_csc_heavy_rows_same_row_groups(fmt):
                    val=np.ones(2 * n + 7))
     xd = gen.vector(n, 97, kind=gen.SMALLINT)
     check(D, fmt, xd, np.zeros(3), 1.0, 0.0, parts=2, exact=True)
+
+
+# ------------------------------------------------------------ CG (NEXT f4)
+def _spd_stencil(N, diag=30.0, kind=None):
+    A = gen.stencil27(N, kind=gen.ONES)
+    rows = np.repeat(np.arange(A["m"]), np.diff(A["ptr"]))
+    A["val"] = np.where(A["idx"] == rows, diag, -1.0)
+    return A
+
+
+def _cg_gpu(A, fmt, b, parts, dtype, tol, maxit):
+    import paper_2209_07552_b200 as M
+    import torch
+    B = as_fmt(to_dtype(A, dtype), fmt)
+    ctx = M.Context(0, 1, None, 0, parts)
+    if fmt in ("coo", "coo_col"):
+        ctx.partition(fmt, B["m"], B["n"], idx=B["idx"], val=B["val"], coo_row=coo_of_csr(B))
+    else:
+        ctx.partition(fmt, B["m"], B["n"], ptr=B["ptr"], idx=B["idx"], val=B["val"])
+    tdt = torch.float64 if dtype == np.float64 else torch.float32
+    bd = torch.as_tensor(b.astype(dtype)).cuda()
+    xd = torch.zeros(A["n"], dtype=tdt, device="cuda")
+    it, rr = ctx.cg(bd, xd, tol=tol, maxit=maxit, check_every=1)
+    x = xd.cpu().numpy().astype(np.float64)
+    ctx.close()
+    return x, it, rr
+
+
+@pytest.mark.parametrize("fmt", FMTS)
+@pytest.mark.parametrize("parts", [1, 3])
+def test_cg_matches_oracle(fmt, parts):
+    """msrep_cg on the SPD stencil (diag 30, off -1) with b = A x*: converges to x*, within one
+    iteration of the oracle's textbook CG, fp64."""
+    A = _spd_stencil(16)
+    m = A["m"]
+    xs = (np.arange(m) % 7 - 3).astype(np.float64)
+    b = oracle.spmv_csr(m, A["ptr"], A["idx"], A["val"], xs, np.zeros(m), 1.0, 0.0)
+    xo, ito, rro = oracle.cg_csr(m, A["ptr"], A["idx"], A["val"], b, np.zeros(m), 1e-11, 500)
+    x, it, rr = _cg_gpu(A, fmt, b, parts, np.float64, 1e-11, 500)
+    assert rr <= 1e-11 and abs(it - ito) <= 1, (it, ito, rr, rro)
+    assert np.max(np.abs(x - xs)) < 1e-9
+    assert np.max(np.abs(x - xo)) < 1e-9
+
+
+def test_cg_fp32_storage():
+    """fp32 storage (fp64 dot products and scalars): converges to x* to fp32 accuracy."""
+    A = _spd_stencil(12)
+    m = A["m"]
+    xs = (np.arange(m) % 5 - 2).astype(np.float64)
+    b = oracle.spmv_csr(m, A["ptr"], A["idx"], A["val"], xs, np.zeros(m), 1.0, 0.0)
+    x, it, rr = _cg_gpu(A, "csr", b, 2, np.float32, 1e-6, 300)
+    assert rr <= 1e-6 and np.max(np.abs(x - xs)) < 1e-4
+
+
+def test_cg_errors():
+    import paper_2209_07552_b200 as M
+    import torch
+    A = gen.kdistinct_csr(20, 30, 3, seed=3)
+    ctx = M.Context(0, 1, None, 0, 1)
+    ctx.partition("csr", 20, 30, ptr=A["ptr"], idx=A["idx"], val=A["val"])
+    with pytest.raises(M.MsrepError) as e:   # not square
+        ctx.cg(torch.zeros(20, dtype=torch.float64, device="cuda"), torch.zeros(30, dtype=torch.float64, device="cuda"))
+    assert e.value.status == 2
+    ctx.close()

@@ -440,3 +440,61 @@ def test_relative_throughput_fig6_two_class():
     assert abs(r - 559 / 1028) < 0.01
     assert oracle.relative_throughput(oracle.nnz_boundaries(int(b[-1]), 8)) > 0.99
     assert oracle.relative_throughput(np.array([0, 5, 10])) == 1.0
+
+
+# ------------------------------------------------------------ CG (NEXT f4)
+def _spd_stencil(N, diag=30.0):
+    """27-point stencil pattern with diagonal `diag`, off-diagonals -1: symmetric and strictly
+    diagonally dominant (26 < diag), hence SPD."""
+    import gen
+    A = gen.stencil27(N, kind=gen.ONES)
+    rows = np.repeat(np.arange(A["m"]), np.diff(A["ptr"]))
+    A["val"] = np.where(A["idx"] == rows, diag, -1.0)
+    return A
+
+
+def test_cg_identity_one_iteration():
+    """A = I: r0 = b, alpha = 1, x1 = b exactly, so CG stops after one iteration."""
+    m = 7
+    b = np.arange(1.0, m + 1)
+    x, it, rr = oracle.cg_csr(m, np.arange(m + 1), np.arange(m, dtype=np.int32), np.ones(m), b, np.zeros(m), 1e-14, 50)
+    assert it == 1 and rr == 0.0 and np.array_equal(x, b)
+
+
+def test_cg_k_distinct_eigenvalues():
+    """Textbook property: on an SPD matrix with k distinct eigenvalues CG terminates in at most
+    k iterations (in exact arithmetic; here the residual after k steps is at rounding level)."""
+    d = np.repeat([1.0, 3.0, 7.0, 10.0], 25)           # k = 4 distinct eigenvalues
+    m = d.size
+    b = np.linspace(-1, 1, m) + 0.3
+    x, it, rr = oracle.cg_csr(m, np.arange(m + 1), np.arange(m, dtype=np.int32), d, b, np.zeros(m), 1e-12, 4)
+    assert it <= 4 and rr < 1e-12
+    assert np.allclose(x, b / d, rtol=1e-12)
+
+
+def test_cg_1d_laplacian_n_steps_and_solution():
+    """tridiag(-1, 2, -1) of size n (SPD, n distinct eigenvalues): CG reaches the exact solution
+    (x* = 1..n, b = A x*) within n iterations, to rounding level."""
+    n = 40
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        for j, v in ((i - 1, -1.0), (i, 2.0), (i + 1, -1.0)):
+            if 0 <= j < n:
+                rows.append(i); cols.append(j); vals.append(v)
+    ptr, idx, val = oracle.coo_to_csr(n, np.array(rows), np.array(cols), np.array(vals))
+    xs = np.arange(1.0, n + 1)
+    b = oracle.spmv_csr(n, ptr, idx, val, xs, np.zeros(n), 1.0, 0.0)
+    x, it, rr = oracle.cg_csr(n, ptr, idx, val, b, np.zeros(n), 1e-13, n)
+    assert it <= n and rr < 1e-12
+    assert np.allclose(x, xs, rtol=1e-10)
+
+
+def test_cg_spd_stencil_recovers_known_solution():
+    """SPD 27-point stencil (diag 30): b = A x* with integer x*, CG from 0 converges to x*."""
+    A = _spd_stencil(6)
+    m = A["m"]
+    xs = (np.arange(m) % 7 - 3).astype(np.float64)
+    b = oracle.spmv_csr(m, A["ptr"], A["idx"], A["val"], xs, np.zeros(m), 1.0, 0.0)
+    x, it, rr = oracle.cg_csr(m, A["ptr"], A["idx"], A["val"], b, np.zeros(m), 1e-12, 500)
+    assert rr <= 1e-12 and 0 < it < 60
+    assert np.max(np.abs(x - xs)) < 1e-10
