@@ -278,7 +278,9 @@ struct Packer {
   int64_t wlo;
   const std::vector<int64_t>& lp;   // local pointer over the window (rank-local nonzeros)
   int64_t cur_r0 = -1, cur_r1 = -1;
-  explicit Packer(Schedule& s, int64_t w, const std::vector<int64_t>& l) : S(s), wlo(w), lp(l) {}
+  const int64_t tnz;                // nonzeros per SEG tile / slab for this value size
+  explicit Packer(Schedule& s, int64_t w, const std::vector<int64_t>& l, int vsize)
+      : S(s), wlo(w), lp(l), tnz(tile_nnz(vsize)) {}
   int64_t ls(int64_t r) const { return lp[(size_t)(r - wlo)]; }
   int64_t le(int64_t r) const { return lp[(size_t)(r - wlo + 1)]; }
   void flush() {
@@ -291,7 +293,7 @@ struct Packer {
     const int64_t len = le(r) - ls(r);
     if (cur_r0 >= 0) {
       const int64_t nz = le(cur_r1 - 1) - ls(cur_r0);
-      if (nz + len > TILE_NNZ || cur_r1 - cur_r0 >= MAX_TILE_ROWS) flush();
+      if (nz + len > tnz || cur_r1 - cur_r0 >= MAX_TILE_ROWS) flush();
     }
     if (cur_r0 < 0) { cur_r0 = r; cur_r1 = r; }
     cur_r1 = r + 1;
@@ -319,8 +321,8 @@ struct Packer {
   }
   // slabs over rank-local nonzeros [z0, z1) of row r; with_records: write partial sums to records
   void slabs(int64_t r, int64_t z0, int64_t z1, bool with_records) {
-    for (int64_t z = z0; z < z1; z += SLAB_NNZ) {
-      const int64_t nz = std::min<int64_t>(SLAB_NNZ, z1 - z);
+    for (int64_t z = z0; z < z1; z += tnz) {
+      const int64_t nz = std::min<int64_t>(tnz, z1 - z);
       S.tiles.push_back({(int32_t)(r - wlo), (int32_t)z, (int32_t)(1 | (nz << 16)), with_records ? S.nrec++ : -1});
       S.nslabs++;
     }
@@ -368,7 +370,7 @@ void rank_segments(msrep_format fmt, int64_t m, int nranks, int vparts, const st
 // slab-split rows), and the tail row (owned, continues into later parts) as
 // slabs whose fix-up adds the head partials of the parts that continue it.
 void build_row_schedule(const Ctx& c, const std::vector<int64_t>& lp, Schedule& S) {
-  Packer pk(S, c.wlo, lp);
+  Packer pk(S, c.wlo, lp, (int)vsz(c.dtype));
   const auto& P = c.parts;
   for (int j = c.P0; j < c.P1; j++) {
     const msrep_part_desc& d = P[(size_t)j];
@@ -388,7 +390,7 @@ void build_row_schedule(const Ctx& c, const std::vector<int64_t>& lp, Schedule& 
     const int64_t rend = tail >= 0 ? tail : d.owned_end;
     auto one_row = [&](int64_t r) {
       const int64_t len = pk.le(r) - pk.ls(r);
-      if (len > TILE_NNZ) {
+      if (len > pk.tnz) {
         pk.flush();
         S.sr_row.push_back(r);
         S.sr_rec.push_back(S.nrec);

@@ -11,7 +11,9 @@ namespace msrep {
 // rows (<= MAX_TILE_ROWS rows, <= TILE_NNZ nonzeros), or a "slab" -- a
 // contiguous piece (<= SLAB_NNZ nonzeros) of one split row whose partial sum
 // goes to a record instead of y.
-constexpr int TILE_NNZ = 512;
+constexpr int TILE_NNZ = 512;        // fp64 SEG tiles and slabs
+constexpr int TILE_NNZ_F32 = 768;    // fp32: ~the bytes of an fp64 tile within the register budget
+__host__ __device__ constexpr int tile_nnz(int vsize) { return vsize == 4 ? TILE_NNZ_F32 : TILE_NNZ; }
 constexpr int MAX_TILE_ROWS = 128;   // rows per segment tile (uint8 tile-local row keys)
 constexpr int SLAB_NNZ = 512;
 #ifndef MSREP_WARPS

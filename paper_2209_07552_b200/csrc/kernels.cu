@@ -104,12 +104,12 @@ __device__ __forceinline__ float ldx(const float* p, uint64_t pol) {
 // no cross-warp synchronisation, so a slow warp never stalls another's loads.
 template <typename VT>
 struct RStage {
-  static constexpr int BYTES = TILE_NNZ + TILE_NNZ * (int)sizeof(VT) + TILE_NNZ * 4;
+  static constexpr int N = tile_nnz((int)sizeof(VT));
+  static constexpr int BYTES = N + N * (int)sizeof(VT) + N * 4;
 };
 
 template <int STAGE_B, int NS, int SCRATCH>
 struct WLayout {
-  static constexpr int S = NS;
   static constexpr int DESC_OFF = NS * STAGE_B;                          // int4 per stage
   static constexpr int SCR_OFF = DESC_OFF + NS * 16;                     // per-warp fp64 scratch
   static constexpr int WARP_B = (SCR_OFF + SCRATCH + 15) & ~15;
@@ -117,7 +117,9 @@ struct WLayout {
   static constexpr int TOTAL = BAR_OFF + WARPS * NS * 8;
 };
 
-constexpr int QMAX = TILE_NNZ / 32;    // 16: nonzeros per lane in a full tile (+1 extra slot when ragged)
+// nonzeros per lane in a full SEG tile / slab (+1 extra slot when ragged): 16 fp64, 32 fp32
+template <typename VT>
+__host__ __device__ constexpr int qmax() { return tile_nnz((int)sizeof(VT)) / 32; }
 
 
 // Warp-level exclusive segmented scan of (key, value) pairs with keys
@@ -181,9 +183,10 @@ using RowLayout = WLayout<(SELL && SStage<VT>::BYTES > RStage<VT>::BYTES) ? SSta
 // One SELL tile with R rows per lane (internal.h): all R*W column indices are read from the
 // slot, then all R*W x gathers are in flight before the first FMA; padding is masked by the
 // row length, so results equal the plain row sums.
-template <typename VT, int R>
+template <typename VT, int R, class Refill>
 __device__ __forceinline__ void sell_tile(const RowLaunch& P, const int4 d, const unsigned char* st, const int lane,
-                                          const VT* __restrict__ x, VT* __restrict__ y, double alpha, double beta) {
+                                          const VT* __restrict__ x, VT* __restrict__ y, double alpha, double beta,
+                                          Refill&& refill) {
   constexpr int V = (int)sizeof(VT);
   constexpr int U = SELL_W_MAX;              // R*W <= U register slots per lane
   const int nrows = d.z & 0xffff, W = d.z >> 16;
@@ -222,11 +225,14 @@ __device__ __forceinline__ void sell_tile(const RowLaunch& P, const int4 d, cons
       y[P.ybase + d.x + row] = (VT)o;
     }
   }
+  __syncwarp();   // the tile was read in place: refill the slot only now
+  refill();
 }
 
 template <typename VT, bool SELL>
 __global__ void __launch_bounds__(WARPS * 32, MSREP_ROW_MINB) rows_kernel(const RowLaunch P) {
   using Lay = RowLayout<VT, SELL>;
+  constexpr int QMAX = qmax<VT>();
   constexpr int V = (int)sizeof(VT);
   constexpr int YR = MAX_TILE_ROWS / 32;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -277,12 +283,10 @@ __global__ void __launch_bounds__(WARPS * 32, MSREP_ROW_MINB) rows_kernel(const 
       // ---- SELL tile (read in place; the slot is refilled after the tile)
       const int nrows = d.z & 0xffff, Wd = d.z >> 16;
       const int R = sell_r(nrows);
-      if (R == 1) sell_tile<VT, 1>(P, d, st, lane, x, y, alpha, beta);
-      else if (R == 2) sell_tile<VT, 2>(P, d, st, lane, x, y, alpha, beta);
-      else sell_tile<VT, 4>(P, d, st, lane, x, y, alpha, beta);
+      if (R == 1) sell_tile<VT, 1>(P, d, st, lane, x, y, alpha, beta, refill);
+      else if (R == 2) sell_tile<VT, 2>(P, d, st, lane, x, y, alpha, beta, refill);
+      else sell_tile<VT, 4>(P, d, st, lane, x, y, alpha, beta, refill);
       (void)Wd;
-      __syncwarp();
-      refill();
       continue;
     }
     const int nrows = d.z & 0xffff, nnz = d.z >> 16;
