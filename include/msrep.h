@@ -194,6 +194,18 @@ msrep_status_t msrep_exchange_plan(msrep_format fmt, msrep_split split, int64_t 
                                    int nranks, int parts_per_rank, const int64_t* ptr, const int32_t* coo_row,
                                    int64_t* seg_out, int64_t* head_row_out, int32_t* head_part_out);
 
+/* Sparse matrix times a block of k dense vectors (SpMM), Y <- alpha*A*X + beta*Y:
+ * the multi-right-hand-side extension of the same partition (
+ * the paper's conclusion on reuse by other sparse kernels).
+ * X: device [n x k], Y: device [m x k], both row-major contiguous (X[c*k + j]),
+ * k in {2, 4, 8}; the matrix is streamed once for all k vectors.  Row formats
+ * (pCSR, pCOO) only -- MSREP_ERR_STATE for pCSC / column-sorted pCOO.
+ * Layouts REPLICATED / OWNED as msrep_spmv (segments are row blocks of Y);
+ * beta == 0: Y not read; alpha == 0: Y = beta*Y.  Asynchronous on `stream`,
+ * collective when nranks > 1. */
+msrep_status_t msrep_spmm(msrep_ctx ctx, const void* alpha, const void* X, const void* beta, void* Y, int k,
+                          msrep_layout layout, void* stream);
+
 /* Conjugate gradient (Hestenes-Stiefel) for a symmetric positive definite A
  * (m == n) on top of msrep_spmv: the iterative-solver use of SpMV that the
  * paper's applications point to (Sec. 6 "Benefits to applications").

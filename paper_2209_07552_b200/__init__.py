@@ -75,6 +75,7 @@ _sig = {
     "msrep_plan_split": [I, I, I64, I64, I, P, P, P],
     "msrep_set_split": [P, I],
     "msrep_cg": [P, P, P, ctypes.c_double, I, I, ctypes.POINTER(I), ctypes.POINTER(ctypes.c_double), P],
+    "msrep_spmm": [P, P, P, P, P, I, I, P],
     "msrep_get_stats": [P, ctypes.POINTER(Stats)],
     "msrep_destroy": [P],
     "msrep_profile_enable": [P, I],
@@ -89,7 +90,7 @@ _lib.msrep_version.argtypes = []
 _lib.msrep_version.restype = ctypes.c_int
 
 EXPORTED = ["msrep_get_unique_id", "msrep_create", "msrep_partition", "msrep_spmv", "msrep_spmv_host",
-            "msrep_plan", "msrep_plan_split", "msrep_set_split", "msrep_cg", "msrep_exchange_plan", "msrep_get_stats", "msrep_destroy", "msrep_last_error", "msrep_version",
+            "msrep_plan", "msrep_plan_split", "msrep_set_split", "msrep_cg", "msrep_spmm", "msrep_exchange_plan", "msrep_get_stats", "msrep_destroy", "msrep_last_error", "msrep_version",
             "msrep_profile_enable", "msrep_profile_read"]
 
 
@@ -197,6 +198,13 @@ def msrep_exchange_plan(fmt, m, n, nnz, nranks, parts_per_rank, ptr=None, coo_ro
     return seg.reshape(nranks, 2), hrow, hpart
 
 
+def msrep_spmm(ctx, alpha, X, beta, Y, k, layout=Y_REPLICATED, stream=None, dtype=F64):
+    """Y (device [m x k], row-major) <- alpha * A * X (device [n x k]) + beta * Y, k in {2, 4, 8}."""
+    a, b = _scalar(alpha, dtype), _scalar(beta, dtype)
+    _check(_lib.msrep_spmm(ctx, ctypes.byref(a), _ptr(X), ctypes.byref(b), _ptr(Y), int(k), layout, stream),
+           "msrep_spmm")
+
+
 def msrep_cg(ctx, b, x, tol=1e-10, maxit=1000, check_every=10, stream=None):
     """CG on the partitioned SPD matrix (include/msrep.h): x (device, in/out) <- iterate.
     Returns (iterations, ||r|| / ||b||)."""
@@ -282,6 +290,13 @@ class Context:
 
     def stats(self):
         return msrep_get_stats(self.h)
+
+    def spmm(self, alpha, X, beta, Y, layout=Y_REPLICATED, stream=None):
+        """X: torch [n, k], Y: torch [m, k] (contiguous, row-major), k in {2, 4, 8}."""
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream().cuda_stream
+        msrep_spmm(self.h, alpha, X, beta, Y, X.shape[1], layout, stream, self.dtype)
 
     def cg(self, b, x, tol=1e-10, maxit=1000, check_every=10, stream=None):
         if stream is None:

@@ -189,6 +189,12 @@ struct Ctx {
   double* d_cg_part = nullptr;
   double* d_cg_sc = nullptr;
 
+  // SpMM: k-wide records / head partials (allocated for k <= 8 on first msrep_spmm)
+  int mm_k = 0;
+  double* d_rec_mm = nullptr;
+  double* d_head_local_mm = nullptr;
+  double* d_head_all_mm = nullptr;
+
   // host-vector path buffers
   void* d_hx = nullptr;
   void* d_hy = nullptr;
@@ -253,6 +259,8 @@ void free_all(Ctx* c) {
   c->d_hx = c->d_hy = nullptr;
   c->d_cg_r = c->d_cg_p = c->d_cg_ap = nullptr;
   c->d_cg_part = c->d_cg_sc = nullptr;
+  c->mm_k = 0;
+  c->d_rec_mm = c->d_head_local_mm = c->d_head_all_mm = nullptr;
 }
 
 template <class T>
@@ -746,13 +754,13 @@ ncclDataType_t nccl_type(msrep_dtype t) { return t == MSREP_F64 ? ncclDouble : n
 
 // allgatherv of per-rank segments of y (in place), as grouped broadcasts.
 msrep_status_t allgatherv_y(Ctx* c, void* y, const std::vector<int64_t>& lo, const std::vector<int64_t>& hi,
-                            cudaStream_t s) {
+                            cudaStream_t s, int k = 1) {
   const size_t V = vsz(c->dtype);
   NCCL_TRY(ncclGroupStart());
   for (int r = 0; r < c->nranks; r++) {
-    const int64_t cnt = hi[(size_t)r] - lo[(size_t)r];
+    const int64_t cnt = (hi[(size_t)r] - lo[(size_t)r]) * k;   // rows x k (row-major blocks)
     if (cnt <= 0) continue;
-    char* p = static_cast<char*>(y) + (size_t)lo[(size_t)r] * V;
+    char* p = static_cast<char*>(y) + (size_t)lo[(size_t)r] * k * V;
     NCCL_TRY(ncclBroadcast(p, p, (size_t)cnt, nccl_type(c->dtype), r, c->comm, s));
   }
   NCCL_TRY(ncclGroupEnd());
@@ -1195,7 +1203,7 @@ msrep_status_t msrep_spmv(msrep_ctx h, const void* alpha_p, const void* x, const
   CUDA_TRY(launch_rows(L, s));
   if (pe) CUDA_TRY(cudaEventRecord(pe, s));
   if (c->nranks > 1 && c->any_flag) {
-    HeadLaunch H{c->vparts, c->d_part_rec, c->d_rec, c->d_head_local};
+    HeadLaunch H{c->vparts, c->d_part_rec, c->d_rec, c->d_head_local, 1};
     CUDA_TRY(launch_heads(H, s));
     NCCL_TRY(ncclAllGather(c->d_head_local, c->d_head_all, (size_t)c->vparts, ncclDouble, c->comm, s));
   }
@@ -1205,10 +1213,68 @@ msrep_status_t msrep_spmv(msrep_ctx h, const void* alpha_p, const void* x, const
     F.sr_row = c->d_sr_row; F.sr_rec = c->d_sr_rec; F.sr_head = c->d_sr_head; F.head_list = c->d_head_list;
     F.part_rec = c->d_part_rec; F.part_lo = c->P0; F.part_hi = c->P1;
     F.head_all = c->d_head_all; F.rec = c->d_rec;
-    F.y = y; F.alpha = alpha; F.beta = beta; F.dtype = dt;
+    F.y = y; F.alpha = alpha; F.beta = beta; F.dtype = dt; F.k = 1;
     CUDA_TRY(launch_fixup(F, s));
   }
   if (gather) TRY(allgatherv_y(c, y, seg_lo, seg_hi, s));
+  return MSREP_OK;
+}
+
+msrep_status_t msrep_spmm(msrep_ctx h, const void* alpha_p, const void* X, const void* beta_p, void* Y, int k,
+                          msrep_layout layout, void* stream) {
+  if (!h) return fail(MSREP_ERR_INVALID_ARG, "ctx is NULL");
+  Ctx* c = reinterpret_cast<Ctx*>(h);
+  if (!c->ready) return fail(MSREP_ERR_STATE, "msrep_spmm before msrep_partition");
+  if (colwise(c->fmt)) return fail(MSREP_ERR_STATE, "msrep_spmm supports the row formats (pCSR, pCOO)");
+  if (k != 2 && k != 4 && k != 8) return fail(MSREP_ERR_INVALID_ARG, "k = %d (must be 2, 4 or 8)", k);
+  if (!alpha_p || !beta_p || (c->m > 0 && !Y) || (c->n > 0 && !X)) return fail(MSREP_ERR_INVALID_ARG, "NULL argument");
+  if (layout != MSREP_Y_REPLICATED && layout != MSREP_Y_OWNED) return fail(MSREP_ERR_INVALID_ARG, "layout %d", (int)layout);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const double alpha = get_scalar(alpha_p, c->dtype), beta = get_scalar(beta_p, c->dtype);
+  const size_t V = vsz(c->dtype);
+  const int dt = c->dtype == MSREP_F64 ? 0 : 1;
+  std::vector<int64_t> seg_lo, seg_hi;
+  owned_segments(c, seg_lo, seg_hi);
+  const int64_t my_lo = seg_lo[(size_t)c->rank], my_hi = seg_hi[(size_t)c->rank];
+  const bool gather = layout == MSREP_Y_REPLICATED && c->nranks > 1;
+  if (alpha == 0.0) {   // reading R12: Y = beta*Y, A and X not read
+    CUDA_TRY(launch_scale(static_cast<char*>(Y) + (size_t)my_lo * k * V, (my_hi - my_lo) * k, beta, dt, s));
+    if (gather) TRY(allgatherv_y(c, Y, seg_lo, seg_hi, s, k));
+    return MSREP_OK;
+  }
+  if (c->mm_k < k) {   // k-wide records and head partials, allocated on first use
+    void* q;
+    TRY(dalloc(c, (size_t)std::max(1, c->nrec) * 8 * 8, &q, s)); c->d_rec_mm = static_cast<double*>(q);
+    TRY(dalloc(c, (size_t)c->vparts * 8 * 8, &q, s)); c->d_head_local_mm = static_cast<double*>(q);
+    if (c->nranks > 1) { TRY(dalloc(c, (size_t)c->np * 8 * 8, &q, s)); c->d_head_all_mm = static_cast<double*>(q); }
+    c->mm_k = 8;
+  }
+  RowLaunch L{};
+  L.tiles = c->d_tiles; L.ntiles = c->ntiles;
+  L.blob = c->d_blob;
+  L.x = X; L.y = Y; L.ybase = c->wlo;
+  L.xmax = c->n > 0 ? (uint32_t)(c->n - 1) : 0u;
+  L.alpha = alpha; L.beta = beta; L.rec = c->d_rec_mm;
+  L.dtype = dt; L.has_sell = c->nsell > 0;
+  cudaEvent_t pe;
+  TRY(prof_begin(c, s, &pe));
+  CUDA_TRY(launch_rows_mm(L, k, s));
+  if (pe) CUDA_TRY(cudaEventRecord(pe, s));
+  if (c->nranks > 1 && c->any_flag) {
+    HeadLaunch H{c->vparts, c->d_part_rec, c->d_rec_mm, c->d_head_local_mm, k};
+    CUDA_TRY(launch_heads(H, s));
+    NCCL_TRY(ncclAllGather(c->d_head_local_mm, c->d_head_all_mm, (size_t)c->vparts * k, ncclDouble, c->comm, s));
+  }
+  if (c->nsplit) {
+    FixupLaunch F{};
+    F.nsplit = c->nsplit;
+    F.sr_row = c->d_sr_row; F.sr_rec = c->d_sr_rec; F.sr_head = c->d_sr_head; F.head_list = c->d_head_list;
+    F.part_rec = c->d_part_rec; F.part_lo = c->P0; F.part_hi = c->P1;
+    F.head_all = c->d_head_all_mm; F.rec = c->d_rec_mm;
+    F.y = Y; F.alpha = alpha; F.beta = beta; F.dtype = dt; F.k = k;
+    CUDA_TRY(launch_fixup(F, s));
+  }
+  if (gather) TRY(allgatherv_y(c, Y, seg_lo, seg_hi, s, k));
   return MSREP_OK;
 }
 

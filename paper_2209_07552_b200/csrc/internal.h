@@ -145,14 +145,17 @@ struct FixupLaunch {
   const double* head_all;                             // head sums of all parts (multi-rank), may be null
   const double* rec;
   void* y; double alpha, beta; int dtype;
+  int k;                                              // vectors (1: SpMV; SpMM block width)
 };
 
 struct HeadLaunch {
   int nlocal; const int32_t* part_rec; const double* rec; double* head_local;
+  int k;
 };
 
 // kernels.cu entry points (all enqueue on `s`)
 cudaError_t launch_rows(const RowLaunch& L, cudaStream_t s);
+cudaError_t launch_rows_mm(const RowLaunch& L, int k, cudaStream_t s);   // SpMM, k in {2, 4, 8}
 cudaError_t launch_cols(const ColLaunch& L, cudaStream_t s);
 cudaError_t launch_fixup(const FixupLaunch& L, cudaStream_t s);
 cudaError_t launch_heads(const HeadLaunch& L, cudaStream_t s);

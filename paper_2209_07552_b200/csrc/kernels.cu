@@ -396,6 +396,277 @@ __global__ void __launch_bounds__(WARPS * 32, MSREP_ROW_MINB) rows_kernel(const 
   }
 }
 
+// ------------------------------------------------------------------ SpMM
+// Y <- alpha*A*X + beta*Y for a block of K vectors (X [n x K], Y [m x K], row-major; the
+// "easily extended" multi-right-hand-side kernel).  Same tile list, blobs and
+// per-warp one-slot TMA ring as rows_kernel: the matrix is streamed once for all K vectors.
+// Each nonzero gathers one K-wide row of X (vector loads, L2 evict_last); lanes batch BG
+// gathers at a time so K-wide accumulators fit the register budget.
+template <typename VT, int K>
+__device__ __forceinline__ void ldx_row(const VT* p, VT (&o)[K], uint64_t pol) {
+  if constexpr (sizeof(VT) == 8) {
+#pragma unroll
+    for (int i = 0; i < K; i += 2)
+      asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(o[i]), "=d"(o[i + 1]) : "l"(p + i), "l"(pol));
+  } else if constexpr (K == 2) {
+    asm("ld.global.nc.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;" : "=f"(o[0]), "=f"(o[1]) : "l"(p), "l"(pol));
+  } else {
+#pragma unroll
+    for (int i = 0; i < K; i += 4)
+      asm("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+          : "=f"(o[i]), "=f"(o[i + 1]), "=f"(o[i + 2]), "=f"(o[i + 3]) : "l"(p + i), "l"(pol));
+  }
+}
+
+// Y row <- alpha * acc + beta * Y row (beta == 0: Y not read)
+template <typename VT, int K>
+__device__ __forceinline__ void mm_write_row(VT* yrow, const double (&acc)[K], double alpha, double beta) {
+#pragma unroll
+  for (int j = 0; j < K; j++) {
+    double o = alpha * acc[j];
+    if (beta != 0.0) o += beta * (double)yrow[j];
+    yrow[j] = (VT)o;
+  }
+}
+
+template <typename VT, int K, bool SELL>
+__global__ void __launch_bounds__(WARPS * 32, MSREP_ROW_MINB) rows_mm_kernel(const RowLaunch P) {
+  using Lay = RowLayout<VT, SELL>;
+  constexpr int QMAX = qmax<VT>();
+  constexpr int V = (int)sizeof(VT);
+  constexpr int BG = K >= 8 ? 1 : (K >= 4 ? 2 : 4);   // gathers in flight per lane per batch (SEG / slab)
+  constexpr int BS = 32 / K;                          // ... for SELL tiles (no chunk held in registers)
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned char* st = smem + warp * Lay::WARP_B;
+  int4* sdesc = reinterpret_cast<int4*>(st + Lay::DESC_OFF);
+  unsigned* written = reinterpret_cast<unsigned*>(st + Lay::SCR_OFF);   // MAX_TILE_ROWS-bit map
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Lay::BAR_OFF) + warp;
+  const int gw = blockIdx.x * WARPS + warp, nw = gridDim.x * WARPS;
+  const VT* __restrict__ x = static_cast<const VT*>(P.x);
+  VT* __restrict__ y = static_cast<VT*>(P.y);
+  const double alpha = P.alpha, beta = P.beta;
+  const uint32_t xmax = P.xmax;
+  const uint64_t xpol = policy_evict_last();
+
+  uint64_t pol = 0;
+  int4 dn = make_int4(0, 0, 0, -1);
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    pol = policy_evict_first();
+    if (gw < P.ntiles) {
+      const int4 d = P.tiles[gw];
+      *sdesc = d;
+      issue_blob(P.blob, d, tile_kind(d), V, st, bar, pol);
+    }
+    if (gw + nw < P.ntiles) dn = P.tiles[gw + nw];
+  }
+  __syncwarp();
+
+  for (int i = 0;; i++) {
+    const int t = gw + i * nw;
+    if (t >= P.ntiles) break;
+    mbar_wait(bar, (uint32_t)(i & 1));
+    const int4 d = *sdesc;
+    auto refill = [&]() {
+      if (lane == 0) {
+        const int tn = t + nw;
+        if (tn < P.ntiles) {
+          *sdesc = dn;
+          issue_blob(P.blob, dn, tile_kind(dn), V, st, bar, pol);
+          if (tn + nw < P.ntiles) dn = P.tiles[tn + nw];
+        }
+      }
+    };
+    if (SELL && d.w == -2) {
+      // ---- SELL tile: lane l walks its R rows; element t of row k at (t*R + k)*32 + l
+      const int nrows = d.z & 0xffff, W = d.z >> 16, R = sell_r(nrows);
+      const uint16_t* lens = reinterpret_cast<const uint16_t*>(st);
+      const VT* sv = reinterpret_cast<const VT*>(st + align16(R * 32 * 2));
+      const uint32_t* sc = reinterpret_cast<const uint32_t*>(st + align16(R * 32 * 2) + W * R * 32 * V);
+      for (int k = 0; k < R; k++) {
+        const int row = k * 32 + lane;
+        const int len = row < nrows ? lens[k * 32 + lane] : 0;
+        double acc[K];
+#pragma unroll
+        for (int j = 0; j < K; j++) acc[j] = 0.0;
+        for (int e0 = 0; e0 < W; e0 += BS) {
+          VT xr[BS][K];
+          VT vv[BS];
+#pragma unroll
+          for (int b = 0; b < BS; b++) {
+            const int e = e0 + b;
+            const bool on = e < len;
+            const uint32_t cc = on ? min(sc[(e * R + k) * 32 + lane], xmax) : 0u;
+            vv[b] = on ? sv[(e * R + k) * 32 + lane] : VT(0);
+            if (on) ldx_row<VT, K>(x + (int64_t)cc * K, xr[b], xpol);
+            else {
+#pragma unroll
+              for (int j = 0; j < K; j++) xr[b][j] = VT(0);
+            }
+          }
+#pragma unroll
+          for (int b = 0; b < BS; b++)
+#pragma unroll
+            for (int j = 0; j < K; j++) acc[j] = fma((double)vv[b], (double)xr[b][j], acc[j]);
+        }
+        if (row < nrows) mm_write_row<VT, K>(y + (P.ybase + d.x + row) * K, acc, alpha, beta);
+      }
+      __syncwarp();
+      refill();
+      continue;
+    }
+    const int nrows = d.z & 0xffff, nnz = d.z >> 16;
+    const bool slab = d.w >= 0;
+    const int q = slab ? 0 : nnz >> 5, r = nnz & 31;
+    const bool extra = !slab && lane < r;
+    uint32_t c[QMAX + 1];
+    VT v[QMAX + 1];
+    uint32_t kp[(QMAX + 4) / 4];
+#pragma unroll
+    for (int u = 0; u < (QMAX + 4) / 4; u++) kp[u] = 0u;
+    if (slab) {
+      const VT* sv = reinterpret_cast<const VT*>(st);
+      const uint32_t* sc = reinterpret_cast<const uint32_t*>(st + align16(nnz * V));
+#pragma unroll
+      for (int u = 0; u < QMAX; u++) {
+        const bool on = lane + 32 * u < nnz;
+        c[u] = on ? min(sc[lane + 32 * u], xmax) : 0u;
+        v[u] = on ? sv[lane + 32 * u] : VT(0);
+      }
+      c[QMAX] = 0u;
+      v[QMAX] = VT(0);
+    } else {
+      const uint8_t* sk = st;
+      const VT* sv = reinterpret_cast<const VT*>(st + align16(nnz));
+      const uint32_t* sc = reinterpret_cast<const uint32_t*>(st + align16(nnz) + align16(nnz * V));
+#pragma unroll
+      for (int j = 0; j <= QMAX; j++) {
+        const bool on = j < QMAX ? j < q : extra;
+        const int sl = (j < QMAX ? j : q) * 32 + lane;
+        c[j] = on ? min(sc[sl], xmax) : 0u;
+        v[j] = on ? sv[sl] : VT(0);
+        if (on) kp[j >> 2] |= (uint32_t)sk[sl] << (8 * (j & 3));
+      }
+    }
+    fence_proxy_async();   // order this lane's generic-proxy reads of the slot before the TMA refill
+    __syncwarp();
+    refill();
+    if (slab) {
+      // ---- slab: K partial sums of one split row -> rec[w*K + j] (natural order, fixed tree)
+      double acc[K];
+#pragma unroll
+      for (int j = 0; j < K; j++) acc[j] = 0.0;
+#pragma unroll
+      for (int u0 = 0; u0 < QMAX; u0 += BG) {
+        VT xr[BG][K];
+#pragma unroll
+        for (int b = 0; b < BG; b++) {
+          if (lane + 32 * (u0 + b) < nnz) ldx_row<VT, K>(x + (int64_t)c[u0 + b] * K, xr[b], xpol);
+          else {
+#pragma unroll
+            for (int j = 0; j < K; j++) xr[b][j] = VT(0);
+          }
+        }
+#pragma unroll
+        for (int b = 0; b < BG; b++)
+#pragma unroll
+          for (int j = 0; j < K; j++) acc[j] = fma((double)v[u0 + b], (double)xr[b][j], acc[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < K; j++) {
+        double a = acc[j];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(FULL, a, off);
+        if (lane == 0) P.rec[(int64_t)d.w * K + j] = a;
+      }
+      continue;
+    }
+    // ---- SEG tile
+    const int64_t yrow0 = P.ybase + d.x;
+    if (lane < MAX_TILE_ROWS / 32) written[lane] = 0u;
+    __syncwarp();
+    auto put_row = [&](int row, const double (&a)[K]) {
+      mm_write_row<VT, K>(y + (yrow0 + row) * K, a, alpha, beta);
+      atomicOr(&written[row >> 5], 1u << (row & 31));
+    };
+    const int len = q + (extra ? 1 : 0);
+    const int key0 = (int)(q > 0 ? (kp[0] & 0xffu) : (kp[QMAX >> 2] >> (8 * (QMAX & 3))) & 0xffu);
+    int cur = len > 0 ? key0 : INT_MAX;
+    int first = cur, nseg = len > 0 ? 1 : 0;
+    double acc[K], firstv[K];
+#pragma unroll
+    for (int j = 0; j < K; j++) { acc[j] = 0.0; firstv[j] = 0.0; }
+#pragma unroll
+    for (int j0 = 0; j0 <= QMAX; j0 += BG) {
+      VT xr[BG][K];
+#pragma unroll
+      for (int b = 0; b < BG; b++) {
+        const int j = j0 + b;
+        const bool on = j <= QMAX && (j < QMAX ? j < q : extra);
+        if (on) ldx_row<VT, K>(x + (int64_t)c[j <= QMAX ? j : QMAX] * K, xr[b], xpol);
+        else {
+#pragma unroll
+          for (int jj = 0; jj < K; jj++) xr[b][jj] = VT(0);
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < BG; b++) {
+        const int j = j0 + b;
+        const bool on = j <= QMAX && (j < QMAX ? j < q : extra);
+        if (on) {
+          const int jc = j <= QMAX ? j : QMAX;
+          const int kk = (int)((kp[jc >> 2] >> (8 * (jc & 3))) & 0xffu);
+          if (kk != cur) {
+            if (nseg == 1) {
+#pragma unroll
+              for (int jj = 0; jj < K; jj++) firstv[jj] = acc[jj];
+            } else {
+              put_row(cur, acc);
+            }
+            nseg++;
+            cur = kk;
+#pragma unroll
+            for (int jj = 0; jj < K; jj++) acc[jj] = 0.0;
+          }
+#pragma unroll
+          for (int jj = 0; jj < K; jj++) acc[jj] = fma((double)v[jc], (double)xr[b][jj], acc[jj]);
+        }
+      }
+    }
+    // rows crossing lanes: one deterministic segmented scan per vector
+    int pk = INT_MIN;
+    double pv[K];
+#pragma unroll
+    for (int jj = 0; jj < K; jj++) warp_seg_scan(cur, acc[jj], pk, pv[jj]);
+    const int next_first = __shfl_down_sync(FULL, key0, 1);
+    const bool next_has = lane < 31 && (q > 0 || lane + 1 < r);
+    if (nseg >= 2) {
+      double h[K];
+#pragma unroll
+      for (int jj = 0; jj < K; jj++) h[jj] = (pk == first) ? firstv[jj] + pv[jj] : firstv[jj];
+      put_row(first, h);
+    }
+    if (nseg >= 1 && !(next_has && next_first == cur)) {
+      double h[K];
+#pragma unroll
+      for (int jj = 0; jj < K; jj++) h[jj] = (pk == cur) ? pv[jj] + acc[jj] : acc[jj];
+      put_row(cur, h);
+    }
+    __syncwarp();
+    // rows of the tile with no nonzero: Y = beta * Y
+    for (int rr = lane; rr < nrows; rr += 32)
+      if (!((written[rr >> 5] >> (rr & 31)) & 1u)) {
+        double z[K];
+#pragma unroll
+        for (int jj = 0; jj < K; jj++) z[jj] = 0.0;
+        mm_write_row<VT, K>(y + (yrow0 + rr) * K, z, alpha, beta);
+      }
+    __syncwarp();
+  }
+}
+
 // ------------------------------------------------------------------ pCSC
 // pCSC per-GPU kernel (Alg. 5 "Launch": each part scatters its
 // columns' contributions into a partial y, "switch the role of x and y",
@@ -692,36 +963,40 @@ __global__ void pack_kernel(const PackLaunch L) {
 }
 
 // --------------------------------------------------------- small kernels
+// one thread per (split row, vector j < k): k = 1 for SpMV, the block width for SpMM; records,
+// head partials and y are k-wide (record r, vector j at r*k + j; y row-major [m x k])
 template <typename VT>
 __global__ void fixup_kernel(const FixupLaunch F) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= F.nsplit) return;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)F.nsplit * F.k) return;
+  const int s = (int)(t / F.k), jv = (int)(t % F.k), K = F.k;
   double acc = 0.0;
-  for (int k = F.sr_rec[2 * s]; k < F.sr_rec[2 * s + 1]; k++) acc = acc + F.rec[k];
+  for (int k = F.sr_rec[2 * s]; k < F.sr_rec[2 * s + 1]; k++) acc = acc + F.rec[(int64_t)k * K + jv];
   for (int h = F.sr_head[2 * s]; h < F.sr_head[2 * s + 1]; h++) {
     const int j = F.head_list[h];
     double hv = 0.0;
     if (j >= F.part_lo && j < F.part_hi) {
       const int jl = j - F.part_lo;
-      for (int k = F.part_rec[2 * jl]; k < F.part_rec[2 * jl + 1]; k++) hv = hv + F.rec[k];
+      for (int k = F.part_rec[2 * jl]; k < F.part_rec[2 * jl + 1]; k++) hv = hv + F.rec[(int64_t)k * K + jv];
     } else {
-      hv = F.head_all[j];
+      hv = F.head_all[(int64_t)j * K + jv];
     }
     acc = acc + hv;
   }
   VT* y = static_cast<VT*>(F.y);
-  const int64_t r = F.sr_row[s];
+  const int64_t r = F.sr_row[s] * K + jv;
   double v = F.alpha * acc;
   if (F.beta != 0.0) v += F.beta * (double)y[r];
   y[r] = (VT)v;
 }
 
 __global__ void heads_kernel(const HeadLaunch H) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= H.nlocal) return;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= H.nlocal * H.k) return;
+  const int j = t / H.k, jv = t % H.k;
   double hv = 0.0;
-  for (int k = H.part_rec[2 * j]; k < H.part_rec[2 * j + 1]; k++) hv = hv + H.rec[k];
-  H.head_local[j] = hv;
+  for (int k = H.part_rec[2 * j]; k < H.part_rec[2 * j + 1]; k++) hv = hv + H.rec[(int64_t)k * H.k + jv];
+  H.head_local[t] = hv;
 }
 
 template <typename VT>
@@ -916,7 +1191,7 @@ cudaError_t launch_pack(const PackLaunch& L, cudaStream_t s) {
 
 cudaError_t launch_fixup(const FixupLaunch& F, cudaStream_t s) {
   if (F.nsplit == 0) return cudaSuccess;
-  int g = (F.nsplit + 127) / 128;
+  int g = (F.nsplit * F.k + 127) / 128;
   if (F.dtype == 0) fixup_kernel<double><<<g, 128, 0, s>>>(F);
   else fixup_kernel<float><<<g, 128, 0, s>>>(F);
   return cudaGetLastError();
@@ -924,7 +1199,7 @@ cudaError_t launch_fixup(const FixupLaunch& F, cudaStream_t s) {
 
 cudaError_t launch_heads(const HeadLaunch& H, cudaStream_t s) {
   if (H.nlocal == 0) return cudaSuccess;
-  heads_kernel<<<(H.nlocal + 127) / 128, 128, 0, s>>>(H);
+  heads_kernel<<<(H.nlocal * H.k + 127) / 128, 128, 0, s>>>(H);
   return cudaGetLastError();
 }
 
@@ -968,6 +1243,33 @@ cudaError_t launch_cg(int op, int dtype, void* a, void* b, void* c, const void* 
     cg_sum_kernel<<<1, CG_THREADS, 0, s>>>(part_in, sc);
   }
   return cudaGetLastError();
+}
+
+namespace {
+template <typename VT, int K, bool SELL>
+cudaError_t launch_rows_mm_t(const RowLaunch& L, cudaStream_t s) {
+  constexpr int b = RowLayout<VT, SELL>::TOTAL;
+  cudaError_t e = set_smem(rows_mm_kernel<VT, K, SELL>, b);
+  if (e) return e;
+  rows_mm_kernel<VT, K, SELL><<<grid_for(rows_mm_kernel<VT, K, SELL>, b, L.ntiles), WARPS * 32, b, s>>>(L);
+  return cudaGetLastError();
+}
+template <typename VT, int K>
+cudaError_t launch_rows_mm_k(const RowLaunch& L, cudaStream_t s) {
+  return L.has_sell ? launch_rows_mm_t<VT, K, true>(L, s) : launch_rows_mm_t<VT, K, false>(L, s);
+}
+}  // namespace
+
+cudaError_t launch_rows_mm(const RowLaunch& L, int k, cudaStream_t s) {
+  if (L.ntiles == 0) return cudaSuccess;
+  if (L.dtype == 0) {
+    if (k == 2) return launch_rows_mm_k<double, 2>(L, s);
+    if (k == 4) return launch_rows_mm_k<double, 4>(L, s);
+    return launch_rows_mm_k<double, 8>(L, s);
+  }
+  if (k == 2) return launch_rows_mm_k<float, 2>(L, s);
+  if (k == 4) return launch_rows_mm_k<float, 4>(L, s);
+  return launch_rows_mm_k<float, 8>(L, s);
 }
 
 }  // namespace msrep

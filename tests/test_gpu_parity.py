@@ -444,3 +444,77 @@ def test_cg_errors():
         ctx.cg(torch.zeros(20, dtype=torch.float64, device="cuda"), torch.zeros(30, dtype=torch.float64, device="cuda"))
     assert e.value.status == 2
     ctx.close()
+
+
+# ------------------------------------------------------------ SpMM (NEXT f4)
+def _spmm_gpu(A, fmt, X, Y, alpha, beta, parts):
+    import paper_2209_07552_b200 as M
+    import torch
+    B = as_fmt(A, fmt)
+    ctx = M.Context(0, 1, None, 0, parts)
+    if fmt == "coo":
+        ctx.partition("coo", B["m"], B["n"], idx=B["idx"], val=B["val"], coo_row=coo_of_csr(B))
+    else:
+        ctx.partition(fmt, B["m"], B["n"], ptr=B["ptr"], idx=B["idx"], val=B["val"])
+    Xd = torch.as_tensor(np.ascontiguousarray(X)).cuda()
+    Yd = torch.as_tensor(np.ascontiguousarray(Y)).cuda()
+    ctx.spmm(alpha, Xd, beta, Yd)
+    torch.cuda.synchronize()
+    out = Yd.cpu().numpy()
+    ctx.close()
+    return out
+
+
+def _spmm_ref(A, X, Y, alpha, beta):
+    return np.stack([oracle_ref(A, X[:, j].copy(), Y[:, j].copy(), alpha, beta) for j in range(X.shape[1])], axis=1)
+
+
+@pytest.mark.parametrize("fmt", ["csr", "coo"])
+@pytest.mark.parametrize("k", [2, 4, 8])
+def test_spmm_bit_exact(fmt, k):
+    """Y = alpha*A*X + beta*Y for k vectors at once equals k oracle SpMVs bit for bit (integer
+    data): R-MAT (SEG tiles, slabs, split rows), the stencil (SELL tiles), short regular rows
+    (4-row-per-lane SELL), a chain row across parts; 1 and 3 parts; beta = 0 and alpha = 0."""
+    cases = [gen.rmat(11, seed=21, kind=gen.SMALLINT), gen.stencil27(9, kind=gen.SMALLINT),
+             gen.kdistinct_csr(700, 900, 5, seed=22, kind=gen.SMALLINT),
+             gen.Sparse(fmt="csr", m=1, n=3000, ptr=np.array([0, 3000], np.int64), idx=np.arange(3000, dtype=np.int32),
+                        val=np.ones(3000))]
+    rng = np.random.default_rng(k)
+    for A in cases:
+        X = rng.integers(-4, 5, (A["n"], k)).astype(np.float64)
+        Y = rng.integers(-4, 5, (A["m"], k)).astype(np.float64)
+        for parts in (1, 3):
+            for alpha, beta in ((1.5, 0.5), (2.0, 0.0), (0.0, -1.0)):
+                got = _spmm_gpu(A, fmt, X, Y, alpha, beta, parts)
+                assert np.array_equal(got, _spmm_ref(A, X, Y, alpha, beta)), (fmt, k, parts, alpha, beta)
+
+
+@pytest.mark.parametrize("k", [2, 4, 8])
+def test_spmm_fp32_tolerance(k):
+    A = to_dtype(gen.rmat(10, seed=23), np.float32)
+    rng = np.random.default_rng(30 + k)
+    X = rng.uniform(-1, 1, (A["n"], k)).astype(np.float32)
+    Y = rng.uniform(-1, 1, (A["m"], k)).astype(np.float32)
+    got = _spmm_gpu(A, "csr", X, Y, 1.5, 0.5, 2)
+    for j in range(k):
+        x, y = X[:, j].copy(), Y[:, j].copy()
+        assert_close(got[:, j], oracle_ref(A, x, y, 1.5, 0.5), row_bound(A, x, y, 1.5, 0.5), np.float32)
+
+
+def test_spmm_rejects_colwise_and_bad_k():
+    import paper_2209_07552_b200 as M
+    import torch
+    A = gen.transpose(gen.kdistinct_csr(50, 40, 3, seed=3))
+    ctx = M.Context(0, 1, None, 0, 1)
+    ctx.partition("csc", 50, 40, ptr=A["ptr"], idx=A["idx"], val=A["val"])
+    with pytest.raises(M.MsrepError) as e:
+        ctx.spmm(1.0, torch.zeros((40, 4), dtype=torch.float64, device="cuda"), 0.0,
+                 torch.zeros((50, 4), dtype=torch.float64, device="cuda"))
+    assert e.value.status == 5
+    B = gen.kdistinct_csr(50, 40, 3, seed=3)
+    ctx.partition("csr", 50, 40, ptr=B["ptr"], idx=B["idx"], val=B["val"])
+    with pytest.raises(M.MsrepError) as e:
+        ctx.spmm(1.0, torch.zeros((40, 3), dtype=torch.float64, device="cuda"), 0.0,
+                 torch.zeros((50, 3), dtype=torch.float64, device="cuda"))
+    assert e.value.status == 1
+    ctx.close()
