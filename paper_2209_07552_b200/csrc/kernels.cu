@@ -5,26 +5,25 @@
 // the design goal is to keep enough bytes in flight to saturate HBM3e.
 //
 //  rows_kernel  pCSR / pCOO per-GPU SpMV (Alg. 3 / Alg. 7 "Launch:
-//               py[i]=<csrSpMVKernel>").  Persistent CTAs
-//               walk a static, row-aligned tile schedule built at partition
-//               time.  Each tile's val / col_idx / row-pointer (or COO row_idx)
-//               slices are staged into shared memory with 1-D TMA bulk copies
-//               (cp.async.bulk + mbarrier, L2 evict_first) in an S-stage ring;
-//               products val*x[col] are formed in a coalesced pass (x gathered
-//               through the read-only path), then a merge-path walk (CSR) or a
-//               key-segmented walk (COO) plus a deterministic block segmented
-//               scan produces whole-row sums, written as y = alpha*s + beta*y
-//               in a coalesced epilogue.  Split rows (rows shared with another
-//               part, and rows longer than a tile) are "slab" tiles
-//               whose partial goes to a record -- no float atomics, so results
-//               are bit-reproducible.
+//               py[i]=<csrSpMVKernel>"): ONE persistent
+//               launch per SpMV.  Every warp owns a one-slot ring of tile blobs
+//               moved by 1-D TMA bulk copies (cp.async.bulk + mbarrier, L2
+//               evict_first) and walks a static tile list built at partition
+//               time (internal.h): SELL tiles (regular rows, lane = row), SEG
+//               tiles (irregular rows, lane-chunked nonzeros with u8 row keys,
+//               reduced in registers and joined by one deterministic warp
+//               segmented scan) and slabs (pieces of split rows, whose
+//               partial goes to a record).  No float atomics: bit-reproducible.
+//  rows_mm_kernel  the same walk for a block of k vectors (SpMM).
 //  fixup_kernel the beta-deferred merge of split rows (reading R6):
 //               y_r = alpha*(tail records + head partials, part order) + beta*y_r.
-//  csc_band_kernel  pCSC scatter (Alg. 5; "switch the role of x
-//               and y"): one CTA per row band, fp64 partial y in
-//               shared memory, band entries TMA-streamed in CSC order, the
-//               alpha/beta epilogue (or the py write for the reduce-scatter)
-//               fused at band end.
+//  csc_band_kernel  pCSC / column-sorted pCOO scatter (Alg. 5, P:418-423;
+//               "switch the role of x and y"): one CTA per row band,
+//               fp64 partial y in shared memory with warp-owned rows (plain
+//               read-modify-writes, no atomics), stage blobs TMA-streamed by a
+//               producer warp, the alpha/beta epilogue (or the py write for the
+//               reduce-scatter) fused at band end.
+//  cg_*         the vector kernels of msrep_cg.
 #include <climits>
 #include <cstdint>
 
@@ -150,12 +149,6 @@ __device__ __forceinline__ void issue_blob(const char* blob, int4 d, int kind, i
   tma_1d(st, blob + (int64_t)d.y * 16, (uint32_t)bytes, bar, pol);
 }
 
-// pCSR / pCOO segment-tile kernel (SELL tiles run in sell_kernel).  Tile kinds:
-//   w >= 0   slab: partial sum of a piece of one split row -> rec[w]
-//   w == -1  SEG tile: whole rows; lane l reduces its contiguous chunk of
-//            nonzeros in registers (keyed by the uint8 tile-local row), rows
-//            crossing lanes are joined by one deterministic warp segmented
-//            scan, y = alpha*s + beta*y is written coalesced.
 // pCSR / pCOO tile kernel: ONE persistent launch per SpMV.  Every warp owns a
 // one-slot TMA ring and walks tiles gw, gw+nw, ... of the rank's tile list
 // (SELL tiles first, then SEG / slab tiles; internal.h).
