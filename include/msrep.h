@@ -157,6 +157,20 @@ msrep_status_t msrep_partition(msrep_ctx ctx, msrep_format fmt, msrep_dtype dtyp
 msrep_status_t msrep_spmv(msrep_ctx ctx, const void* alpha, const void* x, const void* beta, void* y,
                           msrep_layout layout, void* stream);
 
+/* Fused compute + allgather for the row formats ("epilogue peer
+ * stores"): y <- alpha*A*x + beta*y on this rank's owned rows, and every
+ * owned row is ALSO stored, tile by tile from the SpMV epilogue (and the
+ * split-row fix-up), into each of the `nmirror` (<= 8) device buffers
+ * `mirrors` -- the other ranks' y buffers mapped into this process (CUDA IPC
+ * / symmetric memory over NVLink), or local buffers.  With every peer's y in
+ * `mirrors`, each rank ends with the full y without an allgatherv: the
+ * transfer overlaps the SpMV.  When nranks > 1 a one-integer NCCL all-reduce
+ * after the kernels fences the stores (every rank's mirror writes are complete
+ * when the call's work on `stream` completes).  y_in is read only from `y`
+ * (beta != 0).  pCSC / column-sorted pCOO: MSREP_ERR_STATE. */
+msrep_status_t msrep_spmv_mirror(msrep_ctx ctx, const void* alpha, const void* x, const void* beta, void* y,
+                                 int nmirror, void* const* mirrors, void* stream);
+
 /* End-to-end variant with HOST vectors: copies x[n] and (if beta != 0) y[m]
  * from host memory (pinned recommended) to context-owned device buffers,
  * runs msrep_spmv, and copies back the rows this rank's layout defines into

@@ -76,6 +76,7 @@ _sig = {
     "msrep_set_split": [P, I],
     "msrep_cg": [P, P, P, ctypes.c_double, I, I, ctypes.POINTER(I), ctypes.POINTER(ctypes.c_double), P],
     "msrep_spmm": [P, P, P, P, P, I, I, P],
+    "msrep_spmv_mirror": [P, P, P, P, P, I, P, P],
     "msrep_get_stats": [P, ctypes.POINTER(Stats)],
     "msrep_destroy": [P],
     "msrep_profile_enable": [P, I],
@@ -90,7 +91,7 @@ _lib.msrep_version.argtypes = []
 _lib.msrep_version.restype = ctypes.c_int
 
 EXPORTED = ["msrep_get_unique_id", "msrep_create", "msrep_partition", "msrep_spmv", "msrep_spmv_host",
-            "msrep_plan", "msrep_plan_split", "msrep_set_split", "msrep_cg", "msrep_spmm", "msrep_exchange_plan", "msrep_get_stats", "msrep_destroy", "msrep_last_error", "msrep_version",
+            "msrep_plan", "msrep_plan_split", "msrep_set_split", "msrep_cg", "msrep_spmm", "msrep_spmv_mirror", "msrep_exchange_plan", "msrep_get_stats", "msrep_destroy", "msrep_last_error", "msrep_version",
             "msrep_profile_enable", "msrep_profile_read"]
 
 
@@ -205,6 +206,15 @@ def msrep_spmm(ctx, alpha, X, beta, Y, k, layout=Y_REPLICATED, stream=None, dtyp
            "msrep_spmm")
 
 
+def msrep_spmv_mirror(ctx, alpha, x, beta, y, mirrors, stream=None, dtype=F64):
+    """y <- alpha*A*x + beta*y on the owned rows, each row also stored into every buffer in
+    `mirrors` (device pointers or tensors: the peers' y, or local buffers)."""
+    a, b = _scalar(alpha, dtype), _scalar(beta, dtype)
+    arr = (ctypes.c_void_p * max(1, len(mirrors)))(*[_ptr(mm) for mm in mirrors])
+    _check(_lib.msrep_spmv_mirror(ctx, ctypes.byref(a), _ptr(x), ctypes.byref(b), _ptr(y), len(mirrors),
+                                  ctypes.cast(arr, P), stream), "msrep_spmv_mirror")
+
+
 def msrep_cg(ctx, b, x, tol=1e-10, maxit=1000, check_every=10, stream=None):
     """CG on the partitioned SPD matrix (include/msrep.h): x (device, in/out) <- iterate.
     Returns (iterations, ||r|| / ||b||)."""
@@ -290,6 +300,12 @@ class Context:
 
     def stats(self):
         return msrep_get_stats(self.h)
+
+    def spmv_mirror(self, alpha, x, beta, y, mirrors, stream=None):
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream().cuda_stream
+        msrep_spmv_mirror(self.h, alpha, x, beta, y, mirrors, stream, self.dtype)
 
     def spmm(self, alpha, X, beta, Y, layout=Y_REPLICATED, stream=None):
         """X: torch [n, k], Y: torch [m, k] (contiguous, row-major), k in {2, 4, 8}."""

@@ -166,6 +166,7 @@ struct Ctx {
   int32_t* d_part_rec = nullptr;
   double* d_head_local = nullptr;
   double* d_head_all = nullptr;
+  int* d_fence = nullptr;            // msrep_spmv_mirror completion fence (nranks > 1)
   double* d_py = nullptr;
   int64_t py_len = 0;
   // pCSC row-band layout
@@ -1082,6 +1083,8 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
       if (c->nranks > 1) {
         TRY(dalloc(c, (size_t)c->np * 8, &hp, s));
         c->d_head_all = static_cast<double*>(hp);
+        TRY(dalloc(c, 16, &hp, s));
+        c->d_fence = static_cast<int*>(hp);
       }
       c->nheads_local = 0;
       for (int j = P0; j < P1; j++) c->nheads_local += parts[(size_t)j].start_flag ? 1 : 0;
@@ -1138,8 +1141,35 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   return MSREP_OK;
 }
 
+msrep_status_t spmv_impl(msrep_ctx h, const void* alpha_p, const void* x, const void* beta_p, void* y,
+                         msrep_layout layout, void* stream, int nmirror, void* const* mirrors);
+
 msrep_status_t msrep_spmv(msrep_ctx h, const void* alpha_p, const void* x, const void* beta_p, void* y,
                           msrep_layout layout, void* stream) {
+  return spmv_impl(h, alpha_p, x, beta_p, y, layout, stream, 0, nullptr);
+}
+
+msrep_status_t msrep_spmv_mirror(msrep_ctx h, const void* alpha_p, const void* x, const void* beta_p, void* y,
+                                 int nmirror, void* const* mirrors, void* stream) {
+  if (!h) return fail(MSREP_ERR_INVALID_ARG, "ctx is NULL");
+  Ctx* c = reinterpret_cast<Ctx*>(h);
+  if (!c->ready) return fail(MSREP_ERR_STATE, "msrep_spmv_mirror before msrep_partition");
+  if (colwise(c->fmt)) return fail(MSREP_ERR_STATE, "msrep_spmv_mirror supports the row formats (pCSR, pCOO)");
+  if (nmirror < 0 || nmirror > MAX_MIRRORS || (nmirror > 0 && !mirrors))
+    return fail(MSREP_ERR_INVALID_ARG, "nmirror %d (0..%d)", nmirror, MAX_MIRRORS);
+  for (int i = 0; i < nmirror; i++)
+    if (!mirrors[i]) return fail(MSREP_ERR_INVALID_ARG, "mirror %d is NULL", i);
+  TRY(spmv_impl(h, alpha_p, x, beta_p, y, MSREP_Y_OWNED, stream, nmirror, mirrors));
+  if (c->nranks > 1) {   // completion fence: every rank's stores into every mirror are done
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CUDA_TRY(cudaMemsetAsync(c->d_fence, 0, sizeof(int), s));
+    NCCL_TRY(ncclAllReduce(c->d_fence, c->d_fence, 1, ncclInt, ncclSum, c->comm, s));
+  }
+  return MSREP_OK;
+}
+
+msrep_status_t spmv_impl(msrep_ctx h, const void* alpha_p, const void* x, const void* beta_p, void* y,
+                         msrep_layout layout, void* stream, int nmirror, void* const* mirrors) {
   if (!h) return fail(MSREP_ERR_INVALID_ARG, "ctx is NULL");
   Ctx* c = reinterpret_cast<Ctx*>(h);
   if (!c->ready) return fail(MSREP_ERR_STATE, "msrep_spmv before msrep_partition");
@@ -1160,6 +1190,10 @@ msrep_status_t msrep_spmv(msrep_ctx h, const void* alpha_p, const void* x, const
 
   if (alpha == 0.0) {   // reading R12: y = beta*y, A and x not read
     CUDA_TRY(launch_scale(static_cast<char*>(y) + (size_t)my_lo * V, my_hi - my_lo, beta, dt, s));
+    for (int mi = 0; mi < nmirror; mi++)
+      if (my_hi > my_lo)
+        CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(mirrors[mi]) + (size_t)my_lo * V, static_cast<char*>(y) + (size_t)my_lo * V,
+                                 (size_t)(my_hi - my_lo) * V, cudaMemcpyDefault, s));
     if (gather) TRY(allgatherv_y(c, y, seg_lo, seg_hi, s));
     return MSREP_OK;
   }
@@ -1197,7 +1231,8 @@ msrep_status_t msrep_spmv(msrep_ctx h, const void* alpha_p, const void* x, const
   L.xmax = c->n > 0 ? (uint32_t)(c->n - 1) : 0u;
   L.alpha = alpha; L.beta = beta; L.rec = c->d_rec;
   L.dtype = dt; L.has_sell = c->nsell > 0;
-
+  L.nmirror = nmirror;
+  for (int mi = 0; mi < nmirror; mi++) L.mirror[mi] = mirrors[mi];
   cudaEvent_t pe;
   TRY(prof_begin(c, s, &pe));
   CUDA_TRY(launch_rows(L, s));
@@ -1214,6 +1249,8 @@ msrep_status_t msrep_spmv(msrep_ctx h, const void* alpha_p, const void* x, const
     F.part_rec = c->d_part_rec; F.part_lo = c->P0; F.part_hi = c->P1;
     F.head_all = c->d_head_all; F.rec = c->d_rec;
     F.y = y; F.alpha = alpha; F.beta = beta; F.dtype = dt; F.k = 1;
+    F.nmirror = nmirror;
+    for (int mi = 0; mi < nmirror; mi++) F.mirror[mi] = mirrors[mi];
     CUDA_TRY(launch_fixup(F, s));
   }
   if (gather) TRY(allgatherv_y(c, y, seg_lo, seg_hi, s));

@@ -81,6 +81,8 @@ struct PackLaunch {        // build the tile blobs from the rank's plain slices 
   char* blob;
 };
 
+constexpr int MAX_MIRRORS = 8;   // msrep_spmv_mirror: extra y buffers (peer-mapped or local)
+
 struct RowLaunch {
   const int4* tiles; int ntiles;
   const char* blob;
@@ -89,6 +91,7 @@ struct RowLaunch {
   double alpha, beta; double* rec;
   int dtype;                                                 // dtype 0 = f64, 1 = f32
   int has_sell;                                              // tiles begin with SELL tiles
+  int nmirror; void* mirror[MAX_MIRRORS];                    // y rows are also stored here (msrep_spmv_mirror)
 };
 
 // pCSC row-band layout.  The rank's nonzeros are regrouped
@@ -146,6 +149,7 @@ struct FixupLaunch {
   const double* rec;
   void* y; double alpha, beta; int dtype;
   int k;                                              // vectors (1: SpMV; SpMM block width)
+  int nmirror; void* mirror[MAX_MIRRORS];             // split-row results are also stored here
 };
 
 struct HeadLaunch {

@@ -215,7 +215,9 @@ __device__ __forceinline__ void sell_tile(const RowLaunch& P, const int4 d, cons
     if (row < nrows) {
       double o = alpha * acc[k];
       if (beta != 0.0) o += beta * yv[k];
-      y[P.ybase + d.x + row] = (VT)o;
+      const int64_t yi = P.ybase + d.x + row;
+      y[yi] = (VT)o;
+      for (int mi = 0; mi < P.nmirror; mi++) static_cast<VT*>(P.mirror[mi])[yi] = (VT)o;   // fused allgather
     }
   }
   __syncwarp();   // the tile was read in place: refill the slot only now
@@ -383,6 +385,7 @@ __global__ void __launch_bounds__(WARPS * 32, MSREP_ROW_MINB) rows_kernel(const 
         double o = alpha * rsum[rr];
         if (beta != 0.0) o += beta * yin[u];
         __stcs(y + yrow0 + rr, (VT)o);
+        for (int mi = 0; mi < P.nmirror; mi++) static_cast<VT*>(P.mirror[mi])[yrow0 + rr] = (VT)o;   // fused allgather
       }
     }
     __syncwarp();   // rsum is free
@@ -981,6 +984,7 @@ __global__ void fixup_kernel(const FixupLaunch F) {
   double v = F.alpha * acc;
   if (F.beta != 0.0) v += F.beta * (double)y[r];
   y[r] = (VT)v;
+  for (int mi = 0; mi < F.nmirror; mi++) static_cast<VT*>(F.mirror[mi])[r] = (VT)v;
 }
 
 __global__ void heads_kernel(const HeadLaunch H) {

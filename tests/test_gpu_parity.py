@@ -518,3 +518,45 @@ def test_spmm_rejects_colwise_and_bad_k():
                  torch.zeros((50, 3), dtype=torch.float64, device="cuda"))
     assert e.value.status == 1
     ctx.close()
+
+
+# ------------------------------------- fused compute + allgather stores (msrep_spmv_mirror)
+@pytest.mark.parametrize("fmt", ["csr", "coo"])
+@pytest.mark.parametrize("parts", [1, 3])
+def test_spmv_mirror_loopback(fmt, parts):
+    """Loopback check of the epilogue's multi-destination stores on one GPU: the mirrors are
+    local buffers pre-filled with NaN; after the call y and every mirror equal the oracle
+    (bit-exact, integer data), including split rows written by the fix-up (R-MAT heavy rows)
+    and SELL tiles (stencil); alpha = 0 copies beta*y into the mirrors."""
+    import paper_2209_07552_b200 as M
+    import torch
+    for A in (gen.rmat(12, seed=31, kind=gen.SMALLINT), gen.stencil27(10, kind=gen.SMALLINT)):
+        x = gen.vector(A["n"], 32, kind=gen.SMALLINT); y = gen.vector(A["m"], 33, kind=gen.SMALLINT)
+        ctx = M.Context(0, 1, None, 0, parts)
+        if fmt == "coo":
+            ctx.partition("coo", A["m"], A["n"], idx=A["idx"], val=A["val"], coo_row=coo_of_csr(A))
+        else:
+            ctx.partition("csr", A["m"], A["n"], ptr=A["ptr"], idx=A["idx"], val=A["val"])
+        for alpha, beta in ((1.5, 0.5), (0.0, 2.0)):
+            xd = torch.as_tensor(x).cuda(); yd = torch.as_tensor(y.copy()).cuda()
+            mirrors = [torch.full((A["m"],), float("nan"), dtype=torch.float64, device="cuda") for _ in range(3)]
+            ctx.spmv_mirror(alpha, xd, beta, yd, mirrors)
+            torch.cuda.synchronize()
+            ref = oracle_ref(A, x, y, alpha, beta)
+            assert np.array_equal(yd.cpu().numpy(), ref)
+            for mm in mirrors:
+                assert np.array_equal(mm.cpu().numpy(), ref)
+        ctx.close()
+
+
+def test_spmv_mirror_rejects():
+    import paper_2209_07552_b200 as M
+    import torch
+    A = gen.transpose(gen.kdistinct_csr(30, 30, 3, seed=3))
+    ctx = M.Context(0, 1, None, 0, 1)
+    ctx.partition("csc", 30, 30, ptr=A["ptr"], idx=A["idx"], val=A["val"])
+    with pytest.raises(M.MsrepError) as e:
+        z = torch.zeros(30, dtype=torch.float64, device="cuda")
+        ctx.spmv_mirror(1.0, z, 0.0, z.clone(), [z.clone()])
+    assert e.value.status == 5
+    ctx.close()
