@@ -55,8 +55,14 @@ typedef enum { MSREP_F64 = 0, MSREP_F32 = 1 } msrep_dtype;
  *  BLOCK: the paper's "Baseline" (Sec. 5.1): whole row blocks (CSR, COO) or
  *         column blocks (CSC) [floor(i*outer/np), floor((i+1)*outer/np)),
  *         b_i = ptr[floor(i*outer/np)]; never shares a row, imbalanced when the
- *         nonzeros are (Fig. 6).  Same kernels and merge. */
-typedef enum { MSREP_SPLIT_NNZ = 0, MSREP_SPLIT_BLOCK = 1 } msrep_split;
+ *         nonzeros are (Fig. 6).  Same kernels and merge.
+ *  TWO_LEVEL: the paper's NUMA-aware two-level split (Sec. 4.2, Fig.
+ *         2level): nonzeros go to NUMA groups in proportion to their part
+ *         counts, then each group's range is cut by the floor rule; set with
+ *         msrep_set_split_groups.  Not identical to NNZ in general (S:231's
+ *         claim is false, reading R20); parts differ by <= 2.
+ *         (The matrix is device-resident here, so "placement" is the upload.) */
+typedef enum { MSREP_SPLIT_NNZ = 0, MSREP_SPLIT_BLOCK = 1, MSREP_SPLIT_TWO_LEVEL = 2 } msrep_split;
 
 /* Where y ends up after msrep_spmv (reading R19; the paper merges
  * into CPU memory).
@@ -179,8 +185,12 @@ msrep_status_t msrep_spmv_host(msrep_ctx ctx, const void* alpha, const void* x_h
                                void* y_host, msrep_layout layout, void* stream);
 
 /* Select the split used by the next msrep_partition on this context (default
- * MSREP_SPLIT_NNZ).  All ranks must select the same split. */
+ * MSREP_SPLIT_NNZ; NNZ or BLOCK here).  All ranks must select the same split. */
 msrep_status_t msrep_set_split(msrep_ctx ctx, msrep_split split);
+/* Select MSREP_SPLIT_TWO_LEVEL with `ngroups` groups of parts_per_group[g]
+ * consecutive parts (sum = nranks*parts_per_rank, else MSREP_ERR_INVALID_ARG),
+ * e.g. {4, 4} for a DGX with two NUMA nodes of 4 GPUs. */
+msrep_status_t msrep_set_split_groups(msrep_ctx ctx, int ngroups, const int* parts_per_group);
 
 /* Pure host: the np descriptors of Alg. 2/4 (fmt CSR/CSC, ptr = pointer array
  * of length outer+1) or Alg. 6 (fmt COO, coo_row = row_idx[nnz], m = rows).
@@ -190,6 +200,9 @@ msrep_status_t msrep_plan(msrep_format fmt, int64_t outer, int64_t nnz, int np, 
 /* The same for either split (msrep_plan == msrep_plan_split(fmt, MSREP_SPLIT_NNZ, ...)). */
 msrep_status_t msrep_plan_split(msrep_format fmt, msrep_split split, int64_t outer, int64_t nnz, int np,
                                 const int64_t* ptr, const int32_t* coo_row, msrep_part_desc* parts_out);
+/* The same for the two-level split (np = sum of parts_per_group[0..ngroups)). */
+msrep_status_t msrep_plan_groups(msrep_format fmt, int64_t outer, int64_t nnz, int ngroups, const int* parts_per_group,
+                                 const int64_t* ptr, const int32_t* coo_row, msrep_part_desc* parts_out);
 
 /* Pure host: the exchange step of msrep_spmv for nranks > 1 (Sec. 4.3,
  * P:602-607; readings R6, R9, R10) as msrep_spmv performs it, with

@@ -64,6 +64,7 @@ def lib():
             "or_block_boundaries": [I64, P, I64, P],
             "or_block_boundaries_coo": [I64, I64, P, I64, P],
             "or_relative_throughput": [I64, P],
+            "or_two_level_boundaries": [I64, I64, P, P],
             "or_partition_ptr_b": [I64, P, I64, P, P, P],
             "or_partition_coo_b": [I64, P, I64, P, P],
             "or_cg_csr": [I64, P, P, P, P, P, D, I64, P, P],
@@ -216,6 +217,15 @@ def block_boundaries_coo(m, row_idx, np_):
     row_idx = _c(row_idx, np.int64)
     b = np.zeros(np_ + 1, np.int64)
     lib().or_block_boundaries_coo(m, row_idx.size, _p(row_idx), np_, _p(b))
+    return b
+
+
+def two_level_boundaries(nnz, sizes):
+    """Two-level NUMA split (Sec. 4.2): groups get nnz in proportion to their part counts,
+    then each group's range is split among its parts by the floor rule."""
+    sizes = _c(sizes, np.int64)
+    b = np.zeros(int(sizes.sum()) + 1, np.int64)
+    lib().or_two_level_boundaries(nnz, sizes.size, _p(sizes), _p(b))
     return b
 
 

@@ -217,6 +217,24 @@ void or_block_boundaries_coo(int64_t m, int64_t nnz, const int64_t *row_idx, int
     }
 }
 
+/* Two-level split (Sec. 4.2, P:567 and Fig. 2level): level 1 cuts
+ * [0,nnz) among NUMA groups in proportion to their part (GPU) counts,
+ * c_g = floor(D_g*nnz/D) with D_g the prefix sum of the group sizes; level 2
+ * cuts each group's range among its parts with the floor rule,
+ * b = c_g + floor(i*(c_{g+1}-c_g)/d_g).  Writes np+1 boundaries, np = D. */
+void or_two_level_boundaries(int64_t nnz, int64_t ngroups, const int64_t *sizes, int64_t *b)
+{
+    int64_t D = 0;
+    for (int64_t g = 0; g < ngroups; g++) D += sizes[g];
+    int64_t Dg = 0, w = 0;
+    for (int64_t g = 0; g < ngroups; g++) {
+        int64_t c0 = (Dg * nnz) / D, c1 = ((Dg + sizes[g]) * nnz) / D;
+        for (int64_t i = 0; i < sizes[g]; i++) b[w++] = c0 + (i * (c1 - c0)) / sizes[g];
+        Dg += sizes[g];
+    }
+    b[w] = nnz;
+}
+
 /* The workload-imbalance cost model behind Fig. 6: a
  * memory-bound SpMV's time is set by the part with the most nonzeros, so the
  * throughput of a plan relative to a perfectly balanced one is

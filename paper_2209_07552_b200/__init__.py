@@ -24,7 +24,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 # enums (include/msrep.h)
 CSR, CSC, COO, COO_COL = 0, 1, 2, 3
-SPLIT_NNZ, SPLIT_BLOCK = 0, 1
+SPLIT_NNZ, SPLIT_BLOCK, SPLIT_TWO_LEVEL = 0, 1, 2
 SPLITS = {"nnz": SPLIT_NNZ, "block": SPLIT_BLOCK}
 F64, F32 = 0, 1
 Y_REPLICATED, Y_OWNED, Y_SHARDED = 0, 1, 2
@@ -77,6 +77,8 @@ _sig = {
     "msrep_cg": [P, P, P, ctypes.c_double, I, I, ctypes.POINTER(I), ctypes.POINTER(ctypes.c_double), P],
     "msrep_spmm": [P, P, P, P, P, I, I, P],
     "msrep_spmv_mirror": [P, P, P, P, P, I, P, P],
+    "msrep_plan_groups": [I, I64, I64, I, P, P, P, P],
+    "msrep_set_split_groups": [P, I, P],
     "msrep_get_stats": [P, ctypes.POINTER(Stats)],
     "msrep_destroy": [P],
     "msrep_profile_enable": [P, I],
@@ -91,7 +93,7 @@ _lib.msrep_version.argtypes = []
 _lib.msrep_version.restype = ctypes.c_int
 
 EXPORTED = ["msrep_get_unique_id", "msrep_create", "msrep_partition", "msrep_spmv", "msrep_spmv_host",
-            "msrep_plan", "msrep_plan_split", "msrep_set_split", "msrep_cg", "msrep_spmm", "msrep_spmv_mirror", "msrep_exchange_plan", "msrep_get_stats", "msrep_destroy", "msrep_last_error", "msrep_version",
+            "msrep_plan", "msrep_plan_split", "msrep_set_split", "msrep_cg", "msrep_spmm", "msrep_spmv_mirror", "msrep_plan_groups", "msrep_set_split_groups", "msrep_exchange_plan", "msrep_get_stats", "msrep_destroy", "msrep_last_error", "msrep_version",
             "msrep_profile_enable", "msrep_profile_read"]
 
 
@@ -177,6 +179,24 @@ def msrep_plan_split(fmt, split, outer, nnz, np_, ptr=None, coo_row=None):
     _check(_lib.msrep_plan_split(fmt, split, outer, nnz, np_, _ptr(ptr), _ptr(coo_row), _ptr(parts)),
            "msrep_plan_split")
     return parts
+
+
+def msrep_plan_groups(fmt, outer, nnz, groups, ptr=None, coo_row=None):
+    """Two-level split (Sec. 4.2) descriptors; groups = parts per NUMA group."""
+    g = np.ascontiguousarray(groups, np.int32)
+    parts = np.zeros(int(g.sum()), PART_DTYPE)
+    if ptr is not None:
+        ptr = np.ascontiguousarray(ptr, np.int64)
+    if coo_row is not None:
+        coo_row = np.ascontiguousarray(coo_row, np.int32)
+    _check(_lib.msrep_plan_groups(fmt, outer, nnz, g.size, _ptr(g), _ptr(ptr), _ptr(coo_row), _ptr(parts)),
+           "msrep_plan_groups")
+    return parts
+
+
+def msrep_set_split_groups(ctx, groups):
+    g = np.ascontiguousarray(groups, np.int32)
+    _check(_lib.msrep_set_split_groups(ctx, g.size, _ptr(g)), "msrep_set_split_groups")
 
 
 def msrep_set_split(ctx, split):
@@ -275,7 +295,10 @@ class Context:
     def partition(self, fmt, m, n, ptr=None, idx=None, val=None, coo_row=None, stream=None, split="nnz"):
         if isinstance(fmt, str):
             fmt = FORMATS[fmt]
-        msrep_set_split(self.h, SPLITS[split] if isinstance(split, str) else split)
+        if isinstance(split, (list, tuple)):   # two-level: parts per NUMA group
+            msrep_set_split_groups(self.h, split)
+        else:
+            msrep_set_split(self.h, SPLITS[split] if isinstance(split, str) else split)
         val = np.ascontiguousarray(val)
         dtype = F64 if val.dtype == np.float64 else F32
         idx = np.ascontiguousarray(idx, np.int32)

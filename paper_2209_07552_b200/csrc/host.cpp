@@ -71,8 +71,19 @@ constexpr int64_t kMaxRankNnz = kMaxIdx - (1 << 16);
 // P:311-312), or the paper's "Baseline" row/column blocks (Sec. 5.1):
 // b_i = ptr[floor(i*outer/np)] (COO: the first nonzero of row floor(i*m/np)).
 void split_bounds(msrep_format fmt, msrep_split split, int64_t outer, int64_t nnz, int np, const int64_t* ptr,
-                  const int32_t* row, std::vector<int64_t>& b) {
+                  const int32_t* row, std::vector<int64_t>& b, const std::vector<int>* groups = nullptr) {
   b.resize((size_t)np + 1);
+  if (split == MSREP_SPLIT_TWO_LEVEL) {   // Sec. 4.2: groups by part count, then floor rule inside
+    int64_t Dg = 0;
+    size_t w = 0;
+    for (int sz : *groups) {
+      const int64_t c0 = (Dg * nnz) / np, c1 = ((Dg + sz) * nnz) / np;
+      for (int i = 0; i < sz; i++) b[w++] = c0 + ((int64_t)i * (c1 - c0)) / sz;
+      Dg += sz;
+    }
+    b[(size_t)np] = nnz;
+    return;
+  }
   for (int i = 0; i <= np; i++) {
     if (split == MSREP_SPLIT_NNZ) b[(size_t)i] = ((int64_t)i * nnz) / np;
     else if (coo_like(fmt)) {
@@ -134,6 +145,7 @@ struct DevBuf {
 struct Ctx {
   int rank = 0, nranks = 1, vparts = 1, np = 1, device = 0;
   msrep_split split = MSREP_SPLIT_NNZ;
+  std::vector<int> groups;          // MSREP_SPLIT_TWO_LEVEL: parts per NUMA group
   ncclComm_t comm = nullptr;
   msrep_allocator alloc{};
   bool has_alloc = false;
@@ -818,9 +830,51 @@ msrep_status_t msrep_plan(msrep_format fmt, int64_t outer, int64_t nnz, int np, 
   return msrep_plan_split(fmt, MSREP_SPLIT_NNZ, outer, nnz, np, ptr, coo_row, parts_out);
 }
 
+msrep_status_t msrep_plan_groups(msrep_format fmt, int64_t outer, int64_t nnz, int ngroups, const int* parts_per_group,
+                                 const int64_t* ptr, const int32_t* coo_row, msrep_part_desc* parts_out) {
+  if (ngroups < 1 || !parts_per_group || outer < 0 || nnz < 0 || !parts_out)
+    return fail(MSREP_ERR_INVALID_ARG, "bad two-level plan arguments");
+  std::vector<int> g(parts_per_group, parts_per_group + ngroups);
+  int np = 0;
+  for (int v : g) {
+    if (v < 1) return fail(MSREP_ERR_INVALID_ARG, "a group has %d parts", v);
+    np += v;
+  }
+  std::vector<int64_t> b;
+  if (coo_like(fmt)) {
+    if (nnz > 0 && !coo_row) return fail(MSREP_ERR_INVALID_ARG, "COO plan needs its sorted major index");
+    split_bounds(fmt, MSREP_SPLIT_TWO_LEVEL, outer, nnz, np, nullptr, coo_row, b, &g);
+    plan_coo(outer, np, coo_row, b, parts_out);
+  } else if (fmt == MSREP_CSR || fmt == MSREP_CSC) {
+    if (!ptr) return fail(MSREP_ERR_INVALID_ARG, "plan needs ptr");
+    if (ptr[0] != 0 || ptr[outer] != nnz) return fail(MSREP_ERR_DIM_MISMATCH, "ptr[0] != 0 or ptr[outer] != nnz");
+    split_bounds(fmt, MSREP_SPLIT_TWO_LEVEL, outer, nnz, np, ptr, nullptr, b, &g);
+    plan_ptr(outer, np, ptr, b, parts_out);
+  } else {
+    return fail(MSREP_ERR_INVALID_ARG, "unknown format %d", (int)fmt);
+  }
+  return MSREP_OK;
+}
+
+msrep_status_t msrep_set_split_groups(msrep_ctx h, int ngroups, const int* parts_per_group) {
+  if (!h) return fail(MSREP_ERR_INVALID_ARG, "ctx is NULL");
+  Ctx* c = reinterpret_cast<Ctx*>(h);
+  if (ngroups < 1 || !parts_per_group) return fail(MSREP_ERR_INVALID_ARG, "bad groups");
+  int np = 0;
+  for (int i = 0; i < ngroups; i++) {
+    if (parts_per_group[i] < 1) return fail(MSREP_ERR_INVALID_ARG, "group %d has %d parts", i, parts_per_group[i]);
+    np += parts_per_group[i];
+  }
+  if (np != c->np) return fail(MSREP_ERR_INVALID_ARG, "groups hold %d parts, the context has %d", np, c->np);
+  c->groups.assign(parts_per_group, parts_per_group + ngroups);
+  c->split = MSREP_SPLIT_TWO_LEVEL;
+  return MSREP_OK;
+}
+
 msrep_status_t msrep_set_split(msrep_ctx h, msrep_split split) {
   if (!h) return fail(MSREP_ERR_INVALID_ARG, "ctx is NULL");
-  if (split != MSREP_SPLIT_NNZ && split != MSREP_SPLIT_BLOCK) return fail(MSREP_ERR_INVALID_ARG, "unknown split %d", (int)split);
+  if (split != MSREP_SPLIT_NNZ && split != MSREP_SPLIT_BLOCK)
+    return fail(MSREP_ERR_INVALID_ARG, "split %d (use msrep_set_split_groups for the two-level split)", (int)split);
   reinterpret_cast<Ctx*>(h)->split = split;
   return MSREP_OK;
 }
@@ -926,7 +980,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   }
   std::vector<msrep_part_desc> parts((size_t)c->np);
   std::vector<int64_t> bnd;
-  split_bounds(fmt, c->split, outer, nnz, c->np, ptr, coo_row, bnd);
+  split_bounds(fmt, c->split, outer, nnz, c->np, ptr, coo_row, bnd, &c->groups);
   if (coo_like(fmt)) plan_coo(outer, c->np, coo_row, bnd, parts.data());
   else plan_ptr(outer, c->np, ptr, bnd, parts.data());
   const int P0 = c->rank * c->vparts, P1 = P0 + c->vparts;

@@ -176,7 +176,7 @@ using RowLayout = WLayout<(SELL && SStage<VT>::BYTES > RStage<VT>::BYTES) ? SSta
 // One SELL tile with R rows per lane (internal.h): all R*W column indices are read from the
 // slot, then all R*W x gathers are in flight before the first FMA; padding is masked by the
 // row length, so results equal the plain row sums.
-template <typename VT, int R, class Refill>
+template <typename VT, int R, bool MIRROR, class Refill>
 __device__ __forceinline__ void sell_tile(const RowLaunch& P, const int4 d, const unsigned char* st, const int lane,
                                           const VT* __restrict__ x, VT* __restrict__ y, double alpha, double beta,
                                           Refill&& refill) {
@@ -217,14 +217,15 @@ __device__ __forceinline__ void sell_tile(const RowLaunch& P, const int4 d, cons
       if (beta != 0.0) o += beta * yv[k];
       const int64_t yi = P.ybase + d.x + row;
       y[yi] = (VT)o;
-      for (int mi = 0; mi < P.nmirror; mi++) static_cast<VT*>(P.mirror[mi])[yi] = (VT)o;   // fused allgather
+      if constexpr (MIRROR)
+        for (int mi = 0; mi < P.nmirror; mi++) static_cast<VT*>(P.mirror[mi])[yi] = (VT)o;   // fused allgather
     }
   }
   __syncwarp();   // the tile was read in place: refill the slot only now
   refill();
 }
 
-template <typename VT, bool SELL>
+template <typename VT, bool SELL, bool MIRROR>
 __global__ void __launch_bounds__(WARPS * 32, MSREP_ROW_MINB) rows_kernel(const RowLaunch P) {
   using Lay = RowLayout<VT, SELL>;
   constexpr int QMAX = qmax<VT>();
@@ -278,9 +279,9 @@ __global__ void __launch_bounds__(WARPS * 32, MSREP_ROW_MINB) rows_kernel(const 
       // ---- SELL tile (read in place; the slot is refilled after the tile)
       const int nrows = d.z & 0xffff, Wd = d.z >> 16;
       const int R = sell_r(nrows);
-      if (R == 1) sell_tile<VT, 1>(P, d, st, lane, x, y, alpha, beta, refill);
-      else if (R == 2) sell_tile<VT, 2>(P, d, st, lane, x, y, alpha, beta, refill);
-      else sell_tile<VT, 4>(P, d, st, lane, x, y, alpha, beta, refill);
+      if (R == 1) sell_tile<VT, 1, MIRROR>(P, d, st, lane, x, y, alpha, beta, refill);
+      else if (R == 2) sell_tile<VT, 2, MIRROR>(P, d, st, lane, x, y, alpha, beta, refill);
+      else sell_tile<VT, 4, MIRROR>(P, d, st, lane, x, y, alpha, beta, refill);
       (void)Wd;
       continue;
     }
@@ -385,7 +386,8 @@ __global__ void __launch_bounds__(WARPS * 32, MSREP_ROW_MINB) rows_kernel(const 
         double o = alpha * rsum[rr];
         if (beta != 0.0) o += beta * yin[u];
         __stcs(y + yrow0 + rr, (VT)o);
-        for (int mi = 0; mi < P.nmirror; mi++) static_cast<VT*>(P.mirror[mi])[yrow0 + rr] = (VT)o;   // fused allgather
+        if constexpr (MIRROR)
+          for (int mi = 0; mi < P.nmirror; mi++) static_cast<VT*>(P.mirror[mi])[yrow0 + rr] = (VT)o;   // fused allgather
       }
     }
     __syncwarp();   // rsum is free
@@ -1140,13 +1142,17 @@ int grid_for(K kernel, int smem_bytes, int ntiles) {
   return (int)(want < g ? (want < 1 ? 1 : want) : g);
 }
 
-template <typename VT, bool SELL>
+template <typename VT, bool SELL, bool MIRROR>
 cudaError_t launch_rows_t(const RowLaunch& L, cudaStream_t s) {
   constexpr int b = RowLayout<VT, SELL>::TOTAL;
-  cudaError_t e = set_smem(rows_kernel<VT, SELL>, b);
+  cudaError_t e = set_smem(rows_kernel<VT, SELL, MIRROR>, b);
   if (e) return e;
-  rows_kernel<VT, SELL><<<grid_for(rows_kernel<VT, SELL>, b, L.ntiles), WARPS * 32, b, s>>>(L);
+  rows_kernel<VT, SELL, MIRROR><<<grid_for(rows_kernel<VT, SELL, MIRROR>, b, L.ntiles), WARPS * 32, b, s>>>(L);
   return cudaGetLastError();
+}
+template <typename VT, bool SELL>
+cudaError_t launch_rows_m(const RowLaunch& L, cudaStream_t s) {
+  return L.nmirror > 0 ? launch_rows_t<VT, SELL, true>(L, s) : launch_rows_t<VT, SELL, false>(L, s);
 }
 
 #ifndef MSREP_CB_SMEM_MIN
@@ -1170,8 +1176,8 @@ cudaError_t launch_cols_t(const ColLaunch& L, cudaStream_t s) {
 
 cudaError_t launch_rows(const RowLaunch& L, cudaStream_t s) {
   if (L.ntiles == 0) return cudaSuccess;
-  if (L.has_sell) return L.dtype == 0 ? launch_rows_t<double, true>(L, s) : launch_rows_t<float, true>(L, s);
-  return L.dtype == 0 ? launch_rows_t<double, false>(L, s) : launch_rows_t<float, false>(L, s);
+  if (L.has_sell) return L.dtype == 0 ? launch_rows_m<double, true>(L, s) : launch_rows_m<float, true>(L, s);
+  return L.dtype == 0 ? launch_rows_m<double, false>(L, s) : launch_rows_m<float, false>(L, s);
 }
 
 cudaError_t launch_cols(const ColLaunch& L, cudaStream_t s) {

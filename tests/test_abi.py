@@ -150,3 +150,19 @@ def test_coo_col_plan_matches_csc_and_oracle():
                 assert np.array_equal(a[k], b[k]), k
         ref = oracle.partition_coo(n, cols, np_)
         _parts_equal(M.msrep_plan(M.COO_COL, n, nnz, np_, coo_row=cols), ref)
+
+
+def test_two_level_plan_bit_exact_vs_oracle():
+    """msrep_plan_groups == the oracle's two-level boundaries fed to its Alg. 2 / Alg. 6."""
+    import paper_2209_07552_b200 as M
+    rng = np.random.default_rng(43)
+    for trial in range(200):
+        m = int(rng.integers(1, 50))
+        groups = [int(v) for v in rng.integers(1, 5, int(rng.integers(1, 4)))]
+        lens = rng.integers(0, 7, m) * (rng.random(m) < 0.7)
+        ptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        nnz = int(ptr[-1])
+        b = oracle.two_level_boundaries(nnz, groups)
+        _parts_equal(M.msrep_plan_groups(M.CSR, m, nnz, groups, ptr=ptr), oracle.partition_ptr_b(ptr, b))
+        rows = oracle.csr_to_coo(m, ptr)
+        _parts_equal(M.msrep_plan_groups(M.COO, m, nnz, groups, coo_row=rows), oracle.partition_coo_b(m, rows, b))

@@ -560,3 +560,25 @@ def test_spmv_mirror_rejects():
         ctx.spmv_mirror(1.0, z, 0.0, z.clone(), [z.clone()])
     assert e.value.status == 5
     ctx.close()
+
+
+@pytest.mark.parametrize("fmt", FMTS)
+def test_two_level_split_bit_exact(fmt):
+    """The two-level NUMA split (groups [1, 3] and [4, 4] of parts) through the same kernels and
+    merge: bit-exact on integer R-MAT (split rows at different cut points than the nnz split)."""
+    import paper_2209_07552_b200 as M
+    import torch
+    A = gen.rmat(11, seed=51, kind=gen.SMALLINT)
+    B = as_fmt(A, fmt)
+    x = gen.vector(A["n"], 52, kind=gen.SMALLINT); y = gen.vector(A["m"], 53, kind=gen.SMALLINT)
+    for groups in ([1, 3], [4, 4]):
+        ctx = M.Context(0, 1, None, 0, sum(groups))
+        if fmt in ("coo", "coo_col"):
+            ctx.partition(fmt, B["m"], B["n"], idx=B["idx"], val=B["val"], coo_row=coo_of_csr(B), split=groups)
+        else:
+            ctx.partition(fmt, B["m"], B["n"], ptr=B["ptr"], idx=B["idx"], val=B["val"], split=groups)
+        xd = torch.as_tensor(x).cuda(); yd = torch.as_tensor(y.copy()).cuda()
+        ctx.spmv(1.5, xd, 0.5, yd)
+        torch.cuda.synchronize()
+        assert np.array_equal(yd.cpu().numpy(), oracle_ref(A, x, y, 1.5, 0.5)), (fmt, groups)
+        ctx.close()

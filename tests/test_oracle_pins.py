@@ -498,3 +498,39 @@ def test_cg_spd_stencil_recovers_known_solution():
     x, it, rr = oracle.cg_csr(m, A["ptr"], A["idx"], A["val"], b, np.zeros(m), 1e-12, 500)
     assert rr <= 1e-12 and 0 < it < 60
     assert np.max(np.abs(x - xs)) < 1e-10
+
+
+# --------------------------------------------- two-level NUMA split (NEXT f3)
+def test_two_level_spec_examples():
+    """nnz=12 on groups [3,3] (Summit node) and nnz=16 on [4,4] (DGX-1): 2 per part."""
+    assert oracle.two_level_boundaries(12, [3, 3]).tolist() == list(range(0, 13, 2))
+    assert oracle.two_level_boundaries(16, [4, 4]).tolist() == list(range(0, 17, 2))
+    assert oracle.two_level_boundaries(7, [1]).tolist() == [0, 7]
+
+
+def test_two_level_differs_from_single_level_counterexample():
+    """S:231 claims the composition equals the single-level split; it does not.
+    nnz=2 on [1,3]: level 1 gives the groups [0,0) and [0,2); level 2 cuts [0,2) in 3 ->
+    [0,0,0,1,2], while floor(i*2/4) = [0,0,1,1,2]."""
+    assert oracle.two_level_boundaries(2, [1, 3]).tolist() == [0, 0, 0, 1, 2]
+    assert oracle.nnz_boundaries(2, 4).tolist() == [0, 0, 1, 1, 2]
+
+
+def test_two_level_balance_and_coincidence():
+    """Within a group parts differ by <= 1 nonzero; across the whole plan by <= 2; and with
+    equal groups whose part count divides nnz the two levels reproduce the single-level cut."""
+    rng = np.random.default_rng(41)
+    for _ in range(300):
+        sizes = rng.integers(1, 5, int(rng.integers(1, 5)))
+        nnz = int(rng.integers(0, 200))
+        b = oracle.two_level_boundaries(nnz, sizes)
+        d = np.diff(b)
+        assert b[0] == 0 and b[-1] == nnz and (d >= 0).all()
+        assert d.max() - d.min() <= 2
+        w = 0
+        for s in sizes:
+            assert d[w:w + s].max() - d[w:w + s].min() <= 1
+            w += s
+    for g, per in ((2, 4), (3, 2), (2, 3)):
+        nnz = g * per * 7
+        assert np.array_equal(oracle.two_level_boundaries(nnz, [per] * g), oracle.nnz_boundaries(nnz, g * per))
