@@ -121,6 +121,13 @@ typedef struct {
   int64_t tile_bytes;        /* bytes of the rank's tile blobs as stored on the GPU (what one
                                 SpMV streams from HBM for A, incl. 16-B / SELL padding)      */
   int64_t nsell;             /* SELL tiles among the rank's tiles (regular pCSR rows)        */
+  double phase_ms[4];        /* partition_ms split into: [0] argument validation (O(m + nnz)
+                                host scans), [1] plan (split, Alg. 2/4/6 descriptors, local
+                                pointer), [2] device layout schedule (host), [3] upload of the
+                                slice + GPU-side rebase / packing up to the sync  */
+  int64_t residency;         /* msrep_residency of the partition                             */
+  int64_t nchunks;           /* MSREP_RESIDENT_HOST: chunks streamed per SpMV (else 0)       */
+  int64_t host_bytes;        /* MSREP_RESIDENT_HOST: pinned bytes streamed H2D per SpMV      */
 } msrep_stats;
 
 /* NCCL unique id for the communicator (rank 0 creates it, the caller
@@ -183,6 +190,25 @@ msrep_status_t msrep_spmv_mirror(msrep_ctx ctx, const void* alpha, const void* x
  * y.  Synchronous: returns after y is written. */
 msrep_status_t msrep_spmv_host(msrep_ctx ctx, const void* alpha, const void* x_host, const void* beta,
                                void* y_host, msrep_layout layout, void* stream);
+
+/* Where the rank's partition lives between calls (the
+ * paper's own timed regime, "partitioning ... and distributing the
+ * partitions to the GPUs" inside every measured call).
+ *   MSREP_RESIDENT_DEVICE (default): the device layout is built once and kept
+ *     in HBM; msrep_spmv streams it from HBM.
+ *   MSREP_RESIDENT_HOST (out-of-core): msrep_partition builds the same device
+ *     layout chunk by chunk on the GPU and parks it in pinned host memory;
+ *     every msrep_spmv / msrep_spmm / msrep_cg streams it back H2D in chunks of
+ *     <= chunk_bytes through two device staging buffers on a copy stream,
+ *     the kernel of chunk k overlapping the copy of chunk k+1.  Device memory
+ *     held: 2 staging buffers + the per-tile descriptors, whatever the size of
+ *     A, so the rank's slice may exceed HBM (the partition step itself needs
+ *     the rank's val/idx span of one chunk on the device at a time).
+ * chunk_bytes: 0 -> 256 MiB; a chunk always holds at least one tile / row
+ * band.  Applies to the next msrep_partition.  Errors: MSREP_ERR_INVALID_ARG
+ * (unknown residency, chunk_bytes < 0). */
+typedef enum { MSREP_RESIDENT_DEVICE = 0, MSREP_RESIDENT_HOST = 1 } msrep_residency;
+msrep_status_t msrep_set_residency(msrep_ctx ctx, msrep_residency residency, int64_t chunk_bytes);
 
 /* Select the split used by the next msrep_partition on this context (default
  * MSREP_SPLIT_NNZ; NNZ or BLOCK here).  All ranks must select the same split. */

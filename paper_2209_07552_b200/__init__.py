@@ -28,6 +28,8 @@ SPLIT_NNZ, SPLIT_BLOCK, SPLIT_TWO_LEVEL = 0, 1, 2
 SPLITS = {"nnz": SPLIT_NNZ, "block": SPLIT_BLOCK}
 F64, F32 = 0, 1
 Y_REPLICATED, Y_OWNED, Y_SHARDED = 0, 1, 2
+RESIDENT_DEVICE, RESIDENT_HOST = 0, 1
+RESIDENCY = {"device": RESIDENT_DEVICE, "host": RESIDENT_HOST}
 STATUS = {0: "MSREP_OK", 1: "MSREP_ERR_INVALID_ARG", 2: "MSREP_ERR_DIM_MISMATCH", 3: "MSREP_ERR_UNSORTED_COO",
           4: "MSREP_ERR_TOO_LARGE", 5: "MSREP_ERR_STATE", 6: "MSREP_ERR_OOM", 7: "MSREP_ERR_CUDA",
           8: "MSREP_ERR_NCCL"}
@@ -50,7 +52,9 @@ class Stats(ctypes.Structure):
         "nparts", "nranks", "parts_per_rank", "nnz_rank", "rows_window", "owned_rows", "distinct_cols", "ntiles",
         "nslabs", "nsplit_rows", "nheads_local", "alg_bytes", "alg_bytes_beta0", "kernels_per_spmv",
         "device_bytes")] + [("partition_ms", ctypes.c_double), ("tile_bytes", ctypes.c_int64),
-                                         ("nsell", ctypes.c_int64)]
+                                         ("nsell", ctypes.c_int64),
+                                         ("phase_ms", ctypes.c_double * 4), ("residency", ctypes.c_int64),
+                                         ("nchunks", ctypes.c_int64), ("host_bytes", ctypes.c_int64)]
 
 
 class Allocator(ctypes.Structure):
@@ -74,6 +78,7 @@ _sig = {
     "msrep_exchange_plan": [I, I, I64, I64, I64, I, I, P, P, P, P, P],
     "msrep_plan_split": [I, I, I64, I64, I, P, P, P],
     "msrep_set_split": [P, I],
+    "msrep_set_residency": [P, I, I64],
     "msrep_cg": [P, P, P, ctypes.c_double, I, I, ctypes.POINTER(I), ctypes.POINTER(ctypes.c_double), P],
     "msrep_spmm": [P, P, P, P, P, I, I, P],
     "msrep_spmv_mirror": [P, P, P, P, P, I, P, P],
@@ -93,7 +98,7 @@ _lib.msrep_version.argtypes = []
 _lib.msrep_version.restype = ctypes.c_int
 
 EXPORTED = ["msrep_get_unique_id", "msrep_create", "msrep_partition", "msrep_spmv", "msrep_spmv_host",
-            "msrep_plan", "msrep_plan_split", "msrep_set_split", "msrep_cg", "msrep_spmm", "msrep_spmv_mirror", "msrep_plan_groups", "msrep_set_split_groups", "msrep_exchange_plan", "msrep_get_stats", "msrep_destroy", "msrep_last_error", "msrep_version",
+            "msrep_plan", "msrep_plan_split", "msrep_set_split", "msrep_set_residency", "msrep_cg", "msrep_spmm", "msrep_spmv_mirror", "msrep_plan_groups", "msrep_set_split_groups", "msrep_exchange_plan", "msrep_get_stats", "msrep_destroy", "msrep_last_error", "msrep_version",
             "msrep_profile_enable", "msrep_profile_read"]
 
 
@@ -203,6 +208,10 @@ def msrep_set_split(ctx, split):
     _check(_lib.msrep_set_split(ctx, split), "msrep_set_split")
 
 
+def msrep_set_residency(ctx, residency, chunk_bytes=0):
+    _check(_lib.msrep_set_residency(ctx, residency, int(chunk_bytes)), "msrep_set_residency")
+
+
 def msrep_exchange_plan(fmt, m, n, nnz, nranks, parts_per_rank, ptr=None, coo_row=None, split=SPLIT_NNZ):
     """Pure host: the multi-rank exchange step msrep_spmv performs (include/msrep.h).
     Returns (seg[nranks, 2] y-row segments per rank, head_row[np], head_part[np])."""
@@ -247,7 +256,7 @@ def msrep_cg(ctx, b, x, tol=1e-10, maxit=1000, check_every=10, stream=None):
 def msrep_get_stats(ctx) -> dict:
     s = Stats()
     _check(_lib.msrep_get_stats(ctx, ctypes.byref(s)), "msrep_get_stats")
-    return {k: getattr(s, k) for k, _ in Stats._fields_}
+    return {k: (list(getattr(s, k)) if k == "phase_ms" else getattr(s, k)) for k, _ in Stats._fields_}
 
 
 def msrep_profile_enable(ctx, enable=True):
@@ -292,7 +301,9 @@ class Context:
             uid = obj[0]
         return cls(rank, world, uid, device, parts_per_rank)
 
-    def partition(self, fmt, m, n, ptr=None, idx=None, val=None, coo_row=None, stream=None, split="nnz"):
+    def partition(self, fmt, m, n, ptr=None, idx=None, val=None, coo_row=None, stream=None, split="nnz",
+                  residency="device", chunk_bytes=0):
+        msrep_set_residency(self.h, RESIDENCY[residency] if isinstance(residency, str) else residency, chunk_bytes)
         if isinstance(fmt, str):
             fmt = FORMATS[fmt]
         if isinstance(split, (list, tuple)):   # two-level: parts per NUMA group

@@ -208,6 +208,18 @@ struct Ctx {
   double* d_head_local_mm = nullptr;
   double* d_head_all_mm = nullptr;
 
+  // MSREP_RESIDENT_HOST: the device layout parked in pinned host memory, streamed per call
+  // in chunks (row formats: tile ranges; pCSC: band ranges) through two staging buffers
+  int residency = MSREP_RESIDENT_DEVICE;
+  int64_t chunk_bytes = (int64_t)256 << 20;
+  struct Chunk { int32_t t0, t1, u0, u1; int64_t off, bytes; bool has_sell; };
+  std::vector<Chunk> chunks;
+  char* h_blob = nullptr;           // pinned (cudaHostAlloc)
+  int64_t h_bytes = 0;
+  char* d_stage[2] = {nullptr, nullptr};
+  cudaStream_t cs = nullptr;        // copy stream
+  cudaEvent_t ev_go = nullptr, ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+
   // host-vector path buffers
   void* d_hx = nullptr;
   void* d_hy = nullptr;
@@ -268,6 +280,11 @@ void free_all(Ctx* c) {
     else cudaFree(b.p);
   }
   c->bufs.clear();
+  if (c->h_blob) cudaFreeHost(c->h_blob);
+  c->h_blob = nullptr;
+  c->h_bytes = 0;
+  c->chunks.clear();
+  c->d_stage[0] = c->d_stage[1] = nullptr;
   c->ready = false;
   c->d_hx = c->d_hy = nullptr;
   c->d_cg_r = c->d_cg_p = c->d_cg_ap = nullptr;
@@ -791,6 +808,47 @@ double get_scalar(const void* p, msrep_dtype t) {
 }  // namespace
 
 // ======================================================================= ABI
+// ------------------------------------------------ host-resident streaming
+msrep_status_t ensure_copy_stream(Ctx* c) {
+  if (c->cs) return MSREP_OK;
+  CUDA_TRY(cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking));
+  for (cudaEvent_t* e : {&c->ev_go, &c->ev_copied[0], &c->ev_copied[1], &c->ev_free[0], &c->ev_free[1]})
+    CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  return MSREP_OK;
+}
+
+// Stream the pinned layout through the two staging buffers: the copy of chunk k (copy stream)
+// waits until the kernel of chunk k-2 (same buffer) has run; the kernel of chunk k (caller's
+// stream) waits for its copy.  launch(chunk, base) enqueues on `s` with base = the staging
+// buffer minus the chunk's layout offset, so layout offsets index it unchanged.
+template <class F>
+msrep_status_t stream_chunks(Ctx* c, cudaStream_t s, F&& launch) {
+  CUDA_TRY(cudaEventRecord(c->ev_go, s));   // earlier work on s (previous calls' reads) is done first
+  CUDA_TRY(cudaStreamWaitEvent(c->cs, c->ev_go, 0));
+  for (size_t k = 0; k < c->chunks.size(); k++) {
+    const auto& ch = c->chunks[k];
+    const int b = (int)(k & 1);
+    if (k >= 2) CUDA_TRY(cudaStreamWaitEvent(c->cs, c->ev_free[b], 0));
+    CUDA_TRY(cudaMemcpyAsync(c->d_stage[b], c->h_blob + ch.off, (size_t)ch.bytes, cudaMemcpyHostToDevice, c->cs));
+    CUDA_TRY(cudaEventRecord(c->ev_copied[b], c->cs));
+    CUDA_TRY(cudaStreamWaitEvent(s, c->ev_copied[b], 0));
+    TRY(launch(ch, static_cast<const char*>(c->d_stage[b]) - ch.off));
+    CUDA_TRY(cudaEventRecord(c->ev_free[b], s));
+  }
+  return MSREP_OK;
+}
+
+msrep_status_t alloc_stages(Ctx* c, cudaStream_t s) {
+  int64_t mx = 16;
+  for (auto& ch : c->chunks) mx = std::max(mx, ch.bytes);
+  for (int b = 0; b < 2; b++) {
+    void* p;
+    TRY(dalloc(c, (size_t)mx, &p, s));
+    c->d_stage[b] = static_cast<char*>(p);
+  }
+  return MSREP_OK;
+}
+
 extern "C" {
 
 const char* msrep_last_error(void) { return g_err.c_str(); }
@@ -879,6 +937,17 @@ msrep_status_t msrep_set_split(msrep_ctx h, msrep_split split) {
   return MSREP_OK;
 }
 
+msrep_status_t msrep_set_residency(msrep_ctx h, msrep_residency residency, int64_t chunk_bytes) {
+  if (!h) return fail(MSREP_ERR_INVALID_ARG, "ctx is NULL");
+  if (residency != MSREP_RESIDENT_DEVICE && residency != MSREP_RESIDENT_HOST)
+    return fail(MSREP_ERR_INVALID_ARG, "residency %d", (int)residency);
+  if (chunk_bytes < 0) return fail(MSREP_ERR_INVALID_ARG, "chunk_bytes < 0");
+  Ctx* c = reinterpret_cast<Ctx*>(h);
+  c->residency = residency;
+  c->chunk_bytes = chunk_bytes ? chunk_bytes : (int64_t)256 << 20;
+  return MSREP_OK;
+}
+
 msrep_status_t msrep_exchange_plan(msrep_format fmt, msrep_split split, int64_t m, int64_t n, int64_t nnz,
                                    int nranks, int parts_per_rank, const int64_t* ptr, const int32_t* coo_row,
                                    int64_t* seg_out, int64_t* head_row_out, int32_t* head_part_out) {
@@ -944,6 +1013,9 @@ msrep_status_t msrep_destroy(msrep_ctx h) {
   cudaDeviceSynchronize();
   free_all(c);
   for (auto& p : c->ev) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
+  if (c->cs) cudaStreamDestroy(c->cs);
+  for (cudaEvent_t e : {c->ev_go, c->ev_copied[0], c->ev_copied[1], c->ev_free[0], c->ev_free[1]})
+    if (e) cudaEventDestroy(e);
   if (c->comm) ncclCommDestroy(c->comm);
   delete c;
   return MSREP_OK;
@@ -956,6 +1028,13 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   Ctx* c = reinterpret_cast<Ctx*>(h);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const auto t0 = std::chrono::steady_clock::now();
+  double phase[4] = {0, 0, 0, 0};
+  auto tl = t0;
+  auto lap = [&](int k) {
+    const auto now = std::chrono::steady_clock::now();
+    phase[k] += std::chrono::duration<double, std::milli>(now - tl).count();
+    tl = now;
+  };
   // ---- validation (before any device work)
   if (fmt != MSREP_CSR && fmt != MSREP_CSC && fmt != MSREP_COO && fmt != MSREP_COO_COL)
     return fail(MSREP_ERR_INVALID_ARG, "format %d", (int)fmt);
@@ -978,16 +1057,19 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     for (int64_t r = 0; r < outer; r++)
       if (ptr[r + 1] < ptr[r]) return fail(MSREP_ERR_DIM_MISMATCH, "ptr decreases at %lld", (long long)r);
   }
+  lap(0);
   std::vector<msrep_part_desc> parts((size_t)c->np);
   std::vector<int64_t> bnd;
   split_bounds(fmt, c->split, outer, nnz, c->np, ptr, coo_row, bnd, &c->groups);
   if (coo_like(fmt)) plan_coo(outer, c->np, coo_row, bnd, parts.data());
   else plan_ptr(outer, c->np, ptr, bnd, parts.data());
+  lap(1);
   const int P0 = c->rank * c->vparts, P1 = P0 + c->vparts;
   const int64_t B_lo = bnd[(size_t)P0], B_hi = bnd[(size_t)P1];
   if (B_hi - B_lo >= kMaxRankNnz) return fail(MSREP_ERR_TOO_LARGE, "rank holds %lld nonzeros (>= 2^31 - 2^16)", (long long)(B_hi - B_lo));
   for (int64_t k = B_lo; k < B_hi; k++)
     if (idx[k] < 0 || idx[k] >= inner) return fail(MSREP_ERR_DIM_MISMATCH, "index %lld out of range", (long long)k);
+  lap(0);
 
   CUDA_TRY(cudaSetDevice(c->device));
   CUDA_TRY(cudaStreamSynchronize(s));
@@ -1038,12 +1120,14 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   }
 
   const int64_t nz_r = B_hi - B_lo;
+  lap(1);
   if (colwise(fmt)) {
     // ---- pCSC: row-band layout built on the host threads, uploaded once
     CscBands CB;
     int sms = 148;
     CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
     TRY(build_csc_bands(*c, lp, idx, val, V, sms, CB));
+    lap(2);
     c->csplit = CB.split_items;
     TRY(upload_vec(c, CB.items, &c->d_citems, s));
     TRY(upload_vec(c, CB.units, &c->d_cunits, s));
@@ -1053,7 +1137,33 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     TRY(upload_vec(c, CB.item_off, &c->d_item_off, s));
     TRY(upload_vec(c, CB.band_item, &c->d_band_item, s));
     TRY(upload_vec(c, CB.split, &c->d_split, s));
-    TRY(upload(c, CB.blob.get(), (size_t)CB.bytes, &c->d_cblob, s));
+    if (c->residency == MSREP_RESIDENT_HOST) {
+      // park the band blobs in pinned memory; chunks = runs of whole bands (and, in split
+      // mode, the units of those bands) of <= chunk_bytes
+      CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&c->h_blob), (size_t)std::max<int64_t>(16, CB.bytes), cudaHostAllocDefault));
+      memcpy(c->h_blob, CB.blob.get(), (size_t)CB.bytes);
+      c->h_bytes = CB.bytes;
+      auto band_off = [&](int64_t b) {
+        const int32_t i = CB.band_item[(size_t)b];
+        return i < (int32_t)CB.items.size() ? CB.item_off[(size_t)i] : CB.bytes;
+      };
+      size_t u = 0;
+      for (int64_t b = 0; b < CB.nb;) {
+        const int64_t off0 = band_off(b);
+        int64_t e = b + 1;
+        while (e < CB.nb && band_off(e + 1) - off0 <= c->chunk_bytes) e++;
+        Ctx::Chunk ch{(int32_t)b, (int32_t)e, (int32_t)u, 0, off0, band_off(e) - off0, false};
+        while (u < CB.units.size() && CB.units[u].x < e) u++;
+        ch.u1 = (int32_t)u;
+        c->chunks.push_back(ch);
+        b = e;
+      }
+      c->d_cblob = nullptr;
+      TRY(ensure_copy_stream(c));
+      TRY(alloc_stages(c, s));
+    } else {
+      TRY(upload(c, CB.blob.get(), (size_t)CB.bytes, &c->d_cblob, s));
+    }
     c->cnb = CB.nb;
     c->citems = (int64_t)CB.items.size();
     c->ntiles = 0; c->nsell = 0; c->nslabs = 0; c->nrec = 0; c->nsplit = 0;
@@ -1071,21 +1181,75 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     // ---- schedule
     Schedule S;
     build_row_schedule(*c, lp, S);
+    lap(2);
     c->ntiles = (int)(S.tiles.size() + S.sell.size());
     c->nsell = (int)S.sell.size();
     c->nslabs = S.nslabs;
     c->nrec = S.nrec;
     c->nsplit = (int)S.sr_row.size();
 
-    // ---- upload this rank's slice (the only H2D of A) and build the tile blobs on the GPU
+    // ---- tile order (SELL tiles first) and blob offsets
+    static_assert(sizeof(TileHost) == sizeof(int4), "tile");
+    S.tiles.insert(S.tiles.begin(), S.sell.begin(), S.sell.end());   // one list: SELL tiles first
+    const size_t nt = S.tiles.size();
+    std::vector<int32_t> blob16(nt);
+    int64_t blob_total = 0;
+    for (size_t t = 0; t < nt; t++) {
+      const TileHost& th = S.tiles[t];
+      const int kind = th.rec == -2 ? KIND_SELL : th.rec >= 0 ? KIND_SLAB : KIND_SEG;
+      if (blob_total / 16 >= (int64_t)1 << 31) return fail(MSREP_ERR_TOO_LARGE, "tile blob exceeds 32 GiB");
+      blob16[t] = (int32_t)(blob_total / 16);
+      blob_total += blob_bytes(kind, th.packed & 0xffff, th.packed >> 16, (int)V);
+    }
+    // ---- pack groups: all tiles at once (device-resident), or chunks of <= chunk_bytes of
+    // layout (host-resident), each with the span of rank-local nonzeros its tiles read
+    const bool host_res = c->residency == MSREP_RESIDENT_HOST;
+    struct Group { int32_t t0, t1; int64_t z0, z1; };
+    std::vector<Group> groups;
+    {
+      auto tile_end = [&](size_t t) { return t + 1 < nt ? (int64_t)blob16[t + 1] * 16 : blob_total; };
+      auto zspan = [&](const TileHost& th, int64_t& z0, int64_t& z1) {
+        z0 = th.nz0;
+        z1 = th.rec == -2 ? lp[(size_t)th.row0 + (size_t)(th.packed & 0xffff)] : th.nz0 + (th.packed >> 16);
+      };
+      const int64_t cap = host_res ? c->chunk_bytes : INT64_MAX;
+      size_t t = 0;
+      while (t < nt) {
+        Group g{(int32_t)t, (int32_t)t, INT64_MAX, 0};
+        const int64_t off0 = (int64_t)blob16[t] * 16;
+        while (t < nt && (t == (size_t)g.t0 || tile_end(t) - off0 <= cap)) {
+          int64_t z0, z1;
+          zspan(S.tiles[t], z0, z1);
+          g.z0 = std::min(g.z0, z0);
+          g.z1 = std::max(g.z1, z1);
+          t++;
+        }
+        g.t1 = (int32_t)t;
+        groups.push_back(g);
+        if (host_res) {
+          Ctx::Chunk ch{g.t0, g.t1, 0, 0, off0, tile_end(t - 1) - off0, S.tiles[(size_t)g.t0].rec == -2};
+          c->chunks.push_back(ch);
+        }
+      }
+    }
+    int64_t span = 0;
+    for (auto& g : groups) span = std::max(span, g.z1 - g.z0);
+    if (!host_res) span = nz_r;
+
+    // ---- upload the slice (the only H2D of A) and build the tile blobs on the GPU
     const size_t mark = c->bufs.size();   // temporaries allocated from here are freed after packing
     void* vp;
-    TRY(dalloc(c, (size_t)nz_r * V, &vp, s));
-    if (nz_r) CUDA_TRY(cudaMemcpyAsync(vp, static_cast<const char*>(val) + (size_t)B_lo * V, (size_t)nz_r * V, cudaMemcpyHostToDevice, s));
-    int32_t *d_idx, *d_aux;
-    TRY(upload(c, idx + B_lo, (size_t)nz_r, &d_idx, s));
+    TRY(dalloc(c, (size_t)span * V, &vp, s));
+    int32_t *d_idx, *d_aux = nullptr, *d_crow = nullptr;
+    {
+      void* ip;
+      TRY(dalloc(c, (size_t)span * 4, &ip, s));
+      d_idx = static_cast<int32_t*>(ip);
+    }
     if (fmt == MSREP_COO) {
-      TRY(upload(c, coo_row + B_lo, (size_t)nz_r, &d_aux, s));
+      void* ap;
+      TRY(dalloc(c, (size_t)span * 4, &ap, s));
+      d_crow = static_cast<int32_t*>(ap);
     } else {
       // upload the global pointer slice and rebase it on the GPU (Sec. 4.1)
       int64_t* d_g;
@@ -1095,31 +1259,51 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
       d_aux = static_cast<int32_t*>(ap);
       CUDA_TRY(launch_rebase(d_g, d_aux, W + 1, B_lo, B_hi, s));
     }
-    static_assert(sizeof(TileHost) == sizeof(int4), "tile");
-    S.tiles.insert(S.tiles.begin(), S.sell.begin(), S.sell.end());   // one list: SELL tiles first
-    std::vector<int32_t> blob16(S.tiles.size());
-    int64_t blob_total = 0;
-    for (size_t t = 0; t < S.tiles.size(); t++) {
-      const TileHost& th = S.tiles[t];
-      const int kind = th.rec == -2 ? KIND_SELL : th.rec >= 0 ? KIND_SLAB : KIND_SEG;
-      if (blob_total / 16 >= (int64_t)1 << 31) return fail(MSREP_ERR_TOO_LARGE, "tile blob exceeds 32 GiB");
-      blob16[t] = (int32_t)(blob_total / 16);
-      blob_total += blob_bytes(kind, th.packed & 0xffff, th.packed >> 16, (int)V);
-    }
     int4* d_tiles_orig;
     int32_t* d_blob16;
-    TRY(upload(c, reinterpret_cast<const int4*>(S.tiles.data()), S.tiles.size(), &d_tiles_orig, s));
+    TRY(upload(c, reinterpret_cast<const int4*>(S.tiles.data()), nt, &d_tiles_orig, s));
     TRY(upload_vec(c, blob16, &d_blob16, s));
     const size_t keep_from = c->bufs.size();
+    int64_t pack_bytes = host_res ? 16 : blob_total;
+    for (auto& ch : c->chunks) pack_bytes = std::max(pack_bytes, ch.bytes);
     void* bp;
-    TRY(dalloc(c, (size_t)std::max<int64_t>(16, blob_total), &bp, s));
-    c->d_blob = static_cast<char*>(bp);
-    PackLaunch PL{d_tiles_orig, d_blob16, (int)S.tiles.size(), vp, d_idx, d_aux, fmt == MSREP_COO, (int)V, c->wlo, c->d_blob};
-    CUDA_TRY(launch_pack(PL, s));
+    TRY(dalloc(c, (size_t)std::max<int64_t>(16, pack_bytes), &bp, s));
+    char* d_pack = static_cast<char*>(bp);
+    if (host_res) {
+      CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&c->h_blob), (size_t)std::max<int64_t>(16, blob_total), cudaHostAllocDefault));
+      c->h_bytes = blob_total;
+      c->d_blob = nullptr;
+    } else {
+      c->d_blob = d_pack;
+    }
+    for (size_t gi = 0; gi < groups.size(); gi++) {
+      const Group& g = groups[gi];
+      const int64_t zn = g.z1 - g.z0;
+      if (zn > 0) {
+        CUDA_TRY(cudaMemcpyAsync(vp, static_cast<const char*>(val) + (size_t)(B_lo + g.z0) * V, (size_t)zn * V, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(d_idx, idx + B_lo + g.z0, (size_t)zn * 4, cudaMemcpyHostToDevice, s));
+        if (d_crow) CUDA_TRY(cudaMemcpyAsync(d_crow, coo_row + B_lo + g.z0, (size_t)zn * 4, cudaMemcpyHostToDevice, s));
+      }
+      const int64_t off0 = (int64_t)blob16[(size_t)g.t0] * 16;
+      // pointers shifted by the group's first nonzero / layout offset: tiles index them unchanged
+      PackLaunch PL{d_tiles_orig + g.t0, d_blob16 + g.t0, g.t1 - g.t0,
+                    static_cast<const char*>(vp) - (size_t)g.z0 * V, d_idx - g.z0,
+                    d_crow ? d_crow - g.z0 : d_aux, fmt == MSREP_COO, (int)V, c->wlo,
+                    host_res ? d_pack - off0 : d_pack};
+      CUDA_TRY(launch_pack(PL, s));
+      if (host_res)
+        CUDA_TRY(cudaMemcpyAsync(c->h_blob + off0, d_pack, (size_t)c->chunks[gi].bytes, cudaMemcpyDeviceToHost, s));
+    }
     std::vector<TileHost> fin(S.tiles);
     for (size_t t = 0; t < fin.size(); t++) fin[t].nz0 = blob16[t];
     CUDA_TRY(cudaStreamSynchronize(s));
-    release_range(c, mark, keep_from);   // plain slices are no longer needed: the blobs hold the partition
+    // plain slices are no longer needed: the blobs hold the partition (host-resident: the
+    // pinned copy does, and the packing buffer goes too)
+    release_range(c, mark, host_res ? c->bufs.size() : keep_from);
+    if (host_res) {
+      TRY(ensure_copy_stream(c));
+      TRY(alloc_stages(c, s));
+    }
     TRY(upload(c, reinterpret_cast<const int4*>(fin.data()), fin.size(), &c->d_tiles, s));
     c->blob_bytes = blob_total;
     void* rp;
@@ -1145,6 +1329,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     }
   }
   CUDA_TRY(cudaStreamSynchronize(s));
+  lap(3);
   const auto t1 = std::chrono::steady_clock::now();
 
   // ---- stats (X_p by bitmap; outside the partition timer)
@@ -1155,6 +1340,10 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   st.rows_window = W;
   st.ntiles = colwise(fmt) ? c->citems : c->ntiles; st.nsell = c->nsell; st.nslabs = c->nslabs; st.nsplit_rows = c->nsplit; st.nheads_local = c->nheads_local;
   st.partition_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  for (int k = 0; k < 4; k++) st.phase_ms[k] = phase[k];
+  st.residency = c->residency;
+  st.nchunks = (int64_t)c->chunks.size();
+  st.host_bytes = c->h_bytes;
   int64_t X = 0;
   if (colwise(fmt)) {
     X = W;   // pCSC reads x only over its column window
@@ -1184,9 +1373,10 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   st.owned_rows = own;
   st.alg_bytes = base + ybytes_b1;
   st.alg_bytes_beta0 = base + ybytes_b0;
+  const int64_t nmain = c->chunks.empty() ? 1 : (int64_t)c->chunks.size();   // main-kernel launches
   if (colwise(fmt))
-    st.kernels_per_spmv = (c->cnb ? 1 : 0) + ((c->nranks > 1 || c->csplit) ? 1 /*py epilogue*/ : 0) + (c->csplit ? 1 /*memset*/ : 0);
-  else st.kernels_per_spmv = (c->ntiles ? 1 : 0) + (c->nranks > 1 && c->any_flag ? 1 : 0) + (c->nsplit ? 1 : 0);
+    st.kernels_per_spmv = (c->cnb ? nmain : 0) + ((c->nranks > 1 || c->csplit) ? 1 /*py epilogue*/ : 0) + (c->csplit ? 1 /*memset*/ : 0);
+  else st.kernels_per_spmv = (c->ntiles ? nmain : 0) + (c->nranks > 1 && c->any_flag ? 1 : 0) + (c->nsplit ? 1 : 0);
   int64_t db = 0;
   for (auto& b : c->bufs) db += (int64_t)b.bytes;
   st.device_bytes = db;
@@ -1265,7 +1455,19 @@ msrep_status_t spmv_impl(msrep_ctx h, const void* alpha_p, const void* x, const 
     L.m = c->m; L.alpha = alpha; L.beta = beta; L.dtype = dt;
     cudaEvent_t pe;
     TRY(prof_begin(c, s, &pe));
-    CUDA_TRY(launch_cols(L, s));
+    if (c->residency == MSREP_RESIDENT_HOST) {
+      TRY(stream_chunks(c, s, [&](const Ctx::Chunk& ch, const char* base) -> msrep_status_t {
+        ColLaunch Lc = L;
+        Lc.blob = base;
+        Lc.band0 = ch.t0; Lc.nb = ch.t1 - ch.t0;
+        Lc.units = L.units ? L.units + ch.u0 : nullptr; Lc.nunits = ch.u1 - ch.u0;
+        if (Lc.split_items && Lc.nunits == 0) return MSREP_OK;
+        CUDA_TRY(launch_cols(Lc, s));
+        return MSREP_OK;
+      }));
+    } else {
+      CUDA_TRY(launch_cols(L, s));
+    }
     if (pe) CUDA_TRY(cudaEventRecord(pe, s));
     if (c->nranks > 1) {
       double* shard = c->d_py + (size_t)c->rank * c->shard;
@@ -1289,7 +1491,17 @@ msrep_status_t spmv_impl(msrep_ctx h, const void* alpha_p, const void* x, const 
   for (int mi = 0; mi < nmirror; mi++) L.mirror[mi] = mirrors[mi];
   cudaEvent_t pe;
   TRY(prof_begin(c, s, &pe));
-  CUDA_TRY(launch_rows(L, s));
+  if (c->residency == MSREP_RESIDENT_HOST) {
+    TRY(stream_chunks(c, s, [&](const Ctx::Chunk& ch, const char* base) -> msrep_status_t {
+      RowLaunch Lc = L;
+      Lc.tiles = c->d_tiles + ch.t0; Lc.ntiles = ch.t1 - ch.t0;
+      Lc.blob = base; Lc.has_sell = ch.has_sell;
+      CUDA_TRY(launch_rows(Lc, s));
+      return MSREP_OK;
+    }));
+  } else {
+    CUDA_TRY(launch_rows(L, s));
+  }
   if (pe) CUDA_TRY(cudaEventRecord(pe, s));
   if (c->nranks > 1 && c->any_flag) {
     HeadLaunch H{c->vparts, c->d_part_rec, c->d_rec, c->d_head_local, 1};
@@ -1349,7 +1561,17 @@ msrep_status_t msrep_spmm(msrep_ctx h, const void* alpha_p, const void* X, const
   L.dtype = dt; L.has_sell = c->nsell > 0;
   cudaEvent_t pe;
   TRY(prof_begin(c, s, &pe));
-  CUDA_TRY(launch_rows_mm(L, k, s));
+  if (c->residency == MSREP_RESIDENT_HOST) {
+    TRY(stream_chunks(c, s, [&](const Ctx::Chunk& ch, const char* base) -> msrep_status_t {
+      RowLaunch Lc = L;
+      Lc.tiles = c->d_tiles + ch.t0; Lc.ntiles = ch.t1 - ch.t0;
+      Lc.blob = base; Lc.has_sell = ch.has_sell;
+      CUDA_TRY(launch_rows_mm(Lc, k, s));
+      return MSREP_OK;
+    }));
+  } else {
+    CUDA_TRY(launch_rows_mm(L, k, s));
+  }
   if (pe) CUDA_TRY(cudaEventRecord(pe, s));
   if (c->nranks > 1 && c->any_flag) {
     HeadLaunch H{c->vparts, c->d_part_rec, c->d_rec_mm, c->d_head_local_mm, k};

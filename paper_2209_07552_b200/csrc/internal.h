@@ -123,7 +123,7 @@ struct ColLaunch {
   const int64_t* item_off;    // byte offset of each item's first stage blob
   const int32_t* band_item;   // [nb + 1]: items of band b are [band_item[b], band_item[b+1])
   const int32_t* split;       // [nb * (CB_W + 1)]: warp w owns band rows [split[b*(CB_W+1)+w], ...[w+1])
-  int nb;
+  int nb, band0;              // bands [band0, band0 + nb) (band0 > 0: a host-resident chunk)
   const char* blob;
   const void* x; int64_t xbase;                              // x index of window column 0
   void* out; int64_t m;                                      // fused: y (dtype); else fp64 py

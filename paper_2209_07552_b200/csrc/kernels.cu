@@ -788,7 +788,7 @@ __global__ void __launch_bounds__(CB_THREADS, 1) csc_band_kernel(const ColLaunch
         stage(make_int4(-1, 0, 0, 0), nullptr, 0);
         return;
       }
-      for (int b = blockIdx.x; b < P.nb; b += gridDim.x) {
+      for (int b = P.band0 + blockIdx.x; b < P.band0 + P.nb; b += gridDim.x) {
         const int i0 = P.band_item[b], i1 = P.band_item[b + 1];
         if (i0 == i1) {   // empty band: still written out (zeros / beta*y)
           stage(make_int4(b, 0, 0, 1), nullptr, 0);

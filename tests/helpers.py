@@ -45,7 +45,7 @@ def assert_close(got, ref, bound, dtype):
                            f"got {got[bad][:5]} ref {ref[bad][:5]} bound {bound[bad][:5]}")
 
 
-def run_gpu(A, fmt, x, y, alpha, beta, parts=1, layout=None, host_path=False, ctx=None, repeat=1):
+def run_gpu(A, fmt, x, y, alpha, beta, parts=1, layout=None, host_path=False, ctx=None, repeat=1, **pkw):
     """Partition A (gen.Sparse CSR or CSC) as `fmt` on cuda:0 with `parts` virtual parts; return y."""
     import torch
     import paper_2209_07552_b200 as M
@@ -55,16 +55,16 @@ def run_gpu(A, fmt, x, y, alpha, beta, parts=1, layout=None, host_path=False, ct
         ctx = M.Context(0, 1, None, 0, parts)
     if fmt == "csr":
         assert A["fmt"] == "csr"
-        ctx.partition("csr", A["m"], A["n"], ptr=A["ptr"], idx=A["idx"], val=A["val"])
+        ctx.partition("csr", A["m"], A["n"], ptr=A["ptr"], idx=A["idx"], val=A["val"], **pkw)
     elif fmt == "coo":
         assert A["fmt"] == "csr"
-        ctx.partition("coo", A["m"], A["n"], idx=A["idx"], val=A["val"], coo_row=coo_of_csr(A))
+        ctx.partition("coo", A["m"], A["n"], idx=A["idx"], val=A["val"], coo_row=coo_of_csr(A), **pkw)
     elif fmt == "coo_col":   # column-sorted COO: coo_row carries the sorted column ids
         assert A["fmt"] == "csc"
-        ctx.partition("coo_col", A["m"], A["n"], idx=A["idx"], val=A["val"], coo_row=coo_of_csr(A))
+        ctx.partition("coo_col", A["m"], A["n"], idx=A["idx"], val=A["val"], coo_row=coo_of_csr(A), **pkw)
     else:
         assert A["fmt"] == "csc"
-        ctx.partition("csc", A["m"], A["n"], ptr=A["ptr"], idx=A["idx"], val=A["val"])
+        ctx.partition("csc", A["m"], A["n"], ptr=A["ptr"], idx=A["idx"], val=A["val"], **pkw)
     if layout is None:
         layout = M.Y_REPLICATED
     if host_path:
