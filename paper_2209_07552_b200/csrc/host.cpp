@@ -136,6 +136,22 @@ void plan_coo(int64_t m, int np, const int32_t* row, const std::vector<int64_t>&
   }
 }
 
+// ------------------------------------------------ host threads for the partition scans
+// The partition's O(nnz) host passes run on the host threads, one contiguous index range each
+// (Sec. 4.1, "we parallelize the partition process through multi-threading").
+int host_threads(int64_t n) {
+  if (n < ((int64_t)1 << 20)) return 1;
+  return (int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+}
+template <class F>   // f(lo, hi) over [0, n) in T contiguous ranges
+void par_ranges(int64_t n, F&& f) {
+  const int T = host_threads(n);
+  if (T == 1) { f((int64_t)0, n); return; }
+  std::vector<std::thread> th;
+  for (int t = 1; t < T; t++) th.emplace_back([&, t] { f(n * t / T, n * (t + 1) / T); });
+  f((int64_t)0, n / T);
+  for (auto& x : th) x.join();
+}
 // ---------------------------------------------------------------- memory
 struct DevBuf {
   void* p = nullptr;
@@ -220,6 +236,11 @@ struct Ctx {
   cudaStream_t cs = nullptr;        // copy stream
   cudaEvent_t ev_go = nullptr, ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
 
+  // partition uploads from pageable caller memory: a pinned two-slot ring (host threads copy
+  // into one slot while the DMA drains the other)
+  char* h_ring[2] = {nullptr, nullptr};
+  cudaEvent_t ring_ev[2] = {nullptr, nullptr};
+
   // host-vector path buffers
   void* d_hx = nullptr;
   void* d_hy = nullptr;
@@ -293,11 +314,42 @@ void free_all(Ctx* c) {
   c->d_rec_mm = c->d_head_local_mm = c->d_head_all_mm = nullptr;
 }
 
+// H2D of `bytes` from pageable host memory, enqueued on s.  Large copies go through the pinned
+// ring: the host threads fill slot i%2 (after its previous DMA has drained) while the DMA of
+// the other slot runs, so the copy proceeds at the pinned H2D rate instead of the driver's
+// pageable path (Sec. 4.1 partition optimisation).
+constexpr size_t kRingSlot = (size_t)32 << 20;
+msrep_status_t h2d(Ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (bytes < ((size_t)8 << 20)) {
+    if (bytes) CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+    return MSREP_OK;
+  }
+  if (!c->h_ring[0]) {
+    for (int b = 0; b < 2; b++) {
+      CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&c->h_ring[b]), kRingSlot, cudaHostAllocDefault));
+      CUDA_TRY(cudaEventCreateWithFlags(&c->ring_ev[b], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventRecord(c->ring_ev[b], s));
+    }
+  }
+  const char* sp = static_cast<const char*>(src);
+  char* dp = static_cast<char*>(dst);
+  for (size_t off = 0, i = 0; off < bytes; off += kRingSlot, i++) {
+    const int b = (int)(i & 1);
+    const size_t len = std::min(kRingSlot, bytes - off);
+    CUDA_TRY(cudaEventSynchronize(c->ring_ev[b]));
+    char* slot = c->h_ring[b];
+    par_ranges((int64_t)len, [&](int64_t lo, int64_t hi) { memcpy(slot + lo, sp + off + lo, (size_t)(hi - lo)); });
+    CUDA_TRY(cudaMemcpyAsync(dp + off, slot, len, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaEventRecord(c->ring_ev[b], s));
+  }
+  return MSREP_OK;
+}
+
 template <class T>
 msrep_status_t upload(Ctx* c, const T* host, size_t count, T** out, cudaStream_t s) {
   void* p;
   TRY(dalloc(c, count * sizeof(T), &p, s));
-  if (count) CUDA_TRY(cudaMemcpyAsync(p, host, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  TRY(h2d(c, p, host, count * sizeof(T), s));
   *out = static_cast<T*>(p);
   return MSREP_OK;
 }
@@ -808,6 +860,24 @@ double get_scalar(const void* p, msrep_dtype t) {
 }  // namespace
 
 // ======================================================================= ABI
+// smallest k in [0, n) with bad(k) != 0 (and that code), or -1
+template <class F>
+int64_t par_first_bad(int64_t n, int* code, F&& bad) {
+  std::atomic<int64_t> first{INT64_MAX};
+  par_ranges(n, [&](int64_t lo, int64_t hi) {
+    for (int64_t k = lo; k < hi && k < first.load(std::memory_order_relaxed); k++)
+      if (bad(k)) {
+        int64_t cur = first.load();
+        while (k < cur && !first.compare_exchange_weak(cur, k)) {}
+        break;
+      }
+  });
+  const int64_t k = first.load();
+  if (k == INT64_MAX) return -1;
+  *code = bad(k);
+  return k;
+}
+
 // ------------------------------------------------ host-resident streaming
 msrep_status_t ensure_copy_stream(Ctx* c) {
   if (c->cs) return MSREP_OK;
@@ -1014,6 +1084,10 @@ msrep_status_t msrep_destroy(msrep_ctx h) {
   free_all(c);
   for (auto& p : c->ev) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
   if (c->cs) cudaStreamDestroy(c->cs);
+  for (int b = 0; b < 2; b++) {
+    if (c->h_ring[b]) cudaFreeHost(c->h_ring[b]);
+    if (c->ring_ev[b]) cudaEventDestroy(c->ring_ev[b]);
+  }
   for (cudaEvent_t e : {c->ev_go, c->ev_copied[0], c->ev_copied[1], c->ev_free[0], c->ev_free[1]})
     if (e) cudaEventDestroy(e);
   if (c->comm) ncclCommDestroy(c->comm);
@@ -1046,16 +1120,20 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   if (coo_like(fmt)) {
     if (nnz > 0 && !coo_row) return fail(MSREP_ERR_INVALID_ARG, "COO needs its sorted major index (coo_row)");
     const char* what = fmt == MSREP_COO ? "(row, col)" : "(col, row)";
-    for (int64_t k = 0; k < nnz; k++) {
-      if (coo_row[k] < 0 || coo_row[k] >= outer) return fail(MSREP_ERR_DIM_MISMATCH, "major index [%lld] out of range", (long long)k);
-      if (k > 0 && (coo_row[k] < coo_row[k - 1] || (coo_row[k] == coo_row[k - 1] && idx[k] < idx[k - 1])))
-        return fail(MSREP_ERR_UNSORTED_COO, "COO not sorted by %s at %lld", what, (long long)k);
-    }
+    int code = 0;
+    const int64_t k = par_first_bad(nnz, &code, [&](int64_t q) -> int {
+      if (coo_row[q] < 0 || coo_row[q] >= outer) return 1;
+      if (q > 0 && (coo_row[q] < coo_row[q - 1] || (coo_row[q] == coo_row[q - 1] && idx[q] < idx[q - 1]))) return 2;
+      return 0;
+    });
+    if (k >= 0 && code == 1) return fail(MSREP_ERR_DIM_MISMATCH, "major index [%lld] out of range", (long long)k);
+    if (k >= 0) return fail(MSREP_ERR_UNSORTED_COO, "COO not sorted by %s at %lld", what, (long long)k);
   } else {
     if (!ptr) return fail(MSREP_ERR_INVALID_ARG, "ptr NULL");
     if (ptr[0] != 0 || ptr[outer] != nnz) return fail(MSREP_ERR_DIM_MISMATCH, "ptr[0] != 0 or ptr[%lld] != nnz", (long long)outer);
-    for (int64_t r = 0; r < outer; r++)
-      if (ptr[r + 1] < ptr[r]) return fail(MSREP_ERR_DIM_MISMATCH, "ptr decreases at %lld", (long long)r);
+    int code = 0;
+    const int64_t r = par_first_bad(outer, &code, [&](int64_t q) -> int { return ptr[q + 1] < ptr[q] ? 1 : 0; });
+    if (r >= 0) return fail(MSREP_ERR_DIM_MISMATCH, "ptr decreases at %lld", (long long)r);
   }
   lap(0);
   std::vector<msrep_part_desc> parts((size_t)c->np);
@@ -1067,8 +1145,13 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   const int P0 = c->rank * c->vparts, P1 = P0 + c->vparts;
   const int64_t B_lo = bnd[(size_t)P0], B_hi = bnd[(size_t)P1];
   if (B_hi - B_lo >= kMaxRankNnz) return fail(MSREP_ERR_TOO_LARGE, "rank holds %lld nonzeros (>= 2^31 - 2^16)", (long long)(B_hi - B_lo));
-  for (int64_t k = B_lo; k < B_hi; k++)
-    if (idx[k] < 0 || idx[k] >= inner) return fail(MSREP_ERR_DIM_MISMATCH, "index %lld out of range", (long long)k);
+  {
+    int code = 0;
+    const int64_t k = par_first_bad(B_hi - B_lo, &code, [&](int64_t q) -> int {
+      return (idx[B_lo + q] < 0 || idx[B_lo + q] >= inner) ? 1 : 0;
+    });
+    if (k >= 0) return fail(MSREP_ERR_DIM_MISMATCH, "index %lld out of range", (long long)(B_lo + k));
+  }
   lap(0);
 
   CUDA_TRY(cudaSetDevice(c->device));
@@ -1109,9 +1192,18 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   const int64_t W = c->whi - c->wlo;
   lp.resize((size_t)W + 1);
   if (coo_like(fmt)) {
-    std::fill(lp.begin(), lp.end(), 0);
-    for (int64_t k = B_lo; k < B_hi; k++) lp[(size_t)(coo_row[k] - c->wlo) + 1]++;
-    for (int64_t w = 0; w < W; w++) lp[(size_t)w + 1] += lp[(size_t)w];
+    // local pointer of a sorted major index: lp[w] = first rank-local k with coo_row >= wlo + w;
+    // every row is written by the thread whose range holds the first nonzero at or after it
+    const int64_t nzr = B_hi - B_lo;
+    const int32_t* cr = coo_row + B_lo;
+    par_ranges(nzr, [&](int64_t lo, int64_t hi) {
+      for (int64_t k = lo; k < hi; k++) {
+        const int64_t prev = k == 0 ? c->wlo - 1 : (int64_t)cr[k - 1];
+        for (int64_t r = prev + 1; r <= (int64_t)cr[k]; r++) lp[(size_t)(r - c->wlo)] = k;
+      }
+    });
+    const int64_t last = nzr ? (int64_t)cr[nzr - 1] - c->wlo + 1 : 0;
+    for (int64_t w = last; w <= W; w++) lp[(size_t)w] = nzr;
   } else {
     for (int64_t w = 0; w <= W; w++) {
       int64_t v = ptr[c->wlo + w];
@@ -1141,7 +1233,11 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
       // park the band blobs in pinned memory; chunks = runs of whole bands (and, in split
       // mode, the units of those bands) of <= chunk_bytes
       CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&c->h_blob), (size_t)std::max<int64_t>(16, CB.bytes), cudaHostAllocDefault));
-      memcpy(c->h_blob, CB.blob.get(), (size_t)CB.bytes);
+      {
+        char* hb = c->h_blob;
+        const char* sb = CB.blob.get();
+        par_ranges(CB.bytes, [&](int64_t lo, int64_t hi) { memcpy(hb + lo, sb + lo, (size_t)(hi - lo)); });
+      }
       c->h_bytes = CB.bytes;
       auto band_off = [&](int64_t b) {
         const int32_t i = CB.band_item[(size_t)b];
@@ -1280,9 +1376,9 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
       const Group& g = groups[gi];
       const int64_t zn = g.z1 - g.z0;
       if (zn > 0) {
-        CUDA_TRY(cudaMemcpyAsync(vp, static_cast<const char*>(val) + (size_t)(B_lo + g.z0) * V, (size_t)zn * V, cudaMemcpyHostToDevice, s));
-        CUDA_TRY(cudaMemcpyAsync(d_idx, idx + B_lo + g.z0, (size_t)zn * 4, cudaMemcpyHostToDevice, s));
-        if (d_crow) CUDA_TRY(cudaMemcpyAsync(d_crow, coo_row + B_lo + g.z0, (size_t)zn * 4, cudaMemcpyHostToDevice, s));
+        TRY(h2d(c, vp, static_cast<const char*>(val) + (size_t)(B_lo + g.z0) * V, (size_t)zn * V, s));
+        TRY(h2d(c, d_idx, idx + B_lo + g.z0, (size_t)zn * 4, s));
+        if (d_crow) TRY(h2d(c, d_crow, coo_row + B_lo + g.z0, (size_t)zn * 4, s));
       }
       const int64_t off0 = (int64_t)blob16[(size_t)g.t0] * 16;
       // pointers shifted by the group's first nonzero / layout offset: tiles index them unchanged
@@ -1349,7 +1445,11 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     X = W;   // pCSC reads x only over its column window
   } else {
     std::vector<uint64_t> bits((size_t)(inner + 63) / 64, 0);
-    for (int64_t k = B_lo; k < B_hi; k++) bits[(size_t)idx[k] >> 6] |= 1ull << (idx[k] & 63);
+    uint64_t* bw = bits.data();
+    par_ranges(B_hi - B_lo, [&](int64_t lo, int64_t hi) {
+      for (int64_t k = B_lo + lo; k < B_lo + hi; k++)
+        __atomic_fetch_or(&bw[(size_t)idx[k] >> 6], 1ull << (idx[k] & 63), __ATOMIC_RELAXED);
+    });
     for (uint64_t w : bits) X += __builtin_popcountll(w);
   }
   st.distinct_cols = X;

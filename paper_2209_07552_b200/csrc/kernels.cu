@@ -85,14 +85,27 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+// x gathers (scalar).  MSREP_XLOAD selects the L1 policy (tuning builds, tools/variant.sh):
+// 0 = read-only path, L1 allocate; 1 = L1::no_allocate (default: R-MAT and tall-skinny gathers
+// 5-6 % faster than 0, profiles/r1_xload_variants.txt); 2 = .cg (L2 only)
+#ifndef MSREP_XLOAD
+#define MSREP_XLOAD 1
+#endif
+#if MSREP_XLOAD == 1
+#define XLD_OP "ld.global.nc.L1::no_allocate.L2::cache_hint"
+#elif MSREP_XLOAD == 2
+#define XLD_OP "ld.global.cg.L2::cache_hint"
+#else
+#define XLD_OP "ld.global.nc.L2::cache_hint"
+#endif
 __device__ __forceinline__ double ldx(const double* p, uint64_t pol) {
   double v;
-  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  asm(XLD_OP ".f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
   return v;
 }
 __device__ __forceinline__ float ldx(const float* p, uint64_t pol) {
   float v;
-  asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  asm(XLD_OP ".f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
   return v;
 }
 
