@@ -773,7 +773,7 @@ msrep_status_t build_csc_bands(const Ctx& c, const std::vector<int64_t>& lp, con
       for (int w = 0; w < CB_W; w++) B.item_hw.push_back((int32_t)(asame[(size_t)(k0 + w)] / 32));
       const int64_t nst = (L + CB_SEG - 1) / CB_SEG;
       const int64_t last = ((L - (nst - 1) * CB_SEG) + 3) & ~(int64_t)3;
-      if (nst >= ((int64_t)1 << 31)) return fail(MSREP_ERR_TOO_LARGE, "pCSC warp list too long");
+      if (nst >= ((int64_t)1 << 20)) return fail(MSREP_ERR_TOO_LARGE, "pCSC warp list too long (>= 2^20 stages)");
       key_item[(size_t)(b * B.nch + ch)] = (int64_t)B.items.size();
       B.items.push_back(make_int4((int32_t)b, (int32_t)nst, (int32_t)(ch * B.chunk), (int32_t)last));
       B.item_off.push_back(bytes);

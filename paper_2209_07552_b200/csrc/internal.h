@@ -11,8 +11,14 @@ namespace msrep {
 // rows (<= MAX_TILE_ROWS rows, <= TILE_NNZ nonzeros), or a "slab" -- a
 // contiguous piece (<= SLAB_NNZ nonzeros) of one split row whose partial sum
 // goes to a record instead of y.
-constexpr int TILE_NNZ = 512;        // fp64 SEG tiles and slabs
-constexpr int TILE_NNZ_F32 = 768;    // fp32: ~the bytes of an fp64 tile within the register budget
+#ifndef MSREP_TILE_NNZ
+#define MSREP_TILE_NNZ 512
+#endif
+#ifndef MSREP_TILE_NNZ_F32
+#define MSREP_TILE_NNZ_F32 768
+#endif
+constexpr int TILE_NNZ = MSREP_TILE_NNZ;           // fp64 SEG tiles and slabs (a multiple of 32)
+constexpr int TILE_NNZ_F32 = MSREP_TILE_NNZ_F32;   // fp32: ~the bytes of an fp64 tile within the register budget
 __host__ __device__ constexpr int tile_nnz(int vsize) { return vsize == 4 ? TILE_NNZ_F32 : TILE_NNZ; }
 constexpr int MAX_TILE_ROWS = 128;   // rows per segment tile (uint8 tile-local row keys)
 constexpr int SLAB_NNZ = 512;
@@ -118,6 +124,7 @@ constexpr uint32_t CB_HOLE = 0xffffffffu;
 #define MSREP_CB_SEG 128
 #endif
 constexpr int CB_SEG = MSREP_CB_SEG;       // entries per warp per pipeline stage
+static_assert(CB_SEG % 32 == 0 && CB_SEG < 2048, "stage descriptors pack seg in 11 bits");
 struct ColLaunch {
   const int4* items;          // per item: {band, nstages, window col base, last-stage entries per warp}
   const int64_t* item_off;    // byte offset of each item's first stage blob

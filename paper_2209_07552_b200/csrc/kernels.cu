@@ -714,7 +714,7 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 // one consumer warp's share of a stage, in registers
 template <typename VT>
 struct CBStage {
-  int4 d;                 // {band (-1: end), seg | stage << 8, window col base, last | same-row << 1 | item << 2}
+  int4 d;                 // {band (-1: end), seg | stage << 11, window col base, last | same-row << 1 | item << 2}
   uint32_t pk[CB_PER];
   VT v[CB_PER], xv[CB_PER];
 };
@@ -728,7 +728,7 @@ __device__ __forceinline__ void cb_load(CBStage<VT>& S, int it, const unsigned c
   const int s = it % CB_NS;
   mbar_wait(&full[s], (uint32_t)((it / CB_NS) & 1));
   S.d = sdesc[s];
-  const int seg = S.d.y & 0xff;
+  const int seg = S.d.y & 0x7ff;
   const unsigned char* st = smem + L::ST_OFF + s * L::STAGE;
   const VT* sv = reinterpret_cast<const VT*>(st) + warp * seg;
   const uint32_t* sp = reinterpret_cast<const uint32_t*>(st + CB_W * seg * V) + warp * seg;
@@ -791,7 +791,7 @@ __global__ void __launch_bounds__(CB_THREADS, 1) csc_band_kernel(const ColLaunch
             for (int sg = s0; sg < s1; sg++) {
               const int seg = sg == item.y - 1 ? item.w : CB_SEG;
               const int bytes = CB_W * seg * (V + 4);
-              stage(make_int4(b, seg | (sg << 8), item.z, (g + sg == un.z - 1 ? 1 : 0) | (sg < hst ? 2 : 0) | (i << 2)),
+              stage(make_int4(b, seg | (sg << 11), item.z, (g + sg == un.z - 1 ? 1 : 0) | (sg < hst ? 2 : 0) | (i << 2)),
                     src, bytes);
               src += bytes;
             }
@@ -814,7 +814,7 @@ __global__ void __launch_bounds__(CB_THREADS, 1) csc_band_kernel(const ColLaunch
           for (int sg = 0; sg < item.y; sg++) {
             const int seg = sg == item.y - 1 ? item.w : CB_SEG;
             const int bytes = CB_W * seg * (V + 4);
-            stage(make_int4(b, seg | (sg << 8), item.z,
+            stage(make_int4(b, seg | (sg << 11), item.z,
                             ((i == i1 - 1 && sg == item.y - 1) ? 1 : 0) | (sg < hst ? 2 : 0) | (i << 2)), src, bytes);
             src += bytes;
           }
@@ -838,7 +838,7 @@ __global__ void __launch_bounds__(CB_THREADS, 1) csc_band_kernel(const ColLaunch
     // the scatter: 32 distinct rows per step, steps in list order (deterministic)
     if (A.d.w & 2) {   // this stage may hold SAME-ROW groups (heavy rows; placed first in each list)
       const int hw = P.item_hw[(A.d.w >> 2) * CB_W + warp];   // same-row groups leading this warp's list
-      const int j0 = (A.d.y >> 8) * CB_PER;                   // list step of k = 0
+      const int j0 = (A.d.y >> 11) * CB_PER;                   // list step of k = 0
 #pragma unroll
       for (int k = 0; k < CB_PER; k++) {
         if (j0 + k < hw) {   // 32 entries of one heavy row: one warp-reduced update
