@@ -14,8 +14,8 @@ import csv,sys
 r=list(csv.reader(sys.stdin)); h=r[0]; v=r[2]
 d=dict(zip(h,v))
 try:
-    rd=float(d['dram__bytes_read.sum']); wr=float(d['dram__bytes_write.sum']); un=r[1][h.index('dram__bytes_read.sum')]
-    print('   dram read', rd, un, 'write', wr, un)
+    rd=float(d['dram__bytes_read.sum']); wr=float(d['dram__bytes_write.sum'])
+    print('   dram read', rd, r[1][h.index('dram__bytes_read.sum')], 'write', wr, r[1][h.index('dram__bytes_write.sum')])
 except Exception as e: print(e)
 "
 ncu -i $rep --page source --csv --print-source sass > /tmp/_sass.csv 2>/dev/null
