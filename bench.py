@@ -353,7 +353,7 @@ def main():
             "clocks": clocks,
             "partition_ms": st["partition_ms"],
             "stats_rank0": {k: st[k] for k in ("nnz_rank", "ntiles", "nsell", "nslabs", "nsplit_rows",
-                                               "distinct_cols", "kernels_per_spmv", "tile_bytes")},
+                                               "distinct_cols", "kernels_per_spmv", "tile_bytes", "x_no_allocate")},
         }
         print(json.dumps(out), flush=True)
     ctx.close()

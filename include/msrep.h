@@ -128,6 +128,8 @@ typedef struct {
   int64_t residency;         /* msrep_residency of the partition                             */
   int64_t nchunks;           /* MSREP_RESIDENT_HOST: chunks streamed per SpMV (else 0)       */
   int64_t host_bytes;        /* MSREP_RESIDENT_HOST: pinned bytes streamed H2D per SpMV      */
+  int64_t x_no_allocate;     /* x-gather L1 policy picked at partition (1: L1::no_allocate; timed
+                                both ways on the built layout, or forced by MSREP_XLOAD=0|1)  */
 } msrep_stats;
 
 /* NCCL unique id for the communicator (rank 0 creates it, the caller

@@ -54,7 +54,8 @@ class Stats(ctypes.Structure):
         "device_bytes")] + [("partition_ms", ctypes.c_double), ("tile_bytes", ctypes.c_int64),
                                          ("nsell", ctypes.c_int64),
                                          ("phase_ms", ctypes.c_double * 4), ("residency", ctypes.c_int64),
-                                         ("nchunks", ctypes.c_int64), ("host_bytes", ctypes.c_int64)]
+                                         ("nchunks", ctypes.c_int64), ("host_bytes", ctypes.c_int64),
+                                         ("x_no_allocate", ctypes.c_int64)]
 
 
 class Allocator(ctypes.Structure):

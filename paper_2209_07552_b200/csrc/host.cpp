@@ -226,6 +226,7 @@ struct Ctx {
 
   // MSREP_RESIDENT_HOST: the device layout parked in pinned host memory, streamed per call
   // in chunks (row formats: tile ranges; pCSC: band ranges) through two staging buffers
+  int xna = 0;                      // x-gather L1 policy of the partition (1: L1::no_allocate)
   int residency = MSREP_RESIDENT_DEVICE;
   int64_t chunk_bytes = (int64_t)256 << 20;
   struct Chunk { int32_t t0, t1, u0, u1; int64_t off, bytes; bool has_sell; };
@@ -878,6 +879,75 @@ int64_t par_first_bad(int64_t n, int* code, F&& bad) {
   return k;
 }
 
+// ------------------------------------------------ main-kernel launch descriptors
+RowLaunch row_launch(const Ctx* c, const void* x, void* y, double alpha, double beta) {
+  RowLaunch L{};
+  L.tiles = c->d_tiles; L.ntiles = c->ntiles;
+  L.blob = c->d_blob;
+  L.x = x; L.y = y; L.ybase = c->wlo;
+  L.xmax = c->n > 0 ? (uint32_t)(c->n - 1) : 0u;
+  L.alpha = alpha; L.beta = beta; L.rec = c->d_rec;
+  L.dtype = c->dtype == MSREP_F64 ? 0 : 1; L.has_sell = c->nsell > 0;
+  L.xna = c->xna;
+  return L;
+}
+ColLaunch col_launch(const Ctx* c, const void* x, void* y, double alpha, double beta) {
+  ColLaunch L{};
+  L.items = c->d_citems; L.item_off = c->d_item_off; L.band_item = c->d_band_item; L.split = c->d_split;
+  L.nb = (int)c->cnb; L.blob = c->d_cblob;
+  L.x = x; L.xbase = c->wlo;
+  L.split_items = c->csplit; L.nunits = (int)c->cunits; L.units = c->d_cunits; L.item_hst = c->d_item_hst;
+  L.item_hw = c->d_item_hw;
+  L.fused = c->nranks == 1 && !c->csplit;
+  L.out = L.fused ? y : static_cast<void*>(c->d_py);
+  L.m = c->m; L.alpha = alpha; L.beta = beta; L.dtype = c->dtype == MSREP_F64 ? 0 : 1;
+  L.xna = c->xna;
+  return L;
+}
+
+// x-gather L1 policy.  Whether the L1 should allocate the x lines depends on the matrix: gathers
+// that neighbouring rows / warps of an SM re-hit (stencil pCOO, banded, block-diagonal, short-wide
+// pCSC) want it; gathers with no reuse inside an SM (R-MAT, uniform random) are 5-6 % faster with
+// L1::no_allocate (profiles/r1_xload_variants.txt, r1_suite_sweep.jsonl).  Both policies give
+// identical bits, so the partition times the main kernel once with each on the built layout
+// (dummy x = 0, y into scratch; 1 warm-up + 3 timed launches) and keeps the faster.  MSREP_XLOAD=0|1
+// in the environment forces a policy.  Host-resident and small partitions (< 2^20 nonzeros)
+// keep the allocating policy.
+msrep_status_t tune_xload(Ctx* c, cudaStream_t s, int64_t nz_r) {
+  const char* env = getenv("MSREP_XLOAD");
+  if (env && (env[0] == '0' || env[0] == '1') && env[1] == 0) { c->xna = env[0] - '0'; return MSREP_OK; }
+  c->xna = 0;
+  if (c->residency == MSREP_RESIDENT_HOST || nz_r < ((int64_t)1 << 20)) return MSREP_OK;
+  const size_t V = vsz(c->dtype), mark = c->bufs.size();
+  void *dx, *dy;
+  TRY(dalloc(c, (size_t)std::max<int64_t>(1, c->n) * V, &dx, s));
+  TRY(dalloc(c, (size_t)std::max<int64_t>(1, c->m) * V, &dy, s));
+  CUDA_TRY(cudaMemsetAsync(dx, 0, (size_t)std::max<int64_t>(1, c->n) * V, s));
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  float best = 0.f;
+  int pick = 0;
+  for (int na = 0; na < 2; na++) {
+    c->xna = na;
+    float ms = 0.f;
+    for (int it = 0; it < 4; it++) {
+      if (it == 1) CUDA_TRY(cudaEventRecord(e0, s));
+      if (colwise(c->fmt)) CUDA_TRY(launch_cols(col_launch(c, dx, dy, 1.0, 0.0), s));
+      else CUDA_TRY(launch_rows(row_launch(c, dx, dy, 1.0, 0.0), s));
+    }
+    CUDA_TRY(cudaEventRecord(e1, s));
+    CUDA_TRY(cudaEventSynchronize(e1));
+    CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+    if (na == 0 || ms < best) { best = ms; pick = na; }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  c->xna = pick;
+  release_range(c, mark, c->bufs.size());
+  return MSREP_OK;
+}
+
 // ------------------------------------------------ host-resident streaming
 msrep_status_t ensure_copy_stream(Ctx* c) {
   if (c->cs) return MSREP_OK;
@@ -1427,6 +1497,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   CUDA_TRY(cudaStreamSynchronize(s));
   lap(3);
   const auto t1 = std::chrono::steady_clock::now();
+  TRY(tune_xload(c, s, nz_r));   // outside the partition timer: a measurement, not partitioning
 
   // ---- stats (X_p by bitmap; outside the partition timer)
   msrep_stats& st = c->stats;
@@ -1440,6 +1511,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   st.residency = c->residency;
   st.nchunks = (int64_t)c->chunks.size();
   st.host_bytes = c->h_bytes;
+  st.x_no_allocate = c->xna;
   int64_t X = 0;
   if (colwise(fmt)) {
     X = W;   // pCSC reads x only over its column window
@@ -1543,16 +1615,8 @@ msrep_status_t spmv_impl(msrep_ctx h, const void* alpha_p, const void* x, const 
   }
 
   if (colwise(c->fmt)) {
-    ColLaunch L{};
-    L.items = c->d_citems; L.item_off = c->d_item_off; L.band_item = c->d_band_item; L.split = c->d_split;
-    L.nb = (int)c->cnb; L.blob = c->d_cblob;
-    L.x = x; L.xbase = c->wlo;
-    L.split_items = c->csplit; L.nunits = (int)c->cunits; L.units = c->d_cunits; L.item_hst = c->d_item_hst;
-    L.item_hw = c->d_item_hw;
-    L.fused = c->nranks == 1 && !c->csplit;
-    L.out = L.fused ? y : static_cast<void*>(c->d_py);
+    ColLaunch L = col_launch(c, x, y, alpha, beta);
     if (c->csplit) CUDA_TRY(cudaMemsetAsync(c->d_py, 0, (size_t)c->m * 8, s));   // items add into py
-    L.m = c->m; L.alpha = alpha; L.beta = beta; L.dtype = dt;
     cudaEvent_t pe;
     TRY(prof_begin(c, s, &pe));
     if (c->residency == MSREP_RESIDENT_HOST) {
@@ -1580,13 +1644,7 @@ msrep_status_t spmv_impl(msrep_ctx h, const void* alpha_p, const void* x, const 
     return MSREP_OK;
   }
 
-  RowLaunch L{};
-  L.tiles = c->d_tiles; L.ntiles = c->ntiles;
-  L.blob = c->d_blob;
-  L.x = x; L.y = y; L.ybase = c->wlo;
-  L.xmax = c->n > 0 ? (uint32_t)(c->n - 1) : 0u;
-  L.alpha = alpha; L.beta = beta; L.rec = c->d_rec;
-  L.dtype = dt; L.has_sell = c->nsell > 0;
+  RowLaunch L = row_launch(c, x, y, alpha, beta);
   L.nmirror = nmirror;
   for (int mi = 0; mi < nmirror; mi++) L.mirror[mi] = mirrors[mi];
   cudaEvent_t pe;

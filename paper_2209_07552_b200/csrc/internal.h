@@ -98,6 +98,7 @@ struct RowLaunch {
   int dtype;                                                 // dtype 0 = f64, 1 = f32
   int has_sell;                                              // tiles begin with SELL tiles
   int nmirror; void* mirror[MAX_MIRRORS];                    // y rows are also stored here (msrep_spmv_mirror)
+  int xna;                                                   // x gathers with L1::no_allocate (SEG / slab tiles)
 };
 
 // pCSC row-band layout.  The rank's nonzeros are regrouped
@@ -143,6 +144,7 @@ struct ColLaunch {
   const int4* units;
   const int32_t* item_hst;    // [items]: stages [0, item_hst[i]) may hold same-row groups
   const int32_t* item_hw;     // [items * CB_W]: same-row groups leading warp w's list of item i
+  int xna;                    // x gathers with L1::no_allocate
 };
 
 struct FixupLaunch {

@@ -85,27 +85,23 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
-// x gathers (scalar).  MSREP_XLOAD selects the L1 policy (tuning builds, tools/variant.sh):
-// 0 = read-only path, L1 allocate; 1 = L1::no_allocate (default: R-MAT and tall-skinny gathers
-// 5-6 % faster than 0, profiles/r1_xload_variants.txt); 2 = .cg (L2 only)
-#ifndef MSREP_XLOAD
-#define MSREP_XLOAD 1
-#endif
-#if MSREP_XLOAD == 1
-#define XLD_OP "ld.global.nc.L1::no_allocate.L2::cache_hint"
-#elif MSREP_XLOAD == 2
-#define XLD_OP "ld.global.cg.L2::cache_hint"
-#else
-#define XLD_OP "ld.global.nc.L2::cache_hint"
-#endif
+// x gathers (scalar).  NA selects the L1 policy per partition (RowLaunch / ColLaunch .xna, chosen
+// by msrep_partition, host.cpp "x-gather L1 policy"): NA = L1::no_allocate, for gathers without
+// reuse inside an SM (R-MAT, uniform random: 5-6 % faster, profiles/r1_xload_variants.txt); else
+// the read-only path with L1 allocation, for gathers that neighbouring rows / warps re-hit
+// (stencil pCOO, banded, block-diagonal, short-wide pCSC).
+template <bool NA>
 __device__ __forceinline__ double ldx(const double* p, uint64_t pol) {
   double v;
-  asm(XLD_OP ".f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  if constexpr (NA) asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  else asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
   return v;
 }
+template <bool NA>
 __device__ __forceinline__ float ldx(const float* p, uint64_t pol) {
   float v;
-  asm(XLD_OP ".f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  if constexpr (NA) asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  else asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
   return v;
 }
 
@@ -238,7 +234,7 @@ __device__ __forceinline__ void sell_tile(const RowLaunch& P, const int4 d, cons
   refill();
 }
 
-template <typename VT, bool SELL, bool MIRROR>
+template <typename VT, bool SELL, bool MIRROR, bool NA>
 __global__ void __launch_bounds__(WARPS * 32, MSREP_ROW_MINB) rows_kernel(const RowLaunch P) {
   using Lay = RowLayout<VT, SELL>;
   constexpr int QMAX = qmax<VT>();
@@ -339,7 +335,7 @@ __global__ void __launch_bounds__(WARPS * 32, MSREP_ROW_MINB) rows_kernel(const 
     VT xv[QMAX + 1];
     if (slab) {
 #pragma unroll
-      for (int u = 0; u < QMAX; u++) xv[u] = lane + 32 * u < nnz ? ldx(x + c[u], xpol) : VT(0);
+      for (int u = 0; u < QMAX; u++) xv[u] = lane + 32 * u < nnz ? ldx<NA>(x + c[u], xpol) : VT(0);
       double acc = 0.0;
 #pragma unroll
       for (int u = 0; u < QMAX; u++) acc = fma((double)v[u], (double)xv[u], acc);   // padding: 0 * 0
@@ -358,7 +354,7 @@ __global__ void __launch_bounds__(WARPS * 32, MSREP_ROW_MINB) rows_kernel(const 
 #pragma unroll
     for (int j = 0; j <= QMAX; j++) {
       const bool on = j < QMAX ? j < q : extra;
-      xv[j] = on ? ldx(x + c[j], xpol) : VT(0);
+      xv[j] = on ? ldx<NA>(x + c[j], xpol) : VT(0);
     }
     for (int rr = lane; rr < nrows; rr += 32) rsum[rr] = 0.0;
     __syncwarp();
@@ -719,7 +715,7 @@ struct CBStage {
   VT v[CB_PER], xv[CB_PER];
 };
 
-template <typename VT>
+template <typename VT, bool NA>
 __device__ __forceinline__ void cb_load(CBStage<VT>& S, int it, const unsigned char* smem, const int4* sdesc,
                                         uint64_t* full, uint64_t* empty, const VT* x, uint64_t xpol, int warp,
                                         int lane) {
@@ -743,10 +739,10 @@ __device__ __forceinline__ void cb_load(CBStage<VT>& S, int it, const unsigned c
   if (lane == 0) mbar_arrive(&empty[s]);   // the stage is free: the data is in registers
   const VT* xb = x + S.d.z;
 #pragma unroll
-  for (int k = 0; k < CB_PER; k++) S.xv[k] = S.pk[k] != CB_HOLE ? ldx(xb + (S.pk[k] >> CB_LOG2), xpol) : VT(0);
+  for (int k = 0; k < CB_PER; k++) S.xv[k] = S.pk[k] != CB_HOLE ? ldx<NA>(xb + (S.pk[k] >> CB_LOG2), xpol) : VT(0);
 }
 
-template <typename VT>
+template <typename VT, bool NA>
 __global__ void __launch_bounds__(CB_THREADS, 1) csc_band_kernel(const ColLaunch P) {
   using L = CBLayout<VT>;
   constexpr int V = (int)sizeof(VT);
@@ -832,9 +828,9 @@ __global__ void __launch_bounds__(CB_THREADS, 1) csc_band_kernel(const ColLaunch
   named_bar_sync(1, CB_NC);
   CBStage<VT> A, B;
   int it = 0;
-  cb_load(A, it++, smem, sdesc, full, empty, x, xpol, warp, lane);
+  cb_load<VT, NA>(A, it++, smem, sdesc, full, empty, x, xpol, warp, lane);
   while (A.d.x >= 0) {
-    cb_load(B, it++, smem, sdesc, full, empty, x, xpol, warp, lane);   // next stage's gathers fly during A's scatter
+    cb_load<VT, NA>(B, it++, smem, sdesc, full, empty, x, xpol, warp, lane);   // next stage's gathers fly during A's scatter
     // the scatter: 32 distinct rows per step, steps in list order (deterministic)
     if (A.d.w & 2) {   // this stage may hold SAME-ROW groups (heavy rows; placed first in each list)
       const int hw = P.item_hw[(A.d.w >> 2) * CB_W + warp];   // same-row groups leading this warp's list
@@ -1155,13 +1151,17 @@ int grid_for(K kernel, int smem_bytes, int ntiles) {
   return (int)(want < g ? (want < 1 ? 1 : want) : g);
 }
 
+template <typename VT, bool SELL, bool MIRROR, bool NA>
+cudaError_t launch_rows_k(const RowLaunch& L, cudaStream_t s) {
+  constexpr int b = RowLayout<VT, SELL>::TOTAL;
+  cudaError_t e = set_smem(rows_kernel<VT, SELL, MIRROR, NA>, b);
+  if (e) return e;
+  rows_kernel<VT, SELL, MIRROR, NA><<<grid_for(rows_kernel<VT, SELL, MIRROR, NA>, b, L.ntiles), WARPS * 32, b, s>>>(L);
+  return cudaGetLastError();
+}
 template <typename VT, bool SELL, bool MIRROR>
 cudaError_t launch_rows_t(const RowLaunch& L, cudaStream_t s) {
-  constexpr int b = RowLayout<VT, SELL>::TOTAL;
-  cudaError_t e = set_smem(rows_kernel<VT, SELL, MIRROR>, b);
-  if (e) return e;
-  rows_kernel<VT, SELL, MIRROR><<<grid_for(rows_kernel<VT, SELL, MIRROR>, b, L.ntiles), WARPS * 32, b, s>>>(L);
-  return cudaGetLastError();
+  return L.xna ? launch_rows_k<VT, SELL, MIRROR, true>(L, s) : launch_rows_k<VT, SELL, MIRROR, false>(L, s);
 }
 template <typename VT, bool SELL>
 cudaError_t launch_rows_m(const RowLaunch& L, cudaStream_t s) {
@@ -1171,18 +1171,22 @@ cudaError_t launch_rows_m(const RowLaunch& L, cudaStream_t s) {
 #ifndef MSREP_CB_SMEM_MIN
 #define MSREP_CB_SMEM_MIN (116 * 1024)
 #endif
-template <typename VT>
-cudaError_t launch_cols_t(const ColLaunch& L, cudaStream_t s) {
+template <typename VT, bool NA>
+cudaError_t launch_cols_k(const ColLaunch& L, cudaStream_t s) {
   // at least MSREP_CB_SMEM_MIN: exactly one CTA per SM (two would share an SM while another idles);
   // no more than the layout needs: the rest of the 256 KB is L1, which holds the x-gather misses
   constexpr int b = CBLayout<VT>::TOTAL > MSREP_CB_SMEM_MIN ? CBLayout<VT>::TOTAL : MSREP_CB_SMEM_MIN;
-  cudaError_t e = set_smem(csc_band_kernel<VT>, b);
+  cudaError_t e = set_smem(csc_band_kernel<VT, NA>, b);
   if (e) return e;
   const int units = L.split_items ? L.nunits : L.nb;
   const int g = units < num_sms() ? units : num_sms();
   if (g < 1) return cudaSuccess;
-  csc_band_kernel<VT><<<g, CB_THREADS, b, s>>>(L);
+  csc_band_kernel<VT, NA><<<g, CB_THREADS, b, s>>>(L);
   return cudaGetLastError();
+}
+template <typename VT>
+cudaError_t launch_cols_t(const ColLaunch& L, cudaStream_t s) {
+  return L.xna ? launch_cols_k<VT, true>(L, s) : launch_cols_k<VT, false>(L, s);
 }
 
 }  // namespace
