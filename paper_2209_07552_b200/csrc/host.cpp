@@ -208,6 +208,8 @@ struct Ctx {
   int4* d_cunits = nullptr;
   int32_t* d_item_hst = nullptr;
   int32_t* d_item_hw = nullptr;
+  int32_t* d_item_sst = nullptr;
+  int32_t* d_item_sg = nullptr;
   int64_t cunits = 0;
   int nheads_local = 0;
 
@@ -527,6 +529,8 @@ struct CscBands {
   std::vector<int4> units;                // split mode: {band, first stage, end stage, 0} (band stage order)
   std::vector<int32_t> item_hst;          // [items]: stages that may hold same-row groups
   std::vector<int32_t> item_hw;           // [items * CB_W]: same-row groups leading each warp list
+  std::vector<int32_t> item_sst;          // [items]: first stage that may hold segmented groups
+  std::vector<int32_t> item_sg;           // [items * CB_W]: first segmented group of each warp list
   std::vector<int4> items;                // {band, nstages, window col base, last-stage seg}
   std::vector<int64_t> item_off;          // byte offset of each item's blob
   std::vector<int32_t> band_item;         // [nb + 1]
@@ -542,8 +546,13 @@ struct CscBands {
 // `pend` for a later group, and a group that cannot be filled while entries
 // remain is closed with holes.  emit(pos, e) receives every output position
 // with its entry (e < 0: hole).  Returns the arranged length.
+#ifndef MSREP_SEG_RATIO
+#define MSREP_SEG_RATIO 3
+#endif
+constexpr int64_t SEG_RATIO = MSREP_SEG_RATIO;   // segmented tail iff greedy groups >= SEG_RATIO x segmented groups
 struct ArrangeScratch {
   int64_t same = 0;   // entries the last arrange_list placed in same-row groups
+  int64_t seg_from = INT64_MAX;   // list position (a multiple of 32) where its segmented groups start
   std::vector<int64_t> pend, rest;
   std::vector<int> rows;
   std::vector<uint64_t> used;
@@ -606,7 +615,12 @@ int64_t arrange_list(const uint32_t* pk, int64_t n, ArrangeScratch& A, Emit&& em
     A.same = (int64_t)heavy.size();
     for (int r : order) A.taken[(size_t)r] = 0;
   }
-  // 2. greedy distinct-row groups over the remaining entries
+  // 2. greedy distinct-row groups over the remaining entries.  When a group cannot be filled with
+  // distinct rows while entries remain (the rest sits on fewer than 32 rows), the group is closed
+  // with holes and everything left is emitted as SEGMENTED groups: sorted by row (list order
+  // within a row), so each group's rows form contiguous runs that the kernel reduces with one
+  // warp segmented scan -- no more holes, still no atomics.
+  A.seg_from = INT64_MAX;
   A.pend.clear();
   if (A.used.size() != (size_t)(CB_ROWS / 64)) A.used.assign(CB_ROWS / 64, 0);   // cleared per group
   int64_t next = 0;
@@ -632,9 +646,30 @@ int64_t arrange_list(const uint32_t* pk, int64_t n, ArrangeScratch& A, Emit&& em
       if (busy(e)) A.pend.push_back(e); else take(e);
     }
     const int real = g;
-    if (g < 32 && (next < nr || !A.pend.empty()))   // close the group with holes
+    const bool stuck = g < 32 && (next < nr || !A.pend.empty());
+    if (stuck)   // close the group with holes
       for (; g < 32; g++) emit(w++, -1);
     for (int k = 0; k < real; k++) A.used[grp[k] >> 6] &= ~(1ull << (grp[k] & 63));
+    if (stuck && A.seg_from == INT64_MAX) {
+      // the greedy pass needs about max-entries-per-row more groups for what is left (one entry
+      // of a row per group); segmented groups need ceil(left / 32) but cost several distinct
+      // groups each (a 5-step shuffle scan): switch only when that wins clearly
+      std::vector<int64_t> left(A.pend.begin(), A.pend.end());
+      for (int64_t q = next; q < nr; q++) left.push_back(A.rest[(size_t)q]);
+      int32_t mx = 0;
+      for (int64_t e : left) mx = std::max(mx, ++A.taken[(size_t)rowof(e)]);
+      for (int64_t e : left) A.taken[(size_t)rowof(e)] = 0;
+      const int64_t seg_groups = ((int64_t)left.size() + 31) / 32;
+      if ((int64_t)mx >= SEG_RATIO * seg_groups + SEG_RATIO) {   // segmented groups for everything left: stable by row
+        next = nr;
+        A.pend.clear();
+        std::stable_sort(left.begin(), left.end(), [&](int64_t a, int64_t b) { return rowof(a) < rowof(b); });
+        A.seg_from = w;
+        for (int64_t e : left) emit(w++, e);
+      } else {
+        A.seg_from = INT64_MAX - 1;   // decided: greedy (with holes) to the end of the list
+      }
+    }
   }
   for (int r : A.rows) A.cnt[(size_t)r] = 0;   // leave the scratch zero
   return w;
@@ -749,12 +784,13 @@ msrep_status_t build_csc_bands(const Ctx& c, const std::vector<int64_t>& lp, con
     next_key = 0;
   };
   // 2. arranged length of every list (holes included)
-  std::vector<int64_t> alen((size_t)keys, 0), asame((size_t)keys, 0);
+  std::vector<int64_t> alen((size_t)keys, 0), asame((size_t)keys, 0), aseg((size_t)keys, INT64_MAX);
   each_key([&](int64_t k, ArrangeScratch& scr) {
     const int64_t b0 = kbeg[(size_t)k], n = kbeg[(size_t)k + 1] - b0;
     scr.same = 0;
     alen[(size_t)k] = n ? arrange_list(tpk.get() + b0, n, scr, [](int64_t, int64_t) {}) : 0;
     asame[(size_t)k] = scr.same;
+    aseg[(size_t)k] = scr.seg_from;
   });
   // 3. items: one per non-empty (band, chunk); stage geometry and blob offsets
   B.band_item.assign((size_t)B.nb + 1, 0);
@@ -772,6 +808,13 @@ msrep_status_t build_csc_bands(const Ctx& c, const std::vector<int64_t>& lp, con
       if (L == 0) continue;
       B.item_hst.push_back((int32_t)((H + CB_SEG - 1) / CB_SEG));
       for (int w = 0; w < CB_W; w++) B.item_hw.push_back((int32_t)(asame[(size_t)(k0 + w)] / 32));
+      int64_t S0 = INT64_MAX;   // first stage that may hold segmented groups; per warp: first group
+      for (int w = 0; w < CB_W; w++) {
+        const int64_t a = aseg[(size_t)(k0 + w)] >= INT64_MAX - 1 ? INT64_MAX : aseg[(size_t)(k0 + w)];
+        S0 = std::min(S0, a == INT64_MAX ? INT64_MAX : a / CB_SEG);
+        B.item_sg.push_back(a == INT64_MAX ? INT32_MAX : (int32_t)(a / 32));
+      }
+      B.item_sst.push_back(S0 == INT64_MAX ? INT32_MAX : (int32_t)S0);
       const int64_t nst = (L + CB_SEG - 1) / CB_SEG;
       const int64_t last = ((L - (nst - 1) * CB_SEG) + 3) & ~(int64_t)3;
       if (nst >= ((int64_t)1 << 20)) return fail(MSREP_ERR_TOO_LARGE, "pCSC warp list too long (>= 2^20 stages)");
@@ -897,7 +940,7 @@ ColLaunch col_launch(const Ctx* c, const void* x, void* y, double alpha, double 
   L.nb = (int)c->cnb; L.blob = c->d_cblob;
   L.x = x; L.xbase = c->wlo;
   L.split_items = c->csplit; L.nunits = (int)c->cunits; L.units = c->d_cunits; L.item_hst = c->d_item_hst;
-  L.item_hw = c->d_item_hw;
+  L.item_hw = c->d_item_hw; L.item_sst = c->d_item_sst; L.item_sg = c->d_item_sg;
   L.fused = c->nranks == 1 && !c->csplit;
   L.out = L.fused ? y : static_cast<void*>(c->d_py);
   L.m = c->m; L.alpha = alpha; L.beta = beta; L.dtype = c->dtype == MSREP_F64 ? 0 : 1;
@@ -1295,6 +1338,8 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     TRY(upload_vec(c, CB.units, &c->d_cunits, s));
     TRY(upload_vec(c, CB.item_hst, &c->d_item_hst, s));
     TRY(upload_vec(c, CB.item_hw, &c->d_item_hw, s));
+    TRY(upload_vec(c, CB.item_sst, &c->d_item_sst, s));
+    TRY(upload_vec(c, CB.item_sg, &c->d_item_sg, s));
     c->cunits = (int64_t)CB.units.size();
     TRY(upload_vec(c, CB.item_off, &c->d_item_off, s));
     TRY(upload_vec(c, CB.band_item, &c->d_band_item, s));

@@ -144,6 +144,8 @@ struct ColLaunch {
   const int4* units;
   const int32_t* item_hst;    // [items]: stages [0, item_hst[i]) may hold same-row groups
   const int32_t* item_hw;     // [items * CB_W]: same-row groups leading warp w's list of item i
+  const int32_t* item_sst;    // [items]: stages [item_sst[i], ...) may hold segmented groups
+  const int32_t* item_sg;     // [items * CB_W]: first segmented group (list step) of warp w's list
   int xna;                    // x gathers with L1::no_allocate
 };
 

@@ -710,7 +710,7 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 // one consumer warp's share of a stage, in registers
 template <typename VT>
 struct CBStage {
-  int4 d;                 // {band (-1: end), seg | stage << 11, window col base, last | same-row << 1 | item << 2}
+  int4 d;                 // {band (-1: end), seg | stage << 11, window col base, last | same-row << 1 | segmented << 2 | item << 3}
   uint32_t pk[CB_PER];
   VT v[CB_PER], xv[CB_PER];
 };
@@ -781,13 +781,14 @@ __global__ void __launch_bounds__(CB_THREADS, 1) csc_band_kernel(const ColLaunch
           for (int i = i0; i < i1 && g < un.z; i++) {
             const int4 item = P.items[i];
             if (g + item.y <= un.y) { g += item.y; continue; }
-            const int hst = P.item_hst[i];
+            const int hst = P.item_hst[i], sst = P.item_sst[i];
             const int s0 = un.y > g ? un.y - g : 0, s1 = min(item.y, un.z - g);
             const char* src = P.blob + P.item_off[i] + (int64_t)s0 * CB_W * CB_SEG * (V + 4);
             for (int sg = s0; sg < s1; sg++) {
               const int seg = sg == item.y - 1 ? item.w : CB_SEG;
               const int bytes = CB_W * seg * (V + 4);
-              stage(make_int4(b, seg | (sg << 11), item.z, (g + sg == un.z - 1 ? 1 : 0) | (sg < hst ? 2 : 0) | (i << 2)),
+              stage(make_int4(b, seg | (sg << 11), item.z,
+                              (g + sg == un.z - 1 ? 1 : 0) | (sg < hst ? 2 : 0) | (sg >= sst ? 4 : 0) | (i << 3)),
                     src, bytes);
               src += bytes;
             }
@@ -806,12 +807,13 @@ __global__ void __launch_bounds__(CB_THREADS, 1) csc_band_kernel(const ColLaunch
         for (int i = i0; i < i1; i++) {
           const int4 item = P.items[i];
           const char* src = P.blob + P.item_off[i];
-          const int hst = P.item_hst[i];
+          const int hst = P.item_hst[i], sst = P.item_sst[i];
           for (int sg = 0; sg < item.y; sg++) {
             const int seg = sg == item.y - 1 ? item.w : CB_SEG;
             const int bytes = CB_W * seg * (V + 4);
             stage(make_int4(b, seg | (sg << 11), item.z,
-                            ((i == i1 - 1 && sg == item.y - 1) ? 1 : 0) | (sg < hst ? 2 : 0) | (i << 2)), src, bytes);
+                            ((i == i1 - 1 && sg == item.y - 1) ? 1 : 0) | (sg < hst ? 2 : 0) | (sg >= sst ? 4 : 0) |
+                                (i << 3)), src, bytes);
             src += bytes;
           }
         }
@@ -832,9 +834,12 @@ __global__ void __launch_bounds__(CB_THREADS, 1) csc_band_kernel(const ColLaunch
   while (A.d.x >= 0) {
     cb_load<VT, NA>(B, it++, smem, sdesc, full, empty, x, xpol, warp, lane);   // next stage's gathers fly during A's scatter
     // the scatter: 32 distinct rows per step, steps in list order (deterministic)
-    if (A.d.w & 2) {   // this stage may hold SAME-ROW groups (heavy rows; placed first in each list)
-      const int hw = P.item_hw[(A.d.w >> 2) * CB_W + warp];   // same-row groups leading this warp's list
-      const int j0 = (A.d.y >> 11) * CB_PER;                   // list step of k = 0
+    if (A.d.w & 6) {   // this stage may hold SAME-ROW groups (heavy rows; first in each list) or
+                       // SEGMENTED groups (row-sorted runs; last in each list)
+      const int item = A.d.w >> 3;
+      const int hw = (A.d.w & 2) ? P.item_hw[item * CB_W + warp] : 0;         // same-row groups leading the list
+      const int sgw = (A.d.w & 4) ? P.item_sg[item * CB_W + warp] : INT_MAX;  // first segmented group
+      const int j0 = (A.d.y >> 11) * CB_PER;                                  // list step of k = 0
 #pragma unroll
       for (int k = 0; k < CB_PER; k++) {
         if (j0 + k < hw) {   // 32 entries of one heavy row: one warp-reduced update
@@ -843,6 +848,19 @@ __global__ void __launch_bounds__(CB_THREADS, 1) csc_band_kernel(const ColLaunch
           for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(FULL, t, off);
           if (lane == 0) acc[A.pk[k] & (CB_ROWS - 1)] += t;
           __syncwarp();   // visible to the next step's lanes
+        } else if (j0 + k >= sgw) {   // rows in contiguous runs: inclusive segmented scan, run ends update
+          const bool real = A.pk[k] != CB_HOLE;
+          const int key = real ? (int)(A.pk[k] & (CB_ROWS - 1)) : -1 - lane;   // holes: own runs
+          double t = real ? (double)A.v[k] * (double)A.xv[k] : 0.0;
+#pragma unroll
+          for (int off = 1; off < 32; off <<= 1) {
+            const int k2 = __shfl_up_sync(FULL, key, off);
+            const double t2 = __shfl_up_sync(FULL, t, off);
+            if (lane >= off && k2 == key) t += t2;
+          }
+          const int kn = __shfl_down_sync(FULL, key, 1);
+          if (real && (lane == 31 || kn != key)) acc[key] += t;
+          __syncwarp();
         } else if (A.pk[k] != CB_HOLE) {
           double* a = acc + (A.pk[k] & (CB_ROWS - 1));
           *a = fma((double)A.v[k], (double)A.xv[k], *a);

@@ -382,6 +382,31 @@ def test_csc_heavy_rows_same_row_groups(fmt):
     check(D, fmt, xd, np.zeros(3), 1.0, 0.0, parts=2, exact=True)
 
 
+@pytest.mark.parametrize("fmt", ["csc", "coo_col"])
+def test_csc_segmented_groups_few_rows(fmt):
+    """Warp lists whose entries sit on fewer than 32 rows (40 rows of 700 entries in one band,
+    plus sparse light rows): after the same-row groups the greedy distinct-row pass gets stuck and
+    the rest of the list becomes row-sorted SEGMENTED groups (one warp segmented scan each) --
+    bit-exact on integer data, fp32 within tolerance, 1 and 2 parts."""
+    rng = np.random.default_rng(131)
+    m, n = 8192, 200_000
+    heavy = set(range(0, m, m // 40))
+    ptr = [0]; idx = []
+    for r in range(m):
+        k = 700 if r in heavy else int(rng.integers(0, 3))
+        idx.append(np.sort(rng.choice(n, k, replace=False)))
+        ptr.append(ptr[-1] + k)
+    idx = np.concatenate(idx).astype(np.int32)
+    A = gen.Sparse(fmt="csr", m=m, n=n, ptr=np.array(ptr, np.int64), idx=idx,
+                   val=rng.integers(-4, 5, idx.size).astype(np.float64))
+    x = gen.vector(n, 132, kind=gen.SMALLINT); y = gen.vector(m, 133, kind=gen.SMALLINT)
+    for parts in (1, 2):
+        check(A, fmt, x, y, 1.5, 0.5, parts=parts, exact=True)
+    B = to_dtype(A, np.float32)
+    xb = gen.vector(n, 134, dtype=np.float32); yb = gen.vector(m, 135, dtype=np.float32)
+    check(B, fmt, xb, yb, 1.5, 0.5, parts=1)
+
+
 # ------------------------------------------------------------ CG (NEXT f4)
 def _spd_stencil(N, diag=30.0, kind=None):
     A = gen.stencil27(N, kind=gen.ONES)
