@@ -173,6 +173,9 @@ __device__ __forceinline__ void issue_blob(const char* blob, int4 d, int kind, i
 //         warp segmented scan, y = alpha*s + beta*y is written coalesced.
 //   slab: partial sum of a piece of one split row -> rec[w] (natural order,
 //         fixed shuffle tree: bit-reproducible).
+#ifndef MSREP_ROW_MINB_F32
+#define MSREP_ROW_MINB_F32 2
+#endif
 #ifndef MSREP_ROW_MINB
 #define MSREP_ROW_MINB 2
 #endif
@@ -235,7 +238,8 @@ __device__ __forceinline__ void sell_tile(const RowLaunch& P, const int4 d, cons
 }
 
 template <typename VT, bool SELL, bool MIRROR, bool NA>
-__global__ void __launch_bounds__(WARPS * 32, MSREP_ROW_MINB) rows_kernel(const RowLaunch P) {
+__global__ void __launch_bounds__(WARPS * 32, sizeof(VT) == 4 ? MSREP_ROW_MINB_F32 : MSREP_ROW_MINB)
+    rows_kernel(const RowLaunch P) {
   using Lay = RowLayout<VT, SELL>;
   constexpr int QMAX = qmax<VT>();
   constexpr int V = (int)sizeof(VT);
