@@ -229,6 +229,7 @@ struct Ctx {
   // MSREP_RESIDENT_HOST: the device layout parked in pinned host memory, streamed per call
   // in chunks (row formats: tile ranges; pCSC: band ranges) through two staging buffers
   int xna = 0;                      // x-gather L1 policy of the partition (1: L1::no_allocate)
+  bool split_launch = false;        // SELL tiles and SEG tiles run as two launches (each >= 5-10 % of nnz)
   int residency = MSREP_RESIDENT_DEVICE;
   int64_t chunk_bytes = (int64_t)256 << 20;
   struct Chunk { int32_t t0, t1, u0, u1; int64_t off, bytes; bool has_sell; };
@@ -309,6 +310,7 @@ void free_all(Ctx* c) {
   c->h_bytes = 0;
   c->chunks.clear();
   c->d_stage[0] = c->d_stage[1] = nullptr;
+  c->split_launch = false;
   c->ready = false;
   c->d_hx = c->d_hy = nullptr;
   c->d_cg_r = c->d_cg_p = c->d_cg_ap = nullptr;
@@ -462,7 +464,7 @@ void rank_segments(msrep_format fmt, int64_t m, int nranks, int vparts, const st
 // [R_j, R_{j+1}) packed into row-aligned tiles (rows longer than a tile become
 // slab-split rows), and the tail row (owned, continues into later parts) as
 // slabs whose fix-up adds the head partials of the parts that continue it.
-void build_row_schedule(const Ctx& c, const std::vector<int64_t>& lp, Schedule& S) {
+void build_row_schedule(const Ctx& c, const std::vector<int64_t>& lp, Schedule& S, bool allow_sell = true) {
   Packer pk(S, c.wlo, lp, (int)vsz(c.dtype));
   const auto& P = c.parts;
   for (int j = c.P0; j < c.P1; j++) {
@@ -496,7 +498,7 @@ void build_row_schedule(const Ctx& c, const std::vector<int64_t>& lp, Schedule& 
       }
     };
     for (int64_t r = d.owned_begin; r < rend;) {
-      if (c.fmt == MSREP_CSR) {
+      if (allow_sell) {   // SELL tiles for regular rows: pCSR, and pCOO too (window pointer uploaded for packing)
         const int64_t e = pk.try_sell(r, rend);
         if (e > r) { r = e; continue; }
       }
@@ -948,6 +950,22 @@ ColLaunch col_launch(const Ctx* c, const void* x, void* y, double alpha, double 
   return L;
 }
 
+// The device-resident tile walk: one launch, or (split_launch) the SELL tiles [0, nsell) with the
+// SELL instantiation and the SEG / slab tiles with the SEG one (k = 1: SpMV, else SpMM).
+msrep_status_t launch_row_tiles(const Ctx* c, const RowLaunch& L, int k, cudaStream_t s) {
+  auto run = [&](const RowLaunch& X) { return k == 1 ? launch_rows(X, s) : launch_rows_mm(X, k, s); };
+  if (!c->split_launch) {
+    CUDA_TRY(run(L));
+    return MSREP_OK;
+  }
+  RowLaunch a = L, b = L;
+  a.ntiles = c->nsell;
+  b.tiles = L.tiles + c->nsell; b.ntiles = L.ntiles - c->nsell; b.has_sell = 0;
+  CUDA_TRY(run(a));
+  CUDA_TRY(run(b));
+  return MSREP_OK;
+}
+
 // x-gather L1 policy.  Whether the L1 should allocate the x lines depends on the matrix: gathers
 // that neighbouring rows / warps of an SM re-hit (stencil pCOO, banded, block-diagonal, short-wide
 // pCSC) want it; gathers with no reuse inside an SM (R-MAT, uniform random) are 5-6 % faster with
@@ -977,7 +995,7 @@ msrep_status_t tune_xload(Ctx* c, cudaStream_t s, int64_t nz_r) {
     for (int it = 0; it < 4; it++) {
       if (it == 1) CUDA_TRY(cudaEventRecord(e0, s));
       if (colwise(c->fmt)) CUDA_TRY(launch_cols(col_launch(c, dx, dy, 1.0, 0.0), s));
-      else CUDA_TRY(launch_rows(row_launch(c, dx, dy, 1.0, 0.0), s));
+      else TRY(launch_row_tiles(c, row_launch(c, dx, dy, 1.0, 0.0), 1, s));
     }
     CUDA_TRY(cudaEventRecord(e1, s));
     CUDA_TRY(cudaEventSynchronize(e1));
@@ -1392,6 +1410,23 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     // ---- schedule
     Schedule S;
     build_row_schedule(*c, lp, S);
+    {
+      // A few SELL tiles among many SEG tiles cost more than they save: their presence selects
+      // the SELL instantiation of rows_kernel for the whole launch, whose SEG path ran 2.5x
+      // slower on an R-MAT part with 1 SELL tile in 195K (profiles/r1_scaling_projection.jsonl,
+      // tools/dbg_part.py).  Keep SELL tiles only if they hold >= 10 % of the rank's nonzeros.
+      int64_t sell_nz = 0;
+      for (const TileHost& t : S.sell)
+        sell_nz += lp[(size_t)t.row0 + (size_t)(t.packed & 0xffff)] - lp[(size_t)t.row0];
+      if (!S.sell.empty() && sell_nz * 10 < nz_r) {
+        S = Schedule{};
+        build_row_schedule(*c, lp, S, false);
+        sell_nz = 0;
+      }
+      // ... and when SEG tiles hold a real share too, they get their own launch of the SEG
+      // instantiation instead of riding in the SELL one
+      c->split_launch = !S.sell.empty() && (nz_r - sell_nz) * 20 >= nz_r;
+    }
     lap(2);
     c->ntiles = (int)(S.tiles.size() + S.sell.size());
     c->nsell = (int)S.sell.size();
@@ -1428,7 +1463,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
       while (t < nt) {
         Group g{(int32_t)t, (int32_t)t, INT64_MAX, 0};
         const int64_t off0 = (int64_t)blob16[t] * 16;
-        while (t < nt && (t == (size_t)g.t0 || tile_end(t) - off0 <= cap)) {
+        while (t < nt && (t == (size_t)g.t0 || (tile_end(t) - off0 <= cap && t != S.sell.size()))) {
           int64_t z0, z1;
           zspan(S.tiles[t], z0, z1);
           g.z0 = std::min(g.z0, z0);
@@ -1457,10 +1492,15 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
       TRY(dalloc(c, (size_t)span * 4, &ip, s));
       d_idx = static_cast<int32_t*>(ip);
     }
+    int32_t* d_lp = nullptr;   // window-local pointer for SELL packing
     if (fmt == MSREP_COO) {
       void* ap;
       TRY(dalloc(c, (size_t)span * 4, &ap, s));
       d_crow = static_cast<int32_t*>(ap);
+      if (c->nsell) {   // the COO local pointer was counted on the host (plan phase)
+        std::vector<int32_t> lp32(lp.begin(), lp.end());
+        TRY(upload_vec(c, lp32, &d_lp, s));
+      }
     } else {
       // upload the global pointer slice and rebase it on the GPU (Sec. 4.1)
       int64_t* d_g;
@@ -1469,6 +1509,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
       TRY(dalloc(c, ((size_t)W + 1) * 4, &ap, s));
       d_aux = static_cast<int32_t*>(ap);
       CUDA_TRY(launch_rebase(d_g, d_aux, W + 1, B_lo, B_hi, s));
+      d_lp = d_aux;
     }
     int4* d_tiles_orig;
     int32_t* d_blob16;
@@ -1500,7 +1541,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
       PackLaunch PL{d_tiles_orig + g.t0, d_blob16 + g.t0, g.t1 - g.t0,
                     static_cast<const char*>(vp) - (size_t)g.z0 * V, d_idx - g.z0,
                     d_crow ? d_crow - g.z0 : d_aux, fmt == MSREP_COO, (int)V, c->wlo,
-                    host_res ? d_pack - off0 : d_pack};
+                    host_res ? d_pack - off0 : d_pack, d_lp};
       CUDA_TRY(launch_pack(PL, s));
       if (host_res)
         CUDA_TRY(cudaMemcpyAsync(c->h_blob + off0, d_pack, (size_t)c->chunks[gi].bytes, cudaMemcpyDeviceToHost, s));
@@ -1593,7 +1634,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   const int64_t nmain = c->chunks.empty() ? 1 : (int64_t)c->chunks.size();   // main-kernel launches
   if (colwise(fmt))
     st.kernels_per_spmv = (c->cnb ? nmain : 0) + ((c->nranks > 1 || c->csplit) ? 1 /*py epilogue*/ : 0) + (c->csplit ? 1 /*memset*/ : 0);
-  else st.kernels_per_spmv = (c->ntiles ? nmain : 0) + (c->nranks > 1 && c->any_flag ? 1 : 0) + (c->nsplit ? 1 : 0);
+  else st.kernels_per_spmv = (c->ntiles ? nmain + (c->split_launch && c->chunks.empty() ? 1 : 0) : 0) + (c->nranks > 1 && c->any_flag ? 1 : 0) + (c->nsplit ? 1 : 0);
   int64_t db = 0;
   for (auto& b : c->bufs) db += (int64_t)b.bytes;
   st.device_bytes = db;
@@ -1703,7 +1744,7 @@ msrep_status_t spmv_impl(msrep_ctx h, const void* alpha_p, const void* x, const 
       return MSREP_OK;
     }));
   } else {
-    CUDA_TRY(launch_rows(L, s));
+    TRY(launch_row_tiles(c, L, 1, s));
   }
   if (pe) CUDA_TRY(cudaEventRecord(pe, s));
   if (c->nranks > 1 && c->any_flag) {
@@ -1773,7 +1814,7 @@ msrep_status_t msrep_spmm(msrep_ctx h, const void* alpha_p, const void* X, const
       return MSREP_OK;
     }));
   } else {
-    CUDA_TRY(launch_rows_mm(L, k, s));
+    TRY(launch_row_tiles(c, L, k, s));
   }
   if (pe) CUDA_TRY(cudaEventRecord(pe, s));
   if (c->nranks > 1 && c->any_flag) {

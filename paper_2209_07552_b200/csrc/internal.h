@@ -85,6 +85,7 @@ struct PackLaunch {        // build the tile blobs from the rank's plain slices 
   const void* val; const int32_t* idx; const int32_t* ptr;    // ptr: window-local pointer (CSR), or COO row ids
   int coo; int vsize; int64_t row_base;                       // COO: global row of window row 0
   char* blob;
+  const int32_t* lptr;                                        // window-local pointer (SELL tiles; CSR: == ptr)
 };
 
 constexpr int MAX_MIRRORS = 8;   // msrep_spmv_mirror: extra y buffers (peer-mapped or local)

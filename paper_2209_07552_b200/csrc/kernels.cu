@@ -944,8 +944,8 @@ __global__ void pack_kernel(const PackLaunch L) {
     int* ix = reinterpret_cast<int*>(vb0 + W * R * 32 * L.vsize);
     for (int k = 0; k < R; k++) {
       const int row = k * 32 + lane;
-      const int rs = row < nrows ? L.ptr[d.x + row] : 0;
-      const int len = row < nrows ? L.ptr[d.x + row + 1] - rs : 0;
+      const int rs = row < nrows ? L.lptr[d.x + row] : 0;
+      const int len = row < nrows ? L.lptr[d.x + row + 1] - rs : 0;
       lens[k * 32 + lane] = (uint16_t)len;
       for (int t = 0; t < W; t++) {
         const bool on = t < len;
@@ -1215,6 +1215,9 @@ cudaError_t launch_cols_t(const ColLaunch& L, cudaStream_t s) {
 
 cudaError_t launch_rows(const RowLaunch& L, cudaStream_t s) {
   if (L.ntiles == 0) return cudaSuccess;
+#ifdef MSREP_FORCE_SELL_INST   // tuning experiment: the SELL instantiation for every launch
+  if (true) return L.dtype == 0 ? launch_rows_m<double, true>(L, s) : launch_rows_m<float, true>(L, s);
+#endif
   if (L.has_sell) return L.dtype == 0 ? launch_rows_m<double, true>(L, s) : launch_rows_m<float, true>(L, s);
   return L.dtype == 0 ? launch_rows_m<double, false>(L, s) : launch_rows_m<float, false>(L, s);
 }

@@ -328,6 +328,33 @@ def test_csc_split_items_short_wide(parts):
     check(B, "csc", xb, yb, 1.5, 0.5, parts=parts)
 
 
+@pytest.mark.parametrize("fmt", ["csr", "coo"])
+def test_sell_and_seg_split_launch(fmt):
+    """Stencil rows (SELL tiles) stacked over R-MAT rows (SEG tiles / slabs), each a real share of
+    the nonzeros: the two tile kinds run as two launches of their own kernel instantiations
+    (kernels_per_spmv counts both) -- bit-exact, 1 and 3 parts, device- and host-resident."""
+    import paper_2209_07552_b200 as M
+    S = gen.stencil27(12, kind=gen.SMALLINT)
+    R = gen.rmat(11, seed=141, kind=gen.SMALLINT)
+    n = max(S["n"], R["n"])
+    A = gen.Sparse(fmt="csr", m=S["m"] + R["m"], n=n,
+                   ptr=np.concatenate([S["ptr"], R["ptr"][1:] + S["ptr"][-1]]).astype(np.int64),
+                   idx=np.concatenate([S["idx"], R["idx"]]).astype(np.int32),
+                   val=np.concatenate([S["val"], R["val"]]))
+    x = gen.vector(n, 142, kind=gen.SMALLINT); y = gen.vector(A["m"], 143, kind=gen.SMALLINT)
+    ref = oracle_ref(A, x, y, 1.5, 0.5)
+    for parts in (1, 3):
+        for kw in ({}, {"residency": "host", "chunk_bytes": 32 << 10}):
+            ctx = M.Context(0, 1, None, 0, parts)
+            got = run_gpu(A, fmt, x, y, 1.5, 0.5, ctx=ctx, **kw)
+            st = ctx.stats()
+            ctx.close()
+            assert np.array_equal(got, ref), (fmt, parts, kw)
+            assert st["nsell"] > 0
+            if not kw:
+                assert st["kernels_per_spmv"] >= 2, st
+
+
 # ------------------------------------------------ Baseline row/column-block split (NEXT f1)
 @pytest.mark.parametrize("fmt", FMTS)
 @pytest.mark.parametrize("parts", [2, 5, 8])
@@ -353,17 +380,19 @@ def test_block_split_bit_exact(fmt, parts):
 
 
 @pytest.mark.parametrize("k", [1, 3, 6, 8, 12, 16, 20])
-def test_sell_rows_per_lane(k):
+@pytest.mark.parametrize("fmt", ["csr", "coo"])
+def test_sell_rows_per_lane(k, fmt):
     """Regular short rows become SELL tiles with R = 4 / 2 / 1 rows per lane (R*W <= 32), incl.
-    ragged last tiles and a sprinkle of empty rows: bit-exact vs the oracle."""
+    ragged last tiles and a sprinkle of empty rows: bit-exact vs the oracle.  pCOO packs its SELL
+    tiles from the window pointer counted on the host."""
     A = gen.kdistinct_csr(32 * 4 * 7 + 45, 5000, k, seed=90 + k, kind=gen.SMALLINT)
     x = gen.vector(A["n"], 91, kind=gen.SMALLINT); y = gen.vector(A["m"], 92, kind=gen.SMALLINT)
     for parts in (1, 3):
-        check(A, "csr", x, y, 1.5, 0.5, parts=parts, exact=True)
+        check(A, fmt, x, y, 1.5, 0.5, parts=parts, exact=True)
     # shorter rows mixed in (padding <= 1/8 may still hold or not): still exact
     B = gen.two_class(32 * 4 * 9, 4000, 9, 4, k, 0.5, kind=gen.SMALLINT)
     xb = gen.vector(B["n"], 93, kind=gen.SMALLINT); yb = gen.vector(B["m"], 94, kind=gen.SMALLINT)
-    check(B, "csr", xb, yb, 2.0, 0.5, parts=2, exact=True)
+    check(B, fmt, xb, yb, 2.0, 0.5, parts=2, exact=True)
 
 
 @pytest.mark.parametrize("fmt", ["csc", "coo_col"])
