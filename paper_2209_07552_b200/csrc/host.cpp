@@ -1463,7 +1463,8 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
       while (t < nt) {
         Group g{(int32_t)t, (int32_t)t, INT64_MAX, 0};
         const int64_t off0 = (int64_t)blob16[t] * 16;
-        while (t < nt && (t == (size_t)g.t0 || (tile_end(t) - off0 <= cap && t != S.sell.size()))) {
+        // host-resident chunks also break where the SELL tiles end (one instantiation per chunk)
+        while (t < nt && (t == (size_t)g.t0 || (tile_end(t) - off0 <= cap && !(host_res && t == S.sell.size())))) {
           int64_t z0, z1;
           zspan(S.tiles[t], z0, z1);
           g.z0 = std::min(g.z0, z0);
