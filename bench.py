@@ -346,6 +346,12 @@ def main():
                          "kernel_avg_ms": kern_avg_ms, "alg_bytes_per_launch": alg_bytes,
                          "peak_kind": peak_kind + " (MEASURED_PEAKS.json hbm_gbs, a copy)" if peak_kind == "measured"
                          else peak_kind},
+            "roofline_gather": {"bound": "x-gather requests", "achieved": A.nnz / (kern_avg_ms * 1e-3) / 1e9,
+                                "peak": 272.0, "unit": "G gathers/s",
+                                "frac": A.nnz / (kern_avg_ms * 1e-3) / 1e9 / 272.0,
+                                "peak_kind": "measured: pure random-gather kernel, L2-resident x (profiles/r1_gatherbench.txt)",
+                                "note": "one x gather per nonzero; binds for random column patterns (R-MAT, tall-skinny); "
+                                        "coalesced patterns merge requests, so frac > 1 means gathers do not bind"},
             "cpu_baseline": cpu,
             "e2e": {"value": flops / (e2e_step_ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": e2e_step_ms,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "api": "msrep_spmv_host"},
