@@ -136,8 +136,45 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def host_info():
+    """Host facts reported beside the oracle's time (SURVEY 8(d) "oracle timing")."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"host_cpus": os.cpu_count(), "cpu_model": model}
+
+
+class pinned_core:
+    """Pin this process to one core while the single-threaded oracle is timed (restored after)."""
+
+    def __enter__(self):
+        self.saved = None
+        try:
+            self.saved = os.sched_getaffinity(0)
+            os.sched_setaffinity(0, {min(self.saved)})
+        except (AttributeError, OSError):
+            self.saved = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.saved is not None:
+            os.sched_setaffinity(0, self.saved)
+
+
 def cpu_baseline(A, seconds):
-    """The oracle as it stands (single-threaded C), timed on the host on a bounded sample."""
+    """The oracle as it stands (single-threaded C), timed on the host on a bounded sample, pinned
+    to one core."""
+    with pinned_core():
+        return _cpu_baseline(A, seconds)
+
+
+def _cpu_baseline(A, seconds):
     import oracle
     t_end = time.perf_counter() + seconds
     x = gen.vector(A["n"], 101, dtype=A["val"].dtype)
@@ -160,7 +197,7 @@ def cpu_baseline(A, seconds):
         if time.perf_counter() >= t_end:
             break
     dt = time.perf_counter() - t0
-    return {"value": flops / dt / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": "oracle",
+    return {"value": flops / dt / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": "oracle", **host_info(),
             "sample": f"{reps} single-threaded oracle SpMVs over 1/{nblk} row blocks of the same matrix "
                       f"({flops / 2:.3g} nonzeros total, {dt:.1f} s)"}
 
@@ -186,20 +223,21 @@ def run_reference(a):
         else:
             oracle.spmv_csc(A["m"], r1 - r0, ptr, A["idx"][z0:z1], A["val"][z0:z1], x[r0:r1], y, ALPHA, BETA)
         return z1 - z0
-    for i in range(a.warmup):
-        step(i)
-    nz, t0 = 0, time.perf_counter()
-    for i in range(a.steps):
-        nz += step(i)
-    dt = time.perf_counter() - t0
+    with pinned_core():
+        for i in range(a.warmup):
+            step(i)
+        nz, t0 = 0, time.perf_counter()
+        for i in range(a.steps):
+            nz += step(i)
+        dt = time.perf_counter() - t0
     v = 2.0 * nz / dt / 1e9
     out = {"metric": METRIC, "value": v, "unit": "GFLOP/s", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
            "ms_per_step": dt * 1e3 / max(1, a.steps), "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": a.dtype, "data": "synthetic", "impl": "reference",
            "config": {"workload": workload_name(a, A), "format": "p" + a.format.upper(),
                       "sample": f"each step = one 1/{nblk} row block of the matrix (~{A.nnz // nblk} nnz)"},
-           "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": 1, "kind": "oracle",
-                            "sample": f"{a.steps} steps, 1/{nblk} row blocks, single-threaded oracle"},
+           "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": 1, "kind": "oracle", **host_info(),
+                            "sample": f"{a.steps} steps, 1/{nblk} row blocks, single-threaded oracle pinned to one core"},
            "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
