@@ -25,6 +25,7 @@
 //               reduce-scatter) fused at band end.
 //  cg_*         the vector kernels of msrep_cg.
 #include <climits>
+#include <mutex>
 #include <cstdint>
 
 #include "internal.h"
@@ -1158,15 +1159,41 @@ int elementwise_grid(int64_t n) {
   return (int)(g < 1 ? 1 : (g > cap ? cap : g));
 }
 
+// Per (kernel, device) launch facts, so a launch does not repeat cudaFuncSetAttribute and the
+// occupancy query (microseconds of host time that show up between back-to-back small SpMVs).
+struct KFacts { const void* fn; int dev, smem, occ; };
+KFacts g_kf[128];
+int g_nkf = 0;
+std::mutex g_kf_mu;
+KFacts* kfacts(const void* fn) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_kf_mu);
+  for (int i = 0; i < g_nkf; i++)
+    if (g_kf[i].fn == fn && g_kf[i].dev == dev) return &g_kf[i];
+  if (g_nkf == 128) g_nkf = 0;   // never reached with the kernels of this file; stay correct anyway
+  g_kf[g_nkf] = {fn, dev, -1, -1};
+  return &g_kf[g_nkf++];
+}
+
 template <typename K>
 cudaError_t set_smem(K kernel, int bytes) {
-  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  KFacts* f = kfacts(reinterpret_cast<const void*>(kernel));
+  if (f->smem == bytes) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) { f->smem = bytes; f->occ = -1; }
+  return e;
 }
 
 template <typename K>
 int grid_for(K kernel, int smem_bytes, int ntiles) {
-  int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, WARPS * 32, smem_bytes);
+  KFacts* f = kfacts(reinterpret_cast<const void*>(kernel));
+  int occ = f->occ;
+  if (occ < 0) {
+    occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, WARPS * 32, smem_bytes);
+    f->occ = occ;
+  }
   if (occ < 1) occ = 1;
   const int64_t want = ((int64_t)ntiles + WARPS - 1) / WARPS;
   const int64_t g = (int64_t)num_sms() * occ;
