@@ -478,6 +478,32 @@ def test_cg_matches_oracle(fmt, parts):
     assert np.max(np.abs(x - xo)) < 1e-9
 
 
+@pytest.mark.parametrize("fmt", ["csr", "csc"])
+def test_cg_graph_matches_eager(fmt, monkeypatch):
+    """msrep_cg replays a captured CUDA graph of two iterations (single rank, device-resident);
+    with even convergence checks it takes the same iterations and the same iterates, bit for
+    bit, as the eager loop (MSREP_CG_GRAPH=0)."""
+    import paper_2209_07552_b200 as M
+    import torch
+    A = _spd_stencil(14)
+    m = A["m"]
+    xs = (np.arange(m) % 5 - 2).astype(np.float64)
+    b = torch.as_tensor(oracle.spmv_csr(m, A["ptr"], A["idx"], A["val"], xs, np.zeros(m), 1.0, 0.0)).cuda()
+    res = []
+    for env in ("1", "0"):
+        monkeypatch.setenv("MSREP_CG_GRAPH", env)
+        B = as_fmt(A, fmt)
+        ctx = M.Context(0, 1, None, 0, 2)
+        ctx.partition(fmt, B["m"], B["n"], ptr=B["ptr"], idx=B["idx"], val=B["val"])
+        xd = torch.zeros(m, dtype=torch.float64, device="cuda")
+        it, rr = ctx.cg(b, xd, tol=1e-11, maxit=300, check_every=4)
+        res.append((it, rr, xd.cpu().numpy()))
+        ctx.close()
+    assert res[0][0] == res[1][0] and res[0][1] == res[1][1], (res[0][:2], res[1][:2])
+    assert np.array_equal(res[0][2], res[1][2])
+    assert np.max(np.abs(res[0][2] - xs)) < 1e-9
+
+
 def test_cg_fp32_storage():
     """fp32 storage (fp64 dot products and scalars): converges to x* to fp32 accuracy."""
     A = _spd_stencil(12)
