@@ -249,6 +249,16 @@ msrep_status_t msrep_exchange_plan(msrep_format fmt, msrep_split split, int64_t 
                                    int nranks, int parts_per_rank, const int64_t* ptr, const int32_t* coo_row,
                                    int64_t* seg_out, int64_t* head_row_out, int32_t* head_part_out);
 
+/* Pure host test hook for the pCSC band layout (DESIGN.md sec. 5 "pCSC"): arranges ONE warp list
+ * the way msrep_partition does.  pk[n]: packed entries in list (CSC) order, row = pk & 8191.
+ * order_out[cap] receives the arranged list: entry index, or -1 for a hole; *len_out its length
+ * (MSREP_ERR_INVALID_ARG if cap is too small); *same_out the number of leading positions in
+ * same-row groups (32 entries of one row each); *seg_from_out the first position of the trailing
+ * segmented groups (rows non-decreasing, list order within a row), or -1 if there are none.
+ * Between them every aligned group of 32 holds distinct rows.  No device, no context. */
+msrep_status_t msrep_debug_arrange(const uint32_t* pk, int64_t n, int64_t* order_out, int64_t cap, int64_t* len_out,
+                                   int64_t* same_out, int64_t* seg_from_out);
+
 /* Sparse matrix times a block of k dense vectors (SpMM), Y <- alpha*A*X + beta*Y:
  * the multi-right-hand-side extension of the same partition (
  * the paper's conclusion on reuse by other sparse kernels).

@@ -80,6 +80,7 @@ _sig = {
     "msrep_plan_split": [I, I, I64, I64, I, P, P, P],
     "msrep_set_split": [P, I],
     "msrep_set_residency": [P, I, I64],
+    "msrep_debug_arrange": [P, I64, P, I64, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)],
     "msrep_cg": [P, P, P, ctypes.c_double, I, I, ctypes.POINTER(I), ctypes.POINTER(ctypes.c_double), P],
     "msrep_spmm": [P, P, P, P, P, I, I, P],
     "msrep_spmv_mirror": [P, P, P, P, P, I, P, P],
@@ -99,7 +100,7 @@ _lib.msrep_version.argtypes = []
 _lib.msrep_version.restype = ctypes.c_int
 
 EXPORTED = ["msrep_get_unique_id", "msrep_create", "msrep_partition", "msrep_spmv", "msrep_spmv_host",
-            "msrep_plan", "msrep_plan_split", "msrep_set_split", "msrep_set_residency", "msrep_cg", "msrep_spmm", "msrep_spmv_mirror", "msrep_plan_groups", "msrep_set_split_groups", "msrep_exchange_plan", "msrep_get_stats", "msrep_destroy", "msrep_last_error", "msrep_version",
+            "msrep_plan", "msrep_plan_split", "msrep_set_split", "msrep_set_residency", "msrep_debug_arrange", "msrep_cg", "msrep_spmm", "msrep_spmv_mirror", "msrep_plan_groups", "msrep_set_split_groups", "msrep_exchange_plan", "msrep_get_stats", "msrep_destroy", "msrep_last_error", "msrep_version",
             "msrep_profile_enable", "msrep_profile_read"]
 
 
@@ -211,6 +212,18 @@ def msrep_set_split(ctx, split):
 
 def msrep_set_residency(ctx, residency, chunk_bytes=0):
     _check(_lib.msrep_set_residency(ctx, residency, int(chunk_bytes)), "msrep_set_residency")
+
+
+def msrep_debug_arrange(pk):
+    """Host test hook: the arranged pCSC warp list of packed entries pk (uint32, row = pk & 8191).
+    Returns (order, same, seg_from): order[i] = entry index or -1 (hole)."""
+    pk = np.ascontiguousarray(pk, np.uint32)
+    cap = 64 * max(1, pk.size) + 64
+    order = np.empty(cap, np.int64)
+    ln, same, seg = I64(), I64(), I64()
+    _check(_lib.msrep_debug_arrange(_ptr(pk), pk.size, _ptr(order), cap, ctypes.byref(ln), ctypes.byref(same),
+                                    ctypes.byref(seg)), "msrep_debug_arrange")
+    return order[:ln.value].copy(), same.value, seg.value
 
 
 def msrep_exchange_plan(fmt, m, n, nnz, nranks, parts_per_rank, ptr=None, coo_row=None, split=SPLIT_NNZ):

@@ -1139,6 +1139,24 @@ msrep_status_t msrep_set_split(msrep_ctx h, msrep_split split) {
   return MSREP_OK;
 }
 
+msrep_status_t msrep_debug_arrange(const uint32_t* pk, int64_t n, int64_t* order_out, int64_t cap, int64_t* len_out,
+                                   int64_t* same_out, int64_t* seg_from_out) {
+  if (n < 0 || (n > 0 && !pk) || !len_out || !same_out || !seg_from_out || (cap > 0 && !order_out))
+    return fail(MSREP_ERR_INVALID_ARG, "bad msrep_debug_arrange arguments");
+  ArrangeScratch A;
+  std::vector<int64_t> out;
+  const int64_t len = n ? arrange_list(pk, n, A, [&](int64_t pos, int64_t e) {
+    if ((int64_t)out.size() <= pos) out.resize((size_t)pos + 1, -1);
+    out[(size_t)pos] = e;
+  }) : 0;
+  if (len > cap) return fail(MSREP_ERR_INVALID_ARG, "cap %lld < arranged length %lld", (long long)cap, (long long)len);
+  for (int64_t i = 0; i < len; i++) order_out[i] = i < (int64_t)out.size() ? out[(size_t)i] : -1;
+  *len_out = len;
+  *same_out = A.same;
+  *seg_from_out = A.seg_from >= INT64_MAX - 1 ? -1 : A.seg_from;
+  return MSREP_OK;
+}
+
 msrep_status_t msrep_set_residency(msrep_ctx h, msrep_residency residency, int64_t chunk_bytes) {
   if (!h) return fail(MSREP_ERR_INVALID_ARG, "ctx is NULL");
   if (residency != MSREP_RESIDENT_DEVICE && residency != MSREP_RESIDENT_HOST)
