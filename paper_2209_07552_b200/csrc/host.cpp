@@ -982,8 +982,11 @@ msrep_status_t tune_xload(Ctx* c, cudaStream_t s, int64_t nz_r) {
   if (c->residency == MSREP_RESIDENT_HOST || nz_r < ((int64_t)1 << 20)) return MSREP_OK;
   const size_t V = vsz(c->dtype), mark = c->bufs.size();
   void *dx, *dy;
-  TRY(dalloc(c, (size_t)std::max<int64_t>(1, c->n) * V, &dx, s));
-  TRY(dalloc(c, (size_t)std::max<int64_t>(1, c->m) * V, &dy, s));
+  if (dalloc(c, (size_t)std::max<int64_t>(1, c->n) * V, &dx, s) != MSREP_OK ||
+      dalloc(c, (size_t)std::max<int64_t>(1, c->m) * V, &dy, s) != MSREP_OK) {
+    release_range(c, mark, c->bufs.size());   // no room for the probe vectors: keep the default policy
+    return MSREP_OK;
+  }
   CUDA_TRY(cudaMemsetAsync(dx, 0, (size_t)std::max<int64_t>(1, c->n) * V, s));
   cudaEvent_t e0, e1;
   CUDA_TRY(cudaEventCreate(&e0));
