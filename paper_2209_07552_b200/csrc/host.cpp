@@ -332,7 +332,13 @@ msrep_status_t h2d(Ctx* c, void* dst, const void* src, size_t bytes, cudaStream_
   }
   if (!c->h_ring[0]) {
     for (int b = 0; b < 2; b++) {
-      CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&c->h_ring[b]), kRingSlot, cudaHostAllocDefault));
+      if (cudaHostAlloc(reinterpret_cast<void**>(&c->h_ring[b]), kRingSlot, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();   // no pinned memory to spare: the driver's pageable path still works
+        if (c->h_ring[0]) cudaFreeHost(c->h_ring[0]);
+        c->h_ring[0] = c->h_ring[1] = nullptr;
+        CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+        return MSREP_OK;
+      }
       CUDA_TRY(cudaEventCreateWithFlags(&c->ring_ev[b], cudaEventDisableTiming));
       CUDA_TRY(cudaEventRecord(c->ring_ev[b], s));
     }
