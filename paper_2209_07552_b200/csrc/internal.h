@@ -54,8 +54,14 @@ constexpr int SELL_R_MAX = 4;
 __host__ __device__ inline int align16(int b) { return (b + 15) & ~15; }
 // rows per lane of a SELL tile of `nrows` rows (1, 2 or 4)
 __host__ __device__ inline int sell_r(int nrows) { return nrows <= 32 ? 1 : (nrows <= 64 ? 2 : 4); }
+// SEG keys: lane l's p-th nonzero has its u8 key at byte (p/4)*128 + 4*l + p%4, so a lane loads 4
+// keys with one 32-bit shared-memory read (a conflict-free 32-lane vector per 4 positions)
+__host__ __device__ inline int seg_key_bytes(int nnz) {
+  const int npos = (nnz >> 5) + ((nnz & 31) ? 1 : 0);
+  return 128 * ((npos + 3) >> 2);
+}
 __host__ __device__ inline int blob_aux_bytes(int kind, int nrows, int nnz) {
-  return kind == KIND_SEG ? align16(nnz) : (kind == KIND_SELL ? align16(sell_r(nrows) * 32 * 2) : 0);
+  return kind == KIND_SEG ? seg_key_bytes(nnz) : (kind == KIND_SELL ? align16(sell_r(nrows) * 32 * 2) : 0);
 }
 // for KIND_SELL, `nnz` is the slice width W
 __host__ __device__ inline int blob_bytes(int kind, int nrows, int nnz, int vsize) {
@@ -73,6 +79,15 @@ __host__ __device__ inline int seg_slot(int e, int nnz) {
   if (e < big) { lane = e / (q + 1); j = e - lane * (q + 1); }
   else { lane = r + (e - big) / q; j = e - (lane * q + r); }
   return j < q ? j * 32 + lane : 32 * q + lane;
+}
+// byte of element e's key in the SEG key block (seg_key_bytes)
+__host__ __device__ inline int seg_key_off(int e, int nnz) {
+  const int q = nnz >> 5, r = nnz & 31;
+  const int big = r * (q + 1);
+  int lane, j;
+  if (e < big) { lane = e / (q + 1); j = e - lane * (q + 1); }
+  else { lane = r + (e - big) / q; j = e - (lane * q + r); }
+  return (j >> 2) * 128 + lane * 4 + (j & 3);   // j == q is the extra position
 }
 
 // int4 tile descriptor: x = first row, window-local; y = blob offset in

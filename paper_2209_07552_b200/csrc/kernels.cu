@@ -321,16 +321,21 @@ __global__ void __launch_bounds__(WARPS * 32, sizeof(VT) == 4 ? MSREP_ROW_MINB_F
       c[QMAX] = 0u;
       v[QMAX] = VT(0);
     } else {
-      const uint8_t* sk = st;
-      const VT* sv = reinterpret_cast<const VT*>(st + align16(nnz));
-      const uint32_t* sc = reinterpret_cast<const uint32_t*>(st + align16(nnz) + align16(nnz * V));
+      const uint32_t* skw = reinterpret_cast<const uint32_t*>(st) + lane;   // keys, 4 per word
+      const VT* sv = reinterpret_cast<const VT*>(st + seg_key_bytes(nnz));
+      const uint32_t* sc = reinterpret_cast<const uint32_t*>(st + seg_key_bytes(nnz) + align16(nnz * V));
+      const int npos = q + (extra ? 1 : 0);
+      static_assert(QMAX % 4 == 0, "the extra key has register word QMAX / 4 to itself");
+#pragma unroll
+      for (int u = 0; u < QMAX / 4; u++) kp[u] = u * 4 < npos ? skw[u * 32] : 0u;
+      if (extra)   // the extra position q moves to register position QMAX (one byte read)
+        kp[QMAX / 4] = (uint32_t)st[(q >> 2) * 128 + lane * 4 + (q & 3)] << (8 * (QMAX & 3));
 #pragma unroll
       for (int j = 0; j <= QMAX; j++) {
         const bool on = j < QMAX ? j < q : extra;
         const int sl = (j < QMAX ? j : q) * 32 + lane;
         c[j] = on ? min(sc[sl], xmax) : 0u;
         v[j] = on ? sv[sl] : VT(0);
-        if (on) kp[j >> 2] |= (uint32_t)sk[sl] << (8 * (j & 3));
       }
     }
     fence_proxy_async();   // order this lane's generic-proxy reads of the slot before the TMA refill
@@ -550,16 +555,21 @@ __global__ void __launch_bounds__(WARPS * 32, MSREP_ROW_MINB) rows_mm_kernel(con
       c[QMAX] = 0u;
       v[QMAX] = VT(0);
     } else {
-      const uint8_t* sk = st;
-      const VT* sv = reinterpret_cast<const VT*>(st + align16(nnz));
-      const uint32_t* sc = reinterpret_cast<const uint32_t*>(st + align16(nnz) + align16(nnz * V));
+      const uint32_t* skw = reinterpret_cast<const uint32_t*>(st) + lane;   // keys, 4 per word
+      const VT* sv = reinterpret_cast<const VT*>(st + seg_key_bytes(nnz));
+      const uint32_t* sc = reinterpret_cast<const uint32_t*>(st + seg_key_bytes(nnz) + align16(nnz * V));
+      const int npos = q + (extra ? 1 : 0);
+      static_assert(QMAX % 4 == 0, "the extra key has register word QMAX / 4 to itself");
+#pragma unroll
+      for (int u = 0; u < QMAX / 4; u++) kp[u] = u * 4 < npos ? skw[u * 32] : 0u;
+      if (extra)   // the extra position q moves to register position QMAX (one byte read)
+        kp[QMAX / 4] = (uint32_t)st[(q >> 2) * 128 + lane * 4 + (q & 3)] << (8 * (QMAX & 3));
 #pragma unroll
       for (int j = 0; j <= QMAX; j++) {
         const bool on = j < QMAX ? j < q : extra;
         const int sl = (j < QMAX ? j : q) * 32 + lane;
         c[j] = on ? min(sc[sl], xmax) : 0u;
         v[j] = on ? sv[sl] : VT(0);
-        if (on) kp[j >> 2] |= (uint32_t)sk[sl] << (8 * (j & 3));
       }
     }
     fence_proxy_async();   // order this lane's generic-proxy reads of the slot before the TMA refill
@@ -971,17 +981,17 @@ __global__ void pack_kernel(const PackLaunch L) {
   }
   // SEG tile: [key u8][val][col] in lane-chunked slot order (internal.h)
   uint8_t* key = reinterpret_cast<uint8_t*>(b);
-  char* vb0 = b + align16(nnz);
+  char* vb0 = b + seg_key_bytes(nnz);
   int* ix = reinterpret_cast<int*>(vb0 + align16(nnz * L.vsize));
   if (L.coo) {
     const int64_t r0 = L.row_base + d.x;
-    for (int e = lane; e < nnz; e += 32) key[seg_slot(e, nnz)] = (uint8_t)(L.ptr[z0 + e] - r0);
+    for (int e = lane; e < nnz; e += 32) key[seg_key_off(e, nnz)] = (uint8_t)(L.ptr[z0 + e] - r0);
   } else {
     for (int j = 0; j < nrows; j++) {
       int e0 = L.ptr[d.x + j], e1 = L.ptr[d.x + j + 1];
       e0 = min(max(e0, z0), z0 + nnz) - z0;
       e1 = min(max(e1, z0), z0 + nnz) - z0;
-      for (int e = e0 + lane; e < e1; e += 32) key[seg_slot(e, nnz)] = (uint8_t)j;
+      for (int e = e0 + lane; e < e1; e += 32) key[seg_key_off(e, nnz)] = (uint8_t)j;
     }
   }
   for (int e = lane; e < nnz; e += 32) {
