@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(WARPS * 32, sizeof(VT) == 4 ? MSREP_ROW_MINB_F
 #pragma unroll
       for (int u = 0; u < QMAX; u++) {
         const bool on = lane + 32 * u < nnz;
-        c[u] = on ? min(sc[lane + 32 * u], xmax) : 0u;
+        c[u] = on ? sc[lane + 32 * u] : 0u;   // range-checked at partition
         v[u] = on ? sv[lane + 32 * u] : VT(0);
       }
       c[QMAX] = 0u;
@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(WARPS * 32, sizeof(VT) == 4 ? MSREP_ROW_MINB_F
       for (int j = 0; j <= QMAX; j++) {
         const bool on = j < QMAX ? j < q : extra;
         const int sl = (j < QMAX ? j : q) * 32 + lane;
-        c[j] = on ? min(sc[sl], xmax) : 0u;
+        c[j] = on ? sc[sl] : 0u;   // range-checked at partition; padding masked
         v[j] = on ? sv[sl] : VT(0);
       }
     }
@@ -549,7 +549,7 @@ __global__ void __launch_bounds__(WARPS * 32, MSREP_ROW_MINB) rows_mm_kernel(con
 #pragma unroll
       for (int u = 0; u < QMAX; u++) {
         const bool on = lane + 32 * u < nnz;
-        c[u] = on ? min(sc[lane + 32 * u], xmax) : 0u;
+        c[u] = on ? sc[lane + 32 * u] : 0u;   // range-checked at partition
         v[u] = on ? sv[lane + 32 * u] : VT(0);
       }
       c[QMAX] = 0u;
@@ -568,7 +568,7 @@ __global__ void __launch_bounds__(WARPS * 32, MSREP_ROW_MINB) rows_mm_kernel(con
       for (int j = 0; j <= QMAX; j++) {
         const bool on = j < QMAX ? j < q : extra;
         const int sl = (j < QMAX ? j : q) * 32 + lane;
-        c[j] = on ? min(sc[sl], xmax) : 0u;
+        c[j] = on ? sc[sl] : 0u;   // range-checked at partition; padding masked
         v[j] = on ? sv[sl] : VT(0);
       }
     }
