@@ -30,8 +30,9 @@ constexpr int WARPS = MSREP_WARPS;   // warps per CTA (each with its own TMA rin
 // Device layout: every tile is one contiguous, 16-byte aligned "blob"; each
 // segment is padded to 16 bytes so one TMA bulk copy moves the tile.
 //
-// SEG tile (pCSR and pCOO irregular rows): [key u8 x nnz][val x nnz][col i32 x nnz]
-//   key = tile-local row of the nonzero.  Lane-chunked order: lane l owns the
+// SEG tile (pCSR and pCOO irregular rows): [keys][val x nnz][col i32 x nnz]
+//   key = tile-local row of the nonzero (u8), 4 per 32-bit word in lane order (seg_key_off:
+//   lane l's p-th key at byte (p/4)*128 + 4l + p%4; seg_key_bytes).  Lane-chunked order: lane l owns the
 //   contiguous nonzeros [b_l, b_l + len_l) of the tile, b_l = l*q + min(l, r),
 //   len_l = q + (l < r), with q = nnz / 32, r = nnz % 32; its j-th nonzero
 //   (j < q) sits in slot j*32 + l and its extra one (j == q, l < r) in slot
