@@ -388,7 +388,9 @@ struct Packer {
   void flush() {
     if (cur_r0 < 0) return;
     const int64_t nrows = cur_r1 - cur_r0, z0 = ls(cur_r0), nz = le(cur_r1 - 1) - z0;
-    S.tiles.push_back({(int32_t)(cur_r0 - wlo), (int32_t)z0, (int32_t)(nrows | (nz << 16)), -1});
+    bool dense = true;   // no empty row: the kernel writes every row's sum, no scratch zeroing
+    for (int64_t r = cur_r0; r < cur_r1 && dense; r++) dense = le(r) > ls(r);
+    S.tiles.push_back({(int32_t)(cur_r0 - wlo), (int32_t)z0, (int32_t)(nrows | (nz << 16)), dense ? KIND_W_SEG_DENSE : -1});
     cur_r0 = cur_r1 = -1;
   }
   void add_row(int64_t r) {

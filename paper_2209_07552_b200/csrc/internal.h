@@ -93,7 +93,8 @@ __host__ __device__ inline int seg_key_off(int e, int nnz) {
 
 // int4 tile descriptor: x = first row, window-local; y = blob offset in
 // 16-byte units; z = nrows | (nnz << 16) (SELL: nrows | (W << 16)); w = kind
-// of work (>= 0: slab record index; -1: SEG tile; -2: SELL).
+// of work (>= 0: slab record index; -1: SEG tile; -4: SEG tile without empty rows; -2: SELL).
+constexpr int KIND_W_SEG_DENSE = -4;
 struct TileHost { int32_t row0, nz0, packed, rec; };
 
 struct PackLaunch {        // build the tile blobs from the rank's plain slices (partition time)

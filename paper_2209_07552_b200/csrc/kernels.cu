@@ -366,8 +366,10 @@ __global__ void __launch_bounds__(WARPS * 32, sizeof(VT) == 4 ? MSREP_ROW_MINB_F
       const bool on = j < QMAX ? j < q : extra;
       xv[j] = on ? ldx<NA>(x + c[j], xpol) : VT(0);
     }
-    for (int rr = lane; rr < nrows; rr += 32) rsum[rr] = 0.0;
-    __syncwarp();
+    if (d.w != KIND_W_SEG_DENSE) {   // rows without entries must read 0 (a dense tile writes every row)
+      for (int rr = lane; rr < nrows; rr += 32) rsum[rr] = 0.0;
+      __syncwarp();
+    }
     // ---- walk the lane's chunk: complete rows inside it go straight to rsum
     const int len = q + (extra ? 1 : 0);
     const int key0 = (int)(q > 0 ? (kp[0] & 0xffu) : (kp[QMAX >> 2] >> (8 * (QMAX & 3))) & 0xffu);
