@@ -166,3 +166,20 @@ def test_two_level_plan_bit_exact_vs_oracle():
         _parts_equal(M.msrep_plan_groups(M.CSR, m, nnz, groups, ptr=ptr), oracle.partition_ptr_b(ptr, b))
         rows = oracle.csr_to_coo(m, ptr)
         _parts_equal(M.msrep_plan_groups(M.COO, m, nnz, groups, coo_row=rows), oracle.partition_coo_b(m, rows, b))
+
+
+def test_plan_bit_exact_vs_oracle_exhaustive_5x5():
+    """The library's binary-search partitioner (msrep_plan, CSR and row-sorted COO) equals the
+    oracle's linear scan on every row-pointer array with m, n <= 5 and np in 1..nnz+2."""
+    import itertools
+    import paper_2209_07552_b200 as M
+    for m in range(1, 6):
+        for lens in itertools.product(range(6), repeat=m):
+            ptr = np.zeros(m + 1, np.int64)
+            ptr[1:] = np.cumsum(lens)
+            nnz = int(ptr[-1])
+            rows = np.repeat(np.arange(m), lens).astype(np.int32)
+            for np_ in range(1, nnz + 3):
+                ref, _, _ = oracle.partition_ptr(ptr, np_)
+                _parts_equal(M.msrep_plan(M.CSR, m, nnz, np_, ptr=ptr), ref)
+                _parts_equal(M.msrep_plan(M.COO, m, nnz, np_, coo_row=rows), ref)

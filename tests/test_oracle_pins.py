@@ -534,3 +534,80 @@ def test_two_level_balance_and_coincidence():
     for g, per in ((2, 4), (3, 2), (2, 3)):
         nnz = g * per * 7
         assert np.array_equal(oracle.two_level_boundaries(nnz, [per] * g), oracle.nnz_boundaries(nnz, g * per))
+
+
+# ------------------------------------------------------------ tolerance scale (oracle item 6)
+def test_row_bound_worked_E(golden_E):
+    """or_row_bound_csr on fixture E with sign-mixed x, negative alpha/beta:
+    hand-worked values (tests/golden/row_bound_E.json).  A dropped fabs, a missing |alpha|, a signed
+    beta term or a beta term read when beta == 0 each changes one of them."""
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "row_bound_E.json")) as f:
+        G = json.load(f)
+    rp, ci, v = E_csr(golden_E)
+    x = np.array(G["x"], np.float64)
+    for case in G["cases"]:
+        y = np.array([float(t) for t in case["y"]], np.float64)
+        got = oracle.row_bound_csr(4, rp, ci, v, x, y, case["alpha"], case["beta"])
+        assert got.tolist() == case["expect"], case
+
+
+def test_row_bound_dense_brute_force():
+    """bound = |alpha| * (|A| @ |x|) + |beta * y| against numpy dense brute force, m, n <= 64 (P3 style).
+    Small-integer data: every partial sum is exact, so the comparison is bit-for-bit; U[-1,1) data
+    within 1e-14 relative."""
+    rng = np.random.default_rng(4242)
+    for trial in range(60):
+        m, n = (int(t) for t in rng.integers(1, 65, 2))
+        r, c, _ = random_matrix(rng, m, n, [0.02, 0.2, 0.6][trial % 3])
+        ints = trial % 2 == 0
+        v = rng.integers(-4, 5, r.size).astype(np.float64) if ints else rng.uniform(-1, 1, r.size)
+        x = rng.integers(-4, 5, n).astype(np.float64) if ints else rng.uniform(-1, 1, n)
+        y = rng.integers(-4, 5, m).astype(np.float64) if ints else rng.uniform(-1, 1, m)
+        A = dense_of(m, n, r, c, v)
+        rp, ci, vv = oracle.coo_to_csr(m, r, c, v)
+        for alpha, beta in [(1.0, 0.0), (-2.0, 0.5), (0.5, -3.0), (0.0, 2.0), (-1.5, -1.0)]:
+            ref = abs(alpha) * (np.abs(A) @ np.abs(x)) + (np.abs(beta * y) if beta != 0.0 else 0.0)
+            got = oracle.row_bound_csr(m, rp, ci, vv, x, y, alpha, beta)
+            if ints:
+                assert np.array_equal(got, ref), (trial, alpha, beta)
+            else:
+                assert np.allclose(got, ref, rtol=1e-14, atol=0.0), (trial, alpha, beta)
+            assert np.all(got >= 0.0)
+
+
+def test_row_bound_fp32_reads_fp32_values():
+    """fp32 data: the bound is taken over the stored fp32 values (converted exactly to fp64)."""
+    rng = np.random.default_rng(7)
+    m, n = 30, 40
+    r, c, v = random_matrix(rng, m, n, 0.3)
+    v32 = v.astype(np.float32)
+    x32 = rng.uniform(-1, 1, n).astype(np.float32)
+    y32 = rng.uniform(-1, 1, m).astype(np.float32)
+    rp, ci, vv = oracle.coo_to_csr(m, r, c, v32)
+    got = oracle.row_bound_csr(m, rp, ci, vv, x32, y32, 1.5, -0.5)
+    A = dense_of(m, n, r, c, v32.astype(np.float64))
+    ref = 1.5 * (np.abs(A) @ np.abs(x32.astype(np.float64))) + np.abs(-0.5 * y32.astype(np.float64))
+    assert np.allclose(got, ref, rtol=1e-14, atol=0.0)
+
+
+def all_row_pointers(max_m=5, max_len=5):
+    """Every row-pointer array of an m x n matrix with m, n <= 5 (the partition depends only on
+    row_ptr, so every row-length vector in {0..5}^m, m = 1..5, covers every structure)."""
+    for m in range(1, max_m + 1):
+        for lens in itertools.product(range(max_len + 1), repeat=m):
+            rp = np.zeros(m + 1, np.int64)
+            rp[1:] = np.cumsum(lens)
+            yield m, rp
+
+
+def test_partition_roundtrip_exhaustive_5x5():
+    """S:253 / S:549: merge(partition) == id and every descriptor invariant, EXHAUSTIVE over all
+    row-length vectors with m, n <= 5 (9330 pointer arrays) and np in 1..nnz+2."""
+    count = 0
+    for m, rp in all_row_pointers():
+        for np_ in range(1, int(rp[-1]) + 3):
+            _check_roundtrip(m, rp, np_)
+            count += 1
+    assert count == sum(6 ** m * (2.5 * m + 2) for m in range(1, 6)) == 130635   # sum of (nnz + 2)
