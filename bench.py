@@ -1,20 +1,26 @@
 #!/usr/bin/env python
 """bench.py -- msRep nnz-balanced SpMV on B200 (driver contract).
 
-One step = one msrep_spmv (y <- alpha*A*x + beta*y, alpha=1.5, beta=0.5) over
-the whole matrix, split nnz-balanced over N GPUs (one process per GPU).
-Default workload: BASELINE.json configs[1], the 2,048,383-row 27-point
-stencil (54,439,939 nnz), pCSR, fp64.  Metric: GFLOP/s (2*nnz per SpMV,
-whole job), with the HBM roofline of the dominant kernel alongside.
+One step = one msrep_spmv (y <- alpha*A*x + beta*y, alpha=1.5, beta=0.5) over the whole matrix,
+split nnz-balanced over N GPUs (one process per GPU).  Default workload: BASELINE.json configs[2],
+the largest single-GPU config -- R-MAT scale 24 (16,777,216 rows, 263,419,028 nnz), pCSR, fp64.
+Metric: GFLOP/s (2*nnz per SpMV, whole job), with the HBM roofline of the dominant kernel.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config stencil|rmat|tallskinny|random1k]
-                  [--format csr|coo|csc] [--dtype f64|f32] [--layout replicated|owned|sharded]
-                  [--impl msrep|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config rmat|stencil|tallskinny|random1k|suite-...]
+                  [--format csr|coo|csc|coo_col] [--dtype f64|f32] [--layout replicated|owned|sharded]
+                  [--impl msrep|reference] [--hot-x -1|0|1] [--xload -1|0|1]
+
+--gpus N without a torchrun environment re-launches itself under torch.distributed.run with N
+ranks (127.0.0.1), and fails with exit code 2 if fewer than N GPUs are visible.  With N > 1
+every rank builds only the rows its nonzero range touches (gen.config_rows; rank 0 broadcasts
+the pointer array) and partitions through msrep_partition_slice.
 """
 import argparse
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -28,15 +34,17 @@ import gen  # noqa: E402
 
 ALPHA, BETA = 1.5, 0.5
 METRIC = "SpMV GFLOP/s and HBM GB/s (% of 8 TB/s) at 1/2/4/8 B200, per format"
+NVLINK_GBPS = 900.0   # NVLink 5, per direction per GPU (nominal)
+T1_CACHE = os.path.join(ROOT, ".bench_cache")
 
 
-def parse():
+def parse(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=2000)
     p.add_argument("--warmup", type=int, default=20)
     p.add_argument("--impl", default="msrep", choices=["msrep", "reference"])
-    p.add_argument("--config", default="stencil",
+    p.add_argument("--config", default="rmat",
                    choices=["stencil", "rmat", "tallskinny", "random1k"] +
                    [f"suite-{s}-{z}" for s in gen.SUITE_SHAPES for z in gen.SUITE_SIZES])
     p.add_argument("--format", default=None, choices=["csr", "coo", "csc", "coo_col"])
@@ -46,12 +54,16 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--parts-per-rank", type=int, default=1)
+    p.add_argument("--hot-x", type=int, default=-1, choices=[-1, 0, 1],
+                   help="MSREP_TUNE_HOT_X: shared-memory hot-x cache (-1 auto, 0 off, 1 on)")
+    p.add_argument("--xload", type=int, default=-1, choices=[-1, 0, 1],
+                   help="MSREP_TUNE_XLOAD: x-gather L1 policy (-1 timed at partition, 0 allocate, 1 no_allocate)")
     p.add_argument("--fused", action="store_true",
                    help="N>1 row formats: fused allgather (msrep_spmv_mirror into the peers' y over NVLink, "
                         "torch symmetric memory) instead of SpMV + NCCL allgatherv")
     p.add_argument("--split", default="nnz", choices=["nnz", "block"],
                    help="nnz: msRep's nnz-balanced split; block: the paper's row/column-block Baseline")
-    a = p.parse_args()
+    a = p.parse_args(argv)
     if a.format is None:
         a.format = "csc" if a.config == "tallskinny" else "csr"
     if a.layout is None:
@@ -68,21 +80,33 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
+def colwise(a):
+    return a.format in ("csc", "coo_col")
+
+
 def build_matrix(a):
     """Synthetic matrix of the named config (gen/, seeded): CSR, or CSC for pCSC."""
     A = gen.make_config(a.config)
-    colwise = a.format in ("csc", "coo_col")
-    if colwise and A["fmt"] == "csr":
+    if colwise(a) and A["fmt"] == "csr":
         A = gen.transpose(A)
-    if not colwise and A["fmt"] == "csc":
+    if not colwise(a) and A["fmt"] == "csc":
         A = gen.transpose(A)
     if a.dtype == "f32":
         A["val"] = A["val"].astype(np.float32)
     return A
 
 
-def workload_name(a, A):
-    return f"{a.config}_{a.format}_{a.dtype}_m{A['m']}_n{A['n']}_nnz{A.nnz}"
+def rank_local_ok(a):
+    """Rank-local generation needs the config's native compressed format (no transpose) and a
+    pointer format (msrep_partition_slice takes CSR / CSC)."""
+    if a.config not in gen.LOCAL_CONFIGS or a.format not in ("csr", "csc"):
+        return False
+    native = "csc" if a.config == "tallskinny" else "csr"
+    return a.format == native
+
+
+def workload_name(a, m, n, nnz):
+    return f"{a.config}_{a.format}_{a.dtype}_m{m}_n{n}_nnz{nnz}"
 
 
 class ClockSampler:
@@ -167,14 +191,14 @@ class pinned_core:
             os.sched_setaffinity(0, self.saved)
 
 
-def cpu_baseline(A, seconds):
+def cpu_baseline(A, seconds, what):
     """The oracle as it stands (single-threaded C), timed on the host on a bounded sample, pinned
     to one core."""
     with pinned_core():
-        return _cpu_baseline(A, seconds)
+        return _cpu_baseline(A, seconds, what)
 
 
-def _cpu_baseline(A, seconds):
+def _cpu_baseline(A, seconds, what):
     import oracle
     t_end = time.perf_counter() + seconds
     x = gen.vector(A["n"], 101, dtype=A["val"].dtype)
@@ -198,7 +222,7 @@ def _cpu_baseline(A, seconds):
             break
     dt = time.perf_counter() - t0
     return {"value": flops / dt / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": "oracle", **host_info(),
-            "sample": f"{reps} single-threaded oracle SpMVs over 1/{nblk} row blocks of the same matrix "
+            "sample": f"{reps} single-threaded oracle SpMVs over 1/{nblk} blocks of {what} "
                       f"({flops / 2:.3g} nonzeros total, {dt:.1f} s)"}
 
 
@@ -213,6 +237,7 @@ def run_reference(a):
     y = gen.vector(A["m"], 102, dtype=A["val"].dtype)
     outer = A["m"] if A["fmt"] == "csr" else A["n"]
     nblk = max(1, int(round(A.nnz / 1_000_000)))    # ~1M nonzeros (~5-10 ms) per step
+
     def step(i):
         b = i % nblk
         r0, r1 = outer * b // nblk, outer * (b + 1) // nblk
@@ -234,7 +259,7 @@ def run_reference(a):
     out = {"metric": METRIC, "value": v, "unit": "GFLOP/s", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
            "ms_per_step": dt * 1e3 / max(1, a.steps), "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": a.dtype, "data": "synthetic", "impl": "reference",
-           "config": {"workload": workload_name(a, A), "format": "p" + a.format.upper(),
+           "config": {"workload": workload_name(a, A["m"], A["n"], A.nnz), "format": "p" + a.format.upper(),
                       "sample": f"each step = one 1/{nblk} row block of the matrix (~{A.nnz // nblk} nnz)"},
            "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": 1, "kind": "oracle", **host_info(),
                             "sample": f"{a.steps} steps, 1/{nblk} row blocks, single-threaded oracle pinned to one core"},
@@ -242,154 +267,294 @@ def run_reference(a):
     print(json.dumps(out), flush=True)
 
 
+def spawn(a):
+    """--gpus N outside torchrun: relaunch under torch.distributed.run with N local ranks."""
+    import torch
+    have = torch.cuda.device_count()
+    if have < a.gpus:
+        print(f"bench.py: --gpus {a.gpus} needs {a.gpus} visible GPUs, found {have}", file=sys.stderr, flush=True)
+        return 2
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def build_local(a, rank, world, ppr, dist, torch, M):
+    """Rank-local matrix: the pointer array (rank 0 builds it and broadcasts it), then only the rows
+    this rank's nonzero range touches.  Returns (fmt, m, n, ptr, r0, r1, idx, val)."""
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if world > 1:
+        head = [None]
+        if rank == 0:
+            fmt, m, n, ptr = gen.config_pointer(a.config)
+            head = [(fmt, m, n, ptr.size)]
+        dist.broadcast_object_list(head, src=0)
+        fmt, m, n, plen = head[0]
+        t = torch.as_tensor(ptr).to(dev) if rank == 0 else torch.empty(plen, dtype=torch.int64, device=dev)
+        dist.broadcast(t, src=0)
+        ptr = t.cpu().numpy()
+        del t
+    else:
+        fmt, m, n, ptr = gen.config_pointer(a.config)
+    outer = n if fmt == "csc" else m
+    nnz = int(ptr[-1])
+    parts = M.msrep_plan_split(M.FORMATS[fmt], M.SPLITS[a.split], outer, nnz, world * ppr, ptr=ptr)
+    mine = parts[rank * ppr:(rank + 1) * ppr]
+    ne = mine[mine["start_row"] >= 0]
+    if ne.size:
+        r0, r1 = int(ne["start_row"][0]), int(ne["end_row"][-1]) + 1
+    else:
+        r0 = r1 = 0
+    idx, val = gen.config_rows(a.config, ptr, r0, r1)
+    if a.dtype == "f32":
+        val = val.astype(np.float32)
+    return fmt, m, n, ptr, r0, r1, idx, val
+
+
+def t1_cache_path(wl):
+    try:
+        st = os.stat(os.path.join(ROOT, "paper_2209_07552_b200", "libmsrep.so"))
+        tag = f"{int(st.st_mtime)}_{st.st_size}"
+    except OSError:
+        tag = "nolib"
+    return os.path.join(T1_CACHE, f"t1_{wl}_{tag}.json")
+
+
+def timed(step, steps, stream, torch):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1)
+
+
 def main():
     a = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if a.impl == "reference":
         run_reference(a)
-        return
+        return 0
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn(a)
+    if world != a.gpus:
+        print(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world}", file=sys.stderr, flush=True)
+        return 2
+    if world > 1:   # NCCL communicator lines (nranks, transport) on stderr, for the record
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     import torch
     import torch.distributed as dist
     import paper_2209_07552_b200 as M
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    A = build_matrix(a)
-    fmt = M.FORMATS[a.format]
-    layout = {"replicated": M.Y_REPLICATED, "owned": M.Y_OWNED, "sharded": M.Y_SHARDED}[a.layout]
+    ppr = a.parts_per_rank
     if world > 1:
-        ctx = M.Context.from_torch_dist(device=local, parts_per_rank=a.parts_per_rank)
+        ctx = M.Context.from_torch_dist(device=local, parts_per_rank=ppr)
     else:
-        ctx = M.Context(0, 1, None, local, a.parts_per_rank)
-    coo = a.format in ("coo", "coo_col")   # COO views carry their sorted major index (rows / columns)
-    coo_row = gen.expand_rows(A) if coo else None
-    ctx.partition(a.format, A["m"], A["n"], ptr=None if coo else A["ptr"], idx=A["idx"], val=A["val"],
-                  coo_row=coo_row, split=a.split)
-    del coo_row
+        ctx = M.Context(0, 1, None, local, ppr)
+    ctx.set_tuning("hot_x", a.hot_x)
+    ctx.set_tuning("xload", a.xload)
+    local_gen = rank_local_ok(a)
+    A = None
+    if local_gen:
+        fmt, m, n, ptr, r0, r1, idx, val = build_local(a, rank, world, ppr, dist, torch, M)
+        nnz = int(ptr[-1])
+        ctx.partition_slice(fmt, m, n, ptr, idx, val, int(ptr[r0]), split=a.split)
+        # rank 0's rows for the CPU baseline (the oracle on the same entries this rank holds)
+        loc = gen.Sparse(fmt=fmt, m=(r1 - r0) if fmt == "csr" else m, n=n if fmt == "csr" else (r1 - r0),
+                         ptr=ptr[r0:r1 + 1] - ptr[r0], idx=idx, val=val)
+        cpu_what = "the whole matrix" if world == 1 else f"rank 0's {r1 - r0} {'rows' if fmt == 'csr' else 'columns'}"
+        del ptr
+    else:
+        A = build_matrix(a)
+        m, n, nnz = A["m"], A["n"], A.nnz
+        coo = a.format in ("coo", "coo_col")   # COO views carry their sorted major index (rows / columns)
+        coo_row = gen.expand_rows(A) if coo else None
+        ctx.partition(a.format, m, n, ptr=None if coo else A["ptr"], idx=A["idx"], val=A["val"],
+                      coo_row=coo_row, split=a.split)
+        del coo_row
+        loc, cpu_what = A, "the whole matrix"
     st = ctx.stats()
-    vdt = A["val"].dtype
+    wl = workload_name(a, m, n, nnz)
+    vdt = np.float32 if a.dtype == "f32" else np.float64
     tdt = torch.float64 if vdt == np.float64 else torch.float32
     V = 8 if vdt == np.float64 else 4
-    x = torch.as_tensor(gen.vector(A["n"], 101, dtype=vdt)).cuda()
-    y0 = torch.as_tensor(gen.vector(A["m"], 102, dtype=vdt)).cuda()
+    x = torch.as_tensor(gen.vector(n, 101, dtype=vdt)).cuda()
+    y0 = torch.as_tensor(gen.vector(m, 102, dtype=vdt)).cuda()
     y = y0.clone()
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
+    lay = {"replicated": M.Y_REPLICATED, "owned": M.Y_OWNED, "sharded": M.Y_SHARDED}
+    layout = lay[a.layout]
     step = lambda: ctx.spmv(ALPHA, x, BETA, y, layout, sh)
     if a.fused and world > 1 and a.format in ("csr", "coo"):
         # y lives in symmetric memory; every rank stores its owned rows into all peers' y from the
         # SpMV epilogue (msrep_spmv_mirror): the allgather overlaps the SpMV tile by tile
         import torch.distributed._symmetric_memory as symm_mem
-        ys = symm_mem.empty(A["m"], dtype=tdt, device=f"cuda:{local}")
+        ys = symm_mem.empty(m, dtype=tdt, device=f"cuda:{local}")
         hdl = symm_mem.rendezvous(ys, dist.group.WORLD)
-        peers = [hdl.get_buffer(r, (A["m"],), tdt) for r in range(world) if r != rank]
+        peers = [hdl.get_buffer(r, (m,), tdt) for r in range(world) if r != rank]
         ys.copy_(y)
         y = ys
         step = lambda: ctx.spmv_mirror(ALPHA, x, BETA, y, peers, sh)
 
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(vals):
+        t = torch.tensor(vals, device="cuda", dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return [float(v) for v in t]
+
     for _ in range(max(3, a.warmup)):
         step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
+    barrier()
     M.msrep_profile_enable(ctx.h, True)
     M.msrep_profile_read(ctx.h, reset=True)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(local)
     with sampler:
-        e0.record(stream)
-        for _ in range(a.steps):
-            step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
+        ms = timed(step, a.steps, stream, torch)
+    barrier()
     kern_ms, kern_n = M.msrep_profile_read(ctx.h, reset=True)
     M.msrep_profile_enable(ctx.h, False)
-    t = torch.tensor([ms, kern_ms / max(1, kern_n)], device="cuda", dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max, kern_avg_ms = float(t[0]), float(t[1])
+    ms_max, kern_avg_ms = max_over_ranks([ms, kern_ms / max(1, kern_n)])
     step_ms = ms_max / a.steps
-    flops = 2.0 * A.nnz
+    flops = 2.0 * nnz
     value = flops / (step_ms * 1e-3) / 1e9
 
+    # N > 1: the other layout of the format timed the same way (OWNED for the row formats,
+    # SHARDED for the column formats: no allgather), merge share and NVLink bytes per rank
+    per_layout = {a.layout: {"ms_per_step": step_ms}}
+    if world > 1 and not a.fused:
+        other = "sharded" if colwise(a) else "owned"
+        if other != a.layout:
+            st2 = lambda: ctx.spmv(ALPHA, x, BETA, y, lay[other], sh)
+            for _ in range(max(3, a.warmup)):
+                st2()
+            barrier()
+            ms2 = max_over_ranks([timed(st2, a.steps, stream, torch)])[0]
+            per_layout[other] = {"ms_per_step": ms2 / a.steps}
+            barrier()
+    for k, d in per_layout.items():
+        d["merge_share"] = max(0.0, 1.0 - kern_avg_ms / d["ms_per_step"])
+        d["gflops"] = flops / (d["ms_per_step"] * 1e-3) / 1e9
+    t1 = None
+    cpath = t1_cache_path(wl)
+    if world == 1 and rank == 0 and ppr == 1 and a.split == "nnz":
+        os.makedirs(T1_CACHE, exist_ok=True)
+        with open(cpath, "w") as f:
+            json.dump({"t1_ms": step_ms, "workload": wl}, f)
+    elif os.path.exists(cpath):
+        with open(cpath) as f:
+            t1 = json.load(f)["t1_ms"]
+    if t1:
+        for d in per_layout.values():
+            d["E_p"] = t1 / (world * d["ms_per_step"])
+    if world > 1:
+        if colwise(a):   # reduce-scatter of the fp64 partial y (ring: (1 - 1/p) of it each way) + allgather
+            shard = -(-m // world)
+            nv_rs = (world - 1) * shard * 8
+            nv_ag = (m - min(shard, m)) * V
+            nv = {"reduce_scatter_bytes": nv_rs, "allgather_bytes": nv_ag}
+            merge_b = nv_rs + (nv_ag if a.layout == "replicated" else 0)
+        else:            # allgatherv of the owned y segments: every other rank's rows come in
+            ag = (m - st["owned_rows"]) * V
+            nv = {"allgatherv_bytes": ag, "head_exchange_bytes": world * ppr * 8}
+            merge_b = ag if a.layout == "replicated" else 0
+        merge_ms = max(1e-6, step_ms - kern_avg_ms)
+        nv["merge_GBps"] = merge_b / (merge_ms * 1e-3) / 1e9
+        nv["frac_of_nvlink"] = nv["merge_GBps"] / NVLINK_GBPS
+        nv["note"] = f"rank {rank}'s ingress per step over the merge time (step - kernel), vs {NVLINK_GBPS:.0f} GB/s"
+    else:
+        nv = None
+
     # e2e through the public host-vector API: H2D x (and y_in), SpMV, D2H y, every step
-    xh = torch.empty(A["n"], dtype=tdt, pin_memory=True)
+    xh = torch.empty(n, dtype=tdt, pin_memory=True)
     xh.copy_(x.cpu())
-    yh = torch.empty(A["m"], dtype=tdt, pin_memory=True)
+    yh = torch.empty(m, dtype=tdt, pin_memory=True)
     yh.copy_(y0.cpu())
-    seg = st["owned_rows"] if a.layout == "owned" else A["m"]
+    seg = st["owned_rows"] if a.layout == "owned" else m
     for _ in range(3):
         ctx.spmv_host(ALPHA, xh.data_ptr(), BETA, yh.data_ptr(), layout, sh)
-    if world > 1:
-        dist.barrier()
+    barrier()
     ke = a.e2e_steps
-    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    f0.record(stream)
-    for _ in range(ke):
-        ctx.spmv_host(ALPHA, xh.data_ptr(), BETA, yh.data_ptr(), layout, sh)
-    f1.record(stream)
-    torch.cuda.synchronize()
-    te = torch.tensor([f0.elapsed_time(f1)], device="cuda", dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_step_ms = float(te[0]) / ke
-    own_in = st["owned_rows"] if world > 1 else A["m"]
-    h2d = A["n"] * V + own_in * V
+    e2e_step_ms = max_over_ranks([timed(lambda: ctx.spmv_host(ALPHA, xh.data_ptr(), BETA, yh.data_ptr(), layout, sh),
+                                        ke, stream, torch)])[0] / ke
+    own_in = st["owned_rows"] if world > 1 else m
+    h2d = n * V + own_in * V
     d2h = seg * V
 
-    # roofline of the dominant kernel (per rank 0's launch; algorithmic bytes / event-timed duration)
+    # roofline of the dominant kernel (rank 0's launch; algorithmic bytes / event-timed duration)
     hbm_peak, peak_kind = load_peaks()
-    kname = "csc_band_kernel" if a.format in ("csc", "coo_col") else "rows_kernel"
+    kname = "csc_band_kernel" if colwise(a) else "rows_kernel"
     traffic = None
     try:   # DRAM bytes per launch of that kernel from a committed `ncu --set full` capture (profiles/)
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            tr = json.load(f).get(workload_name(a, A))
-        if tr and tr.get("kernel") == kname:
+            tr = json.load(f).get(wl)
+        if tr and tr.get("kernel") == kname and (world == 1 or tr.get("n_gpus", 1) == world):
             traffic = tr["dram_bytes_per_launch"]
     except Exception:
         traffic = None
-    alg_bytes = st["alg_bytes"]
-    achieved = alg_bytes / (kern_avg_ms * 1e-3) / 1e9
+    alg_bytes, stream_bytes = st["alg_bytes"], st["stream_bytes"]
+    # pCOO: the 4-B row ids of its algorithmic count are never streamed (the tiles carry u8 keys),
+    # so the roofline counts the smaller of the two (DESIGN.md sec. 8)
+    roof_bytes = min(alg_bytes, stream_bytes) if a.format == "coo" else alg_bytes
+    achieved = roof_bytes / (kern_avg_ms * 1e-3) / 1e9
     step_gbs = alg_bytes / (step_ms * 1e-3) / 1e9
 
     cpu = None
-    if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        cpu = cpu_baseline(A, a.cpu_seconds)
+    if rank == 0 and not a.no_cpu_baseline:
+        cpu = cpu_baseline(loc, a.cpu_seconds, cpu_what)
+    barrier()
     if rank == 0:
         clocks = sampler.summary()
         out = {
             "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": a.dtype, "data": "synthetic (gen/, seeded; no SuiteSparse offline)",
-            "config": {"workload": workload_name(a, A), "format": "p" + a.format.upper(), "layout": a.layout,
-                       "m": A["m"], "n": A["n"], "nnz": A.nnz, "alpha": ALPHA, "beta": BETA,
-                       "parts_per_rank": a.parts_per_rank, "split": a.split,
+            "config": {"workload": wl, "format": "p" + a.format.upper(), "layout": a.layout,
+                       "m": m, "n": n, "nnz": nnz, "alpha": ALPHA, "beta": BETA,
+                       "parts_per_rank": ppr, "split": a.split,
                        "merge": "fused epilogue stores into peer y (msrep_spmv_mirror)" if (a.fused and world > 1)
                                 else "NCCL allgatherv / reduce-scatter",
+                       "matrix_build": "rank-local rows (msrep_partition_slice)" if local_gen else "whole matrix per rank",
                        "l2": "no flush: per-step matrix bytes exceed the 126 MB L2 (inputs larger than L2); "
                              "x stays L2-resident across steps as in an iterative solver",
                        "parallelism": f"nnz-balanced dp{world}"},
-            "hbm": {"alg_bytes_per_step_rank0": alg_bytes, "step_GBps_rank0": step_gbs,
-                    "frac_of_8TBps": step_gbs / 8000.0},
+            "hbm": {"alg_bytes_per_step_rank0": alg_bytes, "stream_bytes_per_step_rank0": stream_bytes,
+                    "step_GBps_rank0": step_gbs, "frac_of_8TBps": step_gbs / 8000.0},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic, "kernel": kname,
                          "kernel_avg_ms": kern_avg_ms, "alg_bytes_per_launch": alg_bytes,
+                         "bytes_counted": "min(alg, stream)" if a.format == "coo" else "alg",
+                         "frac_of_8TBps": achieved / 8000.0,
                          "peak_kind": peak_kind + " (MEASURED_PEAKS.json hbm_gbs, a copy)" if peak_kind == "measured"
                          else peak_kind},
-            "roofline_gather": {"bound": "x-gather requests", "achieved": A.nnz / (kern_avg_ms * 1e-3) / 1e9,
+            "roofline_gather": {"bound": "x-gather requests", "achieved": nnz / world / (kern_avg_ms * 1e-3) / 1e9,
                                 "peak": 272.0, "unit": "G gathers/s",
-                                "frac": A.nnz / (kern_avg_ms * 1e-3) / 1e9 / 272.0,
+                                "frac": nnz / world / (kern_avg_ms * 1e-3) / 1e9 / 272.0,
+                                "hot_x_share": st["hot_nnz"] / max(1, st["nnz_rank"]),
                                 "peak_kind": "measured: pure random-gather kernel, L2-resident x (profiles/r1_gatherbench.txt)",
-                                "note": "one x gather per nonzero; binds for random column patterns (R-MAT, tall-skinny); "
-                                        "coalesced patterns merge requests, so frac > 1 means gathers do not bind"},
+                                "note": "one x gather per nonzero (the hot-x share is served from shared memory); "
+                                        "binds for random column patterns (R-MAT, tall-skinny)"},
+            "layouts": per_layout,
+            "nvlink": nv,
+            "nccl": {"nranks": world, "version": ".".join(map(str, torch.cuda.nccl.version())),
+                     "init_log": "stderr (NCCL_DEBUG=INFO, NCCL_DEBUG_SUBSYS=INIT)"} if world > 1 else None,
             "cpu_baseline": cpu,
             "e2e": {"value": flops / (e2e_step_ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": e2e_step_ms,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "api": "msrep_spmv_host"},
@@ -397,13 +562,15 @@ def main():
             "clocks": clocks,
             "partition_ms": st["partition_ms"],
             "stats_rank0": {k: st[k] for k in ("nnz_rank", "ntiles", "nsell", "nslabs", "nsplit_rows",
-                                               "distinct_cols", "kernels_per_spmv", "tile_bytes", "x_no_allocate")},
+                                               "distinct_cols", "kernels_per_spmv", "tile_bytes", "x_no_allocate",
+                                               "nhot", "hot_nnz")},
         }
         print(json.dumps(out), flush=True)
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

@@ -51,6 +51,9 @@ def lib():
             "gen_kvar_fill": [I64, I64, U64, I, P, P, P],
             "gen_expand_ptr": [I64, P, P],
             "gen_transpose": [I64, I64, P, P, P, P, P, P],
+            "gen_kdistinct_fill_rows": [I64, I64, I64, U64, I, I, I64, I64, P, P, P],
+            "gen_stencil27_fill_rows": [I64, U64, I, I64, I64, P, P, P],
+            "gen_rmat_fill_rows": [I, D, D, D, D, U64, I, I, I64, I64, P, P, P],
         }
         for k, a in sig.items():
             getattr(L, k).argtypes = a
@@ -244,3 +247,55 @@ def suite(name, kind=UNIFORM):
         m = max(1, target // 500)
         return kdistinct_csr(m, 50 * m, 500, seed=seed, kind=kind)
     raise KeyError(name)
+
+
+# ---------------------------------------------------------- rank-local generation
+# A config's pointer array alone (every rank needs it for the plan), then only the rows a rank's
+# nonzero range touches: bench.py with N > 1 never builds the whole matrix on a rank.
+LOCAL_CONFIGS = ("random1k", "stencil", "rmat", "tallskinny")
+
+
+def config_pointer(name):
+    """(fmt, m, n, ptr) of a config without its entries (CSR; CSC for tallskinny)."""
+    if name == "random1k":
+        m, n, k = 1000, 1000, 10
+        return "csr", m, n, np.arange(m + 1, dtype=np.int64) * k
+    if name == "tallskinny":
+        m, n, k = 50_000_000, 1_000_000, 500
+        return "csc", m, n, np.arange(n + 1, dtype=np.int64) * k
+    if name == "stencil":
+        N = 127
+        counts = np.empty(N ** 3, np.int64)
+        lib().gen_stencil27_count(N, _p(counts))
+        m = N ** 3
+    elif name == "rmat":
+        scale = 24
+        m = 1 << scale
+        counts = np.empty(m, np.int64)
+        lib().gen_rmat_count(scale, float(16 * m), 0.57, 0.19, 0.19, 3, 0, _p(counts))
+    else:
+        raise KeyError(name)
+    ptr = np.zeros(m + 1, np.int64)
+    np.cumsum(counts, out=ptr[1:])
+    return "csr", m, m, ptr
+
+
+def config_rows(name, ptr, r0, r1, kind=UNIFORM):
+    """idx, val of rows (CSC: columns) [r0, r1) of a config, nonzeros ptr[r0] .. ptr[r1]."""
+    nz = int(ptr[r1] - ptr[r0])
+    idx = np.empty(max(nz, 1), np.int32)[:nz]
+    val = np.empty(max(nz, 1), np.float64)[:nz]
+    if nz == 0:
+        return idx, val
+    L = lib()
+    if name == "random1k":
+        L.gen_kdistinct_fill_rows(1000, 1000, 10, 1, kind, 0, r0, r1, _p(ptr), _p(idx), _p(val))
+    elif name == "tallskinny":
+        L.gen_kdistinct_fill_rows(1_000_000, 50_000_000, 500, 4, kind, 1, r0, r1, _p(ptr), _p(idx), _p(val))
+    elif name == "stencil":
+        L.gen_stencil27_fill_rows(127, 2, kind, r0, r1, _p(ptr), _p(idx), _p(val))
+    elif name == "rmat":
+        L.gen_rmat_fill_rows(24, float(16 * (1 << 24)), 0.57, 0.19, 0.19, 3, 0, kind, r0, r1, _p(ptr), _p(idx), _p(val))
+    else:
+        raise KeyError(name)
+    return idx, val

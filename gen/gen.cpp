@@ -307,6 +307,49 @@ void gen_expand_ptr(int64_t m, const int64_t* ptr, int32_t* out) {
   parallel_rows(m, [&](int64_t r, std::vector<int64_t>&) { for (int64_t j = ptr[r]; j < ptr[r + 1]; j++) out[j] = (int32_t)r; });
 }
 
+// --- rank-local generation: rows (CSC: columns) [r0, r1) only, written from idx / val = the
+// buffers of nonzeros [ptr[r0], ptr[r1]) -- each row is a pure function of (seed, row), so a rank
+// can build just the rows its nonzero range touches (bench.py with N > 1).
+void gen_kdistinct_fill_rows(int64_t outer, int64_t inner, int64_t k, uint64_t seed, int kind, int transpose,
+                             int64_t r0, int64_t r1, const int64_t* ptr, int32_t* idx, double* val) {
+  (void)outer;
+  const int64_t base = ptr[r0];
+  parallel_rows(r1 - r0, [&](int64_t q, std::vector<int64_t>& s) {
+    const int64_t r = r0 + q;
+    k_distinct(seed, r, inner, k, s);
+    const int64_t o = ptr[r] - base;
+    for (size_t t = 0; t < s.size(); t++) {
+      idx[o + (int64_t)t] = (int32_t)s[t];
+      val[o + (int64_t)t] = transpose ? entry_value(seed, kind, s[t], r) : entry_value(seed, kind, r, s[t]);
+    }
+  });
+}
+void gen_stencil27_fill_rows(int64_t N, uint64_t seed, int kind, int64_t r0, int64_t r1, const int64_t* ptr,
+                             int32_t* idx, double* val) {
+  const int64_t base = ptr[r0];
+  parallel_rows(r1 - r0, [&](int64_t q, std::vector<int64_t>&) {
+    const int64_t r = r0 + q;
+    int64_t i = r / (N * N), j = (r / N) % N, k = r % N, o = ptr[r] - base;
+    for (int di = -1; di <= 1; di++) for (int dj = -1; dj <= 1; dj++) for (int dk = -1; dk <= 1; dk++) {
+      int64_t a = i + di, b = j + dj, c = k + dk;
+      if (a < 0 || a >= N || b < 0 || b >= N || c < 0 || c >= N) continue;
+      int64_t col = (a * N + b) * N + c;
+      idx[o] = (int32_t)col; val[o] = entry_value(seed, kind, r, col); o++;
+    }
+  });
+}
+void gen_rmat_fill_rows(int scale, double edges, double a, double b, double c, uint64_t seed, int permute, int kind,
+                        int64_t r0, int64_t r1, const int64_t* ptr, int32_t* idx, double* val) {
+  Rmat P{scale, edges, a, b, c, seed};
+  const int64_t base = ptr[r0];
+  parallel_rows(r1 - r0, [&](int64_t q, std::vector<int64_t>& s) {
+    const int64_t r = r0 + q;
+    rmat_row_perm(P, permute, r, s);
+    const int64_t o = ptr[r] - base;
+    for (size_t t = 0; t < s.size(); t++) { idx[o + (int64_t)t] = (int32_t)s[t]; val[o + (int64_t)t] = entry_value(seed, kind, r, s[t]); }
+  });
+}
+
 }  // extern "C"
 
 extern "C" {

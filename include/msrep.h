@@ -129,7 +129,12 @@ typedef struct {
   int64_t nchunks;           /* MSREP_RESIDENT_HOST: chunks streamed per SpMV (else 0)       */
   int64_t host_bytes;        /* MSREP_RESIDENT_HOST: pinned bytes streamed H2D per SpMV      */
   int64_t x_no_allocate;     /* x-gather L1 policy picked at partition (1: L1::no_allocate; timed
-                                both ways on the built layout, or forced by MSREP_XLOAD=0|1)  */
+                                both ways on the built layout, or set by MSREP_TUNE_XLOAD)    */
+  int64_t nhot;              /* hot-x cache entries (MSREP_TUNE_HOT_X; 0: no cache)          */
+  int64_t hot_nnz;           /* nonzeros whose x gather the hot cache serves                 */
+  int64_t stream_bytes;      /* bytes the built layout moves per SpMV (beta != 0): tile blobs
+                                as stored + x entries + y; pCOO stores u8 tile row keys, not
+                                the 4-B row ids alg_bytes counts                              */
 } msrep_stats;
 
 /* NCCL unique id for the communicator (rank 0 creates it, the caller
@@ -162,6 +167,18 @@ msrep_status_t msrep_create(msrep_ctx* out, int rank, int nranks, const uint8_t 
 msrep_status_t msrep_partition(msrep_ctx ctx, msrep_format fmt, msrep_dtype dtype, int64_t m, int64_t n,
                                int64_t nnz, const int64_t* ptr, const int32_t* idx, const int32_t* coo_row,
                                const void* val, msrep_part_desc* parts_out, void* stream);
+
+/* The same for a rank that holds only a slice of the entries (each GPU needs only its own
+ * partition): ptr is the full pointer array (CSR row_ptr[m+1] / CSC col_ptr[n+1]; every rank needs
+ * it to plan all np parts), idx_slice / val_slice hold global nonzero positions
+ * [slice_begin, slice_end).  The slice must contain this rank's range [b_{rank*ppr},
+ * b_{(rank+1)*ppr}) under the context's split (msrep_plan / msrep_plan_split tell it in advance),
+ * else MSREP_ERR_INVALID_ARG.  CSR / CSC only (the COO plan reads the row index at every cut).
+ * Otherwise identical to msrep_partition (same layout, same results). */
+msrep_status_t msrep_partition_slice(msrep_ctx ctx, msrep_format fmt, msrep_dtype dtype, int64_t m, int64_t n,
+                                     int64_t nnz, const int64_t* ptr, const int32_t* idx_slice,
+                                     const void* val_slice, int64_t slice_begin, int64_t slice_end,
+                                     msrep_part_desc* parts_out, void* stream);
 
 /* y <- alpha*A*x + beta*y on device memory.  alpha, beta: host
  * scalars of the partition's dtype.  x: device [n], identical on every rank
@@ -211,6 +228,23 @@ msrep_status_t msrep_spmv_host(msrep_ctx ctx, const void* alpha, const void* x_h
  * (unknown residency, chunk_bytes < 0). */
 typedef enum { MSREP_RESIDENT_DEVICE = 0, MSREP_RESIDENT_HOST = 1 } msrep_residency;
 msrep_status_t msrep_set_residency(msrep_ctx ctx, msrep_residency residency, int64_t chunk_bytes);
+
+/* Tuning knobs of a context (explicit API, no environment switches).  Each
+ * knob keeps the arithmetic identical (same bits); only speed changes.
+ *   MSREP_TUNE_XLOAD    x-gather L1 policy of the SpMV kernels, applied by the
+ *                       next msrep_partition: -1 (default) time both policies
+ *                       on the built layout and keep the faster; 0 allocate in
+ *                       L1; 1 ld.global.nc.L1::no_allocate.
+ *   MSREP_TUNE_CG_GRAPH msrep_cg replays a CUDA graph of two iterations where
+ *                       supported: 1 (default) on, 0 eager launches.
+ *   MSREP_TUNE_HOT_X    shared-memory cache of the rank's hottest x entries for
+ *                       the row formats, applied by the next
+ *                       msrep_partition: -1 (default) when the top columns hold
+ *                       enough of the rank's nonzeros, 0 off, 1 on whenever
+ *                       any column qualifies.
+ * Errors: MSREP_ERR_INVALID_ARG (unknown knob or value). */
+typedef enum { MSREP_TUNE_XLOAD = 0, MSREP_TUNE_CG_GRAPH = 1, MSREP_TUNE_HOT_X = 2 } msrep_tuning;
+msrep_status_t msrep_set_tuning(msrep_ctx ctx, msrep_tuning knob, int value);
 
 /* Select the split used by the next msrep_partition on this context (default
  * MSREP_SPLIT_NNZ; NNZ or BLOCK here).  All ranks must select the same split. */

@@ -15,7 +15,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("MSREP_LIB_VARIANT") or os.path.join(_HERE, "libmsrep.so")   # variant: tuning builds
+LIB_PATH = os.path.join(_HERE, "libmsrep.so")   # the in-tree build only (tuning builds: tools/variant.sh)
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libmsrep.so not built at {LIB_PATH}: run `make` (or __graft_entry__.build()) first")
@@ -34,6 +34,8 @@ STATUS = {0: "MSREP_OK", 1: "MSREP_ERR_INVALID_ARG", 2: "MSREP_ERR_DIM_MISMATCH"
           4: "MSREP_ERR_TOO_LARGE", 5: "MSREP_ERR_STATE", 6: "MSREP_ERR_OOM", 7: "MSREP_ERR_CUDA",
           8: "MSREP_ERR_NCCL"}
 FORMATS = {"csr": CSR, "csc": CSC, "coo": COO, "coo_col": COO_COL}
+TUNE_XLOAD, TUNE_CG_GRAPH, TUNE_HOT_X = 0, 1, 2
+TUNING = {"xload": TUNE_XLOAD, "cg_graph": TUNE_CG_GRAPH, "hot_x": TUNE_HOT_X}
 
 
 class PartDesc(ctypes.Structure):
@@ -55,7 +57,8 @@ class Stats(ctypes.Structure):
                                          ("nsell", ctypes.c_int64),
                                          ("phase_ms", ctypes.c_double * 4), ("residency", ctypes.c_int64),
                                          ("nchunks", ctypes.c_int64), ("host_bytes", ctypes.c_int64),
-                                         ("x_no_allocate", ctypes.c_int64)]
+                                         ("x_no_allocate", ctypes.c_int64), ("nhot", ctypes.c_int64),
+                                         ("hot_nnz", ctypes.c_int64), ("stream_bytes", ctypes.c_int64)]
 
 
 class Allocator(ctypes.Structure):
@@ -73,12 +76,14 @@ _sig = {
     "msrep_get_unique_id": [P],
     "msrep_create": [ctypes.POINTER(P), I, I, P, I, I, P],
     "msrep_partition": [P, I, I, I64, I64, I64, P, P, P, P, P, P],
+    "msrep_partition_slice": [P, I, I, I64, I64, I64, P, P, P, I64, I64, P, P],
     "msrep_spmv": [P, P, P, P, P, I, P],
     "msrep_spmv_host": [P, P, P, P, P, I, P],
     "msrep_plan": [I, I64, I64, I, P, P, P],
     "msrep_exchange_plan": [I, I, I64, I64, I64, I, I, P, P, P, P, P],
     "msrep_plan_split": [I, I, I64, I64, I, P, P, P],
     "msrep_set_split": [P, I],
+    "msrep_set_tuning": [P, I, I],
     "msrep_set_residency": [P, I, I64],
     "msrep_debug_arrange": [P, I64, P, I64, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)],
     "msrep_cg": [P, P, P, ctypes.c_double, I, I, ctypes.POINTER(I), ctypes.POINTER(ctypes.c_double), P],
@@ -99,8 +104,8 @@ _lib.msrep_last_error.restype = ctypes.c_char_p
 _lib.msrep_version.argtypes = []
 _lib.msrep_version.restype = ctypes.c_int
 
-EXPORTED = ["msrep_get_unique_id", "msrep_create", "msrep_partition", "msrep_spmv", "msrep_spmv_host",
-            "msrep_plan", "msrep_plan_split", "msrep_set_split", "msrep_set_residency", "msrep_debug_arrange", "msrep_cg", "msrep_spmm", "msrep_spmv_mirror", "msrep_plan_groups", "msrep_set_split_groups", "msrep_exchange_plan", "msrep_get_stats", "msrep_destroy", "msrep_last_error", "msrep_version",
+EXPORTED = ["msrep_get_unique_id", "msrep_create", "msrep_partition", "msrep_partition_slice", "msrep_spmv", "msrep_spmv_host",
+            "msrep_plan", "msrep_plan_split", "msrep_set_split", "msrep_set_tuning", "msrep_set_residency", "msrep_debug_arrange", "msrep_cg", "msrep_spmm", "msrep_spmv_mirror", "msrep_plan_groups", "msrep_set_split_groups", "msrep_exchange_plan", "msrep_get_stats", "msrep_destroy", "msrep_last_error", "msrep_version",
             "msrep_profile_enable", "msrep_profile_read"]
 
 
@@ -117,6 +122,34 @@ def _ptr(a):
     if hasattr(a, "data_ptr"):           # torch tensor
         return a.data_ptr()
     return a.ctypes.data
+
+
+_NP_DTYPE = {F64: np.float64, F32: np.float32}
+
+
+def _check_vec(t, dtype, count, name):
+    """A device vector handed to the library: a CUDA tensor of the partition's dtype, contiguous,
+    with >= count elements (a raw int pointer is passed through unchecked)."""
+    if t is None or isinstance(t, int):
+        return
+    import torch
+    want = torch.float64 if dtype == F64 else torch.float32
+    if not (t.is_cuda and t.is_contiguous() and t.dtype == want and t.numel() >= count):
+        raise ValueError(f"{name}: need a contiguous CUDA {want} tensor with >= {count} elements, got "
+                         f"{t.dtype} {tuple(t.shape)} on {t.device} (contiguous={t.is_contiguous()})")
+
+
+def _check_host_vec(a, dtype, count, name):
+    if a is None or isinstance(a, int):
+        return
+    if hasattr(a, "data_ptr"):   # pinned torch tensor
+        import torch
+        want = torch.float64 if dtype == F64 else torch.float32
+        ok = (not a.is_cuda) and a.is_contiguous() and a.dtype == want and a.numel() >= count
+    else:
+        ok = a.flags["C_CONTIGUOUS"] and a.dtype == _NP_DTYPE[dtype] and a.size >= count
+    if not ok:
+        raise ValueError(f"{name}: need a contiguous host {_NP_DTYPE[dtype].__name__} array with >= {count} elements")
 
 
 # ------------------------------------------------------------ C-ABI mirrors
@@ -208,6 +241,13 @@ def msrep_set_split_groups(ctx, groups):
 
 def msrep_set_split(ctx, split):
     _check(_lib.msrep_set_split(ctx, split), "msrep_set_split")
+
+
+def msrep_set_tuning(ctx, knob, value):
+    """knob: TUNE_XLOAD / TUNE_CG_GRAPH / TUNE_HOT_X (or its TUNING name), value as include/msrep.h."""
+    if isinstance(knob, str):
+        knob = TUNING[knob]
+    _check(_lib.msrep_set_tuning(ctx, int(knob), int(value)), "msrep_set_tuning")
 
 
 def msrep_set_residency(ctx, residency, chunk_bytes=0):
@@ -325,9 +365,18 @@ class Context:
         else:
             msrep_set_split(self.h, SPLITS[split] if isinstance(split, str) else split)
         val = np.ascontiguousarray(val)
-        dtype = F64 if val.dtype == np.float64 else F32
+        if val.dtype == np.float64:
+            dtype = F64
+        elif val.dtype == np.float32:
+            dtype = F32
+        else:
+            raise ValueError(f"val dtype {val.dtype}: the library takes float64 or float32 values")
         idx = np.ascontiguousarray(idx, np.int32)
         nnz = idx.size
+        if val.size != nnz:
+            raise ValueError(f"val has {val.size} entries, idx {nnz}")
+        if coo_row is not None and np.asarray(coo_row).size != nnz:
+            raise ValueError(f"coo_row has {np.asarray(coo_row).size} entries, idx {nnz}")
         if ptr is not None:
             ptr = np.ascontiguousarray(ptr, np.int64)
         if coo_row is not None:
@@ -337,19 +386,56 @@ class Context:
         self.dtype, self.fmt, self.m, self.n, self.nnz = dtype, fmt, m, n, nnz
         return self.parts
 
+    def set_tuning(self, knob, value):
+        msrep_set_tuning(self.h, knob, value)
+
+    def partition_slice(self, fmt, m, n, ptr, idx_slice, val_slice, slice_begin, stream=None, split="nnz"):
+        """CSR / CSC partition from a slice of the entries: idx_slice / val_slice hold global nonzero
+        positions [slice_begin, slice_begin + len) and must cover this rank's range
+        (msrep_partition_slice)."""
+        msrep_set_residency(self.h, RESIDENT_DEVICE, 0)
+        if isinstance(fmt, str):
+            fmt = FORMATS[fmt]
+        msrep_set_split(self.h, SPLITS[split] if isinstance(split, str) else split)
+        val = np.ascontiguousarray(val_slice)
+        if val.dtype not in (np.float64, np.float32):
+            raise ValueError(f"val dtype {val.dtype}: the library takes float64 or float32 values")
+        dtype = F64 if val.dtype == np.float64 else F32
+        idx = np.ascontiguousarray(idx_slice, np.int32)
+        if val.size != idx.size:
+            raise ValueError(f"val slice has {val.size} entries, idx slice {idx.size}")
+        ptr = np.ascontiguousarray(ptr, np.int64)
+        nnz = int(ptr[-1])
+        np_ = self.nranks * self.parts_per_rank
+        parts = np.zeros(np_, PART_DTYPE)
+        _check(_lib.msrep_partition_slice(self.h, fmt, dtype, m, n, nnz, _ptr(ptr), _ptr(idx), _ptr(val),
+                                          int(slice_begin), int(slice_begin) + idx.size, _ptr(parts), stream),
+               "msrep_partition_slice")
+        self.parts = parts
+        self.dtype, self.fmt, self.m, self.n, self.nnz = dtype, fmt, m, n, nnz
+        return parts
+
     def spmv(self, alpha, x, beta, y, layout=Y_REPLICATED, stream=None):
+        _check_vec(x, self.dtype, self.n, "x")
+        _check_vec(y, self.dtype, self.m, "y")
         if stream is None:
             import torch
             stream = torch.cuda.current_stream().cuda_stream
         msrep_spmv(self.h, alpha, x, beta, y, layout, stream, self.dtype)
 
     def spmv_host(self, alpha, x_host, beta, y_host, layout=Y_REPLICATED, stream=None):
+        _check_host_vec(x_host, self.dtype, self.n, "x_host")
+        _check_host_vec(y_host, self.dtype, self.m, "y_host")
         msrep_spmv_host(self.h, alpha, x_host, beta, y_host, layout, stream, self.dtype)
 
     def stats(self):
         return msrep_get_stats(self.h)
 
     def spmv_mirror(self, alpha, x, beta, y, mirrors, stream=None):
+        _check_vec(x, self.dtype, self.n, "x")
+        _check_vec(y, self.dtype, self.m, "y")
+        for i, mm in enumerate(mirrors):
+            _check_vec(mm, self.dtype, self.m, f"mirrors[{i}]")
         if stream is None:
             import torch
             stream = torch.cuda.current_stream().cuda_stream
@@ -357,12 +443,19 @@ class Context:
 
     def spmm(self, alpha, X, beta, Y, layout=Y_REPLICATED, stream=None):
         """X: torch [n, k], Y: torch [m, k] (contiguous, row-major), k in {2, 4, 8}."""
+        k = X.shape[1]
+        _check_vec(X, self.dtype, self.n * k, "X")
+        _check_vec(Y, self.dtype, self.m * k, "Y")
+        if Y.dim() != 2 or Y.shape[1] != k:
+            raise ValueError(f"Y shape {tuple(Y.shape)} does not match X's k = {k}")
         if stream is None:
             import torch
             stream = torch.cuda.current_stream().cuda_stream
         msrep_spmm(self.h, alpha, X, beta, Y, X.shape[1], layout, stream, self.dtype)
 
     def cg(self, b, x, tol=1e-10, maxit=1000, check_every=10, stream=None):
+        _check_vec(b, self.dtype, self.m, "b")   # m != n is the library's MSREP_ERR_DIM_MISMATCH
+        _check_vec(x, self.dtype, self.n, "x")
         if stream is None:
             import torch
             stream = torch.cuda.current_stream().cuda_stream

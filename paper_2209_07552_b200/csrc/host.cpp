@@ -204,8 +204,13 @@ struct Ctx {
   int32_t* d_split = nullptr;
   char* d_cblob = nullptr;
   int64_t cnb = 0, citems = 0;
-  bool csplit = false;
-  int4* d_cunits = nullptr;
+  int4* d_cunits = nullptr;          // units of work (see CscBands)
+  int2* d_bsplit = nullptr;
+  double* d_slots = nullptr;
+  int4* d_tasks = nullptr;
+  int* d_tickets = nullptr;
+  int* d_ctr = nullptr;
+  int64_t ntasks = 0, nslots = 0;
   int32_t* d_item_hst = nullptr;
   int32_t* d_item_hw = nullptr;
   int32_t* d_item_sst = nullptr;
@@ -229,10 +234,13 @@ struct Ctx {
   // MSREP_RESIDENT_HOST: the device layout parked in pinned host memory, streamed per call
   // in chunks (row formats: tile ranges; pCSC: band ranges) through two staging buffers
   int xna = 0;                      // x-gather L1 policy of the partition (1: L1::no_allocate)
+  int32_t* d_hot = nullptr;         // hot-x columns by slot (row formats, device-resident)
+  int nhot = 0;
+  int64_t hot_nnz = 0;              // the rank's nonzeros whose x comes from the hot cache
   bool split_launch = false;        // SELL tiles and SEG tiles run as two launches (each >= 5-10 % of nnz)
   int residency = MSREP_RESIDENT_DEVICE;
   int64_t chunk_bytes = (int64_t)256 << 20;
-  struct Chunk { int32_t t0, t1, u0, u1; int64_t off, bytes; bool has_sell; };
+  struct Chunk { int32_t t0, t1, u0, u1; int64_t off, bytes; bool has_sell; int32_t k0 = 0, k1 = 0; };
   std::vector<Chunk> chunks;
   char* h_blob = nullptr;           // pinned (cudaHostAlloc)
   int64_t h_bytes = 0;
@@ -245,12 +253,17 @@ struct Ctx {
   // into one slot while the DMA drains the other)
   char* h_ring[2] = {nullptr, nullptr};
   cudaEvent_t ring_ev[2] = {nullptr, nullptr};
+  bool ring_disabled = false;       // the pinned ring could not be allocated: pageable copies
 
   // host-vector path buffers
   void* d_hx = nullptr;
   void* d_hy = nullptr;
 
   msrep_stats stats{};
+  // msrep_set_tuning knobs
+  int tune_xload = -1;              // -1 auto, 0 allocate, 1 no_allocate
+  int tune_cg_graph = 1;
+  int tune_hot = -1;                // -1 auto, 0 off, 1 on
 
   // profiling hook: event pairs around the dominant kernel
   bool prof = false;
@@ -314,6 +327,9 @@ void free_all(Ctx* c) {
   c->split_launch = false;
   c->ready = false;
   c->d_hx = c->d_hy = nullptr;
+  c->d_hot = nullptr;
+  c->nhot = 0;
+  c->hot_nnz = 0;
   c->d_cg_r = c->d_cg_p = c->d_cg_ap = nullptr;
   c->d_cg_part = c->d_cg_sc = nullptr;
   c->mm_k = 0;
@@ -330,18 +346,26 @@ msrep_status_t h2d(Ctx* c, void* dst, const void* src, size_t bytes, cudaStream_
     if (bytes) CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
     return MSREP_OK;
   }
-  if (!c->h_ring[0]) {
+  if (!c->h_ring[0] && !c->ring_disabled) {
     for (int b = 0; b < 2; b++) {
       if (cudaHostAlloc(reinterpret_cast<void**>(&c->h_ring[b]), kRingSlot, cudaHostAllocDefault) != cudaSuccess) {
         cudaGetLastError();   // no pinned memory to spare: the driver's pageable path still works
-        if (c->h_ring[0]) cudaFreeHost(c->h_ring[0]);
-        c->h_ring[0] = c->h_ring[1] = nullptr;
-        CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
-        return MSREP_OK;
+        for (int q = 0; q < 2; q++) {
+          if (c->h_ring[q]) cudaFreeHost(c->h_ring[q]);
+          if (c->ring_ev[q]) cudaEventDestroy(c->ring_ev[q]);
+          c->h_ring[q] = nullptr;
+          c->ring_ev[q] = nullptr;
+        }
+        c->ring_disabled = true;   // do not retry the pinned allocation on every later upload
+        break;
       }
       CUDA_TRY(cudaEventCreateWithFlags(&c->ring_ev[b], cudaEventDisableTiming));
       CUDA_TRY(cudaEventRecord(c->ring_ev[b], s));
     }
+  }
+  if (!c->h_ring[0]) {
+    CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+    return MSREP_OK;
   }
   const char* sp = static_cast<const char*>(src);
   char* dp = static_cast<char*>(dst);
@@ -536,8 +560,10 @@ void build_row_schedule(const Ctx& c, const std::vector<int64_t>& lp, Schedule& 
 struct CscBands {
   int64_t nb = 0, nch = 1, bytes = 0;     // bands, column chunks, blob bytes
   int64_t chunk = CB_CHUNK;               // columns per chunk
-  bool split_items = false;               // split mode: stage ranges of items are the units of work
-  std::vector<int4> units;                // split mode: {band, first stage, end stage, 0} (band stage order)
+  std::vector<int4> units;                // {band, first stage, end stage, slot (-1: whole band)}
+  std::vector<int2> bsplit;               // [nb]: {first slot, slots} of a split band, {0, 0} otherwise
+  std::vector<int4> tasks;                // reduction tasks {band, first row, end row, 0} (band order)
+  int64_t nslots = 0;
   std::vector<int32_t> item_hst;          // [items]: stages that may hold same-row groups
   std::vector<int32_t> item_hw;           // [items * CB_W]: same-row groups leading each warp list
   std::vector<int32_t> item_sst;          // [items]: first stage that may hold segmented groups
@@ -560,7 +586,8 @@ struct CscBands {
 #ifndef MSREP_SEG_RATIO
 #define MSREP_SEG_RATIO 3
 #endif
-constexpr int64_t SEG_RATIO = MSREP_SEG_RATIO;   // segmented tail iff greedy groups >= SEG_RATIO x segmented groups
+constexpr int64_t SEG_RATIO = MSREP_SEG_RATIO;
+constexpr int64_t CB_TASK_ROWS = 512;   // rows of a split band per reduction task   // segmented tail iff greedy groups >= SEG_RATIO x segmented groups
 struct ArrangeScratch {
   int64_t same = 0;   // entries the last arrange_list placed in same-row groups
   int64_t seg_from = INT64_MAX;   // list position (a multiple of 32) where its segmented groups start
@@ -837,24 +864,32 @@ msrep_status_t build_csc_bands(const Ctx& c, const std::vector<int64_t>& lp, con
   }
   B.band_item[(size_t)B.nb] = (int32_t)B.items.size();
   B.bytes = bytes;
-  // split mode: few bands, or a band much heavier than one SM's share -> units = stage ranges
+  // Units of work (fetched dynamically by the CTAs, largest first): a whole band, or -- for a band
+  // heavier than `per` stages (R-MAT's first bands, short-wide matrices with fewer bands than SMs)
+  // -- equal stage ranges of it, each parking its partial rows in a slot; the band's rows are then
+  // reduced over its slots in slot order by reduction tasks of CB_TASK_ROWS rows (deterministic).
   {
-    int64_t tot = 0, heaviest = 0;
+    std::vector<int64_t> st((size_t)B.nb, 0);
+    int64_t tot = 0;
     for (int64_t b = 0; b < B.nb; b++) {
-      int64_t st = 0;
-      for (int32_t i = B.band_item[(size_t)b]; i < B.band_item[(size_t)b + 1]; i++) st += B.items[(size_t)i].y;
-      tot += st;
-      heaviest = std::max(heaviest, st);
+      for (int32_t i = B.band_item[(size_t)b]; i < B.band_item[(size_t)b + 1]; i++) st[(size_t)b] += B.items[(size_t)i].y;
+      tot += st[(size_t)b];
     }
-    B.split_items = B.nb < (int64_t)sms || heaviest * sms > 2 * tot;
-    if (B.split_items) {   // units: stage ranges of a band (across its items), >= 64 stages
-      const int64_t per = std::max<int64_t>(32, (tot + 4 * (int64_t)sms - 1) / (4 * (int64_t)sms));
-      for (int64_t b = 0; b < B.nb; b++) {
-        int64_t st = 0;
-        for (int32_t i = B.band_item[(size_t)b]; i < B.band_item[(size_t)b + 1]; i++) st += B.items[(size_t)i].y;
-        for (int64_t sb = 0; sb < st; sb += per)
-          B.units.push_back(make_int4((int32_t)b, (int32_t)sb, (int32_t)std::min<int64_t>(st, sb + per), 0));
-      }
+    // a band is split when it holds more than one SM's share of the stages (tot / sms), into
+    // pieces of about half a share: with largest-first dynamic fetching the tail is then short
+    const int64_t share = std::max<int64_t>(64, (tot + sms - 1) / sms), per = share / 2;
+    B.bsplit.assign((size_t)B.nb, make_int2(0, 0));
+    for (int64_t b = 0; b < B.nb; b++) {
+      const int64_t sb = st[(size_t)b];
+      const int64_t k = sb > share ? (sb + per - 1) / per : 1;
+      if (k == 1) { B.units.push_back(make_int4((int32_t)b, 0, (int32_t)sb, -1)); continue; }
+      B.bsplit[(size_t)b] = make_int2((int32_t)B.nslots, (int32_t)k);
+      for (int64_t q = 0; q < k; q++)
+        B.units.push_back(make_int4((int32_t)b, (int32_t)(sb * q / k), (int32_t)(sb * (q + 1) / k), (int32_t)(B.nslots + q)));
+      B.nslots += k;
+      const int64_t nr = std::min<int64_t>(CB_ROWS, c.m - b * CB_ROWS);
+      for (int64_t r = 0; r < nr; r += CB_TASK_ROWS)
+        B.tasks.push_back(make_int4((int32_t)b, (int32_t)r, (int32_t)std::min<int64_t>(nr, r + CB_TASK_ROWS), 0));
     }
   }
   B.blob.reset(new char[(size_t)std::max<int64_t>(16, bytes)]);
@@ -943,6 +978,7 @@ RowLaunch row_launch(const Ctx* c, const void* x, void* y, double alpha, double 
   L.alpha = alpha; L.beta = beta; L.rec = c->d_rec;
   L.dtype = c->dtype == MSREP_F64 ? 0 : 1; L.has_sell = c->nsell > 0;
   L.xna = c->xna;
+  L.hot = c->d_hot; L.nhot = c->nhot;
   return L;
 }
 ColLaunch col_launch(const Ctx* c, const void* x, void* y, double alpha, double beta) {
@@ -950,9 +986,10 @@ ColLaunch col_launch(const Ctx* c, const void* x, void* y, double alpha, double 
   L.items = c->d_citems; L.item_off = c->d_item_off; L.band_item = c->d_band_item; L.split = c->d_split;
   L.nb = (int)c->cnb; L.blob = c->d_cblob;
   L.x = x; L.xbase = c->wlo;
-  L.split_items = c->csplit; L.nunits = (int)c->cunits; L.units = c->d_cunits; L.item_hst = c->d_item_hst;
-  L.item_hw = c->d_item_hw; L.item_sst = c->d_item_sst; L.item_sg = c->d_item_sg;
-  L.fused = c->nranks == 1 && !c->csplit;
+  L.nunits = (int)c->cunits; L.units = c->d_cunits; L.bsplit = c->d_bsplit; L.slots = c->d_slots;
+  L.ntasks = (int)c->ntasks; L.tasks = c->d_tasks; L.tickets = c->d_tickets; L.ctr = c->d_ctr;
+  L.item_hst = c->d_item_hst; L.item_hw = c->d_item_hw; L.item_sst = c->d_item_sst; L.item_sg = c->d_item_sg;
+  L.fused = c->nranks == 1;
   L.out = L.fused ? y : static_cast<void*>(c->d_py);
   L.m = c->m; L.alpha = alpha; L.beta = beta; L.dtype = c->dtype == MSREP_F64 ? 0 : 1;
   L.xna = c->xna;
@@ -980,12 +1017,11 @@ msrep_status_t launch_row_tiles(const Ctx* c, const RowLaunch& L, int k, cudaStr
 // pCSC) want it; gathers with no reuse inside an SM (R-MAT, uniform random) are 5-6 % faster with
 // L1::no_allocate (profiles/r1_xload_variants.txt, r1_suite_sweep.jsonl).  Both policies give
 // identical bits, so the partition times the main kernel once with each on the built layout
-// (dummy x = 0, y into scratch; 1 warm-up + 3 timed launches) and keeps the faster.  MSREP_XLOAD=0|1
-// in the environment forces a policy.  Host-resident and small partitions (< 2^20 nonzeros)
+// (dummy x = 0, y into scratch; 1 warm-up + 3 timed launches) and keeps the faster.
+// msrep_set_tuning(MSREP_TUNE_XLOAD, 0|1) forces a policy.  Host-resident and small partitions (< 2^20 nonzeros)
 // keep the allocating policy.
 msrep_status_t tune_xload(Ctx* c, cudaStream_t s, int64_t nz_r) {
-  const char* env = getenv("MSREP_XLOAD");
-  if (env && (env[0] == '0' || env[0] == '1') && env[1] == 0) { c->xna = env[0] - '0'; return MSREP_OK; }
+  if (c->tune_xload >= 0) { c->xna = c->tune_xload; return MSREP_OK; }
   c->xna = 0;
   if (c->residency == MSREP_RESIDENT_HOST || nz_r < ((int64_t)1 << 20)) return MSREP_OK;
   const size_t V = vsz(c->dtype), mark = c->bufs.size();
@@ -1140,6 +1176,26 @@ msrep_status_t msrep_set_split_groups(msrep_ctx h, int ngroups, const int* parts
   c->groups.assign(parts_per_group, parts_per_group + ngroups);
   c->split = MSREP_SPLIT_TWO_LEVEL;
   return MSREP_OK;
+}
+
+msrep_status_t msrep_set_tuning(msrep_ctx h, msrep_tuning knob, int value) {
+  if (!h) return fail(MSREP_ERR_INVALID_ARG, "ctx is NULL");
+  Ctx* c = reinterpret_cast<Ctx*>(h);
+  switch (knob) {
+    case MSREP_TUNE_XLOAD:
+      if (value < -1 || value > 1) return fail(MSREP_ERR_INVALID_ARG, "MSREP_TUNE_XLOAD %d (-1, 0, 1)", value);
+      c->tune_xload = value;
+      return MSREP_OK;
+    case MSREP_TUNE_CG_GRAPH:
+      if (value < 0 || value > 1) return fail(MSREP_ERR_INVALID_ARG, "MSREP_TUNE_CG_GRAPH %d (0, 1)", value);
+      c->tune_cg_graph = value;
+      return MSREP_OK;
+    case MSREP_TUNE_HOT_X:
+      if (value < -1 || value > 1) return fail(MSREP_ERR_INVALID_ARG, "MSREP_TUNE_HOT_X %d (-1, 0, 1)", value);
+      c->tune_hot = value;
+      return MSREP_OK;
+  }
+  return fail(MSREP_ERR_INVALID_ARG, "unknown tuning knob %d", (int)knob);
 }
 
 msrep_status_t msrep_set_split(msrep_ctx h, msrep_split split) {
@@ -1382,20 +1438,19 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
     TRY(build_csc_bands(*c, lp, idx, val, V, sms, CB));
     lap(2);
-    c->csplit = CB.split_items;
     TRY(upload_vec(c, CB.items, &c->d_citems, s));
-    TRY(upload_vec(c, CB.units, &c->d_cunits, s));
     TRY(upload_vec(c, CB.item_hst, &c->d_item_hst, s));
     TRY(upload_vec(c, CB.item_hw, &c->d_item_hw, s));
     TRY(upload_vec(c, CB.item_sst, &c->d_item_sst, s));
     TRY(upload_vec(c, CB.item_sg, &c->d_item_sg, s));
-    c->cunits = (int64_t)CB.units.size();
     TRY(upload_vec(c, CB.item_off, &c->d_item_off, s));
     TRY(upload_vec(c, CB.band_item, &c->d_band_item, s));
     TRY(upload_vec(c, CB.split, &c->d_split, s));
+    // units in band order -> chunk ranges (host-resident: runs of whole bands) -> largest first
+    // inside each chunk (the CTAs fetch them in list order)
+    std::vector<std::pair<int64_t, int64_t>> uranges;
     if (c->residency == MSREP_RESIDENT_HOST) {
-      // park the band blobs in pinned memory; chunks = runs of whole bands (and, in split
-      // mode, the units of those bands) of <= chunk_bytes
+      // park the band blobs in pinned memory; chunks = runs of whole bands of <= chunk_bytes
       CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&c->h_blob), (size_t)std::max<int64_t>(16, CB.bytes), cudaHostAllocDefault));
       {
         char* hb = c->h_blob;
@@ -1407,7 +1462,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
         const int32_t i = CB.band_item[(size_t)b];
         return i < (int32_t)CB.items.size() ? CB.item_off[(size_t)i] : CB.bytes;
       };
-      size_t u = 0;
+      size_t u = 0, k = 0;
       for (int64_t b = 0; b < CB.nb;) {
         const int64_t off0 = band_off(b);
         int64_t e = b + 1;
@@ -1415,20 +1470,45 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
         Ctx::Chunk ch{(int32_t)b, (int32_t)e, (int32_t)u, 0, off0, band_off(e) - off0, false};
         while (u < CB.units.size() && CB.units[u].x < e) u++;
         ch.u1 = (int32_t)u;
+        ch.k0 = (int32_t)k;
+        while (k < CB.tasks.size() && CB.tasks[k].x < e) k++;
+        ch.k1 = (int32_t)k;
         c->chunks.push_back(ch);
+        uranges.push_back({ch.u0, ch.u1});
         b = e;
       }
       c->d_cblob = nullptr;
       TRY(ensure_copy_stream(c));
       TRY(alloc_stages(c, s));
     } else {
+      uranges.push_back({0, (int64_t)CB.units.size()});
       TRY(upload(c, CB.blob.get(), (size_t)CB.bytes, &c->d_cblob, s));
+    }
+    for (auto& r : uranges)
+      std::stable_sort(CB.units.begin() + r.first, CB.units.begin() + r.second,
+                       [](const int4& a, const int4& b) { return a.z - a.y > b.z - b.y; });
+    TRY(upload_vec(c, CB.units, &c->d_cunits, s));
+    TRY(upload_vec(c, CB.bsplit, &c->d_bsplit, s));
+    TRY(upload_vec(c, CB.tasks, &c->d_tasks, s));
+    c->cunits = (int64_t)CB.units.size();
+    c->ntasks = (int64_t)CB.tasks.size();
+    c->nslots = CB.nslots;
+    {
+      void* q;
+      TRY(dalloc(c, (size_t)std::max<int64_t>(1, CB.nslots) * CB_ROWS * 8, &q, s));
+      c->d_slots = static_cast<double*>(q);
+      TRY(dalloc(c, (size_t)std::max<int64_t>(1, CB.nb) * 4, &q, s));
+      c->d_tickets = static_cast<int*>(q);
+      CUDA_TRY(cudaMemsetAsync(q, 0, (size_t)std::max<int64_t>(1, CB.nb) * 4, s));
+      TRY(dalloc(c, 16, &q, s));
+      c->d_ctr = static_cast<int*>(q);
+      CUDA_TRY(cudaMemsetAsync(q, 0, 16, s));
     }
     c->cnb = CB.nb;
     c->citems = (int64_t)CB.items.size();
     c->ntiles = 0; c->nsell = 0; c->nslabs = 0; c->nrec = 0; c->nsplit = 0;
     c->blob_bytes = CB.bytes + c->citems * 24 + (CB.nb + 1) * 4 + CB.nb * (CB_W + 1) * 4;
-    c->py_len = c->nranks > 1 ? c->shard * c->nranks : (c->csplit ? m : 0);
+    c->py_len = c->nranks > 1 ? c->shard * c->nranks : 0;
     if (c->py_len) {
       void* pp;
       TRY(dalloc(c, (size_t)c->py_len * 8, &pp, s));
@@ -1547,7 +1627,65 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     int32_t* d_blob16;
     TRY(upload(c, reinterpret_cast<const int4*>(S.tiles.data()), nt, &d_tiles_orig, s));
     TRY(upload_vec(c, blob16, &d_blob16, s));
+    // ---- hot x (device-resident row layouts whose SEG / slab tiles run in the SEG instantiation):
+    // the rank's most-gathered columns get slots in a shared-memory copy of x
+    std::vector<int32_t> hot;
+    int32_t* d_hotslot = nullptr;
+    bool idx_up = false;
+    c->nhot = 0;
+    c->hot_nnz = 0;
+    if (!host_res && c->tune_hot != 0 && nz_r > 0 && n > 0 && (c->nsell == 0 || c->split_launch)) {
+      int sms = 148;
+      CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+      TRY(h2d(c, d_idx, idx + B_lo, (size_t)nz_r * 4, s));
+      idx_up = true;
+      void* dp;
+      TRY(dalloc(c, (size_t)n * 4, &dp, s));
+      int32_t* d_deg = static_cast<int32_t*>(dp);
+      CUDA_TRY(cudaMemsetAsync(d_deg, 0, (size_t)n * 4, s));
+      CUDA_TRY(launch_col_degree(d_idx, nz_r, d_deg, s));
+      std::vector<int32_t> deg((size_t)n);
+      CUDA_TRY(cudaMemcpyAsync(deg.data(), d_deg, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaStreamSynchronize(s));
+      // a slot costs one gather per CTA per launch: worth it from 4 gathers per SM on
+      const int32_t min_deg = 4 * sms;
+      const int T = host_threads(n);
+      std::vector<std::vector<int32_t>> cand((size_t)T);
+      par_ranges(n, [&](int64_t lo, int64_t hi) {
+        const int t = (int)(lo * T / std::max<int64_t>(1, n));
+        auto& v = cand[(size_t)std::min(t, T - 1)];
+        for (int64_t q = lo; q < hi; q++)
+          if (deg[(size_t)q] >= min_deg) v.push_back((int32_t)q);
+      });
+      for (auto& v : cand) hot.insert(hot.end(), v.begin(), v.end());
+      const size_t H = (size_t)hot_max((int)V);
+      auto hotter = [&](int32_t a, int32_t b) { return deg[(size_t)a] != deg[(size_t)b] ? deg[(size_t)a] > deg[(size_t)b] : a < b; };
+      if (hot.size() > H) {
+        std::nth_element(hot.begin(), hot.begin() + (ptrdiff_t)H, hot.end(), hotter);
+        hot.resize(H);
+      }
+      std::sort(hot.begin(), hot.end(), hotter);   // slot 0 = the hottest column
+      int64_t cap_nz = 0;
+      for (int32_t q : hot) cap_nz += deg[(size_t)q];
+      // auto: only when the hot columns carry >= 5 % of the rank's gathers (power-law columns)
+      const bool on = c->tune_hot == 1 ? !hot.empty() : (cap_nz * 20 >= nz_r && nz_r >= ((int64_t)1 << 20));
+      if (on) {
+        TRY(dalloc(c, (size_t)n * 4, &dp, s));
+        d_hotslot = static_cast<int32_t*>(dp);
+        CUDA_TRY(cudaMemsetAsync(d_hotslot, 0xff, (size_t)n * 4, s));   // -1: cold
+        c->nhot = (int)hot.size();
+        c->hot_nnz = cap_nz;
+      } else {
+        hot.clear();
+      }
+    }
     const size_t keep_from = c->bufs.size();
+    if (c->nhot) {
+      TRY(upload_vec(c, hot, &c->d_hot, s));
+      CUDA_TRY(launch_hot_slots(c->d_hot, c->nhot, d_hotslot, s));
+    } else {
+      c->d_hot = nullptr;
+    }
     int64_t pack_bytes = host_res ? 16 : blob_total;
     for (auto& ch : c->chunks) pack_bytes = std::max(pack_bytes, ch.bytes);
     void* bp;
@@ -1565,7 +1703,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
       const int64_t zn = g.z1 - g.z0;
       if (zn > 0) {
         TRY(h2d(c, vp, static_cast<const char*>(val) + (size_t)(B_lo + g.z0) * V, (size_t)zn * V, s));
-        TRY(h2d(c, d_idx, idx + B_lo + g.z0, (size_t)zn * 4, s));
+        if (!idx_up) TRY(h2d(c, d_idx, idx + B_lo + g.z0, (size_t)zn * 4, s));
         if (d_crow) TRY(h2d(c, d_crow, coo_row + B_lo + g.z0, (size_t)zn * 4, s));
       }
       const int64_t off0 = (int64_t)blob16[(size_t)g.t0] * 16;
@@ -1573,7 +1711,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
       PackLaunch PL{d_tiles_orig + g.t0, d_blob16 + g.t0, g.t1 - g.t0,
                     static_cast<const char*>(vp) - (size_t)g.z0 * V, d_idx - g.z0,
                     d_crow ? d_crow - g.z0 : d_aux, fmt == MSREP_COO, (int)V, c->wlo,
-                    host_res ? d_pack - off0 : d_pack, d_lp};
+                    host_res ? d_pack - off0 : d_pack, d_lp, d_hotslot};
       CUDA_TRY(launch_pack(PL, s));
       if (host_res)
         CUDA_TRY(cudaMemcpyAsync(c->h_blob + off0, d_pack, (size_t)c->chunks[gi].bytes, cudaMemcpyDeviceToHost, s));
@@ -1630,6 +1768,8 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   st.nchunks = (int64_t)c->chunks.size();
   st.host_bytes = c->h_bytes;
   st.x_no_allocate = c->xna;
+  st.nhot = c->nhot;
+  st.hot_nnz = c->hot_nnz;
   int64_t X = 0;
   if (colwise(fmt)) {
     X = W;   // pCSC reads x only over its column window
@@ -1651,7 +1791,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     // the rank's entries + its column pointer + its x window + (p > 1) the fp64 py write and the
     // shard read after the reduce-scatter; p = 1 fuses alpha/beta into the band kernel (no py)
     base = nz_r * (int64_t)(V + 4) + (fmt == MSREP_COO_COL ? nz_r * 4 : (W + 1) * 4) + W * (int64_t)V +
-           ((c->nranks > 1 || c->csplit) ? m * 8 + rows_out * 8 : 0);
+           (c->nranks > 1 ? m * 8 + rows_out * 8 : 0);
     ybytes_b1 = rows_out * (int64_t)V * 2;
     ybytes_b0 = rows_out * (int64_t)V;
   } else {
@@ -1661,11 +1801,15 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     ybytes_b0 = own * (int64_t)V;
   }
   st.owned_rows = own;
+  // what the built layout moves per SpMV: the stored blobs (incl. padding, SEG keys instead of COO
+  // row ids), the x entries, y (beta != 0) -- and p > 1 pCSC's py round trip
+  st.stream_bytes = c->blob_bytes + (colwise(fmt) ? W : X) * (int64_t)V + ybytes_b1 +
+                    (colwise(fmt) && c->nranks > 1 ? m * 8 + own * 8 : 0);
   st.alg_bytes = base + ybytes_b1;
   st.alg_bytes_beta0 = base + ybytes_b0;
   const int64_t nmain = c->chunks.empty() ? 1 : (int64_t)c->chunks.size();   // main-kernel launches
   if (colwise(fmt))
-    st.kernels_per_spmv = (c->cnb ? nmain : 0) + ((c->nranks > 1 || c->csplit) ? 1 /*py epilogue*/ : 0) + (c->csplit ? 1 /*memset*/ : 0);
+    st.kernels_per_spmv = (c->cunits ? nmain : 0) + (c->nranks > 1 ? 1 /*shard epilogue*/ : 0);
   else st.kernels_per_spmv = (c->ntiles ? nmain + (c->split_launch && c->chunks.empty() ? 1 : 0) : 0) + (c->nranks > 1 && c->any_flag ? 1 : 0) + (c->nsplit ? 1 : 0);
   int64_t db = 0;
   for (auto& b : c->bufs) db += (int64_t)b.bytes;
@@ -1673,6 +1817,36 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   st.tile_bytes = c->blob_bytes;
   c->ready = true;
   return MSREP_OK;
+}
+
+msrep_status_t msrep_partition_slice(msrep_ctx h, msrep_format fmt, msrep_dtype dtype, int64_t m, int64_t n,
+                                     int64_t nnz, const int64_t* ptr, const int32_t* idx_slice,
+                                     const void* val_slice, int64_t slice_begin, int64_t slice_end,
+                                     msrep_part_desc* parts_out, void* stream) {
+  if (!h) return fail(MSREP_ERR_INVALID_ARG, "ctx is NULL");
+  Ctx* c = reinterpret_cast<Ctx*>(h);
+  if (fmt != MSREP_CSR && fmt != MSREP_CSC) return fail(MSREP_ERR_INVALID_ARG, "msrep_partition_slice takes CSR or CSC");
+  if (dtype != MSREP_F64 && dtype != MSREP_F32) return fail(MSREP_ERR_INVALID_ARG, "dtype %d", (int)dtype);
+  if (m < 0 || n < 0 || nnz < 0 || !ptr) return fail(MSREP_ERR_INVALID_ARG, "bad dimensions or ptr NULL");
+  if (m >= kMaxIdx || n >= kMaxIdx) return fail(MSREP_ERR_TOO_LARGE, "m, n must be < 2^31");
+  if (slice_begin < 0 || slice_end < slice_begin || slice_end > nnz)
+    return fail(MSREP_ERR_INVALID_ARG, "slice [%lld, %lld) outside [0, nnz)", (long long)slice_begin, (long long)slice_end);
+  const int64_t outer = fmt == MSREP_CSC ? n : m;
+  if (ptr[0] != 0 || ptr[outer] != nnz) return fail(MSREP_ERR_DIM_MISMATCH, "ptr[0] != 0 or ptr[%lld] != nnz", (long long)outer);
+  std::vector<int64_t> bnd;
+  split_bounds(fmt, c->split, outer, nnz, c->np, ptr, nullptr, bnd, &c->groups);
+  const int P0 = c->rank * c->vparts, P1 = P0 + c->vparts;
+  const int64_t lo = bnd[(size_t)P0], hi = bnd[(size_t)P1];
+  if (lo < hi && (lo < slice_begin || hi > slice_end))
+    return fail(MSREP_ERR_INVALID_ARG, "slice [%lld, %lld) does not hold this rank's nonzeros [%lld, %lld)",
+                (long long)slice_begin, (long long)slice_end, (long long)lo, (long long)hi);
+  if (lo < hi && (!idx_slice || !val_slice)) return fail(MSREP_ERR_INVALID_ARG, "idx/val NULL");
+  // msrep_partition reads idx / val of CSR / CSC only at this rank's positions [lo, hi): hand it
+  // base addresses that put global position slice_begin at the start of the slices
+  const size_t V = vsz(dtype);
+  const int32_t* idx = reinterpret_cast<const int32_t*>(reinterpret_cast<uintptr_t>(idx_slice) - (uintptr_t)slice_begin * 4);
+  const void* val = reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(val_slice) - (uintptr_t)slice_begin * V);
+  return msrep_partition(h, fmt, dtype, m, n, nnz, ptr, idx, nullptr, val, parts_out, stream);
 }
 
 msrep_status_t spmv_impl(msrep_ctx h, const void* alpha_p, const void* x, const void* beta_p, void* y,
@@ -1734,7 +1908,6 @@ msrep_status_t spmv_impl(msrep_ctx h, const void* alpha_p, const void* x, const 
 
   if (colwise(c->fmt)) {
     ColLaunch L = col_launch(c, x, y, alpha, beta);
-    if (c->csplit) CUDA_TRY(cudaMemsetAsync(c->d_py, 0, (size_t)c->m * 8, s));   // items add into py
     cudaEvent_t pe;
     TRY(prof_begin(c, s, &pe));
     if (c->residency == MSREP_RESIDENT_HOST) {
@@ -1742,8 +1915,8 @@ msrep_status_t spmv_impl(msrep_ctx h, const void* alpha_p, const void* x, const 
         ColLaunch Lc = L;
         Lc.blob = base;
         Lc.band0 = ch.t0; Lc.nb = ch.t1 - ch.t0;
-        Lc.units = L.units ? L.units + ch.u0 : nullptr; Lc.nunits = ch.u1 - ch.u0;
-        if (Lc.split_items && Lc.nunits == 0) return MSREP_OK;
+        Lc.units = L.units + ch.u0; Lc.nunits = ch.u1 - ch.u0;
+        Lc.tasks = L.tasks + ch.k0; Lc.ntasks = ch.k1 - ch.k0;
         CUDA_TRY(launch_cols(Lc, s));
         return MSREP_OK;
       }));
@@ -1756,8 +1929,6 @@ msrep_status_t spmv_impl(msrep_ctx h, const void* alpha_p, const void* x, const 
       NCCL_TRY(ncclReduceScatter(c->d_py, shard, (size_t)c->shard, ncclDouble, ncclSum, c->comm, s));
       CUDA_TRY(launch_axpby_py(shard, static_cast<char*>(y) + (size_t)my_lo * V, my_hi - my_lo, alpha, beta, dt, s));
       if (gather) TRY(allgatherv_y(c, y, seg_lo, seg_hi, s));
-    } else if (c->csplit) {
-      CUDA_TRY(launch_axpby_py(c->d_py, y, c->m, alpha, beta, dt, s));
     }
     return MSREP_OK;
   }
@@ -1835,6 +2006,7 @@ msrep_status_t msrep_spmm(msrep_ctx h, const void* alpha_p, const void* X, const
   L.xmax = c->n > 0 ? (uint32_t)(c->n - 1) : 0u;
   L.alpha = alpha; L.beta = beta; L.rec = c->d_rec_mm;
   L.dtype = dt; L.has_sell = c->nsell > 0;
+  L.hot = c->d_hot;   // SpMM untags hot column ids through the list (no shared-memory cache)
   cudaEvent_t pe;
   TRY(prof_begin(c, s, &pe));
   if (c->residency == MSREP_RESIDENT_HOST) {
@@ -1971,11 +2143,10 @@ msrep_status_t msrep_cg(msrep_ctx h, const void* b, void* x, double tol, int max
   // iteration is launch-bound for small systems (pCSR 110K rows: 0.0228 -> 0.0181 ms/iteration;
   // 2M rows: 0.152 -> 0.147, profiles/r1_cg_graph.jsonl).  Single rank, device-resident, row
   // formats (a replayed pCSC iteration measured 30 % slower than eager), profiling off;
-  // MSREP_CG_GRAPH=0 disables it.  The convergence check then runs every 2*ceil(check_every/2)
+  // msrep_set_tuning(MSREP_TUNE_CG_GRAPH, 0) disables it.  The convergence check then runs every 2*ceil(check_every/2)
   // iterations; the iterates are the same kernels in the same order as the eager loop.
-  const char* genv = getenv("MSREP_CG_GRAPH");
   const bool graph = c->nranks == 1 && c->residency == MSREP_RESIDENT_DEVICE && !colwise(c->fmt) && !c->prof &&
-                     maxit >= 8 && !(genv && genv[0] == '0');
+                     maxit >= 8 && c->tune_cg_graph;
   if (graph && !(rs <= stop)) {
     if (!c->gs) CUDA_TRY(cudaStreamCreateWithFlags(&c->gs, cudaStreamNonBlocking));
     cudaEvent_t ev;

@@ -27,6 +27,15 @@ constexpr int SLAB_NNZ = 512;
 #endif
 constexpr int WARPS = MSREP_WARPS;   // warps per CTA (each with its own TMA ring)
 
+// Hot-x cache (row formats): the rank's most-gathered columns (by nonzero count,
+// chosen at partition time) get a slot in a CTA-wide shared-memory copy of x, refilled at every
+// launch; SEG / slab tiles carry HOT_TAG | slot instead of the column id for them.  One CTA of
+// HOT_WARPS warps per SM holds HOT_BYTES of x (12288 fp64 / 24576 fp32 entries).
+constexpr uint32_t HOT_TAG = 0x80000000u;
+constexpr int HOT_WARPS = 16;
+constexpr int HOT_BYTES = 96 * 1024;
+__host__ __device__ constexpr int hot_max(int vsize) { return HOT_BYTES / vsize; }
+
 // Device layout: every tile is one contiguous, 16-byte aligned "blob"; each
 // segment is padded to 16 bytes so one TMA bulk copy moves the tile.
 //
@@ -103,6 +112,7 @@ struct PackLaunch {        // build the tile blobs from the rank's plain slices 
   int coo; int vsize; int64_t row_base;                       // COO: global row of window row 0
   char* blob;
   const int32_t* lptr;                                        // window-local pointer (SELL tiles; CSR: == ptr)
+  const int32_t* hotslot;                                     // [n]: hot-x slot of a column, -1 if cold; NULL: no hot x
 };
 
 constexpr int MAX_MIRRORS = 8;   // msrep_spmv_mirror: extra y buffers (peer-mapped or local)
@@ -117,6 +127,7 @@ struct RowLaunch {
   int has_sell;                                              // tiles begin with SELL tiles
   int nmirror; void* mirror[MAX_MIRRORS];                    // y rows are also stored here (msrep_spmv_mirror)
   int xna;                                                   // x gathers with L1::no_allocate (SEG / slab tiles)
+  const int32_t* hot; int nhot;                              // hot-x columns by slot (nhot == 0: no hot x)
 };
 
 // pCSC row-band layout.  The rank's nonzeros are regrouped
@@ -155,11 +166,17 @@ struct ColLaunch {
   void* out; int64_t m;                                      // fused: y (dtype); else fp64 py
   double alpha, beta;
   int fused; int dtype;
-  // split mode (few bands, or bands much heavier than one SM's share): the units of work are
-  // stage ranges of a band, {band, first stage, end stage, 0} counted over the band's items in
-  // order; each unit adds its partial band into py
-  int split_items, nunits;
-  const int4* units;
+  // Units of work, fetched dynamically (ctr[0]) by the CTAs, largest first: {band, first stage,
+  // end stage, slot}, stages counted over the band's items in order.  slot < 0: the whole band,
+  // written out at the unit's end; slot >= 0: a stage range of a heavy ("split") band whose
+  // partial rows go to slots[slot][CB_ROWS] -- the band's slots are reduced in slot order by the
+  // reduction tasks at the end of the launch (deterministic, no atomics on values).
+  int nunits; const int4* units;
+  const int2* bsplit;         // [total bands]: {first slot, slots} of a split band ({0, 0} otherwise)
+  double* slots;
+  int ntasks; const int4* tasks;   // reduction tasks {band, first row, end row (band-local), 0}
+  int* tickets;               // [total bands]: units of a split band that have written their slot
+  int* ctr;                   // [4]: next unit, finished CTAs, next task (reset by the last CTA)
   const int32_t* item_hst;    // [items]: stages [0, item_hst[i]) may hold same-row groups
   const int32_t* item_hw;     // [items * CB_W]: same-row groups leading warp w's list of item i
   const int32_t* item_sst;    // [items]: stages [item_sst[i], ...) may hold segmented groups
@@ -198,6 +215,8 @@ cudaError_t launch_axpby_py(const double* py, void* y, int64_t count, double alp
 cudaError_t launch_rebase(const int64_t* gptr, int32_t* lptr, int64_t count, int64_t lo, int64_t hi,
                           cudaStream_t s);                                                  // clamp(gptr,lo,hi)-lo
 cudaError_t launch_pack(const PackLaunch& L, cudaStream_t s);
+cudaError_t launch_col_degree(const int32_t* idx, int64_t nz, int32_t* deg, cudaStream_t s);   // deg[idx[i]]++
+cudaError_t launch_hot_slots(const int32_t* hot, int nhot, int32_t* slot, cudaStream_t s);      // slot[hot[k]] = k
 // CG vector kernels on an owned segment of n entries (kernels.cu).  sc = device scalars
 // {rs (parity 0), rs (parity 1), -, bnorm2}; part_in / part_out = CG_PARTS per-block partial
 // sums (every consumer block re-sums part_in in the same fixed order).

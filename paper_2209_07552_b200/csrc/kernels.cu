@@ -117,13 +117,14 @@ struct RStage {
   static constexpr int BYTES = N + N * (int)sizeof(VT) + N * 4;
 };
 
-template <int STAGE_B, int NS, int SCRATCH>
+template <int STAGE_B, int NS, int SCRATCH, int NW = WARPS, int HOTB = 0>
 struct WLayout {
   static constexpr int DESC_OFF = NS * STAGE_B;                          // int4 per stage
   static constexpr int SCR_OFF = DESC_OFF + NS * 16;                     // per-warp fp64 scratch
   static constexpr int WARP_B = (SCR_OFF + SCRATCH + 15) & ~15;
-  static constexpr int BAR_OFF = WARPS * WARP_B;
-  static constexpr int TOTAL = BAR_OFF + WARPS * NS * 8;
+  static constexpr int HOT_OFF = NW * WARP_B;                            // CTA-wide hot x cache (HOTB bytes)
+  static constexpr int BAR_OFF = HOT_OFF + HOTB;
+  static constexpr int TOTAL = BAR_OFF + NW * NS * 8;
 };
 
 // nonzeros per lane in a full SEG tile / slab (+1 extra slot when ragged): 16 fp64, 32 fp32
@@ -182,9 +183,49 @@ __device__ __forceinline__ void issue_blob(const char* blob, int4 d, int kind, i
 #endif
 template <typename VT>
 struct SStage { static constexpr int BYTES = SELL_R_MAX * 32 * 2 + SELL_W_MAX * SELL_ROWS * ((int)sizeof(VT) + 4); };
-template <typename VT, bool SELL>
+template <typename VT, bool SELL, bool HOT = false>
 using RowLayout = WLayout<(SELL && SStage<VT>::BYTES > RStage<VT>::BYTES) ? SStage<VT>::BYTES : RStage<VT>::BYTES, 1,
-                          MAX_TILE_ROWS * 8>;
+                          MAX_TILE_ROWS * 8, HOT ? HOT_WARPS : WARPS, HOT ? HOT_BYTES : 0>;
+
+// x gather of a SEG / slab column id: tagged ids (bit 31, internal.h HOT_TAG) read the CTA's
+// shared-memory copy of the rank's hottest x entries, the others go through L2.  Branch-free: one
+// predicated LDS and one predicated LDG into the same register, so all of a lane's gathers stay
+// in flight together (a branch per gather serialises the two paths, 1.3 -> 2.2 ms on R-MAT).
+template <bool NA>
+__device__ __forceinline__ double ldx_sel(const double* x, uint32_t hbase, uint32_t c, uint64_t pol) {
+  double v;
+  if constexpr (NA) asm("{\n\t.reg .pred p;\n\t.reg .u32 ci, sa;\n\t.reg .u64 ga;\n\t"
+                        "setp.lt.s32 p, %1, 0;\n\tand.b32 ci, %1, 0x7fffffff;\n\tmad.lo.u32 sa, ci, 8, %2;\n\t"
+                        "mad.wide.u32 ga, %1, 8, %3;\n\t@p ld.shared.f64 %0, [sa];\n\t"
+                        "@!p ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [ga], %4;\n\t}"
+                        : "=d"(v) : "r"(c), "r"(hbase), "l"(x), "l"(pol));
+  else asm("{\n\t.reg .pred p;\n\t.reg .u32 ci, sa;\n\t.reg .u64 ga;\n\t"
+           "setp.lt.s32 p, %1, 0;\n\tand.b32 ci, %1, 0x7fffffff;\n\tmad.lo.u32 sa, ci, 8, %2;\n\t"
+           "mad.wide.u32 ga, %1, 8, %3;\n\t@p ld.shared.f64 %0, [sa];\n\t"
+           "@!p ld.global.nc.L2::cache_hint.f64 %0, [ga], %4;\n\t}"
+           : "=d"(v) : "r"(c), "r"(hbase), "l"(x), "l"(pol));
+  return v;
+}
+template <bool NA>
+__device__ __forceinline__ float ldx_sel(const float* x, uint32_t hbase, uint32_t c, uint64_t pol) {
+  float v;
+  if constexpr (NA) asm("{\n\t.reg .pred p;\n\t.reg .u32 ci, sa;\n\t.reg .u64 ga;\n\t"
+                        "setp.lt.s32 p, %1, 0;\n\tand.b32 ci, %1, 0x7fffffff;\n\tmad.lo.u32 sa, ci, 4, %2;\n\t"
+                        "mad.wide.u32 ga, %1, 4, %3;\n\t@p ld.shared.f32 %0, [sa];\n\t"
+                        "@!p ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [ga], %4;\n\t}"
+                        : "=f"(v) : "r"(c), "r"(hbase), "l"(x), "l"(pol));
+  else asm("{\n\t.reg .pred p;\n\t.reg .u32 ci, sa;\n\t.reg .u64 ga;\n\t"
+           "setp.lt.s32 p, %1, 0;\n\tand.b32 ci, %1, 0x7fffffff;\n\tmad.lo.u32 sa, ci, 4, %2;\n\t"
+           "mad.wide.u32 ga, %1, 4, %3;\n\t@p ld.shared.f32 %0, [sa];\n\t"
+           "@!p ld.global.nc.L2::cache_hint.f32 %0, [ga], %4;\n\t}"
+           : "=f"(v) : "r"(c), "r"(hbase), "l"(x), "l"(pol));
+  return v;
+}
+template <bool HOT, bool NA, typename VT>
+__device__ __forceinline__ VT ldx_hot(const VT* x, uint32_t hbase, uint32_t c, uint64_t pol) {
+  if constexpr (HOT) return ldx_sel<NA>(x, hbase, c, pol);
+  else return ldx<NA>(x + c, pol);
+}
 
 // One SELL tile with R rows per lane (internal.h): all R*W column indices are read from the
 // slot, then all R*W x gathers are in flight before the first FMA; padding is masked by the
@@ -238,10 +279,12 @@ __device__ __forceinline__ void sell_tile(const RowLaunch& P, const int4 d, cons
   refill();
 }
 
-template <typename VT, bool SELL, bool MIRROR, bool NA>
-__global__ void __launch_bounds__(WARPS * 32, sizeof(VT) == 4 ? MSREP_ROW_MINB_F32 : MSREP_ROW_MINB)
+template <typename VT, bool SELL, bool MIRROR, bool NA, bool HOT>
+__global__ void __launch_bounds__(HOT ? HOT_WARPS * 32 : WARPS * 32,
+                                  HOT ? 1 : (sizeof(VT) == 4 ? MSREP_ROW_MINB_F32 : MSREP_ROW_MINB))
     rows_kernel(const RowLaunch P) {
-  using Lay = RowLayout<VT, SELL>;
+  using Lay = RowLayout<VT, SELL, HOT>;
+  constexpr int NW = HOT ? HOT_WARPS : WARPS;
   constexpr int QMAX = qmax<VT>();
   constexpr int V = (int)sizeof(VT);
   constexpr int YR = MAX_TILE_ROWS / 32;
@@ -251,13 +294,15 @@ __global__ void __launch_bounds__(WARPS * 32, sizeof(VT) == 4 ? MSREP_ROW_MINB_F
   int4* sdesc = reinterpret_cast<int4*>(st + Lay::DESC_OFF);
   double* rsum = reinterpret_cast<double*>(st + Lay::SCR_OFF);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Lay::BAR_OFF) + warp;
-  const int gw = blockIdx.x * WARPS + warp, nw = gridDim.x * WARPS;
+  const int gw = blockIdx.x * NW + warp, nw = gridDim.x * NW;
 
   const VT* __restrict__ x = static_cast<const VT*>(P.x);
   VT* __restrict__ y = static_cast<VT*>(P.y);
   const double alpha = P.alpha, beta = P.beta;
   const uint32_t xmax = P.xmax;
   const uint64_t xpol = policy_evict_last();
+  VT* hx = reinterpret_cast<VT*>(smem + Lay::HOT_OFF);
+  const uint32_t hbase = saddr(hx);
 
   uint64_t pol = 0;
   int4 dn = make_int4(0, 0, 0, -1);
@@ -271,6 +316,26 @@ __global__ void __launch_bounds__(WARPS * 32, sizeof(VT) == 4 ? MSREP_ROW_MINB_F
       issue_blob(P.blob, d, tile_kind(d), V, st, bar, pol);
     }
     if (gw + nw < P.ntiles) dn = P.tiles[gw + nw];
+  }
+  if constexpr (HOT) {   // the CTA's copy of the hot x entries, gathered while the first tiles land
+    constexpr int U = 8, T = NW * 32;
+    for (int k0 = 0; k0 < P.nhot; k0 += U * T) {
+      int cs[U];
+      VT xs[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int k = k0 + u * T + (int)threadIdx.x;
+        cs[u] = k < P.nhot ? __ldg(P.hot + k) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) xs[u] = __ldg(x + cs[u]);
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int k = k0 + u * T + (int)threadIdx.x;
+        if (k < P.nhot) hx[k] = xs[u];
+      }
+    }
+    __syncthreads();
   }
   __syncwarp();
 
@@ -345,7 +410,7 @@ __global__ void __launch_bounds__(WARPS * 32, sizeof(VT) == 4 ? MSREP_ROW_MINB_F
     VT xv[QMAX + 1];
     if (slab) {
 #pragma unroll
-      for (int u = 0; u < QMAX; u++) xv[u] = lane + 32 * u < nnz ? ldx<NA>(x + c[u], xpol) : VT(0);
+      for (int u = 0; u < QMAX; u++) xv[u] = lane + 32 * u < nnz ? ldx_hot<HOT, NA>(x, hbase, c[u], xpol) : VT(0);
       double acc = 0.0;
 #pragma unroll
       for (int u = 0; u < QMAX; u++) acc = fma((double)v[u], (double)xv[u], acc);   // padding: 0 * 0
@@ -364,7 +429,7 @@ __global__ void __launch_bounds__(WARPS * 32, sizeof(VT) == 4 ? MSREP_ROW_MINB_F
 #pragma unroll
     for (int j = 0; j <= QMAX; j++) {
       const bool on = j < QMAX ? j < q : extra;
-      xv[j] = on ? ldx<NA>(x + c[j], xpol) : VT(0);
+      xv[j] = on ? ldx_hot<HOT, NA>(x, hbase, c[j], xpol) : VT(0);
     }
     if (d.w != KIND_W_SEG_DENSE) {   // rows without entries must read 0 (a dense tile writes every row)
       for (int rr = lane; rr < nrows; rr += 32) rsum[rr] = 0.0;
@@ -446,6 +511,12 @@ __device__ __forceinline__ void mm_write_row(VT* yrow, const double (&acc)[K], d
     if (beta != 0.0) o += beta * (double)yrow[j];
     yrow[j] = (VT)o;
   }
+}
+
+// a SEG / slab column id of a hot-x partition (tag bit set) -> the column (SpMM gathers K-wide rows
+// of X, which the SpMV's shared-memory x cache does not hold)
+__device__ __forceinline__ uint32_t untag(const RowLaunch& P, uint32_t c) {
+  return (c & HOT_TAG) ? (uint32_t)__ldg(P.hot + (c & ~HOT_TAG)) : c;
 }
 
 template <typename VT, int K, bool SELL>
@@ -587,7 +658,7 @@ __global__ void __launch_bounds__(WARPS * 32, MSREP_ROW_MINB) rows_mm_kernel(con
         VT xr[BG][K];
 #pragma unroll
         for (int b = 0; b < BG; b++) {
-          if (lane + 32 * (u0 + b) < nnz) ldx_row<VT, K>(x + (int64_t)c[u0 + b] * K, xr[b], xpol);
+          if (lane + 32 * (u0 + b) < nnz) ldx_row<VT, K>(x + (int64_t)untag(P, c[u0 + b]) * K, xr[b], xpol);
           else {
 #pragma unroll
             for (int j = 0; j < K; j++) xr[b][j] = VT(0);
@@ -629,7 +700,7 @@ __global__ void __launch_bounds__(WARPS * 32, MSREP_ROW_MINB) rows_mm_kernel(con
       for (int b = 0; b < BG; b++) {
         const int j = j0 + b;
         const bool on = j <= QMAX && (j < QMAX ? j < q : extra);
-        if (on) ldx_row<VT, K>(x + (int64_t)c[j <= QMAX ? j : QMAX] * K, xr[b], xpol);
+        if (on) ldx_row<VT, K>(x + (int64_t)untag(P, c[j <= QMAX ? j : QMAX]) * K, xr[b], xpol);
         else {
 #pragma unroll
           for (int jj = 0; jj < K; jj++) xr[b][jj] = VT(0);
@@ -716,18 +787,27 @@ struct CBLayout {
   static constexpr int STAGE = CB_W * CB_SEG * ((int)sizeof(VT) + 4);
   static constexpr int ST_OFF = CB_ROWS * 8;
   static constexpr int DESC_OFF = ST_OFF + CB_NS * STAGE;
-  static constexpr int BAR_OFF = DESC_OFF + CB_NS * 16;
+  static constexpr int META_OFF = DESC_OFF + CB_NS * 16;   // per stage: [w] same-row groups, [16 + w] first segmented group
+  static constexpr int MISC_OFF = META_OFF + CB_NS * 32 * 4;
+  static constexpr int BAR_OFF = MISC_OFF + 16;
   static constexpr int TOTAL = BAR_OFF + 2 * CB_NS * 8;
 };
 
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 // one consumer warp's share of a stage, in registers
 template <typename VT>
 struct CBStage {
-  int4 d;                 // {band (-1: end), seg | stage << 11, window col base, last | same-row << 1 | segmented << 2 | item << 3}
+  int4 d;                 // {band (-1: end), seg | stage << 11, window col base (unit end: slot), flags}
+                          // flags: 1 unit end (no entries) | 2 same-row groups | 4 segmented groups
+  int hw, sg;             // this warp's same-row groups / first segmented group of the stage's list
   uint32_t pk[CB_PER];
   VT v[CB_PER], xv[CB_PER];
 };
@@ -741,6 +821,9 @@ __device__ __forceinline__ void cb_load(CBStage<VT>& S, int it, const unsigned c
   const int s = it % CB_NS;
   mbar_wait(&full[s], (uint32_t)((it / CB_NS) & 1));
   S.d = sdesc[s];
+  const int* meta = reinterpret_cast<const int*>(smem + L::META_OFF) + s * 32;
+  S.hw = (S.d.w & 2) ? meta[warp] : 0;
+  S.sg = (S.d.w & 4) ? meta[16 + warp] : INT_MAX;
   const int seg = S.d.y & 0x7ff;
   const unsigned char* st = smem + L::ST_OFF + s * L::STAGE;
   const VT* sv = reinterpret_cast<const VT*>(st) + warp * seg;
@@ -759,6 +842,39 @@ __device__ __forceinline__ void cb_load(CBStage<VT>& S, int it, const unsigned c
   for (int k = 0; k < CB_PER; k++) S.xv[k] = S.pk[k] != CB_HOLE ? ldx<NA>(xb + (S.pk[k] >> CB_LOG2), xpol) : VT(0);
 }
 
+// CB_PUT rows (row0 + i*stride, i < CB_PUT, those < row_end) receive their full sums a[i]:
+// y = alpha*a + beta*y (fused, one rank holds the whole sum), else the fp64 py of the
+// reduce-scatter.  The y loads of the batch are all issued before the first store.
+constexpr int CB_PUT = 4;
+template <typename VT>
+__device__ __forceinline__ void cb_put(const ColLaunch& P, int64_t row0, int stride, int64_t row_end,
+                                       const double (&a)[CB_PUT]) {
+  if (P.fused) {
+    VT* y = static_cast<VT*>(P.out);
+    double yv[CB_PUT];
+#pragma unroll
+    for (int i = 0; i < CB_PUT; i++) {
+      const int64_t r = row0 + (int64_t)i * stride;
+      yv[i] = (P.beta != 0.0 && r < row_end) ? (double)__ldcs(y + r) : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < CB_PUT; i++) {
+      const int64_t r = row0 + (int64_t)i * stride;
+      if (r < row_end) {
+        double o = P.alpha * a[i];
+        if (P.beta != 0.0) o += P.beta * yv[i];
+        __stcs(y + r, (VT)o);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < CB_PUT; i++) {
+      const int64_t r = row0 + (int64_t)i * stride;
+      if (r < row_end) __stcs(static_cast<double*>(P.out) + r, a[i]);
+    }
+  }
+}
+
 template <typename VT, bool NA>
 __global__ void __launch_bounds__(CB_THREADS, 1) csc_band_kernel(const ColLaunch P) {
   using L = CBLayout<VT>;
@@ -766,6 +882,7 @@ __global__ void __launch_bounds__(CB_THREADS, 1) csc_band_kernel(const ColLaunch
   extern __shared__ __align__(128) unsigned char smem[];
   double* acc = reinterpret_cast<double*>(smem);
   int4* sdesc = reinterpret_cast<int4*>(smem + L::DESC_OFF);
+  int* misc = reinterpret_cast<int*>(smem + L::MISC_OFF);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
   uint64_t* empty = full + CB_NS;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -778,65 +895,53 @@ __global__ void __launch_bounds__(CB_THREADS, 1) csc_band_kernel(const ColLaunch
   }
   __syncthreads();
 
-  if (warp == CB_W) {   // ---- producer (one lane): bands -> items -> stage blobs
-    if (lane == 0) {
-      const uint64_t pol = policy_evict_first();
-      int it = 0;
-      auto stage = [&](int4 d, const char* src, int bytes) {
-        const int s = it % CB_NS;
-        if (it >= CB_NS) mbar_wait(&empty[s], (uint32_t)(((it / CB_NS) - 1) & 1));
+  if (warp == CB_W) {   // ---- producer warp: units (fetched dynamically) -> items -> stage blobs
+    const uint64_t pol = policy_evict_first();
+    int* meta = reinterpret_cast<int*>(smem + L::META_OFF);
+    int it = 0;
+    auto stage = [&](int4 d, const char* src, int bytes, int hw, int sg) {
+      const int s = it % CB_NS;
+      if (it >= CB_NS) mbar_wait(&empty[s], (uint32_t)(((it / CB_NS) - 1) & 1));
+      if ((d.w & 6) && lane < CB_W) { meta[s * 32 + lane] = hw; meta[s * 32 + 16 + lane] = sg; }
+      __syncwarp();
+      if (lane == 0) {
         sdesc[s] = d;
         mbar_arrive_expect_tx(&full[s], (uint32_t)bytes);
         if (bytes) tma_1d(smem + L::ST_OFF + s * L::STAGE, src, (uint32_t)bytes, &full[s], pol);
-        it++;
-      };
-      if (P.split_items) {   // one unit (a stage range of a band) at a time; each ends a partial band
-        for (int u = blockIdx.x; u < P.nunits; u += gridDim.x) {
-          const int4 un = P.units[u];
-          const int b = un.x, i0 = P.band_item[b], i1 = P.band_item[b + 1];
-          int g = 0;   // band stage index
-          for (int i = i0; i < i1 && g < un.z; i++) {
-            const int4 item = P.items[i];
-            if (g + item.y <= un.y) { g += item.y; continue; }
-            const int hst = P.item_hst[i], sst = P.item_sst[i];
-            const int s0 = un.y > g ? un.y - g : 0, s1 = min(item.y, un.z - g);
-            const char* src = P.blob + P.item_off[i] + (int64_t)s0 * CB_W * CB_SEG * (V + 4);
-            for (int sg = s0; sg < s1; sg++) {
-              const int seg = sg == item.y - 1 ? item.w : CB_SEG;
-              const int bytes = CB_W * seg * (V + 4);
-              stage(make_int4(b, seg | (sg << 11), item.z,
-                              (g + sg == un.z - 1 ? 1 : 0) | (sg < hst ? 2 : 0) | (sg >= sst ? 4 : 0) | (i << 3)),
-                    src, bytes);
-              src += bytes;
-            }
-            g += item.y;
-          }
-        }
-        stage(make_int4(-1, 0, 0, 0), nullptr, 0);
-        return;
       }
-      for (int b = P.band0 + blockIdx.x; b < P.band0 + P.nb; b += gridDim.x) {
-        const int i0 = P.band_item[b], i1 = P.band_item[b + 1];
-        if (i0 == i1) {   // empty band: still written out (zeros / beta*y)
-          stage(make_int4(b, 0, 0, 1), nullptr, 0);
-          continue;
+      __syncwarp();
+      it++;
+    };
+    for (;;) {
+      int u = 0;
+      if (lane == 0) u = atomicAdd(&P.ctr[0], 1);
+      u = __shfl_sync(FULL, u, 0);
+      if (u >= P.nunits) break;
+      const int4 un = P.units[u];
+      const int b = un.x, i0 = P.band_item[b], i1 = P.band_item[b + 1];
+      int g = 0;   // band stage index of the item's first stage
+      for (int i = i0; i < i1 && g < un.z; i++) {
+        const int4 item = P.items[i];
+        if (g + item.y <= un.y) { g += item.y; continue; }
+        const int hst = P.item_hst[i], sst = P.item_sst[i];
+        const int q0 = un.y > g ? un.y - g : 0, q1 = min(item.y, un.z - g);
+        int hw = 0, sgw = INT_MAX;   // lane w < CB_W: warp w's list heads (loaded once per item)
+        if (lane < CB_W) {
+          if (q0 < hst) hw = P.item_hw[(int64_t)i * CB_W + lane];
+          if (q1 > sst) sgw = P.item_sg[(int64_t)i * CB_W + lane];
         }
-        for (int i = i0; i < i1; i++) {
-          const int4 item = P.items[i];
-          const char* src = P.blob + P.item_off[i];
-          const int hst = P.item_hst[i], sst = P.item_sst[i];
-          for (int sg = 0; sg < item.y; sg++) {
-            const int seg = sg == item.y - 1 ? item.w : CB_SEG;
-            const int bytes = CB_W * seg * (V + 4);
-            stage(make_int4(b, seg | (sg << 11), item.z,
-                            ((i == i1 - 1 && sg == item.y - 1) ? 1 : 0) | (sg < hst ? 2 : 0) | (sg >= sst ? 4 : 0) |
-                                (i << 3)), src, bytes);
-            src += bytes;
-          }
+        const char* src = P.blob + P.item_off[i] + (int64_t)q0 * CB_W * CB_SEG * (V + 4);
+        for (int q = q0; q < q1; q++) {
+          const int seg = q == item.y - 1 ? item.w : CB_SEG;
+          const int bytes = CB_W * seg * (V + 4);
+          stage(make_int4(b, seg | (q << 11), item.z, (q < hst ? 2 : 0) | (q >= sst ? 4 : 0)), src, bytes, hw, sgw);
+          src += bytes;
         }
+        g += item.y;
       }
-      stage(make_int4(-1, 0, 0, 0), nullptr, 0);
+      stage(make_int4(b, 0, un.w, 1), nullptr, 0, 0, 0);   // unit end: write out (slot < 0) or park the partial rows
     }
+    stage(make_int4(-1, 0, 0, 0), nullptr, 0, 0, 0);
     return;
   }
 
@@ -853,9 +958,7 @@ __global__ void __launch_bounds__(CB_THREADS, 1) csc_band_kernel(const ColLaunch
     // the scatter: 32 distinct rows per step, steps in list order (deterministic)
     if (A.d.w & 6) {   // this stage may hold SAME-ROW groups (heavy rows; first in each list) or
                        // SEGMENTED groups (row-sorted runs; last in each list)
-      const int item = A.d.w >> 3;
-      const int hw = (A.d.w & 2) ? P.item_hw[item * CB_W + warp] : 0;         // same-row groups leading the list
-      const int sgw = (A.d.w & 4) ? P.item_sg[item * CB_W + warp] : INT_MAX;  // first segmented group
+      const int hw = A.hw, sgw = A.sg;
       const int j0 = (A.d.y >> 11) * CB_PER;                                  // list step of k = 0
 #pragma unroll
       for (int k = 0; k < CB_PER; k++) {
@@ -884,7 +987,6 @@ __global__ void __launch_bounds__(CB_THREADS, 1) csc_band_kernel(const ColLaunch
         }
       }
     } else {
-      // the scatter: 32 distinct rows per step, steps in list order (deterministic)
 #pragma unroll
       for (int k = 0; k < CB_PER; k++)
         if (A.pk[k] != CB_HOLE) {
@@ -892,49 +994,82 @@ __global__ void __launch_bounds__(CB_THREADS, 1) csc_band_kernel(const ColLaunch
           *a = fma((double)A.v[k], (double)A.xv[k], *a);
         }
     }
-    if (A.d.w & 1) {   // band (or split unit) complete: this warp writes its rows once and re-zeroes them
+    if (A.d.w & 1) {   // unit complete: this warp writes its rows once and re-zeroes them
       __syncwarp();
-      const int b = A.d.x;
+      const int b = A.d.x, slot = A.d.z;
       const int lo = P.split[b * (CB_W + 1) + warp], hi = P.split[b * (CB_W + 1) + warp + 1];
-      const int64_t r0 = (int64_t)b * CB_ROWS;
-      if (P.fused) {
-        VT* y = static_cast<VT*>(P.out) + r0;
-        const double alpha = P.alpha, beta = P.beta;
-        for (int rb = lo; rb < hi; rb += 128) {
-          double yv[4];
+      if (slot < 0) {   // the whole band: its rows are complete
+        const int64_t r0 = (int64_t)b * CB_ROWS;
+        for (int rb = lo + lane; rb < hi; rb += 32 * CB_PUT) {
+          double a[CB_PUT];
 #pragma unroll
-          for (int u = 0; u < 4; u++) {
-            const int r = rb + lane + 32 * u;
-            yv[u] = (beta != 0.0 && r < hi) ? (double)__ldcs(y + r) : 0.0;
+          for (int i = 0; i < CB_PUT; i++) {
+            const int r = rb + 32 * i;
+            a[i] = r < hi ? acc[r] : 0.0;
+            if (r < hi) acc[r] = 0.0;
           }
-#pragma unroll
-          for (int u = 0; u < 4; u++) {
-            const int r = rb + lane + 32 * u;
-            if (r < hi) {
-              double o = alpha * acc[r];
-              if (beta != 0.0) o += beta * yv[u];
-              __stcs(y + r, (VT)o);
-              acc[r] = 0.0;
-            }
-          }
+          cb_put<VT>(P, r0 + rb, 32, r0 + hi, a);
         }
-      } else if (P.split_items) {   // partial band of one item: add (other items of the band do too)
-        double* py = static_cast<double*>(P.out) + r0;
+      } else {          // a stage range of a split band: park the partial rows in the unit's slot
+        double* sl = P.slots + (int64_t)slot * CB_ROWS;
         for (int r = lo + lane; r < hi; r += 32) {
-          const double a = acc[r];
-          if (a != 0.0) atomicAdd(py + r, a);
+          __stcg(sl + r, acc[r]);
           acc[r] = 0.0;
         }
-      } else {
-        double* py = static_cast<double*>(P.out) + r0;
-        for (int r = lo + lane; r < hi; r += 32) {
-          __stcs(py + r, acc[r]);
-          acc[r] = 0.0;
-        }
+        __threadfence();
+        named_bar_sync(1, CB_NC);
+        if (threadIdx.x == 0) atomicAdd(&P.tickets[b], 1);   // after every warp's rows are visible
       }
-      named_bar_sync(1, CB_NC);   // every warp's rows are written and zero before the next band
+      named_bar_sync(1, CB_NC);   // every warp's rows are written and zero before the next unit
     }
     A = B;
+  }
+
+  // ---- reduction tasks: rows of a split band = the band's slots added in slot order (stage order),
+  // once every unit of the band has parked its rows (deterministic whichever CTA runs it)
+  for (;;) {
+    if (threadIdx.x == 0) misc[0] = atomicAdd(&P.ctr[2], 1);
+    named_bar_sync(1, CB_NC);
+    const int t = misc[0];
+    if (t >= P.ntasks) break;
+    const int4 tk = P.tasks[t];
+    const int2 bs = P.bsplit[tk.x];
+    if (threadIdx.x == 0)
+      while (ld_acquire_gpu(P.tickets + tk.x) < bs.y) __nanosleep(256);
+    named_bar_sync(1, CB_NC);
+    __threadfence();
+    const int64_t r0 = (int64_t)tk.x * CB_ROWS;
+    for (int rb = tk.y + threadIdx.x; rb < tk.z; rb += CB_NC * CB_PUT) {
+      double a[CB_PUT];
+#pragma unroll
+      for (int i = 0; i < CB_PUT; i++) {
+        const int r = rb + CB_NC * i;
+        const double* sp = P.slots + (int64_t)bs.x * CB_ROWS + (r < tk.z ? r : tk.y);
+        // slot order (= stage order) fixed: q = 0, 1, ...; 4 loads in flight per step
+        double t = 0.0;
+        int q = 0;
+        for (; q + 4 <= bs.y; q += 4) {
+          const double l0 = __ldcg(sp + (int64_t)q * CB_ROWS), l1 = __ldcg(sp + (int64_t)(q + 1) * CB_ROWS);
+          const double l2 = __ldcg(sp + (int64_t)(q + 2) * CB_ROWS), l3 = __ldcg(sp + (int64_t)(q + 3) * CB_ROWS);
+          t = (((t + l0) + l1) + l2) + l3;
+        }
+        for (; q < bs.y; q++) t += __ldcg(sp + (int64_t)q * CB_ROWS);
+        a[i] = t;
+      }
+      cb_put<VT>(P, r0 + rb, CB_NC, r0 + tk.z, a);
+    }
+    named_bar_sync(1, CB_NC);   // misc[0] is read by every thread before the next fetch
+  }
+  // the last CTA to finish resets the work counters and the split bands' tickets for the next launch
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&P.ctr[1], 1) == (int)gridDim.x - 1) {
+      for (int t = 0; t < P.ntasks; t++) P.tickets[P.tasks[t].x] = 0;
+      P.ctr[0] = 0;
+      P.ctr[2] = 0;
+      __threadfence();
+      P.ctr[1] = 0;
+    }
   }
 }
 
@@ -943,6 +1078,12 @@ __global__ void __launch_bounds__(CB_THREADS, 1) csc_band_kernel(const ColLaunch
 // designed kernels"): one warp per tile copies the tile's aux / val / idx into
 // its contiguous blob.  aux for pointer kinds = tile-local pointer, i.e.
 // clamp(ptr[row0 + j], z0, z1) - z0 for j = 0..nrows (the rebase of Alg. 2 l.12).
+__device__ __forceinline__ int pack_col(const PackLaunch& L, int c) {
+  if (!L.hotslot) return c;
+  const int h = L.hotslot[c];
+  return h >= 0 ? (int)(HOT_TAG | (uint32_t)h) : c;
+}
+
 __global__ void pack_kernel(const PackLaunch L) {
   const int lane = threadIdx.x & 31;
   const int t = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
@@ -977,7 +1118,7 @@ __global__ void pack_kernel(const PackLaunch L) {
     for (int k = lane; k < nnz; k += 32) {
       if (L.vsize == 8) reinterpret_cast<double*>(b)[k] = static_cast<const double*>(L.val)[z0 + k];
       else reinterpret_cast<float*>(b)[k] = static_cast<const float*>(L.val)[z0 + k];
-      ix[k] = L.idx[z0 + k];
+      ix[k] = pack_col(L, L.idx[z0 + k]);
     }
     return;
   }
@@ -1000,8 +1141,18 @@ __global__ void pack_kernel(const PackLaunch L) {
     const int sl = seg_slot(e, nnz);
     if (L.vsize == 8) reinterpret_cast<double*>(vb0)[sl] = static_cast<const double*>(L.val)[z0 + e];
     else reinterpret_cast<float*>(vb0)[sl] = static_cast<const float*>(L.val)[z0 + e];
-    ix[sl] = L.idx[z0 + e];
+    ix[sl] = pack_col(L, L.idx[z0 + e]);
   }
+}
+
+// hot-x selection (partition time): nonzeros per column of the rank's slice, and the slot table
+__global__ void col_degree_kernel(const int32_t* __restrict__ idx, int64_t nz, int32_t* __restrict__ deg) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nz; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(deg + idx[i], 1);
+}
+__global__ void hot_slot_kernel(const int32_t* __restrict__ hot, int nhot, int32_t* __restrict__ slot) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < nhot) slot[hot[k]] = k;
 }
 
 // --------------------------------------------------------- small kernels
@@ -1125,7 +1276,10 @@ template <typename VT>
 __global__ void cg_update_xr_kernel(VT* __restrict__ x, VT* __restrict__ r, const VT* __restrict__ p,
                                     const VT* __restrict__ ap, int64_t n, const double* sc, int par,
                                     const double* part_in, double* part_out) {
-  const double alpha = sc[par] / sum_parts(part_in);
+  // rs == 0: the previous iteration converged exactly (r = p = 0): nothing to do, no 0/0.  pAp == 0
+  // with rs > 0 is a breakdown (A not SPD) and still yields inf/NaN for the host check.
+  const double rs = sc[par], pap = sum_parts(part_in);
+  const double alpha = rs != 0.0 ? rs / pap : 0.0;
   double acc = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     x[i] = (VT)((double)x[i] + alpha * (double)p[i]);
@@ -1142,7 +1296,7 @@ template <typename VT>
 __global__ void cg_update_p_kernel(VT* __restrict__ p, const VT* __restrict__ r, int64_t n, double* sc, int par,
                                    const double* part_in) {
   const double rs_new = sum_parts(part_in);
-  const double beta = rs_new / sc[par];
+  const double beta = sc[par] != 0.0 ? rs_new / sc[par] : 0.0;   // converged exactly: p = r = 0
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = (VT)((double)r[i] + beta * (double)p[i]);
   if (blockIdx.x == 0 && threadIdx.x == 0) sc[par ^ 1] = rs_new;
@@ -1154,15 +1308,20 @@ __global__ void cg_sum_kernel(const double* part, double* out) {
   if (threadIdx.x == 0) *out = t;
 }
 
-int g_sms = 0;
+// SM count per device (a process may drive several GPUs)
+std::mutex g_kf_mu;
+int g_sms[64] = {0};
 int num_sms() {
-  if (g_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_sms <= 0) g_sms = 148;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  std::lock_guard<std::mutex> lk(g_kf_mu);
+  if (g_sms[dev] == 0) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    g_sms[dev] = v > 0 ? v : 148;
   }
-  return g_sms;
+  return g_sms[dev];
 }
 
 int elementwise_grid(int64_t n) {
@@ -1173,56 +1332,71 @@ int elementwise_grid(int64_t n) {
 
 // Per (kernel, device) launch facts, so a launch does not repeat cudaFuncSetAttribute and the
 // occupancy query (microseconds of host time that show up between back-to-back small SpMVs).
+// Every read and write of the table holds g_kf_mu (contexts may launch from several host threads).
 struct KFacts { const void* fn; int dev, smem, occ; };
-KFacts g_kf[128];
+KFacts g_kf[256];
 int g_nkf = 0;
-std::mutex g_kf_mu;
-KFacts* kfacts(const void* fn) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lk(g_kf_mu);
+// index of (fn, current device) in g_kf, created on first use; -1 if the table is full
+int kfacts_locked(const void* fn, int dev) {
   for (int i = 0; i < g_nkf; i++)
-    if (g_kf[i].fn == fn && g_kf[i].dev == dev) return &g_kf[i];
-  if (g_nkf == 128) g_nkf = 0;   // never reached with the kernels of this file; stay correct anyway
+    if (g_kf[i].fn == fn && g_kf[i].dev == dev) return i;
+  if (g_nkf == 256) return -1;   // more (kernel, device) pairs than this file has: no caching
   g_kf[g_nkf] = {fn, dev, -1, -1};
-  return &g_kf[g_nkf++];
+  return g_nkf++;
 }
 
 template <typename K>
 cudaError_t set_smem(K kernel, int bytes) {
-  KFacts* f = kfacts(reinterpret_cast<const void*>(kernel));
-  if (f->smem == bytes) return cudaSuccess;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_kf_mu);
+  const int i = kfacts_locked(reinterpret_cast<const void*>(kernel), dev);
+  if (i >= 0 && g_kf[i].smem == bytes) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e == cudaSuccess) { f->smem = bytes; f->occ = -1; }
+  if (e == cudaSuccess && i >= 0) { g_kf[i].smem = bytes; g_kf[i].occ = -1; }
   return e;
 }
 
 template <typename K>
-int grid_for(K kernel, int smem_bytes, int ntiles) {
-  KFacts* f = kfacts(reinterpret_cast<const void*>(kernel));
-  int occ = f->occ;
-  if (occ < 0) {
-    occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, WARPS * 32, smem_bytes);
-    f->occ = occ;
+int grid_for(K kernel, int smem_bytes, int ntiles, int warps = WARPS) {
+  const int sms = num_sms();
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int occ = -1;
+  {
+    std::lock_guard<std::mutex> lk(g_kf_mu);
+    const int i = kfacts_locked(reinterpret_cast<const void*>(kernel), dev);
+    if (i >= 0) occ = g_kf[i].occ;
+    if (occ < 0) {
+      occ = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, warps * 32, smem_bytes);
+      if (i >= 0) g_kf[i].occ = occ;
+    }
   }
   if (occ < 1) occ = 1;
-  const int64_t want = ((int64_t)ntiles + WARPS - 1) / WARPS;
-  const int64_t g = (int64_t)num_sms() * occ;
+  const int64_t want = ((int64_t)ntiles + warps - 1) / warps;
+  const int64_t g = (int64_t)sms * occ;
   return (int)(want < g ? (want < 1 ? 1 : want) : g);
 }
 
-template <typename VT, bool SELL, bool MIRROR, bool NA>
+template <typename VT, bool SELL, bool MIRROR, bool NA, bool HOT>
 cudaError_t launch_rows_k(const RowLaunch& L, cudaStream_t s) {
-  constexpr int b = RowLayout<VT, SELL>::TOTAL;
-  cudaError_t e = set_smem(rows_kernel<VT, SELL, MIRROR, NA>, b);
+  constexpr int b = RowLayout<VT, SELL, HOT>::TOTAL;
+  constexpr int nw = HOT ? HOT_WARPS : WARPS;
+  static_assert(b <= 227 * 1024, "rows_kernel shared memory");
+  cudaError_t e = set_smem(rows_kernel<VT, SELL, MIRROR, NA, HOT>, b);
   if (e) return e;
-  rows_kernel<VT, SELL, MIRROR, NA><<<grid_for(rows_kernel<VT, SELL, MIRROR, NA>, b, L.ntiles), WARPS * 32, b, s>>>(L);
+  rows_kernel<VT, SELL, MIRROR, NA, HOT>
+      <<<grid_for(rows_kernel<VT, SELL, MIRROR, NA, HOT>, b, L.ntiles, nw), nw * 32, b, s>>>(L);
   return cudaGetLastError();
 }
 template <typename VT, bool SELL, bool MIRROR>
 cudaError_t launch_rows_t(const RowLaunch& L, cudaStream_t s) {
-  return L.xna ? launch_rows_k<VT, SELL, MIRROR, true>(L, s) : launch_rows_k<VT, SELL, MIRROR, false>(L, s);
+  if constexpr (!SELL) {   // the hot x cache serves SEG / slab tiles (SELL launches gather through L2)
+    if (L.nhot > 0)
+      return L.xna ? launch_rows_k<VT, false, MIRROR, true, true>(L, s) : launch_rows_k<VT, false, MIRROR, false, true>(L, s);
+  }
+  return L.xna ? launch_rows_k<VT, SELL, MIRROR, true, false>(L, s) : launch_rows_k<VT, SELL, MIRROR, false, false>(L, s);
 }
 template <typename VT, bool SELL>
 cudaError_t launch_rows_m(const RowLaunch& L, cudaStream_t s) {
@@ -1239,8 +1413,7 @@ cudaError_t launch_cols_k(const ColLaunch& L, cudaStream_t s) {
   constexpr int b = CBLayout<VT>::TOTAL > MSREP_CB_SMEM_MIN ? CBLayout<VT>::TOTAL : MSREP_CB_SMEM_MIN;
   cudaError_t e = set_smem(csc_band_kernel<VT, NA>, b);
   if (e) return e;
-  const int units = L.split_items ? L.nunits : L.nb;
-  const int g = units < num_sms() ? units : num_sms();
+  const int g = L.nunits < num_sms() ? L.nunits : num_sms();
   if (g < 1) return cudaSuccess;
   csc_band_kernel<VT, NA><<<g, CB_THREADS, b, s>>>(L);
   return cudaGetLastError();
@@ -1262,7 +1435,7 @@ cudaError_t launch_rows(const RowLaunch& L, cudaStream_t s) {
 }
 
 cudaError_t launch_cols(const ColLaunch& L, cudaStream_t s) {
-  if (L.nb == 0) return cudaSuccess;
+  if (L.nunits == 0) return cudaSuccess;
   return L.dtype == 0 ? launch_cols_t<double>(L, s) : launch_cols_t<float>(L, s);
 }
 
@@ -1299,6 +1472,18 @@ cudaError_t launch_axpby_py(const double* py, void* y, int64_t n, double alpha, 
   if (n <= 0) return cudaSuccess;
   if (dtype == 0) axpby_kernel<double><<<elementwise_grid(n), 256, 0, s>>>(py, (double*)y, n, alpha, beta);
   else axpby_kernel<float><<<elementwise_grid(n), 256, 0, s>>>(py, (float*)y, n, alpha, beta);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_col_degree(const int32_t* idx, int64_t nz, int32_t* deg, cudaStream_t s) {
+  if (nz <= 0) return cudaSuccess;
+  col_degree_kernel<<<elementwise_grid(nz), 256, 0, s>>>(idx, nz, deg);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hot_slots(const int32_t* hot, int nhot, int32_t* slot, cudaStream_t s) {
+  if (nhot <= 0) return cudaSuccess;
+  hot_slot_kernel<<<(nhot + 255) / 256, 256, 0, s>>>(hot, nhot, slot);
   return cudaGetLastError();
 }
 

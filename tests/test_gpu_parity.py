@@ -189,8 +189,9 @@ def test_deterministic_and_layout_invariant(fmt):
     x = gen.vector(A["n"], 1); y = gen.vector(A["m"], 2)
     B = as_fmt(A, fmt)
     outs = run_gpu(B, fmt, x, y, 1.5, 0.5, parts=4, repeat=3)
-    if fmt in ("csr", "coo"):   # no float atomics on the row path: bit-reproducible
-        assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+    # no float atomics anywhere (pCSC split bands are reduced over their slots in slot order):
+    # every format is bit-reproducible run to run
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
     assert_close(outs[0], oracle_ref(A, x, y, 1.5, 0.5), row_bound(A, x, y, 1.5, 0.5), np.float64)
 
 
@@ -315,10 +316,25 @@ def test_suite_shapes_fp32_tolerance(shape, fmt):
     check(A, fmt, x, y, 1.5, 0.5, parts=2)
 
 
+@pytest.mark.parametrize("fmt", ["csc", "coo_col"])
+@pytest.mark.parametrize("parts", [1, 3])
+def test_csc_split_bands_reproducible(fmt, parts):
+    """Heavy bands (R-MAT's first rows; a short-wide matrix with fewer bands than SMs) are cut into
+    stage-range units whose partial rows are reduced over slots in slot order: U[-1,1) results are
+    bit-identical run to run, and within tau of the oracle."""
+    for A in (gen.rmat(16, seed=21), gen.kdistinct_csr(3000, 400_000, 300, seed=22)):
+        x = gen.vector(A["n"], 1); y = gen.vector(A["m"], 2)
+        outs = run_gpu(as_fmt(A, fmt), fmt, x, y, 1.5, 0.5, parts=parts, repeat=4)
+        for o in outs[1:]:
+            assert np.array_equal(outs[0], o)
+        assert_close(outs[0], oracle_ref(A, x, y, 1.5, 0.5), row_bound(A, x, y, 1.5, 0.5), np.float64)
+
+
 @pytest.mark.parametrize("parts", [1, 2])
 def test_csc_split_items_short_wide(parts):
-    """Fewer row bands than SMs (m = 3 bands): the pCSC split-item path (partial bands added into
-    py, then the alpha/beta epilogue) -- integer data, bit-exact; and fp32 within tolerance."""
+    """Fewer row bands than SMs (m = 3 bands): every band is cut into stage-range units whose
+    partial rows go to slots, reduced in slot order at the end of the launch -- integer data,
+    bit-exact; and fp32 within tolerance."""
     A = gen.kdistinct_csr(3 * 8192 - 5, 300_000, 40, seed=71, kind=gen.SMALLINT)
     x = gen.vector(A["n"], 72, kind=gen.SMALLINT); y = gen.vector(A["m"], 73, kind=gen.SMALLINT)
     check(A, "csc", x, y, 1.5, 0.5, parts=parts, exact=True)
@@ -479,10 +495,10 @@ def test_cg_matches_oracle(fmt, parts):
 
 
 @pytest.mark.parametrize("fmt", ["csr", "csc"])
-def test_cg_graph_matches_eager(fmt, monkeypatch):
+def test_cg_graph_matches_eager(fmt):
     """msrep_cg replays a captured CUDA graph of two iterations (single rank, device-resident);
     with even convergence checks it takes the same iterations and the same iterates, bit for
-    bit, as the eager loop (MSREP_CG_GRAPH=0)."""
+    bit, as the eager loop (msrep_set_tuning(MSREP_TUNE_CG_GRAPH, 0))."""
     import paper_2209_07552_b200 as M
     import torch
     A = _spd_stencil(14)
@@ -490,10 +506,10 @@ def test_cg_graph_matches_eager(fmt, monkeypatch):
     xs = (np.arange(m) % 5 - 2).astype(np.float64)
     b = torch.as_tensor(oracle.spmv_csr(m, A["ptr"], A["idx"], A["val"], xs, np.zeros(m), 1.0, 0.0)).cuda()
     res = []
-    for env in ("1", "0"):
-        monkeypatch.setenv("MSREP_CG_GRAPH", env)
+    for graph in (1, 0):
         B = as_fmt(A, fmt)
         ctx = M.Context(0, 1, None, 0, 2)
+        ctx.set_tuning("cg_graph", graph)
         ctx.partition(fmt, B["m"], B["n"], ptr=B["ptr"], idx=B["idx"], val=B["val"])
         xd = torch.zeros(m, dtype=torch.float64, device="cuda")
         it, rr = ctx.cg(b, xd, tol=1e-11, maxit=300, check_every=4)
@@ -512,6 +528,57 @@ def test_cg_fp32_storage():
     b = oracle.spmv_csr(m, A["ptr"], A["idx"], A["val"], xs, np.zeros(m), 1.0, 0.0)
     x, it, rr = _cg_gpu(A, "csr", b, 2, np.float32, 1e-6, 300)
     assert rr <= 1e-6 and np.max(np.abs(x - xs)) < 1e-4
+
+
+@pytest.mark.parametrize("fmt", FMTS)
+@pytest.mark.parametrize("graph", [1, 0])
+def test_cg_exact_convergence_no_nan(fmt, graph):
+    """Identity matrix: CG converges exactly in one iteration (r = p = 0 afterwards).  The extra
+    iterations the graph period / check interval run past that point must be no-ops (alpha, beta
+    guarded against 0/0), not a NaN "breakdown"."""
+    import paper_2209_07552_b200 as M
+    import torch
+    m = 5000
+    A = gen.Sparse(fmt="csr", m=m, n=m, ptr=np.arange(m + 1, dtype=np.int64), idx=np.arange(m, dtype=np.int32),
+                   val=np.ones(m))
+    B = as_fmt(A, fmt)
+    ctx = M.Context(0, 1, None, 0, 2)
+    ctx.set_tuning("cg_graph", graph)
+    if fmt in ("coo", "coo_col"):
+        ctx.partition(fmt, m, m, idx=B["idx"], val=B["val"], coo_row=coo_of_csr(B))
+    else:
+        ctx.partition(fmt, m, m, ptr=B["ptr"], idx=B["idx"], val=B["val"])
+    b = (np.arange(m) % 9 - 4).astype(np.float64)
+    xd = torch.zeros(m, dtype=torch.float64, device="cuda")
+    it, rr = ctx.cg(torch.as_tensor(b).cuda(), xd, tol=0.0, maxit=12, check_every=1)
+    assert rr == 0.0 and it >= 1
+    assert np.array_equal(xd.cpu().numpy(), b)
+    ctx.close()
+
+
+def test_binding_rejects_bad_arguments():
+    """The binding validates what it hands to the C ABI: value dtype, array lengths, and device
+    vectors (CUDA, contiguous, the partition's dtype, long enough)."""
+    import paper_2209_07552_b200 as M
+    import torch
+    A = gen.kdistinct_csr(50, 40, 3, seed=3)
+    ctx = M.Context(0, 1, None, 0, 1)
+    with pytest.raises(ValueError):
+        ctx.partition("csr", 50, 40, ptr=A["ptr"], idx=A["idx"], val=A["val"].astype(np.int64))
+    with pytest.raises(ValueError):
+        ctx.partition("csr", 50, 40, ptr=A["ptr"], idx=A["idx"], val=A["val"][:-1])
+    ctx.partition("csr", 50, 40, ptr=A["ptr"], idx=A["idx"], val=A["val"])
+    x = torch.zeros(40, dtype=torch.float64, device="cuda"); y = torch.zeros(50, dtype=torch.float64, device="cuda")
+    ctx.spmv(1.0, x, 0.0, y)
+    for bad_x, bad_y in [(x.float(), y), (x.cpu(), y), (x, y[:49]), (x, torch.zeros(100, dtype=torch.float64,
+                                                                                     device="cuda")[::2])]:
+        with pytest.raises(ValueError):
+            ctx.spmv(1.0, bad_x, 0.0, bad_y)
+    with pytest.raises(ValueError):
+        ctx.spmv_host(1.0, np.zeros(40, np.float32), 0.0, np.zeros(50))
+    with pytest.raises(M.MsrepError):
+        ctx.set_tuning("xload", 5)
+    ctx.close()
 
 
 def test_cg_errors():

@@ -12,7 +12,7 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("fmt", FMTS)
-def test_xload_policies_bit_identical(fmt, monkeypatch):
+def test_xload_policies_bit_identical(fmt):
     import paper_2209_07552_b200 as M
     cases = [gen.rmat(17, seed=111, kind=gen.SMALLINT), gen.stencil27(40, kind=gen.SMALLINT)]
     for A in cases:
@@ -20,12 +20,9 @@ def test_xload_policies_bit_identical(fmt, monkeypatch):
         x = gen.vector(A["n"], 112, kind=gen.SMALLINT); y = gen.vector(A["m"], 113, kind=gen.SMALLINT)
         ref = oracle_ref(A, x, y, 1.5, 0.5)
         picks = []
-        for forced in ("0", "1", None):
-            if forced is None:
-                monkeypatch.delenv("MSREP_XLOAD", raising=False)
-            else:
-                monkeypatch.setenv("MSREP_XLOAD", forced)
+        for forced in (0, 1, -1):
             ctx = M.Context(0, 1, None, 0, 2)
+            ctx.set_tuning("xload", forced)   # msrep_set_tuning(MSREP_TUNE_XLOAD, ...)
             got = run_gpu(as_fmt(A, fmt), fmt, x, y, 1.5, 0.5, ctx=ctx)
             picks.append(ctx.stats()["x_no_allocate"])
             ctx.close()
