@@ -57,6 +57,8 @@ def lib():
             "or_owner_linear": [I64, P, I64],
             "or_partition_ptr": [I64, P, I64, P, P],
             "or_partition_coo": [I64, I64, P, I64, P],
+            "or_partition_coo_unsorted": [I64, P, I64, P],
+            "or_exec_coo_unsorted": [I64, I64, P, P, P, I, P, P, D, D, I64],
             "or_exec_csr": [I64, P, P, P, I, P, P, D, D, I64],
             "or_exec_coo": [I64, I64, P, P, P, I, P, P, D, D, I64],
             "or_exec_csc": [I64, I64, P, P, P, I, P, P, D, D, I64],
@@ -281,6 +283,24 @@ def exec_coo(m, row_idx, col_idx, val, x, y, alpha, beta, np_):
     val = np.ascontiguousarray(val); x = _c(x, val.dtype); out = np.array(y, dtype=val.dtype, copy=True)
     lib().or_exec_coo(m, row_idx.size, _p(row_idx), _p(col_idx), _p(val), _dt(val), _p(x), _p(out),
                       alpha, beta, np_)
+    return out
+
+
+def partition_coo_unsorted(row_idx, np_):
+    """Unsorted COO (Sec. 3.2.3): nnz split by position; per part its smallest and
+    largest row, no flag, no owned rows."""
+    row_idx = _c(row_idx, np.int64)
+    parts = np.zeros(np_, PART_DTYPE)
+    lib().or_partition_coo_unsorted(row_idx.size, _p(row_idx), np_, _p(parts))
+    return parts
+
+
+def exec_coo_unsorted(m, row_idx, col_idx, val, x, y, alpha, beta, np_):
+    """Unsorted pCOO: per-part full-length partial y, summed in part order (column-style merge)."""
+    row_idx = _c(row_idx, np.int64); col_idx = _c(col_idx, np.int32)
+    val = np.ascontiguousarray(val); x = _c(x, val.dtype); out = np.array(y, dtype=val.dtype, copy=True)
+    lib().or_exec_coo_unsorted(m, row_idx.size, _p(row_idx), _p(col_idx), _p(val), _dt(val), _p(x), _p(out),
+                               alpha, beta, np_)
     return out
 
 

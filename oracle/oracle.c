@@ -433,6 +433,53 @@ void or_exec_coo(int64_t m, int64_t nnz, const int64_t *row_idx, const int32_t *
     free(sum); free(parts);
 }
 
+/* Unsorted COO (Sec. 3.2.3): "if the elements are unsorted ... elements in a
+ * particular partition can spread among the entire matrix".  The nnz split is by position in the
+ * given triplet order (Alg. 6 l.2-3, b_i = floor(i*nnz/np)); a part's rows are not contiguous, so
+ * its descriptor reports the smallest and largest row it touches (reading R25), no flag and no
+ * owned rows, and -- as the paper says for this case -- the merge is the column-style one: every
+ * part produces a full-length partial y (like pCSC), summed in part order. */
+void or_partition_coo_unsorted(int64_t nnz, const int64_t *row_idx, int64_t np, or_part *parts)
+{
+    int64_t *b = (int64_t *)malloc((size_t)(np + 1) * sizeof(int64_t));
+    or_nnz_boundaries(nnz, np, b);
+    for (int64_t i = 0; i < np; i++) {
+        or_part *p = &parts[i];
+        p->start_idx = b[i];
+        p->end_idx = b[i + 1] - 1;
+        p->pad_ = 0;
+        p->start_flag = 0;
+        p->owned_begin = 0;
+        p->owned_end = 0;
+        p->start_row = -1;
+        p->end_row = -1;
+        for (int64_t k = b[i]; k < b[i + 1]; k++) {
+            if (p->start_row < 0 || row_idx[k] < p->start_row) p->start_row = row_idx[k];
+            if (p->end_row < 0 || row_idx[k] > p->end_row) p->end_row = row_idx[k];
+        }
+    }
+    free(b);
+}
+
+void or_exec_coo_unsorted(int64_t m, int64_t nnz, const int64_t *row_idx, const int32_t *col_idx,
+                          const void *val, int dtype, const void *x, void *y,
+                          double alpha, double beta, int64_t np)
+{
+    or_part *parts = (or_part *)malloc((size_t)np * sizeof(or_part));
+    or_partition_coo_unsorted(nnz, row_idx, np, parts);
+    double *sum_y = (double *)calloc((size_t)(m > 0 ? m : 1), sizeof(double));
+    double *py = (double *)malloc((size_t)(m > 0 ? m : 1) * sizeof(double));
+    for (int64_t i = 0; i < np; i++) {
+        for (int64_t r = 0; r < m; r++) py[r] = 0.0;
+        if (alpha != 0.0)
+            for (int64_t k = parts[i].start_idx; k <= parts[i].end_idx; k++)
+                py[row_idx[k]] = py[row_idx[k]] + get_val(val, dtype, k) * get_val(x, dtype, col_idx[k]);
+        for (int64_t r = 0; r < m; r++) sum_y[r] = sum_y[r] + py[r];   /* sum_y += py[i] */
+    }
+    for (int64_t r = 0; r < m; r++) put_val(y, dtype, r, finish(alpha, sum_y[r], beta, y, dtype, r));
+    free(py); free(sum_y); free(parts);
+}
+
 /* Column format (pCSC, Alg. 5; Sec. 4.3): part i
  * scatters its columns' nonzeros into its own full-length py_i; the merge is
  * sum_y = sum_i py_i (part order), y = alpha*sum_y + beta*y_in. */

@@ -611,3 +611,62 @@ def test_partition_roundtrip_exhaustive_5x5():
             _check_roundtrip(m, rp, np_)
             count += 1
     assert count == sum(6 ** m * (2.5 * m + 2) for m in range(1, 6)) == 130635   # sum of (nnz + 2)
+
+
+# ------------------------------------------------------------ unsorted pCOO
+def test_unsorted_coo_fixture_E_hand_worked():
+    """Fixture E's triplets in the order (3,3,5) (0,2,2) (1,1,3) (0,0,1) (3,0,4), np = 2: the nnz
+    split by position gives parts {0,1} and {2,3,4}; both touch rows 0..3 (reading R25: smallest and
+    largest row, no flag, no owned rows).  Partial vectors (x = 1): part 0 -> [2,0,0,5], part 1 ->
+    [1,3,0,4]; their sum is the plain SpMV [3,3,0,9] (worked by hand from S:96)."""
+    r = np.array([3, 0, 1, 0, 3]); c = np.array([3, 2, 1, 0, 0], np.int32); v = np.array([5.0, 2, 3, 1, 4])
+    parts = oracle.partition_coo_unsorted(r, 2)
+    assert parts["start_idx"].tolist() == [0, 2] and parts["end_idx"].tolist() == [1, 4]
+    assert parts["start_row"].tolist() == [0, 0] and parts["end_row"].tolist() == [3, 3]
+    assert parts["start_flag"].tolist() == [0, 0] and parts["owned_end"].tolist() == [0, 0]
+    assert oracle.exec_coo_unsorted(4, r, c, v, np.ones(4), np.zeros(4), 1.0, 0.0, 2).tolist() == [3, 3, 0, 9]
+    # part 0 alone (its two triplets) is the partial vector [2, 0, 0, 5]
+    assert oracle.exec_coo_unsorted(4, r[:2], c[:2], v[:2], np.ones(4), np.zeros(4), 1.0, 0.0, 1).tolist() == [2, 0, 0, 5]
+    # beta applied once: alpha 2, beta 10, y 1 -> [16, 16, 10, 28] (S:97)
+    assert oracle.exec_coo_unsorted(4, r, c, v, np.ones(4), np.ones(4), 2.0, 10.0, 5).tolist() == [16, 16, 10, 28]
+
+
+def test_unsorted_coo_partition_brute_force():
+    """Descriptors = positions b_i = floor(i*nnz/np) and the min / max row of each slice (numpy);
+    empty parts have rows -1."""
+    rng = np.random.default_rng(44)
+    for trial in range(200):
+        nnz = int(rng.integers(0, 60))
+        r = rng.integers(0, 30, nnz)
+        np_ = int(rng.integers(1, nnz + 4))
+        parts = oracle.partition_coo_unsorted(r, np_)
+        b = [(i * nnz) // np_ for i in range(np_ + 1)]
+        for i, p in enumerate(parts):
+            assert p["start_idx"] == b[i] and p["end_idx"] == b[i + 1] - 1
+            sl = r[b[i]:b[i + 1]]
+            assert (p["start_row"], p["end_row"]) == ((sl.min(), sl.max()) if sl.size else (-1, -1))
+            assert p["start_flag"] == 0 and p["owned_begin"] == 0 and p["owned_end"] == 0
+
+
+def test_unsorted_coo_exec_permutation_invariant_and_dense():
+    """Any triplet order, any np: the unsorted executor equals the sorted-COO SpMV bit for bit on
+    small-integer data (every sum exact) and the numpy dense product within tau on U[-1,1)."""
+    rng = np.random.default_rng(45)
+    for trial in range(40):
+        m, n = (int(t) for t in rng.integers(1, 65, 2))
+        r, c, _ = random_matrix(rng, m, n, [0.02, 0.2, 0.5][trial % 3])
+        ints = trial % 2 == 0
+        v = rng.integers(-4, 5, r.size).astype(np.float64) if ints else rng.uniform(-1, 1, r.size)
+        x = rng.integers(-4, 5, n).astype(np.float64) if ints else rng.uniform(-1, 1, n)
+        y = rng.integers(-4, 5, m).astype(np.float64) if ints else rng.uniform(-1, 1, m)
+        perm = rng.permutation(r.size)
+        ru, cu, vu = r[perm], c[perm].astype(np.int32), v[perm]
+        A = dense_of(m, n, r, c, v)
+        for alpha, beta in [(1.0, 0.0), (2.0, 0.5), (-1.0, 1.0), (0.0, 2.0)]:
+            ref = oracle.spmv_coo(m, r, c, v, x, y, alpha, beta)
+            np_ = int(rng.integers(1, 10))
+            got = oracle.exec_coo_unsorted(m, ru, cu, vu, x, y, alpha, beta, np_)
+            if ints:
+                assert np.array_equal(got, ref), (trial, alpha, beta, np_)
+            bound = abs(alpha) * (np.abs(A) @ np.abs(x)) + np.abs(beta * y)
+            assert np.all(np.abs(got - (alpha * (A @ x) + beta * y)) <= 1e-13 * bound + 1e-300)
