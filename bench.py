@@ -54,8 +54,12 @@ def parse(argv=None):
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--parts-per-rank", type=int, default=1)
-    p.add_argument("--hot-x", type=int, default=-1, choices=[-1, 0, 1],
-                   help="MSREP_TUNE_HOT_X: shared-memory hot-x cache (-1 auto, 0 off, 1 on)")
+    p.add_argument("--hot-x", type=int, default=-1,
+                   help="MSREP_TUNE_HOT_X: shared-memory hot-x cache (-1 auto, 0 off, 1 on, k > 1: k KiB)")
+    p.add_argument("--compact-x", type=int, default=-1, choices=[-1, 0, 1],
+                   help="MSREP_TUNE_COMPACT_X: gather the rank's distinct x entries first (-1 auto, 0 off, 1 on)")
+    p.add_argument("--hot-cluster", type=int, default=1, choices=[1, 2],
+                   help="MSREP_TUNE_HOT_CLUSTER: CTAs sharing one hot-x cache over DSMEM")
     p.add_argument("--xload", type=int, default=-1, choices=[-1, 0, 1],
                    help="MSREP_TUNE_XLOAD: x-gather L1 policy (-1 timed at partition, 0 allocate, 1 no_allocate)")
     p.add_argument("--fused", action="store_true",
@@ -364,6 +368,8 @@ def main():
         ctx = M.Context(0, 1, None, local, ppr)
     ctx.set_tuning("hot_x", a.hot_x)
     ctx.set_tuning("xload", a.xload)
+    ctx.set_tuning("compact_x", a.compact_x)
+    ctx.set_tuning("hot_cluster", a.hot_cluster)
     local_gen = rank_local_ok(a)
     A = None
     if local_gen:
@@ -563,7 +569,7 @@ def main():
             "partition_ms": st["partition_ms"],
             "stats_rank0": {k: st[k] for k in ("nnz_rank", "ntiles", "nsell", "nslabs", "nsplit_rows",
                                                "distinct_cols", "kernels_per_spmv", "tile_bytes", "x_no_allocate",
-                                               "nhot", "hot_nnz")},
+                                               "nhot", "hot_nnz", "x_compact")},
         }
         print(json.dumps(out), flush=True)
     ctx.close()

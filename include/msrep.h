@@ -44,8 +44,16 @@ typedef struct msrep_ctx_s* msrep_ctx;
  * MSREP_COO_COL is a COO sorted by column (ties by row), the variant the paper
  * describes and defers (merged "like pCSC", P:597 Fig. col-gather):
  * Alg. 6 runs on the column ids, parts own column ranges, partial y vectors
- * are summed (reduce-scatter).  It uses the pCSC kernel. */
-typedef enum { MSREP_CSR = 0, MSREP_CSC = 1, MSREP_COO = 2, MSREP_COO_COL = 3 } msrep_format;
+ * are summed (reduce-scatter).  It uses the pCSC kernel.
+ * MSREP_COO_UNSORTED is a COO in any order ("if the elements are
+ * unsorted ... elements in a particular partition can spread among the entire
+ * matrix"): coo_row = row_idx, idx = col_idx.  The nnz split is by position;
+ * a part's descriptor carries its smallest / largest row (DESIGN.md reading
+ * R25), no flag, no owned rows; each rank sorts its own triplets by column at
+ * partition time and runs the pCSC kernel, and the partial y vectors are
+ * merged column-style (reduce-scatter; layouts REPLICATED / SHARDED).  Split:
+ * nnz or two-level (no row blocks). */
+typedef enum { MSREP_CSR = 0, MSREP_CSC = 1, MSREP_COO = 2, MSREP_COO_COL = 3, MSREP_COO_UNSORTED = 4 } msrep_format;
 
 typedef enum { MSREP_F64 = 0, MSREP_F32 = 1 } msrep_dtype;
 
@@ -132,6 +140,7 @@ typedef struct {
                                 both ways on the built layout, or set by MSREP_TUNE_XLOAD)    */
   int64_t nhot;              /* hot-x cache entries (MSREP_TUNE_HOT_X; 0: no cache)          */
   int64_t hot_nnz;           /* nonzeros whose x gather the hot cache serves                 */
+  int64_t x_compact;         /* compact-x entries (MSREP_TUNE_COMPACT_X; 0: gathers read x)   */
   int64_t stream_bytes;      /* bytes the built layout moves per SpMV (beta != 0): tile blobs
                                 as stored + x entries + y; pCOO stores u8 tile row keys, not
                                 the 4-B row ids alg_bytes counts                              */
@@ -159,6 +168,7 @@ msrep_status_t msrep_create(msrep_ctx* out, int rank, int nranks, const uint8_t 
  *   COO: ptr = NULL,         idx = col_idx[nnz], coo_row = row_idx[nnz] (row-sorted)
  *   COO_COL: ptr = NULL,     idx = row_idx[nnz], coo_row = col_idx[nnz] (column-sorted:
  *            coo_row carries the sorted major index)
+ *   COO_UNSORTED: ptr = NULL, idx = col_idx[nnz], coo_row = row_idx[nnz], any order
  *   val = [nnz] of dtype.
  * All host arrays are borrowed read-only for the duration of the call (the
  * call synchronises `stream` before returning).  parts_out, if not NULL,
@@ -241,9 +251,21 @@ msrep_status_t msrep_set_residency(msrep_ctx ctx, msrep_residency residency, int
  *                       the row formats, applied by the next
  *                       msrep_partition: -1 (default) when the top columns hold
  *                       enough of the rank's nonzeros, 0 off, 1 on whenever
- *                       any column qualifies.
+ *                       any column qualifies, 2..96: on with a cache of that
+ *                       many KiB (default size 32 KiB; auto: fp64 only).
+ *   MSREP_TUNE_COMPACT_X compact x for the row formats, applied by the next
+ *                       msrep_partition: the tiles index the rank's distinct
+ *                       columns and every SpMV first gathers x' = x[cols]
+ *                       (one launch): -1 (default) when x is >= 32 MB, 0 off, 1 on.
+ *   MSREP_TUNE_HOT_CLUSTER CTAs sharing one hot-x cache, applied by the next
+ *                       msrep_partition: 1 (default) -- every CTA holds the
+ *                       whole cache; 2 -- the kernel runs as CTA pairs
+ *                       (thread-block clusters) and each CTA holds half of the
+ *                       hot entries, read by its partner over distributed shared
+ *                       memory (twice the entries, but measured slower on R-MAT).
  * Errors: MSREP_ERR_INVALID_ARG (unknown knob or value). */
-typedef enum { MSREP_TUNE_XLOAD = 0, MSREP_TUNE_CG_GRAPH = 1, MSREP_TUNE_HOT_X = 2 } msrep_tuning;
+typedef enum { MSREP_TUNE_XLOAD = 0, MSREP_TUNE_CG_GRAPH = 1, MSREP_TUNE_HOT_X = 2, MSREP_TUNE_COMPACT_X = 3,
+               MSREP_TUNE_HOT_CLUSTER = 4 } msrep_tuning;
 msrep_status_t msrep_set_tuning(msrep_ctx ctx, msrep_tuning knob, int value);
 
 /* Select the split used by the next msrep_partition on this context (default

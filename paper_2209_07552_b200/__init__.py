@@ -23,7 +23,7 @@ if not os.path.exists(LIB_PATH):
 _lib = ctypes.CDLL(LIB_PATH)
 
 # enums (include/msrep.h)
-CSR, CSC, COO, COO_COL = 0, 1, 2, 3
+CSR, CSC, COO, COO_COL, COO_UNSORTED = 0, 1, 2, 3, 4
 SPLIT_NNZ, SPLIT_BLOCK, SPLIT_TWO_LEVEL = 0, 1, 2
 SPLITS = {"nnz": SPLIT_NNZ, "block": SPLIT_BLOCK}
 F64, F32 = 0, 1
@@ -33,9 +33,10 @@ RESIDENCY = {"device": RESIDENT_DEVICE, "host": RESIDENT_HOST}
 STATUS = {0: "MSREP_OK", 1: "MSREP_ERR_INVALID_ARG", 2: "MSREP_ERR_DIM_MISMATCH", 3: "MSREP_ERR_UNSORTED_COO",
           4: "MSREP_ERR_TOO_LARGE", 5: "MSREP_ERR_STATE", 6: "MSREP_ERR_OOM", 7: "MSREP_ERR_CUDA",
           8: "MSREP_ERR_NCCL"}
-FORMATS = {"csr": CSR, "csc": CSC, "coo": COO, "coo_col": COO_COL}
-TUNE_XLOAD, TUNE_CG_GRAPH, TUNE_HOT_X = 0, 1, 2
-TUNING = {"xload": TUNE_XLOAD, "cg_graph": TUNE_CG_GRAPH, "hot_x": TUNE_HOT_X}
+FORMATS = {"csr": CSR, "csc": CSC, "coo": COO, "coo_col": COO_COL, "coo_unsorted": COO_UNSORTED}
+TUNE_XLOAD, TUNE_CG_GRAPH, TUNE_HOT_X, TUNE_COMPACT_X, TUNE_HOT_CLUSTER = 0, 1, 2, 3, 4
+TUNING = {"xload": TUNE_XLOAD, "cg_graph": TUNE_CG_GRAPH, "hot_x": TUNE_HOT_X, "compact_x": TUNE_COMPACT_X,
+          "hot_cluster": TUNE_HOT_CLUSTER}
 
 
 class PartDesc(ctypes.Structure):
@@ -58,7 +59,8 @@ class Stats(ctypes.Structure):
                                          ("phase_ms", ctypes.c_double * 4), ("residency", ctypes.c_int64),
                                          ("nchunks", ctypes.c_int64), ("host_bytes", ctypes.c_int64),
                                          ("x_no_allocate", ctypes.c_int64), ("nhot", ctypes.c_int64),
-                                         ("hot_nnz", ctypes.c_int64), ("stream_bytes", ctypes.c_int64)]
+                                         ("hot_nnz", ctypes.c_int64), ("x_compact", ctypes.c_int64),
+                                         ("stream_bytes", ctypes.c_int64)]
 
 
 class Allocator(ctypes.Structure):

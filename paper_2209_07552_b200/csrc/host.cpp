@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -62,9 +63,10 @@ constexpr int64_t kMaxIdx = (int64_t)1 << 31;
 
 // column-wise formats merge partial y vectors (pCSC, column-sorted pCOO); COO formats carry
 // their sorted major index (row ids, or column ids for MSREP_COO_COL) in `coo_row`
-inline bool colwise(msrep_format f) { return f == MSREP_CSC || f == MSREP_COO_COL; }
-inline bool coo_like(msrep_format f) { return f == MSREP_COO || f == MSREP_COO_COL; }
+inline bool colwise(msrep_format f) { return f == MSREP_CSC || f == MSREP_COO_COL || f == MSREP_COO_UNSORTED; }
+inline bool coo_like(msrep_format f) { return f == MSREP_COO || f == MSREP_COO_COL || f == MSREP_COO_UNSORTED; }
 constexpr int64_t kMaxRankNnz = kMaxIdx - (1 << 16);
+constexpr int64_t COMPACT_X_MIN_BYTES = (int64_t)32 << 20;   // auto compact x when x is >= 32 MB (L2 126 MB)
 
 // ------------------------------------------------------------ descriptors
 // Part boundaries b[0..np]: the nnz split b_i = floor(i*nnz/np) (Alg. 2 l.2-3,
@@ -133,6 +135,28 @@ void plan_coo(int64_t m, int np, const int32_t* row, const std::vector<int64_t>&
     d.start_row = row[b0];
     d.end_row = row[b1 - 1];
     d.start_flag = (b0 > 0 && row[b0 - 1] == row[b0]) ? 1 : 0;
+  }
+}
+
+// Unsorted COO (Sec. 3.2.3; reading R25): parts are position ranges of the triplet
+// list; a part reports the smallest and largest row it touches, no flag, no owned rows (its
+// partial y spans the matrix and is merged column-style).
+void plan_coo_unsorted(int np, const int32_t* row, const std::vector<int64_t>& b, msrep_part_desc* P) {
+  for (int i = 0; i < np; i++) {
+    const int64_t b0 = b[(size_t)i], b1 = b[(size_t)i + 1];
+    msrep_part_desc& d = P[i];
+    d.start_idx = b0;
+    d.end_idx = b1 - 1;
+    d.reserved = 0;
+    d.start_flag = 0;
+    d.owned_begin = d.owned_end = 0;
+    int64_t lo = -1, hi = -1;
+    for (int64_t k = b0; k < b1; k++) {
+      if (lo < 0 || row[k] < lo) lo = row[k];
+      if (hi < 0 || row[k] > hi) hi = row[k];
+    }
+    d.start_row = lo;
+    d.end_row = hi;
   }
 }
 
@@ -237,6 +261,13 @@ struct Ctx {
   int32_t* d_hot = nullptr;         // hot-x columns by slot (row formats, device-resident)
   int nhot = 0;
   int64_t hot_nnz = 0;              // the rank's nonzeros whose x comes from the hot cache
+  int64_t nxc = 0;                  // compact x entries (0: the kernels gather from x itself)
+  int hot_cluster = 1;              // the partition's hot-x sharing (tune_hot_cluster when built)
+  int32_t* d_xcols = nullptr;       // the rank's distinct columns, ascending (compact x -> column)
+  void* d_xc = nullptr;             // x' = x[d_xcols], gathered at the start of every SpMV
+  void* d_xc_mm = nullptr;          // SpMM: X' (nxc x 8 entries), allocated on first use
+  int tune_compact = -1;
+  int tune_hot_cluster = 1;         // CTAs of a cluster sharing one hot-x cache over DSMEM (1 or 2)
   bool split_launch = false;        // SELL tiles and SEG tiles run as two launches (each >= 5-10 % of nnz)
   int residency = MSREP_RESIDENT_DEVICE;
   int64_t chunk_bytes = (int64_t)256 << 20;
@@ -330,6 +361,9 @@ void free_all(Ctx* c) {
   c->d_hot = nullptr;
   c->nhot = 0;
   c->hot_nnz = 0;
+  c->nxc = 0;
+  c->d_xcols = nullptr;
+  c->d_xc = c->d_xc_mm = nullptr;
   c->d_cg_r = c->d_cg_p = c->d_cg_ap = nullptr;
   c->d_cg_part = c->d_cg_sc = nullptr;
   c->mm_k = 0;
@@ -978,8 +1012,21 @@ RowLaunch row_launch(const Ctx* c, const void* x, void* y, double alpha, double 
   L.alpha = alpha; L.beta = beta; L.rec = c->d_rec;
   L.dtype = c->dtype == MSREP_F64 ? 0 : 1; L.has_sell = c->nsell > 0;
   L.xna = c->xna;
-  L.hot = c->d_hot; L.nhot = c->nhot;
+  L.hot = c->d_hot; L.nhot = c->nhot; L.hot_cluster = c->hot_cluster;
+  if (c->nxc) { L.x = c->d_xc; L.xmax = (uint32_t)(c->nxc - 1); }   // the SpMV gathers x' first (prepare_x)
   return L;
+}
+
+// compact x: x' = x[xcols] (k-wide rows for SpMM) on s, before the tile kernel that reads it
+msrep_status_t prepare_x(Ctx* c, const void* x, int k, cudaStream_t s) {
+  if (!c->nxc) return MSREP_OK;
+  void* dst = c->d_xc;
+  if (k > 1) {
+    if (!c->d_xc_mm) TRY(dalloc(c, (size_t)c->nxc * 8 * vsz(c->dtype), &c->d_xc_mm, s));
+    dst = c->d_xc_mm;
+  }
+  CUDA_TRY(launch_gather_x(x, c->d_xcols, c->nxc, k, dst, c->dtype == MSREP_F64 ? 0 : 1, s));
+  return MSREP_OK;
 }
 ColLaunch col_launch(const Ctx* c, const void* x, void* y, double alpha, double beta) {
   ColLaunch L{};
@@ -1117,7 +1164,12 @@ msrep_status_t msrep_plan_split(msrep_format fmt, msrep_split split, int64_t out
   if (np < 1 || outer < 0 || nnz < 0 || !parts_out) return fail(MSREP_ERR_INVALID_ARG, "bad plan arguments");
   if (split != MSREP_SPLIT_NNZ && split != MSREP_SPLIT_BLOCK) return fail(MSREP_ERR_INVALID_ARG, "unknown split %d", (int)split);
   std::vector<int64_t> b;
-  if (coo_like(fmt)) {
+  if (fmt == MSREP_COO_UNSORTED) {   // positions only; coo_row = the row of each triplet
+    if (nnz > 0 && !coo_row) return fail(MSREP_ERR_INVALID_ARG, "unsorted COO plan needs row_idx");
+    if (split != MSREP_SPLIT_NNZ) return fail(MSREP_ERR_INVALID_ARG, "unsorted COO takes the nnz split only");
+    split_bounds(fmt, split, outer, nnz, np, nullptr, nullptr, b);
+    plan_coo_unsorted(np, coo_row, b, parts_out);
+  } else if (coo_like(fmt)) {
     if (nnz > 0 && !coo_row) return fail(MSREP_ERR_INVALID_ARG, "COO plan needs its sorted major index");
     split_bounds(fmt, split, outer, nnz, np, nullptr, coo_row, b);
     plan_coo(outer, np, coo_row, b, parts_out);
@@ -1190,8 +1242,17 @@ msrep_status_t msrep_set_tuning(msrep_ctx h, msrep_tuning knob, int value) {
       if (value < 0 || value > 1) return fail(MSREP_ERR_INVALID_ARG, "MSREP_TUNE_CG_GRAPH %d (0, 1)", value);
       c->tune_cg_graph = value;
       return MSREP_OK;
+    case MSREP_TUNE_COMPACT_X:
+      if (value < -1 || value > 1) return fail(MSREP_ERR_INVALID_ARG, "MSREP_TUNE_COMPACT_X %d (-1, 0, 1)", value);
+      c->tune_compact = value;
+      return MSREP_OK;
+    case MSREP_TUNE_HOT_CLUSTER:
+      if (value != 1 && value != 2) return fail(MSREP_ERR_INVALID_ARG, "MSREP_TUNE_HOT_CLUSTER %d (1, 2)", value);
+      c->tune_hot_cluster = value;
+      return MSREP_OK;
     case MSREP_TUNE_HOT_X:
-      if (value < -1 || value > 1) return fail(MSREP_ERR_INVALID_ARG, "MSREP_TUNE_HOT_X %d (-1, 0, 1)", value);
+      if (value < -1 || value > HOT_BYTES / 1024)
+        return fail(MSREP_ERR_INVALID_ARG, "MSREP_TUNE_HOT_X %d (-1, 0, 1, or 2..%d KiB)", value, HOT_BYTES / 1024);
       c->tune_hot = value;
       return MSREP_OK;
   }
@@ -1328,14 +1389,23 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     tl = now;
   };
   // ---- validation (before any device work)
-  if (fmt != MSREP_CSR && fmt != MSREP_CSC && fmt != MSREP_COO && fmt != MSREP_COO_COL)
+  if (fmt != MSREP_CSR && fmt != MSREP_CSC && fmt != MSREP_COO && fmt != MSREP_COO_COL && fmt != MSREP_COO_UNSORTED)
     return fail(MSREP_ERR_INVALID_ARG, "format %d", (int)fmt);
+  if (fmt == MSREP_COO_UNSORTED && c->split == MSREP_SPLIT_BLOCK)
+    return fail(MSREP_ERR_INVALID_ARG, "unsorted COO has no row blocks: use the nnz (or two-level) split");
   if (dtype != MSREP_F64 && dtype != MSREP_F32) return fail(MSREP_ERR_INVALID_ARG, "dtype %d", (int)dtype);
   if (m < 0 || n < 0 || nnz < 0) return fail(MSREP_ERR_INVALID_ARG, "negative dimension");
   if (m >= kMaxIdx || n >= kMaxIdx) return fail(MSREP_ERR_TOO_LARGE, "m, n must be < 2^31");
   if (nnz > 0 && (!idx || !val)) return fail(MSREP_ERR_INVALID_ARG, "idx/val NULL");
   const int64_t outer = colwise(fmt) ? n : m, inner = colwise(fmt) ? m : n;
-  if (coo_like(fmt)) {
+  if (fmt == MSREP_COO_UNSORTED) {   // any order: only the index ranges are checked
+    if (nnz > 0 && !coo_row) return fail(MSREP_ERR_INVALID_ARG, "unsorted COO needs row_idx (coo_row)");
+    int code = 0;
+    const int64_t k = par_first_bad(nnz, &code, [&](int64_t q) -> int {
+      return (coo_row[q] < 0 || coo_row[q] >= m) ? 1 : ((idx[q] < 0 || idx[q] >= n) ? 2 : 0);
+    });
+    if (k >= 0) return fail(MSREP_ERR_DIM_MISMATCH, "%s index [%lld] out of range", code == 1 ? "row" : "column", (long long)k);
+  } else if (coo_like(fmt)) {
     if (nnz > 0 && !coo_row) return fail(MSREP_ERR_INVALID_ARG, "COO needs its sorted major index (coo_row)");
     const char* what = fmt == MSREP_COO ? "(row, col)" : "(col, row)";
     int code = 0;
@@ -1357,7 +1427,8 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   std::vector<msrep_part_desc> parts((size_t)c->np);
   std::vector<int64_t> bnd;
   split_bounds(fmt, c->split, outer, nnz, c->np, ptr, coo_row, bnd, &c->groups);
-  if (coo_like(fmt)) plan_coo(outer, c->np, coo_row, bnd, parts.data());
+  if (fmt == MSREP_COO_UNSORTED) plan_coo_unsorted(c->np, coo_row, bnd, parts.data());
+  else if (coo_like(fmt)) plan_coo(outer, c->np, coo_row, bnd, parts.data());
   else plan_ptr(outer, c->np, ptr, bnd, parts.data());
   lap(1);
   const int P0 = c->rank * c->vparts, P1 = P0 + c->vparts;
@@ -1365,9 +1436,9 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   if (B_hi - B_lo >= kMaxRankNnz) return fail(MSREP_ERR_TOO_LARGE, "rank holds %lld nonzeros (>= 2^31 - 2^16)", (long long)(B_hi - B_lo));
   {
     int code = 0;
-    const int64_t k = par_first_bad(B_hi - B_lo, &code, [&](int64_t q) -> int {
+    const int64_t k = fmt == MSREP_COO_UNSORTED ? -1 : par_first_bad(B_hi - B_lo, &code, [&](int64_t q) -> int {
       return (idx[B_lo + q] < 0 || idx[B_lo + q] >= inner) ? 1 : 0;
-    });
+    });   // (unsorted COO: both indices were range-checked above)
     if (k >= 0) return fail(MSREP_ERR_DIM_MISMATCH, "index %lld out of range", (long long)(B_lo + k));
   }
   lap(0);
@@ -1385,12 +1456,45 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   // ---- window and local pointer (clamped form of Alg. 2 l.11-12, reading R5)
   const size_t V = vsz(dtype);
   std::vector<int64_t> lp;
+  // unsorted COO: this rank's triplets, stably counting-sorted by column, are a column-sorted COO
+  // slice; from here on the rank builds the same band layout as MSREP_COO_COL (the partial y of
+  // its parts spans the matrix and is merged column-style)
+  std::vector<int32_t> us_col, us_row;
+  std::unique_ptr<char[]> us_val;
+  if (fmt == MSREP_COO_UNSORTED) {
+    const int64_t nzr = B_hi - B_lo;
+    int64_t cmin = n, cmax = -1;
+    for (int64_t k = B_lo; k < B_hi; k++) { cmin = std::min<int64_t>(cmin, idx[k]); cmax = std::max<int64_t>(cmax, idx[k]); }
+    us_col.resize((size_t)nzr);
+    us_row.resize((size_t)nzr);
+    us_val.reset(new char[(size_t)std::max<int64_t>(1, nzr) * V]);
+    if (nzr > 0) {
+      std::vector<int64_t> cnt((size_t)(cmax - cmin + 2), 0);
+      for (int64_t k = B_lo; k < B_hi; k++) cnt[(size_t)(idx[k] - cmin + 1)]++;
+      for (size_t q = 1; q < cnt.size(); q++) cnt[q] += cnt[q - 1];
+      for (int64_t k = B_lo; k < B_hi; k++) {
+        const int64_t d = cnt[(size_t)(idx[k] - cmin)]++;
+        us_col[(size_t)d] = idx[k];
+        us_row[(size_t)d] = coo_row[k];
+        memcpy(us_val.get() + (size_t)d * V, static_cast<const char*>(val) + (size_t)k * V, V);
+      }
+    }
+    // global-position views: position B_lo + q of the views is element q of the sorted slice
+    coo_row = reinterpret_cast<const int32_t*>(reinterpret_cast<uintptr_t>(us_col.data()) - (uintptr_t)B_lo * 4);
+    idx = reinterpret_cast<const int32_t*>(reinterpret_cast<uintptr_t>(us_row.data()) - (uintptr_t)B_lo * 4);
+    val = reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(us_val.get()) - (uintptr_t)B_lo * V);
+    fmt = MSREP_COO_COL;   // the rank's layout (c->fmt keeps MSREP_COO_UNSORTED)
+  }
   if (colwise(fmt)) {
     int64_t lo = -1, hi = -1;
-    for (int j = P0; j < P1; j++) {
-      if (parts[(size_t)j].start_idx > parts[(size_t)j].end_idx) continue;
-      if (lo < 0) lo = parts[(size_t)j].start_row;
-      hi = parts[(size_t)j].end_row + 1;
+    if (c->fmt == MSREP_COO_UNSORTED) {   // the column window of the sorted slice
+      if (B_hi > B_lo) { lo = coo_row[B_lo]; hi = (int64_t)coo_row[B_hi - 1] + 1; }
+    } else {
+      for (int j = P0; j < P1; j++) {
+        if (parts[(size_t)j].start_idx > parts[(size_t)j].end_idx) continue;
+        if (lo < 0) lo = parts[(size_t)j].start_row;
+        hi = parts[(size_t)j].end_row + 1;
+      }
     }
     if (lo < 0) lo = hi = 0;
     c->wlo = lo; c->whi = hi;
@@ -1627,14 +1731,22 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     int32_t* d_blob16;
     TRY(upload(c, reinterpret_cast<const int4*>(S.tiles.data()), nt, &d_tiles_orig, s));
     TRY(upload_vec(c, blob16, &d_blob16, s));
-    // ---- hot x (device-resident row layouts whose SEG / slab tiles run in the SEG instantiation):
-    // the rank's most-gathered columns get slots in a shared-memory copy of x
-    std::vector<int32_t> hot;
-    int32_t* d_hotslot = nullptr;
+    // ---- x layout of the rank (device-resident row formats):
+    //  * compact x: the rank's distinct columns in column order; the tiles carry compact column ids
+    //    and every SpMV first gathers x' = x[cols] (one sequential pass over x), so the gathers hit
+    //    an x' that fits in L2 next to the matrix stream instead of the whole x;
+    //  * hot x: the most-gathered columns get slots in a shared-memory copy of x' per CTA; SEG / slab
+    //    tiles carry HOT_TAG | slot for them (the SELL instantiation has no hot path).
+    std::vector<int32_t> hot, xcols;
+    int32_t *d_hotslot = nullptr, *d_colmap = nullptr, *dp_hot_tmp = nullptr;
     bool idx_up = false;
     c->nhot = 0;
     c->hot_nnz = 0;
-    if (!host_res && c->tune_hot != 0 && nz_r > 0 && n > 0 && (c->nsell == 0 || c->split_launch)) {
+    c->nxc = 0;
+    const bool want_hot = !host_res && c->tune_hot != 0 && nz_r > 0 && n > 0 && (c->nsell == 0 || c->split_launch);
+    const bool want_cx = !host_res && nz_r > 0 && n > 0 &&
+                         (c->tune_compact == 1 || (c->tune_compact == -1 && (int64_t)n * (int64_t)V >= COMPACT_X_MIN_BYTES));
+    if (want_hot || want_cx) {
       int sms = 148;
       CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
       TRY(h2d(c, d_idx, idx + B_lo, (size_t)nz_r * 4, s));
@@ -1647,42 +1759,80 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
       std::vector<int32_t> deg((size_t)n);
       CUDA_TRY(cudaMemcpyAsync(deg.data(), d_deg, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
       CUDA_TRY(cudaStreamSynchronize(s));
-      // a slot costs one gather per CTA per launch: worth it from 4 gathers per SM on
+      // a hot slot costs one gather per CTA per launch: worth it from 4 gathers per SM on
       const int32_t min_deg = 4 * sms;
-      const int T = host_threads(n);
-      std::vector<std::vector<int32_t>> cand((size_t)T);
+      std::mutex mu;
+      std::vector<std::pair<int64_t, std::vector<int32_t>>> used;
       par_ranges(n, [&](int64_t lo, int64_t hi) {
-        const int t = (int)(lo * T / std::max<int64_t>(1, n));
-        auto& v = cand[(size_t)std::min(t, T - 1)];
-        for (int64_t q = lo; q < hi; q++)
-          if (deg[(size_t)q] >= min_deg) v.push_back((int32_t)q);
+        std::vector<int32_t> v, u;
+        for (int64_t q = lo; q < hi; q++) {
+          if (want_hot && deg[(size_t)q] >= min_deg) v.push_back((int32_t)q);
+          if (want_cx && deg[(size_t)q] > 0) u.push_back((int32_t)q);
+        }
+        std::lock_guard<std::mutex> lk(mu);
+        hot.insert(hot.end(), v.begin(), v.end());
+        used.push_back({lo, std::move(u)});
       });
-      for (auto& v : cand) hot.insert(hot.end(), v.begin(), v.end());
-      const size_t H = (size_t)hot_max((int)V);
-      auto hotter = [&](int32_t a, int32_t b) { return deg[(size_t)a] != deg[(size_t)b] ? deg[(size_t)a] > deg[(size_t)b] : a < b; };
-      if (hot.size() > H) {
-        std::nth_element(hot.begin(), hot.begin() + (ptrdiff_t)H, hot.end(), hotter);
-        hot.resize(H);
+      if (want_cx) {
+        std::sort(used.begin(), used.end(), [](const auto& p, const auto& q) { return p.first < q.first; });
+        for (auto& u : used) xcols.insert(xcols.end(), u.second.begin(), u.second.end());
+        // auto: only when the rank touches <= 3/4 of x (R-MAT scale 24: 44 %); a power-law matrix
+        // that touches every column gains nothing from the extra gather
+        if (c->tune_compact == 1 || (int64_t)xcols.size() * 4 <= (int64_t)n * 3) {
+          TRY(dalloc(c, (size_t)n * 4, &dp, s));
+          d_colmap = static_cast<int32_t*>(dp);   // column -> compact id (filled from the kept list below)
+          c->nxc = (int64_t)xcols.size();
+        } else {
+          xcols.clear();
+        }
       }
-      std::sort(hot.begin(), hot.end(), hotter);   // slot 0 = the hottest column
-      int64_t cap_nz = 0;
-      for (int32_t q : hot) cap_nz += deg[(size_t)q];
-      // auto: only when the hot columns carry >= 5 % of the rank's gathers (power-law columns)
-      const bool on = c->tune_hot == 1 ? !hot.empty() : (cap_nz * 20 >= nz_r && nz_r >= ((int64_t)1 << 20));
-      if (on) {
-        TRY(dalloc(c, (size_t)n * 4, &dp, s));
-        d_hotslot = static_cast<int32_t*>(dp);
-        CUDA_TRY(cudaMemsetAsync(d_hotslot, 0xff, (size_t)n * 4, s));   // -1: cold
-        c->nhot = (int)hot.size();
-        c->hot_nnz = cap_nz;
-      } else {
-        hot.clear();
+      used.clear();
+      if (want_hot) {
+        // cache size: MSREP_TUNE_HOT_X = k > 1 asks for k KiB; else HOT_AUTO_BYTES.  Shared memory
+        // and L1 share the SM's 256 KB, and the gathers still missing need L1 room in flight
+        const int64_t want = c->tune_hot > 1 ? std::min<int64_t>((int64_t)c->tune_hot << 10, HOT_BYTES) : HOT_AUTO_BYTES;
+        const size_t H = (size_t)(want / (int64_t)V) * (size_t)c->tune_hot_cluster;   // per CTA x CTAs sharing
+        auto hotter = [&](int32_t a, int32_t b) { return deg[(size_t)a] != deg[(size_t)b] ? deg[(size_t)a] > deg[(size_t)b] : a < b; };
+        if (hot.size() > H) {
+          std::nth_element(hot.begin(), hot.begin() + (ptrdiff_t)H, hot.end(), hotter);
+          hot.resize(H);
+        }
+        std::sort(hot.begin(), hot.end(), hotter);   // slot 0 = the hottest column
+        int64_t cap_nz = 0;
+        for (int32_t q : hot) cap_nz += deg[(size_t)q];
+        // auto: only when the hot columns carry >= 5 % of the rank's gathers (power-law columns)
+        // (fp32: the hot instantiation of the fp32 tile walk spills registers, 1.07 -> 1.81 ms on R-MAT,
+        // profiles/r2_hot_x_ab.txt -- off unless forced)
+        const bool on = c->tune_hot >= 1 ? !hot.empty()
+                                         : (V == 8 && cap_nz * 20 >= nz_r && nz_r >= ((int64_t)1 << 20));
+        if (on) {
+          TRY(dalloc(c, (size_t)n * 4, &dp, s));
+          d_hotslot = static_cast<int32_t*>(dp);
+          CUDA_TRY(cudaMemsetAsync(d_hotslot, 0xff, (size_t)n * 4, s));   // -1: cold
+          c->nhot = (int)hot.size();
+          c->hot_nnz = cap_nz;
+          c->hot_cluster = c->tune_hot_cluster;
+          TRY(upload_vec(c, hot, &dp_hot_tmp, s));   // original ids, for the slot table
+        } else {
+          hot.clear();
+        }
       }
     }
     const size_t keep_from = c->bufs.size();
+    c->d_xcols = nullptr;
+    c->d_xc = nullptr;
+    if (c->nxc) {
+      TRY(upload_vec(c, xcols, &c->d_xcols, s));
+      CUDA_TRY(launch_hot_slots(c->d_xcols, (int)c->nxc, d_colmap, s));   // colmap[xcols[k]] = k
+      void* q;
+      TRY(dalloc(c, (size_t)c->nxc * V, &q, s));
+      c->d_xc = q;
+    }
     if (c->nhot) {
+      CUDA_TRY(launch_hot_slots(dp_hot_tmp, c->nhot, d_hotslot, s));
+      if (c->nxc)   // the kernels read x': hot slots are filled from compact ids
+        for (auto& q : hot) q = (int32_t)(std::lower_bound(xcols.begin(), xcols.end(), q) - xcols.begin());
       TRY(upload_vec(c, hot, &c->d_hot, s));
-      CUDA_TRY(launch_hot_slots(c->d_hot, c->nhot, d_hotslot, s));
     } else {
       c->d_hot = nullptr;
     }
@@ -1711,7 +1861,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
       PackLaunch PL{d_tiles_orig + g.t0, d_blob16 + g.t0, g.t1 - g.t0,
                     static_cast<const char*>(vp) - (size_t)g.z0 * V, d_idx - g.z0,
                     d_crow ? d_crow - g.z0 : d_aux, fmt == MSREP_COO, (int)V, c->wlo,
-                    host_res ? d_pack - off0 : d_pack, d_lp, d_hotslot};
+                    host_res ? d_pack - off0 : d_pack, d_lp, d_hotslot, d_colmap};
       CUDA_TRY(launch_pack(PL, s));
       if (host_res)
         CUDA_TRY(cudaMemcpyAsync(c->h_blob + off0, d_pack, (size_t)c->chunks[gi].bytes, cudaMemcpyDeviceToHost, s));
@@ -1769,6 +1919,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   st.host_bytes = c->h_bytes;
   st.x_no_allocate = c->xna;
   st.nhot = c->nhot;
+  st.x_compact = c->nxc;
   st.hot_nnz = c->hot_nnz;
   int64_t X = 0;
   if (colwise(fmt)) {
@@ -1810,7 +1961,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   const int64_t nmain = c->chunks.empty() ? 1 : (int64_t)c->chunks.size();   // main-kernel launches
   if (colwise(fmt))
     st.kernels_per_spmv = (c->cunits ? nmain : 0) + (c->nranks > 1 ? 1 /*shard epilogue*/ : 0);
-  else st.kernels_per_spmv = (c->ntiles ? nmain + (c->split_launch && c->chunks.empty() ? 1 : 0) : 0) + (c->nranks > 1 && c->any_flag ? 1 : 0) + (c->nsplit ? 1 : 0);
+  else st.kernels_per_spmv = (c->ntiles ? nmain + (c->split_launch && c->chunks.empty() ? 1 : 0) : 0) + (c->nranks > 1 && c->any_flag ? 1 : 0) + (c->nsplit ? 1 : 0) + (c->nxc ? 1 : 0);
   int64_t db = 0;
   for (auto& b : c->bufs) db += (int64_t)b.bytes;
   st.device_bytes = db;
@@ -1933,6 +2084,7 @@ msrep_status_t spmv_impl(msrep_ctx h, const void* alpha_p, const void* x, const 
     return MSREP_OK;
   }
 
+  TRY(prepare_x(c, x, 1, s));
   RowLaunch L = row_launch(c, x, y, alpha, beta);
   L.nmirror = nmirror;
   for (int mi = 0; mi < nmirror; mi++) L.mirror[mi] = mirrors[mi];
@@ -2007,6 +2159,8 @@ msrep_status_t msrep_spmm(msrep_ctx h, const void* alpha_p, const void* X, const
   L.alpha = alpha; L.beta = beta; L.rec = c->d_rec_mm;
   L.dtype = dt; L.has_sell = c->nsell > 0;
   L.hot = c->d_hot;   // SpMM untags hot column ids through the list (no shared-memory cache)
+  TRY(prepare_x(c, X, k, s));
+  if (c->nxc) { L.x = c->d_xc_mm; L.xmax = (uint32_t)(c->nxc - 1); }
   cudaEvent_t pe;
   TRY(prof_begin(c, s, &pe));
   if (c->residency == MSREP_RESIDENT_HOST) {

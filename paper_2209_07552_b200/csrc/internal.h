@@ -30,11 +30,15 @@ constexpr int WARPS = MSREP_WARPS;   // warps per CTA (each with its own TMA rin
 // Hot-x cache (row formats): the rank's most-gathered columns (by nonzero count,
 // chosen at partition time) get a slot in a CTA-wide shared-memory copy of x, refilled at every
 // launch; SEG / slab tiles carry HOT_TAG | slot instead of the column id for them.  One CTA of
-// HOT_WARPS warps per SM holds HOT_BYTES of x (12288 fp64 / 24576 fp32 entries).
+// HOT_WARPS warps per SM holds up to HOT_BYTES of x (sized per partition: HOT_AUTO_BYTES by
+// default, MSREP_TUNE_HOT_X KiB when set).
 constexpr uint32_t HOT_TAG = 0x80000000u;
 constexpr int HOT_WARPS = 16;
 constexpr int HOT_BYTES = 96 * 1024;
-__host__ __device__ constexpr int hot_max(int vsize) { return HOT_BYTES / vsize; }
+#ifndef MSREP_HOT_AUTO_KB
+#define MSREP_HOT_AUTO_KB 32
+#endif
+constexpr int HOT_AUTO_BYTES = MSREP_HOT_AUTO_KB * 1024;
 
 // Device layout: every tile is one contiguous, 16-byte aligned "blob"; each
 // segment is padded to 16 bytes so one TMA bulk copy moves the tile.
@@ -113,6 +117,7 @@ struct PackLaunch {        // build the tile blobs from the rank's plain slices 
   char* blob;
   const int32_t* lptr;                                        // window-local pointer (SELL tiles; CSR: == ptr)
   const int32_t* hotslot;                                     // [n]: hot-x slot of a column, -1 if cold; NULL: no hot x
+  const int32_t* colmap;                                      // [n]: compact-x id of a column; NULL: no compact x
 };
 
 constexpr int MAX_MIRRORS = 8;   // msrep_spmv_mirror: extra y buffers (peer-mapped or local)
@@ -128,6 +133,7 @@ struct RowLaunch {
   int nmirror; void* mirror[MAX_MIRRORS];                    // y rows are also stored here (msrep_spmv_mirror)
   int xna;                                                   // x gathers with L1::no_allocate (SEG / slab tiles)
   const int32_t* hot; int nhot;                              // hot-x columns by slot (nhot == 0: no hot x)
+  int hot_cluster;                                           // 2: slots split over a CTA pair (DSMEM), else 1
 };
 
 // pCSC row-band layout.  The rank's nonzeros are regrouped
@@ -217,6 +223,8 @@ cudaError_t launch_rebase(const int64_t* gptr, int32_t* lptr, int64_t count, int
 cudaError_t launch_pack(const PackLaunch& L, cudaStream_t s);
 cudaError_t launch_col_degree(const int32_t* idx, int64_t nz, int32_t* deg, cudaStream_t s);   // deg[idx[i]]++
 cudaError_t launch_hot_slots(const int32_t* hot, int nhot, int32_t* slot, cudaStream_t s);      // slot[hot[k]] = k
+// out[i*k + j] = x[cols[i]*k + j], i < n, j < k (compact x for SpMV k = 1, SpMM k > 1)
+cudaError_t launch_gather_x(const void* x, const int32_t* cols, int64_t n, int k, void* out, int dtype, cudaStream_t s);
 // CG vector kernels on an owned segment of n entries (kernels.cu).  sc = device scalars
 // {rs (parity 0), rs (parity 1), -, bnorm2}; part_in / part_out = CG_PARTS per-block partial
 // sums (every consumer block re-sums part_in in the same fixed order).

@@ -24,6 +24,7 @@
 //               producer warp, the alpha/beta epilogue (or the py write for the
 //               reduce-scatter) fused at band end.
 //  cg_*         the vector kernels of msrep_cg.
+#include <algorithm>
 #include <climits>
 #include <mutex>
 #include <cstdint>
@@ -117,14 +118,14 @@ struct RStage {
   static constexpr int BYTES = N + N * (int)sizeof(VT) + N * 4;
 };
 
-template <int STAGE_B, int NS, int SCRATCH, int NW = WARPS, int HOTB = 0>
+template <int STAGE_B, int NS, int SCRATCH, int NW = WARPS>
 struct WLayout {
   static constexpr int DESC_OFF = NS * STAGE_B;                          // int4 per stage
   static constexpr int SCR_OFF = DESC_OFF + NS * 16;                     // per-warp fp64 scratch
   static constexpr int WARP_B = (SCR_OFF + SCRATCH + 15) & ~15;
-  static constexpr int HOT_OFF = NW * WARP_B;                            // CTA-wide hot x cache (HOTB bytes)
-  static constexpr int BAR_OFF = HOT_OFF + HOTB;
+  static constexpr int BAR_OFF = NW * WARP_B;
   static constexpr int TOTAL = BAR_OFF + NW * NS * 8;
+  static constexpr int HOT_OFF = (TOTAL + 15) & ~15;                     // CTA-wide hot x cache (sized per launch)
 };
 
 // nonzeros per lane in a full SEG tile / slab (+1 extra slot when ragged): 16 fp64, 32 fp32
@@ -185,44 +186,64 @@ template <typename VT>
 struct SStage { static constexpr int BYTES = SELL_R_MAX * 32 * 2 + SELL_W_MAX * SELL_ROWS * ((int)sizeof(VT) + 4); };
 template <typename VT, bool SELL, bool HOT = false>
 using RowLayout = WLayout<(SELL && SStage<VT>::BYTES > RStage<VT>::BYTES) ? SStage<VT>::BYTES : RStage<VT>::BYTES, 1,
-                          MAX_TILE_ROWS * 8, HOT ? HOT_WARPS : WARPS, HOT ? HOT_BYTES : 0>;
+                          MAX_TILE_ROWS * 8, HOT ? HOT_WARPS : WARPS>;
 
 // x gather of a SEG / slab column id: tagged ids (bit 31, internal.h HOT_TAG) read the CTA's
 // shared-memory copy of the rank's hottest x entries, the others go through L2.  Branch-free: one
 // predicated LDS and one predicated LDG into the same register, so all of a lane's gathers stay
 // in flight together (a branch per gather serialises the two paths, 1.3 -> 2.2 ms on R-MAT).
+// hot-x address of slot s: the slots are spread over the CL CTAs of the cluster, hpc per CTA; hb[r]
+// is CTA r's cache base in the shared::cluster window (CL == 1: the CTA's own shared memory)
+struct HotRef { uint32_t hb0, hb1, hpc; };
 template <bool NA>
-__device__ __forceinline__ double ldx_sel(const double* x, uint32_t hbase, uint32_t c, uint64_t pol) {
+__device__ __forceinline__ double ldx_sel(const double* x, const HotRef& h, uint32_t c, uint64_t pol) {
   double v;
-  if constexpr (NA) asm("{\n\t.reg .pred p;\n\t.reg .u32 ci, sa;\n\t.reg .u64 ga;\n\t"
-                        "setp.lt.s32 p, %1, 0;\n\tand.b32 ci, %1, 0x7fffffff;\n\tmad.lo.u32 sa, ci, 8, %2;\n\t"
-                        "mad.wide.u32 ga, %1, 8, %3;\n\t@p ld.shared.f64 %0, [sa];\n\t"
-                        "@!p ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [ga], %4;\n\t}"
-                        : "=d"(v) : "r"(c), "r"(hbase), "l"(x), "l"(pol));
-  else asm("{\n\t.reg .pred p;\n\t.reg .u32 ci, sa;\n\t.reg .u64 ga;\n\t"
-           "setp.lt.s32 p, %1, 0;\n\tand.b32 ci, %1, 0x7fffffff;\n\tmad.lo.u32 sa, ci, 8, %2;\n\t"
-           "mad.wide.u32 ga, %1, 8, %3;\n\t@p ld.shared.f64 %0, [sa];\n\t"
-           "@!p ld.global.nc.L2::cache_hint.f64 %0, [ga], %4;\n\t}"
-           : "=d"(v) : "r"(c), "r"(hbase), "l"(x), "l"(pol));
+  if constexpr (NA) asm("{\n\t.reg .pred p, q;\n\t.reg .u32 ci, sa, hb;\n\t.reg .u64 ga;\n\t"
+                        "setp.lt.s32 p, %1, 0;\n\tand.b32 ci, %1, 0x7fffffff;\n\tsetp.ge.u32 q, ci, %4;\n\t"
+                        "selp.b32 hb, %3, %2, q;\n\t@q sub.u32 ci, ci, %4;\n\tmad.lo.u32 sa, ci, 8, hb;\n\t"
+                        "mad.wide.u32 ga, %1, 8, %5;\n\t@p ld.shared::cluster.f64 %0, [sa];\n\t"
+                        "@!p ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [ga], %6;\n\t}"
+                        : "=d"(v) : "r"(c), "r"(h.hb0), "r"(h.hb1), "r"(h.hpc), "l"(x), "l"(pol));
+  else asm("{\n\t.reg .pred p, q;\n\t.reg .u32 ci, sa, hb;\n\t.reg .u64 ga;\n\t"
+           "setp.lt.s32 p, %1, 0;\n\tand.b32 ci, %1, 0x7fffffff;\n\tsetp.ge.u32 q, ci, %4;\n\t"
+           "selp.b32 hb, %3, %2, q;\n\t@q sub.u32 ci, ci, %4;\n\tmad.lo.u32 sa, ci, 8, hb;\n\t"
+           "mad.wide.u32 ga, %1, 8, %5;\n\t@p ld.shared::cluster.f64 %0, [sa];\n\t"
+           "@!p ld.global.nc.L2::cache_hint.f64 %0, [ga], %6;\n\t}"
+           : "=d"(v) : "r"(c), "r"(h.hb0), "r"(h.hb1), "r"(h.hpc), "l"(x), "l"(pol));
   return v;
 }
 template <bool NA>
-__device__ __forceinline__ float ldx_sel(const float* x, uint32_t hbase, uint32_t c, uint64_t pol) {
+__device__ __forceinline__ float ldx_sel(const float* x, const HotRef& h, uint32_t c, uint64_t pol) {
   float v;
-  if constexpr (NA) asm("{\n\t.reg .pred p;\n\t.reg .u32 ci, sa;\n\t.reg .u64 ga;\n\t"
-                        "setp.lt.s32 p, %1, 0;\n\tand.b32 ci, %1, 0x7fffffff;\n\tmad.lo.u32 sa, ci, 4, %2;\n\t"
-                        "mad.wide.u32 ga, %1, 4, %3;\n\t@p ld.shared.f32 %0, [sa];\n\t"
-                        "@!p ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [ga], %4;\n\t}"
-                        : "=f"(v) : "r"(c), "r"(hbase), "l"(x), "l"(pol));
-  else asm("{\n\t.reg .pred p;\n\t.reg .u32 ci, sa;\n\t.reg .u64 ga;\n\t"
-           "setp.lt.s32 p, %1, 0;\n\tand.b32 ci, %1, 0x7fffffff;\n\tmad.lo.u32 sa, ci, 4, %2;\n\t"
-           "mad.wide.u32 ga, %1, 4, %3;\n\t@p ld.shared.f32 %0, [sa];\n\t"
-           "@!p ld.global.nc.L2::cache_hint.f32 %0, [ga], %4;\n\t}"
-           : "=f"(v) : "r"(c), "r"(hbase), "l"(x), "l"(pol));
+  if constexpr (NA) asm("{\n\t.reg .pred p, q;\n\t.reg .u32 ci, sa, hb;\n\t.reg .u64 ga;\n\t"
+                        "setp.lt.s32 p, %1, 0;\n\tand.b32 ci, %1, 0x7fffffff;\n\tsetp.ge.u32 q, ci, %4;\n\t"
+                        "selp.b32 hb, %3, %2, q;\n\t@q sub.u32 ci, ci, %4;\n\tmad.lo.u32 sa, ci, 4, hb;\n\t"
+                        "mad.wide.u32 ga, %1, 4, %5;\n\t@p ld.shared::cluster.f32 %0, [sa];\n\t"
+                        "@!p ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [ga], %6;\n\t}"
+                        : "=f"(v) : "r"(c), "r"(h.hb0), "r"(h.hb1), "r"(h.hpc), "l"(x), "l"(pol));
+  else asm("{\n\t.reg .pred p, q;\n\t.reg .u32 ci, sa, hb;\n\t.reg .u64 ga;\n\t"
+           "setp.lt.s32 p, %1, 0;\n\tand.b32 ci, %1, 0x7fffffff;\n\tsetp.ge.u32 q, ci, %4;\n\t"
+           "selp.b32 hb, %3, %2, q;\n\t@q sub.u32 ci, ci, %4;\n\tmad.lo.u32 sa, ci, 4, hb;\n\t"
+           "mad.wide.u32 ga, %1, 4, %5;\n\t@p ld.shared::cluster.f32 %0, [sa];\n\t"
+           "@!p ld.global.nc.L2::cache_hint.f32 %0, [ga], %6;\n\t}"
+           : "=f"(v) : "r"(c), "r"(h.hb0), "r"(h.hb1), "r"(h.hpc), "l"(x), "l"(pol));
   return v;
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t a, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 template <bool HOT, bool NA, typename VT>
-__device__ __forceinline__ VT ldx_hot(const VT* x, uint32_t hbase, uint32_t c, uint64_t pol) {
+__device__ __forceinline__ VT ldx_hot(const VT* x, const HotRef& hbase, uint32_t c, uint64_t pol) {
   if constexpr (HOT) return ldx_sel<NA>(x, hbase, c, pol);
   else return ldx<NA>(x + c, pol);
 }
@@ -279,7 +300,7 @@ __device__ __forceinline__ void sell_tile(const RowLaunch& P, const int4 d, cons
   refill();
 }
 
-template <typename VT, bool SELL, bool MIRROR, bool NA, bool HOT>
+template <typename VT, bool SELL, bool MIRROR, bool NA, bool HOT, int CL>
 __global__ void __launch_bounds__(HOT ? HOT_WARPS * 32 : WARPS * 32,
                                   HOT ? 1 : (sizeof(VT) == 4 ? MSREP_ROW_MINB_F32 : MSREP_ROW_MINB))
     rows_kernel(const RowLaunch P) {
@@ -302,7 +323,16 @@ __global__ void __launch_bounds__(HOT ? HOT_WARPS * 32 : WARPS * 32,
   const uint32_t xmax = P.xmax;
   const uint64_t xpol = policy_evict_last();
   VT* hx = reinterpret_cast<VT*>(smem + Lay::HOT_OFF);
-  const uint32_t hbase = saddr(hx);
+  // CL == 2: the hot slots are split over the CTA pair of the cluster (slots [r*hpc, (r+1)*hpc) in
+  // CTA r), read through distributed shared memory -- twice the hot entries per SM of L1 given up
+  HotRef hbase{saddr(hx), saddr(hx), 0x7fffffffu};
+  int hlo = 0, hhi = P.nhot;
+  if constexpr (HOT && CL == 2) {
+    const uint32_t hpc = (uint32_t)((P.nhot + 1) / 2), me = cluster_ctarank();
+    hbase = HotRef{mapa_shared(saddr(hx), 0), mapa_shared(saddr(hx), 1), hpc};
+    hlo = (int)(me * hpc);
+    hhi = min(P.nhot, (int)((me + 1) * hpc));
+  }
 
   uint64_t pol = 0;
   int4 dn = make_int4(0, 0, 0, -1);
@@ -317,25 +347,26 @@ __global__ void __launch_bounds__(HOT ? HOT_WARPS * 32 : WARPS * 32,
     }
     if (gw + nw < P.ntiles) dn = P.tiles[gw + nw];
   }
-  if constexpr (HOT) {   // the CTA's copy of the hot x entries, gathered while the first tiles land
+  if constexpr (HOT) {   // the CTA's copy of (its share of) the hot x entries, gathered while the first tiles land
     constexpr int U = 8, T = NW * 32;
-    for (int k0 = 0; k0 < P.nhot; k0 += U * T) {
+    for (int k0 = hlo; k0 < hhi; k0 += U * T) {
       int cs[U];
       VT xs[U];
 #pragma unroll
       for (int u = 0; u < U; u++) {
         const int k = k0 + u * T + (int)threadIdx.x;
-        cs[u] = k < P.nhot ? __ldg(P.hot + k) : 0;
+        cs[u] = k < hhi ? __ldg(P.hot + k) : 0;
       }
 #pragma unroll
       for (int u = 0; u < U; u++) xs[u] = __ldg(x + cs[u]);
 #pragma unroll
       for (int u = 0; u < U; u++) {
         const int k = k0 + u * T + (int)threadIdx.x;
-        if (k < P.nhot) hx[k] = xs[u];
+        if (k < hhi) hx[k - hlo] = xs[u];
       }
     }
-    __syncthreads();
+    if constexpr (CL == 2) cluster_sync();   // both halves filled before any remote read
+    else __syncthreads();
   }
   __syncwarp();
 
@@ -478,6 +509,7 @@ __global__ void __launch_bounds__(HOT ? HOT_WARPS * 32 : WARPS * 32,
     }
     __syncwarp();   // rsum is free
   }
+  if constexpr (HOT && CL == 2) cluster_sync();   // the partner CTA may still read this CTA's hot half
 }
 
 // ------------------------------------------------------------------ SpMM
@@ -981,18 +1013,23 @@ __global__ void __launch_bounds__(CB_THREADS, 1) csc_band_kernel(const ColLaunch
           const int kn = __shfl_down_sync(FULL, key, 1);
           if (real && (lane == 31 || kn != key)) acc[key] += t;
           __syncwarp();
-        } else if (A.pk[k] != CB_HOLE) {
-          double* a = acc + (A.pk[k] & (CB_ROWS - 1));
-          *a = fma((double)A.v[k], (double)A.xv[k], *a);
+        } else {
+          if (A.pk[k] != CB_HOLE) {
+            double* a = acc + (A.pk[k] & (CB_ROWS - 1));
+            *a = fma((double)A.v[k], (double)A.xv[k], *a);
+          }
+          __syncwarp();   // a row of this step may recur in another lane at the next step
         }
       }
     } else {
 #pragma unroll
-      for (int k = 0; k < CB_PER; k++)
+      for (int k = 0; k < CB_PER; k++) {
         if (A.pk[k] != CB_HOLE) {
           double* a = acc + (A.pk[k] & (CB_ROWS - 1));
           *a = fma((double)A.v[k], (double)A.xv[k], *a);
         }
+        __syncwarp();   // a row of this step may recur in another lane at the next step
+      }
     }
     if (A.d.w & 1) {   // unit complete: this warp writes its rows once and re-zeroes them
       __syncwarp();
@@ -1079,9 +1116,11 @@ __global__ void __launch_bounds__(CB_THREADS, 1) csc_band_kernel(const ColLaunch
 // its contiguous blob.  aux for pointer kinds = tile-local pointer, i.e.
 // clamp(ptr[row0 + j], z0, z1) - z0 for j = 0..nrows (the rebase of Alg. 2 l.12).
 __device__ __forceinline__ int pack_col(const PackLaunch& L, int c) {
-  if (!L.hotslot) return c;
-  const int h = L.hotslot[c];
-  return h >= 0 ? (int)(HOT_TAG | (uint32_t)h) : c;
+  if (L.hotslot) {
+    const int h = L.hotslot[c];
+    if (h >= 0) return (int)(HOT_TAG | (uint32_t)h);
+  }
+  return L.colmap ? L.colmap[c] : c;
 }
 
 __global__ void pack_kernel(const PackLaunch L) {
@@ -1106,7 +1145,7 @@ __global__ void pack_kernel(const PackLaunch L) {
         const int sl = (t * R + k) * 32 + lane;
         if (L.vsize == 8) reinterpret_cast<double*>(vb0)[sl] = on ? static_cast<const double*>(L.val)[rs + t] : 0.0;
         else reinterpret_cast<float*>(vb0)[sl] = on ? static_cast<const float*>(L.val)[rs + t] : 0.0f;
-        ix[sl] = on ? L.idx[rs + t] : 0;
+        ix[sl] = on ? (L.colmap ? L.colmap[L.idx[rs + t]] : L.idx[rs + t]) : 0;
       }
     }
     return;
@@ -1153,6 +1192,32 @@ __global__ void col_degree_kernel(const int32_t* __restrict__ idx, int64_t nz, i
 __global__ void hot_slot_kernel(const int32_t* __restrict__ hot, int nhot, int32_t* __restrict__ slot) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k < nhot) slot[hot[k]] = k;
+}
+// compact x (every SpMV of a compact-x partition): x' rows = x rows of the listed columns
+template <typename VT, int K>
+__global__ void gather_x_kernel(const VT* __restrict__ x, const int32_t* __restrict__ cols, int64_t n,
+                                VT* __restrict__ out) {
+  // one compact entry (K values) per thread, 4 independent entries per thread in flight
+  constexpr int U = 4;
+  const int64_t i0 = (blockIdx.x * (int64_t)blockDim.x) * U + threadIdx.x;
+  int32_t c[U];
+#pragma unroll
+  for (int u = 0; u < U; u++) {
+    const int64_t i = i0 + (int64_t)u * blockDim.x;
+    c[u] = i < n ? __ldcs(cols + i) : 0;
+  }
+  VT v[U][K];
+#pragma unroll
+  for (int u = 0; u < U; u++)
+#pragma unroll
+    for (int j = 0; j < K; j++) v[u][j] = i0 + (int64_t)u * blockDim.x < n ? __ldg(x + (int64_t)c[u] * K + j) : VT(0);
+#pragma unroll
+  for (int u = 0; u < U; u++) {
+    const int64_t i = i0 + (int64_t)u * blockDim.x;
+    if (i < n)
+#pragma unroll
+      for (int j = 0; j < K; j++) out[i * K + j] = v[u][j];
+  }
 }
 
 // --------------------------------------------------------- small kernels
@@ -1379,24 +1444,44 @@ int grid_for(K kernel, int smem_bytes, int ntiles, int warps = WARPS) {
   return (int)(want < g ? (want < 1 ? 1 : want) : g);
 }
 
-template <typename VT, bool SELL, bool MIRROR, bool NA, bool HOT>
+template <typename VT, bool SELL, bool MIRROR, bool NA, bool HOT, int CL>
 cudaError_t launch_rows_k(const RowLaunch& L, cudaStream_t s) {
-  constexpr int b = RowLayout<VT, SELL, HOT>::TOTAL;
+  using Lay = RowLayout<VT, SELL, HOT>;
   constexpr int nw = HOT ? HOT_WARPS : WARPS;
-  static_assert(b <= 227 * 1024, "rows_kernel shared memory");
-  cudaError_t e = set_smem(rows_kernel<VT, SELL, MIRROR, NA, HOT>, b);
+  static_assert(Lay::HOT_OFF + (HOT ? HOT_BYTES : 0) <= 227 * 1024, "rows_kernel shared memory");
+  const int b = HOT ? Lay::HOT_OFF + ((L.nhot + CL - 1) / CL) * (int)sizeof(VT) : Lay::TOTAL;
+  auto kern = rows_kernel<VT, SELL, MIRROR, NA, HOT, CL>;
+  cudaError_t e = set_smem(kern, b);
   if (e) return e;
-  rows_kernel<VT, SELL, MIRROR, NA, HOT>
-      <<<grid_for(rows_kernel<VT, SELL, MIRROR, NA, HOT>, b, L.ntiles, nw), nw * 32, b, s>>>(L);
+  int g = grid_for(kern, b, L.ntiles, nw);
+  if constexpr (CL == 1) {
+    kern<<<g, nw * 32, b, s>>>(L);
+  } else {   // CTA pairs (one CTA per SM, the two SMs of a TPC) sharing their hot halves over DSMEM
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(nw * 32); cfg.dynamicSmemBytes = (size_t)b; cfg.stream = s;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    int maxc = 0;
+    cfg.gridDim = dim3(CL);
+    if (cudaOccupancyMaxActiveClusters(&maxc, kern, &cfg) != cudaSuccess || maxc < 1) { cudaGetLastError(); maxc = 1; }
+    g = std::max(CL, std::min(g / CL * CL, maxc * CL));
+    cfg.gridDim = dim3(g);
+    e = cudaLaunchKernelEx(&cfg, kern, L);
+    if (e) return e;
+  }
   return cudaGetLastError();
 }
 template <typename VT, bool SELL, bool MIRROR>
 cudaError_t launch_rows_t(const RowLaunch& L, cudaStream_t s) {
   if constexpr (!SELL) {   // the hot x cache serves SEG / slab tiles (SELL launches gather through L2)
+    if (L.nhot > 0 && L.hot_cluster == 2)
+      return L.xna ? launch_rows_k<VT, false, MIRROR, true, true, 2>(L, s) : launch_rows_k<VT, false, MIRROR, false, true, 2>(L, s);
     if (L.nhot > 0)
-      return L.xna ? launch_rows_k<VT, false, MIRROR, true, true>(L, s) : launch_rows_k<VT, false, MIRROR, false, true>(L, s);
+      return L.xna ? launch_rows_k<VT, false, MIRROR, true, true, 1>(L, s) : launch_rows_k<VT, false, MIRROR, false, true, 1>(L, s);
   }
-  return L.xna ? launch_rows_k<VT, SELL, MIRROR, true, false>(L, s) : launch_rows_k<VT, SELL, MIRROR, false, false>(L, s);
+  return L.xna ? launch_rows_k<VT, SELL, MIRROR, true, false, 1>(L, s) : launch_rows_k<VT, SELL, MIRROR, false, false, 1>(L, s);
 }
 template <typename VT, bool SELL>
 cudaError_t launch_rows_m(const RowLaunch& L, cudaStream_t s) {
@@ -1484,6 +1569,25 @@ cudaError_t launch_col_degree(const int32_t* idx, int64_t nz, int32_t* deg, cuda
 cudaError_t launch_hot_slots(const int32_t* hot, int nhot, int32_t* slot, cudaStream_t s) {
   if (nhot <= 0) return cudaSuccess;
   hot_slot_kernel<<<(nhot + 255) / 256, 256, 0, s>>>(hot, nhot, slot);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_x(const void* x, const int32_t* cols, int64_t n, int k, void* out, int dtype, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const unsigned g = (unsigned)((n + 1023) / 1024);   // 256 threads x 4 entries per block
+#define MSREP_GATHER(VT, K) gather_x_kernel<VT, K><<<g, 256, 0, s>>>((const VT*)x, cols, n, (VT*)out)
+  if (dtype == 0) {
+    if (k == 1) MSREP_GATHER(double, 1);
+    else if (k == 2) MSREP_GATHER(double, 2);
+    else if (k == 4) MSREP_GATHER(double, 4);
+    else MSREP_GATHER(double, 8);
+  } else {
+    if (k == 1) MSREP_GATHER(float, 1);
+    else if (k == 2) MSREP_GATHER(float, 2);
+    else if (k == 4) MSREP_GATHER(float, 4);
+    else MSREP_GATHER(float, 8);
+  }
+#undef MSREP_GATHER
   return cudaGetLastError();
 }
 

@@ -11,6 +11,13 @@ def coo_of_csr(A):
     return gen.expand_rows(A)
 
 
+def shuffled_triplets(A, seed=77):
+    """The triplets of a CSR gen.Sparse in a seeded random order (row, col, val)."""
+    rows = gen.expand_rows(A)
+    perm = np.random.default_rng(seed).permutation(A.nnz)
+    return rows[perm].copy(), A["idx"][perm].copy(), A["val"][perm].copy()
+
+
 def to_dtype(A, dtype):
     B = gen.Sparse(A)
     B["val"] = A["val"].astype(dtype)
@@ -62,6 +69,10 @@ def run_gpu(A, fmt, x, y, alpha, beta, parts=1, layout=None, host_path=False, ct
     elif fmt == "coo_col":   # column-sorted COO: coo_row carries the sorted column ids
         assert A["fmt"] == "csc"
         ctx.partition("coo_col", A["m"], A["n"], idx=A["idx"], val=A["val"], coo_row=coo_of_csr(A), **pkw)
+    elif fmt == "coo_unsorted":   # any triplet order: A is CSR, shuffled with a seeded permutation
+        assert A["fmt"] == "csr"
+        r, c, v = shuffled_triplets(A)
+        ctx.partition("coo_unsorted", A["m"], A["n"], idx=c, val=v, coo_row=r, **pkw)
     else:
         assert A["fmt"] == "csc"
         ctx.partition("csc", A["m"], A["n"], ptr=A["ptr"], idx=A["idx"], val=A["val"], **pkw)

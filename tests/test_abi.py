@@ -183,3 +183,16 @@ def test_plan_bit_exact_vs_oracle_exhaustive_5x5():
                 ref, _, _ = oracle.partition_ptr(ptr, np_)
                 _parts_equal(M.msrep_plan(M.CSR, m, nnz, np_, ptr=ptr), ref)
                 _parts_equal(M.msrep_plan(M.COO, m, nnz, np_, coo_row=rows), ref)
+
+
+def test_plan_unsorted_coo_matches_oracle():
+    """msrep_plan(MSREP_COO_UNSORTED) == the oracle's unsorted-COO descriptors (positions, min/max
+    row), random orders and np up to nnz + 3."""
+    import paper_2209_07552_b200 as M
+    rng = np.random.default_rng(46)
+    for trial in range(200):
+        nnz = int(rng.integers(0, 80))
+        rows = rng.integers(0, 40, nnz).astype(np.int32)
+        for np_ in (1, 2, 3, 7, nnz + 3):
+            _parts_equal(M.msrep_plan(M.COO_UNSORTED, 40, nnz, np_, coo_row=rows),
+                         oracle.partition_coo_unsorted(rows, np_))

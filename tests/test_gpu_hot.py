@@ -12,27 +12,59 @@ from tests.helpers import assert_close, coo_of_csr, oracle_ref, row_bound, run_g
 pytestmark = pytest.mark.gpu
 
 
-def _ctx(hot, parts):
+def _ctx(hot, parts, compact=1):
     import paper_2209_07552_b200 as M
     ctx = M.Context(0, 1, None, 0, parts)
     ctx.set_tuning("hot_x", hot)
+    ctx.set_tuning("compact_x", compact)
     return ctx
 
 
 @pytest.mark.parametrize("fmt", ["csr", "coo"])
 @pytest.mark.parametrize("parts", [1, 3])
-def test_hot_x_bit_exact(fmt, parts):
+@pytest.mark.parametrize("compact", [1, 0])
+def test_hot_x_bit_exact(fmt, parts, compact):
+    """Hot cache forced on (also at a 4 KiB size), off and automatic, with and without compact x."""
     A = gen.rmat(18, seed=31, kind=gen.SMALLINT)
     x = gen.vector(A["n"], 32, kind=gen.SMALLINT); y = gen.vector(A["m"], 33, kind=gen.SMALLINT)
     ref = oracle_ref(A, x, y, 1.5, 0.5)
-    nhot = []
-    for hot in (1, 0, -1):
-        ctx = _ctx(hot, parts)
+    nhot, ncx = [], []
+    for hot in (1, 4, 0, -1):
+        ctx = _ctx(hot, parts, compact)
         got = run_gpu(A, fmt, x, y, 1.5, 0.5, ctx=ctx)
         nhot.append(ctx.stats()["nhot"])
+        ncx.append(ctx.stats()["x_compact"])
         ctx.close()
-        assert np.array_equal(got, ref), (fmt, parts, hot)
-    assert nhot[0] > 0 and nhot[1] == 0
+        assert np.array_equal(got, ref), (fmt, parts, hot, compact)
+    assert nhot[0] > 0 and 0 < nhot[1] <= 4096 // 8 and nhot[2] == 0
+    assert all((v > 0) == bool(compact) for v in ncx)
+
+
+@pytest.mark.parametrize("fmt", ["csr", "coo"])
+def test_compact_x_stencil_and_small(fmt):
+    """Compact x forced on for SELL-tile matrices (all tiles index x') and a tiny matrix."""
+    for A in (gen.stencil27(30, kind=gen.SMALLINT), gen.kdistinct_csr(50, 400, 3, seed=9, kind=gen.SMALLINT)):
+        x = gen.vector(A["n"], 32, kind=gen.SMALLINT); y = gen.vector(A["m"], 33, kind=gen.SMALLINT)
+        ctx = _ctx(0, 2, 1)
+        got = run_gpu(A, fmt, x, y, 1.5, 0.5, ctx=ctx)
+        assert ctx.stats()["x_compact"] > 0
+        ctx.close()
+        assert np.array_equal(got, oracle_ref(A, x, y, 1.5, 0.5))
+
+
+@pytest.mark.parametrize("cluster", [1, 2])
+def test_hot_x_cluster_pairs_bit_exact(cluster):
+    """MSREP_TUNE_HOT_CLUSTER = 2: the hot entries are split over the two CTAs of a thread-block
+    cluster and read over distributed shared memory -- same bits."""
+    A = gen.rmat(17, seed=38, kind=gen.SMALLINT)
+    x = gen.vector(A["n"], 39, kind=gen.SMALLINT); y = gen.vector(A["m"], 40, kind=gen.SMALLINT)
+    ctx = _ctx(8, 2, 1)
+    ctx.set_tuning("hot_cluster", cluster)
+    got = run_gpu(A, "csr", x, y, 1.5, 0.5, ctx=ctx)
+    st = ctx.stats()
+    ctx.close()
+    assert st["nhot"] > 0
+    assert np.array_equal(got, oracle_ref(A, x, y, 1.5, 0.5))
 
 
 def test_hot_x_fp32_and_uniform():
@@ -40,7 +72,7 @@ def test_hot_x_fp32_and_uniform():
         A = gen.rmat(17, seed=34)
         A["val"] = A["val"].astype(dtype)
         x = gen.vector(A["n"], 35, dtype=dtype); y = gen.vector(A["m"], 36, dtype=dtype)
-        ctx = _ctx(1, 2)
+        ctx = _ctx(1, 2, -1)
         got = run_gpu(A, "csr", x, y, 1.5, 0.5, ctx=ctx)
         assert ctx.stats()["nhot"] > 0
         ctx.close()

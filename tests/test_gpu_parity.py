@@ -251,6 +251,41 @@ def test_config3_rmat_full_size_bit_exact(fmt):
 
 
 @pytest.mark.slow
+@pytest.mark.parametrize("fmt", ["csr", "coo", "csc"])
+def test_config2_stencil_full_size_fp32_bit_exact(fmt):
+    """fp32 storage at full size, small-integer data (|y| < 2^24): fp64 accumulation makes every
+    order exact, so the fp32 result equals the oracle bit for bit (pin P5)."""
+    A = to_dtype(gen.stencil27(127, kind=gen.SMALLINT), np.float32)
+    m = A["m"]
+    x = gen.vector(m, 5, kind=gen.SMALLINT, dtype=np.float32); y = gen.vector(m, 6, kind=gen.SMALLINT, dtype=np.float32)
+    check(A, fmt, x, y, 1.5, 0.5, exact=True)
+
+
+@pytest.mark.slow
+def test_config3_rmat_full_size_fp32_bit_exact():
+    A = to_dtype(gen.rmat(24, seed=3, kind=gen.SMALLINT), np.float32)
+    x = gen.vector(A["n"], 7, kind=gen.SMALLINT, dtype=np.float32); y = gen.vector(A["m"], 8, kind=gen.SMALLINT, dtype=np.float32)
+    check(A, "csr", x, y, 2.0, 0.5, exact=True)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("fmt", ["csc", "coo_col"])
+def test_config3_rmat_full_size_column_formats_bit_exact(fmt):
+    """R-MAT scale 24 through the pCSC band layout (its heavy first bands are split into slot units)
+    and the column-sorted pCOO, fp64, bit-exact."""
+    A = gen.rmat(24, seed=3, kind=gen.SMALLINT)
+    x = gen.vector(A["n"], 7, kind=gen.SMALLINT); y = gen.vector(A["m"], 8, kind=gen.SMALLINT)
+    check(A, fmt, x, y, 2.0, 0.5, exact=True)
+
+
+@pytest.mark.slow
+def test_config4_tallskinny_fp32_bit_exact():
+    A = to_dtype(gen.kdistinct_csc(50_000_000, 1_000_000, 500, seed=4, kind=gen.SMALLINT), np.float32)
+    x = gen.vector(A["n"], 9, kind=gen.SMALLINT, dtype=np.float32); y = gen.vector(A["m"], 10, kind=gen.SMALLINT, dtype=np.float32)
+    check(A, "csc", x, y, 2.0, 0.5, exact=True)
+
+
+@pytest.mark.slow
 def test_config4_tallskinny_csc_sampled():
     A = gen.kdistinct_csc(50_000_000, 1_000_000, 500, seed=4, kind=gen.SMALLINT)
     x = gen.vector(A["n"], 9, kind=gen.SMALLINT); y = gen.vector(A["m"], 10, kind=gen.SMALLINT)

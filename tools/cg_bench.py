@@ -18,6 +18,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--format", default="csr")
 ap.add_argument("--iters", type=int, default=200)
 ap.add_argument("--N", type=int, default=127, help="stencil grid edge (127: config 2)")
+ap.add_argument("--graph", type=int, default=1, help="MSREP_TUNE_CG_GRAPH (1: CUDA-graph replay, 0: eager)")
 a = ap.parse_args()
 A = gen.stencil27(a.N, kind=gen.ONES)
 rows = np.repeat(np.arange(A["m"]), np.diff(A["ptr"]))
@@ -25,6 +26,7 @@ A["val"] = np.where(A["idx"] == rows, 30.0, -1.0)
 if a.format in ("csc", "coo_col"):
     A = gen.transpose(A)
 ctx = M.Context(0, 1, None, 0, 1)
+ctx.set_tuning("cg_graph", a.graph)
 coo = a.format in ("coo", "coo_col")
 ctx.partition(a.format, A["m"], A["n"], ptr=None if coo else A["ptr"], idx=A["idx"], val=A["val"],
               coo_row=gen.expand_rows(A) if coo else None)
@@ -42,6 +44,6 @@ ms = e0.elapsed_time(e1) / it
 vec_bytes = 12 * A["m"] * 8          # dot(p,Ap) 2, update x,r (4 rd + 2 wr) 6, update p (2 rd + 1 wr) 3, residual ~1
 alg = st["alg_bytes_beta0"] + vec_bytes
 print(json.dumps({"what": "msrep_cg on the SPD 27-point stencil", "format": a.format,
-                  "cuda_graph": os.environ.get("MSREP_CG_GRAPH", "1") != "0", "m": A["m"], "nnz": A.nnz,
+                  "cuda_graph": bool(a.graph), "m": A["m"], "nnz": A.nnz,
                   "iterations": it, "relres": rr, "ms_per_iter": ms, "spmv_alg_bytes": st["alg_bytes_beta0"],
                   "vector_bytes": vec_bytes, "GBps": alg / (ms * 1e-3) / 1e9}), flush=True)

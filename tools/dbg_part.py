@@ -11,10 +11,9 @@ b0, b1 = int(d["start_idx"]), int(d["end_idx"]) + 1
 o0, o1 = int(d["start_row"]), int(d["end_row"]) + 1
 ptr = np.clip(A["ptr"][o0:o1 + 1], b0, b1) - b0
 x = torch.as_tensor(gen.vector(A["n"], 7)).cuda()
-for pol in ("0", "1", None):
-    if pol is None: os.environ.pop("MSREP_XLOAD", None)
-    else: os.environ["MSREP_XLOAD"] = pol
+for pol in (0, 1, -1):
     ctx = M.Context(0, 1, None, 0, 1)
+    ctx.set_tuning("xload", pol)
     ctx.partition("csr", o1 - o0, A["n"], ptr=ptr, idx=A["idx"][b0:b1], val=A["val"][b0:b1])
     y = torch.zeros(o1 - o0, dtype=torch.float64, device="cuda")
     for _ in range(3): ctx.spmv(1.0, x, 0.0, y)
