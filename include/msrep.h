@@ -141,6 +141,9 @@ typedef struct {
   int64_t nhot;              /* hot-x cache entries (MSREP_TUNE_HOT_X; 0: no cache)          */
   int64_t hot_nnz;           /* nonzeros whose x gather the hot cache serves                 */
   int64_t x_compact;         /* compact-x entries (MSREP_TUNE_COMPACT_X; 0: gathers read x)   */
+  int64_t gpu_numa_node;     /* NUMA node of the GPU's PCI function (sysfs; -1 unknown)      */
+  int64_t host_numa_node;    /* MSREP_RESIDENT_HOST: node of the pinned layout's first page,
+                                allocated preferred on gpu_numa_node; else -1    */
   int64_t stream_bytes;      /* bytes the built layout moves per SpMV (beta != 0): tile blobs
                                 as stored + x entries + y; pCOO stores u8 tile row keys, not
                                 the 4-B row ids alg_bytes counts                              */
@@ -319,11 +322,12 @@ msrep_status_t msrep_debug_arrange(const uint32_t* pk, int64_t n, int64_t* order
  * the multi-right-hand-side extension of the same partition (
  * the paper's conclusion on reuse by other sparse kernels).
  * X: device [n x k], Y: device [m x k], both row-major contiguous (X[c*k + j]),
- * k in {2, 4, 8}; the matrix is streamed once for all k vectors.  Row formats
- * (pCSR, pCOO) only -- MSREP_ERR_STATE for pCSC / column-sorted pCOO.
- * Layouts REPLICATED / OWNED as msrep_spmv (segments are row blocks of Y);
- * beta == 0: Y not read; alpha == 0: Y = beta*Y.  Asynchronous on `stream`,
- * collective when nranks > 1. */
+ * k in {2, 4, 8}.  Row formats (pCSR, pCOO): the matrix is streamed once for
+ * all k vectors (layouts REPLICATED / OWNED).  Column formats (pCSC, column-sorted
+ * and unsorted pCOO): one strided pass of the band kernel per vector -- each
+ * with the column-style merge when nranks > 1 -- (layouts REPLICATED / SHARDED).
+ * Segments are row blocks of Y; beta == 0: Y not read; alpha == 0: Y = beta*Y.
+ * Asynchronous on `stream`, collective when nranks > 1. */
 msrep_status_t msrep_spmm(msrep_ctx ctx, const void* alpha, const void* X, const void* beta, void* Y, int k,
                           msrep_layout layout, void* stream);
 

@@ -60,6 +60,7 @@ class Stats(ctypes.Structure):
                                          ("nchunks", ctypes.c_int64), ("host_bytes", ctypes.c_int64),
                                          ("x_no_allocate", ctypes.c_int64), ("nhot", ctypes.c_int64),
                                          ("hot_nnz", ctypes.c_int64), ("x_compact", ctypes.c_int64),
+                                         ("gpu_numa_node", ctypes.c_int64), ("host_numa_node", ctypes.c_int64),
                                          ("stream_bytes", ctypes.c_int64)]
 
 

@@ -9,6 +9,7 @@
 // owned y segment.
 #include <algorithm>
 #include <atomic>
+#include <cctype>
 #include <climits>
 #include <cmath>
 #include <chrono>
@@ -21,8 +22,12 @@
 #include <thread>
 #include <vector>
 
+#include <sys/syscall.h>
+#include <unistd.h>
+
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "internal.h"
 #include "msrep.h"
@@ -30,6 +35,28 @@
 using namespace msrep;
 
 namespace {
+
+// NVTX ranges (header-only NVTX v3; free when no tool is attached): the partition phases and the
+// steps of msrep_spmv (kernel, head exchange, fix-up, collective) show up by name in nsys / ncu
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
+struct NvtxSeq {   // consecutive ranges (phases); the open one is closed on scope exit, error paths too
+  bool on = false;
+  void next(const char* name) {
+    if (on) nvtxRangePop();
+    nvtxRangePushA(name);
+    on = true;
+  }
+  void end() {
+    if (on) nvtxRangePop();
+    on = false;
+  }
+  ~NvtxSeq() { end(); }
+};
 
 thread_local std::string g_err;
 
@@ -176,6 +203,48 @@ void par_ranges(int64_t n, F&& f) {
   f((int64_t)0, n / T);
   for (auto& x : th) x.join();
 }
+// ------------------------------------------------ NUMA placement of pinned host memory
+// Sec. 4.2: host-resident partitions are copied to the GPUs every call, so they should
+// live on the GPU's own NUMA node (without it the paper saw no scaling past 3 GPUs on Summit,
+// P:849).  The node is the one sysfs reports for the GPU's PCI function; pinned buffers are
+// allocated under a preferred-node memory policy (cudaHostAlloc touches and pins the pages, so they
+// land there), then the thread's policy is restored.  No libnuma: the two syscalls directly.
+constexpr int kMpolDefault = 0, kMpolPreferred = 1, kMpolFNode = 1, kMpolFAddr = 2;
+
+int gpu_numa_node(int device) {
+  char bus[64] = {0};
+  if (cudaDeviceGetPCIBusId(bus, sizeof bus, device) != cudaSuccess) { cudaGetLastError(); return -1; }
+  for (char* q = bus; *q; q++) *q = (char)tolower(*q);
+  char path[160];
+  snprintf(path, sizeof path, "/sys/bus/pci/devices/%s/numa_node", bus);
+  FILE* f = fopen(path, "r");
+  if (!f) return -1;
+  int node = -1;
+  if (fscanf(f, "%d", &node) != 1) node = -1;
+  fclose(f);
+  return node;
+}
+
+// node of the page holding p (-1: unknown)
+int page_numa_node(const void* p) {
+  int node = -1;
+  if (!p || syscall(SYS_get_mempolicy, &node, nullptr, 0, const_cast<void*>(p), kMpolFNode | kMpolFAddr) != 0) return -1;
+  return node;
+}
+
+// cudaHostAlloc with the pages preferred on `node` (node < 0: plain cudaHostAlloc)
+cudaError_t host_alloc_on(void** out, size_t bytes, int node) {
+  bool bound = false;
+  if (node >= 0 && node < 1024) {
+    unsigned long mask[1024 / (8 * sizeof(unsigned long))] = {0};
+    mask[node / (8 * sizeof(unsigned long))] = 1ul << (node % (8 * sizeof(unsigned long)));
+    bound = syscall(SYS_set_mempolicy, kMpolPreferred, mask, (unsigned long)1024) == 0;
+  }
+  const cudaError_t e = cudaHostAlloc(out, bytes, cudaHostAllocDefault);
+  if (bound) syscall(SYS_set_mempolicy, kMpolDefault, nullptr, 0ul);
+  return e;
+}
+
 // ---------------------------------------------------------------- memory
 struct DevBuf {
   void* p = nullptr;
@@ -184,6 +253,7 @@ struct DevBuf {
 
 struct Ctx {
   int rank = 0, nranks = 1, vparts = 1, np = 1, device = 0;
+  int numa_node = -1;               // the GPU's NUMA node (sysfs), for pinned host buffers
   msrep_split split = MSREP_SPLIT_NNZ;
   std::vector<int> groups;          // MSREP_SPLIT_TWO_LEVEL: parts per NUMA group
   ncclComm_t comm = nullptr;
@@ -231,10 +301,9 @@ struct Ctx {
   int4* d_cunits = nullptr;          // units of work (see CscBands)
   int2* d_bsplit = nullptr;
   double* d_slots = nullptr;
-  int4* d_tasks = nullptr;
   int* d_tickets = nullptr;
   int* d_ctr = nullptr;
-  int64_t ntasks = 0, nslots = 0;
+  int64_t nslots = 0;
   int32_t* d_item_hst = nullptr;
   int32_t* d_item_hw = nullptr;
   int32_t* d_item_sst = nullptr;
@@ -271,7 +340,7 @@ struct Ctx {
   bool split_launch = false;        // SELL tiles and SEG tiles run as two launches (each >= 5-10 % of nnz)
   int residency = MSREP_RESIDENT_DEVICE;
   int64_t chunk_bytes = (int64_t)256 << 20;
-  struct Chunk { int32_t t0, t1, u0, u1; int64_t off, bytes; bool has_sell; int32_t k0 = 0, k1 = 0; };
+  struct Chunk { int32_t t0, t1, u0, u1; int64_t off, bytes; bool has_sell; };
   std::vector<Chunk> chunks;
   char* h_blob = nullptr;           // pinned (cudaHostAlloc)
   int64_t h_bytes = 0;
@@ -382,7 +451,7 @@ msrep_status_t h2d(Ctx* c, void* dst, const void* src, size_t bytes, cudaStream_
   }
   if (!c->h_ring[0] && !c->ring_disabled) {
     for (int b = 0; b < 2; b++) {
-      if (cudaHostAlloc(reinterpret_cast<void**>(&c->h_ring[b]), kRingSlot, cudaHostAllocDefault) != cudaSuccess) {
+      if (host_alloc_on(reinterpret_cast<void**>(&c->h_ring[b]), kRingSlot, c->numa_node) != cudaSuccess) {
         cudaGetLastError();   // no pinned memory to spare: the driver's pageable path still works
         for (int q = 0; q < 2; q++) {
           if (c->h_ring[q]) cudaFreeHost(c->h_ring[q]);
@@ -596,7 +665,6 @@ struct CscBands {
   int64_t chunk = CB_CHUNK;               // columns per chunk
   std::vector<int4> units;                // {band, first stage, end stage, slot (-1: whole band)}
   std::vector<int2> bsplit;               // [nb]: {first slot, slots} of a split band, {0, 0} otherwise
-  std::vector<int4> tasks;                // reduction tasks {band, first row, end row, 0} (band order)
   int64_t nslots = 0;
   std::vector<int32_t> item_hst;          // [items]: stages that may hold same-row groups
   std::vector<int32_t> item_hw;           // [items * CB_W]: same-row groups leading each warp list
@@ -621,7 +689,13 @@ struct CscBands {
 #define MSREP_SEG_RATIO 3
 #endif
 constexpr int64_t SEG_RATIO = MSREP_SEG_RATIO;
-constexpr int64_t CB_TASK_ROWS = 512;   // rows of a split band per reduction task   // segmented tail iff greedy groups >= SEG_RATIO x segmented groups
+#ifndef MSREP_CB_SPLIT_DIV
+#define MSREP_CB_SPLIT_DIV 1   // pCSC: split a band holding more than share / DIV stages (share = stages / SMs)
+#endif
+#ifndef MSREP_CB_PIECE_DIV
+#define MSREP_CB_PIECE_DIV 2   // ... into units of about share / DIV stages
+#endif
+   // segmented tail iff greedy groups >= SEG_RATIO x segmented groups
 struct ArrangeScratch {
   int64_t same = 0;   // entries the last arrange_list placed in same-row groups
   int64_t seg_from = INT64_MAX;   // list position (a multiple of 32) where its segmented groups start
@@ -747,8 +821,15 @@ int64_t arrange_list(const uint32_t* pk, int64_t n, ArrangeScratch& A, Emit&& em
   return w;
 }
 
+thread_local double g_csc_ms[6];   // sub-phase times of the last build_csc_bands (diagnostics)
 msrep_status_t build_csc_bands(const Ctx& c, const std::vector<int64_t>& lp, const int32_t* idx, const void* val,
                                size_t V, int sms, CscBands& B) {
+  auto tq = std::chrono::steady_clock::now();
+  auto lapq = [&](int k) {
+    const auto now = std::chrono::steady_clock::now();
+    g_csc_ms[k] = std::chrono::duration<double, std::milli>(now - tq).count();
+    tq = now;
+  };
   const int64_t W = c.whi - c.wlo;
   const int64_t nz = c.B_hi - c.B_lo;
   const int32_t* rows = idx + c.B_lo;
@@ -802,21 +883,32 @@ msrep_status_t build_csc_bands(const Ctx& c, const std::vector<int64_t>& lp, con
     sp[CB_W] = (int32_t)nr;
   }
   rc.reset();
-  auto warp_of = [&](int64_t b, int32_t ro) {
-    const int32_t* sp = &B.split[(size_t)(b * SW)];
-    const int w = (int)(std::upper_bound(sp, sp + SW, ro) - sp) - 1;
-    return w < CB_W - 1 ? w : CB_W - 1;
-  };
-  auto key_of = [&](int64_t q, int32_t r) {
-    const int64_t b = r / CB_ROWS;
-    return (b * B.nch + q / B.chunk) * CB_W + warp_of(b, r % CB_ROWS);
-  };
-  // 1. stable counting sort by key into temporary (pk, val) arrays
+  lapq(0);
+  // warp owning each row (a byte per row): the sort below needs no search per entry
+  std::unique_ptr<uint8_t[]> wl(new uint8_t[(size_t)std::max<int64_t>(1, c.m)]);
+  run([&](int t) {
+    for (int64_t b = B.nb * t / T; b < B.nb * (t + 1) / T; b++) {
+      const int32_t* sp = &B.split[(size_t)(b * SW)];
+      const int64_t r0 = b * CB_ROWS, nr = std::min<int64_t>(CB_ROWS, c.m - r0);
+      int w = 0;
+      for (int64_t o = 0; o < nr; o++) {
+        while (w < CB_W - 1 && o >= sp[w + 1]) w++;
+        wl[(size_t)(r0 + o)] = (uint8_t)w;
+      }
+    }
+  });
+  const int64_t nch = B.nch, chunk = B.chunk;
+  // 1. stable counting sort by key = (band, column chunk, warp) into temporary (pk, val) arrays
   std::vector<std::vector<int64_t>> off((size_t)T, std::vector<int64_t>((size_t)keys, 0));
   run([&](int t) {
-    auto& o = off[(size_t)t];
-    for (int64_t q = cb[(size_t)t]; q < cb[(size_t)t + 1]; q++)
-      for (int64_t z = lp[(size_t)q]; z < lp[(size_t)q + 1]; z++) o[(size_t)key_of(q, rows[z])]++;
+    int64_t* o = off[(size_t)t].data();
+    for (int64_t q = cb[(size_t)t]; q < cb[(size_t)t + 1]; q++) {
+      const int64_t qc = q / chunk;
+      for (int64_t z = lp[(size_t)q]; z < lp[(size_t)q + 1]; z++) {
+        const int32_t r = rows[z];
+        o[(((int64_t)(r >> CB_LOG2)) * nch + qc) * CB_W + wl[(size_t)r]]++;
+      }
+    }
   });
   std::vector<int64_t> kbeg((size_t)keys + 1);
   int64_t run_off = 0;
@@ -831,18 +923,29 @@ msrep_status_t build_csc_bands(const Ctx& c, const std::vector<int64_t>& lp, con
   kbeg[(size_t)keys] = run_off;
   std::unique_ptr<uint32_t[]> tpk(new uint32_t[(size_t)std::max<int64_t>(1, nz)]);
   std::unique_ptr<char[]> tval(new char[(size_t)std::max<int64_t>(1, nz) * V]);
-  run([&](int t) {
-    auto& o = off[(size_t)t];
-    for (int64_t q = cb[(size_t)t]; q < cb[(size_t)t + 1]; q++)
-      for (int64_t z = lp[(size_t)q]; z < lp[(size_t)q + 1]; z++) {
-        const int32_t r = rows[z];
-        const int64_t dst = o[(size_t)key_of(q, r)]++;
-        tpk[(size_t)dst] = (uint32_t)(r % CB_ROWS) | ((uint32_t)(q % B.chunk) << CB_LOG2);
-        memcpy(tval.get() + (size_t)dst * V, vals + (size_t)z * V, V);
+  auto scatter = [&](auto vtag) {
+    using VT = decltype(vtag);
+    const VT* vv = reinterpret_cast<const VT*>(vals);
+    VT* tv = reinterpret_cast<VT*>(tval.get());
+    run([&](int t) {
+      int64_t* o = off[(size_t)t].data();
+      for (int64_t q = cb[(size_t)t]; q < cb[(size_t)t + 1]; q++) {
+        const int64_t qc = q / chunk;
+        const uint32_t qm = (uint32_t)(q - qc * chunk) << CB_LOG2;
+        for (int64_t z = lp[(size_t)q]; z < lp[(size_t)q + 1]; z++) {
+          const int32_t r = rows[z];
+          const int64_t dst = o[(((int64_t)(r >> CB_LOG2)) * nch + qc) * CB_W + wl[(size_t)r]]++;
+          tpk[(size_t)dst] = (uint32_t)(r & (CB_ROWS - 1)) | qm;
+          tv[(size_t)dst] = vv[(size_t)z];
+        }
       }
-  });
+    });
+  };
+  if (V == 8) scatter(double{}); else scatter(float{});
+  wl.reset();
   off.clear();
   off.shrink_to_fit();
+  lapq(1);
   std::atomic<int64_t> next_key{0};
   auto each_key = [&](auto&& f) {
     run([&](int) {
@@ -864,6 +967,7 @@ msrep_status_t build_csc_bands(const Ctx& c, const std::vector<int64_t>& lp, con
     asame[(size_t)k] = scr.same;
     aseg[(size_t)k] = scr.seg_from;
   });
+  lapq(2);
   // 3. items: one per non-empty (band, chunk); stage geometry and blob offsets
   B.band_item.assign((size_t)B.nb + 1, 0);
   std::vector<int64_t> key_item((size_t)(B.nb * B.nch), -1);
@@ -901,7 +1005,7 @@ msrep_status_t build_csc_bands(const Ctx& c, const std::vector<int64_t>& lp, con
   // Units of work (fetched dynamically by the CTAs, largest first): a whole band, or -- for a band
   // heavier than `per` stages (R-MAT's first bands, short-wide matrices with fewer bands than SMs)
   // -- equal stage ranges of it, each parking its partial rows in a slot; the band's rows are then
-  // reduced over its slots in slot order by reduction tasks of CB_TASK_ROWS rows (deterministic).
+  // reduced over its slots in slot order by the band's last unit to finish (deterministic).
   {
     std::vector<int64_t> st((size_t)B.nb, 0);
     int64_t tot = 0;
@@ -911,21 +1015,20 @@ msrep_status_t build_csc_bands(const Ctx& c, const std::vector<int64_t>& lp, con
     }
     // a band is split when it holds more than one SM's share of the stages (tot / sms), into
     // pieces of about half a share: with largest-first dynamic fetching the tail is then short
-    const int64_t share = std::max<int64_t>(64, (tot + sms - 1) / sms), per = share / 2;
+    const int64_t share = std::max<int64_t>(64, (tot + sms - 1) / sms);
+    const int64_t per = std::max<int64_t>(16, share / MSREP_CB_PIECE_DIV), cut = share / MSREP_CB_SPLIT_DIV;
     B.bsplit.assign((size_t)B.nb, make_int2(0, 0));
     for (int64_t b = 0; b < B.nb; b++) {
       const int64_t sb = st[(size_t)b];
-      const int64_t k = sb > share ? (sb + per - 1) / per : 1;
+      const int64_t k = sb > cut ? (sb + per - 1) / per : 1;
       if (k == 1) { B.units.push_back(make_int4((int32_t)b, 0, (int32_t)sb, -1)); continue; }
       B.bsplit[(size_t)b] = make_int2((int32_t)B.nslots, (int32_t)k);
       for (int64_t q = 0; q < k; q++)
         B.units.push_back(make_int4((int32_t)b, (int32_t)(sb * q / k), (int32_t)(sb * (q + 1) / k), (int32_t)(B.nslots + q)));
       B.nslots += k;
-      const int64_t nr = std::min<int64_t>(CB_ROWS, c.m - b * CB_ROWS);
-      for (int64_t r = 0; r < nr; r += CB_TASK_ROWS)
-        B.tasks.push_back(make_int4((int32_t)b, (int32_t)r, (int32_t)std::min<int64_t>(nr, r + CB_TASK_ROWS), 0));
     }
   }
+  lapq(3);
   B.blob.reset(new char[(size_t)std::max<int64_t>(16, bytes)]);
   // 4. write every list into its item's stage blobs; pad it with holes to the item's length
   each_key([&](int64_t k, ArrangeScratch& scr) {
@@ -948,6 +1051,7 @@ msrep_status_t build_csc_bands(const Ctx& c, const std::vector<int64_t>& lp, con
     int64_t pos = n ? arrange_list(tpk.get() + b0, n, scr, put) : 0;
     for (; pos < L; pos++) put(pos, -1);
   });
+  lapq(4);
   return MSREP_OK;
 }
 
@@ -1033,8 +1137,9 @@ ColLaunch col_launch(const Ctx* c, const void* x, void* y, double alpha, double 
   L.items = c->d_citems; L.item_off = c->d_item_off; L.band_item = c->d_band_item; L.split = c->d_split;
   L.nb = (int)c->cnb; L.blob = c->d_cblob;
   L.x = x; L.xbase = c->wlo;
+  L.xs = 1; L.ys = 1;
   L.nunits = (int)c->cunits; L.units = c->d_cunits; L.bsplit = c->d_bsplit; L.slots = c->d_slots;
-  L.ntasks = (int)c->ntasks; L.tasks = c->d_tasks; L.tickets = c->d_tickets; L.ctr = c->d_ctr;
+  L.tickets = c->d_tickets; L.ctr = c->d_ctr;
   L.item_hst = c->d_item_hst; L.item_hw = c->d_item_hw; L.item_sst = c->d_item_sst; L.item_sg = c->d_item_sg;
   L.fused = c->nranks == 1;
   L.out = L.fused ? y : static_cast<void*>(c->d_py);
@@ -1340,6 +1445,7 @@ msrep_status_t msrep_create(msrep_ctx* out, int rank, int nranks, const uint8_t 
   c->vparts = parts_per_rank;
   c->np = nranks * parts_per_rank;
   c->device = device;
+  c->numa_node = gpu_numa_node(device);
   if (alloc) { c->alloc = *alloc; c->has_alloc = true; }
   if (nranks > 1) {
     ncclUniqueId u;
@@ -1380,13 +1486,18 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   if (!h) return fail(MSREP_ERR_INVALID_ARG, "ctx is NULL");
   Ctx* c = reinterpret_cast<Ctx*>(h);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Nvtx nv_all("msrep_partition");
   const auto t0 = std::chrono::steady_clock::now();
   double phase[4] = {0, 0, 0, 0};
+  static const char* kPhase[4] = {"partition: validate", "partition: plan", "partition: schedule", "partition: upload+pack"};
   auto tl = t0;
+  NvtxSeq nv_phase;
+  nv_phase.next(kPhase[0]);
   auto lap = [&](int k) {
     const auto now = std::chrono::steady_clock::now();
     phase[k] += std::chrono::duration<double, std::milli>(now - tl).count();
     tl = now;
+    nv_phase.next(kPhase[k == 3 ? 3 : k + 1]);
   };
   // ---- validation (before any device work)
   if (fmt != MSREP_CSR && fmt != MSREP_CSC && fmt != MSREP_COO && fmt != MSREP_COO_COL && fmt != MSREP_COO_UNSORTED)
@@ -1555,7 +1666,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     std::vector<std::pair<int64_t, int64_t>> uranges;
     if (c->residency == MSREP_RESIDENT_HOST) {
       // park the band blobs in pinned memory; chunks = runs of whole bands of <= chunk_bytes
-      CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&c->h_blob), (size_t)std::max<int64_t>(16, CB.bytes), cudaHostAllocDefault));
+      CUDA_TRY(host_alloc_on(reinterpret_cast<void**>(&c->h_blob), (size_t)std::max<int64_t>(16, CB.bytes), c->numa_node));
       {
         char* hb = c->h_blob;
         const char* sb = CB.blob.get();
@@ -1566,7 +1677,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
         const int32_t i = CB.band_item[(size_t)b];
         return i < (int32_t)CB.items.size() ? CB.item_off[(size_t)i] : CB.bytes;
       };
-      size_t u = 0, k = 0;
+      size_t u = 0;
       for (int64_t b = 0; b < CB.nb;) {
         const int64_t off0 = band_off(b);
         int64_t e = b + 1;
@@ -1574,9 +1685,6 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
         Ctx::Chunk ch{(int32_t)b, (int32_t)e, (int32_t)u, 0, off0, band_off(e) - off0, false};
         while (u < CB.units.size() && CB.units[u].x < e) u++;
         ch.u1 = (int32_t)u;
-        ch.k0 = (int32_t)k;
-        while (k < CB.tasks.size() && CB.tasks[k].x < e) k++;
-        ch.k1 = (int32_t)k;
         c->chunks.push_back(ch);
         uranges.push_back({ch.u0, ch.u1});
         b = e;
@@ -1593,9 +1701,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
                        [](const int4& a, const int4& b) { return a.z - a.y > b.z - b.y; });
     TRY(upload_vec(c, CB.units, &c->d_cunits, s));
     TRY(upload_vec(c, CB.bsplit, &c->d_bsplit, s));
-    TRY(upload_vec(c, CB.tasks, &c->d_tasks, s));
     c->cunits = (int64_t)CB.units.size();
-    c->ntasks = (int64_t)CB.tasks.size();
     c->nslots = CB.nslots;
     {
       void* q;
@@ -1842,7 +1948,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     TRY(dalloc(c, (size_t)std::max<int64_t>(16, pack_bytes), &bp, s));
     char* d_pack = static_cast<char*>(bp);
     if (host_res) {
-      CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&c->h_blob), (size_t)std::max<int64_t>(16, blob_total), cudaHostAllocDefault));
+      CUDA_TRY(host_alloc_on(reinterpret_cast<void**>(&c->h_blob), (size_t)std::max<int64_t>(16, blob_total), c->numa_node));
       c->h_bytes = blob_total;
       c->d_blob = nullptr;
     } else {
@@ -1902,6 +2008,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   }
   CUDA_TRY(cudaStreamSynchronize(s));
   lap(3);
+  nv_phase.end();
   const auto t1 = std::chrono::steady_clock::now();
   TRY(tune_xload(c, s, nz_r));   // outside the partition timer: a measurement, not partitioning
 
@@ -1920,6 +2027,8 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   st.x_no_allocate = c->xna;
   st.nhot = c->nhot;
   st.x_compact = c->nxc;
+  st.gpu_numa_node = c->numa_node;
+  st.host_numa_node = c->h_blob ? page_numa_node(c->h_blob) : -1;
   st.hot_nnz = c->hot_nnz;
   int64_t X = 0;
   if (colwise(fmt)) {
@@ -2027,9 +2136,46 @@ msrep_status_t msrep_spmv_mirror(msrep_ctx h, const void* alpha_p, const void* x
   return MSREP_OK;
 }
 
+// Column formats (pCSC, column-sorted / unsorted pCOO): vector j of a k-wide row-major block (k = 1:
+// SpMV) -- the band kernel with strides k, then for nranks > 1 the reduce-scatter of the fp64
+// partial y and the alpha/beta epilogue on this rank's shard [my_lo, my_hi) (Sec. 4.3)
+msrep_status_t col_spmv(Ctx* c, double alpha, const void* x, double beta, void* y, int k, int j, int64_t my_lo,
+                        int64_t my_hi, cudaStream_t s) {
+  const size_t V = vsz(c->dtype);
+  const int dt = c->dtype == MSREP_F64 ? 0 : 1;
+  ColLaunch L = col_launch(c, static_cast<const char*>(x) + (size_t)j * V, static_cast<char*>(y) + (size_t)j * V,
+                           alpha, beta);
+  L.xs = k;
+  L.ys = k;
+  cudaEvent_t pe;
+  TRY(prof_begin(c, s, &pe));
+  if (c->residency == MSREP_RESIDENT_HOST) {
+    TRY(stream_chunks(c, s, [&](const Ctx::Chunk& ch, const char* base) -> msrep_status_t {
+      ColLaunch Lc = L;
+      Lc.blob = base;
+      Lc.band0 = ch.t0; Lc.nb = ch.t1 - ch.t0;
+      Lc.units = L.units + ch.u0; Lc.nunits = ch.u1 - ch.u0;
+      CUDA_TRY(launch_cols(Lc, s));
+      return MSREP_OK;
+    }));
+  } else {
+    CUDA_TRY(launch_cols(L, s));
+  }
+  if (pe) CUDA_TRY(cudaEventRecord(pe, s));
+  if (c->nranks > 1) {
+    double* shard = c->d_py + (size_t)c->rank * c->shard;
+    NCCL_TRY(ncclReduceScatter(c->d_py, shard, (size_t)c->shard, ncclDouble, ncclSum, c->comm, s));
+    CUDA_TRY(launch_axpby_py(shard, static_cast<char*>(y) + ((size_t)my_lo * k + j) * V, my_hi - my_lo, alpha, beta,
+                             dt, s, k));
+  }
+  return MSREP_OK;
+}
+
 msrep_status_t spmv_impl(msrep_ctx h, const void* alpha_p, const void* x, const void* beta_p, void* y,
                          msrep_layout layout, void* stream, int nmirror, void* const* mirrors) {
   if (!h) return fail(MSREP_ERR_INVALID_ARG, "ctx is NULL");
+  Nvtx nv_call("msrep_spmv");
+  NvtxSeq nv;
   Ctx* c = reinterpret_cast<Ctx*>(h);
   if (!c->ready) return fail(MSREP_ERR_STATE, "msrep_spmv before msrep_partition");
   if (!alpha_p || !beta_p) return fail(MSREP_ERR_INVALID_ARG, "alpha/beta NULL");
@@ -2058,33 +2204,18 @@ msrep_status_t spmv_impl(msrep_ctx h, const void* alpha_p, const void* x, const 
   }
 
   if (colwise(c->fmt)) {
-    ColLaunch L = col_launch(c, x, y, alpha, beta);
-    cudaEvent_t pe;
-    TRY(prof_begin(c, s, &pe));
-    if (c->residency == MSREP_RESIDENT_HOST) {
-      TRY(stream_chunks(c, s, [&](const Ctx::Chunk& ch, const char* base) -> msrep_status_t {
-        ColLaunch Lc = L;
-        Lc.blob = base;
-        Lc.band0 = ch.t0; Lc.nb = ch.t1 - ch.t0;
-        Lc.units = L.units + ch.u0; Lc.nunits = ch.u1 - ch.u0;
-        Lc.tasks = L.tasks + ch.k0; Lc.ntasks = ch.k1 - ch.k0;
-        CUDA_TRY(launch_cols(Lc, s));
-        return MSREP_OK;
-      }));
-    } else {
-      CUDA_TRY(launch_cols(L, s));
-    }
-    if (pe) CUDA_TRY(cudaEventRecord(pe, s));
-    if (c->nranks > 1) {
-      double* shard = c->d_py + (size_t)c->rank * c->shard;
-      NCCL_TRY(ncclReduceScatter(c->d_py, shard, (size_t)c->shard, ncclDouble, ncclSum, c->comm, s));
-      CUDA_TRY(launch_axpby_py(shard, static_cast<char*>(y) + (size_t)my_lo * V, my_hi - my_lo, alpha, beta, dt, s));
-      if (gather) TRY(allgatherv_y(c, y, seg_lo, seg_hi, s));
+    nv.next("spmv: band kernel + reduce-scatter");
+    TRY(col_spmv(c, alpha, x, beta, y, 1, 0, my_lo, my_hi, s));
+    if (gather) {
+      nv.next("spmv: allgatherv");
+      TRY(allgatherv_y(c, y, seg_lo, seg_hi, s));
     }
     return MSREP_OK;
   }
 
+  nv.next("spmv: compact x gather");
   TRY(prepare_x(c, x, 1, s));
+  nv.next("spmv: tile kernel");
   RowLaunch L = row_launch(c, x, y, alpha, beta);
   L.nmirror = nmirror;
   for (int mi = 0; mi < nmirror; mi++) L.mirror[mi] = mirrors[mi];
@@ -2103,11 +2234,13 @@ msrep_status_t spmv_impl(msrep_ctx h, const void* alpha_p, const void* x, const 
   }
   if (pe) CUDA_TRY(cudaEventRecord(pe, s));
   if (c->nranks > 1 && c->any_flag) {
+    nv.next("spmv: head exchange");
     HeadLaunch H{c->vparts, c->d_part_rec, c->d_rec, c->d_head_local, 1};
     CUDA_TRY(launch_heads(H, s));
     NCCL_TRY(ncclAllGather(c->d_head_local, c->d_head_all, (size_t)c->vparts, ncclDouble, c->comm, s));
   }
   if (c->nsplit) {
+    nv.next("spmv: fix-up");
     FixupLaunch F{};
     F.nsplit = c->nsplit;
     F.sr_row = c->d_sr_row; F.sr_rec = c->d_sr_rec; F.sr_head = c->d_sr_head; F.head_list = c->d_head_list;
@@ -2118,7 +2251,10 @@ msrep_status_t spmv_impl(msrep_ctx h, const void* alpha_p, const void* x, const 
     for (int mi = 0; mi < nmirror; mi++) F.mirror[mi] = mirrors[mi];
     CUDA_TRY(launch_fixup(F, s));
   }
-  if (gather) TRY(allgatherv_y(c, y, seg_lo, seg_hi, s));
+  if (gather) {
+    nv.next("spmv: allgatherv");
+    TRY(allgatherv_y(c, y, seg_lo, seg_hi, s));
+  }
   return MSREP_OK;
 }
 
@@ -2127,10 +2263,11 @@ msrep_status_t msrep_spmm(msrep_ctx h, const void* alpha_p, const void* X, const
   if (!h) return fail(MSREP_ERR_INVALID_ARG, "ctx is NULL");
   Ctx* c = reinterpret_cast<Ctx*>(h);
   if (!c->ready) return fail(MSREP_ERR_STATE, "msrep_spmm before msrep_partition");
-  if (colwise(c->fmt)) return fail(MSREP_ERR_STATE, "msrep_spmm supports the row formats (pCSR, pCOO)");
   if (k != 2 && k != 4 && k != 8) return fail(MSREP_ERR_INVALID_ARG, "k = %d (must be 2, 4 or 8)", k);
   if (!alpha_p || !beta_p || (c->m > 0 && !Y) || (c->n > 0 && !X)) return fail(MSREP_ERR_INVALID_ARG, "NULL argument");
-  if (layout != MSREP_Y_REPLICATED && layout != MSREP_Y_OWNED) return fail(MSREP_ERR_INVALID_ARG, "layout %d", (int)layout);
+  if (colwise(c->fmt) ? (layout != MSREP_Y_REPLICATED && layout != MSREP_Y_SHARDED)
+                      : (layout != MSREP_Y_REPLICATED && layout != MSREP_Y_OWNED))
+    return fail(MSREP_ERR_INVALID_ARG, "layout %d for this format", (int)layout);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const double alpha = get_scalar(alpha_p, c->dtype), beta = get_scalar(beta_p, c->dtype);
   const size_t V = vsz(c->dtype);
@@ -2141,6 +2278,11 @@ msrep_status_t msrep_spmm(msrep_ctx h, const void* alpha_p, const void* X, const
   const bool gather = layout == MSREP_Y_REPLICATED && c->nranks > 1;
   if (alpha == 0.0) {   // reading R12: Y = beta*Y, A and X not read
     CUDA_TRY(launch_scale(static_cast<char*>(Y) + (size_t)my_lo * k * V, (my_hi - my_lo) * k, beta, dt, s));
+    if (gather) TRY(allgatherv_y(c, Y, seg_lo, seg_hi, s, k));
+    return MSREP_OK;
+  }
+  if (colwise(c->fmt)) {   // one strided pass of the band kernel (and merge) per vector of the block
+    for (int j = 0; j < k; j++) TRY(col_spmv(c, alpha, X, beta, Y, k, j, my_lo, my_hi, s));
     if (gather) TRY(allgatherv_y(c, Y, seg_lo, seg_hi, s, k));
     return MSREP_OK;
   }

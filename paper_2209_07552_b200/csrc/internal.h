@@ -169,20 +169,20 @@ struct ColLaunch {
   int nb, band0;              // bands [band0, band0 + nb) (band0 > 0: a host-resident chunk)
   const char* blob;
   const void* x; int64_t xbase;                              // x index of window column 0
+  int xs, ys;                 // element strides of x and (fused) y: 1 for SpMV; k for one vector of an SpMM block
   void* out; int64_t m;                                      // fused: y (dtype); else fp64 py
   double alpha, beta;
   int fused; int dtype;
   // Units of work, fetched dynamically (ctr[0]) by the CTAs, largest first: {band, first stage,
   // end stage, slot}, stages counted over the band's items in order.  slot < 0: the whole band,
   // written out at the unit's end; slot >= 0: a stage range of a heavy ("split") band whose
-  // partial rows go to slots[slot][CB_ROWS] -- the band's slots are reduced in slot order by the
-  // reduction tasks at the end of the launch (deterministic, no atomics on values).
+  // partial rows go to slots[slot][CB_ROWS] -- the band's LAST unit to finish (ticket) adds the
+  // band's slots in slot order and writes the rows (deterministic, no atomics on values).
   int nunits; const int4* units;
   const int2* bsplit;         // [total bands]: {first slot, slots} of a split band ({0, 0} otherwise)
   double* slots;
-  int ntasks; const int4* tasks;   // reduction tasks {band, first row, end row (band-local), 0}
   int* tickets;               // [total bands]: units of a split band that have written their slot
-  int* ctr;                   // [4]: next unit, finished CTAs, next task (reset by the last CTA)
+  int* ctr;                   // [2]: next unit, finished CTAs (reset by the last CTA)
   const int32_t* item_hst;    // [items]: stages [0, item_hst[i]) may hold same-row groups
   const int32_t* item_hw;     // [items * CB_W]: same-row groups leading warp w's list of item i
   const int32_t* item_sst;    // [items]: stages [item_sst[i], ...) may hold segmented groups
@@ -217,7 +217,7 @@ cudaError_t launch_fixup(const FixupLaunch& L, cudaStream_t s);
 cudaError_t launch_heads(const HeadLaunch& L, cudaStream_t s);
 cudaError_t launch_scale(void* y, int64_t count, double beta, int dtype, cudaStream_t s);   // y = beta*y
 cudaError_t launch_axpby_py(const double* py, void* y, int64_t count, double alpha, double beta, int dtype,
-                            cudaStream_t s);                                                // y = alpha*py + beta*y
+                            cudaStream_t s, int ystride = 1);                               // y = alpha*py + beta*y
 cudaError_t launch_rebase(const int64_t* gptr, int32_t* lptr, int64_t count, int64_t lo, int64_t hi,
                           cudaStream_t s);                                                  // clamp(gptr,lo,hi)-lo
 cudaError_t launch_pack(const PackLaunch& L, cudaStream_t s);

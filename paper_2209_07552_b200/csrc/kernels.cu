@@ -320,7 +320,6 @@ __global__ void __launch_bounds__(HOT ? HOT_WARPS * 32 : WARPS * 32,
   const VT* __restrict__ x = static_cast<const VT*>(P.x);
   VT* __restrict__ y = static_cast<VT*>(P.y);
   const double alpha = P.alpha, beta = P.beta;
-  const uint32_t xmax = P.xmax;
   const uint64_t xpol = policy_evict_last();
   VT* hx = reinterpret_cast<VT*>(smem + Lay::HOT_OFF);
   // CL == 2: the hot slots are split over the CTA pair of the cluster (slots [r*hpc, (r+1)*hpc) in
@@ -811,6 +810,10 @@ __global__ void __launch_bounds__(WARPS * 32, MSREP_ROW_MINB) rows_mm_kernel(con
 #define MSREP_CB_NS 4
 #endif
 constexpr int CB_NS = MSREP_CB_NS;         // stages
+#ifndef MSREP_CB_DEPTH
+#define MSREP_CB_DEPTH 2
+#endif
+constexpr int CB_DEPTH = MSREP_CB_DEPTH;   // stages a consumer warp holds in registers (2 or 3)
 constexpr int CB_NC = CB_W * 32;
 constexpr int CB_THREADS = CB_NC + 32;     // + one producer warp
 constexpr int CB_PER = CB_SEG / 32;        // entries per lane per stage
@@ -828,11 +831,6 @@ struct CBLayout {
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
-__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 
 // one consumer warp's share of a stage, in registers
 template <typename VT>
@@ -847,7 +845,7 @@ struct CBStage {
 template <typename VT, bool NA>
 __device__ __forceinline__ void cb_load(CBStage<VT>& S, int it, const unsigned char* smem, const int4* sdesc,
                                         uint64_t* full, uint64_t* empty, const VT* x, uint64_t xpol, int warp,
-                                        int lane) {
+                                        int lane, int xs) {
   using L = CBLayout<VT>;
   constexpr int V = (int)sizeof(VT);
   const int s = it % CB_NS;
@@ -869,9 +867,10 @@ __device__ __forceinline__ void cb_load(CBStage<VT>& S, int it, const unsigned c
   fence_proxy_async();   // the stage's reads are ordered before the producer's next TMA into it
   __syncwarp();
   if (lane == 0) mbar_arrive(&empty[s]);   // the stage is free: the data is in registers
-  const VT* xb = x + S.d.z;
+  const VT* xb = x + (int64_t)S.d.z * xs;
 #pragma unroll
-  for (int k = 0; k < CB_PER; k++) S.xv[k] = S.pk[k] != CB_HOLE ? ldx<NA>(xb + (S.pk[k] >> CB_LOG2), xpol) : VT(0);
+  for (int k = 0; k < CB_PER; k++)
+    S.xv[k] = S.pk[k] != CB_HOLE ? ldx<NA>(xb + (int64_t)(S.pk[k] >> CB_LOG2) * xs, xpol) : VT(0);
 }
 
 // CB_PUT rows (row0 + i*stride, i < CB_PUT, those < row_end) receive their full sums a[i]:
@@ -887,7 +886,7 @@ __device__ __forceinline__ void cb_put(const ColLaunch& P, int64_t row0, int str
 #pragma unroll
     for (int i = 0; i < CB_PUT; i++) {
       const int64_t r = row0 + (int64_t)i * stride;
-      yv[i] = (P.beta != 0.0 && r < row_end) ? (double)__ldcs(y + r) : 0.0;
+      yv[i] = (P.beta != 0.0 && r < row_end) ? (double)__ldcs(y + r * P.ys) : 0.0;
     }
 #pragma unroll
     for (int i = 0; i < CB_PUT; i++) {
@@ -895,7 +894,7 @@ __device__ __forceinline__ void cb_put(const ColLaunch& P, int64_t row0, int str
       if (r < row_end) {
         double o = P.alpha * a[i];
         if (P.beta != 0.0) o += P.beta * yv[i];
-        __stcs(y + r, (VT)o);
+        __stcs(y + r * P.ys, (VT)o);
       }
     }
   } else {
@@ -944,32 +943,59 @@ __global__ void __launch_bounds__(CB_THREADS, 1) csc_band_kernel(const ColLaunch
       __syncwarp();
       it++;
     };
-    for (;;) {
+    // the next unit is fetched (and its band's item range loaded) one unit ahead, and the item
+    // descriptors of a band come in warp-wide batches of 32 -- R-MAT bands average ~3 stages per
+    // item, so per-item dependent loads would starve the stage ring
+    auto fetch = [&](int4& un, int& i0, int& i1) {
       int u = 0;
       if (lane == 0) u = atomicAdd(&P.ctr[0], 1);
       u = __shfl_sync(FULL, u, 0);
-      if (u >= P.nunits) break;
-      const int4 un = P.units[u];
-      const int b = un.x, i0 = P.band_item[b], i1 = P.band_item[b + 1];
+      if (u >= P.nunits) return false;
+      un = P.units[u];
+      i0 = P.band_item[un.x];
+      i1 = P.band_item[un.x + 1];
+      return true;
+    };
+    int4 un;
+    int i0, i1;
+    // a unit is claimed only when the previous one is fully issued (claiming ahead would hoard units
+    // at the tail: banded pCSC 0.27 -> 0.50 ms); the stage ring covers the fetch latency
+    while (fetch(un, i0, i1)) {
+      const int b = un.x;
       int g = 0;   // band stage index of the item's first stage
-      for (int i = i0; i < i1 && g < un.z; i++) {
-        const int4 item = P.items[i];
-        if (g + item.y <= un.y) { g += item.y; continue; }
-        const int hst = P.item_hst[i], sst = P.item_sst[i];
-        const int q0 = un.y > g ? un.y - g : 0, q1 = min(item.y, un.z - g);
-        int hw = 0, sgw = INT_MAX;   // lane w < CB_W: warp w's list heads (loaded once per item)
-        if (lane < CB_W) {
-          if (q0 < hst) hw = P.item_hw[(int64_t)i * CB_W + lane];
-          if (q1 > sst) sgw = P.item_sg[(int64_t)i * CB_W + lane];
+      for (int ib = i0; ib < i1 && g < un.z; ib += 32) {
+        int4 it4 = make_int4(0, 0, 0, 0);
+        int hst_l = 0, sst_l = INT_MAX;
+        int64_t off_l = 0;
+        if (ib + lane < i1) {
+          it4 = P.items[ib + lane];
+          hst_l = P.item_hst[ib + lane];
+          sst_l = P.item_sst[ib + lane];
+          off_l = P.item_off[ib + lane];
         }
-        const char* src = P.blob + P.item_off[i] + (int64_t)q0 * CB_W * CB_SEG * (V + 4);
-        for (int q = q0; q < q1; q++) {
-          const int seg = q == item.y - 1 ? item.w : CB_SEG;
-          const int bytes = CB_W * seg * (V + 4);
-          stage(make_int4(b, seg | (q << 11), item.z, (q < hst ? 2 : 0) | (q >= sst ? 4 : 0)), src, bytes, hw, sgw);
-          src += bytes;
+        const int nb_items = min(32, i1 - ib);
+        for (int t = 0; t < nb_items && g < un.z; t++) {
+          const int iy = __shfl_sync(FULL, it4.y, t);
+          if (g + iy <= un.y) { g += iy; continue; }
+          const int iz = __shfl_sync(FULL, it4.z, t), iw = __shfl_sync(FULL, it4.w, t);
+          const int hst = __shfl_sync(FULL, hst_l, t), sst = __shfl_sync(FULL, sst_l, t);
+          const int64_t off = __shfl_sync(FULL, off_l, t);
+          const int i = ib + t;
+          const int q0 = un.y > g ? un.y - g : 0, q1 = min(iy, un.z - g);
+          int hw = 0, sgw = INT_MAX;   // lane w < CB_W: warp w's list heads (loaded once per item)
+          if (lane < CB_W) {
+            if (q0 < hst) hw = P.item_hw[(int64_t)i * CB_W + lane];
+            if (q1 > sst) sgw = P.item_sg[(int64_t)i * CB_W + lane];
+          }
+          const char* src = P.blob + off + (int64_t)q0 * CB_W * CB_SEG * (V + 4);
+          for (int q = q0; q < q1; q++) {
+            const int seg = q == iy - 1 ? iw : CB_SEG;
+            const int bytes = CB_W * seg * (V + 4);
+            stage(make_int4(b, seg | (q << 11), iz, (q < hst ? 2 : 0) | (q >= sst ? 4 : 0)), src, bytes, hw, sgw);
+            src += bytes;
+          }
+          g += iy;
         }
-        g += item.y;
       }
       stage(make_int4(b, 0, un.w, 1), nullptr, 0, 0, 0);   // unit end: write out (slot < 0) or park the partial rows
     }
@@ -978,15 +1004,26 @@ __global__ void __launch_bounds__(CB_THREADS, 1) csc_band_kernel(const ColLaunch
   }
 
   // ---- consumer warps
-  const VT* __restrict__ x = static_cast<const VT*>(P.x) + P.xbase;
+  const VT* __restrict__ x = static_cast<const VT*>(P.x) + P.xbase * P.xs;
   const uint64_t xpol = policy_evict_last();
   for (int r = threadIdx.x; r < CB_ROWS; r += CB_NC) acc[r] = 0.0;
   named_bar_sync(1, CB_NC);
-  CBStage<VT> A, B;
+  // CB_DEPTH stages in registers: while stage A is scattered the x gathers of the next stage(s) are
+  // in flight
+  CBStage<VT> A, B, C;
   int it = 0;
-  cb_load<VT, NA>(A, it++, smem, sdesc, full, empty, x, xpol, warp, lane);
+  cb_load<VT, NA>(A, it++, smem, sdesc, full, empty, x, xpol, warp, lane, P.xs);
+  if constexpr (CB_DEPTH == 3) {
+    if (A.d.x >= 0) cb_load<VT, NA>(B, it++, smem, sdesc, full, empty, x, xpol, warp, lane, P.xs);
+    else B = A;
+  }
   while (A.d.x >= 0) {
-    cb_load<VT, NA>(B, it++, smem, sdesc, full, empty, x, xpol, warp, lane);   // next stage's gathers fly during A's scatter
+    if constexpr (CB_DEPTH == 3) {
+      if (B.d.x >= 0) cb_load<VT, NA>(C, it++, smem, sdesc, full, empty, x, xpol, warp, lane, P.xs);
+      else C = B;   // past the terminator: nothing more comes
+    } else {
+      cb_load<VT, NA>(B, it++, smem, sdesc, full, empty, x, xpol, warp, lane, P.xs);
+    }
     // the scatter: 32 distinct rows per step, steps in list order (deterministic)
     if (A.d.w & 6) {   // this stage may hold SAME-ROW groups (heavy rows; first in each list) or
                        // SEGMENTED groups (row-sorted runs; last in each list)
@@ -1055,55 +1092,48 @@ __global__ void __launch_bounds__(CB_THREADS, 1) csc_band_kernel(const ColLaunch
         }
         __threadfence();
         named_bar_sync(1, CB_NC);
-        if (threadIdx.x == 0) atomicAdd(&P.tickets[b], 1);   // after every warp's rows are visible
+        if (threadIdx.x == 0)   // after every warp's rows are visible; the band's last unit reduces it
+          misc[0] = atomicAdd(&P.tickets[b], 1) == P.bsplit[b].y - 1;
+        named_bar_sync(1, CB_NC);
+        if (misc[0]) {
+          // every unit of the band has parked its rows: y rows = the slots added in slot (= stage)
+          // order, whichever CTA comes last -- deterministic; 4 slot loads in flight per step
+          __threadfence();
+          const int2 bs = P.bsplit[b];
+          const int64_t r0 = (int64_t)b * CB_ROWS;
+          const int nr = (int)min((int64_t)CB_ROWS, P.m - r0);
+          for (int rb = threadIdx.x; rb < nr; rb += CB_NC * CB_PUT) {
+            double a[CB_PUT];
+#pragma unroll
+            for (int i = 0; i < CB_PUT; i++) {
+              const int r = rb + CB_NC * i;
+              const double* sp = P.slots + (int64_t)bs.x * CB_ROWS + (r < nr ? r : 0);
+              double t = 0.0;
+              int q = 0;
+              for (; q + 4 <= bs.y; q += 4) {
+                const double l0 = __ldcg(sp + (int64_t)q * CB_ROWS), l1 = __ldcg(sp + (int64_t)(q + 1) * CB_ROWS);
+                const double l2 = __ldcg(sp + (int64_t)(q + 2) * CB_ROWS), l3 = __ldcg(sp + (int64_t)(q + 3) * CB_ROWS);
+                t = (((t + l0) + l1) + l2) + l3;
+              }
+              for (; q < bs.y; q++) t += __ldcg(sp + (int64_t)q * CB_ROWS);
+              a[i] = t;
+            }
+            cb_put<VT>(P, r0 + rb, CB_NC, r0 + nr, a);
+          }
+          if (threadIdx.x == 0) P.tickets[b] = 0;   // ready for the next launch (stream-ordered)
+        }
       }
       named_bar_sync(1, CB_NC);   // every warp's rows are written and zero before the next unit
     }
     A = B;
+    if constexpr (CB_DEPTH == 3) B = C;
   }
 
-  // ---- reduction tasks: rows of a split band = the band's slots added in slot order (stage order),
-  // once every unit of the band has parked its rows (deterministic whichever CTA runs it)
-  for (;;) {
-    if (threadIdx.x == 0) misc[0] = atomicAdd(&P.ctr[2], 1);
-    named_bar_sync(1, CB_NC);
-    const int t = misc[0];
-    if (t >= P.ntasks) break;
-    const int4 tk = P.tasks[t];
-    const int2 bs = P.bsplit[tk.x];
-    if (threadIdx.x == 0)
-      while (ld_acquire_gpu(P.tickets + tk.x) < bs.y) __nanosleep(256);
-    named_bar_sync(1, CB_NC);
-    __threadfence();
-    const int64_t r0 = (int64_t)tk.x * CB_ROWS;
-    for (int rb = tk.y + threadIdx.x; rb < tk.z; rb += CB_NC * CB_PUT) {
-      double a[CB_PUT];
-#pragma unroll
-      for (int i = 0; i < CB_PUT; i++) {
-        const int r = rb + CB_NC * i;
-        const double* sp = P.slots + (int64_t)bs.x * CB_ROWS + (r < tk.z ? r : tk.y);
-        // slot order (= stage order) fixed: q = 0, 1, ...; 4 loads in flight per step
-        double t = 0.0;
-        int q = 0;
-        for (; q + 4 <= bs.y; q += 4) {
-          const double l0 = __ldcg(sp + (int64_t)q * CB_ROWS), l1 = __ldcg(sp + (int64_t)(q + 1) * CB_ROWS);
-          const double l2 = __ldcg(sp + (int64_t)(q + 2) * CB_ROWS), l3 = __ldcg(sp + (int64_t)(q + 3) * CB_ROWS);
-          t = (((t + l0) + l1) + l2) + l3;
-        }
-        for (; q < bs.y; q++) t += __ldcg(sp + (int64_t)q * CB_ROWS);
-        a[i] = t;
-      }
-      cb_put<VT>(P, r0 + rb, CB_NC, r0 + tk.z, a);
-    }
-    named_bar_sync(1, CB_NC);   // misc[0] is read by every thread before the next fetch
-  }
-  // the last CTA to finish resets the work counters and the split bands' tickets for the next launch
+  // the last CTA to finish resets the work counter for the next launch (every CTA has stopped fetching)
   if (threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(&P.ctr[1], 1) == (int)gridDim.x - 1) {
-      for (int t = 0; t < P.ntasks; t++) P.tickets[P.tasks[t].x] = 0;
       P.ctr[0] = 0;
-      P.ctr[2] = 0;
       __threadfence();
       P.ctr[1] = 0;
     }
@@ -1265,11 +1295,12 @@ __global__ void scale_kernel(VT* y, int64_t n, double beta) {
 }
 
 template <typename VT>
-__global__ void axpby_kernel(const double* __restrict__ py, VT* __restrict__ y, int64_t n, double alpha, double beta) {
+__global__ void axpby_kernel(const double* __restrict__ py, VT* __restrict__ y, int64_t n, double alpha, double beta,
+                             int ys) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double v = alpha * py[i];
-    if (beta != 0.0) v += beta * (double)y[i];
-    y[i] = (VT)v;
+    if (beta != 0.0) v += beta * (double)y[i * ys];
+    y[i * ys] = (VT)v;
   }
 }
 
@@ -1553,10 +1584,10 @@ cudaError_t launch_scale(void* y, int64_t n, double beta, int dtype, cudaStream_
 }
 
 cudaError_t launch_axpby_py(const double* py, void* y, int64_t n, double alpha, double beta, int dtype,
-                            cudaStream_t s) {
+                            cudaStream_t s, int ys) {
   if (n <= 0) return cudaSuccess;
-  if (dtype == 0) axpby_kernel<double><<<elementwise_grid(n), 256, 0, s>>>(py, (double*)y, n, alpha, beta);
-  else axpby_kernel<float><<<elementwise_grid(n), 256, 0, s>>>(py, (float*)y, n, alpha, beta);
+  if (dtype == 0) axpby_kernel<double><<<elementwise_grid(n), 256, 0, s>>>(py, (double*)y, n, alpha, beta, ys);
+  else axpby_kernel<float><<<elementwise_grid(n), 256, 0, s>>>(py, (float*)y, n, alpha, beta, ys);
   return cudaGetLastError();
 }
 

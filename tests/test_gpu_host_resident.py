@@ -151,3 +151,21 @@ def test_set_residency_rejects():
         M.msrep_set_residency(ctx.h, M.RESIDENT_HOST, -1)
     assert e.value.status == 1
     ctx.close()
+
+
+@pytest.mark.parametrize("fmt", ["csr", "csc"])
+def test_host_resident_pinned_on_gpu_numa_node(fmt):
+    """P:561-567 (Sec. 4.2): the pinned host copy of the partition is allocated on the GPU's own NUMA
+    node (sysfs numa_node of the GPU's PCI function); the page's node is read back with
+    get_mempolicy.  Boxes without NUMA information report -1 for both."""
+    import paper_2209_07552_b200 as M
+    A = gen.rmat(14, seed=95, kind=gen.SMALLINT)
+    B = A if fmt == "csr" else gen.transpose(A)
+    ctx = M.Context(0, 1, None, 0, 1)
+    ctx.partition(fmt, A["m"], A["n"], ptr=B["ptr"], idx=B["idx"], val=B["val"], residency="host", chunk_bytes=1 << 20)
+    st = ctx.stats()
+    ctx.close()
+    if st["gpu_numa_node"] >= 0:
+        assert st["host_numa_node"] == st["gpu_numa_node"], st
+    else:
+        assert st["host_numa_node"] in (-1, 0)

@@ -634,8 +634,8 @@ def _spmm_gpu(A, fmt, X, Y, alpha, beta, parts):
     import torch
     B = as_fmt(A, fmt)
     ctx = M.Context(0, 1, None, 0, parts)
-    if fmt == "coo":
-        ctx.partition("coo", B["m"], B["n"], idx=B["idx"], val=B["val"], coo_row=coo_of_csr(B))
+    if fmt in ("coo", "coo_col"):
+        ctx.partition(fmt, B["m"], B["n"], idx=B["idx"], val=B["val"], coo_row=coo_of_csr(B))
     else:
         ctx.partition(fmt, B["m"], B["n"], ptr=B["ptr"], idx=B["idx"], val=B["val"])
     Xd = torch.as_tensor(np.ascontiguousarray(X)).cuda()
@@ -651,7 +651,7 @@ def _spmm_ref(A, X, Y, alpha, beta):
     return np.stack([oracle_ref(A, X[:, j].copy(), Y[:, j].copy(), alpha, beta) for j in range(X.shape[1])], axis=1)
 
 
-@pytest.mark.parametrize("fmt", ["csr", "coo"])
+@pytest.mark.parametrize("fmt", FMTS)
 @pytest.mark.parametrize("k", [2, 4, 8])
 def test_spmm_bit_exact(fmt, k):
     """Y = alpha*A*X + beta*Y for k vectors at once equals k oracle SpMVs bit for bit (integer
@@ -683,16 +683,30 @@ def test_spmm_fp32_tolerance(k):
         assert_close(got[:, j], oracle_ref(A, x, y, 1.5, 0.5), row_bound(A, x, y, 1.5, 0.5), np.float32)
 
 
-def test_spmm_rejects_colwise_and_bad_k():
+@pytest.mark.parametrize("k", [2, 8])
+def test_spmm_column_formats_fp32_and_split_bands(k):
+    """pCSC SpMM (one strided band-kernel pass per vector): fp32 within tolerance on a short-wide
+    matrix whose bands are split into slot units, and the unsorted pCOO path."""
+    A = to_dtype(gen.kdistinct_csr(3000, 200_000, 60, seed=24), np.float32)
+    rng = np.random.default_rng(40 + k)
+    X = rng.uniform(-1, 1, (A["n"], k)).astype(np.float32)
+    Y = rng.uniform(-1, 1, (A["m"], k)).astype(np.float32)
+    got = _spmm_gpu(A, "csc", X, Y, 1.5, 0.5, 3)
+    for j in range(k):
+        x, y = X[:, j].copy(), Y[:, j].copy()
+        assert_close(got[:, j], oracle_ref(A, x, y, 1.5, 0.5), row_bound(A, x, y, 1.5, 0.5), np.float32)
+
+
+def test_spmm_rejects_bad_layout_and_k():
     import paper_2209_07552_b200 as M
     import torch
     A = gen.transpose(gen.kdistinct_csr(50, 40, 3, seed=3))
     ctx = M.Context(0, 1, None, 0, 1)
     ctx.partition("csc", 50, 40, ptr=A["ptr"], idx=A["idx"], val=A["val"])
-    with pytest.raises(M.MsrepError) as e:
+    with pytest.raises(M.MsrepError) as e:   # OWNED is a row-format layout
         ctx.spmm(1.0, torch.zeros((40, 4), dtype=torch.float64, device="cuda"), 0.0,
-                 torch.zeros((50, 4), dtype=torch.float64, device="cuda"))
-    assert e.value.status == 5
+                 torch.zeros((50, 4), dtype=torch.float64, device="cuda"), layout=M.Y_OWNED)
+    assert e.value.status == 1
     B = gen.kdistinct_csr(50, 40, 3, seed=3)
     ctx.partition("csr", 50, 40, ptr=B["ptr"], idx=B["idx"], val=B["val"])
     with pytest.raises(M.MsrepError) as e:
