@@ -266,9 +266,12 @@ msrep_status_t msrep_set_residency(msrep_ctx ctx, msrep_residency residency, int
  *                       (thread-block clusters) and each CTA holds half of the
  *                       hot entries, read by its partner over distributed shared
  *                       memory (twice the entries, but measured slower on R-MAT).
+ *   MSREP_TUNE_SELL     sliced-ELL tiles for runs of regular rows (row formats),
+ *                       applied by the next msrep_partition: 1 (default) on,
+ *                       0 every row goes to SEG tiles / slabs.
  * Errors: MSREP_ERR_INVALID_ARG (unknown knob or value). */
 typedef enum { MSREP_TUNE_XLOAD = 0, MSREP_TUNE_CG_GRAPH = 1, MSREP_TUNE_HOT_X = 2, MSREP_TUNE_COMPACT_X = 3,
-               MSREP_TUNE_HOT_CLUSTER = 4 } msrep_tuning;
+               MSREP_TUNE_HOT_CLUSTER = 4, MSREP_TUNE_SELL = 5 } msrep_tuning;
 msrep_status_t msrep_set_tuning(msrep_ctx ctx, msrep_tuning knob, int value);
 
 /* Select the split used by the next msrep_partition on this context (default

@@ -336,6 +336,7 @@ struct Ctx {
   void* d_xc = nullptr;             // x' = x[d_xcols], gathered at the start of every SpMV
   void* d_xc_mm = nullptr;          // SpMM: X' (nxc x 8 entries), allocated on first use
   int tune_compact = -1;
+  int tune_sell = 1;                // SELL tiles for regular rows (0: SEG tiles only)
   int tune_hot_cluster = 1;         // CTAs of a cluster sharing one hot-x cache over DSMEM (1 or 2)
   bool split_launch = false;        // SELL tiles and SEG tiles run as two launches (each >= 5-10 % of nnz)
   int residency = MSREP_RESIDENT_DEVICE;
@@ -1355,6 +1356,10 @@ msrep_status_t msrep_set_tuning(msrep_ctx h, msrep_tuning knob, int value) {
       if (value != 1 && value != 2) return fail(MSREP_ERR_INVALID_ARG, "MSREP_TUNE_HOT_CLUSTER %d (1, 2)", value);
       c->tune_hot_cluster = value;
       return MSREP_OK;
+    case MSREP_TUNE_SELL:
+      if (value < 0 || value > 1) return fail(MSREP_ERR_INVALID_ARG, "MSREP_TUNE_SELL %d (0, 1)", value);
+      c->tune_sell = value;
+      return MSREP_OK;
     case MSREP_TUNE_HOT_X:
       if (value < -1 || value > HOT_BYTES / 1024)
         return fail(MSREP_ERR_INVALID_ARG, "MSREP_TUNE_HOT_X %d (-1, 0, 1, or 2..%d KiB)", value, HOT_BYTES / 1024);
@@ -1730,7 +1735,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   } else {
     // ---- schedule
     Schedule S;
-    build_row_schedule(*c, lp, S);
+    build_row_schedule(*c, lp, S, c->tune_sell != 0);
     {
       // A few SELL tiles among many SEG tiles cost more than they save: their presence selects
       // the SELL instantiation of rows_kernel for the whole launch, whose SEG path ran 2.5x

@@ -20,7 +20,11 @@ namespace msrep {
 constexpr int TILE_NNZ = MSREP_TILE_NNZ;           // fp64 SEG tiles and slabs (a multiple of 32)
 constexpr int TILE_NNZ_F32 = MSREP_TILE_NNZ_F32;   // fp32: ~the bytes of an fp64 tile within the register budget
 __host__ __device__ constexpr int tile_nnz(int vsize) { return vsize == 4 ? TILE_NNZ_F32 : TILE_NNZ; }
-constexpr int MAX_TILE_ROWS = 128;   // rows per segment tile (uint8 tile-local row keys)
+#ifndef MSREP_MAX_TILE_ROWS
+#define MSREP_MAX_TILE_ROWS 128
+#endif
+constexpr int MAX_TILE_ROWS = MSREP_MAX_TILE_ROWS;   // rows per segment tile (uint8 tile-local row keys: <= 256)
+static_assert(MAX_TILE_ROWS % 32 == 0 && MAX_TILE_ROWS <= 256, "SEG row keys are u8");
 constexpr int SLAB_NNZ = 512;
 #ifndef MSREP_WARPS
 #define MSREP_WARPS 8

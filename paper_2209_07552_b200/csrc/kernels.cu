@@ -1479,7 +1479,7 @@ template <typename VT, bool SELL, bool MIRROR, bool NA, bool HOT, int CL>
 cudaError_t launch_rows_k(const RowLaunch& L, cudaStream_t s) {
   using Lay = RowLayout<VT, SELL, HOT>;
   constexpr int nw = HOT ? HOT_WARPS : WARPS;
-  static_assert(Lay::HOT_OFF + (HOT ? HOT_BYTES : 0) <= 227 * 1024, "rows_kernel shared memory");
+  static_assert(Lay::HOT_OFF + (HOT ? HOT_AUTO_BYTES : 0) <= 227 * 1024, "rows_kernel shared memory");
   const int b = HOT ? Lay::HOT_OFF + ((L.nhot + CL - 1) / CL) * (int)sizeof(VT) : Lay::TOTAL;
   auto kern = rows_kernel<VT, SELL, MIRROR, NA, HOT, CL>;
   cudaError_t e = set_smem(kern, b);
