@@ -141,6 +141,8 @@ typedef struct {
   int64_t nhot;              /* hot-x cache entries (MSREP_TUNE_HOT_X; 0: no cache)          */
   int64_t hot_nnz;           /* nonzeros whose x gather the hot cache serves                 */
   int64_t x_compact;         /* compact-x entries (MSREP_TUNE_COMPACT_X; 0: gathers read x)   */
+  int64_t sell_1cta;         /* SELL-tile launches at one CTA per SM (timed with the x-gather
+                                policy at partition; 0: two CTAs per SM)                      */
   int64_t gpu_numa_node;     /* NUMA node of the GPU's PCI function (sysfs; -1 unknown)      */
   int64_t host_numa_node;    /* MSREP_RESIDENT_HOST: node of the pinned layout's first page,
                                 allocated preferred on gpu_numa_node; else -1    */
@@ -163,6 +165,17 @@ msrep_status_t msrep_get_unique_id(uint8_t id[128]);
  * Makes `device` current on the calling thread. */
 msrep_status_t msrep_create(msrep_ctx* out, int rank, int nranks, const uint8_t id[128], int device,
                             int parts_per_rank, const msrep_allocator* alloc);
+
+/* Test transport for the multi-rank merge on ONE device: creates nranks (<= 8)
+ * contexts of this process on `device`, ranks 0..nranks-1, whose collectives
+ * (head-partial all-gather, allgatherv of y, reduce-scatter of the partial y,
+ * CG all-reduces, the mirror fence) meet in-process instead of in NCCL: every
+ * rank is driven by its own host thread and calls the same sequence of
+ * collective API calls, as the NCCL ranks would.  Data movement is stream-
+ * ordered device copies and rank-ordered sum kernels, so every device kernel of
+ * the N > 1 path runs for real on one GPU.  out[nranks] receives the contexts;
+ * destroy each with msrep_destroy.  Errors: MSREP_ERR_INVALID_ARG. */
+msrep_status_t msrep_create_loopback(msrep_ctx* out, int nranks, int device, int parts_per_rank);
 
 /* Partition the caller's global matrix with Alg. 2/4/6 and upload this rank's
  * contiguous nonzero range to its GPU (the only host->device transfer of A).

@@ -60,6 +60,7 @@ class Stats(ctypes.Structure):
                                          ("nchunks", ctypes.c_int64), ("host_bytes", ctypes.c_int64),
                                          ("x_no_allocate", ctypes.c_int64), ("nhot", ctypes.c_int64),
                                          ("hot_nnz", ctypes.c_int64), ("x_compact", ctypes.c_int64),
+                                         ("sell_1cta", ctypes.c_int64),
                                          ("gpu_numa_node", ctypes.c_int64), ("host_numa_node", ctypes.c_int64),
                                          ("stream_bytes", ctypes.c_int64)]
 
@@ -78,6 +79,7 @@ P, I64, I32, I = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int
 _sig = {
     "msrep_get_unique_id": [P],
     "msrep_create": [ctypes.POINTER(P), I, I, P, I, I, P],
+    "msrep_create_loopback": [P, I, I, I],
     "msrep_partition": [P, I, I, I64, I64, I64, P, P, P, P, P, P],
     "msrep_partition_slice": [P, I, I, I64, I64, I64, P, P, P, I64, I64, P, P],
     "msrep_spmv": [P, P, P, P, P, I, P],
@@ -107,7 +109,7 @@ _lib.msrep_last_error.restype = ctypes.c_char_p
 _lib.msrep_version.argtypes = []
 _lib.msrep_version.restype = ctypes.c_int
 
-EXPORTED = ["msrep_get_unique_id", "msrep_create", "msrep_partition", "msrep_partition_slice", "msrep_spmv", "msrep_spmv_host",
+EXPORTED = ["msrep_get_unique_id", "msrep_create", "msrep_create_loopback", "msrep_partition", "msrep_partition_slice", "msrep_spmv", "msrep_spmv_host",
             "msrep_plan", "msrep_plan_split", "msrep_set_split", "msrep_set_tuning", "msrep_set_residency", "msrep_debug_arrange", "msrep_cg", "msrep_spmm", "msrep_spmv_mirror", "msrep_plan_groups", "msrep_set_split_groups", "msrep_exchange_plan", "msrep_get_stats", "msrep_destroy", "msrep_last_error", "msrep_version",
             "msrep_profile_enable", "msrep_profile_read"]
 
@@ -343,6 +345,21 @@ class Context:
         self.fmt = CSR
         self.parts = None
         self.m = self.n = self.nnz = 0
+
+    @classmethod
+    def loopback_group(cls, nranks, device=0, parts_per_rank=1):
+        """nranks contexts on ONE device whose collectives meet in-process (msrep_create_loopback):
+        drive each from its own thread with the same call sequence, as NCCL ranks would be."""
+        arr = (P * nranks)()
+        _check(_lib.msrep_create_loopback(ctypes.cast(arr, P), nranks, device, parts_per_rank), "msrep_create_loopback")
+        out = []
+        for r in range(nranks):
+            c = cls.__new__(cls)
+            c.rank, c.nranks, c.device, c.parts_per_rank = r, nranks, device, parts_per_rank
+            c.h = P(arr[r])
+            c.dtype, c.fmt, c.parts, c.m, c.n, c.nnz = F64, CSR, None, 0, 0, 0
+            out.append(c)
+        return out
 
     @classmethod
     def from_torch_dist(cls, device=None, parts_per_rank=1):

@@ -9,6 +9,7 @@
 // owned y segment.
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
 #include <cctype>
 #include <climits>
 #include <cmath>
@@ -245,6 +246,37 @@ cudaError_t host_alloc_on(void** out, size_t bytes, int node) {
   return e;
 }
 
+// ------------------------------------------------ in-process loopback transport
+// msrep_create_loopback: nranks contexts of ONE process on one device, each driven by its own host
+// thread, whose collectives meet here instead of in NCCL -- the multi-rank merge (head exchange,
+// owner fix-up, allgatherv, reduce-scatter + shard epilogue, CG all-reduces, mirror fence) then
+// runs on the device with real ranks on a single GPU.  Protocol per collective: every rank records
+// an event after its producing work and publishes its buffers (barrier 1), waits on every peer's
+// event and moves / reduces the data it receives with stream-ordered copies and kernels, records a
+// second event (barrier 2), and waits on the peers' second events before its stream goes on, so no
+// rank overwrites a buffer a peer is still reading.  Sums run in rank order (deterministic).
+struct LoopGroup {
+  int n = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  std::vector<const void*> src;   // per rank: the buffer it contributes
+  std::vector<void*> dst;         // per rank: the buffer it receives into
+  std::vector<cudaEvent_t> ev1, ev2;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const uint64_t g = gen;
+    if (++arrived == n) {
+      arrived = 0;
+      gen++;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+
 // ---------------------------------------------------------------- memory
 struct DevBuf {
   void* p = nullptr;
@@ -257,6 +289,9 @@ struct Ctx {
   msrep_split split = MSREP_SPLIT_NNZ;
   std::vector<int> groups;          // MSREP_SPLIT_TWO_LEVEL: parts per NUMA group
   ncclComm_t comm = nullptr;
+  std::shared_ptr<LoopGroup> loop;  // msrep_create_loopback (else NCCL when nranks > 1)
+  double* d_loop_scratch = nullptr; // loopback all-reduce staging
+  size_t loop_scratch_bytes = 0;
   msrep_allocator alloc{};
   bool has_alloc = false;
 
@@ -327,6 +362,7 @@ struct Ctx {
   // MSREP_RESIDENT_HOST: the device layout parked in pinned host memory, streamed per call
   // in chunks (row formats: tile ranges; pCSC: band ranges) through two staging buffers
   int xna = 0;                      // x-gather L1 policy of the partition (1: L1::no_allocate)
+  int sell_1cta = 0;                // SELL launches at one CTA per SM (timed at partition)
   int32_t* d_hot = nullptr;         // hot-x columns by slot (row formats, device-resident)
   int nhot = 0;
   int64_t hot_nnz = 0;              // the rank's nonzeros whose x comes from the hot cache
@@ -434,6 +470,8 @@ void free_all(Ctx* c) {
   c->nxc = 0;
   c->d_xcols = nullptr;
   c->d_xc = c->d_xc_mm = nullptr;
+  c->d_loop_scratch = nullptr;
+  c->loop_scratch_bytes = 0;
   c->d_cg_r = c->d_cg_p = c->d_cg_ap = nullptr;
   c->d_cg_part = c->d_cg_sc = nullptr;
   c->mm_k = 0;
@@ -1063,10 +1101,100 @@ msrep_status_t upload_vec(Ctx* c, const std::vector<T>& v, T** out, cudaStream_t
 
 ncclDataType_t nccl_type(msrep_dtype t) { return t == MSREP_F64 ? ncclDouble : ncclFloat; }
 
+// ---- collectives of the merge: NCCL, or the loopback group (same buffer semantics)
+// loopback phase 1: publish (src, dst) after this rank's work on s, wait for every peer's work
+msrep_status_t loop_enter(Ctx* c, const void* src, void* dst, cudaStream_t s) {
+  LoopGroup& G = *c->loop;
+  CUDA_TRY(cudaEventRecord(G.ev1[(size_t)c->rank], s));
+  G.src[(size_t)c->rank] = src;
+  G.dst[(size_t)c->rank] = dst;
+  G.barrier();
+  for (int q = 0; q < G.n; q++)
+    if (q != c->rank) CUDA_TRY(cudaStreamWaitEvent(s, G.ev1[(size_t)q], 0));
+  return MSREP_OK;
+}
+// loopback phase 2: every rank has finished reading the peers' buffers before anyone goes on
+msrep_status_t loop_leave(Ctx* c, cudaStream_t s) {
+  LoopGroup& G = *c->loop;
+  CUDA_TRY(cudaEventRecord(G.ev2[(size_t)c->rank], s));
+  G.barrier();
+  for (int q = 0; q < G.n; q++)
+    if (q != c->rank) CUDA_TRY(cudaStreamWaitEvent(s, G.ev2[(size_t)q], 0));
+  G.barrier();   // the slots may be republished by the next collective only after every wait above
+  return MSREP_OK;
+}
+msrep_status_t loop_scratch(Ctx* c, size_t bytes, cudaStream_t s) {
+  if (c->loop_scratch_bytes >= bytes) return MSREP_OK;
+  void* p;
+  TRY(dalloc(c, bytes, &p, s));
+  c->d_loop_scratch = static_cast<double*>(p);
+  c->loop_scratch_bytes = bytes;
+  return MSREP_OK;
+}
+msrep_status_t reduce_peers(Ctx* c, const void* const* srcs, size_t elem_off, size_t count, void* dst, int is_int,
+                            cudaStream_t s) {
+  SumLaunch L{};
+  L.n = c->nranks;
+  for (int q = 0; q < c->nranks; q++) L.src[q] = srcs[q];
+  L.off = (int64_t)elem_off;
+  L.count = (int64_t)count;
+  L.dst = dst;
+  L.is_int = is_int;
+  CUDA_TRY(launch_sum_peers(L, s));
+  return MSREP_OK;
+}
+
+// recv[q*count .. (q+1)*count) = rank q's send (fp64)
+msrep_status_t comm_allgather(Ctx* c, const double* send, double* recv, size_t count, cudaStream_t s) {
+  if (!c->loop) {
+    NCCL_TRY(ncclAllGather(send, recv, count, ncclDouble, c->comm, s));
+    return MSREP_OK;
+  }
+  TRY(loop_enter(c, send, recv, s));
+  for (int q = 0; q < c->nranks; q++)
+    if (count) CUDA_TRY(cudaMemcpyAsync(recv + (size_t)q * count, c->loop->src[(size_t)q], count * 8, cudaMemcpyDeviceToDevice, s));
+  return loop_leave(c, s);
+}
+// buf[rank*count .. (rank+1)*count) = sum over ranks of their buf segment (fp64, in place)
+msrep_status_t comm_reduce_scatter(Ctx* c, double* buf, size_t count, cudaStream_t s) {
+  if (!c->loop) {
+    NCCL_TRY(ncclReduceScatter(buf, buf + (size_t)c->rank * count, count, ncclDouble, ncclSum, c->comm, s));
+    return MSREP_OK;
+  }
+  TRY(loop_enter(c, buf, buf, s));
+  // each rank writes only its own segment of its own buffer; peers read the other segments
+  TRY(reduce_peers(c, c->loop->src.data(), (size_t)c->rank * count, count, buf + (size_t)c->rank * count, 0, s));
+  return loop_leave(c, s);
+}
+// buf = sum over ranks (in place; fp64 or int32)
+msrep_status_t comm_allreduce(Ctx* c, void* buf, size_t count, bool is_int, cudaStream_t s) {
+  if (!c->loop) {
+    NCCL_TRY(ncclAllReduce(buf, buf, count, is_int ? ncclInt : ncclDouble, ncclSum, c->comm, s));
+    return MSREP_OK;
+  }
+  TRY(loop_scratch(c, count * 8 + 16, s));
+  TRY(loop_enter(c, buf, buf, s));
+  TRY(reduce_peers(c, c->loop->src.data(), 0, count, c->d_loop_scratch, is_int ? 1 : 0, s));
+  TRY(loop_leave(c, s));   // every peer has read this rank's buf: overwrite it now
+  CUDA_TRY(cudaMemcpyAsync(buf, c->d_loop_scratch, count * (is_int ? 4 : 8), cudaMemcpyDeviceToDevice, s));
+  return MSREP_OK;
+}
+
 // allgatherv of per-rank segments of y (in place), as grouped broadcasts.
 msrep_status_t allgatherv_y(Ctx* c, void* y, const std::vector<int64_t>& lo, const std::vector<int64_t>& hi,
                             cudaStream_t s, int k = 1) {
   const size_t V = vsz(c->dtype);
+  if (c->loop) {   // pull every peer's owned segment into this rank's y
+    TRY(loop_enter(c, y, y, s));
+    for (int r = 0; r < c->nranks; r++) {
+      const int64_t cnt = (hi[(size_t)r] - lo[(size_t)r]) * k;
+      if (r == c->rank || cnt <= 0) continue;
+      const size_t off = (size_t)lo[(size_t)r] * k * V;
+      CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(y) + off, static_cast<const char*>(c->loop->src[(size_t)r]) + off,
+                               (size_t)cnt * V, cudaMemcpyDeviceToDevice, s));
+    }
+    return loop_leave(c, s);
+  }
   NCCL_TRY(ncclGroupStart());
   for (int r = 0; r < c->nranks; r++) {
     const int64_t cnt = (hi[(size_t)r] - lo[(size_t)r]) * k;   // rows x k (row-major blocks)
@@ -1117,7 +1245,7 @@ RowLaunch row_launch(const Ctx* c, const void* x, void* y, double alpha, double 
   L.alpha = alpha; L.beta = beta; L.rec = c->d_rec;
   L.dtype = c->dtype == MSREP_F64 ? 0 : 1; L.has_sell = c->nsell > 0;
   L.xna = c->xna;
-  L.hot = c->d_hot; L.nhot = c->nhot; L.hot_cluster = c->hot_cluster;
+  L.hot = c->d_hot; L.nhot = c->nhot; L.hot_cluster = c->hot_cluster; L.sell_1cta = c->sell_1cta;
   if (c->nxc) { L.x = c->d_xc; L.xmax = (uint32_t)(c->nxc - 1); }   // the SpMV gathers x' first (prepare_x)
   return L;
 }
@@ -1174,6 +1302,7 @@ msrep_status_t launch_row_tiles(const Ctx* c, const RowLaunch& L, int k, cudaStr
 // msrep_set_tuning(MSREP_TUNE_XLOAD, 0|1) forces a policy.  Host-resident and small partitions (< 2^20 nonzeros)
 // keep the allocating policy.
 msrep_status_t tune_xload(Ctx* c, cudaStream_t s, int64_t nz_r) {
+  c->sell_1cta = 0;
   if (c->tune_xload >= 0) { c->xna = c->tune_xload; return MSREP_OK; }
   c->xna = 0;
   if (c->residency == MSREP_RESIDENT_HOST || nz_r < ((int64_t)1 << 20)) return MSREP_OK;
@@ -1190,8 +1319,12 @@ msrep_status_t tune_xload(Ctx* c, cudaStream_t s, int64_t nz_r) {
   CUDA_TRY(cudaEventCreate(&e1));
   float best = 0.f;
   int pick = 0;
-  for (int na = 0; na < 2; na++) {
+  // row layouts with SELL tiles also try one CTA per SM for the SELL launches: (policy, occupancy)
+  const int combos = (!colwise(c->fmt) && c->nsell > 0) ? 4 : 2;
+  for (int cb = 0; cb < combos; cb++) {
+    const int na = cb & 1;
     c->xna = na;
+    c->sell_1cta = cb >> 1;
     float ms = 0.f;
     for (int it = 0; it < 4; it++) {
       if (it == 1) CUDA_TRY(cudaEventRecord(e0, s));
@@ -1201,11 +1334,12 @@ msrep_status_t tune_xload(Ctx* c, cudaStream_t s, int64_t nz_r) {
     CUDA_TRY(cudaEventRecord(e1, s));
     CUDA_TRY(cudaEventSynchronize(e1));
     CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
-    if (na == 0 || ms < best) { best = ms; pick = na; }
+    if (cb == 0 || ms < best) { best = ms; pick = cb; }
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  c->xna = pick;
+  c->xna = pick & 1;
+  c->sell_1cta = pick >> 1;
   release_range(c, mark, c->bufs.size());
   return MSREP_OK;
 }
@@ -1465,6 +1599,36 @@ msrep_status_t msrep_create(msrep_ctx* out, int rank, int nranks, const uint8_t 
   return MSREP_OK;
 }
 
+msrep_status_t msrep_create_loopback(msrep_ctx* out, int nranks, int device, int parts_per_rank) {
+  if (!out) return fail(MSREP_ERR_INVALID_ARG, "out is NULL");
+  if (nranks < 1 || nranks > MAX_LOOP_RANKS || parts_per_rank < 1)
+    return fail(MSREP_ERR_INVALID_ARG, "nranks %d (1..%d) / parts_per_rank %d", nranks, MAX_LOOP_RANKS, parts_per_rank);
+  for (int r = 0; r < nranks; r++) out[r] = nullptr;
+  CUDA_TRY(cudaSetDevice(device));
+  auto G = std::make_shared<LoopGroup>();
+  G->n = nranks;
+  G->src.assign((size_t)nranks, nullptr);
+  G->dst.assign((size_t)nranks, nullptr);
+  G->ev1.assign((size_t)nranks, nullptr);
+  G->ev2.assign((size_t)nranks, nullptr);
+  for (int r = 0; r < nranks; r++) {
+    CUDA_TRY(cudaEventCreateWithFlags(&G->ev1[(size_t)r], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&G->ev2[(size_t)r], cudaEventDisableTiming));
+  }
+  for (int r = 0; r < nranks; r++) {
+    Ctx* c = new Ctx();
+    c->rank = r;
+    c->nranks = nranks;
+    c->vparts = parts_per_rank;
+    c->np = nranks * parts_per_rank;
+    c->device = device;
+    c->numa_node = gpu_numa_node(device);
+    c->loop = G;
+    out[r] = reinterpret_cast<msrep_ctx>(c);
+  }
+  return MSREP_OK;
+}
+
 msrep_status_t msrep_destroy(msrep_ctx h) {
   if (!h) return MSREP_OK;
   Ctx* c = reinterpret_cast<Ctx*>(h);
@@ -1481,6 +1645,10 @@ msrep_status_t msrep_destroy(msrep_ctx h) {
   for (cudaEvent_t e : {c->ev_go, c->ev_copied[0], c->ev_copied[1], c->ev_free[0], c->ev_free[1]})
     if (e) cudaEventDestroy(e);
   if (c->comm) ncclCommDestroy(c->comm);
+  if (c->loop && c->loop.use_count() == 1) {   // the group's last context
+    for (auto e : c->loop->ev1) if (e) cudaEventDestroy(e);
+    for (auto e : c->loop->ev2) if (e) cudaEventDestroy(e);
+  }
   delete c;
   return MSREP_OK;
 }
@@ -2032,6 +2200,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   st.x_no_allocate = c->xna;
   st.nhot = c->nhot;
   st.x_compact = c->nxc;
+  st.sell_1cta = c->sell_1cta;
   st.gpu_numa_node = c->numa_node;
   st.host_numa_node = c->h_blob ? page_numa_node(c->h_blob) : -1;
   st.hot_nnz = c->hot_nnz;
@@ -2136,7 +2305,7 @@ msrep_status_t msrep_spmv_mirror(msrep_ctx h, const void* alpha_p, const void* x
   if (c->nranks > 1) {   // completion fence: every rank's stores into every mirror are done
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     CUDA_TRY(cudaMemsetAsync(c->d_fence, 0, sizeof(int), s));
-    NCCL_TRY(ncclAllReduce(c->d_fence, c->d_fence, 1, ncclInt, ncclSum, c->comm, s));
+    TRY(comm_allreduce(c, c->d_fence, 1, true, s));
   }
   return MSREP_OK;
 }
@@ -2169,7 +2338,7 @@ msrep_status_t col_spmv(Ctx* c, double alpha, const void* x, double beta, void* 
   if (pe) CUDA_TRY(cudaEventRecord(pe, s));
   if (c->nranks > 1) {
     double* shard = c->d_py + (size_t)c->rank * c->shard;
-    NCCL_TRY(ncclReduceScatter(c->d_py, shard, (size_t)c->shard, ncclDouble, ncclSum, c->comm, s));
+    TRY(comm_reduce_scatter(c, c->d_py, (size_t)c->shard, s));
     CUDA_TRY(launch_axpby_py(shard, static_cast<char*>(y) + ((size_t)my_lo * k + j) * V, my_hi - my_lo, alpha, beta,
                              dt, s, k));
   }
@@ -2242,7 +2411,7 @@ msrep_status_t spmv_impl(msrep_ctx h, const void* alpha_p, const void* x, const 
     nv.next("spmv: head exchange");
     HeadLaunch H{c->vparts, c->d_part_rec, c->d_rec, c->d_head_local, 1};
     CUDA_TRY(launch_heads(H, s));
-    NCCL_TRY(ncclAllGather(c->d_head_local, c->d_head_all, (size_t)c->vparts, ncclDouble, c->comm, s));
+    TRY(comm_allgather(c, c->d_head_local, c->d_head_all, (size_t)c->vparts, s));
   }
   if (c->nsplit) {
     nv.next("spmv: fix-up");
@@ -2325,7 +2494,7 @@ msrep_status_t msrep_spmm(msrep_ctx h, const void* alpha_p, const void* X, const
   if (c->nranks > 1 && c->any_flag) {
     HeadLaunch H{c->vparts, c->d_part_rec, c->d_rec_mm, c->d_head_local_mm, k};
     CUDA_TRY(launch_heads(H, s));
-    NCCL_TRY(ncclAllGather(c->d_head_local_mm, c->d_head_all_mm, (size_t)c->vparts * k, ncclDouble, c->comm, s));
+    TRY(comm_allgather(c, c->d_head_local_mm, c->d_head_all_mm, (size_t)c->vparts * k, s));
   }
   if (c->nsplit) {
     FixupLaunch F{};
@@ -2403,7 +2572,7 @@ msrep_status_t msrep_cg(msrep_ctx h, const void* b, void* x, double tol, int max
   double* p1 = c->d_cg_part;              // partial sums of p.Ap (and of r0.r0, b.b at the start)
   double* p2 = c->d_cg_part + CG_PARTS;   // partial sums of r.r
   auto allreduce_parts = [&](double* part) -> msrep_status_t {   // same partials on every rank
-    if (c->nranks > 1) NCCL_TRY(ncclAllReduce(part, part, CG_PARTS, ncclDouble, ncclSum, c->comm, s));
+    if (c->nranks > 1) TRY(comm_allreduce(c, part, CG_PARTS, false, s));
     return MSREP_OK;
   };
   // r0 = b - A x0, p0 = r0, rs = r0.r0 (sc[0], parity 0), bnorm2 = b.b (sc[3])
@@ -2427,9 +2596,9 @@ msrep_status_t msrep_cg(msrep_ctx h, const void* b, void* x, double tol, int max
     if (c->nranks > 1) TRY(allgatherv_y(c, c->d_cg_p, lo_v, hi_v, st));   // the SpMV needs the whole p
     TRY(msrep_spmv(h, one, c->d_cg_p, zero, c->d_cg_ap, lay, st));        // Ap, owned rows
     CUDA_TRY(launch_cg(CG_DOT, dt, off(c->d_cg_p), off(c->d_cg_ap), nullptr, nullptr, nloc, sc, par, nullptr, p1, st));
-    if (c->nranks > 1) NCCL_TRY(ncclAllReduce(p1, p1, CG_PARTS, ncclDouble, ncclSum, c->comm, st));
+    if (c->nranks > 1) TRY(comm_allreduce(c, p1, CG_PARTS, false, st));
     CUDA_TRY(launch_cg(CG_UPDATE_XR, dt, off(x), off(c->d_cg_r), off(c->d_cg_p), off(c->d_cg_ap), nloc, sc, par, p1, p2, st));
-    if (c->nranks > 1) NCCL_TRY(ncclAllReduce(p2, p2, CG_PARTS, ncclDouble, ncclSum, c->comm, st));
+    if (c->nranks > 1) TRY(comm_allreduce(c, p2, CG_PARTS, false, st));
     CUDA_TRY(launch_cg(CG_UPDATE_P, dt, off(c->d_cg_p), off(c->d_cg_r), nullptr, nullptr, nloc, sc, par, p2, nullptr, st));
     return MSREP_OK;
   };

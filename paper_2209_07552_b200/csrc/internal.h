@@ -138,6 +138,7 @@ struct RowLaunch {
   int xna;                                                   // x gathers with L1::no_allocate (SEG / slab tiles)
   const int32_t* hot; int nhot;                              // hot-x columns by slot (nhot == 0: no hot x)
   int hot_cluster;                                           // 2: slots split over a CTA pair (DSMEM), else 1
+  int sell_1cta;                                             // SELL-instantiation launches at one CTA per SM
 };
 
 // pCSC row-band layout.  The rank's nonzeros are regrouped
@@ -213,6 +214,15 @@ struct HeadLaunch {
   int k;
 };
 
+// loopback transport (host.cpp LoopGroup): dst[i] = sum over ranks q of src[q][off + i], in rank order
+constexpr int MAX_LOOP_RANKS = 8;
+struct SumLaunch {
+  int n; const void* src[MAX_LOOP_RANKS];
+  int64_t off, count;
+  void* dst;
+  int is_int;   // int32 (the mirror fence) or fp64
+};
+
 // kernels.cu entry points (all enqueue on `s`)
 cudaError_t launch_rows(const RowLaunch& L, cudaStream_t s);
 cudaError_t launch_rows_mm(const RowLaunch& L, int k, cudaStream_t s);   // SpMM, k in {2, 4, 8}
@@ -225,6 +235,7 @@ cudaError_t launch_axpby_py(const double* py, void* y, int64_t count, double alp
 cudaError_t launch_rebase(const int64_t* gptr, int32_t* lptr, int64_t count, int64_t lo, int64_t hi,
                           cudaStream_t s);                                                  // clamp(gptr,lo,hi)-lo
 cudaError_t launch_pack(const PackLaunch& L, cudaStream_t s);
+cudaError_t launch_sum_peers(const SumLaunch& L, cudaStream_t s);
 cudaError_t launch_col_degree(const int32_t* idx, int64_t nz, int32_t* deg, cudaStream_t s);   // deg[idx[i]]++
 cudaError_t launch_hot_slots(const int32_t* hot, int nhot, int32_t* slot, cudaStream_t s);      // slot[hot[k]] = k
 // out[i*k + j] = x[cols[i]*k + j], i < n, j < k (compact x for SpMV k = 1, SpMM k > 1)

@@ -1250,6 +1250,21 @@ __global__ void gather_x_kernel(const VT* __restrict__ x, const int32_t* __restr
   }
 }
 
+// loopback reduce (in-process multi-rank test transport): fixed rank order
+__global__ void sum_peers_kernel(const SumLaunch L) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < L.count; i += (int64_t)gridDim.x * blockDim.x) {
+    if (L.is_int) {
+      int a = 0;
+      for (int q = 0; q < L.n; q++) a += static_cast<const int*>(L.src[q])[L.off + i];
+      static_cast<int*>(L.dst)[i] = a;
+    } else {
+      double a = 0.0;
+      for (int q = 0; q < L.n; q++) a += static_cast<const double*>(L.src[q])[L.off + i];
+      static_cast<double*>(L.dst)[i] = a;
+    }
+  }
+}
+
 // --------------------------------------------------------- small kernels
 // one thread per (split row, vector j < k): k = 1 for SpMV, the block width for SpMM; records,
 // head partials and y are k-wide (record r, vector j at r*k + j; y row-major [m x k])
@@ -1475,12 +1490,19 @@ int grid_for(K kernel, int smem_bytes, int ntiles, int warps = WARPS) {
   return (int)(want < g ? (want < 1 ? 1 : want) : g);
 }
 
+constexpr int SELL_1CTA_SMEM = 116 * 1024;   // > half of the SM's 228 KB: one CTA per SM
 template <typename VT, bool SELL, bool MIRROR, bool NA, bool HOT, int CL>
 cudaError_t launch_rows_k(const RowLaunch& L, cudaStream_t s) {
   using Lay = RowLayout<VT, SELL, HOT>;
   constexpr int nw = HOT ? HOT_WARPS : WARPS;
   static_assert(Lay::HOT_OFF + (HOT ? HOT_AUTO_BYTES : 0) <= 227 * 1024, "rows_kernel shared memory");
-  const int b = HOT ? Lay::HOT_OFF + ((L.nhot + CL - 1) / CL) * (int)sizeof(VT) : Lay::TOTAL;
+  int b = HOT ? Lay::HOT_OFF + ((L.nhot + CL - 1) / CL) * (int)sizeof(VT) : Lay::TOTAL;
+  // SELL launches at one CTA per SM (RowLaunch.sell_1cta, picked by timing at partition): the
+  // larger L1 holds the in-flight misses of random-column short rows (1.7x faster there), while the
+  // stencil's L1-resident gathers prefer two CTAs per SM (profiles/r2_short_rows.jsonl)
+  if constexpr (SELL && !HOT) {
+    if (L.sell_1cta) b = b > SELL_1CTA_SMEM ? b : SELL_1CTA_SMEM;
+  }
   auto kern = rows_kernel<VT, SELL, MIRROR, NA, HOT, CL>;
   cudaError_t e = set_smem(kern, b);
   if (e) return e;
@@ -1588,6 +1610,12 @@ cudaError_t launch_axpby_py(const double* py, void* y, int64_t n, double alpha, 
   if (n <= 0) return cudaSuccess;
   if (dtype == 0) axpby_kernel<double><<<elementwise_grid(n), 256, 0, s>>>(py, (double*)y, n, alpha, beta, ys);
   else axpby_kernel<float><<<elementwise_grid(n), 256, 0, s>>>(py, (float*)y, n, alpha, beta, ys);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sum_peers(const SumLaunch& L, cudaStream_t s) {
+  if (L.count <= 0) return cudaSuccess;
+  sum_peers_kernel<<<elementwise_grid(L.count), 256, 0, s>>>(L);
   return cudaGetLastError();
 }
 

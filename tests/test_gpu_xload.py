@@ -28,3 +28,18 @@ def test_xload_policies_bit_identical(fmt):
             ctx.close()
             assert np.array_equal(got, ref), (fmt, forced)
         assert picks[0] == 0 and picks[1] == 1 and picks[2] in (0, 1)
+
+
+@pytest.mark.parametrize("fmt", ["csr", "coo"])
+def test_sell_occupancy_pick_bit_identical(fmt):
+    """Short regular rows with random columns (SELL tiles): the partition times the SELL launches
+    at two and at one CTA per SM (stats sell_1cta) -- occupancy changes nothing in the bits."""
+    A = gen.kdistinct_csr(400_000, 1_400_000, 6, seed=114, kind=gen.SMALLINT)
+    x = gen.vector(A["n"], 115, kind=gen.SMALLINT); y = gen.vector(A["m"], 116, kind=gen.SMALLINT)
+    import paper_2209_07552_b200 as M
+    ctx = M.Context(0, 1, None, 0, 1)
+    got = run_gpu(A, fmt, x, y, 1.5, 0.5, ctx=ctx)
+    st = ctx.stats()
+    ctx.close()
+    assert st["nsell"] > 0 and st["sell_1cta"] in (0, 1)
+    assert np.array_equal(got, oracle_ref(A, x, y, 1.5, 0.5))
