@@ -384,6 +384,8 @@ struct Ctx {
   char* d_stage[2] = {nullptr, nullptr};
   cudaStream_t cs = nullptr;        // copy stream
   cudaStream_t gs = nullptr;        // msrep_cg graph replay stream
+  cudaStream_t ss = nullptr;        // side stream of the split SELL / SEG launches
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_go = nullptr, ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
 
   // partition uploads from pageable caller memory: a pinned two-slot ring (host threads copy
@@ -1279,17 +1281,28 @@ ColLaunch col_launch(const Ctx* c, const void* x, void* y, double alpha, double 
 
 // The device-resident tile walk: one launch, or (split_launch) the SELL tiles [0, nsell) with the
 // SELL instantiation and the SEG / slab tiles with the SEG one (k = 1: SpMV, else SpMM).
-msrep_status_t launch_row_tiles(const Ctx* c, const RowLaunch& L, int k, cudaStream_t s) {
-  auto run = [&](const RowLaunch& X) { return k == 1 ? launch_rows(X, s) : launch_rows_mm(X, k, s); };
+msrep_status_t launch_row_tiles(Ctx* c, const RowLaunch& L, int k, cudaStream_t s) {
+  auto run = [&](const RowLaunch& X, cudaStream_t st) { return k == 1 ? launch_rows(X, st) : launch_rows_mm(X, k, st); };
   if (!c->split_launch) {
-    CUDA_TRY(run(L));
+    CUDA_TRY(run(L, s));
     return MSREP_OK;
+  }
+  // SELL tiles and SEG tiles in their own instantiations, forked onto a context side stream so the
+  // two launches overlap (each one's tail fills with the other's CTAs) and joined back into s
+  if (!c->ss) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->ss, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   }
   RowLaunch a = L, b = L;
   a.ntiles = c->nsell;
   b.tiles = L.tiles + c->nsell; b.ntiles = L.ntiles - c->nsell; b.has_sell = 0;
-  CUDA_TRY(run(a));
-  CUDA_TRY(run(b));
+  CUDA_TRY(cudaEventRecord(c->ev_fork, s));
+  CUDA_TRY(cudaStreamWaitEvent(c->ss, c->ev_fork, 0));
+  CUDA_TRY(run(a, c->ss));
+  CUDA_TRY(run(b, s));
+  CUDA_TRY(cudaEventRecord(c->ev_join, c->ss));
+  CUDA_TRY(cudaStreamWaitEvent(s, c->ev_join, 0));
   return MSREP_OK;
 }
 
@@ -1638,6 +1651,9 @@ msrep_status_t msrep_destroy(msrep_ctx h) {
   for (auto& p : c->ev) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
   if (c->cs) cudaStreamDestroy(c->cs);
   if (c->gs) cudaStreamDestroy(c->gs);
+  if (c->ss) cudaStreamDestroy(c->ss);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   for (int b = 0; b < 2; b++) {
     if (c->h_ring[b]) cudaFreeHost(c->h_ring[b]);
     if (c->ring_ev[b]) cudaEventDestroy(c->ring_ev[b]);
