@@ -340,8 +340,10 @@ msrep_status_t msrep_debug_arrange(const uint32_t* pk, int64_t n, int64_t* order
  * X: device [n x k], Y: device [m x k], both row-major contiguous (X[c*k + j]),
  * k in {2, 4, 8}.  Row formats (pCSR, pCOO): the matrix is streamed once for
  * all k vectors (layouts REPLICATED / OWNED).  Column formats (pCSC, column-sorted
- * and unsorted pCOO): one strided pass of the band kernel per vector -- each
- * with the column-style merge when nranks > 1 -- (layouts REPLICATED / SHARDED).
+ * and unsorted pCOO): X and Y are copied to k planar vectors (context workspace,
+ * allocated on first use), one band-kernel pass per vector -- each with the
+ * column-style merge when nranks > 1 -- and Y is copied back (layouts
+ * REPLICATED / SHARDED).
  * Segments are row blocks of Y; beta == 0: Y not read; alpha == 0: Y = beta*Y.
  * Asynchronous on `stream`, collective when nranks > 1. */
 msrep_status_t msrep_spmm(msrep_ctx ctx, const void* alpha, const void* X, const void* beta, void* Y, int k,

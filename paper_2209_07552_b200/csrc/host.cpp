@@ -371,6 +371,8 @@ struct Ctx {
   int32_t* d_xcols = nullptr;       // the rank's distinct columns, ascending (compact x -> column)
   void* d_xc = nullptr;             // x' = x[d_xcols], gathered at the start of every SpMV
   void* d_xc_mm = nullptr;          // SpMM: X' (nxc x 8 entries), allocated on first use
+  void* d_mm_planar = nullptr;      // SpMM on the column formats: planar X and Y (k <= 8)
+  size_t mm_planar_bytes = 0;
   int tune_compact = -1;
   int tune_sell = 1;                // SELL tiles for regular rows (0: SEG tiles only)
   int tune_hot_cluster = 1;         // CTAs of a cluster sharing one hot-x cache over DSMEM (1 or 2)
@@ -472,6 +474,8 @@ void free_all(Ctx* c) {
   c->nxc = 0;
   c->d_xcols = nullptr;
   c->d_xc = c->d_xc_mm = nullptr;
+  c->d_mm_planar = nullptr;
+  c->mm_planar_bytes = 0;
   c->d_loop_scratch = nullptr;
   c->loop_scratch_bytes = 0;
   c->d_cg_r = c->d_cg_p = c->d_cg_ap = nullptr;
@@ -1332,22 +1336,24 @@ msrep_status_t tune_xload(Ctx* c, cudaStream_t s, int64_t nz_r) {
   CUDA_TRY(cudaEventCreate(&e1));
   float best = 0.f;
   int pick = 0;
-  // row layouts with SELL tiles also try one CTA per SM for the SELL launches: (policy, occupancy)
+  // row layouts with SELL tiles also try one CTA per SM for the SELL launches: (policy, occupancy).
+  // 2 warm-up + 6 timed launches each; a combination other than the default (allocate, 2 CTAs)
+  // must win by 3 % (a noisy pick cost the CG stencil 15 %)
   const int combos = (!colwise(c->fmt) && c->nsell > 0) ? 4 : 2;
   for (int cb = 0; cb < combos; cb++) {
     const int na = cb & 1;
     c->xna = na;
     c->sell_1cta = cb >> 1;
     float ms = 0.f;
-    for (int it = 0; it < 4; it++) {
-      if (it == 1) CUDA_TRY(cudaEventRecord(e0, s));
+    for (int it = 0; it < 8; it++) {
+      if (it == 2) CUDA_TRY(cudaEventRecord(e0, s));
       if (colwise(c->fmt)) CUDA_TRY(launch_cols(col_launch(c, dx, dy, 1.0, 0.0), s));
       else TRY(launch_row_tiles(c, row_launch(c, dx, dy, 1.0, 0.0), 1, s));
     }
     CUDA_TRY(cudaEventRecord(e1, s));
     CUDA_TRY(cudaEventSynchronize(e1));
     CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
-    if (cb == 0 || ms < best) { best = ms; pick = cb; }
+    if (cb == 0 || ms < best * (pick == 0 ? 0.97f : 1.0f)) { best = ms; pick = cb; }
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
@@ -2471,8 +2477,24 @@ msrep_status_t msrep_spmm(msrep_ctx h, const void* alpha_p, const void* X, const
     if (gather) TRY(allgatherv_y(c, Y, seg_lo, seg_hi, s, k));
     return MSREP_OK;
   }
-  if (colwise(c->fmt)) {   // one strided pass of the band kernel (and merge) per vector of the block
-    for (int j = 0; j < k; j++) TRY(col_spmv(c, alpha, X, beta, Y, k, j, my_lo, my_hi, s));
+  if (colwise(c->fmt)) {
+    // column formats: X and Y go planar (k contiguous vectors), one SpMV pass of the band kernel
+    // (and its merge) per vector, and Y back to row-major -- strided gathers / stores of the row-major
+    // block directly were slower than k SpMVs (stencil k = 8: 0.64x)
+    const size_t nx = (size_t)std::max<int64_t>(1, c->n), ny = (size_t)std::max<int64_t>(1, c->m);
+    if (c->mm_planar_bytes < (nx + ny) * (size_t)k * V) {
+      void* q;
+      TRY(dalloc(c, (nx + ny) * 8 * V, &q, s));   // room for k <= 8
+      c->d_mm_planar = q;
+      c->mm_planar_bytes = (nx + ny) * 8 * V;
+    }
+    char* xt = static_cast<char*>(c->d_mm_planar);
+    char* yt = xt + nx * (size_t)k * V;
+    CUDA_TRY(launch_planar(X, xt, 0, c->n, k, (int64_t)nx, 1, dt, s));
+    if (beta != 0.0) CUDA_TRY(launch_planar(Y, yt, my_lo, my_hi, k, (int64_t)ny, 1, dt, s));
+    for (int j = 0; j < k; j++)
+      TRY(col_spmv(c, alpha, xt + (size_t)j * nx * V, beta, yt + (size_t)j * ny * V, 1, 0, my_lo, my_hi, s));
+    CUDA_TRY(launch_planar(yt, Y, my_lo, my_hi, k, (int64_t)ny, 0, dt, s));
     if (gather) TRY(allgatherv_y(c, Y, seg_lo, seg_hi, s, k));
     return MSREP_OK;
   }
@@ -2490,7 +2512,7 @@ msrep_status_t msrep_spmm(msrep_ctx h, const void* alpha_p, const void* X, const
   L.xmax = c->n > 0 ? (uint32_t)(c->n - 1) : 0u;
   L.alpha = alpha; L.beta = beta; L.rec = c->d_rec_mm;
   L.dtype = dt; L.has_sell = c->nsell > 0;
-  L.hot = c->d_hot;   // SpMM untags hot column ids through the list (no shared-memory cache)
+  L.hot = c->d_hot; L.nhot = c->nhot;   // SpMM untags hot column ids through the list (no shared-memory cache)
   TRY(prepare_x(c, X, k, s));
   if (c->nxc) { L.x = c->d_xc_mm; L.xmax = (uint32_t)(c->nxc - 1); }
   cudaEvent_t pe;

@@ -236,6 +236,9 @@ cudaError_t launch_rebase(const int64_t* gptr, int32_t* lptr, int64_t count, int
                           cudaStream_t s);                                                  // clamp(gptr,lo,hi)-lo
 cudaError_t launch_pack(const PackLaunch& L, cudaStream_t s);
 cudaError_t launch_sum_peers(const SumLaunch& L, cudaStream_t s);
+// rows [r0, r1) of a k-wide row-major block <-> k planar vectors of leading dimension ld
+cudaError_t launch_planar(const void* src, void* dst, int64_t r0, int64_t r1, int k, int64_t ld, int to_planar,
+                          int dtype, cudaStream_t s);
 cudaError_t launch_col_degree(const int32_t* idx, int64_t nz, int32_t* deg, cudaStream_t s);   // deg[idx[i]]++
 cudaError_t launch_hot_slots(const int32_t* hot, int nhot, int32_t* slot, cudaStream_t s);      // slot[hot[k]] = k
 // out[i*k + j] = x[cols[i]*k + j], i < n, j < k (compact x for SpMV k = 1, SpMM k > 1)

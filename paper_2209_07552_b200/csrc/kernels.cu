@@ -545,9 +545,10 @@ __device__ __forceinline__ void mm_write_row(VT* yrow, const double (&acc)[K], d
 }
 
 // a SEG / slab column id of a hot-x partition (tag bit set) -> the column (SpMM gathers K-wide rows
-// of X, which the SpMV's shared-memory x cache does not hold)
-__device__ __forceinline__ uint32_t untag(const RowLaunch& P, uint32_t c) {
-  return (c & HOT_TAG) ? (uint32_t)__ldg(P.hot + (c & ~HOT_TAG)) : c;
+// of X, which the SpMV's shared-memory x cache does not hold); the slot -> column table is copied
+// into shared memory at kernel start (a dependent global load per hot gather was 1.5x slower)
+__device__ __forceinline__ uint32_t untag(const int* hot_s, uint32_t c) {
+  return (c & HOT_TAG) ? (uint32_t)hot_s[c & ~HOT_TAG] : c;
 }
 
 template <typename VT, int K, bool SELL>
@@ -569,6 +570,9 @@ __global__ void __launch_bounds__(WARPS * 32, MSREP_ROW_MINB) rows_mm_kernel(con
   const double alpha = P.alpha, beta = P.beta;
   const uint32_t xmax = P.xmax;
   const uint64_t xpol = policy_evict_last();
+  int* hot_s = reinterpret_cast<int*>(smem + Lay::HOT_OFF);   // P.nhot entries (launch sizes the buffer)
+  for (int k = threadIdx.x; k < P.nhot; k += WARPS * 32) hot_s[k] = __ldg(P.hot + k);
+  __syncthreads();
 
   uint64_t pol = 0;
   int4 dn = make_int4(0, 0, 0, -1);
@@ -689,7 +693,7 @@ __global__ void __launch_bounds__(WARPS * 32, MSREP_ROW_MINB) rows_mm_kernel(con
         VT xr[BG][K];
 #pragma unroll
         for (int b = 0; b < BG; b++) {
-          if (lane + 32 * (u0 + b) < nnz) ldx_row<VT, K>(x + (int64_t)untag(P, c[u0 + b]) * K, xr[b], xpol);
+          if (lane + 32 * (u0 + b) < nnz) ldx_row<VT, K>(x + (int64_t)untag(hot_s, c[u0 + b]) * K, xr[b], xpol);
           else {
 #pragma unroll
             for (int j = 0; j < K; j++) xr[b][j] = VT(0);
@@ -731,7 +735,7 @@ __global__ void __launch_bounds__(WARPS * 32, MSREP_ROW_MINB) rows_mm_kernel(con
       for (int b = 0; b < BG; b++) {
         const int j = j0 + b;
         const bool on = j <= QMAX && (j < QMAX ? j < q : extra);
-        if (on) ldx_row<VT, K>(x + (int64_t)untag(P, c[j <= QMAX ? j : QMAX]) * K, xr[b], xpol);
+        if (on) ldx_row<VT, K>(x + (int64_t)untag(hot_s, c[j <= QMAX ? j : QMAX]) * K, xr[b], xpol);
         else {
 #pragma unroll
           for (int jj = 0; jj < K; jj++) xr[b][jj] = VT(0);
@@ -1265,16 +1269,38 @@ __global__ void sum_peers_kernel(const SumLaunch L) {
   }
 }
 
+// SpMM on the column formats: a block of k row-major vectors <-> k contiguous vectors, rows [r0, r1)
+// (to_planar: dst[j*ld + i] = src[i*k + j]; else dst[i*k + j] = src[j*ld + i])
+template <typename VT>
+__global__ void planar_kernel(const VT* __restrict__ src, VT* __restrict__ dst, int64_t r0, int64_t r1, int k,
+                              int64_t ld, int to_planar) {
+  // a thread per row: the planar side is a coalesced vector per j, the row-major side k contiguous values
+  for (int64_t i = r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r1; i += (int64_t)gridDim.x * blockDim.x) {
+    if (to_planar) {
+      for (int j = 0; j < k; j++) dst[(int64_t)j * ld + i] = src[i * k + j];
+    } else {
+      for (int j = 0; j < k; j++) dst[i * k + j] = src[(int64_t)j * ld + i];
+    }
+  }
+}
+
 // --------------------------------------------------------- small kernels
-// one thread per (split row, vector j < k): k = 1 for SpMV, the block width for SpMM; records,
-// head partials and y are k-wide (record r, vector j at r*k + j; y row-major [m x k])
+// one WARP per (split row, vector j < k): k = 1 for SpMV, the block width for SpMM; records, head
+// partials and y are k-wide (record r, vector j at r*k + j; y row-major [m x k]).  The row's records
+// are summed lane-strided and joined by a fixed shuffle tree (R-MAT's heaviest rows have ~470
+// records: one thread summing them serially made the fix-up 30 us), then lane 0 adds the routed
+// head partials in part order and applies alpha, beta once.  Fixed order: bit-reproducible.
 template <typename VT>
 __global__ void fixup_kernel(const FixupLaunch F) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= (int64_t)F.nsplit * F.k) return;
+  const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= (int64_t)F.nsplit * F.k) return;   // whole warps exit together
   const int s = (int)(t / F.k), jv = (int)(t % F.k), K = F.k;
   double acc = 0.0;
-  for (int k = F.sr_rec[2 * s]; k < F.sr_rec[2 * s + 1]; k++) acc = acc + F.rec[(int64_t)k * K + jv];
+  for (int k = F.sr_rec[2 * s] + lane; k < F.sr_rec[2 * s + 1]; k += 32) acc += F.rec[(int64_t)k * K + jv];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(FULL, acc, off);
+  if (lane != 0) return;
   for (int h = F.sr_head[2 * s]; h < F.sr_head[2 * s + 1]; h++) {
     const int j = F.head_list[h];
     double hv = 0.0;
@@ -1586,7 +1612,7 @@ cudaError_t launch_pack(const PackLaunch& L, cudaStream_t s) {
 
 cudaError_t launch_fixup(const FixupLaunch& F, cudaStream_t s) {
   if (F.nsplit == 0) return cudaSuccess;
-  int g = (F.nsplit * F.k + 127) / 128;
+  const int g = (int)(((int64_t)F.nsplit * F.k * 32 + 127) / 128);   // a warp per (split row, vector)
   if (F.dtype == 0) fixup_kernel<double><<<g, 128, 0, s>>>(F);
   else fixup_kernel<float><<<g, 128, 0, s>>>(F);
   return cudaGetLastError();
@@ -1610,6 +1636,15 @@ cudaError_t launch_axpby_py(const double* py, void* y, int64_t n, double alpha, 
   if (n <= 0) return cudaSuccess;
   if (dtype == 0) axpby_kernel<double><<<elementwise_grid(n), 256, 0, s>>>(py, (double*)y, n, alpha, beta, ys);
   else axpby_kernel<float><<<elementwise_grid(n), 256, 0, s>>>(py, (float*)y, n, alpha, beta, ys);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_planar(const void* src, void* dst, int64_t r0, int64_t r1, int k, int64_t ld, int to_planar,
+                          int dtype, cudaStream_t s) {
+  if (r1 <= r0) return cudaSuccess;
+  const int g = elementwise_grid(r1 - r0);
+  if (dtype == 0) planar_kernel<double><<<g, 256, 0, s>>>((const double*)src, (double*)dst, r0, r1, k, ld, to_planar);
+  else planar_kernel<float><<<g, 256, 0, s>>>((const float*)src, (float*)dst, r0, r1, k, ld, to_planar);
   return cudaGetLastError();
 }
 
@@ -1680,7 +1715,7 @@ cudaError_t launch_cg(int op, int dtype, void* a, void* b, void* c, const void* 
 namespace {
 template <typename VT, int K, bool SELL>
 cudaError_t launch_rows_mm_t(const RowLaunch& L, cudaStream_t s) {
-  constexpr int b = RowLayout<VT, SELL>::TOTAL;
+  const int b = RowLayout<VT, SELL>::HOT_OFF + L.nhot * 4;   // + the hot slot -> column table
   cudaError_t e = set_smem(rows_mm_kernel<VT, K, SELL>, b);
   if (e) return e;
   rows_mm_kernel<VT, K, SELL><<<grid_for(rows_mm_kernel<VT, K, SELL>, b, L.ntiles), WARPS * 32, b, s>>>(L);

@@ -186,3 +186,43 @@ def test_loopback_cg(fmt):
         assert rr <= 1e-12 and np.max(np.abs(xv - xs)) < 1e-9
     assert len({o[0] for o in outs}) == 1
     assert all(np.array_equal(outs[0][2], o[2]) for o in outs)   # replicated, identical iterates
+
+
+@pytest.mark.parametrize("fmt", ["csr", "csc"])
+@pytest.mark.parametrize("world,ppr", [(2, 1), (4, 2)])
+def test_loopback_partition_slice_rank_local(fmt, world, ppr):
+    """bench.py's N > 1 path: every rank holds ONLY the entries of the rows (columns) its nonzero range
+    touches -- gen.config_rows-style slices -- and partitions through msrep_partition_slice; the merged
+    result equals the oracle bit for bit."""
+    import torch
+    import paper_2209_07552_b200 as M
+    A = gen.rmat(13, seed=308, kind=gen.SMALLINT)
+    B = A if fmt == "csr" else gen.transpose(A)
+    x = gen.vector(A["n"], 309, kind=gen.SMALLINT); y = gen.vector(A["m"], 310, kind=gen.SMALLINT)
+    ref = oracle_ref(A, x, y, 1.5, 0.5)
+    outer = A["m"] if fmt == "csr" else A["n"]
+    parts = M.msrep_plan(M.FORMATS[fmt], outer, A.nnz, world * ppr, ptr=B["ptr"])
+
+    def body(r, ctx, st):
+        mine = parts[r * ppr:(r + 1) * ppr]
+        ne = mine[mine["start_row"] >= 0]
+        r0, r1 = int(ne["start_row"][0]), int(ne["end_row"][-1]) + 1
+        z0, z1 = int(B["ptr"][r0]), int(B["ptr"][r1])
+        ctx.partition_slice(fmt, A["m"], A["n"], B["ptr"], B["idx"][z0:z1].copy(), B["val"][z0:z1].copy(), z0,
+                            stream=st.cuda_stream)
+        yd = torch.as_tensor(y).cuda()
+        ctx.spmv(1.5, torch.as_tensor(x).cuda(), 0.5, yd, M.Y_REPLICATED, st.cuda_stream)
+        st.synchronize()
+        return yd.cpu().numpy()
+    for out in _run_ranks(world, ppr, body):
+        assert np.array_equal(out, ref)
+
+
+def test_partition_slice_rejects_short_slice():
+    import paper_2209_07552_b200 as M
+    A = gen.rmat(10, seed=311, kind=gen.SMALLINT)
+    ctx = M.Context(0, 1, None, 0, 1)
+    with pytest.raises(M.MsrepError) as e:   # one rank holds everything: a partial slice is rejected
+        ctx.partition_slice("csr", A["m"], A["n"], A["ptr"], A["idx"][5:].copy(), A["val"][5:].copy(), 5)
+    assert e.value.status == 1
+    ctx.close()

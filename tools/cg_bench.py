@@ -46,4 +46,6 @@ alg = st["alg_bytes_beta0"] + vec_bytes
 print(json.dumps({"what": "msrep_cg on the SPD 27-point stencil", "format": a.format,
                   "cuda_graph": bool(a.graph), "m": A["m"], "nnz": A.nnz,
                   "iterations": it, "relres": rr, "ms_per_iter": ms, "spmv_alg_bytes": st["alg_bytes_beta0"],
-                  "vector_bytes": vec_bytes, "GBps": alg / (ms * 1e-3) / 1e9}), flush=True)
+                  "vector_bytes": vec_bytes, "GBps": alg / (ms * 1e-3) / 1e9,
+                  "x_no_allocate": st["x_no_allocate"], "sell_1cta": st["sell_1cta"], "nsell": st["nsell"],
+                  "split_launch_tiles": st["ntiles"] - st["nsell"]}), flush=True)
