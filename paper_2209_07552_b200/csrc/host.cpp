@@ -23,6 +23,7 @@
 #include <thread>
 #include <vector>
 
+#include <sys/mman.h>
 #include <sys/syscall.h>
 #include <unistd.h>
 
@@ -187,6 +188,20 @@ void plan_coo_unsorted(int np, const int32_t* row, const std::vector<int64_t>& b
     d.end_row = hi;
   }
 }
+
+// ------------------------------------------------ large host scratch on 2 MB pages
+struct HugeBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  explicit HugeBuf(size_t n) : bytes(n) {
+    p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (p == MAP_FAILED) { p = nullptr; throw std::bad_alloc(); }
+    madvise(p, bytes, MADV_HUGEPAGE);
+  }
+  ~HugeBuf() { if (p) munmap(p, bytes); }
+  HugeBuf(const HugeBuf&) = delete;
+  HugeBuf& operator=(const HugeBuf&) = delete;
+};
 
 // ------------------------------------------------ host threads for the partition scans
 // The partition's O(nnz) host passes run on the host threads, one contiguous index range each
@@ -966,8 +981,11 @@ msrep_status_t build_csc_bands(const Ctx& c, const std::vector<int64_t>& lp, con
     }
   }
   kbeg[(size_t)keys] = run_off;
-  std::unique_ptr<uint32_t[]> tpk(new uint32_t[(size_t)std::max<int64_t>(1, nz)]);
-  std::unique_ptr<char[]> tval(new char[(size_t)std::max<int64_t>(1, nz) * V]);
+  // the scatter below writes ~1M random buckets: 2 MB pages cut its TLB misses
+  HugeBuf tpk_b((size_t)std::max<int64_t>(1, nz) * 4), tval_b((size_t)std::max<int64_t>(1, nz) * V);
+  uint32_t* tpk_p = static_cast<uint32_t*>(tpk_b.p);
+  struct { uint32_t* p; uint32_t* get() const { return p; } uint32_t& operator[](size_t i) const { return p[i]; } } tpk{tpk_p};
+  struct { char* p; char* get() const { return p; } } tval{static_cast<char*>(tval_b.p)};
   auto scatter = [&](auto vtag) {
     using VT = decltype(vtag);
     const VT* vv = reinterpret_cast<const VT*>(vals);

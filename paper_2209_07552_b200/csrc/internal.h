@@ -37,7 +37,10 @@ constexpr int WARPS = MSREP_WARPS;   // warps per CTA (each with its own TMA rin
 // HOT_WARPS warps per SM holds up to HOT_BYTES of x (sized per partition: HOT_AUTO_BYTES by
 // default, MSREP_TUNE_HOT_X KiB when set).
 constexpr uint32_t HOT_TAG = 0x80000000u;
-constexpr int HOT_WARPS = 16;
+#ifndef MSREP_HOT_WARPS
+#define MSREP_HOT_WARPS 16
+#endif
+constexpr int HOT_WARPS = MSREP_HOT_WARPS;
 constexpr int HOT_BYTES = 96 * 1024;
 #ifndef MSREP_HOT_AUTO_KB
 #define MSREP_HOT_AUTO_KB 32

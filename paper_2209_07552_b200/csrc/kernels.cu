@@ -471,6 +471,22 @@ __global__ void __launch_bounds__(HOT ? HOT_WARPS * 32 : WARPS * 32,
     int cur = len > 0 ? key0 : INT_MAX;
     int first = cur, nseg = len > 0 ? 1 : 0;
     double acc = 0.0, firstv = 0.0;
+#ifndef MSREP_SEG_BRANCHY
+    // branch-free: the row change of an element is a predicate (predicated rsum store, selects), so
+    // the lanes of a warp never diverge here (a branch per element cost a BSSY/BSYNC pair each)
+#pragma unroll
+    for (int j = 0; j <= QMAX; j++) {
+      const bool on = j < QMAX ? j < q : extra;
+      const int k = (int)((kp[j >> 2] >> (8 * (j & 3))) & 0xffu);
+      const bool nw = on && k != cur;
+      if (nw && nseg >= 2) rsum[cur] = acc;
+      firstv = (nw && nseg == 1) ? acc : firstv;
+      nseg += nw ? 1 : 0;
+      cur = nw ? k : cur;
+      acc = nw ? 0.0 : acc;
+      acc = on ? fma((double)v[j], (double)xv[j], acc) : acc;
+    }
+#else
 #pragma unroll
     for (int j = 0; j <= QMAX; j++) {
       const bool on = j < QMAX ? j < q : extra;
@@ -485,6 +501,7 @@ __global__ void __launch_bounds__(HOT ? HOT_WARPS * 32 : WARPS * 32,
         acc = fma((double)v[j], (double)xv[j], acc);
       }
     }
+#endif
     // ---- join rows that cross lanes: inclusive run of preceding lanes ending in the same row
     int pk;
     double pv;
