@@ -159,7 +159,10 @@ struct RowLaunch {
 // moved by one 1-D TMA.  packed = (row & (CB_ROWS-1)) | ((window col - chunk
 // base) << CB_LOG2); 0xffffffff marks a hole (never a valid entry: a chunk
 // spans CB_CHUNK = 2^19 - 1 columns).
-constexpr int CB_LOG2 = 13;
+#ifndef MSREP_CB_LOG2
+#define MSREP_CB_LOG2 13
+#endif
+constexpr int CB_LOG2 = MSREP_CB_LOG2;
 constexpr int CB_ROWS = 1 << CB_LOG2;      // 8192 rows per band: 64 KB fp64 accumulator
 constexpr int CB_W = 15;                   // consumer warps (+1 producer: 16 warps, 128 registers)
 constexpr int64_t CB_CHUNK = (1ll << (32 - CB_LOG2)) - 1;

@@ -251,6 +251,10 @@ __device__ __forceinline__ VT ldx_hot(const VT* x, const HotRef& hbase, uint32_t
 // One SELL tile with R rows per lane (internal.h): all R*W column indices are read from the
 // slot, then all R*W x gathers are in flight before the first FMA; padding is masked by the
 // row length, so results equal the plain row sums.
+#ifndef MSREP_SELL_EARLY_F32
+#define MSREP_SELL_EARLY_F32 0
+#endif
+constexpr bool SELL_EARLY_F32 = MSREP_SELL_EARLY_F32;
 template <typename VT, int R, bool MIRROR, class Refill>
 __device__ __forceinline__ void sell_tile(const RowLaunch& P, const int4 d, const unsigned char* st, const int lane,
                                           const VT* __restrict__ x, VT* __restrict__ y, double alpha, double beta,
@@ -270,19 +274,38 @@ __device__ __forceinline__ void sell_tile(const RowLaunch& P, const int4 d, cons
     mylen[k] = lens[k * 32 + lane];
     yv[k] = (beta != 0.0 && row < nrows) ? (double)y[P.ybase + d.x + row] : 0.0;
   }
-  uint32_t c[U];
   VT xs[U];
-#pragma unroll
-  for (int u = 0; u < U; u++) c[u] = u < RW ? sc[u * 32 + lane] : 0u;   // no loop-carried state
-#pragma unroll
-  for (int u = 0; u < U; u++) xs[u] = u < RW ? ldg_ro(x + c[u]) : VT(0);
   double acc[R];
 #pragma unroll
   for (int k = 0; k < R; k++) acc[k] = 0.0;
+  if constexpr (V == 4 && SELL_EARLY_F32 && R == 1) {
+    // fp32: the tile's gathers and values fit in registers (2 x 32 slots; each column id is consumed
+    // by its gather), so the slot is refilled as soon as the tile is read -- the next tile's TMA
+    // overlaps this tile's gathers instead of following them (fp64 reads the tile in place)
 #pragma unroll
-  for (int u = 0; u < U; u++) {
-    const int k = u % R, t = u / R;           // compile-time after unrolling
-    if (u < RW && t < mylen[k]) acc[k] = fma((double)sv[u * 32 + lane], (double)xs[u], acc[k]);
+    for (int u = 0; u < U; u++) xs[u] = u < RW ? ldg_ro(x + sc[u * 32 + lane]) : VT(0);
+    VT vr[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) vr[u] = u < RW ? sv[u * 32 + lane] : VT(0);
+    fence_proxy_async();
+    __syncwarp();
+    refill();
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int k = u % R, t = u / R;
+      if (u < RW && t < mylen[k]) acc[k] = fma((double)vr[u], (double)xs[u], acc[k]);
+    }
+  } else {
+    uint32_t c[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) c[u] = u < RW ? sc[u * 32 + lane] : 0u;   // no loop-carried state
+#pragma unroll
+    for (int u = 0; u < U; u++) xs[u] = u < RW ? ldg_ro(x + c[u]) : VT(0);
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int k = u % R, t = u / R;           // compile-time after unrolling
+      if (u < RW && t < mylen[k]) acc[k] = fma((double)sv[u * 32 + lane], (double)xs[u], acc[k]);
+    }
   }
 #pragma unroll
   for (int k = 0; k < R; k++) {
@@ -296,8 +319,10 @@ __device__ __forceinline__ void sell_tile(const RowLaunch& P, const int4 d, cons
         for (int mi = 0; mi < P.nmirror; mi++) static_cast<VT*>(P.mirror[mi])[yi] = (VT)o;   // fused allgather
     }
   }
-  __syncwarp();   // the tile was read in place: refill the slot only now
-  refill();
+  if constexpr (!(V == 4 && SELL_EARLY_F32 && R == 1)) {
+    __syncwarp();   // the tile was read in place: refill the slot only now
+    refill();
+  }
 }
 
 template <typename VT, bool SELL, bool MIRROR, bool NA, bool HOT, int CL>
@@ -471,22 +496,6 @@ __global__ void __launch_bounds__(HOT ? HOT_WARPS * 32 : WARPS * 32,
     int cur = len > 0 ? key0 : INT_MAX;
     int first = cur, nseg = len > 0 ? 1 : 0;
     double acc = 0.0, firstv = 0.0;
-#ifndef MSREP_SEG_BRANCHY
-    // branch-free: the row change of an element is a predicate (predicated rsum store, selects), so
-    // the lanes of a warp never diverge here (a branch per element cost a BSSY/BSYNC pair each)
-#pragma unroll
-    for (int j = 0; j <= QMAX; j++) {
-      const bool on = j < QMAX ? j < q : extra;
-      const int k = (int)((kp[j >> 2] >> (8 * (j & 3))) & 0xffu);
-      const bool nw = on && k != cur;
-      if (nw && nseg >= 2) rsum[cur] = acc;
-      firstv = (nw && nseg == 1) ? acc : firstv;
-      nseg += nw ? 1 : 0;
-      cur = nw ? k : cur;
-      acc = nw ? 0.0 : acc;
-      acc = on ? fma((double)v[j], (double)xv[j], acc) : acc;
-    }
-#else
 #pragma unroll
     for (int j = 0; j <= QMAX; j++) {
       const bool on = j < QMAX ? j < q : extra;
@@ -501,7 +510,6 @@ __global__ void __launch_bounds__(HOT ? HOT_WARPS * 32 : WARPS * 32,
         acc = fma((double)v[j], (double)xv[j], acc);
       }
     }
-#endif
     // ---- join rows that cross lanes: inclusive run of preceding lanes ending in the same row
     int pk;
     double pv;
