@@ -251,10 +251,6 @@ __device__ __forceinline__ VT ldx_hot(const VT* x, const HotRef& hbase, uint32_t
 // One SELL tile with R rows per lane (internal.h): all R*W column indices are read from the
 // slot, then all R*W x gathers are in flight before the first FMA; padding is masked by the
 // row length, so results equal the plain row sums.
-#ifndef MSREP_SELL_EARLY_F32
-#define MSREP_SELL_EARLY_F32 0
-#endif
-constexpr bool SELL_EARLY_F32 = MSREP_SELL_EARLY_F32;
 template <typename VT, int R, bool MIRROR, class Refill>
 __device__ __forceinline__ void sell_tile(const RowLaunch& P, const int4 d, const unsigned char* st, const int lane,
                                           const VT* __restrict__ x, VT* __restrict__ y, double alpha, double beta,
@@ -278,34 +274,15 @@ __device__ __forceinline__ void sell_tile(const RowLaunch& P, const int4 d, cons
   double acc[R];
 #pragma unroll
   for (int k = 0; k < R; k++) acc[k] = 0.0;
-  if constexpr (V == 4 && SELL_EARLY_F32 && R == 1) {
-    // fp32: the tile's gathers and values fit in registers (2 x 32 slots; each column id is consumed
-    // by its gather), so the slot is refilled as soon as the tile is read -- the next tile's TMA
-    // overlaps this tile's gathers instead of following them (fp64 reads the tile in place)
+  uint32_t c[U];
 #pragma unroll
-    for (int u = 0; u < U; u++) xs[u] = u < RW ? ldg_ro(x + sc[u * 32 + lane]) : VT(0);
-    VT vr[U];
+  for (int u = 0; u < U; u++) c[u] = u < RW ? sc[u * 32 + lane] : 0u;   // no loop-carried state
 #pragma unroll
-    for (int u = 0; u < U; u++) vr[u] = u < RW ? sv[u * 32 + lane] : VT(0);
-    fence_proxy_async();
-    __syncwarp();
-    refill();
+  for (int u = 0; u < U; u++) xs[u] = u < RW ? ldg_ro(x + c[u]) : VT(0);
 #pragma unroll
-    for (int u = 0; u < U; u++) {
-      const int k = u % R, t = u / R;
-      if (u < RW && t < mylen[k]) acc[k] = fma((double)vr[u], (double)xs[u], acc[k]);
-    }
-  } else {
-    uint32_t c[U];
-#pragma unroll
-    for (int u = 0; u < U; u++) c[u] = u < RW ? sc[u * 32 + lane] : 0u;   // no loop-carried state
-#pragma unroll
-    for (int u = 0; u < U; u++) xs[u] = u < RW ? ldg_ro(x + c[u]) : VT(0);
-#pragma unroll
-    for (int u = 0; u < U; u++) {
-      const int k = u % R, t = u / R;           // compile-time after unrolling
-      if (u < RW && t < mylen[k]) acc[k] = fma((double)sv[u * 32 + lane], (double)xs[u], acc[k]);
-    }
+  for (int u = 0; u < U; u++) {
+    const int k = u % R, t = u / R;           // compile-time after unrolling
+    if (u < RW && t < mylen[k]) acc[k] = fma((double)sv[u * 32 + lane], (double)xs[u], acc[k]);
   }
 #pragma unroll
   for (int k = 0; k < R; k++) {
@@ -319,10 +296,8 @@ __device__ __forceinline__ void sell_tile(const RowLaunch& P, const int4 d, cons
         for (int mi = 0; mi < P.nmirror; mi++) static_cast<VT*>(P.mirror[mi])[yi] = (VT)o;   // fused allgather
     }
   }
-  if constexpr (!(V == 4 && SELL_EARLY_F32 && R == 1)) {
-    __syncwarp();   // the tile was read in place: refill the slot only now
-    refill();
-  }
+  __syncwarp();   // the tile was read in place: refill the slot only now
+  refill();
 }
 
 template <typename VT, bool SELL, bool MIRROR, bool NA, bool HOT, int CL>
