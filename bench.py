@@ -56,10 +56,13 @@ def parse(argv=None):
     p.add_argument("--parts-per-rank", type=int, default=1)
     p.add_argument("--hot-x", type=int, default=-1,
                    help="MSREP_TUNE_HOT_X: shared-memory hot-x cache (-1 auto, 0 off, 1 on, k > 1: k KiB)")
-    p.add_argument("--compact-x", type=int, default=-1, choices=[-1, 0, 1],
+    p.add_argument("--compact-x", type=int, default=-1, choices=[-1, 0, 1, 2],
                    help="MSREP_TUNE_COMPACT_X: gather the rank's distinct x entries first (-1 auto, 0 off, 1 on)")
     p.add_argument("--hot-cluster", type=int, default=1, choices=[1, 2],
                    help="MSREP_TUNE_HOT_CLUSTER: CTAs sharing one hot-x cache over DSMEM")
+    p.add_argument("--col-layout", type=int, default=-1, choices=[-1, 0, 1],
+                   help="MSREP_TUNE_COL_LAYOUT for pCSC / column-sorted pCOO: -1 auto (row tiles over the GPU-"
+                        "transposed slice), 0 row bands (csc_band_kernel), 1 row tiles")
     p.add_argument("--xload", type=int, default=-1, choices=[-1, 0, 1],
                    help="MSREP_TUNE_XLOAD: x-gather L1 policy (-1 timed at partition, 0 allocate, 1 no_allocate)")
     p.add_argument("--fused", action="store_true",
@@ -370,6 +373,7 @@ def main():
     ctx.set_tuning("xload", a.xload)
     ctx.set_tuning("compact_x", a.compact_x)
     ctx.set_tuning("hot_cluster", a.hot_cluster)
+    ctx.set_tuning("col_layout", a.col_layout)
     local_gen = rank_local_ok(a)
     A = None
     if local_gen:
@@ -506,7 +510,7 @@ def main():
 
     # roofline of the dominant kernel (rank 0's launch; algorithmic bytes / event-timed duration)
     hbm_peak, peak_kind = load_peaks()
-    kname = "csc_band_kernel" if colwise(a) else "rows_kernel"
+    kname = "csc_band_kernel" if (colwise(a) and st["col_layout"] == 0) else "rows_kernel"
     traffic = None
     try:   # DRAM bytes per launch of that kernel from a committed `ncu --set full` capture (profiles/)
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
@@ -533,6 +537,8 @@ def main():
             "warmup": a.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": a.dtype, "data": "synthetic (gen/, seeded; no SuiteSparse offline)",
             "config": {"workload": wl, "format": "p" + a.format.upper(), "layout": a.layout,
+                       "device_layout": ("row bands" if st["col_layout"] == 0 else "row tiles (slice transposed on the GPU)")
+                                        if colwise(a) else "row tiles",
                        "m": m, "n": n, "nnz": nnz, "alpha": ALPHA, "beta": BETA,
                        "parts_per_rank": ppr, "split": a.split,
                        "merge": "fused epilogue stores into peer y (msrep_spmv_mirror)" if (a.fused and world > 1)
@@ -567,9 +573,10 @@ def main():
             "gpu_launches": int(a.steps * st["kernels_per_spmv"]),
             "clocks": clocks,
             "partition_ms": st["partition_ms"],
+            "partition_phase_ms": dict(zip(("validate", "plan", "schedule", "upload_pack"), list(st["phase_ms"]))),
             "stats_rank0": {k: st[k] for k in ("nnz_rank", "ntiles", "nsell", "nslabs", "nsplit_rows",
                                                "distinct_cols", "kernels_per_spmv", "tile_bytes", "x_no_allocate",
-                                               "nhot", "hot_nnz", "x_compact")},
+                                               "nhot", "hot_nnz", "x_compact", "col_layout")},
         }
         print(json.dumps(out), flush=True)
     ctx.close()

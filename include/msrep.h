@@ -149,6 +149,8 @@ typedef struct {
   int64_t stream_bytes;      /* bytes the built layout moves per SpMV (beta != 0): tile blobs
                                 as stored + x entries + y; pCOO stores u8 tile row keys, not
                                 the 4-B row ids alg_bytes counts                              */
+  int64_t col_layout;        /* column formats: 1 row tiles (slice transposed on the GPU), 0 row
+                                bands (MSREP_TUNE_COL_LAYOUT); row formats: -1                */
 } msrep_stats;
 
 /* NCCL unique id for the communicator (rank 0 creates it, the caller
@@ -272,7 +274,9 @@ msrep_status_t msrep_set_residency(msrep_ctx ctx, msrep_residency residency, int
  *   MSREP_TUNE_COMPACT_X compact x for the row formats, applied by the next
  *                       msrep_partition: the tiles index the rank's distinct
  *                       columns and every SpMV first gathers x' = x[cols]
- *                       (one launch): -1 (default) when x is >= 32 MB, 0 off, 1 on.
+ *                       (one launch): -1 (default) when x is >= 32 MB, 0 off, 1 on,
+ *                       2 on with x' in decreasing column degree instead of column
+ *                       order (the most-gathered entries share cache lines).
  *   MSREP_TUNE_HOT_CLUSTER CTAs sharing one hot-x cache, applied by the next
  *                       msrep_partition: 1 (default) -- every CTA holds the
  *                       whole cache; 2 -- the kernel runs as CTA pairs
@@ -282,9 +286,20 @@ msrep_status_t msrep_set_residency(msrep_ctx ctx, msrep_residency residency, int
  *   MSREP_TUNE_SELL     sliced-ELL tiles for runs of regular rows (row formats),
  *                       applied by the next msrep_partition: 1 (default) on,
  *                       0 every row goes to SEG tiles / slabs.
+ *   MSREP_TUNE_COL_LAYOUT device layout of the column formats (pCSC, column-
+ *                       sorted / unsorted pCOO), applied by the next
+ *                       msrep_partition: -1 (default) and 1 -- ROW TILES: the
+ *                       rank's column-ordered slice is transposed on the GPU at
+ *                       partition time (a stable sort by row, "the
+ *                       kernel is invoked with transpose on") and walked by the
+ *                       row-tile kernel, its partial y merged column-style as
+ *                       before; 0 -- ROW BANDS: the column-ordered scatter into
+ *                       shared-memory row bands (csc_band_kernel), built on the
+ *                       host threads.  Both give the exact sums of the rank's
+ *                       entries; the summation order within a row differs.
  * Errors: MSREP_ERR_INVALID_ARG (unknown knob or value). */
 typedef enum { MSREP_TUNE_XLOAD = 0, MSREP_TUNE_CG_GRAPH = 1, MSREP_TUNE_HOT_X = 2, MSREP_TUNE_COMPACT_X = 3,
-               MSREP_TUNE_HOT_CLUSTER = 4, MSREP_TUNE_SELL = 5 } msrep_tuning;
+               MSREP_TUNE_HOT_CLUSTER = 4, MSREP_TUNE_SELL = 5, MSREP_TUNE_COL_LAYOUT = 6 } msrep_tuning;
 msrep_status_t msrep_set_tuning(msrep_ctx ctx, msrep_tuning knob, int value);
 
 /* Select the split used by the next msrep_partition on this context (default

@@ -339,8 +339,13 @@ struct Ctx {
   double* d_head_local = nullptr;
   double* d_head_all = nullptr;
   int* d_fence = nullptr;            // msrep_spmv_mirror completion fence (nranks > 1)
-  double* d_py = nullptr;
+  void* d_py = nullptr;              // column formats, nranks > 1: the partial y of the rank (fp64; row tiles: VT)
   int64_t py_len = 0;
+  bool py_f32 = false;              // d_py holds fp32 (an fp32 partition on row tiles)
+  // column formats on row tiles (MSREP_TUNE_COL_LAYOUT): the slice transposed at partition time
+  bool col_rows = false;
+  int64_t ybase = 0;                // y row of tile window row 0 (row formats: wlo; column formats on row tiles: 0)
+  int64_t xoff = 0, xn = 0;         // x entries the tiles index: x[xoff + j], j < xn (row formats: 0, n)
   // pCSC row-band layout
   int4* d_citems = nullptr;
   int64_t* d_item_off = nullptr;
@@ -420,6 +425,7 @@ struct Ctx {
   int tune_xload = -1;              // -1 auto, 0 allocate, 1 no_allocate
   int tune_cg_graph = 1;
   int tune_hot = -1;                // -1 auto, 0 off, 1 on
+  int tune_col_layout = -1;         // column formats: -1 auto (row tiles), 0 row bands, 1 row tiles
 
   // profiling hook: event pairs around the dominant kernel
   bool prof = false;
@@ -660,16 +666,16 @@ void rank_segments(msrep_format fmt, int64_t m, int nranks, int vparts, const st
 // [R_j, R_{j+1}) packed into row-aligned tiles (rows longer than a tile become
 // slab-split rows), and the tail row (owned, continues into later parts) as
 // slabs whose fix-up adds the head partials of the parts that continue it.
-void build_row_schedule(const Ctx& c, const std::vector<int64_t>& lp, Schedule& S, bool allow_sell = true) {
-  Packer pk(S, c.wlo, lp, (int)vsz(c.dtype));
-  const auto& P = c.parts;
-  for (int j = c.P0; j < c.P1; j++) {
+void build_row_schedule(const std::vector<msrep_part_desc>& P, int P0, int P1, int64_t B_lo, int64_t wlo, int V,
+                        const std::vector<int64_t>& lp, Schedule& S, bool allow_sell = true) {
+  Packer pk(S, wlo, lp, V);
+  for (int j = P0; j < P1; j++) {
     const msrep_part_desc& d = P[(size_t)j];
     const bool empty = d.start_idx > d.end_idx;
-    const int64_t lz1 = d.end_idx + 1 - c.B_lo;
+    const int64_t lz1 = d.end_idx + 1 - B_lo;
     int32_t h0 = S.nrec;
     if (!empty && d.start_flag) {
-      const int64_t r = d.start_row, z0 = d.start_idx - c.B_lo;
+      const int64_t r = d.start_row, z0 = d.start_idx - B_lo;
       pk.slabs(r, z0, std::min<int64_t>(lz1, pk.le(r)), true);
     }
     S.part_rec.push_back(h0);
@@ -1123,6 +1129,67 @@ msrep_status_t upload_vec(Ctx* c, const std::vector<T>& v, T** out, cudaStream_t
   return upload(c, v.data(), v.size(), out, s);
 }
 
+// Column formats on row tiles (MSREP_TUNE_COL_LAYOUT): the rank's nz_r entries [B_lo, B_hi) of a
+// column format, transposed on the GPU into the rank-local row-major slice (transpose.cu):
+//   pCSC               rows = idx, columns from the window-local column pointer lp
+//   column-sorted pCOO rows = idx, columns = major (coo_row)
+//   unsorted pCOO      rows = major (coo_row), columns = idx
+// Column ids become window-local (col - c->wlo).  Outputs on the device (allocated here, after the
+// caller's mark): t_cols / t_vals in row order and the int32 row pointer t_ptr [m + 1]; on the
+// host the same pointer as int64 (lpr), for the tile schedule.  The inputs and sort buffers are
+// freed before returning.
+msrep_status_t transpose_slice(Ctx* c, msrep_format fmt, const std::vector<int64_t>& lp, const int32_t* idx,
+                               const int32_t* coo_row, const void* val, size_t V, cudaStream_t s, int32_t** t_cols,
+                               void** t_vals, int32_t** t_ptr, std::vector<int64_t>& lpr) {
+  const int64_t nz = c->B_hi - c->B_lo, m = c->m;
+  const size_t n1 = (size_t)std::max<int64_t>(1, nz);
+  void* q;
+  TRY(dalloc(c, n1 * 4, &q, s)); *t_cols = static_cast<int32_t*>(q);
+  TRY(dalloc(c, n1 * V, &q, s)); *t_vals = q;
+  TRY(dalloc(c, ((size_t)m + 1) * 4, &q, s)); *t_ptr = static_cast<int32_t*>(q);
+  const size_t tmp_from = c->bufs.size();
+  TransposeLaunch T{};
+  T.n = nz; T.m = m; T.V = (int)V;
+  int32_t *d_rows, *d_cols;
+  const int32_t* rows_h = (fmt == MSREP_COO_UNSORTED ? coo_row : idx) + c->B_lo;
+  TRY(upload(c, rows_h, (size_t)nz, &d_rows, s));
+  TRY(dalloc(c, n1 * 4, &q, s)); d_cols = static_cast<int32_t*>(q);
+  if (fmt == MSREP_CSC) {
+    int64_t* d_lp;
+    TRY(upload_vec(c, lp, &d_lp, s));
+    CUDA_TRY(launch_expand_cols(d_lp, (int64_t)lp.size() - 1, d_cols, s));
+  } else {
+    const int32_t* cols_h = (fmt == MSREP_COO_UNSORTED ? idx : coo_row) + c->B_lo;
+    TRY(h2d(c, d_cols, cols_h, (size_t)nz * 4, s));
+    CUDA_TRY(launch_rebase_cols(d_cols, nz, (int32_t)c->wlo, d_cols, s));
+  }
+  void* d_vals;
+  TRY(dalloc(c, n1 * V, &d_vals, s));
+  TRY(h2d(c, d_vals, static_cast<const char*>(val) + (size_t)c->B_lo * V, (size_t)nz * V, s));
+  uint32_t* sb[4];
+  for (auto& b : sb) {
+    TRY(dalloc(c, n1 * 4, &q, s));
+    b = static_cast<uint32_t*>(q);
+  }
+  TRY(dalloc(c, (size_t)transpose_scratch_words(nz) * 4, &q, s));
+  T.rows = reinterpret_cast<const uint32_t*>(d_rows);
+  T.cols = d_cols;
+  T.vals = d_vals;
+  T.key_a = sb[0]; T.key_b = sb[1]; T.perm_a = sb[2]; T.perm_b = sb[3];
+  T.scratch = static_cast<uint32_t*>(q);
+  T.cols_out = *t_cols; T.vals_out = *t_vals; T.ptr_out = *t_ptr;
+  CUDA_TRY(launch_transpose(T, s));
+  std::vector<int32_t> p32((size_t)m + 1);
+  CUDA_TRY(cudaMemcpyAsync(p32.data(), *t_ptr, ((size_t)m + 1) * 4, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  release_range(c, tmp_from, c->bufs.size());
+  lpr.resize((size_t)m + 1);
+  par_ranges(m + 1, [&](int64_t lo, int64_t hi) {
+    for (int64_t r = lo; r < hi; r++) lpr[(size_t)r] = p32[(size_t)r];
+  });
+  return MSREP_OK;
+}
+
 ncclDataType_t nccl_type(msrep_dtype t) { return t == MSREP_F64 ? ncclDouble : ncclFloat; }
 
 // ---- collectives of the merge: NCCL, or the loopback group (same buffer semantics)
@@ -1179,15 +1246,17 @@ msrep_status_t comm_allgather(Ctx* c, const double* send, double* recv, size_t c
     if (count) CUDA_TRY(cudaMemcpyAsync(recv + (size_t)q * count, c->loop->src[(size_t)q], count * 8, cudaMemcpyDeviceToDevice, s));
   return loop_leave(c, s);
 }
-// buf[rank*count .. (rank+1)*count) = sum over ranks of their buf segment (fp64, in place)
-msrep_status_t comm_reduce_scatter(Ctx* c, double* buf, size_t count, cudaStream_t s) {
+// buf[rank*count .. (rank+1)*count) = sum over ranks of their buf segment (fp64 or fp32, in place)
+msrep_status_t comm_reduce_scatter(Ctx* c, void* buf, size_t count, bool f32, cudaStream_t s) {
+  const size_t E = f32 ? 4 : 8;
+  char* mine = static_cast<char*>(buf) + (size_t)c->rank * count * E;
   if (!c->loop) {
-    NCCL_TRY(ncclReduceScatter(buf, buf + (size_t)c->rank * count, count, ncclDouble, ncclSum, c->comm, s));
+    NCCL_TRY(ncclReduceScatter(buf, mine, count, f32 ? ncclFloat : ncclDouble, ncclSum, c->comm, s));
     return MSREP_OK;
   }
   TRY(loop_enter(c, buf, buf, s));
   // each rank writes only its own segment of its own buffer; peers read the other segments
-  TRY(reduce_peers(c, c->loop->src.data(), (size_t)c->rank * count, count, buf + (size_t)c->rank * count, 0, s));
+  TRY(reduce_peers(c, c->loop->src.data(), (size_t)c->rank * count, count, mine, f32 ? 2 : 0, s));
   return loop_leave(c, s);
 }
 // buf = sum over ranks (in place; fp64 or int32)
@@ -1264,8 +1333,8 @@ RowLaunch row_launch(const Ctx* c, const void* x, void* y, double alpha, double 
   RowLaunch L{};
   L.tiles = c->d_tiles; L.ntiles = c->ntiles;
   L.blob = c->d_blob;
-  L.x = x; L.y = y; L.ybase = c->wlo;
-  L.xmax = c->n > 0 ? (uint32_t)(c->n - 1) : 0u;
+  L.x = static_cast<const char*>(x) + (size_t)c->xoff * vsz(c->dtype); L.y = y; L.ybase = c->ybase;
+  L.xmax = c->xn > 0 ? (uint32_t)(c->xn - 1) : 0u;
   L.alpha = alpha; L.beta = beta; L.rec = c->d_rec;
   L.dtype = c->dtype == MSREP_F64 ? 0 : 1; L.has_sell = c->nsell > 0;
   L.xna = c->xna;
@@ -1282,7 +1351,8 @@ msrep_status_t prepare_x(Ctx* c, const void* x, int k, cudaStream_t s) {
     if (!c->d_xc_mm) TRY(dalloc(c, (size_t)c->nxc * 8 * vsz(c->dtype), &c->d_xc_mm, s));
     dst = c->d_xc_mm;
   }
-  CUDA_TRY(launch_gather_x(x, c->d_xcols, c->nxc, k, dst, c->dtype == MSREP_F64 ? 0 : 1, s));
+  CUDA_TRY(launch_gather_x(static_cast<const char*>(x) + (size_t)c->xoff * k * vsz(c->dtype), c->d_xcols, c->nxc, k, dst,
+                           c->dtype == MSREP_F64 ? 0 : 1, s));
   return MSREP_OK;
 }
 ColLaunch col_launch(const Ctx* c, const void* x, void* y, double alpha, double beta) {
@@ -1357,7 +1427,8 @@ msrep_status_t tune_xload(Ctx* c, cudaStream_t s, int64_t nz_r) {
   // row layouts with SELL tiles also try one CTA per SM for the SELL launches: (policy, occupancy).
   // 2 warm-up + 6 timed launches each; a combination other than the default (allocate, 2 CTAs)
   // must win by 3 % (a noisy pick cost the CG stencil 15 %)
-  const int combos = (!colwise(c->fmt) && c->nsell > 0) ? 4 : 2;
+  const bool bands = colwise(c->fmt) && !c->col_rows;
+  const int combos = (!bands && c->nsell > 0) ? 4 : 2;
   for (int cb = 0; cb < combos; cb++) {
     const int na = cb & 1;
     c->xna = na;
@@ -1365,7 +1436,7 @@ msrep_status_t tune_xload(Ctx* c, cudaStream_t s, int64_t nz_r) {
     float ms = 0.f;
     for (int it = 0; it < 8; it++) {
       if (it == 2) CUDA_TRY(cudaEventRecord(e0, s));
-      if (colwise(c->fmt)) CUDA_TRY(launch_cols(col_launch(c, dx, dy, 1.0, 0.0), s));
+      if (bands) CUDA_TRY(launch_cols(col_launch(c, dx, dy, 1.0, 0.0), s));
       else TRY(launch_row_tiles(c, row_launch(c, dx, dy, 1.0, 0.0), 1, s));
     }
     CUDA_TRY(cudaEventRecord(e1, s));
@@ -1520,7 +1591,7 @@ msrep_status_t msrep_set_tuning(msrep_ctx h, msrep_tuning knob, int value) {
       c->tune_cg_graph = value;
       return MSREP_OK;
     case MSREP_TUNE_COMPACT_X:
-      if (value < -1 || value > 1) return fail(MSREP_ERR_INVALID_ARG, "MSREP_TUNE_COMPACT_X %d (-1, 0, 1)", value);
+      if (value < -1 || value > 2) return fail(MSREP_ERR_INVALID_ARG, "MSREP_TUNE_COMPACT_X %d (-1, 0, 1, 2)", value);
       c->tune_compact = value;
       return MSREP_OK;
     case MSREP_TUNE_HOT_CLUSTER:
@@ -1530,6 +1601,10 @@ msrep_status_t msrep_set_tuning(msrep_ctx h, msrep_tuning knob, int value) {
     case MSREP_TUNE_SELL:
       if (value < 0 || value > 1) return fail(MSREP_ERR_INVALID_ARG, "MSREP_TUNE_SELL %d (0, 1)", value);
       c->tune_sell = value;
+      return MSREP_OK;
+    case MSREP_TUNE_COL_LAYOUT:
+      if (value < -1 || value > 1) return fail(MSREP_ERR_INVALID_ARG, "MSREP_TUNE_COL_LAYOUT %d (-1, 0, 1)", value);
+      c->tune_col_layout = value;
       return MSREP_OK;
     case MSREP_TUNE_HOT_X:
       if (value < -1 || value > HOT_BYTES / 1024)
@@ -1780,12 +1855,20 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   // ---- window and local pointer (clamped form of Alg. 2 l.11-12, reading R5)
   const size_t V = vsz(dtype);
   std::vector<int64_t> lp;
-  // unsorted COO: this rank's triplets, stably counting-sorted by column, are a column-sorted COO
-  // slice; from here on the rank builds the same band layout as MSREP_COO_COL (the partial y of
-  // its parts spans the matrix and is merged column-style)
+  // column formats: row tiles over the slice transposed on the GPU, or the host-built row bands
+  const bool col_rows = colwise(fmt) && c->tune_col_layout != 0;
+  c->col_rows = col_rows;
+  c->ybase = 0;
+  c->xoff = 0;
+  c->xn = n;
+  c->py_f32 = false;
+  // unsorted COO (row bands): this rank's triplets, stably counting-sorted by column, are a
+  // column-sorted COO slice; from here on the rank builds the same band layout as MSREP_COO_COL
+  // (the partial y of its parts spans the matrix and is merged column-style).
+  // On row tiles the triplets go to the GPU transposition as they are (triplet order within a row).
   std::vector<int32_t> us_col, us_row;
   std::unique_ptr<char[]> us_val;
-  if (fmt == MSREP_COO_UNSORTED) {
+  if (fmt == MSREP_COO_UNSORTED && !col_rows) {
     const int64_t nzr = B_hi - B_lo;
     int64_t cmin = n, cmax = -1;
     for (int64_t k = B_lo; k < B_hi; k++) { cmin = std::min<int64_t>(cmin, idx[k]); cmax = std::max<int64_t>(cmax, idx[k]); }
@@ -1811,8 +1894,19 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   }
   if (colwise(fmt)) {
     int64_t lo = -1, hi = -1;
-    if (c->fmt == MSREP_COO_UNSORTED) {   // the column window of the sorted slice
+    if (c->fmt == MSREP_COO_UNSORTED && !col_rows) {   // the column window of the sorted slice
       if (B_hi > B_lo) { lo = coo_row[B_lo]; hi = (int64_t)coo_row[B_hi - 1] + 1; }
+    } else if (c->fmt == MSREP_COO_UNSORTED) {   // the column window of the triplets
+      std::mutex mu;
+      int64_t cmin = n, cmax = -1;
+      par_ranges(B_hi - B_lo, [&](int64_t a, int64_t b) {
+        int64_t l = n, h = -1;
+        for (int64_t k = B_lo + a; k < B_lo + b; k++) { l = std::min<int64_t>(l, idx[k]); h = std::max<int64_t>(h, idx[k]); }
+        std::lock_guard<std::mutex> g(mu);
+        cmin = std::min(cmin, l);
+        cmax = std::max(cmax, h);
+      });
+      if (cmax >= 0) { lo = cmin; hi = cmax + 1; }
     } else {
       for (int j = P0; j < P1; j++) {
         if (parts[(size_t)j].start_idx > parts[(size_t)j].end_idx) continue;
@@ -1836,8 +1930,10 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     c->own_hi = parts[(size_t)P1 - 1].owned_end;
   }
   const int64_t W = c->whi - c->wlo;
-  lp.resize((size_t)W + 1);
-  if (coo_like(fmt)) {
+  if (col_rows && coo_like(fmt)) {
+    // no local pointer: the transposition reads the column of every entry
+  } else if (coo_like(fmt)) {
+    lp.resize((size_t)W + 1);
     // local pointer of a sorted major index: lp[w] = first rank-local k with coo_row >= wlo + w;
     // every row is written by the thread whose range holds the first nonzero at or after it
     const int64_t nzr = B_hi - B_lo;
@@ -1851,6 +1947,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     const int64_t last = nzr ? (int64_t)cr[nzr - 1] - c->wlo + 1 : 0;
     for (int64_t w = last; w <= W; w++) lp[(size_t)w] = nzr;
   } else {
+    lp.resize((size_t)W + 1);
     for (int64_t w = 0; w <= W; w++) {
       int64_t v = ptr[c->wlo + w];
       lp[(size_t)w] = std::min(std::max(v, B_lo), B_hi) - B_lo;
@@ -1859,7 +1956,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
 
   const int64_t nz_r = B_hi - B_lo;
   lap(1);
-  if (colwise(fmt)) {
+  if (colwise(fmt) && !col_rows) {
     // ---- pCSC: row-band layout built on the host threads, uploaded once
     CscBands CB;
     int sms = 148;
@@ -1935,15 +2032,45 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     if (c->py_len) {
       void* pp;
       TRY(dalloc(c, (size_t)c->py_len * 8, &pp, s));
-      c->d_py = static_cast<double*>(pp);
+      c->d_py = pp;
       // rows [m, py_len) are never written by the band kernel: zero them once
-      CUDA_TRY(cudaMemsetAsync(c->d_py + m, 0, (size_t)(c->py_len - m) * 8, s));
+      CUDA_TRY(cudaMemsetAsync(static_cast<double*>(c->d_py) + m, 0, (size_t)(c->py_len - m) * 8, s));
     }
     CUDA_TRY(cudaStreamSynchronize(s));   // host staging buffers are freed on return
   } else {
+    // ---- row tiles: the rank's row slice (row formats) or its column slice transposed on the GPU
+    // (column formats: one part of its own with every row of the matrix, no shared rows -- its
+    // partial y is merged column-style -- and window-local column ids into x[wlo, whi))
+    const bool tr = col_rows;
+    const int64_t rwlo = tr ? 0 : c->wlo;
+    const int64_t nx = tr ? W : n;   // x entries the tiles index
+    c->ybase = rwlo;
+    c->xoff = tr ? c->wlo : 0;
+    c->xn = nx;
+    const size_t mark = c->bufs.size();   // temporaries allocated from here are freed after packing
+    std::vector<int64_t> lpr;
+    int32_t *t_cols = nullptr, *t_ptr = nullptr;
+    void* t_vals = nullptr;
+    if (tr) {
+      TRY(transpose_slice(c, fmt, lp, idx, coo_row, val, V, s, &t_cols, &t_vals, &t_ptr, lpr));
+      lap(3);
+    }
+    const std::vector<int64_t>& LP = tr ? lpr : lp;
+    std::vector<msrep_part_desc> tpart(1);
+    tpart[0].start_idx = 0;
+    tpart[0].end_idx = nz_r - 1;
+    tpart[0].start_row = 0;
+    tpart[0].end_row = m - 1;
+    tpart[0].start_flag = 0;
+    tpart[0].owned_begin = 0;
+    tpart[0].owned_end = m;
     // ---- schedule
     Schedule S;
-    build_row_schedule(*c, lp, S, c->tune_sell != 0);
+    auto schedule = [&](bool sell) {
+      if (tr) build_row_schedule(tpart, 0, 1, 0, 0, (int)V, LP, S, sell);
+      else build_row_schedule(c->parts, c->P0, c->P1, c->B_lo, c->wlo, (int)V, LP, S, sell);
+    };
+    schedule(c->tune_sell != 0);
     {
       // A few SELL tiles among many SEG tiles cost more than they save: their presence selects
       // the SELL instantiation of rows_kernel for the whole launch, whose SEG path ran 2.5x
@@ -1951,10 +2078,10 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
       // tools/dbg_part.py).  Keep SELL tiles only if they hold >= 10 % of the rank's nonzeros.
       int64_t sell_nz = 0;
       for (const TileHost& t : S.sell)
-        sell_nz += lp[(size_t)t.row0 + (size_t)(t.packed & 0xffff)] - lp[(size_t)t.row0];
+        sell_nz += LP[(size_t)t.row0 + (size_t)(t.packed & 0xffff)] - LP[(size_t)t.row0];
       if (!S.sell.empty() && sell_nz * 10 < nz_r) {
         S = Schedule{};
-        build_row_schedule(*c, lp, S, false);
+        schedule(false);
         sell_nz = 0;
       }
       // ... and when SEG tiles hold a real share too, they get their own launch of the SEG
@@ -1990,7 +2117,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
       auto tile_end = [&](size_t t) { return t + 1 < nt ? (int64_t)blob16[t + 1] * 16 : blob_total; };
       auto zspan = [&](const TileHost& th, int64_t& z0, int64_t& z1) {
         z0 = th.nz0;
-        z1 = th.rec == -2 ? lp[(size_t)th.row0 + (size_t)(th.packed & 0xffff)] : th.nz0 + (th.packed >> 16);
+        z1 = th.rec == -2 ? LP[(size_t)th.row0 + (size_t)(th.packed & 0xffff)] : th.nz0 + (th.packed >> 16);
       };
       const int64_t cap = host_res ? c->chunk_bytes : INT64_MAX;
       size_t t = 0;
@@ -2015,20 +2142,25 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     }
     int64_t span = 0;
     for (auto& g : groups) span = std::max(span, g.z1 - g.z0);
-    if (!host_res) span = nz_r;
+    if (!host_res || tr) span = nz_r;   // (transposed: the whole slice is on the device already)
 
     // ---- upload the slice (the only H2D of A) and build the tile blobs on the GPU
-    const size_t mark = c->bufs.size();   // temporaries allocated from here are freed after packing
     void* vp;
-    TRY(dalloc(c, (size_t)span * V, &vp, s));
     int32_t *d_idx, *d_aux = nullptr, *d_crow = nullptr;
-    {
+    int32_t* d_lp = nullptr;   // window-local pointer for SELL packing
+    if (tr) {
+      vp = t_vals;
+      d_idx = t_cols;
+      d_aux = d_lp = t_ptr;
+    } else {
+      TRY(dalloc(c, (size_t)span * V, &vp, s));
       void* ip;
       TRY(dalloc(c, (size_t)span * 4, &ip, s));
       d_idx = static_cast<int32_t*>(ip);
     }
-    int32_t* d_lp = nullptr;   // window-local pointer for SELL packing
-    if (fmt == MSREP_COO) {
+    if (tr) {
+      // the row pointer of the transposed slice is on the device (t_ptr)
+    } else if (fmt == MSREP_COO) {
       void* ap;
       TRY(dalloc(c, (size_t)span * 4, &ap, s));
       d_crow = static_cast<int32_t*>(ap);
@@ -2062,27 +2194,28 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     c->nhot = 0;
     c->hot_nnz = 0;
     c->nxc = 0;
-    const bool want_hot = !host_res && c->tune_hot != 0 && nz_r > 0 && n > 0 && (c->nsell == 0 || c->split_launch);
-    const bool want_cx = !host_res && nz_r > 0 && n > 0 &&
-                         (c->tune_compact == 1 || (c->tune_compact == -1 && (int64_t)n * (int64_t)V >= COMPACT_X_MIN_BYTES));
+    const bool want_hot = !host_res && c->tune_hot != 0 && nz_r > 0 && nx > 0 && (c->nsell == 0 || c->split_launch);
+    const bool want_cx = !host_res && nz_r > 0 && nx > 0 &&
+                         (c->tune_compact == 1 || (c->tune_compact == -1 && (int64_t)nx * (int64_t)V >= COMPACT_X_MIN_BYTES));
+    if (tr) idx_up = true;
     if (want_hot || want_cx) {
       int sms = 148;
       CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
-      TRY(h2d(c, d_idx, idx + B_lo, (size_t)nz_r * 4, s));
+      if (!idx_up) TRY(h2d(c, d_idx, idx + B_lo, (size_t)nz_r * 4, s));
       idx_up = true;
       void* dp;
-      TRY(dalloc(c, (size_t)n * 4, &dp, s));
+      TRY(dalloc(c, (size_t)nx * 4, &dp, s));
       int32_t* d_deg = static_cast<int32_t*>(dp);
-      CUDA_TRY(cudaMemsetAsync(d_deg, 0, (size_t)n * 4, s));
+      CUDA_TRY(cudaMemsetAsync(d_deg, 0, (size_t)nx * 4, s));
       CUDA_TRY(launch_col_degree(d_idx, nz_r, d_deg, s));
-      std::vector<int32_t> deg((size_t)n);
-      CUDA_TRY(cudaMemcpyAsync(deg.data(), d_deg, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
+      std::vector<int32_t> deg((size_t)nx);
+      CUDA_TRY(cudaMemcpyAsync(deg.data(), d_deg, (size_t)nx * 4, cudaMemcpyDeviceToHost, s));
       CUDA_TRY(cudaStreamSynchronize(s));
       // a hot slot costs one gather per CTA per launch: worth it from 4 gathers per SM on
       const int32_t min_deg = 4 * sms;
       std::mutex mu;
       std::vector<std::pair<int64_t, std::vector<int32_t>>> used;
-      par_ranges(n, [&](int64_t lo, int64_t hi) {
+      par_ranges(nx, [&](int64_t lo, int64_t hi) {
         std::vector<int32_t> v, u;
         for (int64_t q = lo; q < hi; q++) {
           if (want_hot && deg[(size_t)q] >= min_deg) v.push_back((int32_t)q);
@@ -2097,10 +2230,12 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
         for (auto& u : used) xcols.insert(xcols.end(), u.second.begin(), u.second.end());
         // auto: only when the rank touches <= 3/4 of x (R-MAT scale 24: 44 %); a power-law matrix
         // that touches every column gains nothing from the extra gather
-        if (c->tune_compact == 1 || (int64_t)xcols.size() * 4 <= (int64_t)n * 3) {
-          TRY(dalloc(c, (size_t)n * 4, &dp, s));
+        if (c->tune_compact >= 1 || (int64_t)xcols.size() * 4 <= (int64_t)nx * 3) {
+          TRY(dalloc(c, (size_t)nx * 4, &dp, s));
           d_colmap = static_cast<int32_t*>(dp);   // column -> compact id (filled from the kept list below)
           c->nxc = (int64_t)xcols.size();
+          if (c->tune_compact == 2)   // degree order: the most-gathered columns share the first lines of x'
+            std::stable_sort(xcols.begin(), xcols.end(), [&](int32_t a, int32_t b) { return deg[(size_t)a] > deg[(size_t)b]; });
         } else {
           xcols.clear();
         }
@@ -2125,9 +2260,9 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
         const bool on = c->tune_hot >= 1 ? !hot.empty()
                                          : (V == 8 && cap_nz * 20 >= nz_r && nz_r >= ((int64_t)1 << 20));
         if (on) {
-          TRY(dalloc(c, (size_t)n * 4, &dp, s));
+          TRY(dalloc(c, (size_t)nx * 4, &dp, s));
           d_hotslot = static_cast<int32_t*>(dp);
-          CUDA_TRY(cudaMemsetAsync(d_hotslot, 0xff, (size_t)n * 4, s));   // -1: cold
+          CUDA_TRY(cudaMemsetAsync(d_hotslot, 0xff, (size_t)nx * 4, s));   // -1: cold
           c->nhot = (int)hot.size();
           c->hot_nnz = cap_nz;
           c->hot_cluster = c->tune_hot_cluster;
@@ -2149,8 +2284,11 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     }
     if (c->nhot) {
       CUDA_TRY(launch_hot_slots(dp_hot_tmp, c->nhot, d_hotslot, s));
-      if (c->nxc)   // the kernels read x': hot slots are filled from compact ids
+      if (c->nxc && c->tune_compact == 2) {   // degree-ordered x': the hot columns are its first entries
+        for (size_t q = 0; q < hot.size(); q++) hot[q] = (int32_t)q;
+      } else if (c->nxc) {   // the kernels read x': hot slots are filled from compact ids
         for (auto& q : hot) q = (int32_t)(std::lower_bound(xcols.begin(), xcols.end(), q) - xcols.begin());
+      }
       TRY(upload_vec(c, hot, &c->d_hot, s));
     } else {
       c->d_hot = nullptr;
@@ -2170,16 +2308,18 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     for (size_t gi = 0; gi < groups.size(); gi++) {
       const Group& g = groups[gi];
       const int64_t zn = g.z1 - g.z0;
-      if (zn > 0) {
+      if (zn > 0 && !tr) {
         TRY(h2d(c, vp, static_cast<const char*>(val) + (size_t)(B_lo + g.z0) * V, (size_t)zn * V, s));
         if (!idx_up) TRY(h2d(c, d_idx, idx + B_lo + g.z0, (size_t)zn * 4, s));
         if (d_crow) TRY(h2d(c, d_crow, coo_row + B_lo + g.z0, (size_t)zn * 4, s));
       }
       const int64_t off0 = (int64_t)blob16[(size_t)g.t0] * 16;
       // pointers shifted by the group's first nonzero / layout offset: tiles index them unchanged
+      // (the transposed slice is whole on the device)
+      const int64_t zb = tr ? 0 : g.z0;
       PackLaunch PL{d_tiles_orig + g.t0, d_blob16 + g.t0, g.t1 - g.t0,
-                    static_cast<const char*>(vp) - (size_t)g.z0 * V, d_idx - g.z0,
-                    d_crow ? d_crow - g.z0 : d_aux, fmt == MSREP_COO, (int)V, c->wlo,
+                    static_cast<const char*>(vp) - (size_t)zb * V, d_idx - zb,
+                    d_crow ? d_crow - zb : d_aux, fmt == MSREP_COO, (int)V, rwlo,
                     host_res ? d_pack - off0 : d_pack, d_lp, d_hotslot, d_colmap};
       CUDA_TRY(launch_pack(PL, s));
       if (host_res)
@@ -2216,7 +2356,19 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
         c->d_fence = static_cast<int*>(hp);
       }
       c->nheads_local = 0;
-      for (int j = P0; j < P1; j++) c->nheads_local += parts[(size_t)j].start_flag ? 1 : 0;
+      if (!tr)
+        for (int j = P0; j < P1; j++) c->nheads_local += parts[(size_t)j].start_flag ? 1 : 0;
+    }
+    if (tr) {   // the rank's partial y for the reduce-scatter (nranks > 1), in the partition's dtype
+      c->py_len = c->nranks > 1 ? c->shard * c->nranks : 0;
+      c->py_f32 = V == 4;
+      if (c->py_len) {
+        void* pp;
+        TRY(dalloc(c, (size_t)c->py_len * V, &pp, s));
+        c->d_py = pp;
+        // rows [m, py_len) are never written by the tiles (they cover rows [0, m)): zero them once
+        CUDA_TRY(cudaMemsetAsync(static_cast<char*>(pp) + (size_t)m * V, 0, (size_t)(c->py_len - m) * V, s));
+      }
     }
   }
   CUDA_TRY(cudaStreamSynchronize(s));
@@ -2231,7 +2383,8 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   st.nparts = c->np; st.nranks = c->nranks; st.parts_per_rank = c->vparts;
   st.nnz_rank = nz_r;
   st.rows_window = W;
-  st.ntiles = colwise(fmt) ? c->citems : c->ntiles; st.nsell = c->nsell; st.nslabs = c->nslabs; st.nsplit_rows = c->nsplit; st.nheads_local = c->nheads_local;
+  const bool bands = colwise(fmt) && !c->col_rows;
+  st.ntiles = bands ? c->citems : c->ntiles; st.nsell = c->nsell; st.nslabs = c->nslabs; st.nsplit_rows = c->nsplit; st.nheads_local = c->nheads_local;
   st.partition_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
   for (int k = 0; k < 4; k++) st.phase_ms[k] = phase[k];
   st.residency = c->residency;
@@ -2244,6 +2397,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   st.gpu_numa_node = c->numa_node;
   st.host_numa_node = c->h_blob ? page_numa_node(c->h_blob) : -1;
   st.hot_nnz = c->hot_nnz;
+  st.col_layout = colwise(fmt) ? (c->col_rows ? 1 : 0) : -1;
   int64_t X = 0;
   if (colwise(fmt)) {
     X = W;   // pCSC reads x only over its column window
@@ -2282,8 +2436,11 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   st.alg_bytes = base + ybytes_b1;
   st.alg_bytes_beta0 = base + ybytes_b0;
   const int64_t nmain = c->chunks.empty() ? 1 : (int64_t)c->chunks.size();   // main-kernel launches
-  if (colwise(fmt))
+  if (bands)
     st.kernels_per_spmv = (c->cunits ? nmain : 0) + (c->nranks > 1 ? 1 /*shard epilogue*/ : 0);
+  else if (colwise(fmt))
+    st.kernels_per_spmv = (c->ntiles ? nmain + (c->split_launch && c->chunks.empty() ? 1 : 0) : 0) + (c->nsplit ? 1 : 0) +
+                          (c->nxc ? 1 : 0) + (c->nranks > 1 ? 1 /*shard epilogue*/ : 0);
   else st.kernels_per_spmv = (c->ntiles ? nmain + (c->split_launch && c->chunks.empty() ? 1 : 0) : 0) + (c->nranks > 1 && c->any_flag ? 1 : 0) + (c->nsplit ? 1 : 0) + (c->nxc ? 1 : 0);
   int64_t db = 0;
   for (auto& b : c->bufs) db += (int64_t)b.bytes;
@@ -2350,6 +2507,34 @@ msrep_status_t msrep_spmv_mirror(msrep_ctx h, const void* alpha_p, const void* x
   return MSREP_OK;
 }
 
+// The row-tile walk of one SpMV (k = 1) or SpMM (k > 1): device-resident, or streamed in chunks
+// from the pinned host copy (MSREP_RESIDENT_HOST)
+msrep_status_t row_tiles_pass(Ctx* c, const RowLaunch& L, int k, cudaStream_t s) {
+  if (c->residency != MSREP_RESIDENT_HOST) return launch_row_tiles(c, L, k, s);
+  return stream_chunks(c, s, [&](const Ctx::Chunk& ch, const char* base) -> msrep_status_t {
+    RowLaunch Lc = L;
+    Lc.tiles = c->d_tiles + ch.t0; Lc.ntiles = ch.t1 - ch.t0;
+    Lc.blob = base; Lc.has_sell = ch.has_sell;
+    CUDA_TRY(k == 1 ? launch_rows(Lc, s) : launch_rows_mm(Lc, k, s));
+    return MSREP_OK;
+  });
+}
+
+// the beta-deferred fix-up of the rank's split rows (records + head partials, reading R6/R10)
+msrep_status_t fixup_pass(Ctx* c, void* y, double alpha, double beta, int k, int nmirror, void* const* mirrors,
+                          double* rec, double* head_all, cudaStream_t s) {
+  FixupLaunch F{};
+  F.nsplit = c->nsplit;
+  F.sr_row = c->d_sr_row; F.sr_rec = c->d_sr_rec; F.sr_head = c->d_sr_head; F.head_list = c->d_head_list;
+  F.part_rec = c->d_part_rec; F.part_lo = c->P0; F.part_hi = c->P1;
+  F.head_all = head_all; F.rec = rec;
+  F.y = y; F.alpha = alpha; F.beta = beta; F.dtype = c->dtype == MSREP_F64 ? 0 : 1; F.k = k;
+  F.nmirror = nmirror;
+  for (int mi = 0; mi < nmirror; mi++) F.mirror[mi] = mirrors[mi];
+  CUDA_TRY(launch_fixup(F, s));
+  return MSREP_OK;
+}
+
 // Column formats (pCSC, column-sorted / unsorted pCOO): vector j of a k-wide row-major block (k = 1:
 // SpMV) -- the band kernel with strides k, then for nranks > 1 the reduce-scatter of the fp64
 // partial y and the alpha/beta epilogue on this rank's shard [my_lo, my_hi) (Sec. 4.3)
@@ -2357,6 +2542,29 @@ msrep_status_t col_spmv(Ctx* c, double alpha, const void* x, double beta, void* 
                         int64_t my_hi, cudaStream_t s) {
   const size_t V = vsz(c->dtype);
   const int dt = c->dtype == MSREP_F64 ? 0 : 1;
+  if (c->col_rows) {
+    // row tiles over the transposed slice (k == 1 here: SpMM passes planar vectors): one rank
+    // writes y = alpha*A_p x + beta*y directly; several write their partial y_p (every row, in
+    // the partition's dtype) for the reduce-scatter and the alpha/beta epilogue on the shard
+    if (k != 1 || j != 0) return fail(MSREP_ERR_STATE, "column format on row tiles: strided vectors");
+    const bool one = c->nranks == 1;
+    void* out = one ? y : c->d_py;
+    const double a = one ? alpha : 1.0, b = one ? beta : 0.0;
+    TRY(prepare_x(c, x, 1, s));
+    RowLaunch L = row_launch(c, x, out, a, b);
+    cudaEvent_t pe;
+    TRY(prof_begin(c, s, &pe));
+    TRY(row_tiles_pass(c, L, 1, s));
+    if (pe) CUDA_TRY(cudaEventRecord(pe, s));
+    if (c->nsplit) TRY(fixup_pass(c, out, a, b, 1, 0, nullptr, c->d_rec, c->d_head_all, s));
+    if (!one) {
+      const char* shard = static_cast<const char*>(c->d_py) + (size_t)c->rank * c->shard * V;
+      TRY(comm_reduce_scatter(c, c->d_py, (size_t)c->shard, c->py_f32, s));
+      CUDA_TRY(launch_axpby_py(shard, c->py_f32 ? 1 : 0, static_cast<char*>(y) + (size_t)my_lo * V, my_hi - my_lo, alpha,
+                               beta, dt, s, 1));
+    }
+    return MSREP_OK;
+  }
   ColLaunch L = col_launch(c, static_cast<const char*>(x) + (size_t)j * V, static_cast<char*>(y) + (size_t)j * V,
                            alpha, beta);
   L.xs = k;
@@ -2377,9 +2585,9 @@ msrep_status_t col_spmv(Ctx* c, double alpha, const void* x, double beta, void* 
   }
   if (pe) CUDA_TRY(cudaEventRecord(pe, s));
   if (c->nranks > 1) {
-    double* shard = c->d_py + (size_t)c->rank * c->shard;
-    TRY(comm_reduce_scatter(c, c->d_py, (size_t)c->shard, s));
-    CUDA_TRY(launch_axpby_py(shard, static_cast<char*>(y) + ((size_t)my_lo * k + j) * V, my_hi - my_lo, alpha, beta,
+    const double* shard = static_cast<const double*>(c->d_py) + (size_t)c->rank * c->shard;
+    TRY(comm_reduce_scatter(c, c->d_py, (size_t)c->shard, false, s));
+    CUDA_TRY(launch_axpby_py(shard, 0, static_cast<char*>(y) + ((size_t)my_lo * k + j) * V, my_hi - my_lo, alpha, beta,
                              dt, s, k));
   }
   return MSREP_OK;
@@ -2435,17 +2643,7 @@ msrep_status_t spmv_impl(msrep_ctx h, const void* alpha_p, const void* x, const 
   for (int mi = 0; mi < nmirror; mi++) L.mirror[mi] = mirrors[mi];
   cudaEvent_t pe;
   TRY(prof_begin(c, s, &pe));
-  if (c->residency == MSREP_RESIDENT_HOST) {
-    TRY(stream_chunks(c, s, [&](const Ctx::Chunk& ch, const char* base) -> msrep_status_t {
-      RowLaunch Lc = L;
-      Lc.tiles = c->d_tiles + ch.t0; Lc.ntiles = ch.t1 - ch.t0;
-      Lc.blob = base; Lc.has_sell = ch.has_sell;
-      CUDA_TRY(launch_rows(Lc, s));
-      return MSREP_OK;
-    }));
-  } else {
-    TRY(launch_row_tiles(c, L, 1, s));
-  }
+  TRY(row_tiles_pass(c, L, 1, s));
   if (pe) CUDA_TRY(cudaEventRecord(pe, s));
   if (c->nranks > 1 && c->any_flag) {
     nv.next("spmv: head exchange");
@@ -2455,15 +2653,7 @@ msrep_status_t spmv_impl(msrep_ctx h, const void* alpha_p, const void* x, const 
   }
   if (c->nsplit) {
     nv.next("spmv: fix-up");
-    FixupLaunch F{};
-    F.nsplit = c->nsplit;
-    F.sr_row = c->d_sr_row; F.sr_rec = c->d_sr_rec; F.sr_head = c->d_sr_head; F.head_list = c->d_head_list;
-    F.part_rec = c->d_part_rec; F.part_lo = c->P0; F.part_hi = c->P1;
-    F.head_all = c->d_head_all; F.rec = c->d_rec;
-    F.y = y; F.alpha = alpha; F.beta = beta; F.dtype = dt; F.k = 1;
-    F.nmirror = nmirror;
-    for (int mi = 0; mi < nmirror; mi++) F.mirror[mi] = mirrors[mi];
-    CUDA_TRY(launch_fixup(F, s));
+    TRY(fixup_pass(c, y, alpha, beta, 1, nmirror, mirrors, c->d_rec, c->d_head_all, s));
   }
   if (gather) {
     nv.next("spmv: allgatherv");
@@ -2495,7 +2685,7 @@ msrep_status_t msrep_spmm(msrep_ctx h, const void* alpha_p, const void* X, const
     if (gather) TRY(allgatherv_y(c, Y, seg_lo, seg_hi, s, k));
     return MSREP_OK;
   }
-  if (colwise(c->fmt)) {
+  if (colwise(c->fmt) && !(c->col_rows && c->nranks == 1)) {
     // column formats: X and Y go planar (k contiguous vectors), one SpMV pass of the band kernel
     // (and its merge) per vector, and Y back to row-major -- strided gathers / stores of the row-major
     // block directly were slower than k SpMVs (stencil k = 8: 0.64x)
@@ -2523,11 +2713,12 @@ msrep_status_t msrep_spmm(msrep_ctx h, const void* alpha_p, const void* X, const
     if (c->nranks > 1) { TRY(dalloc(c, (size_t)c->np * 8 * 8, &q, s)); c->d_head_all_mm = static_cast<double*>(q); }
     c->mm_k = 8;
   }
+  // row formats, and column formats on row tiles at one rank (y written directly, no merge)
   RowLaunch L{};
   L.tiles = c->d_tiles; L.ntiles = c->ntiles;
   L.blob = c->d_blob;
-  L.x = X; L.y = Y; L.ybase = c->wlo;
-  L.xmax = c->n > 0 ? (uint32_t)(c->n - 1) : 0u;
+  L.x = static_cast<const char*>(X) + (size_t)c->xoff * k * V; L.y = Y; L.ybase = c->ybase;
+  L.xmax = c->xn > 0 ? (uint32_t)(c->xn - 1) : 0u;
   L.alpha = alpha; L.beta = beta; L.rec = c->d_rec_mm;
   L.dtype = dt; L.has_sell = c->nsell > 0;
   L.hot = c->d_hot; L.nhot = c->nhot;   // SpMM untags hot column ids through the list (no shared-memory cache)
@@ -2535,32 +2726,14 @@ msrep_status_t msrep_spmm(msrep_ctx h, const void* alpha_p, const void* X, const
   if (c->nxc) { L.x = c->d_xc_mm; L.xmax = (uint32_t)(c->nxc - 1); }
   cudaEvent_t pe;
   TRY(prof_begin(c, s, &pe));
-  if (c->residency == MSREP_RESIDENT_HOST) {
-    TRY(stream_chunks(c, s, [&](const Ctx::Chunk& ch, const char* base) -> msrep_status_t {
-      RowLaunch Lc = L;
-      Lc.tiles = c->d_tiles + ch.t0; Lc.ntiles = ch.t1 - ch.t0;
-      Lc.blob = base; Lc.has_sell = ch.has_sell;
-      CUDA_TRY(launch_rows_mm(Lc, k, s));
-      return MSREP_OK;
-    }));
-  } else {
-    TRY(launch_row_tiles(c, L, k, s));
-  }
+  TRY(row_tiles_pass(c, L, k, s));
   if (pe) CUDA_TRY(cudaEventRecord(pe, s));
   if (c->nranks > 1 && c->any_flag) {
     HeadLaunch H{c->vparts, c->d_part_rec, c->d_rec_mm, c->d_head_local_mm, k};
     CUDA_TRY(launch_heads(H, s));
     TRY(comm_allgather(c, c->d_head_local_mm, c->d_head_all_mm, (size_t)c->vparts * k, s));
   }
-  if (c->nsplit) {
-    FixupLaunch F{};
-    F.nsplit = c->nsplit;
-    F.sr_row = c->d_sr_row; F.sr_rec = c->d_sr_rec; F.sr_head = c->d_sr_head; F.head_list = c->d_head_list;
-    F.part_rec = c->d_part_rec; F.part_lo = c->P0; F.part_hi = c->P1;
-    F.head_all = c->d_head_all_mm; F.rec = c->d_rec_mm;
-    F.y = Y; F.alpha = alpha; F.beta = beta; F.dtype = dt; F.k = k;
-    CUDA_TRY(launch_fixup(F, s));
-  }
+  if (c->nsplit) TRY(fixup_pass(c, Y, alpha, beta, k, 0, nullptr, c->d_rec_mm, c->d_head_all_mm, s));
   if (gather) TRY(allgatherv_y(c, Y, seg_lo, seg_hi, s, k));
   return MSREP_OK;
 }

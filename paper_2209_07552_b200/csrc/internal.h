@@ -226,7 +226,7 @@ struct SumLaunch {
   int n; const void* src[MAX_LOOP_RANKS];
   int64_t off, count;
   void* dst;
-  int is_int;   // int32 (the mirror fence) or fp64
+  int is_int;   // 1: int32 (the mirror fence), 2: fp32, 0: fp64
 };
 
 // kernels.cu entry points (all enqueue on `s`)
@@ -236,8 +236,9 @@ cudaError_t launch_cols(const ColLaunch& L, cudaStream_t s);
 cudaError_t launch_fixup(const FixupLaunch& L, cudaStream_t s);
 cudaError_t launch_heads(const HeadLaunch& L, cudaStream_t s);
 cudaError_t launch_scale(void* y, int64_t count, double beta, int dtype, cudaStream_t s);   // y = beta*y
-cudaError_t launch_axpby_py(const double* py, void* y, int64_t count, double alpha, double beta, int dtype,
-                            cudaStream_t s, int ystride = 1);                               // y = alpha*py + beta*y
+// y = alpha*py + beta*y (py fp64, or fp32 when py_f32)
+cudaError_t launch_axpby_py(const void* py, int py_f32, void* y, int64_t count, double alpha, double beta, int dtype,
+                            cudaStream_t s, int ystride = 1);
 cudaError_t launch_rebase(const int64_t* gptr, int32_t* lptr, int64_t count, int64_t lo, int64_t hi,
                           cudaStream_t s);                                                  // clamp(gptr,lo,hi)-lo
 cudaError_t launch_pack(const PackLaunch& L, cudaStream_t s);
@@ -249,6 +250,26 @@ cudaError_t launch_col_degree(const int32_t* idx, int64_t nz, int32_t* deg, cuda
 cudaError_t launch_hot_slots(const int32_t* hot, int nhot, int32_t* slot, cudaStream_t s);      // slot[hot[k]] = k
 // out[i*k + j] = x[cols[i]*k + j], i < n, j < k (compact x for SpMV k = 1, SpMM k > 1)
 cudaError_t launch_gather_x(const void* x, const int32_t* cols, int64_t n, int k, void* out, int dtype, cudaStream_t s);
+// transpose.cu: a column-format slice of n entries -> the rank-local row-major slice (stable by
+// slice position within a row).  rows = row of each entry (input, also the first pass's keys);
+// key_a/key_b/perm_a/perm_b: [n] each; scratch: transpose_scratch_words(n) words;
+// outputs cols_out / vals_out [n] in row order and ptr_out [m + 1] (int32 row pointer).
+struct TransposeLaunch {
+  int64_t n, m;
+  int V;
+  const uint32_t* rows;
+  const int32_t* cols;
+  const void* vals;
+  uint32_t *key_a, *key_b, *perm_a, *perm_b, *scratch;
+  int32_t* cols_out;
+  void* vals_out;
+  int32_t* ptr_out;
+};
+int64_t transpose_scratch_words(int64_t n);
+cudaError_t launch_transpose(const TransposeLaunch& T, cudaStream_t s);
+cudaError_t launch_expand_cols(const int64_t* lp, int64_t W, int32_t* col, cudaStream_t s);   // col[lp[w]..lp[w+1]) = w
+cudaError_t launch_rebase_cols(const int32_t* v, int64_t n, int32_t base, int32_t* c, cudaStream_t s);   // c = v - base
+
 // CG vector kernels on an owned segment of n entries (kernels.cu).  sc = device scalars
 // {rs (parity 0), rs (parity 1), -, bnorm2}; part_in / part_out = CG_PARTS per-block partial
 // sums (every consumer block re-sums part_in in the same fixed order).

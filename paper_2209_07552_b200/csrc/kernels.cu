@@ -1257,10 +1257,14 @@ __global__ void gather_x_kernel(const VT* __restrict__ x, const int32_t* __restr
 // loopback reduce (in-process multi-rank test transport): fixed rank order
 __global__ void sum_peers_kernel(const SumLaunch L) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < L.count; i += (int64_t)gridDim.x * blockDim.x) {
-    if (L.is_int) {
+    if (L.is_int == 1) {
       int a = 0;
       for (int q = 0; q < L.n; q++) a += static_cast<const int*>(L.src[q])[L.off + i];
       static_cast<int*>(L.dst)[i] = a;
+    } else if (L.is_int == 2) {   // fp32 partials (column formats on row tiles), summed in rank order
+      float a = 0.f;
+      for (int q = 0; q < L.n; q++) a += static_cast<const float*>(L.src[q])[L.off + i];
+      static_cast<float*>(L.dst)[i] = a;
     } else {
       double a = 0.0;
       for (int q = 0; q < L.n; q++) a += static_cast<const double*>(L.src[q])[L.off + i];
@@ -1335,11 +1339,11 @@ __global__ void scale_kernel(VT* y, int64_t n, double beta) {
     y[i] = (VT)(beta != 0.0 ? beta * (double)y[i] : 0.0);
 }
 
-template <typename VT>
-__global__ void axpby_kernel(const double* __restrict__ py, VT* __restrict__ y, int64_t n, double alpha, double beta,
+template <typename VT, typename PT>
+__global__ void axpby_kernel(const PT* __restrict__ py, VT* __restrict__ y, int64_t n, double alpha, double beta,
                              int ys) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    double v = alpha * py[i];
+    double v = alpha * (double)py[i];
     if (beta != 0.0) v += beta * (double)y[i * ys];
     y[i * ys] = (VT)v;
   }
@@ -1631,11 +1635,13 @@ cudaError_t launch_scale(void* y, int64_t n, double beta, int dtype, cudaStream_
   return cudaGetLastError();
 }
 
-cudaError_t launch_axpby_py(const double* py, void* y, int64_t n, double alpha, double beta, int dtype,
+cudaError_t launch_axpby_py(const void* py, int py_f32, void* y, int64_t n, double alpha, double beta, int dtype,
                             cudaStream_t s, int ys) {
   if (n <= 0) return cudaSuccess;
-  if (dtype == 0) axpby_kernel<double><<<elementwise_grid(n), 256, 0, s>>>(py, (double*)y, n, alpha, beta, ys);
-  else axpby_kernel<float><<<elementwise_grid(n), 256, 0, s>>>(py, (float*)y, n, alpha, beta, ys);
+  const int g = elementwise_grid(n);
+  if (py_f32) axpby_kernel<float, float><<<g, 256, 0, s>>>((const float*)py, (float*)y, n, alpha, beta, ys);
+  else if (dtype == 0) axpby_kernel<double, double><<<g, 256, 0, s>>>((const double*)py, (double*)y, n, alpha, beta, ys);
+  else axpby_kernel<float, double><<<g, 256, 0, s>>>((const double*)py, (float*)y, n, alpha, beta, ys);
   return cudaGetLastError();
 }
 

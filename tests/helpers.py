@@ -52,6 +52,26 @@ def assert_close(got, ref, bound, dtype):
                            f"got {got[bad][:5]} ref {ref[bad][:5]} bound {bound[bad][:5]}")
 
 
+# A column format may carry a device-layout suffix: "csc:bands" / "coo_col:bands" /
+# "coo_unsorted:bands" select the host-built row bands (csc_band_kernel), "...:tiles" the row tiles
+# over the GPU-transposed slice (the default for the column formats).
+LAYOUT_SUFFIX = {"bands": 0, "tiles": 1}
+
+
+def split_fmt(fmt):
+    """'csc:bands' -> ('csc', {'col_layout': 0}); 'csr' -> ('csr', {})."""
+    base, _, lay = fmt.partition(":")
+    return base, ({"col_layout": LAYOUT_SUFFIX[lay]} if lay else {})
+
+
+def apply_layout(ctx, fmt):
+    """set the context's tuning for fmt's layout suffix; return the base format"""
+    base, tun = split_fmt(fmt)
+    for k, v in tun.items():
+        ctx.set_tuning(k, v)
+    return base
+
+
 def run_gpu(A, fmt, x, y, alpha, beta, parts=1, layout=None, host_path=False, ctx=None, repeat=1, **pkw):
     """Partition A (gen.Sparse CSR or CSC) as `fmt` on cuda:0 with `parts` virtual parts; return y."""
     import torch
@@ -60,6 +80,7 @@ def run_gpu(A, fmt, x, y, alpha, beta, parts=1, layout=None, host_path=False, ct
     own = ctx is None
     if own:
         ctx = M.Context(0, 1, None, 0, parts)
+    fmt = apply_layout(ctx, fmt)
     if fmt == "csr":
         assert A["fmt"] == "csr"
         ctx.partition("csr", A["m"], A["n"], ptr=A["ptr"], idx=A["idx"], val=A["val"], **pkw)

@@ -1,6 +1,7 @@
 """Small invocations of every kernel of libmsrep, for compute-sanitizer (tests/test_gpu_sanitizer.py):
 rows_kernel (SELL, SEG, slab tiles; hot-x cache; compact x; mirror stores), rows_mm_kernel (SpMM),
-csc_band_kernel (whole bands and split bands with the slot reduction), fixup / heads, pack, rebase,
+csc_band_kernel (whole bands and split bands with the slot reduction), the GPU transposition of the
+column formats (radix sort, row pointer, permute), fixup / heads, pack, rebase,
 the hot-x / compact-x setup kernels, the CG vector kernels.  Checks results against the oracle too,
 so a sanitizer run that changes nothing also proves the path ran."""
 import os
@@ -27,9 +28,11 @@ def main():
         T = gen.transpose(B)
         x = gen.vector(n, 1, kind=gen.SMALLINT); y = gen.vector(m, 2, kind=gen.SMALLINT)
         ref = oracle.spmv_csr(m, B["ptr"], B["idx"], B["val"], x, y, 1.5, 0.5)
-        for fmt in ("csr", "coo", "csc", "coo_col"):
+        for fmt_tag in ("csr", "coo", "csc", "coo_col", "csc:bands", "coo_col:bands"):
+            fmt, _, lay = fmt_tag.partition(":")
             for hot, cx in ((0, 0), (1, 1)):
                 ctx = M.Context(0, 1, None, 0, 3)
+                ctx.set_tuning("col_layout", 0 if lay == "bands" else -1)
                 ctx.set_tuning("hot_x", hot)
                 ctx.set_tuning("compact_x", cx)
                 ctx.set_tuning("xload", 0)
@@ -42,7 +45,7 @@ def main():
                 ctx.spmv(1.5, torch.as_tensor(x).cuda(), 0.5, yd)
                 torch.cuda.synchronize()
                 if not np.array_equal(yd.cpu().numpy(), ref):
-                    print("FAIL", name, fmt, hot, cx, flush=True)
+                    print("FAIL", name, fmt_tag, hot, cx, flush=True)
                     fails += 1
                 if fmt == "csr":
                     k = 4

@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 import gen
-from tests.helpers import assert_close, coo_of_csr, oracle_ref, row_bound, run_gpu, to_dtype
+from tests.helpers import apply_layout, assert_close, coo_of_csr, oracle_ref, row_bound, run_gpu, to_dtype
 from tests.test_gpu_parity import FMTS, as_fmt
 
 pytestmark = pytest.mark.gpu
@@ -17,6 +17,7 @@ CHUNKS = [1, 64 << 10, 0]   # 1 byte: one tile (or band) per chunk; 64 KiB: many
 
 def _ctx_partition(M, B, fmt, parts, **kw):
     ctx = M.Context(0, 1, None, 0, parts)
+    fmt = apply_layout(ctx, fmt)
     if fmt in ("coo", "coo_col"):
         ctx.partition(fmt, B["m"], B["n"], idx=B["idx"], val=B["val"], coo_row=coo_of_csr(B), **kw)
     else:
@@ -76,13 +77,15 @@ def test_host_resident_many_chunks_counted(fmt):
     ctx.close()
 
 
-def test_host_resident_csc_split_items():
-    """pCSC with fewer row bands than SMs (split-item units) streamed band range by band range."""
+@pytest.mark.parametrize("fmt", ["csc:bands", "csc"])
+def test_host_resident_csc_split_items(fmt):
+    """pCSC with fewer row bands than SMs (split-item units) streamed band range by band range; the
+    same matrix on row tiles streamed tile range by tile range."""
     A = gen.kdistinct_csr(3 * 8192 - 5, 300_000, 40, seed=97, kind=gen.SMALLINT)
     x = gen.vector(A["n"], 98, kind=gen.SMALLINT); y = gen.vector(A["m"], 99, kind=gen.SMALLINT)
     for chunk in (1, 1 << 20, 0):
         for parts in (1, 2):
-            got = run_gpu(as_fmt(A, "csc"), "csc", x, y, 1.5, 0.5, parts=parts, residency="host", chunk_bytes=chunk)
+            got = run_gpu(as_fmt(A, fmt), fmt, x, y, 1.5, 0.5, parts=parts, residency="host", chunk_bytes=chunk)
             assert np.array_equal(got, oracle_ref(A, x, y, 1.5, 0.5)), (chunk, parts)
 
 
@@ -126,7 +129,7 @@ def test_host_resident_spmm_and_cg(fmt):
     assert res[0][0] == res[1][0] and np.array_equal(res[0][2], res[1][2])
 
 
-@pytest.mark.parametrize("fmt", ["csr", "csc"])
+@pytest.mark.parametrize("fmt", ["csr", "csc", "csc:bands"])
 def test_host_resident_config2_full_size(fmt):
     """The full N=127 stencil (config 2) streamed from host memory in 64 MiB chunks: closed form
     (interior 0, faces 9, edges 15, corners 19) and bit-exact integer parity."""

@@ -20,18 +20,19 @@ def _ctx(hot, parts, compact=1):
     return ctx
 
 
-@pytest.mark.parametrize("fmt", ["csr", "coo"])
+@pytest.mark.parametrize("fmt", ["csr", "coo", "csc"])
 @pytest.mark.parametrize("parts", [1, 3])
-@pytest.mark.parametrize("compact", [1, 0])
+@pytest.mark.parametrize("compact", [1, 2, 0])
 def test_hot_x_bit_exact(fmt, parts, compact):
-    """Hot cache forced on (also at a 4 KiB size), off and automatic, with and without compact x."""
+    """Hot cache forced on (also at a 4 KiB size), off and automatic, with and without compact x
+    (column-ordered and degree-ordered x'); pCSC on row tiles indexes its column window."""
     A = gen.rmat(18, seed=31, kind=gen.SMALLINT)
     x = gen.vector(A["n"], 32, kind=gen.SMALLINT); y = gen.vector(A["m"], 33, kind=gen.SMALLINT)
     ref = oracle_ref(A, x, y, 1.5, 0.5)
     nhot, ncx = [], []
     for hot in (1, 4, 0, -1):
         ctx = _ctx(hot, parts, compact)
-        got = run_gpu(A, fmt, x, y, 1.5, 0.5, ctx=ctx)
+        got = run_gpu(A if fmt != "csc" else gen.transpose(A), fmt, x, y, 1.5, 0.5, ctx=ctx)
         nhot.append(ctx.stats()["nhot"])
         ncx.append(ctx.stats()["x_compact"])
         ctx.close()

@@ -13,10 +13,11 @@ import pytest
 
 import gen
 import oracle
-from tests.helpers import coo_of_csr, oracle_ref, shuffled_triplets
+from tests.helpers import apply_layout, coo_of_csr, oracle_ref, shuffled_triplets, split_fmt
 
 pytestmark = pytest.mark.gpu
-FMTS = ["csr", "coo", "csc", "coo_col", "coo_unsorted"]
+# column formats on row tiles (default; fp64 / fp32 partial y reduce-scattered) and on row bands
+FMTS = ["csr", "coo", "csc", "coo_col", "coo_unsorted", "csc:bands", "coo_unsorted:bands"]
 
 
 def _run_ranks(world, ppr, body):
@@ -48,6 +49,7 @@ def _run_ranks(world, ppr, body):
 
 def _partition(ctx, fmt, A, T, split, stream):
     sh = stream.cuda_stream
+    fmt = apply_layout(ctx, fmt)
     if fmt == "coo_unsorted":
         r, c, v = shuffled_triplets(A)
         ctx.partition(fmt, A["m"], A["n"], idx=c, val=v, coo_row=r, stream=sh, split=split)
@@ -61,6 +63,7 @@ def _partition(ctx, fmt, A, T, split, stream):
 
 def _segments(fmt, A, world, ppr, split):
     import paper_2209_07552_b200 as M
+    fmt = split_fmt(fmt)[0]
     ptr = coo = None
     if fmt == "csr":
         ptr = A["ptr"]
@@ -94,10 +97,10 @@ def test_loopback_spmv_all_layouts_bit_exact(fmt, world, ppr):
         A = mk()
         T = gen.transpose(A)
         x = gen.vector(A["n"], 302, kind=gen.SMALLINT); y = gen.vector(A["m"], 303, kind=gen.SMALLINT)
-        splits = ["nnz"] if fmt == "coo_unsorted" else ["nnz", "block"]
+        splits = ["nnz"] if fmt.startswith("coo_unsorted") else ["nnz", "block"]
         for split in splits:
             seg = _segments(fmt, A, world, ppr, split)
-            layouts = [M.Y_REPLICATED, M.Y_SHARDED if fmt in ("csc", "coo_col", "coo_unsorted") else M.Y_OWNED]
+            layouts = [M.Y_REPLICATED, M.Y_SHARDED if split_fmt(fmt)[0] in ("csc", "coo_col", "coo_unsorted") else M.Y_OWNED]
             for alpha, beta in [(1.5, -0.5), (2.0, 0.0), (0.0, 2.0)]:
                 ref = oracle_ref(A, x, y, alpha, beta)
 
@@ -122,7 +125,7 @@ def test_loopback_spmv_all_layouts_bit_exact(fmt, world, ppr):
                     assert np.array_equal(part[lo:hi], ref[lo:hi]), tag
 
 
-@pytest.mark.parametrize("fmt", ["csr", "coo", "csc"])
+@pytest.mark.parametrize("fmt", ["csr", "coo", "csc", "csc:bands"])
 def test_loopback_spmm_bit_exact(fmt):
     import torch
     A = gen.rmat(12, seed=304, kind=gen.SMALLINT)
@@ -166,7 +169,7 @@ def test_loopback_mirror_fused_allgather():
         assert np.array_equal(ys[r].cpu().numpy(), ref), r
 
 
-@pytest.mark.parametrize("fmt", ["csr", "csc"])
+@pytest.mark.parametrize("fmt", ["csr", "csc", "csc:bands"])
 def test_loopback_cg(fmt):
     import torch
     S = gen.stencil27(10, kind=gen.ONES)
@@ -228,7 +231,7 @@ def test_partition_slice_rejects_short_slice():
     ctx.close()
 
 
-@pytest.mark.parametrize("fmt", ["csr", "coo"])
+@pytest.mark.parametrize("fmt", ["csr", "coo", "csc", "coo_unsorted"])
 def test_loopback_hot_and_compact_x(fmt):
     """Per-rank hot-x cache and compact x (forced on: the auto rules need bigger slices) under the
     multi-rank merge: each rank relabels its own columns; results stay bit-exact."""
@@ -241,7 +244,7 @@ def test_loopback_hot_and_compact_x(fmt):
     def body(r, ctx, st):
         ctx.set_tuning("hot_x", 1)
         ctx.set_tuning("compact_x", 1)
-        _partition(ctx, fmt, A, None, "nnz", st)
+        _partition(ctx, fmt, A, gen.transpose(A) if fmt == "csc" else None, "nnz", st)
         s = ctx.stats()
         yd = torch.as_tensor(y).cuda()
         ctx.spmv(1.5, torch.as_tensor(x).cuda(), 0.5, yd, M.Y_REPLICATED, st.cuda_stream)
@@ -251,3 +254,30 @@ def test_loopback_hot_and_compact_x(fmt):
     assert all(o[0] > 0 and o[1] > 0 for o in outs), [o[:2] for o in outs]
     for _, _, out in outs:
         assert np.array_equal(out, ref)
+
+
+@pytest.mark.parametrize("fmt", ["csc", "coo_col", "coo_unsorted", "csc:bands"])
+@pytest.mark.parametrize("world,ppr", [(2, 1), (3, 2)])
+def test_loopback_column_formats_fp32(fmt, world, ppr):
+    """fp32 column formats under the merge: on row tiles each rank's partial y is fp32 and the
+    reduce-scatter sums fp32 (rank order); on row bands the partial y is fp64.  Integer data
+    (|y| < 2^24): every rank's result equals the oracle bit for bit."""
+    import torch
+    import paper_2209_07552_b200 as M
+    from tests.helpers import to_dtype
+    A = to_dtype(gen.rmat(13, seed=315, kind=gen.SMALLINT), np.float32)
+    T = gen.transpose(A)
+    x = gen.vector(A["n"], 316, kind=gen.SMALLINT, dtype=np.float32)
+    y = gen.vector(A["m"], 317, kind=gen.SMALLINT, dtype=np.float32)
+    ref = oracle_ref(A, x, y, 1.5, 0.5)
+
+    def body(r, ctx, st):
+        _partition(ctx, fmt, A, T, "nnz", st)
+        s = ctx.stats()
+        yd = torch.as_tensor(y).cuda()
+        ctx.spmv(1.5, torch.as_tensor(x).cuda(), 0.5, yd, M.Y_REPLICATED, st.cuda_stream)
+        st.synchronize()
+        return s["col_layout"], yd.cpu().numpy()
+    for lay, out in _run_ranks(world, ppr, body):
+        assert lay == (0 if fmt.endswith(":bands") else 1)
+        assert out.dtype == np.float32 and np.array_equal(out, ref)

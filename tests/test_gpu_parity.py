@@ -11,14 +11,18 @@ import pytest
 
 import gen
 import oracle
-from tests.helpers import assert_close, coo_of_csr, oracle_ref, row_bound, run_gpu, to_dtype
+from tests.helpers import (apply_layout, assert_close, coo_of_csr, oracle_ref, row_bound, run_gpu, split_fmt,
+                           to_dtype)
 
 pytestmark = pytest.mark.gpu
 
-FMTS = ["csr", "coo", "csc", "coo_col"]   # coo_col: column-sorted pCOO (merged like pCSC)
+# coo_col: column-sorted pCOO (merged like pCSC).  The column formats run on row tiles
+# over the GPU-transposed slice by default; ":bands" selects the host-built row-band layout.
+FMTS = ["csr", "coo", "csc", "coo_col", "csc:bands", "coo_col:bands"]
 
 
 def as_fmt(A, fmt):
+    fmt = split_fmt(fmt)[0]
     if fmt in ("csc", "coo_col"):
         return A if A["fmt"] == "csc" else gen.transpose(A)
     return A if A["fmt"] == "csr" else gen.transpose(A)
@@ -269,7 +273,7 @@ def test_config3_rmat_full_size_fp32_bit_exact():
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("fmt", ["csc", "coo_col"])
+@pytest.mark.parametrize("fmt", ["csc", "coo_col", "csc:bands"])
 def test_config3_rmat_full_size_column_formats_bit_exact(fmt):
     """R-MAT scale 24 through the pCSC band layout (its heavy first bands are split into slot units)
     and the column-sorted pCOO, fp64, bit-exact."""
@@ -286,10 +290,11 @@ def test_config4_tallskinny_fp32_bit_exact():
 
 
 @pytest.mark.slow
-def test_config4_tallskinny_csc_sampled():
+@pytest.mark.parametrize("fmt", ["csc", "csc:bands"])
+def test_config4_tallskinny_csc_sampled(fmt):
     A = gen.kdistinct_csc(50_000_000, 1_000_000, 500, seed=4, kind=gen.SMALLINT)
     x = gen.vector(A["n"], 9, kind=gen.SMALLINT); y = gen.vector(A["m"], 10, kind=gen.SMALLINT)
-    check(A, "csc", x, y, 2.0, 0.5, exact=True)
+    check(A, fmt, x, y, 2.0, 0.5, exact=True)
 
 
 # ------------------------------------------------------ pCSC row-band layout
@@ -302,23 +307,25 @@ def _csc_drop_rows(A, lo, hi):
     return gen.Sparse(fmt="csc", m=A["m"], n=A["n"], ptr=np.cumsum(ptr), idx=A["idx"][keep], val=A["val"][keep])
 
 
+@pytest.mark.parametrize("fmt", ["csc:bands", "csc"])
 @pytest.mark.parametrize("parts", [1, 3])
-def test_csc_bands_column_chunks_bit_exact(parts):
+def test_csc_bands_column_chunks_bit_exact(fmt, parts):
     """Several 8192-row bands (ragged last band), > 2^19 columns (two column chunks per
     band), an entirely empty band: bit-exact vs the oracle on integer data."""
     A = gen.kdistinct_csc(3 * 8192 + 17, (1 << 19) + 1000, 2, seed=41, kind=gen.SMALLINT)
     A = _csc_drop_rows(A, 8192, 2 * 8192)
     x = gen.vector(A["n"], 42, kind=gen.SMALLINT); y = gen.vector(A["m"], 43, kind=gen.SMALLINT)
     for alpha, beta in [(1.5, 0.5), (2.0, 0.0), (-1.0, 1.0)]:
-        check(A, "csc", x, y, alpha, beta, parts=parts, exact=True)
+        check(A, fmt, x, y, alpha, beta, parts=parts, exact=True)
 
 
+@pytest.mark.parametrize("fmt", ["csc:bands", "csc"])
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
-def test_csc_bands_uniform_tolerance(dtype):
+def test_csc_bands_uniform_tolerance(fmt, dtype):
     """Dense-ish columns spanning many bands, U[-1,1) values: per-row tolerance."""
     A = to_dtype(gen.kdistinct_csc(100_000, 3000, 400, seed=44), dtype)
     x = gen.vector(A["n"], 45, dtype=dtype); y = gen.vector(A["m"], 46, dtype=dtype)
-    check(A, "csc", x, y, 1.5, 0.5, parts=2)
+    check(A, fmt, x, y, 1.5, 0.5, parts=2)
 
 
 # --------------------------------------------- config 5: SuiteSparse-shaped suite
@@ -351,7 +358,7 @@ def test_suite_shapes_fp32_tolerance(shape, fmt):
     check(A, fmt, x, y, 1.5, 0.5, parts=2)
 
 
-@pytest.mark.parametrize("fmt", ["csc", "coo_col"])
+@pytest.mark.parametrize("fmt", ["csc:bands", "coo_col:bands", "csc", "coo_unsorted"])
 @pytest.mark.parametrize("parts", [1, 3])
 def test_csc_split_bands_reproducible(fmt, parts):
     """Heavy bands (R-MAT's first rows; a short-wide matrix with fewer bands than SMs) are cut into
@@ -365,18 +372,19 @@ def test_csc_split_bands_reproducible(fmt, parts):
         assert_close(outs[0], oracle_ref(A, x, y, 1.5, 0.5), row_bound(A, x, y, 1.5, 0.5), np.float64)
 
 
+@pytest.mark.parametrize("fmt", ["csc:bands", "csc"])
 @pytest.mark.parametrize("parts", [1, 2])
-def test_csc_split_items_short_wide(parts):
+def test_csc_split_items_short_wide(fmt, parts):
     """Fewer row bands than SMs (m = 3 bands): every band is cut into stage-range units whose
     partial rows go to slots, reduced in slot order at the end of the launch -- integer data,
     bit-exact; and fp32 within tolerance."""
     A = gen.kdistinct_csr(3 * 8192 - 5, 300_000, 40, seed=71, kind=gen.SMALLINT)
     x = gen.vector(A["n"], 72, kind=gen.SMALLINT); y = gen.vector(A["m"], 73, kind=gen.SMALLINT)
-    check(A, "csc", x, y, 1.5, 0.5, parts=parts, exact=True)
-    check(A, "csc", x, y, 2.0, 0.0, parts=parts, exact=True)
+    check(A, fmt, x, y, 1.5, 0.5, parts=parts, exact=True)
+    check(A, fmt, x, y, 2.0, 0.0, parts=parts, exact=True)
     B = to_dtype(gen.kdistinct_csr(1000, 200_000, 300, seed=74), np.float32)
     xb = gen.vector(B["n"], 75, dtype=np.float32); yb = gen.vector(B["m"], 76, dtype=np.float32)
-    check(B, "csc", xb, yb, 1.5, 0.5, parts=parts)
+    check(B, fmt, xb, yb, 1.5, 0.5, parts=parts)
 
 
 @pytest.mark.parametrize("fmt", ["csr", "coo"])
@@ -418,10 +426,11 @@ def test_block_split_bit_exact(fmt, parts):
         B = as_fmt(A, fmt)
         x = gen.vector(A["n"], 81, kind=gen.SMALLINT); y = gen.vector(A["m"], 82, kind=gen.SMALLINT)
         ctx = M.Context(0, 1, None, 0, parts)
-        if fmt in ("coo", "coo_col"):
-            ctx.partition(fmt, B["m"], B["n"], idx=B["idx"], val=B["val"], coo_row=coo_of_csr(B), split="block")
+        pf = apply_layout(ctx, fmt)
+        if pf in ("coo", "coo_col"):
+            ctx.partition(pf, B["m"], B["n"], idx=B["idx"], val=B["val"], coo_row=coo_of_csr(B), split="block")
         else:
-            ctx.partition(fmt, B["m"], B["n"], ptr=B["ptr"], idx=B["idx"], val=B["val"], split="block")
+            ctx.partition(pf, B["m"], B["n"], ptr=B["ptr"], idx=B["idx"], val=B["val"], split="block")
         assert (ctx.parts["start_flag"] == 0).all()
         xd = torch.as_tensor(x).cuda(); yd = torch.as_tensor(y.copy()).cuda()
         ctx.spmv(1.5, xd, 0.5, yd)
@@ -446,7 +455,7 @@ def test_sell_rows_per_lane(k, fmt):
     check(B, fmt, xb, yb, 2.0, 0.5, parts=2, exact=True)
 
 
-@pytest.mark.parametrize("fmt", ["csc", "coo_col"])
+@pytest.mark.parametrize("fmt", ["csc:bands", "coo_col:bands", "csc"])
 def test_csc_heavy_rows_same_row_groups(fmt):
     """Rows with thousands of entries inside one band (R-MAT heavy rows, and a dense row): the
     pCSC lists carry same-row groups of 32 (one warp-reduced update) -- bit-exact."""
@@ -462,7 +471,7 @@ def test_csc_heavy_rows_same_row_groups(fmt):
     check(D, fmt, xd, np.zeros(3), 1.0, 0.0, parts=2, exact=True)
 
 
-@pytest.mark.parametrize("fmt", ["csc", "coo_col"])
+@pytest.mark.parametrize("fmt", ["csc:bands", "coo_col:bands", "csc"])
 def test_csc_segmented_groups_few_rows(fmt):
     """Warp lists whose entries sit on fewer than 32 rows (40 rows of 700 entries in one band,
     plus sparse light rows): after the same-row groups the greedy distinct-row pass gets stuck and
@@ -500,10 +509,11 @@ def _cg_gpu(A, fmt, b, parts, dtype, tol, maxit):
     import torch
     B = as_fmt(to_dtype(A, dtype), fmt)
     ctx = M.Context(0, 1, None, 0, parts)
-    if fmt in ("coo", "coo_col"):
-        ctx.partition(fmt, B["m"], B["n"], idx=B["idx"], val=B["val"], coo_row=coo_of_csr(B))
+    pf = apply_layout(ctx, fmt)
+    if pf in ("coo", "coo_col"):
+        ctx.partition(pf, B["m"], B["n"], idx=B["idx"], val=B["val"], coo_row=coo_of_csr(B))
     else:
-        ctx.partition(fmt, B["m"], B["n"], ptr=B["ptr"], idx=B["idx"], val=B["val"])
+        ctx.partition(pf, B["m"], B["n"], ptr=B["ptr"], idx=B["idx"], val=B["val"])
     tdt = torch.float64 if dtype == np.float64 else torch.float32
     bd = torch.as_tensor(b.astype(dtype)).cuda()
     xd = torch.zeros(A["n"], dtype=tdt, device="cuda")
@@ -579,10 +589,11 @@ def test_cg_exact_convergence_no_nan(fmt, graph):
     B = as_fmt(A, fmt)
     ctx = M.Context(0, 1, None, 0, 2)
     ctx.set_tuning("cg_graph", graph)
-    if fmt in ("coo", "coo_col"):
-        ctx.partition(fmt, m, m, idx=B["idx"], val=B["val"], coo_row=coo_of_csr(B))
+    pf = apply_layout(ctx, fmt)
+    if pf in ("coo", "coo_col"):
+        ctx.partition(pf, m, m, idx=B["idx"], val=B["val"], coo_row=coo_of_csr(B))
     else:
-        ctx.partition(fmt, m, m, ptr=B["ptr"], idx=B["idx"], val=B["val"])
+        ctx.partition(pf, m, m, ptr=B["ptr"], idx=B["idx"], val=B["val"])
     b = (np.arange(m) % 9 - 4).astype(np.float64)
     xd = torch.zeros(m, dtype=torch.float64, device="cuda")
     it, rr = ctx.cg(torch.as_tensor(b).cuda(), xd, tol=0.0, maxit=12, check_every=1)
@@ -634,10 +645,11 @@ def _spmm_gpu(A, fmt, X, Y, alpha, beta, parts):
     import torch
     B = as_fmt(A, fmt)
     ctx = M.Context(0, 1, None, 0, parts)
-    if fmt in ("coo", "coo_col"):
-        ctx.partition(fmt, B["m"], B["n"], idx=B["idx"], val=B["val"], coo_row=coo_of_csr(B))
+    pf = apply_layout(ctx, fmt)
+    if pf in ("coo", "coo_col"):
+        ctx.partition(pf, B["m"], B["n"], idx=B["idx"], val=B["val"], coo_row=coo_of_csr(B))
     else:
-        ctx.partition(fmt, B["m"], B["n"], ptr=B["ptr"], idx=B["idx"], val=B["val"])
+        ctx.partition(pf, B["m"], B["n"], ptr=B["ptr"], idx=B["idx"], val=B["val"])
     Xd = torch.as_tensor(np.ascontiguousarray(X)).cuda()
     Yd = torch.as_tensor(np.ascontiguousarray(Y)).cuda()
     ctx.spmm(alpha, Xd, beta, Yd)
@@ -683,15 +695,16 @@ def test_spmm_fp32_tolerance(k):
         assert_close(got[:, j], oracle_ref(A, x, y, 1.5, 0.5), row_bound(A, x, y, 1.5, 0.5), np.float32)
 
 
+@pytest.mark.parametrize("fmt", ["csc:bands", "csc"])
 @pytest.mark.parametrize("k", [2, 8])
-def test_spmm_column_formats_fp32_and_split_bands(k):
+def test_spmm_column_formats_fp32_and_split_bands(fmt, k):
     """pCSC SpMM (one strided band-kernel pass per vector): fp32 within tolerance on a short-wide
     matrix whose bands are split into slot units, and the unsorted pCOO path."""
     A = to_dtype(gen.kdistinct_csr(3000, 200_000, 60, seed=24), np.float32)
     rng = np.random.default_rng(40 + k)
     X = rng.uniform(-1, 1, (A["n"], k)).astype(np.float32)
     Y = rng.uniform(-1, 1, (A["m"], k)).astype(np.float32)
-    got = _spmm_gpu(A, "csc", X, Y, 1.5, 0.5, 3)
+    got = _spmm_gpu(A, fmt, X, Y, 1.5, 0.5, 3)
     for j in range(k):
         x, y = X[:, j].copy(), Y[:, j].copy()
         assert_close(got[:, j], oracle_ref(A, x, y, 1.5, 0.5), row_bound(A, x, y, 1.5, 0.5), np.float32)
@@ -769,12 +782,53 @@ def test_two_level_split_bit_exact(fmt):
     x = gen.vector(A["n"], 52, kind=gen.SMALLINT); y = gen.vector(A["m"], 53, kind=gen.SMALLINT)
     for groups in ([1, 3], [4, 4]):
         ctx = M.Context(0, 1, None, 0, sum(groups))
-        if fmt in ("coo", "coo_col"):
-            ctx.partition(fmt, B["m"], B["n"], idx=B["idx"], val=B["val"], coo_row=coo_of_csr(B), split=groups)
+        pf = apply_layout(ctx, fmt)
+        if pf in ("coo", "coo_col"):
+            ctx.partition(pf, B["m"], B["n"], idx=B["idx"], val=B["val"], coo_row=coo_of_csr(B), split=groups)
         else:
-            ctx.partition(fmt, B["m"], B["n"], ptr=B["ptr"], idx=B["idx"], val=B["val"], split=groups)
+            ctx.partition(pf, B["m"], B["n"], ptr=B["ptr"], idx=B["idx"], val=B["val"], split=groups)
         xd = torch.as_tensor(x).cuda(); yd = torch.as_tensor(y.copy()).cuda()
         ctx.spmv(1.5, xd, 0.5, yd)
         torch.cuda.synchronize()
         assert np.array_equal(yd.cpu().numpy(), oracle_ref(A, x, y, 1.5, 0.5)), (fmt, groups)
         ctx.close()
+
+
+# ---------------------------------------- column formats on row tiles (GPU-transposed slice)
+@pytest.mark.parametrize("fmt", ["csc", "coo_col", "coo_unsorted"])
+def test_col_row_tiles_repartition_reproducible(fmt):
+    """The GPU transposition is a stable sort: partitioning the same matrix twice builds the same
+    layout, so U[-1,1) results are bit-identical across partitions (not just across calls); the
+    layout is reported (stats col_layout 1; bands 0) and both layouts agree within tau."""
+    import paper_2209_07552_b200 as M
+    A = gen.rmat(15, seed=151)
+    x = gen.vector(A["n"], 152); y = gen.vector(A["m"], 153)
+    outs, lays = [], []
+    for lay in ("", ":bands", ""):
+        ctx = M.Context(0, 1, None, 0, 3)
+        outs.append(run_gpu(as_fmt(A, fmt), fmt + lay, x, y, 1.5, 0.5, ctx=ctx))
+        lays.append(ctx.stats()["col_layout"])
+        ctx.close()
+    assert lays == [1, 0, 1]
+    assert np.array_equal(outs[0], outs[2])
+    for o in outs:
+        assert_close(o, oracle_ref(A, x, y, 1.5, 0.5), row_bound(A, x, y, 1.5, 0.5), np.float64)
+
+
+@pytest.mark.parametrize("m", [1, 2, 255, 256, 257, 65536, 65537])
+def test_col_row_tiles_radix_passes(m):
+    """Row counts around the radix digit boundaries (0..3 passes of 8 bits, m = 1 needs none) and
+    duplicate (row, col) entries in a column: bit-exact on integer data; the rows are tall enough
+    that the sort's 4096-entry tiles and ragged last tile are all exercised."""
+    rng = np.random.default_rng(m)
+    n = 700
+    nz = 30_000
+    rows = rng.integers(0, m, nz)
+    cols = np.sort(rng.integers(0, n, nz))
+    ptr = np.zeros(n + 1, np.int64)
+    np.add.at(ptr, cols + 1, 1)
+    vals = rng.integers(-4, 5, nz).astype(np.float64)
+    A = gen.Sparse(fmt="csc", m=m, n=n, ptr=np.cumsum(ptr), idx=rows.astype(np.int32), val=vals)
+    x = gen.vector(n, 154, kind=gen.SMALLINT); y = gen.vector(m, 155, kind=gen.SMALLINT)
+    for parts in (1, 4):
+        check(A, "csc", x, y, 1.5, 0.5, parts=parts, exact=True)

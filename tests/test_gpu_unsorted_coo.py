@@ -23,21 +23,23 @@ def test_unsorted_fixture_E(golden_E, parts):
         assert got.tolist() == case["expect"]
 
 
+@pytest.mark.parametrize("fmt", ["coo_unsorted", "coo_unsorted:bands"])
 @pytest.mark.parametrize("parts", [1, 3, 5])
-def test_unsorted_rmat_bit_exact(parts):
+def test_unsorted_rmat_bit_exact(fmt, parts):
     A = gen.rmat(15, seed=81, kind=gen.SMALLINT)
     x = gen.vector(A["n"], 82, kind=gen.SMALLINT); y = gen.vector(A["m"], 83, kind=gen.SMALLINT)
     for alpha, beta in [(1.5, 0.5), (2.0, 0.0), (0.0, -1.0), (-1.0, 1.0)]:
-        got = run_gpu(A, "coo_unsorted", x, y, alpha, beta, parts=parts)
+        got = run_gpu(A, fmt, x, y, alpha, beta, parts=parts)
         r, c, v = shuffled_triplets(A)
         assert np.array_equal(got, oracle.exec_coo_unsorted(A["m"], r, c, v, x, y, alpha, beta, parts))
         assert np.array_equal(got, oracle_ref(A, x, y, alpha, beta))
 
 
-def test_unsorted_stencil_and_wide_bit_exact():
+@pytest.mark.parametrize("fmt", ["coo_unsorted", "coo_unsorted:bands"])
+def test_unsorted_stencil_and_wide_bit_exact(fmt):
     for A in (gen.stencil27(30, kind=gen.SMALLINT), gen.kdistinct_csr(2000, 300_000, 40, seed=84, kind=gen.SMALLINT)):
         x = gen.vector(A["n"], 85, kind=gen.SMALLINT); y = gen.vector(A["m"], 86, kind=gen.SMALLINT)
-        got = run_gpu(A, "coo_unsorted", x, y, 1.5, 0.5, parts=3)
+        got = run_gpu(A, fmt, x, y, 1.5, 0.5, parts=3)
         assert np.array_equal(got, oracle_ref(A, x, y, 1.5, 0.5))
 
 
@@ -67,8 +69,9 @@ def test_unsorted_descriptors_and_errors():
     ctx.close()
 
 
-def test_unsorted_host_resident():
+@pytest.mark.parametrize("fmt", ["coo_unsorted", "coo_unsorted:bands"])
+def test_unsorted_host_resident(fmt):
     A = gen.rmat(14, seed=91, kind=gen.SMALLINT)
     x = gen.vector(A["n"], 92, kind=gen.SMALLINT); y = gen.vector(A["m"], 93, kind=gen.SMALLINT)
-    got = run_gpu(A, "coo_unsorted", x, y, 1.5, 0.5, parts=3, residency="host", chunk_bytes=1 << 16)
+    got = run_gpu(A, fmt, x, y, 1.5, 0.5, parts=3, residency="host", chunk_bytes=1 << 16)
     assert np.array_equal(got, oracle_ref(A, x, y, 1.5, 0.5))
