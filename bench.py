@@ -574,9 +574,10 @@ def main():
             "clocks": clocks,
             "partition_ms": st["partition_ms"],
             "partition_phase_ms": dict(zip(("validate", "plan", "schedule", "upload_pack"), list(st["phase_ms"]))),
+            "layout_build_ms": list(st["layout_ms"]),
             "stats_rank0": {k: st[k] for k in ("nnz_rank", "ntiles", "nsell", "nslabs", "nsplit_rows",
                                                "distinct_cols", "kernels_per_spmv", "tile_bytes", "x_no_allocate",
-                                               "nhot", "hot_nnz", "x_compact", "col_layout")},
+                                               "nhot", "hot_nnz", "x_compact", "x_order", "col_layout")},
         }
         print(json.dumps(out), flush=True)
     ctx.close()

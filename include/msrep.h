@@ -151,6 +151,13 @@ typedef struct {
                                 the 4-B row ids alg_bytes counts                              */
   int64_t col_layout;        /* column formats: 1 row tiles (slice transposed on the GPU), 0 row
                                 bands (MSREP_TUNE_COL_LAYOUT); row formats: -1                */
+  double layout_ms[6];       /* the device-layout build inside phase_ms[2..3] (host wall clock):
+                                row tiles: [0] GPU transposition of a column slice (upload, sort,
+                                row pointer), [1] tile schedule, [2] slice upload + column degrees
+                                + hot / compact-x selection, [3] x-layout tables + pack kernels,
+                                [4] tile table / records, [5] before the transposition; row bands:
+                                [0..4] counts, sort, list sizing, items / units, list writes    */
+  int64_t x_order;           /* compact x order: 0 column, 1 decreasing degree; -1 no compact x */
 } msrep_stats;
 
 /* NCCL unique id for the communicator (rank 0 creates it, the caller
@@ -274,9 +281,11 @@ msrep_status_t msrep_set_residency(msrep_ctx ctx, msrep_residency residency, int
  *   MSREP_TUNE_COMPACT_X compact x for the row formats, applied by the next
  *                       msrep_partition: the tiles index the rank's distinct
  *                       columns and every SpMV first gathers x' = x[cols]
- *                       (one launch): -1 (default) when x is >= 32 MB, 0 off, 1 on,
- *                       2 on with x' in decreasing column degree instead of column
- *                       order (the most-gathered entries share cache lines).
+ *                       (one launch): -1 (default) when x is >= 32 MB and either the
+ *                       column degrees are skewed (x' in decreasing degree) or the
+ *                       rank touches <= 3/4 of x (x' in column order); 0 off; 1 on,
+ *                       column order; 2 on, decreasing column degree (the most-
+ *                       gathered entries share cache lines).
  *   MSREP_TUNE_HOT_CLUSTER CTAs sharing one hot-x cache, applied by the next
  *                       msrep_partition: 1 (default) -- every CTA holds the
  *                       whole cache; 2 -- the kernel runs as CTA pairs

@@ -62,7 +62,8 @@ class Stats(ctypes.Structure):
                                          ("hot_nnz", ctypes.c_int64), ("x_compact", ctypes.c_int64),
                                          ("sell_1cta", ctypes.c_int64),
                                          ("gpu_numa_node", ctypes.c_int64), ("host_numa_node", ctypes.c_int64),
-                                         ("stream_bytes", ctypes.c_int64), ("col_layout", ctypes.c_int64)]
+                                         ("stream_bytes", ctypes.c_int64), ("col_layout", ctypes.c_int64),
+                                         ("layout_ms", ctypes.c_double * 6), ("x_order", ctypes.c_int64)]
 
 
 class Allocator(ctypes.Structure):
@@ -315,7 +316,7 @@ def msrep_cg(ctx, b, x, tol=1e-10, maxit=1000, check_every=10, stream=None):
 def msrep_get_stats(ctx) -> dict:
     s = Stats()
     _check(_lib.msrep_get_stats(ctx, ctypes.byref(s)), "msrep_get_stats")
-    return {k: (list(getattr(s, k)) if k == "phase_ms" else getattr(s, k)) for k, _ in Stats._fields_}
+    return {k: (list(getattr(s, k)) if k in ("phase_ms", "layout_ms") else getattr(s, k)) for k, _ in Stats._fields_}
 
 
 def msrep_profile_enable(ctx, enable=True):

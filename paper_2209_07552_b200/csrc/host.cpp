@@ -387,6 +387,7 @@ struct Ctx {
   int nhot = 0;
   int64_t hot_nnz = 0;              // the rank's nonzeros whose x comes from the hot cache
   int64_t nxc = 0;                  // compact x entries (0: the kernels gather from x itself)
+  int x_order = 0;                  // compact x order: 0 column, 1 decreasing degree
   int hot_cluster = 1;              // the partition's hot-x sharing (tune_hot_cluster when built)
   int32_t* d_xcols = nullptr;       // the rank's distinct columns, ascending (compact x -> column)
   void* d_xc = nullptr;             // x' = x[d_xcols], gathered at the start of every SpMV
@@ -1956,12 +1957,20 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
 
   const int64_t nz_r = B_hi - B_lo;
   lap(1);
+  double layout_ms[6] = {0, 0, 0, 0, 0, 0};   // sub-steps of the layout build (stats.layout_ms)
+  auto ts = std::chrono::steady_clock::now();
+  auto sub = [&](int k) {
+    const auto now = std::chrono::steady_clock::now();
+    layout_ms[k] += std::chrono::duration<double, std::milli>(now - ts).count();
+    ts = now;
+  };
   if (colwise(fmt) && !col_rows) {
     // ---- pCSC: row-band layout built on the host threads, uploaded once
     CscBands CB;
     int sms = 148;
     CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
     TRY(build_csc_bands(*c, lp, idx, val, V, sms, CB));
+    for (int k = 0; k < 5; k++) layout_ms[k] = g_csc_ms[k];
     lap(2);
     TRY(upload_vec(c, CB.items, &c->d_citems, s));
     TRY(upload_vec(c, CB.item_hst, &c->d_item_hst, s));
@@ -2052,7 +2061,9 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     int32_t *t_cols = nullptr, *t_ptr = nullptr;
     void* t_vals = nullptr;
     if (tr) {
+      sub(5);
       TRY(transpose_slice(c, fmt, lp, idx, coo_row, val, V, s, &t_cols, &t_vals, &t_ptr, lpr));
+      sub(0);
       lap(3);
     }
     const std::vector<int64_t>& LP = tr ? lpr : lp;
@@ -2067,8 +2078,47 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     // ---- schedule
     Schedule S;
     auto schedule = [&](bool sell) {
-      if (tr) build_row_schedule(tpart, 0, 1, 0, 0, (int)V, LP, S, sell);
-      else build_row_schedule(c->parts, c->P0, c->P1, c->B_lo, c->wlo, (int)V, LP, S, sell);
+      if (!tr) {
+        build_row_schedule(c->parts, c->P0, c->P1, c->B_lo, c->wlo, (int)V, LP, S, sell);
+        return;
+      }
+      // one part of its own with no shared rows: rows cut into fixed chunks of 2^18 (the cut never
+      // depends on the host's thread count, so neither do the tiles nor the bits), scheduled on the
+      // host threads, then concatenated (record indices offset)
+      constexpr int64_t CH = (int64_t)1 << 18;
+      const int64_t nch = std::max<int64_t>(1, (m + CH - 1) / CH);
+      std::vector<Schedule> cs((size_t)nch);
+      std::atomic<int64_t> next{0};
+      auto work = [&] {
+        for (int64_t k; (k = next.fetch_add(1)) < nch;) {
+          const int64_t r0 = k * CH, r1 = std::min(m, r0 + CH);
+          std::vector<msrep_part_desc> d(1, tpart[0]);
+          d[0].start_idx = LP[(size_t)r0];
+          d[0].end_idx = LP[(size_t)r1] - 1;
+          d[0].start_row = r0; d[0].end_row = r1 - 1;
+          d[0].owned_begin = r0; d[0].owned_end = r1;
+          build_row_schedule(d, 0, 1, 0, 0, (int)V, LP, cs[(size_t)k], sell);
+        }
+      };
+      const int T = (int)std::min<int64_t>(nch, host_threads(nz_r + m));
+      std::vector<std::thread> th;
+      for (int t = 1; t < T; t++) th.emplace_back(work);
+      work();
+      for (auto& x : th) x.join();
+      for (Schedule& q : cs) {
+        const int32_t off = S.nrec;
+        for (TileHost t : q.tiles) {
+          if (t.rec >= 0) t.rec += off;
+          S.tiles.push_back(t);
+        }
+        S.sell.insert(S.sell.end(), q.sell.begin(), q.sell.end());
+        S.sr_row.insert(S.sr_row.end(), q.sr_row.begin(), q.sr_row.end());
+        for (int32_t v : q.sr_rec) S.sr_rec.push_back(v + off);
+        S.sr_head.insert(S.sr_head.end(), q.sr_head.begin(), q.sr_head.end());   // no head lists: all 0
+        S.nrec += q.nrec;
+        S.nslabs += q.nslabs;
+      }
+      S.part_rec = {0, S.nrec};
     };
     schedule(c->tune_sell != 0);
     {
@@ -2088,6 +2138,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
       // instantiation instead of riding in the SELL one
       c->split_launch = !S.sell.empty() && (nz_r - sell_nz) * 20 >= nz_r;
     }
+    sub(1);
     lap(2);
     c->ntiles = (int)(S.tiles.size() + S.sell.size());
     c->nsell = (int)S.sell.size();
@@ -2194,9 +2245,10 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     c->nhot = 0;
     c->hot_nnz = 0;
     c->nxc = 0;
+    c->x_order = 0;
     const bool want_hot = !host_res && c->tune_hot != 0 && nz_r > 0 && nx > 0 && (c->nsell == 0 || c->split_launch);
     const bool want_cx = !host_res && nz_r > 0 && nx > 0 &&
-                         (c->tune_compact == 1 || (c->tune_compact == -1 && (int64_t)nx * (int64_t)V >= COMPACT_X_MIN_BYTES));
+                         (c->tune_compact >= 1 || (c->tune_compact == -1 && (int64_t)nx * (int64_t)V >= COMPACT_X_MIN_BYTES));
     if (tr) idx_up = true;
     if (want_hot || want_cx) {
       int sms = 148;
@@ -2228,14 +2280,47 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
       if (want_cx) {
         std::sort(used.begin(), used.end(), [](const auto& p, const auto& q) { return p.first < q.first; });
         for (auto& u : used) xcols.insert(xcols.end(), u.second.begin(), u.second.end());
-        // auto: only when the rank touches <= 3/4 of x (R-MAT scale 24: 44 %); a power-law matrix
-        // that touches every column gains nothing from the extra gather
-        if (c->tune_compact >= 1 || (int64_t)xcols.size() * 4 <= (int64_t)nx * 3) {
+        // auto: degree-ordered x' when the column degrees are skewed -- the columns of >= 8x the
+        // mean degree hold >= 1/5 of the rank's nonzeros (R-MAT, power-law columns: their hot lines
+        // then share L2 sets and L1 instead of being spread over all of x; power-law suite 0.995 ->
+        // 0.778 ms, R-MAT 1.153 -> 1.110, profiles/r2_x_order_ab.txt); else column order when the
+        // rank touches <= 3/4 of x (R-MAT scale 24: 44 %; a uniform matrix that touches every
+        // column gains nothing from the extra gather); else no compact x
+        bool skewed = false;
+        if (!xcols.empty()) {
+          const int64_t thr = 8 * (nz_r / (int64_t)xcols.size());
+          int64_t heavy = 0;
+          for (int32_t q : xcols) heavy += deg[(size_t)q] >= thr ? deg[(size_t)q] : 0;
+          skewed = heavy * 5 >= nz_r;
+        }
+        const int mode = c->tune_compact >= 1 ? c->tune_compact
+                         : skewed ? 2 : ((int64_t)xcols.size() * 4 <= (int64_t)nx * 3 ? 1 : 0);
+        if (mode >= 1) {
           TRY(dalloc(c, (size_t)nx * 4, &dp, s));
           d_colmap = static_cast<int32_t*>(dp);   // column -> compact id (filled from the kept list below)
           c->nxc = (int64_t)xcols.size();
-          if (c->tune_compact == 2)   // degree order: the most-gathered columns share the first lines of x'
-            std::stable_sort(xcols.begin(), xcols.end(), [&](int32_t a, int32_t b) { return deg[(size_t)a] > deg[(size_t)b]; });
+          c->x_order = mode == 2 ? 1 : 0;
+          if (mode == 2) {   // degree order: the most-gathered columns share the first lines of x'
+            // stable by column within a degree: columns of degree >= 2^16 (few) sorted, the rest
+            // counting-sorted by degree (descending)
+            constexpr int32_t CAP = 1 << 16;
+            std::vector<int32_t> out;
+            out.reserve(xcols.size());
+            std::vector<int64_t> cnt((size_t)CAP + 1, 0);
+            for (int32_t q : xcols) {
+              if (deg[(size_t)q] >= CAP) out.push_back(q);
+              else cnt[(size_t)(CAP - deg[(size_t)q])]++;
+            }
+            std::sort(out.begin(), out.end(), [&](int32_t a, int32_t b) {
+              return deg[(size_t)a] != deg[(size_t)b] ? deg[(size_t)a] > deg[(size_t)b] : a < b;
+            });
+            int64_t pos = (int64_t)out.size();
+            for (auto& v : cnt) { const int64_t t = v; v = pos; pos += t; }
+            out.resize(xcols.size());
+            for (int32_t q : xcols)
+              if (deg[(size_t)q] < CAP) out[(size_t)cnt[(size_t)(CAP - deg[(size_t)q])]++] = q;
+            xcols.swap(out);
+          }
         } else {
           xcols.clear();
         }
@@ -2272,6 +2357,8 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
         }
       }
     }
+    CUDA_TRY(cudaStreamSynchronize(s));
+    sub(2);
     const size_t keep_from = c->bufs.size();
     c->d_xcols = nullptr;
     c->d_xc = nullptr;
@@ -2284,7 +2371,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     }
     if (c->nhot) {
       CUDA_TRY(launch_hot_slots(dp_hot_tmp, c->nhot, d_hotslot, s));
-      if (c->nxc && c->tune_compact == 2) {   // degree-ordered x': the hot columns are its first entries
+      if (c->nxc && c->x_order == 1) {   // degree-ordered x': the hot columns are its first entries
         for (size_t q = 0; q < hot.size(); q++) hot[q] = (int32_t)q;
       } else if (c->nxc) {   // the kernels read x': hot slots are filled from compact ids
         for (auto& q : hot) q = (int32_t)(std::lower_bound(xcols.begin(), xcols.end(), q) - xcols.begin());
@@ -2325,6 +2412,8 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
       if (host_res)
         CUDA_TRY(cudaMemcpyAsync(c->h_blob + off0, d_pack, (size_t)c->chunks[gi].bytes, cudaMemcpyDeviceToHost, s));
     }
+    CUDA_TRY(cudaStreamSynchronize(s));
+    sub(3);
     std::vector<TileHost> fin(S.tiles);
     for (size_t t = 0; t < fin.size(); t++) fin[t].nz0 = blob16[t];
     CUDA_TRY(cudaStreamSynchronize(s));
@@ -2372,6 +2461,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     }
   }
   CUDA_TRY(cudaStreamSynchronize(s));
+  if (!colwise(fmt) || col_rows) sub(4);
   lap(3);
   nv_phase.end();
   const auto t1 = std::chrono::steady_clock::now();
@@ -2398,6 +2488,8 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   st.host_numa_node = c->h_blob ? page_numa_node(c->h_blob) : -1;
   st.hot_nnz = c->hot_nnz;
   st.col_layout = colwise(fmt) ? (c->col_rows ? 1 : 0) : -1;
+  st.x_order = c->nxc ? c->x_order : -1;
+  for (int k = 0; k < 6; k++) st.layout_ms[k] = layout_ms[k];
   int64_t X = 0;
   if (colwise(fmt)) {
     X = W;   // pCSC reads x only over its column window
@@ -2840,11 +2932,12 @@ msrep_status_t msrep_cg(msrep_ctx h, const void* b, void* x, double tol, int max
   };
   // CUDA graph of one period (two iterations, eight launches) replayed on a context stream: the
   // iteration is launch-bound for small systems (pCSR 110K rows: 0.0228 -> 0.0181 ms/iteration;
-  // 2M rows: 0.152 -> 0.147, profiles/r1_cg_graph.jsonl).  Single rank, device-resident, row
-  // formats (a replayed pCSC iteration measured 30 % slower than eager), profiling off;
+  // 2M rows: 0.152 -> 0.147, profiles/r1_cg_graph.jsonl).  Single rank, device-resident, row tiles
+  // (row formats and column formats on row tiles; a replayed row-band pCSC iteration measured 30 %
+  // slower than eager), profiling off;
   // msrep_set_tuning(MSREP_TUNE_CG_GRAPH, 0) disables it.  The convergence check then runs every 2*ceil(check_every/2)
   // iterations; the iterates are the same kernels in the same order as the eager loop.
-  const bool graph = c->nranks == 1 && c->residency == MSREP_RESIDENT_DEVICE && !colwise(c->fmt) && !c->prof &&
+  const bool graph = c->nranks == 1 && c->residency == MSREP_RESIDENT_DEVICE && (!colwise(c->fmt) || c->col_rows) && !c->prof &&
                      maxit >= 8 && c->tune_cg_graph;
   if (graph && !(rs <= stop)) {
     if (!c->gs) CUDA_TRY(cudaStreamCreateWithFlags(&c->gs, cudaStreamNonBlocking));

@@ -30,6 +30,37 @@ def test_library_exports_every_declared_symbol():
     assert M.msrep_version() == 1
 
 
+def _header_struct_fields(name):
+    """(field, C type, array length) of `typedef struct {...} name;` in include/msrep.h, in order"""
+    src = open(os.path.join(ROOT, "include", "msrep.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    body = re.search(r"typedef struct \{([^{}]*)\}\s*" + name + ";", src).group(1)
+    out = []
+    for decl in body.split(";"):
+        decl = decl.strip()
+        if not decl:
+            continue
+        ctype, rest = decl.split(None, 1)
+        for f in rest.split(","):
+            m = re.match(r"\s*(\w+)(?:\[(\d+)\])?", f)
+            out.append((m.group(1), ctype, int(m.group(2)) if m.group(2) else 1))
+    return out
+
+
+def test_binding_structs_match_header():
+    """The ctypes mirrors of msrep_stats / msrep_part_desc have the header's fields, in order, with
+    the same types and sizes: a missing field would let msrep_get_stats write past the buffer."""
+    import paper_2209_07552_b200 as M
+    sizes = {"int64_t": 8, "double": 8, "int32_t": 4}
+    for cls, name in ((M.Stats, "msrep_stats"), (M.PartDesc, "msrep_part_desc")):
+        hdr = _header_struct_fields(name)
+        py = [(f, t) for f, t in cls._fields_]
+        assert [f for f, _, _ in hdr] == [f for f, _ in py], name
+        for (f, ct, n), (_, t) in zip(hdr, py):
+            assert ctypes.sizeof(t) == sizes[ct] * n, (name, f)
+        assert ctypes.sizeof(cls) == sum(sizes[ct] * n for _, ct, n in hdr), name
+
+
 def test_library_is_sm100a_and_uses_tma():
     import shutil
     import subprocess

@@ -539,7 +539,7 @@ def test_cg_matches_oracle(fmt, parts):
     assert np.max(np.abs(x - xo)) < 1e-9
 
 
-@pytest.mark.parametrize("fmt", ["csr", "csc"])
+@pytest.mark.parametrize("fmt", ["csr", "csc", "csc:bands"])
 def test_cg_graph_matches_eager(fmt):
     """msrep_cg replays a captured CUDA graph of two iterations (single rank, device-resident);
     with even convergence checks it takes the same iterations and the same iterates, bit for
@@ -555,7 +555,7 @@ def test_cg_graph_matches_eager(fmt):
         B = as_fmt(A, fmt)
         ctx = M.Context(0, 1, None, 0, 2)
         ctx.set_tuning("cg_graph", graph)
-        ctx.partition(fmt, B["m"], B["n"], ptr=B["ptr"], idx=B["idx"], val=B["val"])
+        ctx.partition(apply_layout(ctx, fmt), B["m"], B["n"], ptr=B["ptr"], idx=B["idx"], val=B["val"])
         xd = torch.zeros(m, dtype=torch.float64, device="cuda")
         it, rr = ctx.cg(b, xd, tol=1e-11, maxit=300, check_every=4)
         res.append((it, rr, xd.cpu().numpy()))

@@ -14,10 +14,14 @@ line --config stencil --format csc
 line --config stencil --dtype f32
 line --config rmat --format coo
 line --config rmat --format csc
+line --config rmat --format csc --col-layout 0
+line --config rmat --format coo_col
 line --config rmat --dtype f32
 line --config rmat --layout owned
 line --config tallskinny
+line --config tallskinny --col-layout 0
 line --config tallskinny --dtype f32
+line --config stencil --format csc --col-layout 0
 line --config random1k --steps 5000
 # launch list of the default bench (per-launch GPU time; cold-cache, serialised by ncu)
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $O/launches_rmat.csv \
@@ -34,10 +38,11 @@ prof rmat_rows rows_kernel
 python tools/traffic_from_ncu.py $O/prof_rmat_rows.ncu-rep rmat_csr_f64_m16777216_n16777216_nnz263419028 rows_kernel > $O/traffic_rmat.txt 2>&1
 prof stencil_rows rows_kernel --config stencil
 python tools/traffic_from_ncu.py $O/prof_stencil_rows.ncu-rep stencil_csr_f64_m2048383_n2048383_nnz54439939 rows_kernel > $O/traffic_stencil.txt 2>&1
-prof ts_csc csc_band_kernel --config tallskinny
-python tools/traffic_from_ncu.py $O/prof_ts_csc.ncu-rep tallskinny_csc_f64_m50000000_n1000000_nnz500000000 csc_band_kernel > $O/traffic_ts.txt 2>&1
-prof rmat_csc csc_band_kernel --config rmat --format csc
-python tools/traffic_from_ncu.py $O/prof_rmat_csc.ncu-rep rmat_csc_f64_m16777216_n16777216_nnz263419028 csc_band_kernel > $O/traffic_rmat_csc.txt 2>&1
+prof ts_csc rows_kernel --config tallskinny
+python tools/traffic_from_ncu.py $O/prof_ts_csc.ncu-rep tallskinny_csc_f64_m50000000_n1000000_nnz500000000 rows_kernel > $O/traffic_ts.txt 2>&1
+prof rmat_csc rows_kernel --config rmat --format csc
+python tools/traffic_from_ncu.py $O/prof_rmat_csc.ncu-rep rmat_csc_f64_m16777216_n16777216_nnz263419028 rows_kernel > $O/traffic_rmat_csc.txt 2>&1
+prof ts_bands csc_band_kernel --config tallskinny --col-layout 0
 cp profiles/traffic.json $O/traffic.json
 rm -f $O/*.ncu-rep
 bash tools/suite_sweep.sh && mv gpurun_out/suite_sweep.jsonl $O/

@@ -30,10 +30,10 @@ LAT = 15e-6           # s, one small NCCL collective
 
 
 def time_part(A, fmt, d, x, reps):
-    """ms of one part's SpMV ALONE (its nonzeros as a one-rank matrix)."""
+    """(ms of one part's SpMV ALONE (its nonzeros as a one-rank matrix), its algorithmic bytes)."""
     b0, b1 = int(d["start_idx"]), int(d["end_idx"]) + 1
     if b1 <= b0:
-        return 0.0
+        return 0.0, 0
     o0, o1 = int(d["start_row"]), int(d["end_row"]) + 1          # rows (CSR) / columns (CSC)
     ptr = np.clip(A["ptr"][o0:o1 + 1], b0, b1) - b0
     ctx = M.Context(0, 1, None, 0, 1)
@@ -54,8 +54,9 @@ def time_part(A, fmt, d, x, reps):
         ctx.spmv(1.0, xd, 0.0, yd)
     e1.record()
     torch.cuda.synchronize()
+    ab = ctx.stats()["alg_bytes_beta0"]
     ctx.close()
-    return e0.elapsed_time(e1) / reps
+    return e0.elapsed_time(e1) / reps, ab
 
 
 def main():
@@ -75,7 +76,9 @@ def main():
         t1 = None
         for p in (1, 2, 4, 8):
             plan = M.msrep_plan(M.CSR if fmt == "csr" else M.CSC, outer, A.nnz, p, ptr=A["ptr"])
-            tp = [time_part(A, fmt, d, x, a.reps) for d in plan]
+            tb = [time_part(A, fmt, d, x, a.reps) for d in plan]
+            tp = [t for t, _ in tb]
+            ab = [b for _, b in tb]
             tc = max(tp)
             if p == 1:
                 t1 = tc
@@ -88,6 +91,10 @@ def main():
                 ex_repl = (LAT + (1 - 1 / p) * m * 8 / BW_NVLINK) if p > 1 else 0.0
             out = {"workload": f"{cfg}_{fmt}_f64_m{A['m']}_n{A['n']}_nnz{A.nnz}", "p": p,
                    "part_ms": tp, "t_comp_ms": tc, "imbalance_max_over_mean": tc / (sum(tp) / p),
+                   # the nnz split balances nonzeros, not bytes: each part's algorithmic bytes (beta = 0:
+                   # matrix + x entries + its y rows) and the rate it streams them at
+                   "part_alg_bytes": ab, "bytes_max_over_mean": max(ab) / (sum(ab) / p),
+                   "part_GBps": [b / (t * 1e-3) / 1e9 if t > 0 else 0.0 for t, b in tb],
                    "E_comp": t1 / (p * tc),
                    "exchange_model_ms": {"owned": None if ex_owned is None else ex_owned * 1e3,
                                          "replicated": ex_repl * 1e3},
