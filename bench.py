@@ -53,11 +53,16 @@ def parse(argv=None):
     p.add_argument("--e2e-steps", type=int, default=50)
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--kernel-times", type=int, default=0, metavar="STEPS",
+                   help="after the timed region, profile STEPS SpMVs with torch.profiler (CUPTI) and report "
+                        "the average device time of every kernel per SpMV (kernel_times_us)")
     p.add_argument("--parts-per-rank", type=int, default=1)
     p.add_argument("--hot-x", type=int, default=-1,
                    help="MSREP_TUNE_HOT_X: shared-memory hot-x cache (-1 auto, 0 off, 1 on, k > 1: k KiB)")
     p.add_argument("--compact-x", type=int, default=-1, choices=[-1, 0, 1, 2],
                    help="MSREP_TUNE_COMPACT_X: gather the rank's distinct x entries first (-1 auto, 0 off, 1 on)")
+    p.add_argument("--sell", type=int, default=None, choices=[0, 1, 2],
+                   help="MSREP_TUNE_SELL: 0 SEG tiles only, 1 SELL tiles with 32-bit ids, 2 + narrow SELL tiles")
     p.add_argument("--hot-cluster", type=int, default=1, choices=[1, 2],
                    help="MSREP_TUNE_HOT_CLUSTER: CTAs sharing one hot-x cache over DSMEM")
     p.add_argument("--col-layout", type=int, default=-1, choices=[-1, 0, 1],
@@ -373,6 +378,8 @@ def main():
     ctx.set_tuning("xload", a.xload)
     ctx.set_tuning("compact_x", a.compact_x)
     ctx.set_tuning("hot_cluster", a.hot_cluster)
+    if a.sell is not None:
+        ctx.set_tuning("sell", a.sell)
     ctx.set_tuning("col_layout", a.col_layout)
     local_gen = rank_local_ok(a)
     A = None
@@ -445,6 +452,23 @@ def main():
     step_ms = ms_max / a.steps
     flops = 2.0 * nnz
     value = flops / (step_ms * 1e-3) / 1e9
+
+    # per-kernel device time of one SpMV in a warm, back-to-back run (not cold-cache like ncu):
+    # the split of the step between the tile kernel, the compact-x gather and the fix-up
+    ktimes = None
+    if a.kernel_times > 0 and rank == 0:
+        from torch.profiler import profile, ProfilerActivity
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            for _ in range(a.kernel_times):
+                step()
+            torch.cuda.synchronize()
+        acc = {}
+        for ev in prof.events():
+            if ev.device_type.name == "CUDA" and ev.device_time > 0:
+                nm = ev.name.split("<")[0].split("::")[-1].replace("void ", "").strip() or ev.name[:60]
+                acc[nm] = acc.get(nm, 0.0) + ev.device_time
+        ktimes = {k: v / a.kernel_times for k, v in sorted(acc.items(), key=lambda kv: -kv[1])}
+        barrier()
 
     # N > 1: the other layout of the format timed the same way (OWNED for the row formats,
     # SHARDED for the column formats: no allgather), merge share and NVLink bytes per rank
@@ -520,9 +544,11 @@ def main():
     except Exception:
         traffic = None
     alg_bytes, stream_bytes = st["alg_bytes"], st["stream_bytes"]
-    # pCOO: the 4-B row ids of its algorithmic count are never streamed (the tiles carry u8 keys),
-    # so the roofline counts the smaller of the two
-    roof_bytes = min(alg_bytes, stream_bytes) if a.format == "coo" else alg_bytes
+    # the roofline counts the smaller of the algorithmic bytes and the bytes the built layout
+    # streams: pCOO's 4-B row ids are never streamed (the tiles carry u8 keys), narrow SELL tiles
+    # carry 2-B column offsets instead of 4-B ids -- a compressed layout is
+    # judged against the bytes it really moves, never credited with bytes it skips
+    roof_bytes = min(alg_bytes, stream_bytes)
     achieved = roof_bytes / (kern_avg_ms * 1e-3) / 1e9
     step_gbs = alg_bytes / (step_ms * 1e-3) / 1e9
 
@@ -552,7 +578,8 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic, "kernel": kname,
                          "kernel_avg_ms": kern_avg_ms, "alg_bytes_per_launch": alg_bytes,
-                         "bytes_counted": "min(alg, stream)" if a.format == "coo" else "alg",
+                         "bytes_counted": "stream" if stream_bytes < alg_bytes else "alg",
+                         "stream_bytes_per_launch": stream_bytes,
                          "frac_of_8TBps": achieved / 8000.0,
                          "peak_kind": peak_kind + " (MEASURED_PEAKS.json hbm_gbs, a copy)" if peak_kind == "measured"
                          else peak_kind},
@@ -564,6 +591,7 @@ def main():
                                 "note": "one x gather per nonzero (the hot-x share is served from shared memory); "
                                         "binds for random column patterns (R-MAT, tall-skinny)"},
             "layouts": per_layout,
+            "kernel_times_us": ktimes,
             "nvlink": nv,
             "nccl": {"nranks": world, "version": ".".join(map(str, torch.cuda.nccl.version())),
                      "init_log": "stderr (NCCL_DEBUG=INFO, NCCL_DEBUG_SUBSYS=INIT)"} if world > 1 else None,
@@ -575,7 +603,7 @@ def main():
             "partition_ms": st["partition_ms"],
             "partition_phase_ms": dict(zip(("validate", "plan", "schedule", "upload_pack"), list(st["phase_ms"]))),
             "layout_build_ms": list(st["layout_ms"]),
-            "stats_rank0": {k: st[k] for k in ("nnz_rank", "ntiles", "nsell", "nslabs", "nsplit_rows",
+            "stats_rank0": {k: st[k] for k in ("nnz_rank", "ntiles", "nsell", "nsell_narrow", "nslabs", "nsplit_rows",
                                                "distinct_cols", "kernels_per_spmv", "tile_bytes", "x_no_allocate",
                                                "nhot", "hot_nnz", "x_compact", "x_order", "col_layout")},
         }

@@ -34,7 +34,7 @@ STATUS = {0: "MSREP_OK", 1: "MSREP_ERR_INVALID_ARG", 2: "MSREP_ERR_DIM_MISMATCH"
           4: "MSREP_ERR_TOO_LARGE", 5: "MSREP_ERR_STATE", 6: "MSREP_ERR_OOM", 7: "MSREP_ERR_CUDA",
           8: "MSREP_ERR_NCCL"}
 FORMATS = {"csr": CSR, "csc": CSC, "coo": COO, "coo_col": COO_COL, "coo_unsorted": COO_UNSORTED}
-TUNE_XLOAD, TUNE_CG_GRAPH, TUNE_HOT_X, TUNE_COMPACT_X, TUNE_HOT_CLUSTER, TUNE_SELL, TUNE_COL_LAYOUT = 0, 1, 2, 3, 4, 5, 6
+TUNE_XLOAD, TUNE_CG_GRAPH, TUNE_HOT_X, TUNE_COMPACT_X, TUNE_HOT_CLUSTER, TUNE_SELL, TUNE_COL_LAYOUT = range(7)
 TUNING = {"xload": TUNE_XLOAD, "cg_graph": TUNE_CG_GRAPH, "hot_x": TUNE_HOT_X, "compact_x": TUNE_COMPACT_X,
           "hot_cluster": TUNE_HOT_CLUSTER, "sell": TUNE_SELL, "col_layout": TUNE_COL_LAYOUT}
 
@@ -63,7 +63,8 @@ class Stats(ctypes.Structure):
                                          ("sell_1cta", ctypes.c_int64),
                                          ("gpu_numa_node", ctypes.c_int64), ("host_numa_node", ctypes.c_int64),
                                          ("stream_bytes", ctypes.c_int64), ("col_layout", ctypes.c_int64),
-                                         ("layout_ms", ctypes.c_double * 6), ("x_order", ctypes.c_int64)]
+                                         ("layout_ms", ctypes.c_double * 6), ("x_order", ctypes.c_int64),
+                                         ("nsell_narrow", ctypes.c_int64)]
 
 
 class Allocator(ctypes.Structure):

@@ -390,12 +390,14 @@ struct Ctx {
   int x_order = 0;                  // compact x order: 0 column, 1 decreasing degree
   int hot_cluster = 1;              // the partition's hot-x sharing (tune_hot_cluster when built)
   int32_t* d_xcols = nullptr;       // the rank's distinct columns, ascending (compact x -> column)
+  int32_t* d_xpos = nullptr;        // degree-ordered x': x' row of d_xcols[i] (NULL: row i)
   void* d_xc = nullptr;             // x' = x[d_xcols], gathered at the start of every SpMV
   void* d_xc_mm = nullptr;          // SpMM: X' (nxc x 8 entries), allocated on first use
   void* d_mm_planar = nullptr;      // SpMM on the column formats: planar X and Y (k <= 8)
   size_t mm_planar_bytes = 0;
   int tune_compact = -1;
-  int tune_sell = 1;                // SELL tiles for regular rows (0: SEG tiles only)
+  int64_t nsell_narrow = 0;         // narrow SELL tiles (16-bit column offsets)
+  int tune_sell = 2;                // SELL tiles for regular rows (0: SEG tiles only, 1: 32-bit ids only, 2: + narrow)
   int tune_hot_cluster = 1;         // CTAs of a cluster sharing one hot-x cache over DSMEM (1 or 2)
   bool split_launch = false;        // SELL tiles and SEG tiles run as two launches (each >= 5-10 % of nnz)
   int residency = MSREP_RESIDENT_DEVICE;
@@ -495,6 +497,7 @@ void free_all(Ctx* c) {
   c->hot_nnz = 0;
   c->nxc = 0;
   c->d_xcols = nullptr;
+  c->d_xpos = nullptr;
   c->d_xc = c->d_xc_mm = nullptr;
   c->d_mm_planar = nullptr;
   c->mm_planar_bytes = 0;
@@ -575,8 +578,10 @@ struct Packer {
   const std::vector<int64_t>& lp;   // local pointer over the window (rank-local nonzeros)
   int64_t cur_r0 = -1, cur_r1 = -1;
   const int64_t tnz;                // nonzeros per SEG tile / slab for this value size
-  explicit Packer(Schedule& s, int64_t w, const std::vector<int64_t>& l, int vsize)
-      : S(s), wlo(w), lp(l), tnz(tile_nnz(vsize)) {}
+  const int32_t* lidx;              // rank-local column ids (host), NULL: no narrow SELL tiles
+  const int wn;                     // R * W limit of a narrow SELL tile
+  explicit Packer(Schedule& s, int64_t w, const std::vector<int64_t>& l, int vsize, const int32_t* li = nullptr)
+      : S(s), wlo(w), lp(l), tnz(tile_nnz(vsize)), lidx(li), wn(selln_w_max(vsize)) {}
   int64_t ls(int64_t r) const { return lp[(size_t)(r - wlo)]; }
   int64_t le(int64_t r) const { return lp[(size_t)(r - wlo + 1)]; }
   void flush() {
@@ -596,9 +601,12 @@ struct Packer {
     if (cur_r0 < 0) { cur_r0 = r; cur_r1 = r; }
     cur_r1 = r + 1;
   }
-  // SELL tile for rows [r, r + 32R) (R rows per lane, R*W <= SELL_W_MAX, whole owned rows < rend)
-  // if padding to the longest row is <= 1/8 of the stored elements; tries R = 4, 2, 1.
+  // SELL tile for rows [r, r + 32R) (R rows per lane, whole owned rows < rend) if padding to the
+  // longest row is <= 1/8 of the stored elements; tries R = 4, 2, 1.  Narrow (16-bit column
+  // offsets, R*W <= wn) when every column of the rows lies within 65535 of the smallest, else
+  // R*W <= SELL_W_MAX with 32-bit ids.
   int64_t try_sell(int64_t r, int64_t rend) {
+    const int lim = lidx ? std::max(wn, SELL_W_MAX) : SELL_W_MAX;
     for (int R = SELL_R_MAX; R >= 1; R >>= 1) {
       const int64_t e = std::min<int64_t>(r + 32 * R, rend);
       if (R > 1 && e - r <= 32 * (R / 2)) continue;   // a smaller R covers these rows
@@ -606,13 +614,23 @@ struct Packer {
       bool ok = true;
       for (int64_t q = r; q < e && ok; q++) {
         const int64_t len = le(q) - ls(q);
-        if (len * R > SELL_W_MAX) ok = false;
+        if (len * R > lim) ok = false;
         W = std::max(W, len);
         sum += len;
       }
       if (!ok || W == 0 || 8 * sum < 7 * W * (e - r)) continue;
+      bool narrow = false;
+      if (lidx && W * R <= wn) {
+        int32_t lo = INT32_MAX, hi = INT32_MIN;
+        for (int64_t z = ls(r); z < le(e - 1); z++) {
+          lo = std::min(lo, lidx[z]);
+          hi = std::max(hi, lidx[z]);
+        }
+        narrow = (int64_t)hi - (int64_t)lo <= 65535;
+      }
+      if (!narrow && W * R > SELL_W_MAX) continue;
       flush();
-      S.sell.push_back({(int32_t)(r - wlo), (int32_t)ls(r), (int32_t)((e - r) | (W << 16)), -2});
+      S.sell.push_back({(int32_t)(r - wlo), (int32_t)ls(r), (int32_t)((e - r) | (W << 16)), narrow ? -3 : -2});
       return e;
     }
     return -1;
@@ -668,8 +686,9 @@ void rank_segments(msrep_format fmt, int64_t m, int nranks, int vparts, const st
 // slab-split rows), and the tail row (owned, continues into later parts) as
 // slabs whose fix-up adds the head partials of the parts that continue it.
 void build_row_schedule(const std::vector<msrep_part_desc>& P, int P0, int P1, int64_t B_lo, int64_t wlo, int V,
-                        const std::vector<int64_t>& lp, Schedule& S, bool allow_sell = true) {
-  Packer pk(S, wlo, lp, V);
+                        const std::vector<int64_t>& lp, Schedule& S, bool allow_sell = true,
+                        const int32_t* lidx = nullptr) {
+  Packer pk(S, wlo, lp, V, lidx);
   for (int j = P0; j < P1; j++) {
     const msrep_part_desc& d = P[(size_t)j];
     const bool empty = d.start_idx > d.end_idx;
@@ -1353,7 +1372,7 @@ msrep_status_t prepare_x(Ctx* c, const void* x, int k, cudaStream_t s) {
     dst = c->d_xc_mm;
   }
   CUDA_TRY(launch_gather_x(static_cast<const char*>(x) + (size_t)c->xoff * k * vsz(c->dtype), c->d_xcols, c->nxc, k, dst,
-                           c->dtype == MSREP_F64 ? 0 : 1, s));
+                           c->dtype == MSREP_F64 ? 0 : 1, s, c->d_xpos));
   return MSREP_OK;
 }
 ColLaunch col_launch(const Ctx* c, const void* x, void* y, double alpha, double beta) {
@@ -1600,7 +1619,7 @@ msrep_status_t msrep_set_tuning(msrep_ctx h, msrep_tuning knob, int value) {
       c->tune_hot_cluster = value;
       return MSREP_OK;
     case MSREP_TUNE_SELL:
-      if (value < 0 || value > 1) return fail(MSREP_ERR_INVALID_ARG, "MSREP_TUNE_SELL %d (0, 1)", value);
+      if (value < 0 || value > 2) return fail(MSREP_ERR_INVALID_ARG, "MSREP_TUNE_SELL %d (0, 1, 2)", value);
       c->tune_sell = value;
       return MSREP_OK;
     case MSREP_TUNE_COL_LAYOUT:
@@ -2079,7 +2098,9 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     Schedule S;
     auto schedule = [&](bool sell) {
       if (!tr) {
-        build_row_schedule(c->parts, c->P0, c->P1, c->B_lo, c->wlo, (int)V, LP, S, sell);
+        // narrow SELL tiles (16-bit column offsets) from the host's column ids (MSREP_TUNE_SELL 2)
+        build_row_schedule(c->parts, c->P0, c->P1, c->B_lo, c->wlo, (int)V, LP, S, sell,
+                           c->tune_sell == 2 ? idx + c->B_lo : nullptr);
         return;
       }
       // one part of its own with no shared rows: rows cut into fixed chunks of 2^18 (the cut never
@@ -2134,14 +2155,19 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
         schedule(false);
         sell_nz = 0;
       }
-      // ... and when SEG tiles hold a real share too, they get their own launch of the SEG
-      // instantiation instead of riding in the SELL one
-      c->split_launch = !S.sell.empty() && (nz_r - sell_nz) * 20 >= nz_r;
+      // ... and SEG / slab tiles get their own launch of the SEG instantiation (forked onto a side
+      // stream) when they hold >= 5 % of the nonzeros, and always for fp32 (whose SELL
+      // instantiation walks SELL tiles only); a small fp64 share rides in the SELL launch (a
+      // second launch put its CTAs in the first one's tail: stencil 0.0914 -> 0.0953 ms)
+      c->split_launch = !S.sell.empty() && !S.tiles.empty() && (V == 4 || (nz_r - sell_nz) * 20 >= nz_r);
     }
     sub(1);
     lap(2);
     c->ntiles = (int)(S.tiles.size() + S.sell.size());
     c->nsell = (int)S.sell.size();
+    int64_t nsell_narrow = 0;
+    for (const TileHost& t : S.sell) nsell_narrow += t.rec == -3 ? 1 : 0;
+    c->nsell_narrow = nsell_narrow;
     c->nslabs = S.nslabs;
     c->nrec = S.nrec;
     c->nsplit = (int)S.sr_row.size();
@@ -2154,7 +2180,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     int64_t blob_total = 0;
     for (size_t t = 0; t < nt; t++) {
       const TileHost& th = S.tiles[t];
-      const int kind = th.rec == -2 ? KIND_SELL : th.rec >= 0 ? KIND_SLAB : KIND_SEG;
+      const int kind = th.rec == -2 ? KIND_SELL : th.rec == -3 ? KIND_SELLN : th.rec >= 0 ? KIND_SLAB : KIND_SEG;
       if (blob_total / 16 >= (int64_t)1 << 31) return fail(MSREP_ERR_TOO_LARGE, "tile blob exceeds 32 GiB");
       blob16[t] = (int32_t)(blob_total / 16);
       blob_total += blob_bytes(kind, th.packed & 0xffff, th.packed >> 16, (int)V);
@@ -2168,7 +2194,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
       auto tile_end = [&](size_t t) { return t + 1 < nt ? (int64_t)blob16[t + 1] * 16 : blob_total; };
       auto zspan = [&](const TileHost& th, int64_t& z0, int64_t& z1) {
         z0 = th.nz0;
-        z1 = th.rec == -2 ? LP[(size_t)th.row0 + (size_t)(th.packed & 0xffff)] : th.nz0 + (th.packed >> 16);
+        z1 = (th.rec == -2 || th.rec == -3) ? LP[(size_t)th.row0 + (size_t)(th.packed & 0xffff)] : th.nz0 + (th.packed >> 16);
       };
       const int64_t cap = host_res ? c->chunk_bytes : INT64_MAX;
       size_t t = 0;
@@ -2186,7 +2212,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
         g.t1 = (int32_t)t;
         groups.push_back(g);
         if (host_res) {
-          Ctx::Chunk ch{g.t0, g.t1, 0, 0, off0, tile_end(t - 1) - off0, S.tiles[(size_t)g.t0].rec == -2};
+          Ctx::Chunk ch{g.t0, g.t1, 0, 0, off0, tile_end(t - 1) - off0, S.tiles[(size_t)g.t0].rec == -2 || S.tiles[(size_t)g.t0].rec == -3};
           c->chunks.push_back(ch);
         }
       }
@@ -2239,7 +2265,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     //    an x' that fits in L2 next to the matrix stream instead of the whole x;
     //  * hot x: the most-gathered columns get slots in a shared-memory copy of x' per CTA; SEG / slab
     //    tiles carry HOT_TAG | slot for them (the SELL instantiation has no hot path).
-    std::vector<int32_t> hot, xcols;
+    std::vector<int32_t> hot, xcols, xcols_col;
     int32_t *d_hotslot = nullptr, *d_colmap = nullptr, *dp_hot_tmp = nullptr;
     bool idx_up = false;
     c->nhot = 0;
@@ -2293,14 +2319,17 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
           for (int32_t q : xcols) heavy += deg[(size_t)q] >= thr ? deg[(size_t)q] : 0;
           skewed = heavy * 5 >= nz_r;
         }
-        const int mode = c->tune_compact >= 1 ? c->tune_compact
-                         : skewed ? 2 : ((int64_t)xcols.size() * 4 <= (int64_t)nx * 3 ? 1 : 0);
+        int mode = c->tune_compact >= 1 ? c->tune_compact
+                   : skewed ? 2 : ((int64_t)xcols.size() * 4 <= (int64_t)nx * 3 ? 1 : 0);
+        // narrow SELL tiles need the column order (their 16-bit offsets were checked on column ids)
+        if (mode == 2 && nsell_narrow > 0) mode = 1;
         if (mode >= 1) {
           TRY(dalloc(c, (size_t)nx * 4, &dp, s));
           d_colmap = static_cast<int32_t*>(dp);   // column -> compact id (filled from the kept list below)
           c->nxc = (int64_t)xcols.size();
           c->x_order = mode == 2 ? 1 : 0;
           if (mode == 2) {   // degree order: the most-gathered columns share the first lines of x'
+            xcols_col = xcols;   // the gather of x' reads x in column order (gather_x_kernel pos)
             // stable by column within a degree: columns of degree >= 2^16 (few) sorted, the rest
             // counting-sorted by degree (descending)
             constexpr int32_t CAP = 1 << 16;
@@ -2361,8 +2390,23 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     sub(2);
     const size_t keep_from = c->bufs.size();
     c->d_xcols = nullptr;
+    c->d_xpos = nullptr;
     c->d_xc = nullptr;
-    if (c->nxc) {
+    if (c->nxc && c->x_order == 1) {
+      // degree order: x' row pos[i] holds column xcols_col[i] (ascending), colmap[col] = its x' row
+      std::vector<int32_t> pos(xcols_col.size());
+      {
+        std::vector<int32_t> at((size_t)nx);
+        for (size_t i = 0; i < xcols_col.size(); i++) at[(size_t)xcols_col[i]] = (int32_t)i;
+        for (size_t k2 = 0; k2 < xcols.size(); k2++) pos[(size_t)at[(size_t)xcols[k2]]] = (int32_t)k2;
+      }
+      TRY(upload_vec(c, xcols_col, &c->d_xcols, s));
+      TRY(upload_vec(c, pos, &c->d_xpos, s));
+      CUDA_TRY(launch_hot_slots(c->d_xcols, (int)c->nxc, d_colmap, s, c->d_xpos));   // colmap[xcols_col[i]] = pos[i]
+      void* q;
+      TRY(dalloc(c, (size_t)c->nxc * V, &q, s));
+      c->d_xc = q;
+    } else if (c->nxc) {
       TRY(upload_vec(c, xcols, &c->d_xcols, s));
       CUDA_TRY(launch_hot_slots(c->d_xcols, (int)c->nxc, d_colmap, s));   // colmap[xcols[k]] = k
       void* q;
@@ -2474,7 +2518,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   st.nnz_rank = nz_r;
   st.rows_window = W;
   const bool bands = colwise(fmt) && !c->col_rows;
-  st.ntiles = bands ? c->citems : c->ntiles; st.nsell = c->nsell; st.nslabs = c->nslabs; st.nsplit_rows = c->nsplit; st.nheads_local = c->nheads_local;
+  st.ntiles = bands ? c->citems : c->ntiles; st.nsell = c->nsell; st.nsell_narrow = bands ? 0 : c->nsell_narrow; st.nslabs = c->nslabs; st.nsplit_rows = c->nsplit; st.nheads_local = c->nheads_local;
   st.partition_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
   for (int k = 0; k < 4; k++) st.phase_ms[k] = phase[k];
   st.residency = c->residency;
@@ -2528,12 +2572,13 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   st.alg_bytes = base + ybytes_b1;
   st.alg_bytes_beta0 = base + ybytes_b0;
   const int64_t nmain = c->chunks.empty() ? 1 : (int64_t)c->chunks.size();   // main-kernel launches
+  const bool fixl = c->nsplit > 0;                                            // a fix-up launch per SpMV
   if (bands)
     st.kernels_per_spmv = (c->cunits ? nmain : 0) + (c->nranks > 1 ? 1 /*shard epilogue*/ : 0);
   else if (colwise(fmt))
-    st.kernels_per_spmv = (c->ntiles ? nmain + (c->split_launch && c->chunks.empty() ? 1 : 0) : 0) + (c->nsplit ? 1 : 0) +
+    st.kernels_per_spmv = (c->ntiles ? nmain + (c->split_launch && c->chunks.empty() ? 1 : 0) : 0) + (fixl ? 1 : 0) +
                           (c->nxc ? 1 : 0) + (c->nranks > 1 ? 1 /*shard epilogue*/ : 0);
-  else st.kernels_per_spmv = (c->ntiles ? nmain + (c->split_launch && c->chunks.empty() ? 1 : 0) : 0) + (c->nranks > 1 && c->any_flag ? 1 : 0) + (c->nsplit ? 1 : 0) + (c->nxc ? 1 : 0);
+  else st.kernels_per_spmv = (c->ntiles ? nmain + (c->split_launch && c->chunks.empty() ? 1 : 0) : 0) + (c->nranks > 1 && c->any_flag ? 1 : 0) + (fixl ? 1 : 0) + (c->nxc ? 1 : 0);
   int64_t db = 0;
   for (auto& b : c->bufs) db += (int64_t)b.bytes;
   st.device_bytes = db;

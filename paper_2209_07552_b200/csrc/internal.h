@@ -68,9 +68,15 @@ constexpr int HOT_AUTO_BYTES = MSREP_HOT_AUTO_KB * 1024;
 //   kernel); aux = the 32*R row lengths (uint16, lane-fastest).  R > 1 keeps
 //   tiles of short regular rows big (~1000 elements).  The host only forms a
 //   SELL tile when padding is <= 1/8 of its elements.
-enum TileKind { KIND_SEG = 0, KIND_SLAB = 2, KIND_SELL = 3 };
+enum TileKind { KIND_SEG = 0, KIND_SLAB = 2, KIND_SELL = 3, KIND_SELLN = 4 };
 constexpr int SELL_ROWS = 32;
 constexpr int SELL_W_MAX = 32;    // R * W per lane
+// Narrow SELL tile (KIND_SELLN, descriptor w = -3): the same sliced-ELL geometry, but the column
+// ids are 16-bit offsets from a per-tile base (every column of the tile within 65535 of the
+// smallest one -- banded / stencil rows): [base u32, 12 B pad][lens][val][off u16].  An element
+// costs V + 2 bytes instead of V + 4, so the fp32 tiles may hold R * W <= 64 per lane (64 rows of
+// a 27-point stencil, the bytes of an fp64 tile).
+__host__ __device__ constexpr int selln_w_max(int vsize) { return vsize == 4 ? 64 : 32; }
 constexpr int SELL_R_MAX = 4;
 __host__ __device__ inline int align16(int b) { return (b + 15) & ~15; }
 // rows per lane of a SELL tile of `nrows` rows (1, 2 or 4)
@@ -82,13 +88,19 @@ __host__ __device__ inline int seg_key_bytes(int nnz) {
   return 128 * ((npos + 3) >> 2);
 }
 __host__ __device__ inline int blob_aux_bytes(int kind, int nrows, int nnz) {
-  return kind == KIND_SEG ? seg_key_bytes(nnz) : (kind == KIND_SELL ? align16(sell_r(nrows) * 32 * 2) : 0);
+  return kind == KIND_SEG ? seg_key_bytes(nnz)
+                          : (kind == KIND_SELL ? align16(sell_r(nrows) * 32 * 2)
+                                               : (kind == KIND_SELLN ? 16 + align16(sell_r(nrows) * 32 * 2) : 0));
 }
-// for KIND_SELL, `nnz` is the slice width W
+// for KIND_SELL / KIND_SELLN, `nnz` is the slice width W
 __host__ __device__ inline int blob_bytes(int kind, int nrows, int nnz, int vsize) {
   if (kind == KIND_SELL) {
     const int r32 = sell_r(nrows) * 32;
     return align16(r32 * 2) + nnz * r32 * (vsize + 4);
+  }
+  if (kind == KIND_SELLN) {
+    const int r32 = sell_r(nrows) * 32;
+    return 16 + align16(r32 * 2) + nnz * r32 * vsize + align16(nnz * r32 * 2);
   }
   return blob_aux_bytes(kind, nrows, nnz) + align16(nnz * vsize) + align16(nnz * 4);
 }
@@ -113,7 +125,7 @@ __host__ __device__ inline int seg_key_off(int e, int nnz) {
 
 // int4 tile descriptor: x = first row, window-local; y = blob offset in
 // 16-byte units; z = nrows | (nnz << 16) (SELL: nrows | (W << 16)); w = kind
-// of work (>= 0: slab record index; -1: SEG tile; -4: SEG tile without empty rows; -2: SELL).
+// of work (>= 0: slab record index; -1: SEG tile; -4: SEG tile without empty rows; -2: SELL; -3: narrow SELL).
 constexpr int KIND_W_SEG_DENSE = -4;
 struct TileHost { int32_t row0, nz0, packed, rec; };
 
@@ -247,9 +259,11 @@ cudaError_t launch_sum_peers(const SumLaunch& L, cudaStream_t s);
 cudaError_t launch_planar(const void* src, void* dst, int64_t r0, int64_t r1, int k, int64_t ld, int to_planar,
                           int dtype, cudaStream_t s);
 cudaError_t launch_col_degree(const int32_t* idx, int64_t nz, int32_t* deg, cudaStream_t s);   // deg[idx[i]]++
-cudaError_t launch_hot_slots(const int32_t* hot, int nhot, int32_t* slot, cudaStream_t s);      // slot[hot[k]] = k
+cudaError_t launch_hot_slots(const int32_t* hot, int nhot, int32_t* slot, cudaStream_t s,
+                             const int32_t* val = nullptr);   // slot[hot[k]] = val ? val[k] : k
 // out[i*k + j] = x[cols[i]*k + j], i < n, j < k (compact x for SpMV k = 1, SpMM k > 1)
-cudaError_t launch_gather_x(const void* x, const int32_t* cols, int64_t n, int k, void* out, int dtype, cudaStream_t s);
+cudaError_t launch_gather_x(const void* x, const int32_t* cols, int64_t n, int k, void* out, int dtype, cudaStream_t s,
+                            const int32_t* pos = nullptr);   // out[pos ? pos[i] : i] = x[cols[i]]
 // transpose.cu: a column-format slice of n entries -> the rank-local row-major slice (stable by
 // slice position within a row).  rows = row of each entry (input, also the first pass's keys);
 // key_a/key_b/perm_a/perm_b: [n] each; scratch: transpose_scratch_words(n) words;

@@ -44,6 +44,12 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// Programmatic dependent launch (the SpMV's kernel chain gather_x -> rows -> fix-up): a kernel
+// launched with programmatic stream serialisation runs its prologue while its predecessor drains
+// and waits here before touching anything the predecessor writes; launch_dependents lets the
+// next kernel of the chain be scheduled early (a no-op without a dependent)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)), "r"(bytes) : "memory");
 }
@@ -152,7 +158,9 @@ __device__ __forceinline__ void warp_seg_scan(int key, double val, int& pk, doub
   pv = lane == 0 ? 0.0 : ev;
 }
 
-__device__ __forceinline__ int tile_kind(int4 d) { return d.w >= 0 ? KIND_SLAB : (d.w == -2 ? KIND_SELL : KIND_SEG); }
+__device__ __forceinline__ int tile_kind(int4 d) {
+  return d.w >= 0 ? KIND_SLAB : (d.w == -2 ? KIND_SELL : (d.w == -3 ? KIND_SELLN : KIND_SEG));
+}
 
 __device__ __forceinline__ void issue_blob(const char* blob, int4 d, int kind, int vsize, unsigned char* st,
                                            uint64_t* bar, uint64_t pol) {
@@ -183,7 +191,12 @@ __device__ __forceinline__ void issue_blob(const char* blob, int4 d, int kind, i
 #define MSREP_ROW_MINB 2
 #endif
 template <typename VT>
-struct SStage { static constexpr int BYTES = SELL_R_MAX * 32 * 2 + SELL_W_MAX * SELL_ROWS * ((int)sizeof(VT) + 4); };
+struct SStage {   // the larger of a full 32-bit-id SELL tile and a full narrow one
+  static constexpr int V = (int)sizeof(VT);
+  static constexpr int WIDE = SELL_R_MAX * 32 * 2 + SELL_W_MAX * SELL_ROWS * (V + 4);
+  static constexpr int NARROW = 16 + SELL_R_MAX * 32 * 2 + selln_w_max(V) * SELL_ROWS * (V + 2);
+  static constexpr int BYTES = WIDE > NARROW ? WIDE : NARROW;
+};
 template <typename VT, bool SELL, bool HOT = false>
 using RowLayout = WLayout<(SELL && SStage<VT>::BYTES > RStage<VT>::BYTES) ? SStage<VT>::BYTES : RStage<VT>::BYTES, 1,
                           MAX_TILE_ROWS * 8, HOT ? HOT_WARPS : WARPS>;
@@ -195,40 +208,87 @@ using RowLayout = WLayout<(SELL && SStage<VT>::BYTES > RStage<VT>::BYTES) ? SSta
 // hot-x address of slot s: the slots are spread over the CL CTAs of the cluster, hpc per CTA; hb[r]
 // is CTA r's cache base in the shared::cluster window (CL == 1: the CTA's own shared memory)
 struct HotRef { uint32_t hb0, hb1, hpc; };
-template <bool NA>
-__device__ __forceinline__ double ldx_sel(const double* x, const HotRef& h, uint32_t c, uint64_t pol) {
+// x[off] from a base pointer with the address formed inside the asm (keeps ptxas from holding a
+// 64-bit address per in-flight gather: the narrow SELL tiles keep up to 64 gathers in flight)
+__device__ __forceinline__ double ldg_off(const double* xb, uint32_t off) {
   double v;
-  if constexpr (NA) asm("{\n\t.reg .pred p, q;\n\t.reg .u32 ci, sa, hb;\n\t.reg .u64 ga;\n\t"
-                        "setp.lt.s32 p, %1, 0;\n\tand.b32 ci, %1, 0x7fffffff;\n\tsetp.ge.u32 q, ci, %4;\n\t"
-                        "selp.b32 hb, %3, %2, q;\n\t@q sub.u32 ci, ci, %4;\n\tmad.lo.u32 sa, ci, 8, hb;\n\t"
-                        "mad.wide.u32 ga, %1, 8, %5;\n\t@p ld.shared::cluster.f64 %0, [sa];\n\t"
-                        "@!p ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [ga], %6;\n\t}"
-                        : "=d"(v) : "r"(c), "r"(h.hb0), "r"(h.hb1), "r"(h.hpc), "l"(x), "l"(pol));
-  else asm("{\n\t.reg .pred p, q;\n\t.reg .u32 ci, sa, hb;\n\t.reg .u64 ga;\n\t"
-           "setp.lt.s32 p, %1, 0;\n\tand.b32 ci, %1, 0x7fffffff;\n\tsetp.ge.u32 q, ci, %4;\n\t"
-           "selp.b32 hb, %3, %2, q;\n\t@q sub.u32 ci, ci, %4;\n\tmad.lo.u32 sa, ci, 8, hb;\n\t"
-           "mad.wide.u32 ga, %1, 8, %5;\n\t@p ld.shared::cluster.f64 %0, [sa];\n\t"
-           "@!p ld.global.nc.L2::cache_hint.f64 %0, [ga], %6;\n\t}"
-           : "=d"(v) : "r"(c), "r"(h.hb0), "r"(h.hb1), "r"(h.hpc), "l"(x), "l"(pol));
+  asm("{\n\t.reg .u64 ga;\n\tmad.wide.u32 ga, %1, 8, %2;\n\tld.global.nc.f64 %0, [ga];\n\t}" : "=d"(v) : "r"(off), "l"(xb));
+  return v;
+}
+__device__ __forceinline__ float ldg_off(const float* xb, uint32_t off) {
+  float v;
+  asm("{\n\t.reg .u64 ga;\n\tmad.wide.u32 ga, %1, 4, %2;\n\tld.global.nc.f32 %0, [ga];\n\t}" : "=f"(v) : "r"(off), "l"(xb));
+  return v;
+}
+
+// The asm of one hot-aware gather, predicated on `on` (0: no load, the result is 0) so that a
+// tile's gathers are straight-line code without a branch each.  CL == 2: the slots are split over
+// the CTA pair (slot s lives in CTA s / hpc), read through the shared::cluster window.  CL == 1:
+// the CTA's own copy, plain LDS; the slot address c * V + base in 32 bits drops the tag bit.
+#define MSREP_LDX_PAIR(T, R, SZ, Z, COLD)                                                                \
+  asm("{\n\t.reg .pred p, q, g, o;\n\t.reg .u32 ci, sa, hb;\n\t.reg .u64 ga;\n\t"                          \
+      "setp.ne.u32 o, %7, 0;\n\tsetp.lt.and.s32 p, %1, 0, o;\n\tsetp.ge.and.s32 g, %1, 0, o;\n\t"         \
+      "and.b32 ci, %1, 0x7fffffff;\n\tsetp.ge.u32 q, ci, %4;\n\t"                                          \
+      "selp.b32 hb, %3, %2, q;\n\t@q sub.u32 ci, ci, %4;\n\tmad.lo.u32 sa, ci, " SZ ", hb;\n\t"            \
+      "mad.wide.u32 ga, %1, " SZ ", %5;\n\tmov." T " %0, " Z ";\n\t@p ld.shared::cluster." T " %0, [sa];\n\t" \
+      "@g ld.global.nc" COLD ".L2::cache_hint." T " %0, [ga], %6;\n\t}"                                     \
+      : "=" R(v) : "r"(c), "r"(h.hb0), "r"(h.hb1), "r"(h.hpc), "l"(x), "l"(pol), "r"(on))
+#define MSREP_LDX_OWN(T, R, SZ, Z, COLD)                                                                 \
+  asm("{\n\t.reg .pred p, g, o;\n\t.reg .u32 sa;\n\t.reg .u64 ga;\n\t"                                     \
+      "setp.ne.u32 o, %5, 0;\n\tsetp.lt.and.s32 p, %1, 0, o;\n\tsetp.ge.and.s32 g, %1, 0, o;\n\t"         \
+      "mad.lo.u32 sa, %1, " SZ ", %2;\n\tmad.wide.u32 ga, %1, " SZ ", %3;\n\tmov." T " %0, " Z ";\n\t"     \
+      "@p ld.shared." T " %0, [sa];\n\t@g ld.global.nc" COLD ".L2::cache_hint." T " %0, [ga], %4;\n\t}"   \
+      : "=" R(v) : "r"(c), "r"(h.hb0), "l"(x), "l"(pol), "r"(on))
+#define MSREP_LDX_COLD(T, R, SZ, Z, COLD)                                                                \
+  asm("{\n\t.reg .pred o;\n\t.reg .u64 ga;\n\tsetp.ne.u32 o, %4, 0;\n\tmad.wide.u32 ga, %1, " SZ ", %2;\n\t" \
+      "mov." T " %0, " Z ";\n\t@o ld.global.nc" COLD ".L2::cache_hint." T " %0, [ga], %3;\n\t}"           \
+      : "=" R(v) : "r"(c), "l"(x), "l"(pol), "r"(on))
+#define MSREP_Z64 "0d0000000000000000"
+#define MSREP_Z32 "0f00000000"
+template <bool NA, int CL>
+__device__ __forceinline__ double ldx_sel(const double* x, const HotRef& h, uint32_t c, uint64_t pol, uint32_t on) {
+  double v;
+  if constexpr (CL == 2) {
+    if constexpr (NA) MSREP_LDX_PAIR("f64", "d", "8", MSREP_Z64, ".L1::no_allocate");
+    else MSREP_LDX_PAIR("f64", "d", "8", MSREP_Z64, "");
+  } else {
+    if constexpr (NA) MSREP_LDX_OWN("f64", "d", "8", MSREP_Z64, ".L1::no_allocate");
+    else MSREP_LDX_OWN("f64", "d", "8", MSREP_Z64, "");
+  }
+  return v;
+}
+template <bool NA, int CL>
+__device__ __forceinline__ float ldx_sel(const float* x, const HotRef& h, uint32_t c, uint64_t pol, uint32_t on) {
+  float v;
+  if constexpr (CL == 2) {
+    if constexpr (NA) MSREP_LDX_PAIR("f32", "f", "4", MSREP_Z32, ".L1::no_allocate");
+    else MSREP_LDX_PAIR("f32", "f", "4", MSREP_Z32, "");
+  } else {
+    if constexpr (NA) MSREP_LDX_OWN("f32", "f", "4", MSREP_Z32, ".L1::no_allocate");
+    else MSREP_LDX_OWN("f32", "f", "4", MSREP_Z32, "");
+  }
+  return v;
+}
+// cold-only gather (no hot cache), predicated like ldx_sel
+template <bool NA>
+__device__ __forceinline__ double ldx_on(const double* x, uint32_t c, uint64_t pol, uint32_t on) {
+  double v;
+  if constexpr (NA) MSREP_LDX_COLD("f64", "d", "8", MSREP_Z64, ".L1::no_allocate");
+  else MSREP_LDX_COLD("f64", "d", "8", MSREP_Z64, "");
   return v;
 }
 template <bool NA>
-__device__ __forceinline__ float ldx_sel(const float* x, const HotRef& h, uint32_t c, uint64_t pol) {
+__device__ __forceinline__ float ldx_on(const float* x, uint32_t c, uint64_t pol, uint32_t on) {
   float v;
-  if constexpr (NA) asm("{\n\t.reg .pred p, q;\n\t.reg .u32 ci, sa, hb;\n\t.reg .u64 ga;\n\t"
-                        "setp.lt.s32 p, %1, 0;\n\tand.b32 ci, %1, 0x7fffffff;\n\tsetp.ge.u32 q, ci, %4;\n\t"
-                        "selp.b32 hb, %3, %2, q;\n\t@q sub.u32 ci, ci, %4;\n\tmad.lo.u32 sa, ci, 4, hb;\n\t"
-                        "mad.wide.u32 ga, %1, 4, %5;\n\t@p ld.shared::cluster.f32 %0, [sa];\n\t"
-                        "@!p ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [ga], %6;\n\t}"
-                        : "=f"(v) : "r"(c), "r"(h.hb0), "r"(h.hb1), "r"(h.hpc), "l"(x), "l"(pol));
-  else asm("{\n\t.reg .pred p, q;\n\t.reg .u32 ci, sa, hb;\n\t.reg .u64 ga;\n\t"
-           "setp.lt.s32 p, %1, 0;\n\tand.b32 ci, %1, 0x7fffffff;\n\tsetp.ge.u32 q, ci, %4;\n\t"
-           "selp.b32 hb, %3, %2, q;\n\t@q sub.u32 ci, ci, %4;\n\tmad.lo.u32 sa, ci, 4, hb;\n\t"
-           "mad.wide.u32 ga, %1, 4, %5;\n\t@p ld.shared::cluster.f32 %0, [sa];\n\t"
-           "@!p ld.global.nc.L2::cache_hint.f32 %0, [ga], %6;\n\t}"
-           : "=f"(v) : "r"(c), "r"(h.hb0), "r"(h.hb1), "r"(h.hpc), "l"(x), "l"(pol));
+  if constexpr (NA) MSREP_LDX_COLD("f32", "f", "4", MSREP_Z32, ".L1::no_allocate");
+  else MSREP_LDX_COLD("f32", "f", "4", MSREP_Z32, "");
   return v;
 }
+#undef MSREP_LDX_PAIR
+#undef MSREP_LDX_OWN
+#undef MSREP_LDX_COLD
+#undef MSREP_Z64
+#undef MSREP_Z32
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -242,25 +302,30 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t a, uint32_t rank) {
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-template <bool HOT, bool NA, typename VT>
-__device__ __forceinline__ VT ldx_hot(const VT* x, const HotRef& hbase, uint32_t c, uint64_t pol) {
-  if constexpr (HOT) return ldx_sel<NA>(x, hbase, c, pol);
-  else return ldx<NA>(x + c, pol);
+// Hot-cache kernels branch around a tile position's gather (the branch is warp-uniform except at
+// the ragged extra position, and the slot / global pair stays 5 instructions); the cold-only
+// kernels predicate it instead (R-MAT fp32: 1.135 -> 1.038 ms; with the hot cache the predicated
+// form was the slower one, 1.085 -> 1.118 ms -- profiles/r2_kernel_ab.txt)
+template <bool HOT, bool NA, int CL, typename VT>
+__device__ __forceinline__ VT ldx_hot(const VT* x, const HotRef& hbase, uint32_t c, uint64_t pol, bool on) {
+  if constexpr (HOT) return on ? ldx_sel<NA, CL>(x, hbase, c, pol, 1u) : VT(0);
+  else return ldx_on<NA>(x, c, pol, on ? 1u : 0u);
 }
 
-// One SELL tile with R rows per lane (internal.h): all R*W column indices are read from the
-// slot, then all R*W x gathers are in flight before the first FMA; padding is masked by the
-// row length, so results equal the plain row sums.
-template <typename VT, int R, bool MIRROR, class Refill>
+// One SELL tile with R rows per lane (internal.h): all R*W x gathers are in flight before the
+// first FMA; padding is masked by the row length, so results equal the plain row sums.  NARROW:
+// the column ids are 16-bit offsets from the tile's base (KIND_SELLN), up to selln_w_max entries
+// per lane, read from the slot just before each gather.
+template <typename VT, int R, bool MIRROR, bool NARROW, class Refill>
 __device__ __forceinline__ void sell_tile(const RowLaunch& P, const int4 d, const unsigned char* st, const int lane,
                                           const VT* __restrict__ x, VT* __restrict__ y, double alpha, double beta,
                                           Refill&& refill) {
   constexpr int V = (int)sizeof(VT);
-  constexpr int U = SELL_W_MAX;              // R*W <= U register slots per lane
+  constexpr int U = NARROW ? selln_w_max(V) : SELL_W_MAX;   // R*W <= U register slots per lane
   const int nrows = d.z & 0xffff, W = d.z >> 16;
-  const uint16_t* lens = reinterpret_cast<const uint16_t*>(st);
-  const VT* sv = reinterpret_cast<const VT*>(st + align16(R * 32 * 2));
-  const uint32_t* sc = reinterpret_cast<const uint32_t*>(st + align16(R * 32 * 2) + W * R * 32 * V);
+  const unsigned char* p = st + (NARROW ? 16 : 0);
+  const uint16_t* lens = reinterpret_cast<const uint16_t*>(p);
+  const VT* sv = reinterpret_cast<const VT*>(p + align16(R * 32 * 2));
   const int RW = R * W;
   int mylen[R];
   double yv[R];
@@ -274,11 +339,19 @@ __device__ __forceinline__ void sell_tile(const RowLaunch& P, const int4 d, cons
   double acc[R];
 #pragma unroll
   for (int k = 0; k < R; k++) acc[k] = 0.0;
-  uint32_t c[U];
+  if constexpr (NARROW) {
+    const uint16_t* so = reinterpret_cast<const uint16_t*>(p + align16(R * 32 * 2) + W * R * 32 * V);
+    const VT* xb = x + *reinterpret_cast<const uint32_t*>(st);
 #pragma unroll
-  for (int u = 0; u < U; u++) c[u] = u < RW ? sc[u * 32 + lane] : 0u;   // no loop-carried state
+    for (int u = 0; u < U; u++) xs[u] = u < RW ? ldg_off(xb, so[u * 32 + lane]) : VT(0);
+  } else {
+    const uint32_t* sc = reinterpret_cast<const uint32_t*>(p + align16(R * 32 * 2) + W * R * 32 * V);
+    uint32_t c[U];
 #pragma unroll
-  for (int u = 0; u < U; u++) xs[u] = u < RW ? ldg_ro(x + c[u]) : VT(0);
+    for (int u = 0; u < U; u++) c[u] = u < RW ? sc[u * 32 + lane] : 0u;   // no loop-carried state
+#pragma unroll
+    for (int u = 0; u < U; u++) xs[u] = u < RW ? ldg_ro(x + c[u]) : VT(0);
+  }
 #pragma unroll
   for (int u = 0; u < U; u++) {
     const int k = u % R, t = u / R;           // compile-time after unrolling
@@ -346,6 +419,10 @@ __global__ void __launch_bounds__(HOT ? HOT_WARPS * 32 : WARPS * 32,
     }
     if (gw + nw < P.ntiles) dn = P.tiles[gw + nw];
   }
+  // the tiles are the static partition (their first TMA is in flight already); x, x' and y may be
+  // written by the kernel before this one (compact-x gather, the previous SpMV's fix-up)
+  pdl_wait();
+  pdl_trigger();
   if constexpr (HOT) {   // the CTA's copy of (its share of) the hot x entries, gathered while the first tiles land
     constexpr int U = 8, T = NW * 32;
     for (int k0 = hlo; k0 < hhi; k0 += U * T) {
@@ -384,16 +461,26 @@ __global__ void __launch_bounds__(HOT ? HOT_WARPS * 32 : WARPS * 32,
         }
       }
     };
-    if (SELL && d.w == -2) {
+    if (SELL && (d.w == -2 || d.w == -3)) {
       // ---- SELL tile (read in place; the slot is refilled after the tile)
-      const int nrows = d.z & 0xffff, Wd = d.z >> 16;
-      const int R = sell_r(nrows);
-      if (R == 1) sell_tile<VT, 1, MIRROR>(P, d, st, lane, x, y, alpha, beta, refill);
-      else if (R == 2) sell_tile<VT, 2, MIRROR>(P, d, st, lane, x, y, alpha, beta, refill);
-      else sell_tile<VT, 4, MIRROR>(P, d, st, lane, x, y, alpha, beta, refill);
-      (void)Wd;
+      const int R = sell_r(d.z & 0xffff);
+      if (d.w == -3) {
+        if (R == 1) sell_tile<VT, 1, MIRROR, true>(P, d, st, lane, x, y, alpha, beta, refill);
+        else if (R == 2) sell_tile<VT, 2, MIRROR, true>(P, d, st, lane, x, y, alpha, beta, refill);
+        else sell_tile<VT, 4, MIRROR, true>(P, d, st, lane, x, y, alpha, beta, refill);
+      } else {
+        if (R == 1) sell_tile<VT, 1, MIRROR, false>(P, d, st, lane, x, y, alpha, beta, refill);
+        else if (R == 2) sell_tile<VT, 2, MIRROR, false>(P, d, st, lane, x, y, alpha, beta, refill);
+        else sell_tile<VT, 4, MIRROR, false>(P, d, st, lane, x, y, alpha, beta, refill);
+      }
       continue;
     }
+    // fp32: the SELL instantiation walks SELL tiles only (the host always launches SEG / slab tiles
+    // on their own: a SEG path beside the 64-entry narrow tiles spills, 0.0674 vs 0.0770 ms on the
+    // fp32 stencil); fp64: a small share of SEG tiles rides along (no second launch)
+    if constexpr (SELL && sizeof(VT) == 4) {
+      __trap();
+    } else {
     const int nrows = d.z & 0xffff, nnz = d.z >> 16;
     const bool slab = d.w >= 0;
     // ---- stage -> registers (conflict-free 32-lane vectors), then refill the slot
@@ -440,7 +527,7 @@ __global__ void __launch_bounds__(HOT ? HOT_WARPS * 32 : WARPS * 32,
     VT xv[QMAX + 1];
     if (slab) {
 #pragma unroll
-      for (int u = 0; u < QMAX; u++) xv[u] = lane + 32 * u < nnz ? ldx_hot<HOT, NA>(x, hbase, c[u], xpol) : VT(0);
+      for (int u = 0; u < QMAX; u++) xv[u] = ldx_hot<HOT, NA, CL>(x, hbase, c[u], xpol, lane + 32 * u < nnz);
       double acc = 0.0;
 #pragma unroll
       for (int u = 0; u < QMAX; u++) acc = fma((double)v[u], (double)xv[u], acc);   // padding: 0 * 0
@@ -459,7 +546,7 @@ __global__ void __launch_bounds__(HOT ? HOT_WARPS * 32 : WARPS * 32,
 #pragma unroll
     for (int j = 0; j <= QMAX; j++) {
       const bool on = j < QMAX ? j < q : extra;
-      xv[j] = on ? ldx_hot<HOT, NA>(x, hbase, c[j], xpol) : VT(0);
+      xv[j] = ldx_hot<HOT, NA, CL>(x, hbase, c[j], xpol, on);
     }
     if (d.w != KIND_W_SEG_DENSE) {   // rows without entries must read 0 (a dense tile writes every row)
       for (int rr = lane; rr < nrows; rr += 32) rsum[rr] = 0.0;
@@ -507,6 +594,7 @@ __global__ void __launch_bounds__(HOT ? HOT_WARPS * 32 : WARPS * 32,
       }
     }
     __syncwarp();   // rsum is free
+    }
   }
   if constexpr (HOT && CL == 2) cluster_sync();   // the partner CTA may still read this CTA's hot half
 }
@@ -604,12 +692,16 @@ __global__ void __launch_bounds__(WARPS * 32, MSREP_ROW_MINB) rows_mm_kernel(con
         }
       }
     };
-    if (SELL && d.w == -2) {
+    if (SELL && (d.w == -2 || d.w == -3)) {
       // ---- SELL tile: lane l walks its R rows; element t of row k at (t*R + k)*32 + l
       const int nrows = d.z & 0xffff, W = d.z >> 16, R = sell_r(nrows);
-      const uint16_t* lens = reinterpret_cast<const uint16_t*>(st);
-      const VT* sv = reinterpret_cast<const VT*>(st + align16(R * 32 * 2));
-      const uint32_t* sc = reinterpret_cast<const uint32_t*>(st + align16(R * 32 * 2) + W * R * 32 * V);
+      const bool narrow = d.w == -3;   // 16-bit column offsets from the tile's base (KIND_SELLN)
+      const unsigned char* p0 = st + (narrow ? 16 : 0);
+      const uint16_t* lens = reinterpret_cast<const uint16_t*>(p0);
+      const VT* sv = reinterpret_cast<const VT*>(p0 + align16(R * 32 * 2));
+      const uint32_t* sc = reinterpret_cast<const uint32_t*>(p0 + align16(R * 32 * 2) + W * R * 32 * V);
+      const uint16_t* so = reinterpret_cast<const uint16_t*>(sc);
+      const uint32_t nbase = narrow ? *reinterpret_cast<const uint32_t*>(st) : 0u;
       for (int k = 0; k < R; k++) {
         const int row = k * 32 + lane;
         const int len = row < nrows ? lens[k * 32 + lane] : 0;
@@ -623,7 +715,8 @@ __global__ void __launch_bounds__(WARPS * 32, MSREP_ROW_MINB) rows_mm_kernel(con
           for (int b = 0; b < BS; b++) {
             const int e = e0 + b;
             const bool on = e < len;
-            const uint32_t cc = on ? min(sc[(e * R + k) * 32 + lane], xmax) : 0u;
+            const int sl = (e * R + k) * 32 + lane;
+            const uint32_t cc = on ? min(narrow ? nbase + so[sl] : sc[sl], xmax) : 0u;
             vv[b] = on ? sv[(e * R + k) * 32 + lane] : VT(0);
             if (on) ldx_row<VT, K>(x + (int64_t)cc * K, xr[b], xpol);
             else {
@@ -1164,6 +1257,40 @@ __global__ void pack_kernel(const PackLaunch L) {
   const int4 d = L.tiles[t];
   const int nrows = d.z & 0xffff, nnz = d.z >> 16;
   char* b = L.blob + (int64_t)L.blob16[t] * 16;
+  if (d.w == -3) {   // narrow SELL: as below, column ids as 16-bit offsets from the tile's smallest
+    const int W = nnz, R = sell_r(nrows);
+    auto colof = [&](int z) { return (uint32_t)(L.colmap ? L.colmap[L.idx[z]] : L.idx[z]); };
+    uint32_t lo = 0xffffffffu;
+    for (int k = 0; k < R; k++) {
+      const int row = k * 32 + lane;
+      if (row < nrows)
+        for (int z = L.lptr[d.x + row]; z < L.lptr[d.x + row + 1]; z++) lo = min(lo, colof(z));
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) lo = min(lo, __shfl_xor_sync(FULL, lo, off));
+    if (lane < 4) reinterpret_cast<uint32_t*>(b)[lane] = lane == 0 ? lo : 0u;
+    uint16_t* lens = reinterpret_cast<uint16_t*>(b + 16);
+    char* vb0 = b + 16 + align16(R * 32 * 2);
+    uint16_t* ox = reinterpret_cast<uint16_t*>(vb0 + W * R * 32 * L.vsize);
+    for (int k = 0; k < R; k++) {
+      const int row = k * 32 + lane;
+      const int rs = row < nrows ? L.lptr[d.x + row] : 0;
+      const int len = row < nrows ? L.lptr[d.x + row + 1] - rs : 0;
+      lens[k * 32 + lane] = (uint16_t)len;
+      for (int t = 0; t < W; t++) {
+        const bool on = t < len;
+        const int sl = (t * R + k) * 32 + lane;
+        if (L.vsize == 8) reinterpret_cast<double*>(vb0)[sl] = on ? static_cast<const double*>(L.val)[rs + t] : 0.0;
+        else reinterpret_cast<float*>(vb0)[sl] = on ? static_cast<const float*>(L.val)[rs + t] : 0.0f;
+        ox[sl] = on ? (uint16_t)(colof(rs + t) - lo) : (uint16_t)0;   // span <= 65535 (host-checked)
+      }
+    }
+    if (lane == 0) {   // zero the 16-byte tail padding of the offsets
+      const int used = W * R * 32 * 2;
+      for (int q = used; q < align16(used); q++) reinterpret_cast<char*>(ox)[q] = 0;
+    }
+    return;
+  }
   if (d.w == -2) {   // SELL: lane l owns rows l + 32k (k < R); element t of row k at (t*R + k)*32 + l
     const int W = nnz, R = sell_r(nrows);
     uint16_t* lens = reinterpret_cast<uint16_t*>(b);
@@ -1223,14 +1350,17 @@ __global__ void col_degree_kernel(const int32_t* __restrict__ idx, int64_t nz, i
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nz; i += (int64_t)gridDim.x * blockDim.x)
     atomicAdd(deg + idx[i], 1);
 }
-__global__ void hot_slot_kernel(const int32_t* __restrict__ hot, int nhot, int32_t* __restrict__ slot) {
+__global__ void hot_slot_kernel(const int32_t* __restrict__ hot, int nhot, int32_t* __restrict__ slot,
+                                const int32_t* __restrict__ val) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < nhot) slot[hot[k]] = k;
+  if (k < nhot) slot[hot[k]] = val ? val[k] : k;
 }
 // compact x (every SpMV of a compact-x partition): x' rows = x rows of the listed columns
 template <typename VT, int K>
+// pos != NULL (degree-ordered x'): cols ascending, entry i stored at x' row pos[i] -- the reads of
+// x stay in column order (coalesced sectors) and only the stores scatter (into L2-resident x')
 __global__ void gather_x_kernel(const VT* __restrict__ x, const int32_t* __restrict__ cols, int64_t n,
-                                VT* __restrict__ out) {
+                                VT* __restrict__ out, const int32_t* __restrict__ pos) {
   // one compact entry (K values) per thread, 4 independent entries per thread in flight
   constexpr int U = 4;
   const int64_t i0 = (blockIdx.x * (int64_t)blockDim.x) * U + threadIdx.x;
@@ -1246,12 +1376,23 @@ __global__ void gather_x_kernel(const VT* __restrict__ x, const int32_t* __restr
 #pragma unroll
     for (int j = 0; j < K; j++) v[u][j] = i0 + (int64_t)u * blockDim.x < n ? __ldg(x + (int64_t)c[u] * K + j) : VT(0);
 #pragma unroll
+  int64_t o[U];
+#pragma unroll
+  for (int u = 0; u < U; u++) {
+    const int64_t i = i0 + (int64_t)u * blockDim.x;
+    o[u] = i < n ? (pos ? (int64_t)__ldcs(pos + i) : i) : 0;
+  }
+#pragma unroll
   for (int u = 0; u < U; u++) {
     const int64_t i = i0 + (int64_t)u * blockDim.x;
     if (i < n)
 #pragma unroll
-      for (int j = 0; j < K; j++) out[i * K + j] = v[u][j];
+      for (int j = 0; j < K; j++) out[o[u] * K + j] = v[u][j];
   }
+  // the tile kernel may launch once every block is here (it waits for this grid before reading x');
+  // triggering at the start let its big CTAs take SMs from this grid's later blocks (R-MAT: the
+  // gather 40 -> 87-174 us on the power-law suite)
+  pdl_trigger();
 }
 
 // loopback reduce (in-process multi-rank test transport): fixed rank order
@@ -1289,23 +1430,34 @@ __global__ void planar_kernel(const VT* __restrict__ src, VT* __restrict__ dst, 
 }
 
 // --------------------------------------------------------- small kernels
-// one WARP per (split row, vector j < k): k = 1 for SpMV, the block width for SpMM; records, head
-// partials and y are k-wide (record r, vector j at r*k + j; y row-major [m x k]).  The row's records
-// are summed lane-strided and joined by a fixed shuffle tree (R-MAT's heaviest rows have ~470
-// records: one thread summing them serially made the fix-up 30 us), then lane 0 adds the routed
+// FIX_G = 8 lanes per (split row, vector j < k): k = 1 for SpMV, the block width for SpMM; records,
+// head partials and y are k-wide (record r, vector j at r*k + j; y row-major [m x k]).  The row's
+// records are summed G-strided and joined by a fixed shuffle tree (R-MAT's heaviest rows have ~470
+// records: one thread summing them serially made the fix-up 30 us; a whole warp per row left most
+// lanes idle on its ~5-record average, 16 us per SpMV), then the group's first lane adds the routed
 // head partials in part order and applies alpha, beta once.  Fixed order: bit-reproducible.
+constexpr int FIX_G = 8;
 template <typename VT>
 __global__ void fixup_kernel(const FixupLaunch F) {
-  const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (t >= (int64_t)F.nsplit * F.k) return;   // whole warps exit together
+  constexpr int G = FIX_G;   // lanes per (split row, vector): rows average ~5 records (R-MAT)
+  const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+  const int g = threadIdx.x & (G - 1);
+  if (t >= (int64_t)F.nsplit * F.k) return;   // whole groups exit together (nsplit*k*G threads, G | 32)
+  const unsigned gm = (unsigned)(((1ull << G) - 1) << (threadIdx.x & 31 & ~(G - 1)));
   const int s = (int)(t / F.k), jv = (int)(t % F.k), K = F.k;
+  // the row's metadata and its y_in are independent loads: all in flight before the record sum
+  const int k0 = F.sr_rec[2 * s], k1 = F.sr_rec[2 * s + 1];
+  const int h0 = F.sr_head[2 * s], h1 = F.sr_head[2 * s + 1];
+  VT* y = static_cast<VT*>(F.y);
+  const int64_t r = F.sr_row[s] * K + jv;
+  pdl_wait();   // records and y come from the tile kernel
+  const double yin = (g == 0 && F.beta != 0.0) ? (double)y[r] : 0.0;
   double acc = 0.0;
-  for (int k = F.sr_rec[2 * s] + lane; k < F.sr_rec[2 * s + 1]; k += 32) acc += F.rec[(int64_t)k * K + jv];
+  for (int k = k0 + g; k < k1; k += G) acc += F.rec[(int64_t)k * K + jv];
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(FULL, acc, off);
-  if (lane != 0) return;
-  for (int h = F.sr_head[2 * s]; h < F.sr_head[2 * s + 1]; h++) {
+  for (int off = G / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(gm, acc, off, G);
+  if (g != 0) return;
+  for (int h = h0; h < h1; h++) {
     const int j = F.head_list[h];
     double hv = 0.0;
     if (j >= F.part_lo && j < F.part_hi) {
@@ -1316,10 +1468,8 @@ __global__ void fixup_kernel(const FixupLaunch F) {
     }
     acc = acc + hv;
   }
-  VT* y = static_cast<VT*>(F.y);
-  const int64_t r = F.sr_row[s] * K + jv;
   double v = F.alpha * acc;
-  if (F.beta != 0.0) v += F.beta * (double)y[r];
+  if (F.beta != 0.0) v += F.beta * yin;
   y[r] = (VT)v;
   for (int mi = 0; mi < F.nmirror; mi++) static_cast<VT*>(F.mirror[mi])[r] = (VT)v;
 }
@@ -1538,7 +1688,14 @@ cudaError_t launch_rows_k(const RowLaunch& L, cudaStream_t s) {
   if (e) return e;
   int g = grid_for(kern, b, L.ntiles, nw);
   if constexpr (CL == 1) {
-    kern<<<g, nw * 32, b, s>>>(L);
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = dim3(g); cfg.blockDim = dim3(nw * 32); cfg.dynamicSmemBytes = (size_t)b; cfg.stream = s;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, L);
+    if (e) return e;
   } else {   // CTA pairs (one CTA per SM, the two SMs of a TPC) sharing their hot halves over DSMEM
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute at[1];
@@ -1616,9 +1773,14 @@ cudaError_t launch_pack(const PackLaunch& L, cudaStream_t s) {
 
 cudaError_t launch_fixup(const FixupLaunch& F, cudaStream_t s) {
   if (F.nsplit == 0) return cudaSuccess;
-  const int g = (int)(((int64_t)F.nsplit * F.k * 32 + 127) / 128);   // a warp per (split row, vector)
-  if (F.dtype == 0) fixup_kernel<double><<<g, 128, 0, s>>>(F);
-  else fixup_kernel<float><<<g, 128, 0, s>>>(F);
+  const int g = (int)(((int64_t)F.nsplit * F.k * FIX_G + 255) / 256);   // FIX_G lanes per (split row, vector)
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // prologue under the tile kernel's tail
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = dim3(g); cfg.blockDim = dim3(256); cfg.stream = s; cfg.attrs = at; cfg.numAttrs = 1;
+  cudaError_t e = F.dtype == 0 ? cudaLaunchKernelEx(&cfg, fixup_kernel<double>, F) : cudaLaunchKernelEx(&cfg, fixup_kernel<float>, F);
+  if (e) return e;
   return cudaGetLastError();
 }
 
@@ -1666,16 +1828,17 @@ cudaError_t launch_col_degree(const int32_t* idx, int64_t nz, int32_t* deg, cuda
   return cudaGetLastError();
 }
 
-cudaError_t launch_hot_slots(const int32_t* hot, int nhot, int32_t* slot, cudaStream_t s) {
+cudaError_t launch_hot_slots(const int32_t* hot, int nhot, int32_t* slot, cudaStream_t s, const int32_t* val) {
   if (nhot <= 0) return cudaSuccess;
-  hot_slot_kernel<<<(nhot + 255) / 256, 256, 0, s>>>(hot, nhot, slot);
+  hot_slot_kernel<<<(nhot + 255) / 256, 256, 0, s>>>(hot, nhot, slot, val);
   return cudaGetLastError();
 }
 
-cudaError_t launch_gather_x(const void* x, const int32_t* cols, int64_t n, int k, void* out, int dtype, cudaStream_t s) {
+cudaError_t launch_gather_x(const void* x, const int32_t* cols, int64_t n, int k, void* out, int dtype, cudaStream_t s,
+                            const int32_t* pos) {
   if (n <= 0) return cudaSuccess;
   const unsigned g = (unsigned)((n + 1023) / 1024);   // 256 threads x 4 entries per block
-#define MSREP_GATHER(VT, K) gather_x_kernel<VT, K><<<g, 256, 0, s>>>((const VT*)x, cols, n, (VT*)out)
+#define MSREP_GATHER(VT, K) gather_x_kernel<VT, K><<<g, 256, 0, s>>>((const VT*)x, cols, n, (VT*)out, pos)
   if (dtype == 0) {
     if (k == 1) MSREP_GATHER(double, 1);
     else if (k == 2) MSREP_GATHER(double, 2);

@@ -13,6 +13,24 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
+G = 4096                 # guard elements on both sides of every output buffer
+SENT = -12345.678        # their value: any kernel store outside [0, m) changes it
+
+
+def guarded(host, torch):
+    """A device copy of `host` inside a larger buffer whose G leading and trailing elements hold
+    SENT; returns (view, check) -- check() is True when no store landed outside the view."""
+    a = np.ascontiguousarray(host)
+    buf = torch.full((a.size + 2 * G,), SENT, dtype=torch.float64, device="cuda")
+    buf[G:G + a.size] = torch.as_tensor(a.reshape(-1)).cuda()
+    view = buf[G:G + a.size].view(a.shape)
+
+    def check():
+        b = buf.cpu().numpy()
+        return bool(np.all(b[:G] == SENT) and np.all(b[G + a.size:] == SENT))
+    return view, check
+
+
 def main():
     import torch
     import gen
@@ -41,22 +59,23 @@ def main():
                     ctx.partition(fmt, m, n, idx=C["idx"], val=C["val"], coo_row=gen.expand_rows(C))
                 else:
                     ctx.partition(fmt, m, n, ptr=C["ptr"], idx=C["idx"], val=C["val"])
-                yd = torch.as_tensor(y).cuda()
+                yd, yok = guarded(y, torch)
                 ctx.spmv(1.5, torch.as_tensor(x).cuda(), 0.5, yd)
                 torch.cuda.synchronize()
-                if not np.array_equal(yd.cpu().numpy(), ref):
+                if not (np.array_equal(yd.cpu().numpy(), ref) and yok()):
                     print("FAIL", name, fmt_tag, hot, cx, flush=True)
                     fails += 1
                 if fmt == "csr":
                     k = 4
                     X = torch.as_tensor(np.stack([x] * k, 1).copy()).cuda()
-                    Y = torch.as_tensor(np.stack([y] * k, 1).copy()).cuda()
+                    Y, Yok = guarded(np.stack([y] * k, 1), torch)
                     ctx.spmm(1.5, X, 0.5, Y)
-                    mirror = torch.zeros(m, dtype=torch.float64, device="cuda")
-                    yd = torch.as_tensor(y).cuda()
+                    mirror, mok = guarded(np.zeros(m), torch)
+                    yd, yok = guarded(y, torch)
                     ctx.spmv_mirror(1.5, torch.as_tensor(x).cuda(), 0.5, yd, [mirror])
                     torch.cuda.synchronize()
-                    if not (np.array_equal(Y.cpu().numpy()[:, 2], ref) and np.array_equal(mirror.cpu().numpy(), ref)):
+                    if not (np.array_equal(Y.cpu().numpy()[:, 2], ref) and np.array_equal(mirror.cpu().numpy(), ref)
+                            and Yok() and mok() and yok()):
                         print("FAIL spmm/mirror", name, hot, cx, flush=True)
                         fails += 1
                 ctx.close()

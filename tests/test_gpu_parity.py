@@ -455,6 +455,66 @@ def test_sell_rows_per_lane(k, fmt):
     check(B, fmt, xb, yb, 2.0, 0.5, parts=2, exact=True)
 
 
+def _banded_rows(m, k, span, seed, kind):
+    """m rows of k distinct columns each within [r - span/2, r + span/2] (clipped): narrow SELL rows"""
+    rng = np.random.default_rng(seed)
+    n = m
+    ptr = np.arange(m + 1, dtype=np.int64) * k
+    idx = np.empty(m * k, dtype=np.int32)
+    for r in range(m):
+        lo = max(0, min(n - span, r - span // 2))
+        idx[r * k:(r + 1) * k] = np.sort(rng.choice(span, size=k, replace=False) + lo)
+    val = gen.vector(m * k, seed + 1, kind=kind)
+    return gen.Sparse(fmt="csr", m=m, n=n, ptr=ptr, idx=idx, val=val)
+
+
+@pytest.mark.parametrize("k", [8, 16, 27, 32])
+@pytest.mark.parametrize("fmt", ["csr", "coo"])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_narrow_sell_tiles(k, fmt, dtype):
+    """Narrow SELL tiles (16-bit column offsets from a per-tile base; fp32 up to 64 entries per lane,
+    i.e. R = 2 for 27-point rows) next to 32-bit ones: rows whose columns span < 65536 become
+    narrow, a block of rows spanning the whole x stays wide.  Bit-exact vs the oracle for
+    MSREP_TUNE_SELL 2 (narrow) and 1 (32-bit only), 1 and 3 parts, device- and host-resident,
+    and the SpMM block walk over the same tiles."""
+    import paper_2209_07552_b200 as M
+    import torch
+    m = 32 * 4 * 12 + 37
+    A = _banded_rows(m, k, 20000, 300 + k, gen.SMALLINT)
+    # rows 1024..1279 get a column near the end of a 200K-wide x: those tiles cannot be narrow
+    n = 200_000
+    idx = A["idx"].copy()
+    wide = np.arange(1024, 1280)
+    idx[A["ptr"][wide + 1] - 1] = n - 1 - wide
+    A = gen.Sparse(fmt="csr", m=m, n=n, ptr=A["ptr"], idx=idx, val=A["val"])
+    A = to_dtype(A, dtype)
+    x = gen.vector(n, 311, kind=gen.SMALLINT).astype(dtype); y = gen.vector(m, 312, kind=gen.SMALLINT).astype(dtype)
+    ref = oracle_ref(A, x, y, 1.5, 0.5)
+    for sell in (2, 1):
+        for parts in (1, 3):
+            for kw in ({}, {"residency": "host", "chunk_bytes": 32 << 10}):
+                ctx = M.Context(0, 1, None, 0, parts)
+                ctx.set_tuning("sell", sell)
+                got = run_gpu(A, fmt, x, y, 1.5, 0.5, ctx=ctx, **kw)
+                st = ctx.stats()
+                assert np.array_equal(got, ref), (sell, parts, kw, np.nonzero(got != ref)[0][:8])
+                assert st["nsell"] > 0
+                if sell == 2:
+                    assert 0 < st["nsell_narrow"] < st["nsell"], st
+                else:
+                    assert st["nsell_narrow"] == 0, st
+                if not kw and parts == 1:   # SpMM over the same tiles (4 vectors: 2x, x, -x, 3x)
+                    X = np.stack([2 * x, x, -x, 3 * x], 1).astype(dtype)
+                    Y = np.stack([y] * 4, 1).astype(dtype)
+                    Xd = torch.as_tensor(X).cuda(); Yd = torch.as_tensor(Y).cuda()
+                    ctx.spmm(1.5, Xd, 0.5, Yd)
+                    torch.cuda.synchronize()
+                    got4 = Yd.cpu().numpy()
+                    for j in range(4):
+                        assert np.array_equal(got4[:, j], oracle_ref(A, X[:, j].copy(), y, 1.5, 0.5)), (sell, j)
+                ctx.close()
+
+
 @pytest.mark.parametrize("fmt", ["csc:bands", "coo_col:bands", "csc"])
 def test_csc_heavy_rows_same_row_groups(fmt):
     """Rows with thousands of entries inside one band (R-MAT heavy rows, and a dense row): the

@@ -9,5 +9,5 @@ try:
 except Exception:
     print('BENCH FAILED', t[-2000:]); sys.exit()
 r=d['roofline']
-print(d['config']['workload'], 'GFLOP/s=%.1f'%d['value'], 'ms=%.4f'%d['ms_per_step'], 'kern_ms=%.4f'%r['kernel_avg_ms'], 'frac=%.3f'%r['frac'], 'GBps=%.0f'%r['achieved'], d['stats_rank0'], 'clk', d['clocks'].get('sm_mhz'), 'part_ms', d.get('partition_ms'), d.get('partition_phase_ms'), d.get('layout_build_ms'))
+print(d['config']['workload'], 'GFLOP/s=%.1f'%d['value'], 'ms=%.4f'%d['ms_per_step'], 'kern_ms=%.4f'%r['kernel_avg_ms'], 'frac=%.3f'%r['frac'], 'GBps=%.0f'%r['achieved'], d['stats_rank0'], 'clk', d['clocks'].get('sm_mhz'), 'part_ms', d.get('partition_ms'), d.get('partition_phase_ms'), d.get('layout_build_ms'), 'ktimes', d.get('kernel_times_us'))
 "
