@@ -45,7 +45,7 @@ def parse(argv=None):
     p.add_argument("--warmup", type=int, default=20)
     p.add_argument("--impl", default="msrep", choices=["msrep", "reference"])
     p.add_argument("--config", default="rmat",
-                   choices=["stencil", "rmat", "tallskinny", "random1k"] +
+                   choices=["stencil", "rmat", "rmatperm", "tallskinny", "random1k"] +
                    [f"suite-{s}-{z}" for s in gen.SUITE_SHAPES for z in gen.SUITE_SIZES])
     p.add_argument("--format", default=None, choices=["csr", "coo", "csc", "coo_col"])
     p.add_argument("--dtype", default="f64", choices=["f64", "f32"])

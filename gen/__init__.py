@@ -193,6 +193,7 @@ CONFIGS = {
     "random1k": dict(desc="1,000x1,000 random CSR, exactly 10 distinct columns/row, 10k nnz (config 1)"),
     "stencil": dict(desc="27-point 3D stencil N=127: 2,048,383 rows, 54,439,939 nnz (config 2)"),
     "rmat": dict(desc="R-MAT scale 24, 2^28 samples deduplicated, (a,b,c)=(.57,.19,.19) (config 3)"),
+    "rmatperm": dict(desc="config 3 with a seeded vertex relabelling of rows and columns (the permuted variant)"),
     "tallskinny": dict(desc="50M x 1M, exactly 500 distinct rows/column, 500M nnz, CSC (config 4)"),
 }
 
@@ -203,9 +204,9 @@ def make_config(name, kind=UNIFORM, scale_down=1):
         return kdistinct_csr(1000, 1000, 10, seed=1, kind=kind)
     if name == "stencil":
         return stencil27(127 // scale_down if scale_down > 1 else 127, seed=2, kind=kind)
-    if name == "rmat":
+    if name in ("rmat", "rmatperm"):
         s = 24 - (scale_down.bit_length() - 1 if scale_down > 1 else 0)
-        return rmat(s, seed=3, kind=kind)
+        return rmat(s, seed=3, kind=kind, permute=name == "rmatperm")
     if name == "tallskinny":
         return kdistinct_csc(50_000_000 // scale_down, 1_000_000 // scale_down, 500, seed=4, kind=kind)
     if name.startswith("suite-"):
@@ -252,7 +253,7 @@ def suite(name, kind=UNIFORM):
 # ---------------------------------------------------------- rank-local generation
 # A config's pointer array alone (every rank needs it for the plan), then only the rows a rank's
 # nonzero range touches: bench.py with N > 1 never builds the whole matrix on a rank.
-LOCAL_CONFIGS = ("random1k", "stencil", "rmat", "tallskinny")
+LOCAL_CONFIGS = ("random1k", "stencil", "rmat", "rmatperm", "tallskinny")
 
 
 def config_pointer(name):
@@ -268,11 +269,11 @@ def config_pointer(name):
         counts = np.empty(N ** 3, np.int64)
         lib().gen_stencil27_count(N, _p(counts))
         m = N ** 3
-    elif name == "rmat":
+    elif name in ("rmat", "rmatperm"):
         scale = 24
         m = 1 << scale
         counts = np.empty(m, np.int64)
-        lib().gen_rmat_count(scale, float(16 * m), 0.57, 0.19, 0.19, 3, 0, _p(counts))
+        lib().gen_rmat_count(scale, float(16 * m), 0.57, 0.19, 0.19, 3, int(name == "rmatperm"), _p(counts))
     else:
         raise KeyError(name)
     ptr = np.zeros(m + 1, np.int64)
@@ -294,8 +295,9 @@ def config_rows(name, ptr, r0, r1, kind=UNIFORM):
         L.gen_kdistinct_fill_rows(1_000_000, 50_000_000, 500, 4, kind, 1, r0, r1, _p(ptr), _p(idx), _p(val))
     elif name == "stencil":
         L.gen_stencil27_fill_rows(127, 2, kind, r0, r1, _p(ptr), _p(idx), _p(val))
-    elif name == "rmat":
-        L.gen_rmat_fill_rows(24, float(16 * (1 << 24)), 0.57, 0.19, 0.19, 3, 0, kind, r0, r1, _p(ptr), _p(idx), _p(val))
+    elif name in ("rmat", "rmatperm"):
+        L.gen_rmat_fill_rows(24, float(16 * (1 << 24)), 0.57, 0.19, 0.19, 3, int(name == "rmatperm"), kind, r0, r1,
+                             _p(ptr), _p(idx), _p(val))
     else:
         raise KeyError(name)
     return idx, val

@@ -578,10 +578,12 @@ struct Packer {
   const std::vector<int64_t>& lp;   // local pointer over the window (rank-local nonzeros)
   int64_t cur_r0 = -1, cur_r1 = -1;
   const int64_t tnz;                // nonzeros per SEG tile / slab for this value size
-  const int32_t* lidx;              // rank-local column ids (host), NULL: no narrow SELL tiles
+  const int32_t* lidx;              // rank-local column ids (host), or
+  const int32_t *rlo, *rhi;         // per-window-row column span; both NULL: no narrow SELL tiles
   const int wn;                     // R * W limit of a narrow SELL tile
-  explicit Packer(Schedule& s, int64_t w, const std::vector<int64_t>& l, int vsize, const int32_t* li = nullptr)
-      : S(s), wlo(w), lp(l), tnz(tile_nnz(vsize)), lidx(li), wn(selln_w_max(vsize)) {}
+  explicit Packer(Schedule& s, int64_t w, const std::vector<int64_t>& l, int vsize, const int32_t* li = nullptr,
+                  const int32_t* lo = nullptr, const int32_t* hi = nullptr)
+      : S(s), wlo(w), lp(l), tnz(tile_nnz(vsize)), lidx(li), rlo(lo), rhi(hi), wn(selln_w_max(vsize)) {}
   int64_t ls(int64_t r) const { return lp[(size_t)(r - wlo)]; }
   int64_t le(int64_t r) const { return lp[(size_t)(r - wlo + 1)]; }
   void flush() {
@@ -606,7 +608,8 @@ struct Packer {
   // offsets, R*W <= wn) when every column of the rows lies within 65535 of the smallest, else
   // R*W <= SELL_W_MAX with 32-bit ids.
   int64_t try_sell(int64_t r, int64_t rend) {
-    const int lim = lidx ? std::max(wn, SELL_W_MAX) : SELL_W_MAX;
+    const bool spans = lidx || rlo;
+    const int lim = spans ? std::max(wn, SELL_W_MAX) : SELL_W_MAX;
     for (int R = SELL_R_MAX; R >= 1; R >>= 1) {
       const int64_t e = std::min<int64_t>(r + 32 * R, rend);
       if (R > 1 && e - r <= 32 * (R / 2)) continue;   // a smaller R covers these rows
@@ -620,11 +623,18 @@ struct Packer {
       }
       if (!ok || W == 0 || 8 * sum < 7 * W * (e - r)) continue;
       bool narrow = false;
-      if (lidx && W * R <= wn) {
+      if (spans && W * R <= wn) {
         int32_t lo = INT32_MAX, hi = INT32_MIN;
-        for (int64_t z = ls(r); z < le(e - 1); z++) {
-          lo = std::min(lo, lidx[z]);
-          hi = std::max(hi, lidx[z]);
+        if (lidx) {
+          for (int64_t z = ls(r); z < le(e - 1); z++) {
+            lo = std::min(lo, lidx[z]);
+            hi = std::max(hi, lidx[z]);
+          }
+        } else {
+          for (int64_t q = r; q < e; q++) {
+            lo = std::min(lo, rlo[q - wlo]);
+            hi = std::max(hi, rhi[q - wlo]);
+          }
         }
         narrow = (int64_t)hi - (int64_t)lo <= 65535;
       }
@@ -687,8 +697,8 @@ void rank_segments(msrep_format fmt, int64_t m, int nranks, int vparts, const st
 // slabs whose fix-up adds the head partials of the parts that continue it.
 void build_row_schedule(const std::vector<msrep_part_desc>& P, int P0, int P1, int64_t B_lo, int64_t wlo, int V,
                         const std::vector<int64_t>& lp, Schedule& S, bool allow_sell = true,
-                        const int32_t* lidx = nullptr) {
-  Packer pk(S, wlo, lp, V, lidx);
+                        const int32_t* lidx = nullptr, const int32_t* rlo = nullptr, const int32_t* rhi = nullptr) {
+  Packer pk(S, wlo, lp, V, lidx, rlo, rhi);
   for (int j = P0; j < P1; j++) {
     const msrep_part_desc& d = P[(size_t)j];
     const bool empty = d.start_idx > d.end_idx;
@@ -2096,6 +2106,19 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     tpart[0].owned_end = m;
     // ---- schedule
     Schedule S;
+    // transposed column formats: the rows' column spans come from the device slice (narrow SELL)
+    std::vector<int32_t> span_lo, span_hi;
+    if (tr && c->tune_sell == 2 && m > 0) {
+      void* q;
+      TRY(dalloc(c, (size_t)m * 8, &q, s));
+      int32_t* d_span = static_cast<int32_t*>(q);
+      CUDA_TRY(launch_row_span(t_ptr, t_cols, m, d_span, d_span + m, s));
+      span_lo.resize((size_t)m);
+      span_hi.resize((size_t)m);
+      CUDA_TRY(cudaMemcpyAsync(span_lo.data(), d_span, (size_t)m * 4, cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaMemcpyAsync(span_hi.data(), d_span + m, (size_t)m * 4, cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaStreamSynchronize(s));
+    }
     auto schedule = [&](bool sell) {
       if (!tr) {
         // narrow SELL tiles (16-bit column offsets) from the host's column ids (MSREP_TUNE_SELL 2)
@@ -2118,7 +2141,8 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
           d[0].end_idx = LP[(size_t)r1] - 1;
           d[0].start_row = r0; d[0].end_row = r1 - 1;
           d[0].owned_begin = r0; d[0].owned_end = r1;
-          build_row_schedule(d, 0, 1, 0, 0, (int)V, LP, cs[(size_t)k], sell);
+          build_row_schedule(d, 0, 1, 0, 0, (int)V, LP, cs[(size_t)k], sell, nullptr,
+                             span_lo.empty() ? nullptr : span_lo.data(), span_hi.empty() ? nullptr : span_hi.data());
         }
       };
       const int T = (int)std::min<int64_t>(nch, host_threads(nz_r + m));
@@ -2458,21 +2482,37 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     }
     CUDA_TRY(cudaStreamSynchronize(s));
     sub(3);
+#ifdef MSREP_PHASE_DEBUG   // tuning builds only: where the tile-table phase goes
+    auto dbg_t0 = std::chrono::steady_clock::now();
+    auto dbg = [&](const char* what) {
+      cudaStreamSynchronize(s);
+      const auto now = std::chrono::steady_clock::now();
+      fprintf(stderr, "[msrep phase4] %-24s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(now - dbg_t0).count());
+      dbg_t0 = now;
+    };
+#define MSREP_DBG(w) dbg(w)
+#else
+#define MSREP_DBG(w)
+#endif
     std::vector<TileHost> fin(S.tiles);
     for (size_t t = 0; t < fin.size(); t++) fin[t].nz0 = blob16[t];
     CUDA_TRY(cudaStreamSynchronize(s));
     // plain slices are no longer needed: the blobs hold the partition (host-resident: the
     // pinned copy does, and the packing buffer goes too)
+    MSREP_DBG("fin");
     release_range(c, mark, host_res ? c->bufs.size() : keep_from);
+    MSREP_DBG("release_range");
     if (host_res) {
       TRY(ensure_copy_stream(c));
       TRY(alloc_stages(c, s));
     }
     TRY(upload(c, reinterpret_cast<const int4*>(fin.data()), fin.size(), &c->d_tiles, s));
+    MSREP_DBG("upload tiles");
     c->blob_bytes = blob_total;
     void* rp;
     TRY(dalloc(c, (size_t)std::max(1, S.nrec) * 8, &rp, s));
     c->d_rec = static_cast<double*>(rp);
+    MSREP_DBG("rec");
     {
       TRY(upload_vec(c, S.sr_row, &c->d_sr_row, s));
       TRY(upload_vec(c, S.sr_rec, &c->d_sr_rec, s));
@@ -2503,6 +2543,8 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
         CUDA_TRY(cudaMemsetAsync(static_cast<char*>(pp) + (size_t)m * V, 0, (size_t)(c->py_len - m) * V, s));
       }
     }
+    MSREP_DBG("records + tail");
+#undef MSREP_DBG
   }
   CUDA_TRY(cudaStreamSynchronize(s));
   if (!colwise(fmt) || col_rows) sub(4);

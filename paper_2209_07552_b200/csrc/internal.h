@@ -41,6 +41,11 @@ constexpr uint32_t HOT_TAG = 0x80000000u;
 #define MSREP_HOT_WARPS 16
 #endif
 constexpr int HOT_WARPS = MSREP_HOT_WARPS;
+#ifndef MSREP_HOT_WARPS_F32
+#define MSREP_HOT_WARPS_F32 12
+#endif
+// fp32 SEG tiles hold 768 nonzeros (24 per lane): 16 warps x 128 registers spilled, 12 warps get 170
+__host__ __device__ constexpr int hot_warps(int vsize) { return vsize == 4 ? MSREP_HOT_WARPS_F32 : HOT_WARPS; }
 constexpr int HOT_BYTES = 96 * 1024;
 #ifndef MSREP_HOT_AUTO_KB
 #define MSREP_HOT_AUTO_KB 32
@@ -259,6 +264,8 @@ cudaError_t launch_sum_peers(const SumLaunch& L, cudaStream_t s);
 cudaError_t launch_planar(const void* src, void* dst, int64_t r0, int64_t r1, int k, int64_t ld, int to_planar,
                           int dtype, cudaStream_t s);
 cudaError_t launch_col_degree(const int32_t* idx, int64_t nz, int32_t* deg, cudaStream_t s);   // deg[idx[i]]++
+cudaError_t launch_row_span(const int32_t* ptr, const int32_t* cols, int64_t m, int32_t* lo, int32_t* hi,
+                            cudaStream_t s);   // lo/hi[r] = min/max column of row r (empty: INT_MAX/INT_MIN)
 cudaError_t launch_hot_slots(const int32_t* hot, int nhot, int32_t* slot, cudaStream_t s,
                              const int32_t* val = nullptr);   // slot[hot[k]] = val ? val[k] : k
 // out[i*k + j] = x[cols[i]*k + j], i < n, j < k (compact x for SpMV k = 1, SpMM k > 1)

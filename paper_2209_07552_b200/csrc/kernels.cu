@@ -44,12 +44,6 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-// Programmatic dependent launch (the SpMV's kernel chain gather_x -> rows -> fix-up): a kernel
-// launched with programmatic stream serialisation runs its prologue while its predecessor drains
-// and waits here before touching anything the predecessor writes; launch_dependents lets the
-// next kernel of the chain be scheduled early (a no-op without a dependent)
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)), "r"(bytes) : "memory");
 }
@@ -199,7 +193,7 @@ struct SStage {   // the larger of a full 32-bit-id SELL tile and a full narrow 
 };
 template <typename VT, bool SELL, bool HOT = false>
 using RowLayout = WLayout<(SELL && SStage<VT>::BYTES > RStage<VT>::BYTES) ? SStage<VT>::BYTES : RStage<VT>::BYTES, 1,
-                          MAX_TILE_ROWS * 8, HOT ? HOT_WARPS : WARPS>;
+                          MAX_TILE_ROWS * 8, HOT ? hot_warps((int)sizeof(VT)) : WARPS>;
 
 // x gather of a SEG / slab column id: tagged ids (bit 31, internal.h HOT_TAG) read the CTA's
 // shared-memory copy of the rank's hottest x entries, the others go through L2.  Branch-free: one
@@ -374,11 +368,11 @@ __device__ __forceinline__ void sell_tile(const RowLaunch& P, const int4 d, cons
 }
 
 template <typename VT, bool SELL, bool MIRROR, bool NA, bool HOT, int CL>
-__global__ void __launch_bounds__(HOT ? HOT_WARPS * 32 : WARPS * 32,
+__global__ void __launch_bounds__(HOT ? hot_warps((int)sizeof(VT)) * 32 : WARPS * 32,
                                   HOT ? 1 : (sizeof(VT) == 4 ? MSREP_ROW_MINB_F32 : MSREP_ROW_MINB))
     rows_kernel(const RowLaunch P) {
   using Lay = RowLayout<VT, SELL, HOT>;
-  constexpr int NW = HOT ? HOT_WARPS : WARPS;
+  constexpr int NW = HOT ? hot_warps((int)sizeof(VT)) : WARPS;
   constexpr int QMAX = qmax<VT>();
   constexpr int V = (int)sizeof(VT);
   constexpr int YR = MAX_TILE_ROWS / 32;
@@ -419,10 +413,6 @@ __global__ void __launch_bounds__(HOT ? HOT_WARPS * 32 : WARPS * 32,
     }
     if (gw + nw < P.ntiles) dn = P.tiles[gw + nw];
   }
-  // the tiles are the static partition (their first TMA is in flight already); x, x' and y may be
-  // written by the kernel before this one (compact-x gather, the previous SpMV's fix-up)
-  pdl_wait();
-  pdl_trigger();
   if constexpr (HOT) {   // the CTA's copy of (its share of) the hot x entries, gathered while the first tiles land
     constexpr int U = 8, T = NW * 32;
     for (int k0 = hlo; k0 < hhi; k0 += U * T) {
@@ -1350,6 +1340,20 @@ __global__ void col_degree_kernel(const int32_t* __restrict__ idx, int64_t nz, i
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nz; i += (int64_t)gridDim.x * blockDim.x)
     atomicAdd(deg + idx[i], 1);
 }
+// per-row column span of a row-major slice (narrow SELL eligibility of the transposed column formats)
+__global__ void row_span_kernel(const int32_t* __restrict__ ptr, const int32_t* __restrict__ cols, int64_t m,
+                                int32_t* __restrict__ lo, int32_t* __restrict__ hi) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  int32_t a = INT_MAX, b = INT_MIN;
+  for (int z = ptr[r]; z < ptr[r + 1]; z++) {
+    const int32_t q = cols[z];
+    a = min(a, q);
+    b = max(b, q);
+  }
+  lo[r] = a;
+  hi[r] = b;
+}
 __global__ void hot_slot_kernel(const int32_t* __restrict__ hot, int nhot, int32_t* __restrict__ slot,
                                 const int32_t* __restrict__ val) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1389,10 +1393,6 @@ __global__ void gather_x_kernel(const VT* __restrict__ x, const int32_t* __restr
 #pragma unroll
       for (int j = 0; j < K; j++) out[o[u] * K + j] = v[u][j];
   }
-  // the tile kernel may launch once every block is here (it waits for this grid before reading x');
-  // triggering at the start let its big CTAs take SMs from this grid's later blocks (R-MAT: the
-  // gather 40 -> 87-174 us on the power-law suite)
-  pdl_trigger();
 }
 
 // loopback reduce (in-process multi-rank test transport): fixed rank order
@@ -1450,7 +1450,6 @@ __global__ void fixup_kernel(const FixupLaunch F) {
   const int h0 = F.sr_head[2 * s], h1 = F.sr_head[2 * s + 1];
   VT* y = static_cast<VT*>(F.y);
   const int64_t r = F.sr_row[s] * K + jv;
-  pdl_wait();   // records and y come from the tile kernel
   const double yin = (g == 0 && F.beta != 0.0) ? (double)y[r] : 0.0;
   double acc = 0.0;
   for (int k = k0 + g; k < k1; k += G) acc += F.rec[(int64_t)k * K + jv];
@@ -1674,7 +1673,7 @@ constexpr int SELL_1CTA_SMEM = 116 * 1024;   // > half of the SM's 228 KB: one C
 template <typename VT, bool SELL, bool MIRROR, bool NA, bool HOT, int CL>
 cudaError_t launch_rows_k(const RowLaunch& L, cudaStream_t s) {
   using Lay = RowLayout<VT, SELL, HOT>;
-  constexpr int nw = HOT ? HOT_WARPS : WARPS;
+  constexpr int nw = HOT ? hot_warps((int)sizeof(VT)) : WARPS;
   static_assert(Lay::HOT_OFF + (HOT ? HOT_AUTO_BYTES : 0) <= 227 * 1024, "rows_kernel shared memory");
   int b = HOT ? Lay::HOT_OFF + ((L.nhot + CL - 1) / CL) * (int)sizeof(VT) : Lay::TOTAL;
   // SELL launches at one CTA per SM (RowLaunch.sell_1cta, picked by timing at partition): the
@@ -1688,14 +1687,7 @@ cudaError_t launch_rows_k(const RowLaunch& L, cudaStream_t s) {
   if (e) return e;
   int g = grid_for(kern, b, L.ntiles, nw);
   if constexpr (CL == 1) {
-    cudaLaunchConfig_t cfg{};
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.gridDim = dim3(g); cfg.blockDim = dim3(nw * 32); cfg.dynamicSmemBytes = (size_t)b; cfg.stream = s;
-    cfg.attrs = at; cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, kern, L);
-    if (e) return e;
+    kern<<<g, nw * 32, b, s>>>(L);
   } else {   // CTA pairs (one CTA per SM, the two SMs of a TPC) sharing their hot halves over DSMEM
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute at[1];
@@ -1774,13 +1766,8 @@ cudaError_t launch_pack(const PackLaunch& L, cudaStream_t s) {
 cudaError_t launch_fixup(const FixupLaunch& F, cudaStream_t s) {
   if (F.nsplit == 0) return cudaSuccess;
   const int g = (int)(((int64_t)F.nsplit * F.k * FIX_G + 255) / 256);   // FIX_G lanes per (split row, vector)
-  cudaLaunchConfig_t cfg{};
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // prologue under the tile kernel's tail
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.gridDim = dim3(g); cfg.blockDim = dim3(256); cfg.stream = s; cfg.attrs = at; cfg.numAttrs = 1;
-  cudaError_t e = F.dtype == 0 ? cudaLaunchKernelEx(&cfg, fixup_kernel<double>, F) : cudaLaunchKernelEx(&cfg, fixup_kernel<float>, F);
-  if (e) return e;
+  if (F.dtype == 0) fixup_kernel<double><<<g, 256, 0, s>>>(F);
+  else fixup_kernel<float><<<g, 256, 0, s>>>(F);
   return cudaGetLastError();
 }
 
@@ -1825,6 +1812,12 @@ cudaError_t launch_sum_peers(const SumLaunch& L, cudaStream_t s) {
 cudaError_t launch_col_degree(const int32_t* idx, int64_t nz, int32_t* deg, cudaStream_t s) {
   if (nz <= 0) return cudaSuccess;
   col_degree_kernel<<<elementwise_grid(nz), 256, 0, s>>>(idx, nz, deg);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_row_span(const int32_t* ptr, const int32_t* cols, int64_t m, int32_t* lo, int32_t* hi, cudaStream_t s) {
+  if (m <= 0) return cudaSuccess;
+  row_span_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(ptr, cols, m, lo, hi);
   return cudaGetLastError();
 }
 

@@ -46,3 +46,25 @@ def test_rmat_and_kdistinct_fill_rows_match_whole_fill():
                                   val.ctypes.data_as(P))
         z0 = int(C["ptr"][c0])
         assert np.array_equal(idx, C["idx"][z0:z0 + nz]) and np.array_equal(val, C["val"][z0:z0 + nz])
+
+
+def test_permuted_rmat_is_a_relabelling():
+    """The permuted R-MAT variant (config 3's "permuted variant"): its row-range fill
+    equals its whole fill, it holds exactly as many entries as the unpermuted matrix, and its row
+    and column degree multisets are the same (a vertex relabelling moves entries, it does not add or
+    drop any); heavy rows no longer cluster at low ids."""
+    L = gen.lib()
+    P = ctypes.c_void_p
+    A = gen.rmat(12, seed=3)
+    B = gen.rmat(12, seed=3, permute=True)
+    assert B.nnz == A.nnz
+    assert np.array_equal(np.sort(np.diff(A["ptr"])), np.sort(np.diff(B["ptr"])))
+    assert np.array_equal(np.sort(np.bincount(A["idx"], minlength=4096)), np.sort(np.bincount(B["idx"], minlength=4096)))
+    assert np.argmax(np.diff(B["ptr"])) != 0 or np.argmax(np.diff(A["ptr"])) != 0
+    for r0, r1 in [(0, 4096), (1000, 1100)]:
+        nz = int(B["ptr"][r1] - B["ptr"][r0])
+        idx = np.empty(max(nz, 1), np.int32)[:nz]; val = np.empty(max(nz, 1), np.float64)[:nz]
+        L.gen_rmat_fill_rows(12, float(16 * 4096), 0.57, 0.19, 0.19, 3, 1, 0, r0, r1, B["ptr"].ctypes.data_as(P),
+                             idx.ctypes.data_as(P), val.ctypes.data_as(P))
+        z0 = int(B["ptr"][r0])
+        assert np.array_equal(idx, B["idx"][z0:z0 + nz]) and np.array_equal(val, B["val"][z0:z0 + nz])

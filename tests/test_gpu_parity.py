@@ -469,14 +469,15 @@ def _banded_rows(m, k, span, seed, kind):
 
 
 @pytest.mark.parametrize("k", [8, 16, 27, 32])
-@pytest.mark.parametrize("fmt", ["csr", "coo"])
+@pytest.mark.parametrize("fmt", ["csr", "coo", "csc", "coo_col"])
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 def test_narrow_sell_tiles(k, fmt, dtype):
     """Narrow SELL tiles (16-bit column offsets from a per-tile base; fp32 up to 64 entries per lane,
     i.e. R = 2 for 27-point rows) next to 32-bit ones: rows whose columns span < 65536 become
     narrow, a block of rows spanning the whole x stays wide.  Bit-exact vs the oracle for
     MSREP_TUNE_SELL 2 (narrow) and 1 (32-bit only), 1 and 3 parts, device- and host-resident,
-    and the SpMM block walk over the same tiles."""
+    and the SpMM block walk over the same tiles.  The column formats run on row tiles over their
+    GPU-transposed slice, whose row spans come from the device (row_span_kernel)."""
     import paper_2209_07552_b200 as M
     import torch
     m = 32 * 4 * 12 + 37
@@ -495,7 +496,7 @@ def test_narrow_sell_tiles(k, fmt, dtype):
             for kw in ({}, {"residency": "host", "chunk_bytes": 32 << 10}):
                 ctx = M.Context(0, 1, None, 0, parts)
                 ctx.set_tuning("sell", sell)
-                got = run_gpu(A, fmt, x, y, 1.5, 0.5, ctx=ctx, **kw)
+                got = run_gpu(as_fmt(A, fmt), fmt, x, y, 1.5, 0.5, ctx=ctx, **kw)
                 st = ctx.stats()
                 assert np.array_equal(got, ref), (sell, parts, kw, np.nonzero(got != ref)[0][:8])
                 assert st["nsell"] > 0

@@ -8,10 +8,13 @@ O=gpurun_out/ev; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/gpu.txt
 timeout 900 python bench.py > $O/bench_default.json 2> $O/bench_default.err
 line() { timeout 900 python bench.py --steps ${STEPS:-500} --warmup 10 --e2e-steps 10 "$@" 2>/dev/null | tail -1 >> $O/bench_lines.jsonl; }
-line --config stencil
+line --config stencil --kernel-times 20
+line --config stencil --sell 1
+line --config stencil --dtype f32 --sell 1
 line --config stencil --format coo
 line --config stencil --format csc
 line --config stencil --dtype f32
+line --config rmat --kernel-times 20
 line --config rmat --format coo
 line --config rmat --format csc
 line --config rmat --format csc --col-layout 0
