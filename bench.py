@@ -453,6 +453,19 @@ def main():
     flops = 2.0 * nnz
     value = flops / (step_ms * 1e-3) / 1e9
 
+    # a per-call median from individual event pairs (after the timed region, which
+    # stays exactly K back-to-back steps): min(K, 50) calls, each bracketed by its own events
+    ncall = min(a.steps, 50)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(ncall)]
+    for e0c, e1c in evs:
+        e0c.record(stream)
+        step()
+        e1c.record(stream)
+    torch.cuda.synchronize()
+    per_call = sorted(e0c.elapsed_time(e1c) for e0c, e1c in evs)
+    per_call_median = max_over_ranks([per_call[len(per_call) // 2]])[0] if per_call else None
+    barrier()
+
     # per-kernel device time of one SpMV in a warm, back-to-back run (not cold-cache like ncu):
     # the split of the step between the tile kernel, the compact-x gather and the fix-up
     ktimes = None
@@ -592,6 +605,7 @@ def main():
                                         "binds for random column patterns (R-MAT, tall-skinny)"},
             "layouts": per_layout,
             "kernel_times_us": ktimes,
+            "per_call_median_ms": per_call_median,
             "nvlink": nv,
             "nccl": {"nranks": world, "version": ".".join(map(str, torch.cuda.nccl.version())),
                      "init_log": "stderr (NCCL_DEBUG=INFO, NCCL_DEBUG_SUBSYS=INIT)"} if world > 1 else None,
