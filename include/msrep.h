@@ -283,8 +283,9 @@ msrep_status_t msrep_set_residency(msrep_ctx ctx, msrep_residency residency, int
  *                       msrep_partition: the tiles index the rank's distinct
  *                       columns and every SpMV first gathers x' = x[cols]
  *                       (one launch): -1 (default) when x is >= 32 MB and either the
- *                       column degrees are skewed (x' in decreasing degree) or the
- *                       rank touches <= 3/4 of x (x' in column order); 0 off; 1 on,
+ *                       column degrees are skewed (x' in decreasing degree when it
+ *                       exceeds half the L2, else in column order) or the rank
+ *                       touches <= 3/4 of x (x' in column order); 0 off; 1 on,
  *                       column order; 2 on, decreasing column degree (the most-
  *                       gathered entries share cache lines).
  *   MSREP_TUNE_HOT_CLUSTER CTAs sharing one hot-x cache, applied by the next

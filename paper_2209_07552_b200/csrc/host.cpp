@@ -2330,12 +2330,12 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
       if (want_cx) {
         std::sort(used.begin(), used.end(), [](const auto& p, const auto& q) { return p.first < q.first; });
         for (auto& u : used) xcols.insert(xcols.end(), u.second.begin(), u.second.end());
-        // auto: degree-ordered x' when the column degrees are skewed -- the columns of >= 8x the
-        // mean degree hold >= 1/5 of the rank's nonzeros (R-MAT, power-law columns: their hot lines
-        // then share L2 sets and L1 instead of being spread over all of x; power-law suite 0.995 ->
-        // 0.778 ms, R-MAT 1.153 -> 1.110, profiles/r2_x_order_ab.txt); else column order when the
-        // rank touches <= 3/4 of x (R-MAT scale 24: 44 %; a uniform matrix that touches every
-        // column gains nothing from the extra gather); else no compact x
+        // auto: compact x when the column degrees are skewed -- the columns of >= 8x the mean degree
+        // hold >= 1/5 of the rank's nonzeros (R-MAT, power-law columns) -- in decreasing degree when
+        // x' is too big for the L2 (the warm lines then stay resident together instead of being
+        // spread over all of x'), else in column order; for unskewed matrices column order when the
+        // rank touches <= 3/4 of x (a uniform matrix that touches every column gains nothing from
+        // the extra gather); else no compact x
         bool skewed = false;
         if (!xcols.empty()) {
           const int64_t thr = 8 * (nz_r / (int64_t)xcols.size());
@@ -2343,8 +2343,14 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
           for (int32_t q : xcols) heavy += deg[(size_t)q] >= thr ? deg[(size_t)q] : 0;
           skewed = heavy * 5 >= nz_r;
         }
+        // degree order pays where x' does not fit in half the L2 (power-law suite: 188 MB, 1.00 -> 0.78 ms);
+        // an x' that fits stays in column order, whose gather needs no scatter (R-MAT 59 MB: fp64 step
+        // 1.174 -> 1.162, fp32 1.176 -> 1.102, pCSC 1.213 -> 1.159 ms; profiles/r2_kernel_ab.txt #19)
+        int l2 = 0;
+        if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, c->device) != cudaSuccess || l2 <= 0) l2 = 126 << 20;
+        const bool big_x = (int64_t)xcols.size() * (int64_t)V * 2 > (int64_t)l2;
         int mode = c->tune_compact >= 1 ? c->tune_compact
-                   : skewed ? 2 : ((int64_t)xcols.size() * 4 <= (int64_t)nx * 3 ? 1 : 0);
+                   : skewed ? (big_x ? 2 : 1) : ((int64_t)xcols.size() * 4 <= (int64_t)nx * 3 ? 1 : 0);
         // narrow SELL tiles need the column order (their 16-bit offsets were checked on column ids)
         if (mode == 2 && nsell_narrow > 0) mode = 1;
         if (mode >= 1) {

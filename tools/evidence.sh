@@ -21,6 +21,8 @@ line --config rmat --format csc --col-layout 0
 line --config rmat --format coo_col
 line --config rmat --dtype f32
 line --config rmat --layout owned
+line --config rmatperm
+line --config rmat --compact-x 2
 line --config tallskinny
 line --config tallskinny --col-layout 0
 line --config tallskinny --dtype f32
