@@ -408,6 +408,15 @@ struct Ctx {
   int64_t h_bytes = 0;
   char* d_stage[2] = {nullptr, nullptr};
   cudaStream_t cs = nullptr;        // copy stream
+  // pipelined msrep_spmv_host (one rank, one part, row tiles in row order): host copies of the tile
+  // rows / slab flags and the split rows, the chunking, a D2H stream and per-chunk events
+  std::vector<int32_t> h_tile_row0;         // window-local first row of tile t (final tile order)
+  std::vector<uint8_t> h_tile_slab;         // tile t is a slab (a piece of a split row)
+  std::vector<int64_t> h_sr_row;            // split rows, ascending
+  struct HostChunk { int32_t t0, t1; int64_t r0, r1; int32_t s0, s1; };
+  std::vector<HostChunk> hchunks;           // built on the first pipelined call
+  cudaStream_t cs_out = nullptr;
+  std::vector<cudaEvent_t> hev;             // [0]: x in, [1 + k]: y chunk k in, [1 + C + k]: chunk k computed
   cudaStream_t gs = nullptr;        // msrep_cg graph replay stream
   cudaStream_t ss = nullptr;        // side stream of the split SELL / SEG launches
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -1779,6 +1788,8 @@ msrep_status_t msrep_destroy(msrep_ctx h) {
   free_all(c);
   for (auto& p : c->ev) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
   if (c->cs) cudaStreamDestroy(c->cs);
+  if (c->cs_out) cudaStreamDestroy(c->cs_out);
+  for (cudaEvent_t e : c->hev) if (e) cudaEventDestroy(e);
   if (c->gs) cudaStreamDestroy(c->gs);
   if (c->ss) cudaStreamDestroy(c->ss);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
@@ -2065,6 +2076,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     c->cnb = CB.nb;
     c->citems = (int64_t)CB.items.size();
     c->ntiles = 0; c->nsell = 0; c->nslabs = 0; c->nrec = 0; c->nsplit = 0;
+    c->h_tile_row0.clear(); c->h_tile_slab.clear(); c->h_sr_row.clear(); c->hchunks.clear();
     c->blob_bytes = CB.bytes + c->citems * 24 + (CB.nb + 1) * 4 + CB.nb * (CB_W + 1) * 4;
     c->py_len = c->nranks > 1 ? c->shard * c->nranks : 0;
     if (c->py_len) {
@@ -2502,6 +2514,14 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
 #endif
     std::vector<TileHost> fin(S.tiles);
     for (size_t t = 0; t < fin.size(); t++) fin[t].nz0 = blob16[t];
+    c->h_tile_row0.resize(fin.size());
+    c->h_tile_slab.resize(fin.size());
+    for (size_t t = 0; t < fin.size(); t++) {
+      c->h_tile_row0[t] = fin[t].row0;
+      c->h_tile_slab[t] = fin[t].rec >= 0 ? 1 : 0;
+    }
+    c->h_sr_row = S.sr_row;
+    c->hchunks.clear();
     CUDA_TRY(cudaStreamSynchronize(s));
     // plain slices are no longer needed: the blobs hold the partition (host-resident: the
     // pinned copy does, and the packing buffer goes too)
@@ -2707,9 +2727,11 @@ msrep_status_t row_tiles_pass(Ctx* c, const RowLaunch& L, int k, cudaStream_t s)
 
 // the beta-deferred fix-up of the rank's split rows (records + head partials, reading R6/R10)
 msrep_status_t fixup_pass(Ctx* c, void* y, double alpha, double beta, int k, int nmirror, void* const* mirrors,
-                          double* rec, double* head_all, cudaStream_t s) {
+                          double* rec, double* head_all, cudaStream_t s, int s0 = 0, int s1 = -1) {
   FixupLaunch F{};
-  F.nsplit = c->nsplit;
+  F.s0 = s0;
+  F.nsplit = (s1 < 0 ? c->nsplit : s1) - s0;   // split rows [s0, s1)
+  if (F.nsplit <= 0) return MSREP_OK;
   F.sr_row = c->d_sr_row; F.sr_rec = c->d_sr_rec; F.sr_head = c->d_sr_head; F.head_list = c->d_head_list;
   F.part_rec = c->d_part_rec; F.part_lo = c->P0; F.part_hi = c->P1;
   F.head_all = head_all; F.rec = rec;
@@ -2923,6 +2945,91 @@ msrep_status_t msrep_spmm(msrep_ctx h, const void* alpha_p, const void* X, const
   return MSREP_OK;
 }
 
+// Pipelined host-vector SpMV (one rank, one part, device-resident row tiles in row order -- pCSR,
+// pCOO, or a column format on row tiles -- without a SELL / SEG mix): x goes up whole (any tile may
+// gather any column), then y_in in HOST_CHUNKS row chunks on the copy stream; chunk k's tiles run as
+// soon as its y_in is there, its split rows are fixed up right after, and its y rows go down on a
+// second copy stream while the next chunks go up and compute (PCIe is full duplex).  Chunks end on
+// tile boundaries that are row boundaries and never cut a split row.
+constexpr int HOST_CHUNKS = 8;
+bool host_pipeline_ok(const Ctx* c) {
+  return c->nranks == 1 && c->vparts == 1 && c->residency == MSREP_RESIDENT_DEVICE && c->ntiles >= 2 * HOST_CHUNKS &&
+         (!colwise(c->fmt) || c->col_rows) && (c->nsell == 0 || c->nsell == c->ntiles) &&
+         (int64_t)c->h_tile_row0.size() == c->ntiles;
+}
+msrep_status_t build_host_chunks(Ctx* c) {
+  c->hchunks.clear();
+  const int nt = c->ntiles;
+  std::vector<int32_t> cut{0};
+  for (int k = 1; k < HOST_CHUNKS; k++) {
+    int t = std::max(cut.back() + 1, (int)((int64_t)k * nt / HOST_CHUNKS));
+    // never between two slabs of one split row, never between two tiles starting on the same row
+    while (t < nt && c->h_tile_row0[(size_t)t] == c->h_tile_row0[(size_t)t - 1]) t++;
+    if (t >= nt) break;
+    cut.push_back(t);
+  }
+  cut.push_back(nt);
+  const int64_t rend = c->m;   // one rank, one part: the tiles cover rows [0, m) of y in order
+  for (size_t k = 0; k + 1 < cut.size(); k++) {
+    Ctx::HostChunk hc{};
+    hc.t0 = cut[k];
+    hc.t1 = cut[k + 1];
+    hc.r0 = k == 0 ? 0 : c->ybase + c->h_tile_row0[(size_t)hc.t0];
+    hc.r1 = k + 2 == cut.size() ? rend : c->ybase + c->h_tile_row0[(size_t)hc.t1];
+    hc.s0 = (int32_t)(std::lower_bound(c->h_sr_row.begin(), c->h_sr_row.end(), hc.r0) - c->h_sr_row.begin());
+    hc.s1 = (int32_t)(std::lower_bound(c->h_sr_row.begin(), c->h_sr_row.end(), hc.r1) - c->h_sr_row.begin());
+    c->hchunks.push_back(hc);
+  }
+  if (!c->cs) CUDA_TRY(cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking));
+  if (!c->cs_out) CUDA_TRY(cudaStreamCreateWithFlags(&c->cs_out, cudaStreamNonBlocking));
+  const size_t ne = 1 + 2 * c->hchunks.size() + 1;
+  while (c->hev.size() < ne) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->hev.push_back(e);
+  }
+  return MSREP_OK;
+}
+msrep_status_t spmv_host_pipelined(Ctx* c, double alpha, const void* x_host, double beta, void* y_host, cudaStream_t s) {
+  const size_t V = vsz(c->dtype);
+  if (c->hchunks.empty()) TRY(build_host_chunks(c));
+  const size_t C = c->hchunks.size();
+  cudaEvent_t* ev = c->hev.data();
+  // the caller's stream may still use d_hx / d_hy from an earlier call: copies start after it
+  CUDA_TRY(cudaEventRecord(ev[2 * C + 1], s));
+  CUDA_TRY(cudaStreamWaitEvent(c->cs, ev[2 * C + 1], 0));
+  CUDA_TRY(cudaStreamWaitEvent(c->cs_out, ev[2 * C + 1], 0));
+  if (c->n) CUDA_TRY(cudaMemcpyAsync(c->d_hx, x_host, (size_t)c->n * V, cudaMemcpyHostToDevice, c->cs));
+  CUDA_TRY(cudaEventRecord(ev[0], c->cs));
+  for (size_t k = 0; k < C; k++) {
+    const Ctx::HostChunk& hc = c->hchunks[k];
+    if (beta != 0.0 && hc.r1 > hc.r0)
+      CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(c->d_hy) + hc.r0 * V, static_cast<const char*>(y_host) + hc.r0 * V,
+                               (size_t)(hc.r1 - hc.r0) * V, cudaMemcpyHostToDevice, c->cs));
+    CUDA_TRY(cudaEventRecord(ev[1 + k], c->cs));
+  }
+  CUDA_TRY(cudaStreamWaitEvent(s, ev[0], 0));
+  TRY(prepare_x(c, c->d_hx, 1, s));
+  const RowLaunch L = row_launch(c, c->d_hx, c->d_hy, alpha, beta);
+  for (size_t k = 0; k < C; k++) {
+    const Ctx::HostChunk& hc = c->hchunks[k];
+    CUDA_TRY(cudaStreamWaitEvent(s, ev[1 + k], 0));
+    RowLaunch Lk = L;
+    Lk.tiles = c->d_tiles + hc.t0;
+    Lk.ntiles = hc.t1 - hc.t0;
+    CUDA_TRY(launch_rows(Lk, s));
+    TRY(fixup_pass(c, c->d_hy, alpha, beta, 1, 0, nullptr, c->d_rec, c->d_head_all, s, hc.s0, hc.s1));
+    CUDA_TRY(cudaEventRecord(ev[1 + C + k], s));
+    CUDA_TRY(cudaStreamWaitEvent(c->cs_out, ev[1 + C + k], 0));
+    if (hc.r1 > hc.r0)
+      CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(y_host) + hc.r0 * V, static_cast<char*>(c->d_hy) + hc.r0 * V,
+                               (size_t)(hc.r1 - hc.r0) * V, cudaMemcpyDeviceToHost, c->cs_out));
+  }
+  CUDA_TRY(cudaEventRecord(ev[2 * C + 1], c->cs_out));
+  CUDA_TRY(cudaStreamWaitEvent(s, ev[2 * C + 1], 0));
+  return MSREP_OK;
+}
+
 msrep_status_t msrep_spmv_host(msrep_ctx h, const void* alpha, const void* x_host, const void* beta, void* y_host,
                                msrep_layout layout, void* stream) {
   if (!h) return fail(MSREP_ERR_INVALID_ARG, "ctx is NULL");
@@ -2940,6 +3047,14 @@ msrep_status_t msrep_spmv_host(msrep_ctx h, const void* alpha, const void* x_hos
   int64_t r0 = lo[(size_t)c->rank], r1 = hi[(size_t)c->rank];
   if (layout == MSREP_Y_REPLICATED) { r0 = 0; r1 = c->m; }
   const double b = get_scalar(beta, c->dtype);
+  const double a = get_scalar(alpha, c->dtype);
+  const bool layout_ok = (layout == MSREP_Y_REPLICATED || layout == MSREP_Y_OWNED || layout == MSREP_Y_SHARDED) &&
+                         !(colwise(c->fmt) && layout == MSREP_Y_OWNED) && !(!colwise(c->fmt) && layout == MSREP_Y_SHARDED);
+  if (a != 0.0 && layout_ok && host_pipeline_ok(c)) {   // (bad layouts take the plain path, which reports them)
+    TRY(spmv_host_pipelined(c, a, x_host, b, y_host, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return MSREP_OK;
+  }
   if (c->n) CUDA_TRY(cudaMemcpyAsync(c->d_hx, x_host, (size_t)c->n * V, cudaMemcpyHostToDevice, s));
   // y_in: the rows this rank updates (REPLICATED multi-rank: its own segment is enough, peers send the rest)
   const int64_t i0 = lo[(size_t)c->rank], i1 = hi[(size_t)c->rank];

@@ -219,7 +219,7 @@ struct ColLaunch {
 };
 
 struct FixupLaunch {
-  int nsplit;
+  int nsplit, s0;                                     // split rows [s0, s0 + nsplit)
   const int64_t* sr_row; const int32_t* sr_rec;       // sr_rec[2*s], [2*s+1] : record range
   const int32_t* sr_head;                             // sr_head[2*s], [2*s+1]: range into head_list
   const int32_t* head_list;                           // global part ids

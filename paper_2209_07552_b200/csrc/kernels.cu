@@ -1444,7 +1444,7 @@ __global__ void fixup_kernel(const FixupLaunch F) {
   const int g = threadIdx.x & (G - 1);
   if (t >= (int64_t)F.nsplit * F.k) return;   // whole groups exit together (nsplit*k*G threads, G | 32)
   const unsigned gm = (unsigned)(((1ull << G) - 1) << (threadIdx.x & 31 & ~(G - 1)));
-  const int s = (int)(t / F.k), jv = (int)(t % F.k), K = F.k;
+  const int s = F.s0 + (int)(t / F.k), jv = (int)(t % F.k), K = F.k;
   // the row's metadata and its y_in are independent loads: all in flight before the record sum
   const int k0 = F.sr_rec[2 * s], k1 = F.sr_rec[2 * s + 1];
   const int h0 = F.sr_head[2 * s], h1 = F.sr_head[2 * s + 1];

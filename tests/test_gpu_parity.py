@@ -210,6 +210,54 @@ def test_host_vector_path_matches_device(fmt):
     assert np.array_equal(a, oracle_ref(A, x, y, 2.0, 0.5))
 
 
+@pytest.mark.parametrize("fmt", ["csr", "coo", "csc", "coo_col"])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_host_vector_pipelined_chunks(fmt, dtype):
+    """msrep_spmv_host at one rank and one part runs pipelined: x up whole, y_in up in row chunks,
+    chunk k's tiles and split-row fix-up as soon as its y_in is there, its y rows down while later
+    chunks go up and compute.  Bit-exact vs the device path and the oracle, for beta != 0 and
+    beta == 0 (no y_in copy), every layout the format takes, pageable numpy and pinned torch host
+    vectors, with heavy split rows (R-MAT) and with the hot-x cache and compact x (scale 17); the
+    result must not depend on what y_host held for beta == 0."""
+    import paper_2209_07552_b200 as M
+    import torch
+    for scale in (13, 17):
+        A = to_dtype(gen.rmat(scale, seed=12 + scale, kind=gen.SMALLINT), dtype)
+        x = gen.vector(A["n"], 1, kind=gen.SMALLINT).astype(dtype); y = gen.vector(A["m"], 2, kind=gen.SMALLINT).astype(dtype)
+        B = as_fmt(A, fmt)
+        lays = [M.Y_REPLICATED, M.Y_SHARDED] if fmt in ("csc", "coo_col") else [M.Y_REPLICATED, M.Y_OWNED]
+        for beta in (0.5, 0.0):
+            ref = oracle_ref(A, x, y, 2.0, beta)
+            dev = run_gpu(B, fmt, x, y, 2.0, beta, parts=1)
+            assert np.array_equal(dev, ref), (scale, beta)
+            for lay in lays:
+                for pinned in (False, True):
+                    ctx = M.Context(0, 1, None, 0, 1)
+                    apply_layout(ctx, fmt)
+                    if scale == 17:   # hot-x cache and degree-ordered compact x forced on (x is small here)
+                        ctx.set_tuning("hot_x", 1)
+                        ctx.set_tuning("compact_x", 2)
+                    if fmt in ("coo", "coo_col"):
+                        ctx.partition(fmt, B["m"], B["n"], idx=B["idx"], val=B["val"], coo_row=coo_of_csr(B))
+                    else:
+                        ctx.partition(fmt, B["m"], B["n"], ptr=B["ptr"], idx=B["idx"], val=B["val"])
+                    y0 = y.copy() if beta != 0.0 else np.full_like(y, np.nan)
+                    if pinned:
+                        xh = torch.as_tensor(x).pin_memory(); yh = torch.as_tensor(y0).pin_memory()
+                        for _ in range(2):   # twice: the second call reuses the chunking and events
+                            yh.copy_(torch.as_tensor(y0))
+                            ctx.spmv_host(2.0, xh.data_ptr(), beta, yh.data_ptr(), lay)
+                        got = yh.numpy()
+                    else:
+                        got = y0.copy()
+                        ctx.spmv_host(2.0, x, beta, got, lay)
+                    st = ctx.stats()
+                    ctx.close()
+                    assert np.array_equal(got, ref), (scale, beta, lay, pinned)
+                    if scale == 17 and fmt == "csr" and dtype == np.float64:
+                        assert st["nhot"] > 0 and st["x_compact"] > 0, st
+
+
 def test_owned_layout_writes_only_owned_rows():
     import paper_2209_07552_b200 as M
     A = gen.rmat(12, seed=5, kind=gen.SMALLINT)

@@ -45,7 +45,7 @@ def time_part(A, fmt, d, x, reps):
         ctx.partition("csc", A["m"], o1 - o0, ptr=ptr, idx=A["idx"][b0:b1], val=A["val"][b0:b1])
         xd = torch.as_tensor(x[o0:o1]).cuda()
         yd = torch.zeros(A["m"], dtype=torch.float64, device="cuda")
-    for _ in range(3):
+    for _ in range(10):   # warm: lazy module loading and the first launches stay out of the timing
         ctx.spmv(1.0, xd, 0.0, yd)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
