@@ -174,13 +174,40 @@ def msrep_get_unique_id() -> bytes:
     return bytes(buf)
 
 
-def msrep_create(rank=0, nranks=1, uid: bytes | None = None, device=0, parts_per_rank=1):
+_ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+_FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+
+
+def torch_allocator(device=0):
+    """An msrep_allocator over torch's CUDA caching allocator (the library's device buffers then come
+    from, and go back to, torch's pool).  Returns (struct, keepalive); keep both alive as long as the
+    context (Context(allocator="torch") does)."""
+    import torch
+
+    def _alloc(nbytes, stream, user):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(nbytes), device=device, stream=int(stream or 0))
+        except Exception:   # reported by the library as MSREP_ERR_OOM
+            return None
+
+    def _free(ptr, nbytes, stream, user):
+        if ptr:
+            torch.cuda.caching_allocator_delete(ptr)
+
+    fa, ff = _ALLOC_FN(_alloc), _FREE_FN(_free)
+    st = Allocator(ctypes.cast(fa, ctypes.c_void_p), ctypes.cast(ff, ctypes.c_void_p), None)
+    return st, (fa, ff, st)
+
+
+def msrep_create(rank=0, nranks=1, uid: bytes | None = None, device=0, parts_per_rank=1, alloc=None):
+    """alloc: None (cudaMalloc / cudaFree) or an Allocator struct (see torch_allocator)."""
     h = P()
     idbuf = None
     if uid is not None:
         idbuf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
     _check(_lib.msrep_create(ctypes.byref(h), rank, nranks, ctypes.cast(idbuf, P) if idbuf is not None else None,
-                             device, parts_per_rank, None), "msrep_create")
+                             device, parts_per_rank, ctypes.byref(alloc) if alloc is not None else None),
+           "msrep_create")
     return h
 
 
@@ -340,9 +367,16 @@ class Context:
     communicator from an initialised torch.distributed process group (rank 0's
     unique id is broadcast through it).  All device vectors are torch tensors."""
 
-    def __init__(self, rank=0, nranks=1, uid=None, device=0, parts_per_rank=1):
+    def __init__(self, rank=0, nranks=1, uid=None, device=0, parts_per_rank=1, allocator=None):
+        """allocator: None (cudaMalloc / cudaFree) or "torch" (torch's CUDA caching allocator)."""
         self.rank, self.nranks, self.device, self.parts_per_rank = rank, nranks, device, parts_per_rank
-        self.h = msrep_create(rank, nranks, uid, device, parts_per_rank)
+        self._alloc_keep = None
+        st = None
+        if allocator == "torch":
+            st, self._alloc_keep = torch_allocator(device)
+        elif allocator is not None:
+            raise ValueError(f"allocator {allocator!r}: None or 'torch'")
+        self.h = msrep_create(rank, nranks, uid, device, parts_per_rank, st)
         self.dtype = F64
         self.fmt = CSR
         self.parts = None

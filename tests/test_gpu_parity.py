@@ -258,6 +258,31 @@ def test_host_vector_pipelined_chunks(fmt, dtype):
                         assert st["nhot"] > 0 and st["x_compact"] > 0, st
 
 
+@pytest.mark.parametrize("fmt", ["csr", "csc"])
+def test_torch_allocator_hook(fmt):
+    """msrep_create's allocator hook (Context(allocator="torch")): every device buffer of the partition
+    comes from torch's caching allocator and goes back to it on close; results are the same bits as
+    with cudaMalloc.  Re-partitioning the same context frees the old layout through the hook."""
+    import paper_2209_07552_b200 as M
+    import torch
+    A = gen.rmat(14, seed=21, kind=gen.SMALLINT)
+    B = as_fmt(A, fmt)
+    x = gen.vector(A["n"], 22, kind=gen.SMALLINT); y = gen.vector(A["m"], 23, kind=gen.SMALLINT)
+    ref = oracle_ref(A, x, y, 1.5, 0.5)
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated(0)
+    ctx = M.Context(0, 1, None, 0, 2, allocator="torch")
+    for _ in range(2):   # the second partition releases the first layout through the hook
+        got = run_gpu(B, fmt, x, y, 1.5, 0.5, ctx=ctx)
+        assert np.array_equal(got, ref)
+        held = torch.cuda.memory_allocated(0) - base
+        st = ctx.stats()
+        assert held >= st["device_bytes"] > 0, (held, st["device_bytes"])
+    ctx.close()
+    torch.cuda.synchronize()
+    assert torch.cuda.memory_allocated(0) - base < st["device_bytes"]   # the layout went back to torch's pool
+
+
 def test_owned_layout_writes_only_owned_rows():
     import paper_2209_07552_b200 as M
     A = gen.rmat(12, seed=5, kind=gen.SMALLINT)
