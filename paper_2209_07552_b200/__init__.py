@@ -191,8 +191,11 @@ def torch_allocator(device=0):
             return None
 
     def _free(ptr, nbytes, stream, user):
-        if ptr:
-            torch.cuda.caching_allocator_delete(ptr)
+        try:
+            if ptr:
+                torch.cuda.caching_allocator_delete(ptr)
+        except Exception:   # interpreter teardown: the process is ending anyway
+            pass
 
     fa, ff = _ALLOC_FN(_alloc), _FREE_FN(_free)
     st = Allocator(ctypes.cast(fa, ctypes.c_void_p), ctypes.cast(ff, ctypes.c_void_p), None)
@@ -367,8 +370,9 @@ class Context:
     communicator from an initialised torch.distributed process group (rank 0's
     unique id is broadcast through it).  All device vectors are torch tensors."""
 
-    def __init__(self, rank=0, nranks=1, uid=None, device=0, parts_per_rank=1, allocator=None):
-        """allocator: None (cudaMalloc / cudaFree) or "torch" (torch's CUDA caching allocator)."""
+    def __init__(self, rank=0, nranks=1, uid=None, device=0, parts_per_rank=1, allocator="torch"):
+        """allocator: "torch" (default: the library's device buffers come from torch's CUDA caching
+        allocator) or None (cudaMalloc / cudaFree inside the library)."""
         self.rank, self.nranks, self.device, self.parts_per_rank = rank, nranks, device, parts_per_rank
         self._alloc_keep = None
         st = None

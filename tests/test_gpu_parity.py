@@ -260,9 +260,10 @@ def test_host_vector_pipelined_chunks(fmt, dtype):
 
 @pytest.mark.parametrize("fmt", ["csr", "csc"])
 def test_torch_allocator_hook(fmt):
-    """msrep_create's allocator hook (Context(allocator="torch")): every device buffer of the partition
-    comes from torch's caching allocator and goes back to it on close; results are the same bits as
-    with cudaMalloc.  Re-partitioning the same context frees the old layout through the hook."""
+    """msrep_create's allocator hook (Context(allocator="torch"), the binding's default): every device
+    buffer of the partition comes from torch's caching allocator and goes back to it on close;
+    results are the same bits as with the library's own cudaMalloc (allocator=None).
+    Re-partitioning the same context frees the old layout through the hook."""
     import paper_2209_07552_b200 as M
     import torch
     A = gen.rmat(14, seed=21, kind=gen.SMALLINT)
@@ -281,6 +282,12 @@ def test_torch_allocator_hook(fmt):
     ctx.close()
     torch.cuda.synchronize()
     assert torch.cuda.memory_allocated(0) - base < st["device_bytes"]   # the layout went back to torch's pool
+    # allocator=None: the library's own cudaMalloc / cudaFree, same bits, nothing from torch's pool
+    ctx = M.Context(0, 1, None, 0, 2, allocator=None)
+    got = run_gpu(B, fmt, x, y, 1.5, 0.5, ctx=ctx)
+    assert np.array_equal(got, ref)
+    assert torch.cuda.memory_allocated(0) - base < ctx.stats()["device_bytes"]
+    ctx.close()
 
 
 def test_owned_layout_writes_only_owned_rows():
