@@ -61,9 +61,8 @@ def parse(argv=None):
                    help="MSREP_TUNE_HOT_X: shared-memory hot-x cache (-1 auto, 0 off, 1 on, k > 1: k KiB)")
     p.add_argument("--compact-x", type=int, default=-1, choices=[-1, 0, 1, 2],
                    help="MSREP_TUNE_COMPACT_X: gather the rank's distinct x entries first (-1 auto, 0 off, 1 on)")
-    p.add_argument("--sell", type=int, default=None, choices=[0, 1, 2, 3],
-                   help="MSREP_TUNE_SELL: 0 SEG tiles only, 1 SELL tiles with 32-bit ids, 2 + narrow SELL tiles "
-                        "(fp32: two-slot SELL kernel when every tile fits), 3 = 2 without the two-slot mode")
+    p.add_argument("--sell", type=int, default=None, choices=[0, 1, 2],
+                   help="MSREP_TUNE_SELL: 0 SEG tiles only, 1 SELL tiles with 32-bit ids, 2 + narrow SELL tiles")
     p.add_argument("--hot-cluster", type=int, default=1, choices=[1, 2],
                    help="MSREP_TUNE_HOT_CLUSTER: CTAs sharing one hot-x cache over DSMEM")
     p.add_argument("--col-layout", type=int, default=-1, choices=[-1, 0, 1],
@@ -618,7 +617,7 @@ def main():
             "partition_ms": st["partition_ms"],
             "partition_phase_ms": dict(zip(("validate", "plan", "schedule", "upload_pack"), list(st["phase_ms"]))),
             "layout_build_ms": list(st["layout_ms"]),
-            "stats_rank0": {k: st[k] for k in ("nnz_rank", "ntiles", "nsell", "nsell_narrow", "sell_slots", "nslabs", "nsplit_rows",
+            "stats_rank0": {k: st[k] for k in ("nnz_rank", "ntiles", "nsell", "nsell_narrow", "nslabs", "nsplit_rows",
                                                "distinct_cols", "kernels_per_spmv", "tile_bytes", "x_no_allocate",
                                                "nhot", "hot_nnz", "x_compact", "x_order", "col_layout")},
         }

@@ -159,8 +159,6 @@ typedef struct {
                                 [0..4] counts, sort, list sizing, items / units, list writes    */
   int64_t x_order;           /* compact x order: 0 column, 1 decreasing degree; -1 no compact x */
   int64_t nsell_narrow;      /* narrow SELL tiles among nsell (16-bit column offsets, MSREP_TUNE_SELL 2) */
-  int64_t sell_slots;        /* TMA slots per warp of the SELL launch: 2 for fp32 partitions whose SELL tiles
-                                are all narrow with R*W <= 32 (MSREP_TUNE_SELL 2), else 1          */
 } msrep_stats;
 
 /* NCCL unique id for the communicator (rank 0 creates it, the caller
@@ -296,15 +294,12 @@ msrep_status_t msrep_set_residency(msrep_ctx ctx, msrep_residency residency, int
  *                       (thread-block clusters) and each CTA holds half of the
  *                       hot entries, read by its partner over distributed shared
  *                       memory (twice the entries, but measured slower on R-MAT).
- *   MSREP_TUNE_SELL     sliced-ELL tiles for runs of regular rows (row tiles),
+ *   MSREP_TUNE_SELL     sliced-ELL tiles for runs of regular rows (row formats),
  *                       applied by the next msrep_partition: 2 (default) on,
  *                       with NARROW tiles (16-bit column offsets from a per-tile
- *                       base) wherever a tile's columns span <= 65535; fp32: when
- *                       every SELL tile can be narrow with R*W <= 32, the SELL
- *                       kernel keeps two TMA slots per warp (stats.sell_slots),
- *                       else narrow tiles of up to 64 entries per lane and one
- *                       slot; 3 as 2 without the two-slot mode; 1 on, 32-bit
- *                       column ids only; 0 every row goes to SEG tiles / slabs.
+ *                       base, fp32: up to 64 entries per lane) wherever a tile's
+ *                       columns span <= 65535 (pCSR / pCOO); 1 on, 32-bit column
+ *                       ids only; 0 every row goes to SEG tiles / slabs.
  *   MSREP_TUNE_COL_LAYOUT device layout of the column formats (pCSC, column-
  *                       sorted / unsorted pCOO), applied by the next
  *                       msrep_partition: -1 (default) and 1 -- ROW TILES: the

@@ -64,7 +64,7 @@ class Stats(ctypes.Structure):
                                          ("gpu_numa_node", ctypes.c_int64), ("host_numa_node", ctypes.c_int64),
                                          ("stream_bytes", ctypes.c_int64), ("col_layout", ctypes.c_int64),
                                          ("layout_ms", ctypes.c_double * 6), ("x_order", ctypes.c_int64),
-                                         ("nsell_narrow", ctypes.c_int64), ("sell_slots", ctypes.c_int64)]
+                                         ("nsell_narrow", ctypes.c_int64)]
 
 
 class Allocator(ctypes.Structure):

@@ -397,7 +397,6 @@ struct Ctx {
   size_t mm_planar_bytes = 0;
   int tune_compact = -1;
   int64_t nsell_narrow = 0;         // narrow SELL tiles (16-bit column offsets)
-  int sell_ns2 = 0;                 // fp32 SELL tiles all narrow with R*W <= 32: two-slot SELL kernel
   int tune_sell = 2;                // SELL tiles for regular rows (0: SEG tiles only, 1: 32-bit ids only, 2: + narrow)
   int tune_hot_cluster = 1;         // CTAs of a cluster sharing one hot-x cache over DSMEM (1 or 2)
   bool split_launch = false;        // SELL tiles and SEG tiles run as two launches (each >= 5-10 % of nnz)
@@ -592,9 +591,8 @@ struct Packer {
   const int32_t *rlo, *rhi;         // per-window-row column span; both NULL: no narrow SELL tiles
   const int wn;                     // R * W limit of a narrow SELL tile
   explicit Packer(Schedule& s, int64_t w, const std::vector<int64_t>& l, int vsize, const int32_t* li = nullptr,
-                  const int32_t* lo = nullptr, const int32_t* hi = nullptr, int wn_cap = 0)
-      : S(s), wlo(w), lp(l), tnz(tile_nnz(vsize)), lidx(li), rlo(lo), rhi(hi),
-        wn(wn_cap > 0 ? std::min(wn_cap, selln_w_max(vsize)) : selln_w_max(vsize)) {}
+                  const int32_t* lo = nullptr, const int32_t* hi = nullptr)
+      : S(s), wlo(w), lp(l), tnz(tile_nnz(vsize)), lidx(li), rlo(lo), rhi(hi), wn(selln_w_max(vsize)) {}
   int64_t ls(int64_t r) const { return lp[(size_t)(r - wlo)]; }
   int64_t le(int64_t r) const { return lp[(size_t)(r - wlo + 1)]; }
   void flush() {
@@ -708,9 +706,8 @@ void rank_segments(msrep_format fmt, int64_t m, int nranks, int vparts, const st
 // slabs whose fix-up adds the head partials of the parts that continue it.
 void build_row_schedule(const std::vector<msrep_part_desc>& P, int P0, int P1, int64_t B_lo, int64_t wlo, int V,
                         const std::vector<int64_t>& lp, Schedule& S, bool allow_sell = true,
-                        const int32_t* lidx = nullptr, const int32_t* rlo = nullptr, const int32_t* rhi = nullptr,
-                        int wn_cap = 0) {
-  Packer pk(S, wlo, lp, V, lidx, rlo, rhi, wn_cap);
+                        const int32_t* lidx = nullptr, const int32_t* rlo = nullptr, const int32_t* rhi = nullptr) {
+  Packer pk(S, wlo, lp, V, lidx, rlo, rhi);
   for (int j = P0; j < P1; j++) {
     const msrep_part_desc& d = P[(size_t)j];
     const bool empty = d.start_idx > d.end_idx;
@@ -1381,7 +1378,6 @@ RowLaunch row_launch(const Ctx* c, const void* x, void* y, double alpha, double 
   L.dtype = c->dtype == MSREP_F64 ? 0 : 1; L.has_sell = c->nsell > 0;
   L.xna = c->xna;
   L.hot = c->d_hot; L.nhot = c->nhot; L.hot_cluster = c->hot_cluster; L.sell_1cta = c->sell_1cta;
-  L.sell_ns2 = c->sell_ns2;
   if (c->nxc) { L.x = c->d_xc; L.xmax = (uint32_t)(c->nxc - 1); }   // the SpMV gathers x' first (prepare_x)
   return L;
 }
@@ -1642,7 +1638,7 @@ msrep_status_t msrep_set_tuning(msrep_ctx h, msrep_tuning knob, int value) {
       c->tune_hot_cluster = value;
       return MSREP_OK;
     case MSREP_TUNE_SELL:
-      if (value < 0 || value > 3) return fail(MSREP_ERR_INVALID_ARG, "MSREP_TUNE_SELL %d (0, 1, 2, 3)", value);
+      if (value < 0 || value > 2) return fail(MSREP_ERR_INVALID_ARG, "MSREP_TUNE_SELL %d (0, 1, 2)", value);
       c->tune_sell = value;
       return MSREP_OK;
     case MSREP_TUNE_COL_LAYOUT:
@@ -2124,7 +2120,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     Schedule S;
     // transposed column formats: the rows' column spans come from the device slice (narrow SELL)
     std::vector<int32_t> span_lo, span_hi;
-    if (tr && c->tune_sell >= 2 && m > 0) {
+    if (tr && c->tune_sell == 2 && m > 0) {
       void* q;
       TRY(dalloc(c, (size_t)m * 8, &q, s));
       int32_t* d_span = static_cast<int32_t*>(q);
@@ -2135,16 +2131,11 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
       CUDA_TRY(cudaMemcpyAsync(span_hi.data(), d_span + m, (size_t)m * 4, cudaMemcpyDeviceToHost, s));
       CUDA_TRY(cudaStreamSynchronize(s));
     }
-    // fp32 (MSREP_TUNE_SELL 2): first try narrow SELL tiles of R * W <= 32 only; if every SELL tile
-    // comes out narrow the SELL kernel runs with two slots per warp (RowLaunch.sell_ns2), else the
-    // schedule is redone with narrow tiles of up to 64 entries per lane and one slot
-    int wn_cap = 0;
-    c->sell_ns2 = 0;
     auto schedule = [&](bool sell) {
       if (!tr) {
         // narrow SELL tiles (16-bit column offsets) from the host's column ids (MSREP_TUNE_SELL 2)
         build_row_schedule(c->parts, c->P0, c->P1, c->B_lo, c->wlo, (int)V, LP, S, sell,
-                           c->tune_sell >= 2 ? idx + c->B_lo : nullptr, nullptr, nullptr, wn_cap);
+                           c->tune_sell == 2 ? idx + c->B_lo : nullptr);
         return;
       }
       // one part of its own with no shared rows: rows cut into fixed chunks of 2^18 (the cut never
@@ -2163,7 +2154,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
           d[0].start_row = r0; d[0].end_row = r1 - 1;
           d[0].owned_begin = r0; d[0].owned_end = r1;
           build_row_schedule(d, 0, 1, 0, 0, (int)V, LP, cs[(size_t)k], sell, nullptr,
-                             span_lo.empty() ? nullptr : span_lo.data(), span_hi.empty() ? nullptr : span_hi.data(), wn_cap);
+                             span_lo.empty() ? nullptr : span_lo.data(), span_hi.empty() ? nullptr : span_hi.data());
         }
       };
       const int T = (int)std::min<int64_t>(nch, host_threads(nz_r + m));
@@ -2186,21 +2177,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
       }
       S.part_rec = {0, S.nrec};
     };
-    if (V == 4 && c->tune_sell == 2 && c->residency == MSREP_RESIDENT_DEVICE) {
-      wn_cap = SELLN_NS2_W;
-      schedule(true);
-      bool all_narrow = !S.sell.empty();
-      for (const TileHost& t : S.sell) all_narrow = all_narrow && t.rec == -3;
-      if (all_narrow) {
-        c->sell_ns2 = 1;
-      } else {
-        S = Schedule{};
-        wn_cap = 0;
-        schedule(true);
-      }
-    } else {
-      schedule(c->tune_sell != 0);
-    }
+    schedule(c->tune_sell != 0);
     {
       // A few SELL tiles among many SEG tiles cost more than they save: their presence selects
       // the SELL instantiation of rows_kernel for the whole launch, whose SEG path ran 2.5x
@@ -2213,7 +2190,6 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
         S = Schedule{};
         schedule(false);
         sell_nz = 0;
-        c->sell_ns2 = 0;
       }
       // ... and SEG / slab tiles get their own launch of the SEG instantiation (forked onto a side
       // stream) when they hold >= 5 % of the nonzeros, and always for fp32 (whose SELL
@@ -2610,7 +2586,7 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
   st.nnz_rank = nz_r;
   st.rows_window = W;
   const bool bands = colwise(fmt) && !c->col_rows;
-  st.ntiles = bands ? c->citems : c->ntiles; st.nsell = c->nsell; st.nsell_narrow = bands ? 0 : c->nsell_narrow; st.sell_slots = (!bands && c->nsell) ? (c->sell_ns2 ? 2 : 1) : 0; st.nslabs = c->nslabs; st.nsplit_rows = c->nsplit; st.nheads_local = c->nheads_local;
+  st.ntiles = bands ? c->citems : c->ntiles; st.nsell = c->nsell; st.nsell_narrow = bands ? 0 : c->nsell_narrow; st.nslabs = c->nslabs; st.nsplit_rows = c->nsplit; st.nheads_local = c->nheads_local;
   st.partition_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
   for (int k = 0; k < 4; k++) st.phase_ms[k] = phase[k];
   st.residency = c->residency;

@@ -82,9 +82,6 @@ constexpr int SELL_W_MAX = 32;    // R * W per lane
 // costs V + 2 bytes instead of V + 4, so the fp32 tiles may hold R * W <= 64 per lane (64 rows of
 // a 27-point stencil, the bytes of an fp64 tile).
 __host__ __device__ constexpr int selln_w_max(int vsize) { return vsize == 4 ? 64 : 32; }
-// fp32 partitions whose SELL tiles are all narrow with R * W <= 32 run the SELL kernel with TWO
-// slots per warp (the next tile lands while the current one is gathered): RowLaunch.sell_ns2
-constexpr int SELLN_NS2_W = 32;
 constexpr int SELL_R_MAX = 4;
 __host__ __device__ inline int align16(int b) { return (b + 15) & ~15; }
 // rows per lane of a SELL tile of `nrows` rows (1, 2 or 4)
@@ -162,7 +159,6 @@ struct RowLaunch {
   const int32_t* hot; int nhot;                              // hot-x columns by slot (nhot == 0: no hot x)
   int hot_cluster;                                           // 2: slots split over a CTA pair (DSMEM), else 1
   int sell_1cta;                                             // SELL-instantiation launches at one CTA per SM
-  int sell_ns2;                                              // fp32 SELL launch with two slots per warp (all tiles narrow, R*W <= 32)
 };
 
 // pCSC row-band layout.  The rank's nonzeros are regrouped

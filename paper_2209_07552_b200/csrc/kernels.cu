@@ -126,7 +126,6 @@ struct WLayout {
   static constexpr int BAR_OFF = NW * WARP_B;
   static constexpr int TOTAL = BAR_OFF + NW * NS * 8;
   static constexpr int HOT_OFF = (TOTAL + 15) & ~15;                     // CTA-wide hot x cache (sized per launch)
-  static constexpr int STAGE = STAGE_B, NSLOT = NS;
 };
 
 // nonzeros per lane in a full SEG tile / slab (+1 extra slot when ragged): 16 fp64, 32 fp32
@@ -192,14 +191,9 @@ struct SStage {   // the larger of a full 32-bit-id SELL tile and a full narrow 
   static constexpr int NARROW = 16 + SELL_R_MAX * 32 * 2 + selln_w_max(V) * SELL_ROWS * (V + 2);
   static constexpr int BYTES = WIDE > NARROW ? WIDE : NARROW;
 };
-template <typename VT>
-struct SStageN2 {   // a full narrow SELL tile with R * W <= SELLN_NS2_W (the two-slot ring)
-  static constexpr int BYTES = 16 + SELL_R_MAX * 32 * 2 + SELLN_NS2_W * SELL_ROWS * ((int)sizeof(VT) + 2);
-};
-template <typename VT, bool SELL, bool HOT = false, int NSL = 1>
-using RowLayout = WLayout<NSL == 2 ? SStageN2<VT>::BYTES
-                                   : ((SELL && SStage<VT>::BYTES > RStage<VT>::BYTES) ? SStage<VT>::BYTES : RStage<VT>::BYTES),
-                          NSL, NSL == 2 ? 16 : MAX_TILE_ROWS * 8, HOT ? hot_warps((int)sizeof(VT)) : WARPS>;
+template <typename VT, bool SELL, bool HOT = false>
+using RowLayout = WLayout<(SELL && SStage<VT>::BYTES > RStage<VT>::BYTES) ? SStage<VT>::BYTES : RStage<VT>::BYTES, 1,
+                          MAX_TILE_ROWS * 8, HOT ? hot_warps((int)sizeof(VT)) : WARPS>;
 
 // x gather of a SEG / slab column id: tagged ids (bit 31, internal.h HOT_TAG) read the CTA's
 // shared-memory copy of the rank's hottest x entries, the others go through L2.  Branch-free: one
@@ -316,12 +310,12 @@ __device__ __forceinline__ VT ldx_hot(const VT* x, const HotRef& hbase, uint32_t
 // first FMA; padding is masked by the row length, so results equal the plain row sums.  NARROW:
 // the column ids are 16-bit offsets from the tile's base (KIND_SELLN), up to selln_w_max entries
 // per lane, read from the slot just before each gather.
-template <typename VT, int R, bool MIRROR, bool NARROW, class Refill, int UCAP = 0>
+template <typename VT, int R, bool MIRROR, bool NARROW, class Refill>
 __device__ __forceinline__ void sell_tile(const RowLaunch& P, const int4 d, const unsigned char* st, const int lane,
                                           const VT* __restrict__ x, VT* __restrict__ y, double alpha, double beta,
                                           Refill&& refill) {
   constexpr int V = (int)sizeof(VT);
-  constexpr int U = UCAP ? UCAP : (NARROW ? selln_w_max(V) : SELL_W_MAX);   // R*W <= U register slots per lane
+  constexpr int U = NARROW ? selln_w_max(V) : SELL_W_MAX;   // R*W <= U register slots per lane
   const int nrows = d.z & 0xffff, W = d.z >> 16;
   const unsigned char* p = st + (NARROW ? 16 : 0);
   const uint16_t* lens = reinterpret_cast<const uint16_t*>(p);
@@ -373,24 +367,21 @@ __device__ __forceinline__ void sell_tile(const RowLaunch& P, const int4 d, cons
   refill();
 }
 
-template <typename VT, bool SELL, bool MIRROR, bool NA, bool HOT, int CL, int NSL = 1>
+template <typename VT, bool SELL, bool MIRROR, bool NA, bool HOT, int CL>
 __global__ void __launch_bounds__(HOT ? hot_warps((int)sizeof(VT)) * 32 : WARPS * 32,
                                   HOT ? 1 : (sizeof(VT) == 4 ? MSREP_ROW_MINB_F32 : MSREP_ROW_MINB))
     rows_kernel(const RowLaunch P) {
-  static_assert(NSL == 1 || (SELL && !HOT && sizeof(VT) == 4), "two slots: the fp32 SELL-only kernel");
-  using Lay = RowLayout<VT, SELL, HOT, NSL>;
+  using Lay = RowLayout<VT, SELL, HOT>;
   constexpr int NW = HOT ? hot_warps((int)sizeof(VT)) : WARPS;
   constexpr int QMAX = qmax<VT>();
   constexpr int V = (int)sizeof(VT);
   constexpr int YR = MAX_TILE_ROWS / 32;
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // NSL slots per warp: slot k at st0 + k * STAGE with descriptor sdesc0[k] and mbarrier bar0[k];
-  // tile i of the warp lives in slot i % NSL (phase (i / NSL) & 1)
-  unsigned char* const st0 = smem + warp * Lay::WARP_B;
-  int4* const sdesc0 = reinterpret_cast<int4*>(st0 + Lay::DESC_OFF);
-  double* rsum = reinterpret_cast<double*>(st0 + Lay::SCR_OFF);
-  uint64_t* const bar0 = reinterpret_cast<uint64_t*>(smem + Lay::BAR_OFF) + warp * NSL;
+  unsigned char* st = smem + warp * Lay::WARP_B;
+  int4* sdesc = reinterpret_cast<int4*>(st + Lay::DESC_OFF);
+  double* rsum = reinterpret_cast<double*>(st + Lay::SCR_OFF);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Lay::BAR_OFF) + warp;
   const int gw = blockIdx.x * NW + warp, nw = gridDim.x * NW;
 
   const VT* __restrict__ x = static_cast<const VT*>(P.x);
@@ -412,18 +403,15 @@ __global__ void __launch_bounds__(HOT ? hot_warps((int)sizeof(VT)) * 32 : WARPS 
   uint64_t pol = 0;
   int4 dn = make_int4(0, 0, 0, -1);
   if (lane == 0) {
-#pragma unroll
-    for (int k = 0; k < NSL; k++) mbar_init(bar0 + k, 1);
+    mbar_init(bar, 1);
     fence_mbar_init();
     pol = policy_evict_first();
-#pragma unroll
-    for (int k = 0; k < NSL; k++)
-      if (gw + k * nw < P.ntiles) {
-        const int4 d = P.tiles[gw + k * nw];
-        sdesc0[k] = d;
-        issue_blob(P.blob, d, tile_kind(d), V, st0 + k * Lay::STAGE, bar0 + k, pol);
-      }
-    if (gw + NSL * nw < P.ntiles) dn = P.tiles[gw + NSL * nw];
+    if (gw < P.ntiles) {
+      const int4 d = P.tiles[gw];
+      *sdesc = d;
+      issue_blob(P.blob, d, tile_kind(d), V, st, bar, pol);
+    }
+    if (gw + nw < P.ntiles) dn = P.tiles[gw + nw];
   }
   if constexpr (HOT) {   // the CTA's copy of (its share of) the hot x entries, gathered while the first tiles land
     constexpr int U = 8, T = NW * 32;
@@ -451,15 +439,11 @@ __global__ void __launch_bounds__(HOT ? hot_warps((int)sizeof(VT)) * 32 : WARPS 
   for (int i = 0;; i++) {
     const int t = gw + i * nw;
     if (t >= P.ntiles) break;
-    const int ks = NSL == 1 ? 0 : i % NSL;
-    unsigned char* const st = st0 + ks * Lay::STAGE;
-    int4* const sdesc = sdesc0 + ks;
-    uint64_t* const bar = bar0 + ks;
-    mbar_wait(bar, (uint32_t)((i / NSL) & 1));
+    mbar_wait(bar, (uint32_t)(i & 1));
     const int4 d = *sdesc;
     auto refill = [&]() {
       if (lane == 0) {
-        const int tn = t + NSL * nw;
+        const int tn = t + nw;
         if (tn < P.ntiles) {
           *sdesc = dn;
           issue_blob(P.blob, dn, tile_kind(dn), V, st, bar, pol);
@@ -470,12 +454,7 @@ __global__ void __launch_bounds__(HOT ? hot_warps((int)sizeof(VT)) * 32 : WARPS 
     if (SELL && (d.w == -2 || d.w == -3)) {
       // ---- SELL tile (read in place; the slot is refilled after the tile)
       const int R = sell_r(d.z & 0xffff);
-      if constexpr (NSL == 2) {   // the two-slot kernel: every tile narrow with R*W <= SELLN_NS2_W
-        using RF = decltype(refill)&;
-        if (R == 1) sell_tile<VT, 1, MIRROR, true, RF, SELLN_NS2_W>(P, d, st, lane, x, y, alpha, beta, refill);
-        else if (R == 2) sell_tile<VT, 2, MIRROR, true, RF, SELLN_NS2_W>(P, d, st, lane, x, y, alpha, beta, refill);
-        else sell_tile<VT, 4, MIRROR, true, RF, SELLN_NS2_W>(P, d, st, lane, x, y, alpha, beta, refill);
-      } else if (d.w == -3) {
+      if (d.w == -3) {
         if (R == 1) sell_tile<VT, 1, MIRROR, true>(P, d, st, lane, x, y, alpha, beta, refill);
         else if (R == 2) sell_tile<VT, 2, MIRROR, true>(P, d, st, lane, x, y, alpha, beta, refill);
         else sell_tile<VT, 4, MIRROR, true>(P, d, st, lane, x, y, alpha, beta, refill);
@@ -1691,9 +1670,9 @@ int grid_for(K kernel, int smem_bytes, int ntiles, int warps = WARPS) {
 }
 
 constexpr int SELL_1CTA_SMEM = 116 * 1024;   // > half of the SM's 228 KB: one CTA per SM
-template <typename VT, bool SELL, bool MIRROR, bool NA, bool HOT, int CL, int NSL = 1>
+template <typename VT, bool SELL, bool MIRROR, bool NA, bool HOT, int CL>
 cudaError_t launch_rows_k(const RowLaunch& L, cudaStream_t s) {
-  using Lay = RowLayout<VT, SELL, HOT, NSL>;
+  using Lay = RowLayout<VT, SELL, HOT>;
   constexpr int nw = HOT ? hot_warps((int)sizeof(VT)) : WARPS;
   static_assert(Lay::HOT_OFF + (HOT ? HOT_AUTO_BYTES : 0) <= 227 * 1024, "rows_kernel shared memory");
   int b = HOT ? Lay::HOT_OFF + ((L.nhot + CL - 1) / CL) * (int)sizeof(VT) : Lay::TOTAL;
@@ -1703,7 +1682,7 @@ cudaError_t launch_rows_k(const RowLaunch& L, cudaStream_t s) {
   if constexpr (SELL && !HOT) {
     if (L.sell_1cta) b = b > SELL_1CTA_SMEM ? b : SELL_1CTA_SMEM;
   }
-  auto kern = rows_kernel<VT, SELL, MIRROR, NA, HOT, CL, NSL>;
+  auto kern = rows_kernel<VT, SELL, MIRROR, NA, HOT, CL>;
   cudaError_t e = set_smem(kern, b);
   if (e) return e;
   int g = grid_for(kern, b, L.ntiles, nw);
@@ -1733,11 +1712,6 @@ cudaError_t launch_rows_t(const RowLaunch& L, cudaStream_t s) {
       return L.xna ? launch_rows_k<VT, false, MIRROR, true, true, 2>(L, s) : launch_rows_k<VT, false, MIRROR, false, true, 2>(L, s);
     if (L.nhot > 0)
       return L.xna ? launch_rows_k<VT, false, MIRROR, true, true, 1>(L, s) : launch_rows_k<VT, false, MIRROR, false, true, 1>(L, s);
-  }
-  if constexpr (SELL && sizeof(VT) == 4) {   // every SELL tile narrow with R * W <= 32: two slots per warp
-    if (L.sell_ns2)
-      return L.xna ? launch_rows_k<VT, SELL, MIRROR, true, false, 1, 2>(L, s)
-                   : launch_rows_k<VT, SELL, MIRROR, false, false, 1, 2>(L, s);
   }
   return L.xna ? launch_rows_k<VT, SELL, MIRROR, true, false, 1>(L, s) : launch_rows_k<VT, SELL, MIRROR, false, false, 1>(L, s);
 }

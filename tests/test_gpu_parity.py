@@ -596,39 +596,6 @@ def test_narrow_sell_tiles(k, fmt, dtype):
                 ctx.close()
 
 
-@pytest.mark.parametrize("k", [6, 8, 16, 27, 32])
-@pytest.mark.parametrize("fmt", ["csr", "coo", "csc"])
-def test_sell_two_slot_fp32(k, fmt):
-    """fp32 partitions whose SELL tiles are all narrow with R*W <= 32 run the SELL kernel with two TMA
-    slots per warp (stats.sell_slots == 2; MSREP_TUNE_SELL 3 keeps one slot and 64-entry tiles):
-    bit-exact vs the oracle either way, with parts, the SpMM walk and the pipelined host-vector
-    path."""
-    import paper_2209_07552_b200 as M
-    import torch
-    m = 32 * 4 * 40 + 21
-    A = to_dtype(_banded_rows(m, k, 20000, 500 + k, gen.SMALLINT), np.float32)
-    x = gen.vector(A["n"], 501, kind=gen.SMALLINT).astype(np.float32); y = gen.vector(m, 502, kind=gen.SMALLINT).astype(np.float32)
-    ref = oracle_ref(A, x, y, 1.5, 0.5)
-    for sell, slots in ((2, 2), (3, 1)):
-        for parts in (1, 3):
-            ctx = M.Context(0, 1, None, 0, parts)
-            ctx.set_tuning("sell", sell)
-            got = run_gpu(as_fmt(A, fmt), fmt, x, y, 1.5, 0.5, ctx=ctx)
-            st = ctx.stats()
-            assert np.array_equal(got, ref), (sell, parts)
-            assert st["sell_slots"] == slots and st["nsell_narrow"] == st["nsell"] > 0, st
-            if parts == 1 and fmt != "csc":
-                yh = y.copy()
-                ctx.spmv_host(1.5, x, 0.5, yh)
-                assert np.array_equal(yh, ref), ("host path", sell)
-                X = np.stack([x, 2 * x], 1).astype(np.float32)
-                Yd = torch.as_tensor(np.stack([y, y], 1).astype(np.float32)).cuda()
-                ctx.spmm(1.5, torch.as_tensor(X).cuda(), 0.5, Yd)
-                torch.cuda.synchronize()
-                assert np.array_equal(Yd.cpu().numpy()[:, 1], oracle_ref(A, X[:, 1].copy(), y, 1.5, 0.5)), ("spmm", sell)
-            ctx.close()
-
-
 @pytest.mark.parametrize("fmt", ["csc:bands", "coo_col:bands", "csc"])
 def test_csc_heavy_rows_same_row_groups(fmt):
     """Rows with thousands of entries inside one band (R-MAT heavy rows, and a dense row): the
