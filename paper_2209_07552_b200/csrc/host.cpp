@@ -415,7 +415,7 @@ struct Ctx {
   std::vector<int64_t> h_sr_row;            // split rows, ascending
   struct HostChunk { int32_t t0, t1; int64_t r0, r1; int32_t s0, s1; };
   std::vector<HostChunk> hchunks;           // built on the first pipelined call
-  cudaStream_t cs_out = nullptr;
+  cudaStream_t cs_in = nullptr, cs_out = nullptr;
   std::vector<cudaEvent_t> hev;             // [0]: x in, [1 + k]: y chunk k in, [1 + C + k]: chunk k computed
   cudaStream_t gs = nullptr;        // msrep_cg graph replay stream
   cudaStream_t ss = nullptr;        // side stream of the split SELL / SEG launches
@@ -1788,6 +1788,7 @@ msrep_status_t msrep_destroy(msrep_ctx h) {
   free_all(c);
   for (auto& p : c->ev) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
   if (c->cs) cudaStreamDestroy(c->cs);
+  if (c->cs_in) cudaStreamDestroy(c->cs_in);
   if (c->cs_out) cudaStreamDestroy(c->cs_out);
   for (cudaEvent_t e : c->hev) if (e) cudaEventDestroy(e);
   if (c->gs) cudaStreamDestroy(c->gs);
@@ -2980,7 +2981,8 @@ msrep_status_t build_host_chunks(Ctx* c) {
     hc.s1 = (int32_t)(std::lower_bound(c->h_sr_row.begin(), c->h_sr_row.end(), hc.r1) - c->h_sr_row.begin());
     c->hchunks.push_back(hc);
   }
-  if (!c->cs) CUDA_TRY(cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking));
+  // streams of their own (the host-resident mode's copy stream comes with its events: ensure_copy_stream)
+  if (!c->cs_in) CUDA_TRY(cudaStreamCreateWithFlags(&c->cs_in, cudaStreamNonBlocking));
   if (!c->cs_out) CUDA_TRY(cudaStreamCreateWithFlags(&c->cs_out, cudaStreamNonBlocking));
   const size_t ne = 1 + 2 * c->hchunks.size() + 1;
   while (c->hev.size() < ne) {
@@ -2997,16 +2999,16 @@ msrep_status_t spmv_host_pipelined(Ctx* c, double alpha, const void* x_host, dou
   cudaEvent_t* ev = c->hev.data();
   // the caller's stream may still use d_hx / d_hy from an earlier call: copies start after it
   CUDA_TRY(cudaEventRecord(ev[2 * C + 1], s));
-  CUDA_TRY(cudaStreamWaitEvent(c->cs, ev[2 * C + 1], 0));
+  CUDA_TRY(cudaStreamWaitEvent(c->cs_in, ev[2 * C + 1], 0));
   CUDA_TRY(cudaStreamWaitEvent(c->cs_out, ev[2 * C + 1], 0));
-  if (c->n) CUDA_TRY(cudaMemcpyAsync(c->d_hx, x_host, (size_t)c->n * V, cudaMemcpyHostToDevice, c->cs));
-  CUDA_TRY(cudaEventRecord(ev[0], c->cs));
+  if (c->n) CUDA_TRY(cudaMemcpyAsync(c->d_hx, x_host, (size_t)c->n * V, cudaMemcpyHostToDevice, c->cs_in));
+  CUDA_TRY(cudaEventRecord(ev[0], c->cs_in));
   for (size_t k = 0; k < C; k++) {
     const Ctx::HostChunk& hc = c->hchunks[k];
     if (beta != 0.0 && hc.r1 > hc.r0)
       CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(c->d_hy) + hc.r0 * V, static_cast<const char*>(y_host) + hc.r0 * V,
-                               (size_t)(hc.r1 - hc.r0) * V, cudaMemcpyHostToDevice, c->cs));
-    CUDA_TRY(cudaEventRecord(ev[1 + k], c->cs));
+                               (size_t)(hc.r1 - hc.r0) * V, cudaMemcpyHostToDevice, c->cs_in));
+    CUDA_TRY(cudaEventRecord(ev[1 + k], c->cs_in));
   }
   CUDA_TRY(cudaStreamWaitEvent(s, ev[0], 0));
   TRY(prepare_x(c, c->d_hx, 1, s));

@@ -290,6 +290,29 @@ def test_torch_allocator_hook(fmt):
     ctx.close()
 
 
+def test_host_vector_pipeline_then_host_resident():
+    """One context: a device-resident partition used through the pipelined host-vector path, then
+    re-partitioned host-resident (streamed per call on the copy stream) and back -- the two modes
+    keep their streams and events apart; every result bit-exact."""
+    import paper_2209_07552_b200 as M
+    import torch
+    A = gen.rmat(13, seed=33, kind=gen.SMALLINT)
+    x = gen.vector(A["n"], 34, kind=gen.SMALLINT); y = gen.vector(A["m"], 35, kind=gen.SMALLINT)
+    ref = oracle_ref(A, x, y, 1.5, 0.5)
+    ctx = M.Context(0, 1, None, 0, 1)
+    for res in ("device", "host", "device", "host"):
+        kw = {"residency": res, "chunk_bytes": 64 << 10} if res == "host" else {}
+        ctx.partition("csr", A["m"], A["n"], ptr=A["ptr"], idx=A["idx"], val=A["val"], **kw)
+        yh = y.copy()
+        ctx.spmv_host(1.5, x, 0.5, yh)
+        assert np.array_equal(yh, ref), ("host path", res)
+        yd = torch.as_tensor(y.copy()).cuda()
+        ctx.spmv(1.5, torch.as_tensor(x).cuda(), 0.5, yd)
+        torch.cuda.synchronize()
+        assert np.array_equal(yd.cpu().numpy(), ref), ("device path", res)
+    ctx.close()
+
+
 def test_owned_layout_writes_only_owned_rows():
     import paper_2209_07552_b200 as M
     A = gen.rmat(12, seed=5, kind=gen.SMALLINT)
