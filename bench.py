@@ -366,6 +366,10 @@ def main():
 
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if local >= torch.cuda.device_count():   # no CPU fallback: the product path is the CUDA library
+        print(f"bench.py: rank {rank} needs CUDA device {local}, found {torch.cuda.device_count()} visible",
+              file=sys.stderr, flush=True)
+        return 2
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
