@@ -619,6 +619,37 @@ def test_narrow_sell_tiles(k, fmt, dtype):
                 ctx.close()
 
 
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_narrow_sell_span_boundary(dtype):
+    """A SELL tile is narrow iff its columns span <= 65535 (16-bit offsets from the tile's smallest
+    column): 128-row blocks (one R = 4 SELL tile each) of 8 columns reaching exactly base + 65535
+    are narrow, blocks reaching base + 65536 are not; both bit-exact, including the largest offset
+    65535 itself."""
+    import paper_2209_07552_b200 as M
+    blocks, n = 24, 200_000
+    rows_per = 128
+    m = blocks * rows_per
+    rng = np.random.default_rng(77)
+    ptr = np.arange(m + 1, dtype=np.int64) * 8
+    idx = np.empty(m * 8, dtype=np.int32)
+    for b in range(blocks):
+        base = 1000 * b
+        reach = 65535 if b % 2 == 0 else 65536   # even blocks narrow, odd blocks wide
+        for r in range(b * rows_per, (b + 1) * rows_per):
+            mid = np.sort(rng.choice(np.arange(1, reach), size=6, replace=False))
+            cols = np.concatenate([[base], base + mid, [base + reach]])
+            idx[r * 8:(r + 1) * 8] = cols
+    A = to_dtype(gen.Sparse(fmt="csr", m=m, n=n, ptr=ptr, idx=idx, val=gen.vector(m * 8, 78, kind=gen.SMALLINT)), dtype)
+    x = gen.vector(n, 79, kind=gen.SMALLINT).astype(dtype); y = gen.vector(m, 80, kind=gen.SMALLINT).astype(dtype)
+    ref = oracle_ref(A, x, y, 1.5, 0.5)
+    ctx = M.Context(0, 1, None, 0, 1)
+    got = run_gpu(A, "csr", x, y, 1.5, 0.5, ctx=ctx)
+    st = ctx.stats()
+    ctx.close()
+    assert np.array_equal(got, ref)
+    assert st["nsell"] == blocks and st["nsell_narrow"] == blocks // 2, st
+
+
 @pytest.mark.parametrize("fmt", ["csc:bands", "coo_col:bands", "csc"])
 def test_csc_heavy_rows_same_row_groups(fmt):
     """Rows with thousands of entries inside one band (R-MAT heavy rows, and a dense row): the
