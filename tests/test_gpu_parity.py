@@ -386,6 +386,16 @@ def test_config3_rmat_full_size_column_formats_bit_exact(fmt):
 
 
 @pytest.mark.slow
+@pytest.mark.parametrize("fmt", ["csc", "coo"])
+def test_config3_rmat_full_size_fp32_other_formats_bit_exact(fmt):
+    """R-MAT scale 24 fp32 through pCSC on row tiles (fp32 partial y) and pCOO, bit-exact
+    (integer data: every row sum < 2^24)."""
+    A = to_dtype(gen.rmat(24, seed=3, kind=gen.SMALLINT), np.float32)
+    x = gen.vector(A["n"], 7, kind=gen.SMALLINT, dtype=np.float32); y = gen.vector(A["m"], 8, kind=gen.SMALLINT, dtype=np.float32)
+    check(A, fmt, x, y, 2.0, 0.5, exact=True)
+
+
+@pytest.mark.slow
 def test_config4_tallskinny_fp32_bit_exact():
     A = to_dtype(gen.kdistinct_csc(50_000_000, 1_000_000, 500, seed=4, kind=gen.SMALLINT), np.float32)
     x = gen.vector(A["n"], 9, kind=gen.SMALLINT, dtype=np.float32); y = gen.vector(A["m"], 10, kind=gen.SMALLINT, dtype=np.float32)
