@@ -2501,18 +2501,6 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     }
     CUDA_TRY(cudaStreamSynchronize(s));
     sub(3);
-#ifdef MSREP_PHASE_DEBUG   // tuning builds only: where the tile-table phase goes
-    auto dbg_t0 = std::chrono::steady_clock::now();
-    auto dbg = [&](const char* what) {
-      cudaStreamSynchronize(s);
-      const auto now = std::chrono::steady_clock::now();
-      fprintf(stderr, "[msrep phase4] %-24s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(now - dbg_t0).count());
-      dbg_t0 = now;
-    };
-#define MSREP_DBG(w) dbg(w)
-#else
-#define MSREP_DBG(w)
-#endif
     std::vector<TileHost> fin(S.tiles);
     for (size_t t = 0; t < fin.size(); t++) fin[t].nz0 = blob16[t];
     c->h_tile_row0.resize(fin.size());
@@ -2526,20 +2514,16 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
     CUDA_TRY(cudaStreamSynchronize(s));
     // plain slices are no longer needed: the blobs hold the partition (host-resident: the
     // pinned copy does, and the packing buffer goes too)
-    MSREP_DBG("fin");
     release_range(c, mark, host_res ? c->bufs.size() : keep_from);
-    MSREP_DBG("release_range");
     if (host_res) {
       TRY(ensure_copy_stream(c));
       TRY(alloc_stages(c, s));
     }
     TRY(upload(c, reinterpret_cast<const int4*>(fin.data()), fin.size(), &c->d_tiles, s));
-    MSREP_DBG("upload tiles");
     c->blob_bytes = blob_total;
     void* rp;
     TRY(dalloc(c, (size_t)std::max(1, S.nrec) * 8, &rp, s));
     c->d_rec = static_cast<double*>(rp);
-    MSREP_DBG("rec");
     {
       TRY(upload_vec(c, S.sr_row, &c->d_sr_row, s));
       TRY(upload_vec(c, S.sr_rec, &c->d_sr_rec, s));
@@ -2570,8 +2554,6 @@ msrep_status_t msrep_partition(msrep_ctx h, msrep_format fmt, msrep_dtype dtype,
         CUDA_TRY(cudaMemsetAsync(static_cast<char*>(pp) + (size_t)m * V, 0, (size_t)(c->py_len - m) * V, s));
       }
     }
-    MSREP_DBG("records + tail");
-#undef MSREP_DBG
   }
   CUDA_TRY(cudaStreamSynchronize(s));
   if (!colwise(fmt) || col_rows) sub(4);
