@@ -2934,7 +2934,10 @@ msrep_status_t msrep_spmm(msrep_ctx h, const void* alpha_p, const void* X, const
 // soon as its y_in is there, its split rows are fixed up right after, and its y rows go down on a
 // second copy stream while the next chunks go up and compute (PCIe is full duplex).  Chunks end on
 // tile boundaries that are row boundaries and never cut a split row.
-constexpr int HOST_CHUNKS = 8;
+#ifndef MSREP_HOST_CHUNKS
+#define MSREP_HOST_CHUNKS 16
+#endif
+constexpr int HOST_CHUNKS = MSREP_HOST_CHUNKS;
 bool host_pipeline_ok(const Ctx* c) {
   return c->nranks == 1 && c->vparts == 1 && c->residency == MSREP_RESIDENT_DEVICE && c->ntiles >= 2 * HOST_CHUNKS &&
          (!colwise(c->fmt) || c->col_rows) && (c->nsell == 0 || c->nsell == c->ntiles) &&
