@@ -413,7 +413,7 @@ struct Ctx {
   std::vector<int32_t> h_tile_row0;         // window-local first row of tile t (final tile order)
   std::vector<uint8_t> h_tile_slab;         // tile t is a slab (a piece of a split row)
   std::vector<int64_t> h_sr_row;            // split rows, ascending
-  struct HostChunk { int32_t t0, t1; int64_t r0, r1; int32_t s0, s1; };
+  struct HostChunk { int32_t t0, t1, u0, u1; int64_t r0, r1; int32_t s0, s1; };   // SELL / SEG tile ranges
   std::vector<HostChunk> hchunks;           // built on the first pipelined call
   cudaStream_t cs_in = nullptr, cs_out = nullptr;
   std::vector<cudaEvent_t> hev;             // [0]: x in, [1 + k]: y chunk k in, [1 + C + k]: chunk k computed
@@ -2928,8 +2928,8 @@ msrep_status_t msrep_spmm(msrep_ctx h, const void* alpha_p, const void* X, const
   return MSREP_OK;
 }
 
-// Pipelined host-vector SpMV (one rank, one part, device-resident row tiles in row order -- pCSR,
-// pCOO, or a column format on row tiles -- without a SELL / SEG mix): x goes up whole (any tile may
+// Pipelined host-vector SpMV (one rank, one part, device-resident row tiles -- pCSR, pCOO, or a
+// column format on row tiles): x goes up whole (any tile may
 // gather any column), then y_in in HOST_CHUNKS row chunks on the copy stream; chunk k's tiles run as
 // soon as its y_in is there, its split rows are fixed up right after, and its y rows go down on a
 // second copy stream while the next chunks go up and compute (PCIe is full duplex).  Chunks end on
@@ -2940,28 +2940,35 @@ msrep_status_t msrep_spmm(msrep_ctx h, const void* alpha_p, const void* X, const
 constexpr int HOST_CHUNKS = MSREP_HOST_CHUNKS;
 bool host_pipeline_ok(const Ctx* c) {
   return c->nranks == 1 && c->vparts == 1 && c->residency == MSREP_RESIDENT_DEVICE && c->ntiles >= 2 * HOST_CHUNKS &&
-         (!colwise(c->fmt) || c->col_rows) && (c->nsell == 0 || c->nsell == c->ntiles) &&
-         (int64_t)c->h_tile_row0.size() == c->ntiles;
+         (!colwise(c->fmt) || c->col_rows) && (int64_t)c->h_tile_row0.size() == c->ntiles;
 }
+// Row chunks over both tile lists (SELL tiles [0, nsell) and SEG / slab tiles [nsell, ntiles), each in
+// row order): the cuts are tile-start rows of the merged order, so no tile and no split row (its
+// slabs share their first row) straddles a cut; chunk k runs its SELL range and its SEG range.
 msrep_status_t build_host_chunks(Ctx* c) {
   c->hchunks.clear();
-  const int nt = c->ntiles;
-  std::vector<int32_t> cut{0};
+  const int nt = c->ntiles, ns = c->nsell;
+  const int32_t* r0s = c->h_tile_row0.data();
+  std::vector<int32_t> merged;
+  merged.reserve((size_t)nt);
+  std::merge(r0s, r0s + ns, r0s + ns, r0s + nt, std::back_inserter(merged));
+  std::vector<int32_t> cut{merged.empty() ? 0 : merged[0]};
   for (int k = 1; k < HOST_CHUNKS; k++) {
-    int t = std::max(cut.back() + 1, (int)((int64_t)k * nt / HOST_CHUNKS));
-    // never between two slabs of one split row, never between two tiles starting on the same row
-    while (t < nt && c->h_tile_row0[(size_t)t] == c->h_tile_row0[(size_t)t - 1]) t++;
-    if (t >= nt) break;
-    cut.push_back(t);
+    const int32_t r = merged[(size_t)((int64_t)k * nt / HOST_CHUNKS)];
+    if (r > cut.back()) cut.push_back(r);
   }
-  cut.push_back(nt);
-  const int64_t rend = c->m;   // one rank, one part: the tiles cover rows [0, m) of y in order
-  for (size_t k = 0; k + 1 < cut.size(); k++) {
+  const int64_t rend = c->m;   // one rank, one part: the tiles cover rows [0, m) of y
+  for (size_t k = 0; k < cut.size(); k++) {
+    const bool last = k + 1 == cut.size();
+    const int32_t a = cut[k], b = last ? INT32_MAX : cut[k + 1];
     Ctx::HostChunk hc{};
-    hc.t0 = cut[k];
-    hc.t1 = cut[k + 1];
-    hc.r0 = k == 0 ? 0 : c->ybase + c->h_tile_row0[(size_t)hc.t0];
-    hc.r1 = k + 2 == cut.size() ? rend : c->ybase + c->h_tile_row0[(size_t)hc.t1];
+    hc.t0 = (int32_t)(std::lower_bound(r0s, r0s + ns, a) - r0s);
+    hc.t1 = (int32_t)(std::lower_bound(r0s, r0s + ns, b) - r0s);
+    hc.u0 = (int32_t)(std::lower_bound(r0s + ns, r0s + nt, a) - r0s);
+    hc.u1 = (int32_t)(std::lower_bound(r0s + ns, r0s + nt, b) - r0s);
+    if (k == 0) { hc.t0 = 0; hc.u0 = ns; }
+    hc.r0 = k == 0 ? 0 : c->ybase + a;
+    hc.r1 = last ? rend : c->ybase + b;
     hc.s0 = (int32_t)(std::lower_bound(c->h_sr_row.begin(), c->h_sr_row.end(), hc.r0) - c->h_sr_row.begin());
     hc.s1 = (int32_t)(std::lower_bound(c->h_sr_row.begin(), c->h_sr_row.end(), hc.r1) - c->h_sr_row.begin());
     c->hchunks.push_back(hc);
@@ -3001,10 +3008,19 @@ msrep_status_t spmv_host_pipelined(Ctx* c, double alpha, const void* x_host, dou
   for (size_t k = 0; k < C; k++) {
     const Ctx::HostChunk& hc = c->hchunks[k];
     CUDA_TRY(cudaStreamWaitEvent(s, ev[1 + k], 0));
-    RowLaunch Lk = L;
-    Lk.tiles = c->d_tiles + hc.t0;
-    Lk.ntiles = hc.t1 - hc.t0;
-    CUDA_TRY(launch_rows(Lk, s));
+    if (hc.t1 > hc.t0) {   // the chunk's SELL tiles
+      RowLaunch Lk = L;
+      Lk.tiles = c->d_tiles + hc.t0;
+      Lk.ntiles = hc.t1 - hc.t0;
+      CUDA_TRY(launch_rows(Lk, s));
+    }
+    if (hc.u1 > hc.u0) {   // its SEG / slab tiles, in the SEG instantiation
+      RowLaunch Lk = L;
+      Lk.tiles = c->d_tiles + hc.u0;
+      Lk.ntiles = hc.u1 - hc.u0;
+      Lk.has_sell = 0;
+      CUDA_TRY(launch_rows(Lk, s));
+    }
     TRY(fixup_pass(c, c->d_hy, alpha, beta, 1, 0, nullptr, c->d_rec, c->d_head_all, s, hc.s0, hc.s1));
     CUDA_TRY(cudaEventRecord(ev[1 + C + k], s));
     CUDA_TRY(cudaStreamWaitEvent(c->cs_out, ev[1 + C + k], 0));

@@ -520,6 +520,11 @@ def test_sell_and_seg_split_launch(fmt):
             ctx = M.Context(0, 1, None, 0, parts)
             got = run_gpu(A, fmt, x, y, 1.5, 0.5, ctx=ctx, **kw)
             st = ctx.stats()
+            if parts == 1 and not kw:   # the pipelined host-vector path: row chunks over both tile lists
+                for beta in (0.5, 0.0):
+                    yh = y.copy()
+                    ctx.spmv_host(1.5, x, beta, yh)
+                    assert np.array_equal(yh, oracle_ref(A, x, y, 1.5, beta)), ("host path", fmt, beta)
             ctx.close()
             assert np.array_equal(got, ref), (fmt, parts, kw)
             assert st["nsell"] > 0
